@@ -1,0 +1,145 @@
+/*
+ * prnet.h -- C ABI (v1) of the B200-native PRNet pattern-attention forward.
+ *
+ * The operation (abstract, conclusion; reading fixed in
+ * SURVEY.md §8(c) and restated in DESIGN.md §3): every (window b, channel c)
+ * lookback series x[b][c][0..L) is cut into N = floor(L/S) segments of length
+ * S (the oldest r = L - N*S points are dropped, reading A2); between every pair
+ * of segments a seasonal similarity (Pearson correlation, A4) and a trend
+ * distance (distance between least-squares lines normalised by the series
+ * variance, A5) are evaluated; each is softmax-normalised over rows ("pattern
+ * attention"; temperatures tau_s, tau_t, A6/A9) and aggregates the raw
+ * segments into seasonal and trend patterns P_s, P_t (A10); a linear head over
+ * the segment axis (A7/A8/A11) maps them to M = ceil(H/S) future segments, of
+ * which the first H steps plus a per-step bias form y[b][c][0..H).
+ *
+ * Conventions for every entry point:
+ *  - C linkage, no exceptions cross the boundary; every function returns a
+ *    prnet_status (>= 0).  A human-readable message for the last failure is
+ *    kept per handle (prnet_last_error).
+ *  - Arguments are validated before any work is enqueued (SPEC-style
+ *    "validate first"); on error nothing is written.
+ *  - Device pointers are plain CUDA device addresses (e.g. a torch tensor's
+ *    data_ptr()); host pointers are ordinary (preferably pinned) host memory.
+ *  - All tensors are fp32, C-contiguous, row-major.  Sizes are int64 where they
+ *    can exceed 2^31 elements (Traffic: 1.7e9 elements).
+ *  - Results are deterministic: no atomics; a series' arithmetic does not
+ *    depend on the batch it is in, the launch configuration or the device,
+ *    so a sharded run's outputs equal the unsharded run's bitwise.
+ */
+#ifndef PRNET_H
+#define PRNET_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PRNET_ABI_VERSION 1
+
+typedef struct prnet_handle prnet_handle; /* opaque; owned by the library */
+
+typedef enum {
+  PRNET_OK = 0,
+  PRNET_ERR_INVALID_ARG = 1, /* NULL pointer with B > 0, C < 1, S < 2, L < S, H < 1,
+                                tau <= 0 or non-finite, wrong parameter counts, B < 0,
+                                size overflow, wrong abi_version                       */
+  PRNET_ERR_BAD_STATE = 2,   /* forward before load_params; NULL handle                  */
+  PRNET_ERR_UNSUPPORTED = 3, /* device is not sm_100 (cc 10.x); x/y not 16-byte aligned;
+                                x and y overlap; pointer not on the handle's device;
+                                shape beyond the compiled limits (N > 512, S > 128)    */
+  PRNET_ERR_CUDA = 4,        /* CUDA runtime or launch error (text: prnet_last_error)    */
+  PRNET_ERR_OOM = 5          /* device or pinned-host allocation failed                  */
+} prnet_status;
+
+typedef struct {
+  int32_t abi_version;      /* must equal PRNET_ABI_VERSION                               */
+  int32_t channels;         /* C >= 1                                                     */
+  int32_t lookback;         /* L >= seg_len                                               */
+  int32_t seg_len;          /* S >= 2 (A1: S is an input, e.g. the dominant period)      */
+  int32_t horizon;          /* H >= 1                                                     */
+  int32_t head_per_channel; /* 1: ws/wt are [C][M][N], bias [C][H] (A7, NS "per-channel
+                               linear head"); 0: one shared head [1][M][N], [1][H]       */
+  int32_t metric_variant;   /* 0 = the DESIGN.md §3 reading; other values reserved       */
+  float tau_seasonal;       /* tau_s > 0: softmax temperature of the seasonal branch (A6) */
+  float tau_trend;          /* tau_t > 0: softmax temperature of the trend branch (A6)    */
+  int32_t device;           /* CUDA device ordinal the handle is bound to                 */
+} prnet_config;
+
+/* Create a handle: validates cfg, checks the device is compute capability 10.x,
+ * derives N = L / S (floor), r = L - N*S, M = ceil(H / S), allocates the device
+ * parameter buffers.  cfg is copied.  On error *out = NULL and the message is
+ * available through prnet_last_error(NULL) (thread-local). */
+prnet_status prnet_create(const prnet_config* cfg, prnet_handle** out);
+
+/* Copy the head parameters (HOST arrays, row-major) into the handle:
+ *   w_seasonal [Cw][M][N]  -- W_s[c][m][n]: weight of seasonal pattern n for
+ *                             future segment m (A16: n = 0 oldest, m = 0 first)
+ *   w_trend    [Cw][M][N]  -- W_t, same layout
+ *   bias       [Cw][H]
+ * with Cw = C if head_per_channel else 1.  n_w must equal Cw*M*N and n_b Cw*H.
+ * Synchronises the handle's device before overwriting (so it may be called
+ * again between forwards); the caller must not race it with in-flight work. */
+prnet_status prnet_load_params(prnet_handle* h, const float* w_seasonal, const float* w_trend,
+                               const float* bias, int64_t n_w, int64_t n_b);
+
+/* Forward, DEVICE buffers: x [B][C][L] -> y [B][C][H], enqueued on cuda_stream
+ * (a cudaStream_t; NULL = legacy default stream).  Asynchronous: launch errors
+ * are returned, execution errors surface at the caller's next synchronisation.
+ * x and y must be 16-byte aligned and must not overlap.  B = 0 is a no-op.
+ * No workspace, no per-call state: concurrent forwards on different streams
+ * with one handle are allowed. */
+prnet_status prnet_forward(prnet_handle* h, const float* x, int64_t batch, float* y,
+                           void* cuda_stream);
+
+/* Forward, HOST buffers (end-to-end entry): x_host [B][C][L] -> y_host [B][C][H].
+ * The library streams the batch through the GPU in window chunks, overlapping
+ * the host->device copy of chunk k+1, the kernel on chunk k and the
+ * device->host copy of chunk k-1 on its own streams, using a device staging
+ * workspace it owns (allocated on first use, sized by prnet_set_host_chunk).
+ * Blocking: returns after y_host is fully written.  Host buffers may be
+ * pageable, but only page-locked (pinned) memory gets full PCIe bandwidth. */
+prnet_status prnet_forward_host(prnet_handle* h, const float* x_host, int64_t batch,
+                                float* y_host);
+
+/* Windows per chunk for prnet_forward_host (default: ~256 MiB of input per
+ * chunk).  windows_per_chunk >= 1. */
+prnet_status prnet_set_host_chunk(prnet_handle* h, int64_t windows_per_chunk);
+
+/* Release everything the handle owns.  NULL-safe.  Caller must synchronise. */
+void prnet_destroy(prnet_handle* h);
+
+/* Message of the last failure on h (h == NULL: the calling thread's last
+ * prnet_create failure).  Never NULL; valid until the next call on h. */
+const char* prnet_last_error(const prnet_handle* h);
+
+/* Derived sizes: N = floor(L/S), M = ceil(H/S), r = L - N*S. */
+prnet_status prnet_get_dims(const prnet_handle* h, int32_t* N, int32_t* M, int32_t* r);
+
+/* ---- support / debug exports (not on the timed path) ------------------- */
+
+/* seg [B][C][N][S] (device): seg[b][c][n][t] = x[b][c][r + n*S + t]
+ * (Definition step 2, reading A2).  Bit-exact gather. */
+prnet_status prnet_debug_segments(prnet_handle* h, const float* x, int64_t batch, float* seg,
+                                  void* cuda_stream);
+
+/* a_s, a_t [B][C][N][N] (device): the two attention matrices the forward
+ * computes (same kernel, same arithmetic), rows summing to 1.  Requires N <= 32. */
+prnet_status prnet_debug_attention(prnet_handle* h, const float* x, int64_t batch, float* a_s,
+                                   float* a_t, void* cuda_stream);
+
+/* out3 (device, 3 doubles) = {sum (y - target)^2, sum |y - target|, count} over
+ * n = batch*C*H elements, fp64, fixed reduction order (deterministic).  The
+ * per-rank input of the NCCL all-reduce that forms MSE / MAE. */
+prnet_status prnet_error_sums(prnet_handle* h, const float* y, const float* target,
+                              int64_t batch, double* out3, void* cuda_stream);
+
+/* Kernel-level accounting for the bench (host-side, no device work):
+ * kernel_launches = device kernels one prnet_forward(batch) enqueues. */
+prnet_status prnet_forward_plan(const prnet_handle* h, int64_t batch, int32_t* kernel_launches,
+                                int32_t* variant);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PRNET_H */

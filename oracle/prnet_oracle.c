@@ -1,0 +1,242 @@
+/*
+ * prnet_oracle.c -- plain, slow, single-threaded CPU oracle of the PRNet
+ * pattern-attention forward.  TEST INFRASTRUCTURE ONLY (see prnet_oracle.h):
+ * nothing on the product path includes, links or calls this file.
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n (abstract P:18-23,
+ * conclusion P:44-47); "Def k" = SURVEY.md §8(c) "Definition" step k; "Ax" =
+ * SURVEY.md §8(c) ambiguity register entry x (restated in DESIGN.md §3).
+ *
+ * Every function below follows its definition step literally: plain loops in
+ * the order the definition writes them, fp64 arithmetic, no blocking, no
+ * fusion, no reordering, no reuse of one step's loop for another.
+ */
+#include "prnet_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* Def 6: epsilon inside the seasonal (Pearson) normaliser.  A4. */
+static const double ORACLE_EPS_S = 1e-12;
+/* Def 7: epsilon added to the series variance in the trend normaliser.  A5. */
+static const double ORACLE_EPS_T = 1e-5;
+
+/* Def 1: N = floor(L/S) (N >= 1 needs L >= S), r = L - N*S, M = ceil(H/S).
+ * A1 (S is an input), A2 (drop the oldest r points), A3 (M = ceil). */
+int oracle_dims(int32_t L, int32_t S, int32_t H, int32_t* N, int32_t* r, int32_t* M) {
+  if (S < 2 || L < S || H < 1) return -1;
+  *N = L / S;
+  *r = L - (*N) * S;
+  *M = (H + S - 1) / S;
+  return 0;
+}
+
+/* Def 2: segment n holds x[r + n*S + t], t = 0..S-1; n = 0 is the oldest
+ * segment (A2, A16).  P:21 "similarity between segments". */
+static void oracle_segment(const float* x, int N, int S, int r, double* X) {
+  for (int n = 0; n < N; n++)
+    for (int t = 0; t < S; t++)
+      X[n * S + t] = (double)x[r + n * S + t];
+}
+
+/* Def 3-4: mu_n = (1/S) sum_t X_n[t];  z_n = X_n - mu_n;  nu2_n = sum_t z_n[t]^2;
+ * kappa_n = sum_t ttilde_t z_n[t] / V with ttilde_t = t - (S-1)/2 and
+ * V = sum_t ttilde_t^2 = S(S^2-1)/12.  (A4 seasonal descriptors, A5 trend
+ * descriptors; kappa_n is the least-squares slope of segment n.) */
+static void oracle_descriptors(const double* X, int N, int S, double* mu, double* z,
+                               double* nu2, double* kappa) {
+  double V = 0.0;
+  for (int t = 0; t < S; t++) {
+    double tt = (double)t - 0.5 * (double)(S - 1);
+    V += tt * tt;
+  }
+  for (int n = 0; n < N; n++) {
+    double s = 0.0;
+    for (int t = 0; t < S; t++) s += X[n * S + t];
+    mu[n] = s / (double)S;
+    for (int t = 0; t < S; t++) z[n * S + t] = X[n * S + t] - mu[n];
+    double q = 0.0;
+    for (int t = 0; t < S; t++) q += z[n * S + t] * z[n * S + t];
+    nu2[n] = q;
+    double k = 0.0;
+    for (int t = 0; t < S; t++) {
+      double tt = (double)t - 0.5 * (double)(S - 1);
+      k += tt * z[n * S + t];
+    }
+    kappa[n] = k / V;
+  }
+}
+
+/* Def 5: sigma^2 = (1/(N S)) sum_n [nu2_n + S (mu_n - mubar)^2], mubar = mean_n mu_n:
+ * the population variance of the N*S segmented points (A5 normaliser). */
+static double oracle_series_variance(const double* mu, const double* nu2, int N, int S) {
+  double mbar = 0.0;
+  for (int n = 0; n < N; n++) mbar += mu[n];
+  mbar /= (double)N;
+  double acc = 0.0;
+  for (int n = 0; n < N; n++) acc += nu2[n] + (double)S * (mu[n] - mbar) * (mu[n] - mbar);
+  return acc / ((double)N * (double)S);
+}
+
+/* Def 6 (seasonal metric, "two metrics ... seasonal"; A4):
+ * rho_ij = <z_i, z_j> / sqrt((nu2_i + eps_s)(nu2_j + eps_s)). */
+static void oracle_seasonal_similarity(const double* z, const double* nu2, int N, int S,
+                                       double* rho) {
+  for (int i = 0; i < N; i++)
+    for (int j = 0; j < N; j++) {
+      double g = 0.0;
+      for (int t = 0; t < S; t++) g += z[i * S + t] * z[j * S + t];
+      rho[i * N + j] = g / sqrt((nu2[i] + ORACLE_EPS_S) * (nu2[j] + ORACLE_EPS_S));
+    }
+}
+
+/* Def 7 (trend metric, "... or trend"; A5):
+ * D_ij = (mu_i - mu_j)^2 + ((S^2-1)/12) (kappa_i - kappa_j)^2,
+ * which equals (1/S) ||T_i - T_j||^2 for the least-squares lines
+ * T_n[t] = mu_n + kappa_n ttilde_t. */
+static void oracle_trend_distance(const double* mu, const double* kappa, int N, int S,
+                                  double* D) {
+  double c = ((double)S * (double)S - 1.0) / 12.0;
+  for (int i = 0; i < N; i++)
+    for (int j = 0; j < N; j++) {
+      double dm = mu[i] - mu[j];
+      double dk = kappa[i] - kappa[j];
+      D[i * N + j] = dm * dm + c * dk * dk;
+    }
+}
+
+/* Def 8 (pattern attention weights, "pattern attention mechanism"; A6, A9):
+ * A[i][j] = exp(l_ij - max_k l_ik) / sum_k exp(l_ik - max_k l_ik), dense over all
+ * j including j = i, where l_ij = sign * m_ij / tau. */
+static void oracle_softmax_rows(const double* m, int N, double sign, double scale_inv,
+                                double* A) {
+  for (int i = 0; i < N; i++) {
+    double mx = -INFINITY;
+    for (int j = 0; j < N; j++) {
+      double l = sign * m[i * N + j] * scale_inv;
+      if (l > mx) mx = l;
+    }
+    double s = 0.0;
+    for (int j = 0; j < N; j++) s += exp(sign * m[i * N + j] * scale_inv - mx);
+    for (int j = 0; j < N; j++) A[i * N + j] = exp(sign * m[i * N + j] * scale_inv - mx) / s;
+  }
+}
+
+/* Def 9 (aggregation into patterns, "aggregates similar segments to
+ * extract patterns"; A10): P = A X, (N x N)(N x S). */
+static void oracle_aggregate(const double* A, const double* X, int N, int S, double* P) {
+  for (int i = 0; i < N; i++)
+    for (int t = 0; t < S; t++) {
+      double s = 0.0;
+      for (int j = 0; j < N; j++) s += A[i * N + j] * X[j * S + t];
+      P[i * S + t] = s;
+    }
+}
+
+/* Def 10-11 (linear head, NS "the per-channel linear head maps to the
+ * forecast horizon"; A7, A8, A11, A3):
+ * Y[m][t] = sum_n ws[m][n] P_s[n][t] + wt[m][n] P_t[n][t];
+ * y[h] = Y[h div S][h mod S] + b[h], h = 0..H-1. */
+static void oracle_head(const double* Ps, const double* Pt, const float* ws, const float* wt,
+                        const float* bias, int N, int S, int M, int H, double* Yfull,
+                        double* y) {
+  for (int m = 0; m < M; m++)
+    for (int t = 0; t < S; t++) {
+      double s = 0.0;
+      for (int n = 0; n < N; n++)
+        s += (double)ws[m * N + n] * Ps[n * S + t] + (double)wt[m * N + n] * Pt[n * S + t];
+      Yfull[m * S + t] = s;
+    }
+  for (int h = 0; h < H; h++) y[h] = Yfull[(h / S) * S + (h % S)] + (double)bias[h];
+}
+
+int oracle_series(const float* x, int32_t L, int32_t S, int32_t H, const float* ws,
+                  const float* wt, const float* bias, double tau_s, double tau_t, double* y,
+                  const oracle_debug* dbg) {
+  int32_t N, r, M;
+  if (oracle_dims(L, S, H, &N, &r, &M) != 0) return -1;
+  if (!(tau_s > 0.0) || !(tau_t > 0.0)) return -1;
+  size_t nS = (size_t)N * S, nN = (size_t)N * N, mS = (size_t)M * S;
+  double* X = (double*)malloc(nS * sizeof(double));
+  double* z = (double*)malloc(nS * sizeof(double));
+  double* mu = (double*)malloc(N * sizeof(double));
+  double* nu2 = (double*)malloc(N * sizeof(double));
+  double* kap = (double*)malloc(N * sizeof(double));
+  double* rho = (double*)malloc(nN * sizeof(double));
+  double* D = (double*)malloc(nN * sizeof(double));
+  double* Dh = (double*)malloc(nN * sizeof(double));
+  double* As = (double*)malloc(nN * sizeof(double));
+  double* At = (double*)malloc(nN * sizeof(double));
+  double* Ps = (double*)malloc(nS * sizeof(double));
+  double* Pt = (double*)malloc(nS * sizeof(double));
+  double* Yf = (double*)malloc(mS * sizeof(double));
+
+  oracle_segment(x, N, S, r, X);                                   /* Def 2   */
+  oracle_descriptors(X, N, S, mu, z, nu2, kap);                    /* Def 3-4 */
+  double sigma2 = oracle_series_variance(mu, nu2, N, S);           /* Def 5   */
+  oracle_seasonal_similarity(z, nu2, N, S, rho);                   /* Def 6   */
+  oracle_trend_distance(mu, kap, N, S, D);                         /* Def 7   */
+  for (size_t k = 0; k < nN; k++) Dh[k] = D[k] / (sigma2 + ORACLE_EPS_T);
+  oracle_softmax_rows(rho, N, +1.0, 1.0 / tau_s, As);              /* Def 8   */
+  oracle_softmax_rows(Dh, N, -1.0, 1.0 / tau_t, At);               /* Def 8   */
+  oracle_aggregate(As, X, N, S, Ps);                               /* Def 9   */
+  oracle_aggregate(At, X, N, S, Pt);                               /* Def 9   */
+  oracle_head(Ps, Pt, ws, wt, bias, N, S, M, H, Yf, y);            /* Def 10-11 */
+
+  if (dbg) {
+    if (dbg->seg) memcpy(dbg->seg, X, nS * sizeof(double));
+    if (dbg->mu) memcpy(dbg->mu, mu, N * sizeof(double));
+    if (dbg->nu2) memcpy(dbg->nu2, nu2, N * sizeof(double));
+    if (dbg->kappa) memcpy(dbg->kappa, kap, N * sizeof(double));
+    if (dbg->sigma2) dbg->sigma2[0] = sigma2;
+    if (dbg->rho) memcpy(dbg->rho, rho, nN * sizeof(double));
+    if (dbg->dist) memcpy(dbg->dist, D, nN * sizeof(double));
+    if (dbg->a_s) memcpy(dbg->a_s, As, nN * sizeof(double));
+    if (dbg->a_t) memcpy(dbg->a_t, At, nN * sizeof(double));
+    if (dbg->p_s) memcpy(dbg->p_s, Ps, nS * sizeof(double));
+    if (dbg->p_t) memcpy(dbg->p_t, Pt, nS * sizeof(double));
+    if (dbg->y_full) memcpy(dbg->y_full, Yf, mS * sizeof(double));
+  }
+  free(X); free(z); free(mu); free(nu2); free(kap); free(rho); free(D); free(Dh);
+  free(As); free(At); free(Ps); free(Pt); free(Yf);
+  return 0;
+}
+
+int oracle_forward(const float* x, int64_t B, int32_t C, int32_t L, int32_t S, int32_t H,
+                   const float* ws, const float* wt, const float* bias,
+                   int32_t head_per_channel, double tau_s, double tau_t, float* y,
+                   double* y64) {
+  int32_t N, r, M;
+  if (B < 0 || C < 1 || oracle_dims(L, S, H, &N, &r, &M) != 0) return -1;
+  double* yy = (double*)malloc((size_t)H * sizeof(double));
+  for (int64_t b = 0; b < B; b++)
+    for (int32_t c = 0; c < C; c++) {
+      int64_t cw = head_per_channel ? c : 0;
+      const float* xs = x + (b * C + c) * (int64_t)L;
+      if (oracle_series(xs, L, S, H, ws + cw * M * N, wt + cw * M * N, bias + cw * H, tau_s,
+                        tau_t, yy, NULL) != 0) {
+        free(yy);
+        return -1;
+      }
+      for (int32_t h = 0; h < H; h++) {
+        int64_t o = (b * C + c) * (int64_t)H + h;
+        if (y) y[o] = (float)yy[h];
+        if (y64) y64[o] = yy[h];
+      }
+    }
+  free(yy);
+  return 0;
+}
+
+void oracle_error_sums(const float* y, const float* target, int64_t n, double* out3) {
+  double sse = 0.0, sae = 0.0;
+  for (int64_t i = 0; i < n; i++) {
+    double d = (double)y[i] - (double)target[i];
+    sse += d * d;
+    sae += fabs(d);
+  }
+  out3[0] = sse;
+  out3[1] = sae;
+  out3[2] = (double)n;
+}

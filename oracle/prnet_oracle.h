@@ -1,0 +1,82 @@
+/*
+ * prnet_oracle.h -- CPU ORACLE for the PRNet pattern-attention forward.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this code.  The
+ * product path (paper_2404_02445_b200/, libprnet.so) never includes, links or
+ * calls it, and shares no header, helper or constant with it.
+ *
+ * What it computes (one (window, channel) series x in R^L at a time):
+ *   PAPER.md:19-22 (abstract): segments, "two metrics to evaluate the similarity
+ *   between segments which contain different dominant patterns (seasonal or
+ *   trend)", "a pattern attention mechanism, which aggregates similar segments
+ *   to extract patterns for forecasting"; PAPER.md:45 (conclusion).  The
+ *   method sections (\subfile lines) have no body, so every
+ *   formula is the reading fixed in SURVEY.md §8(c) "Definition" steps 1-11
+ *   and ambiguity register A1-A18, restated in DESIGN.md §3.
+ *
+ * Arithmetic: inputs are fp32 (as the C-ABI receives them); every quantity is
+ * computed in IEEE double, single-threaded, in the order the definition
+ * states; the output is rounded once to fp32 (plus an fp64 copy for tests).
+ *
+ * Parity status of each function: see the comment above it in
+ * prnet_oracle.c and DESIGN.md §4 (pins).  The formulas themselves are
+ * "parity unpinned" against the paper's own equations (absent from the
+ * reference); they are pinned against the closed forms,
+ * invariants, limits and worked examples listed there.
+ */
+#ifndef PRNET_ORACLE_H
+#define PRNET_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Per-series intermediates (all caller-allocated; any pointer may be NULL).
+ * Sizes: seg N*S, mu/nu2/kappa N, rho/dist/a_s/a_t N*N, p_s/p_t N*S,
+ * y_full M*S, y H. Row-major. */
+typedef struct {
+  double* seg;     /* X[n][t]                      (Definition step 2)  */
+  double* mu;      /* mu_n                          (step 4)             */
+  double* nu2;     /* nu^2_n                        (step 4)             */
+  double* kappa;   /* kappa_n                       (step 4)             */
+  double* sigma2;  /* [1] sigma^2                   (step 5)             */
+  double* rho;     /* rho_ij                        (step 6)             */
+  double* dist;    /* D_ij (unnormalised)           (step 7)             */
+  double* a_s;     /* A_s                           (step 8)             */
+  double* a_t;     /* A_t                           (step 8)             */
+  double* p_s;     /* P_s = A_s X                   (step 9)             */
+  double* p_t;     /* P_t = A_t X                   (step 9)             */
+  double* y_full;  /* Y[m][t] before truncation     (step 10)            */
+} oracle_debug;
+
+/* Derived sizes (Definition step 1).  Returns 0 on success, -1 if S < 2,
+ * L < S or H < 1. */
+int oracle_dims(int32_t L, int32_t S, int32_t H, int32_t* N, int32_t* r, int32_t* M);
+
+/* One series.  x: L fp32 values; ws, wt: M*N (row m = future segment m,
+ * column n = pattern n); bias: H.  y: H doubles.  dbg may be NULL.
+ * Returns 0, or -1 on invalid dims / tau <= 0. */
+int oracle_series(const float* x, int32_t L, int32_t S, int32_t H,
+                  const float* ws, const float* wt, const float* bias,
+                  double tau_s, double tau_t, double* y, const oracle_debug* dbg);
+
+/* A batch x[B][C][L] -> y[B][C][H] (fp32, rounded from the fp64 result) and
+ * optionally y64 (fp64).  head_per_channel: 1 -> ws/wt are [C][M][N], bias
+ * [C][H]; 0 -> [1][M][N], [1][H].  Series are processed in (b, c) order,
+ * one after the other.  Returns 0 or -1. */
+int oracle_forward(const float* x, int64_t B, int32_t C, int32_t L, int32_t S,
+                   int32_t H, const float* ws, const float* wt, const float* bias,
+                   int32_t head_per_channel, double tau_s, double tau_t,
+                   float* y, double* y64);
+
+/* Sum of squared and absolute errors of y against target (n values), fp64,
+ * in index order: out[0] = SSE, out[1] = SAE, out[2] = n.  (Bench metric,
+ * PAPER.md:22 "accuracy"; MSE = SSE/n, MAE = SAE/n.) */
+void oracle_error_sums(const float* y, const float* target, int64_t n, double* out3);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
