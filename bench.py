@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Bench of the PRNet pattern-attention forward on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload traffic] [--impl ours|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+One step = one prnet_forward over the workload's whole test set (every
+(window, channel) series), inputs resident in HBM.  Windows are sharded across
+ranks (contiguous balanced ranges, no collective on the hot path); the only
+collective is the all-reduce of the fp64 error sums (MSE/MAE) after the timed
+region, plus the MAX of per-rank times.  Rank 0 prints ONE JSON line.
+
+--impl reference times the CPU oracle (oracle/, as it stands) on the host
+cores on a bounded sample of the same workload -- this tier's reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "PRNet forward windows/sec and HBM GB/s vs peak at 1/2/4/8 B200"
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return dict(FALLBACK_PEAKS), "fallback (B200_PROFILING.md)"
+
+
+def flops_per_series(N, S, M):
+    """Algorithmic FLOPs of the folded formulation: Gram 2N^2S,
+    fold Q = W_s A_s + W_t A_t 4MN^2, Y = Q X 2MNS."""
+    return 2 * N * N * S + 4 * M * N * N + 2 * M * N * S
+
+
+# ------------------------------------------------------------------ clocks (NVML, sampled in a thread)
+class ClockSampler:
+    BAD = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+           "hw_power_brake": 0x80}
+    ALL = {"gpu_idle": 0x1, "applications_clocks": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+           "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+           "hw_power_brake": 0x80, "display_clocks": 0x100}
+
+    def __init__(self, device_index, period_s=0.005):
+        self.samples, self.reasons = [], 0
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - no NVML
+            self.err = str(e)
+        self.period = period_s
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml_unavailable"]}
+        reasons = [k for k, v in self.ALL.items() if self.reasons & v]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ CPU oracle leg
+def _oracle_chunk(args):
+    name, seed, widx, chans = args
+    import oracle
+    w = synth.WORKLOADS[name]
+    N, _, M = synth.derived_dims(w.L, w.S, w.H)
+    s = synth.make_series(w, seed, channels=chans)
+    x, _ = synth.window_batch(s, w, widx)
+    ws, wt, b = synth.make_params(w.C, M, N, w.H, True, seed, w.cfg_id)
+    t0 = time.perf_counter()
+    oracle.forward(x, w.S, w.H, ws[chans], wt[chans], b[chans], True)
+    return time.perf_counter() - t0, len(widx) * len(chans)
+
+
+def cpu_oracle_rate(name, seed, budget_s=12.0, cores=None):
+    """Time the oracle on a bounded sample: whole windows (all channels) spread over
+    the test set, split by channel blocks over `cores` processes.  Returns
+    (windows/s, series/s, cores, sample description)."""
+    import multiprocessing as mp
+    import oracle
+    oracle.build()
+    w = synth.WORKLOADS[name]
+    N, _, M = synth.derived_dims(w.L, w.S, w.H)
+    cores = cores or len(os.sched_getaffinity(0))
+    # calibrate on one window's first few channels
+    dt, n = _oracle_chunk((name, seed, [0], list(range(min(w.C, 8)))))
+    per_series = dt / n
+    n_series = max(w.C, int(budget_s * cores / per_series))
+    n_win = max(1, min(w.windows, n_series // w.C))
+    widx = np.unique(np.linspace(0, w.windows - 1, n_win).astype(int)).tolist()
+    blocks = np.array_split(np.arange(w.C), min(cores, w.C))
+    jobs = [(name, seed, widx, blk.tolist()) for blk in blocks if len(blk)]
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(len(jobs)) as pool:
+        res = pool.map(_oracle_chunk, jobs)
+    wall = time.perf_counter() - t0
+    series = sum(r[1] for r in res)
+    compute = max(r[0] for r in res)
+    rate_series = series / compute
+    return (rate_series / w.C, rate_series, len(jobs),
+            f"{len(widx)} of {w.windows} windows x {w.C} channels ({series} series), "
+            f"{len(jobs)} processes x 1 thread, {compute:.1f} s (wall {wall:.1f} s)")
+
+
+# ------------------------------------------------------------------ distributed helpers
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="traffic", choices=sorted(synth.WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seed", type=int, default=synth.DEFAULT_SEED)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no extras)")
+    args = ap.parse_args()
+
+    rank, world, local = dist_env()
+    w = synth.WORKLOADS[args.workload]
+    N, r, M = synth.derived_dims(w.L, w.S, w.H)
+    B = w.windows
+    cfg = {"workload": w.name, "windows": B, "C": w.C, "L": w.L, "S": w.S, "H": w.H, "N": N,
+           "M": M, "series_per_step": B * w.C, "head": "per-channel",
+           "l2": f"inputs larger than L2 ({B * w.C * w.L * 4 / 1e9:.2f} GB read per step)",
+           "parallelism": f"dp{world}", "seed": args.seed}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        times = []
+        for _ in range(args.warmup + args.steps):
+            wps, sps, cores, sample = cpu_oracle_rate(w.name, args.seed,
+                                                      budget_s=max(1.0, args.cpu_budget / 4))
+            times.append(1.0 / wps)
+        t = times[args.warmup:]
+        value = 1.0 / statistics.mean(t)
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": value, "unit": "windows/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * B / value, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+            "cpu_baseline": {"value": value, "unit": "windows/s", "cores": cores,
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "windows/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}), flush=True)
+        return 0
+
+    import torch
+    import torch.distributed as dist
+    from paper_2404_02445_b200 import PRNet, all_reduce_error_sums, shard_windows
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    start, count = shard_windows(B, world, rank)
+    peaks, peak_src = measured_peaks()
+
+    # ---- inputs: this rank's windows, materialised in HBM (outside the timed region)
+    series = synth.make_series(w, args.seed)
+    sd = torch.from_numpy(series).cuda()
+    x = sd.unfold(1, w.L, 1)[:, w.t0 + start:w.t0 + start + count, :].permute(1, 0, 2).contiguous()
+    tgt = sd[:, w.L:].unfold(1, w.H, 1)[:, w.t0 + start:w.t0 + start + count, :] \
+        .permute(1, 0, 2).contiguous()
+    del sd
+    ws, wt, b = synth.make_params(w.C, M, N, w.H, True, args.seed, w.cfg_id)
+    model = PRNet(w.C, w.L, w.S, w.H, device=local).load(ws, wt, b)
+    y = torch.empty((count, w.C, w.H), dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    plan = model.plan(count)
+
+    for _ in range(args.warmup):
+        model.forward_into(x, y, stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        t_wall = time.perf_counter()
+        for e0, e1 in ev:
+            e0.record(stream)
+            model.forward_into(x, y, stream)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    per_launch = [e0.elapsed_time(e1) for e0, e1 in ev]          # ms, on the launching stream
+    total_ms = ev[0][0].elapsed_time(ev[-1][1])
+    tt = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    total_ms_max = float(tt.item())
+    ms_per_step = total_ms_max / args.steps
+
+    # ---- accuracy metric of this forward (K6 error sums + the one NCCL all-reduce)
+    sums = model.error_sums(y, tgt)
+    mse, mae = all_reduce_error_sums(sums)
+
+    if args.profile:
+        if rank == 0:
+            print(json.dumps({"profile_run": True, "ms_per_step": ms_per_step}), flush=True)
+        return 0
+
+    # ---- end to end through the public API with HOST buffers (H2D + kernel + D2H timed)
+    e2e = None
+    if not args.no_e2e:
+        try:
+            xh = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
+            xh.copy_(x)
+            yh = torch.empty(y.shape, dtype=torch.float32, pin_memory=True)
+            model.forward_host(xh, yh)          # warm-up (allocates the staging ring)
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            for _ in range(args.e2e_steps):
+                model.forward_host(xh, yh)
+            dt = torch.tensor([(time.perf_counter() - t0) / args.e2e_steps], dtype=torch.float64,
+                              device="cuda")
+            if world > 1:
+                dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            assert torch.equal(yh, y.cpu()), "host path disagrees with the device path"
+            e2e = {"value": B / float(dt.item()), "unit": "windows/s",
+                   "h2d_bytes_per_step": int(xh.numel() * 4) * world,
+                   "d2h_bytes_per_step": int(yh.numel() * 4) * world,
+                   "steps": args.e2e_steps, "path": "prnet_forward_host (pinned host buffers)"}
+            del xh, yh
+        except Exception as ex:  # report, never fake
+            e2e = {"value": None, "unit": "windows/s", "error": str(ex)[:200]}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    value = B / (ms_per_step / 1e3)
+    bytes_per_series = 4 * (w.L + w.H)
+    launch_ms = statistics.mean(per_launch)
+    achieved_gbs = count * w.C * bytes_per_series / (launch_ms / 1e3) / 1e9
+    peak_gbs = float(peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"]))
+    fl = flops_per_series(N, w.S, M)
+    achieved_tf = count * w.C * fl / (launch_ms / 1e3) / 1e12
+    clocks = clk.summary()
+    sm_clock = (clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0))
+    fp32_peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(w.name)
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            wps, sps, cores, sample = cpu_oracle_rate(w.name, args.seed, args.cpu_budget)
+            cpu = {"value": wps, "unit": "windows/s", "cores": cores, "kind": "oracle",
+                   "sample": sample, "series_per_s": sps}
+        except Exception as ex:
+            cpu = {"value": None, "unit": "windows/s", "error": str(ex)[:200]}
+
+    out = {
+        "metric": METRIC, "value": value, "unit": "windows/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seasonal+trend+noise series, random-init head; DESIGN.md §5)",
+        "config": cfg,
+        "series_per_s": value * w.C,
+        "hbm_gbs": B * w.C * bytes_per_series / (ms_per_step / 1e3) / 1e9,
+        "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak_gbs, "unit": "GB/s",
+                     "frac": achieved_gbs / peak_gbs, "traffic": traffic,
+                     "kernel": f"prnet_fwd_{plan['variant']}", "launch_ms": launch_ms,
+                     "bytes_per_launch": count * w.C * bytes_per_series, "peak_source": peak_src},
+        "roofline_alu": {"bound": "alu", "achieved": achieved_tf, "unit": "TFLOP/s",
+                         "peak": fp32_peak, "frac": achieved_tf / fp32_peak,
+                         "flops_per_series": fl,
+                         "peak_note": "FP32 FFMA: 148 SMs x 128 lanes x 2 x max SM clock"},
+        "accuracy": {"mse": mse, "mae": mae},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": plan["kernel_launches"] * args.steps,
+        "clocks": clocks,
+        "wall_s_timed_region": t_wall,
+    }
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

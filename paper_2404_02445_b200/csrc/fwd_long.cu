@@ -1,0 +1,229 @@
+// fwd_long.cu -- fused PRNet pattern-attention forward for 32 < N <= 512
+// segments per series (the long-lookback points of the stress sweep,
+// BASELINE.json configs[4]: L up to 5760, S down to 12 -> N up to 480).
+//
+// The N x N similarity matrices no longer fit a warp's registers, and at
+// N = 480 not even shared memory (2 x 922 KB), so the kernel streams rows:
+// one CTA owns one series; warp w takes query rows i = w, w + nwarps, ...;
+// for row i the lanes cover the keys j = lane + 32 k, compute the row's
+// seasonal and trend logits, softmax them with warp reductions, aggregate
+// the pattern rows P_s[i][:], P_t[i][:] (Def 9) and immediately fold them
+// into the head accumulator Y[m][t] += W_s[m][i] P_s[i][t] + W_t[m][i] P_t[i][t]
+// (Def 10) kept per warp in shared memory.  A fixed-order reduction over the
+// warps then adds the bias (Def 11).  The same reading and the
+// same step map as fwd_warp.cu.
+#include "prnet_internal.cuh"
+
+namespace prnet {
+
+template <int KJ>
+__global__ void __launch_bounds__(256) prnet_fwd_long_kernel(FwdArgs a, int rs) {
+  extern __shared__ float4 smem4[];
+  float* smem = reinterpret_cast<float*>(smem4);
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  const int S = a.S, N = a.N, M = a.M, H = a.H, L = a.L, C = a.C;
+  const int MS = M * S;
+
+  float* xr = smem;               // [N][rs]  segments, odd row stride
+  float* zr = xr + N * rs;        // [N][rs]  z
+  float* muS = zr + N * rs;       // [N]
+  float* kapS = muS + N;          // [N]
+  float* invS = kapS + N;         // [N]
+  float* red = invS + N;          // [64]     block reduction scratch
+  float* wrow = red + 64;         // [nwarps][2][N]  softmax rows
+  float* yw = wrow + nwarps * 2 * N;  // [nwarps][M*S] per-warp head accumulators
+
+  const int64_t total = a.B * (int64_t)C;
+  for (int64_t series = blockIdx.x; series < total; series += gridDim.x) {
+    const int c = (int)(series % C);
+    const int cw = a.head_per_channel ? c : 0;
+    const float* gws = a.ws + (int64_t)cw * M * N;
+    const float* gwt = a.wt + (int64_t)cw * M * N;
+
+    // ---- a1: load + segment
+    const float* xg = a.x + series * L + a.r;
+    for (int k = threadIdx.x; k < N * S; k += blockDim.x) {
+      const int n = k / S, t = k - n * S;
+      xr[n * rs + t] = __ldg(xg + k);
+    }
+    for (int k = lane; k < MS; k += 32) yw[warp * MS + k] = 0.f;
+    __syncthreads();
+
+    // ---- a2: descriptors, one thread per segment (shifted by the first value)
+    for (int n = threadIdx.x; n < N; n += blockDim.x) {
+      const float* row = xr + n * rs;
+      const float x0 = row[0];
+      float s = 0.f;
+      for (int t = 0; t < S; t++) s += row[t] - x0;
+      const float m1 = s * a.inv_s;
+      float nu2 = 0.f, kap = 0.f;
+      for (int t = 0; t < S; t++) {
+        const float z = (row[t] - x0) - m1;
+        nu2 = fmaf(z, z, nu2);
+        kap = fmaf((float)t - a.half_s, z, kap);
+        zr[n * rs + t] = z;
+      }
+      muS[n] = x0 + m1;
+      kapS[n] = kap * a.inv_v;
+      invS[n] = rsqrtf(nu2 + kEpsSeasonal);
+      // stash nu2 for sigma^2 in the wrow scratch (free until phase 2)
+      wrow[n] = nu2;
+    }
+    __syncthreads();
+    // sigma^2: fixed-order block reduction (deterministic)
+    float part = 0.f;
+    for (int n = threadIdx.x; n < N; n += blockDim.x) part += muS[n];
+    part = warp_sum(part);
+    if (lane == 0) red[warp] = part;
+    __syncthreads();
+    float mbar = 0.f;
+    for (int w = 0; w < nwarps; w++) mbar += red[w];
+    mbar *= a.inv_n;
+    __syncthreads();
+    part = 0.f;
+    for (int n = threadIdx.x; n < N; n += blockDim.x) {
+      const float d = muS[n] - mbar;
+      part += wrow[n] + (float)S * d * d;
+    }
+    part = warp_sum(part);
+    if (lane == 0) red[32 + warp] = part;
+    __syncthreads();
+    float sig = 0.f;
+    for (int w = 0; w < nwarps; w++) sig += red[32 + w];
+    const float inv_var = 1.0f / (sig * a.inv_ns + kEpsTrend);
+    __syncthreads();  // wrow scratch is reused below
+
+    // ---- a3..a7 streamed over query rows
+    float* wr = wrow + warp * 2 * N;
+    for (int i = warp; i < N; i += nwarps) {
+      float g[KJ];
+#pragma unroll
+      for (int k = 0; k < KJ; k++) g[k] = 0.f;
+      const float* zi = zr + i * rs;
+      for (int t = 0; t < S; t++) {
+        const float zv = zi[t];
+#pragma unroll
+        for (int k = 0; k < KJ; k++) {
+          const int j = lane + 32 * k;
+          if (j < N) g[k] = fmaf(zv, zr[j * rs + t], g[k]);
+        }
+      }
+      const float inv_i = invS[i], mu_i = muS[i], k_i = kapS[i];
+      // seasonal softmax
+      float mx = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < KJ; k++) {
+        const int j = lane + 32 * k;
+        g[k] = j < N ? g[k] * inv_i * invS[j] : -INFINITY;
+        mx = fmaxf(mx, g[k]);
+      }
+      mx = warp_max(mx);
+      float sum = 0.f;
+#pragma unroll
+      for (int k = 0; k < KJ; k++) {
+        const int j = lane + 32 * k;
+        g[k] = j < N ? fast_ex2((g[k] - mx) * a.ks) : 0.f;
+        sum += g[k];
+      }
+      float rsum = 1.0f / warp_sum(sum);
+#pragma unroll
+      for (int k = 0; k < KJ; k++) {
+        const int j = lane + 32 * k;
+        if (j < N) wr[j] = g[k] * rsum;
+      }
+      // trend softmax
+      mx = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < KJ; k++) {
+        const int j = lane + 32 * k;
+        float v = -INFINITY;
+        if (j < N) {
+          const float dm = mu_i - muS[j], dk = k_i - kapS[j];
+          v = -(fmaf(a.vtrend * dk, dk, dm * dm) * inv_var);
+        }
+        g[k] = v;
+        mx = fmaxf(mx, v);
+      }
+      mx = warp_max(mx);
+      sum = 0.f;
+#pragma unroll
+      for (int k = 0; k < KJ; k++) {
+        const int j = lane + 32 * k;
+        g[k] = j < N ? fast_ex2((g[k] - mx) * a.kt) : 0.f;
+        sum += g[k];
+      }
+      rsum = 1.0f / warp_sum(sum);
+#pragma unroll
+      for (int k = 0; k < KJ; k++) {
+        const int j = lane + 32 * k;
+        if (j < N) wr[N + j] = g[k] * rsum;
+      }
+      __syncwarp();
+      // a6: P_s[i][t], P_t[i][t] by lane t; a7: fold row i into Y
+      for (int t = lane; t < S; t += 32) {
+        float ps = 0.f, pt = 0.f;
+        for (int j = 0; j < N; j++) {
+          const float xv = xr[j * rs + t];
+          ps = fmaf(wr[j], xv, ps);
+          pt = fmaf(wr[N + j], xv, pt);
+        }
+        float* yr = yw + warp * MS + t;
+        for (int m = 0; m < M; m++)
+          yr[m * S] = fmaf(__ldg(gws + m * N + i), ps, fmaf(__ldg(gwt + m * N + i), pt, yr[m * S]));
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    // ---- a8: fixed-order reduction over warps + bias
+    const float* gb = a.bias + (int64_t)cw * H;
+    float* yg = a.y + series * H;
+    for (int h = threadIdx.x; h < H; h += blockDim.x) {
+      float v = 0.f;
+      for (int w = 0; w < nwarps; w++) v += yw[w * MS + h];
+      yg[h] = v + gb[h];
+    }
+    __syncthreads();
+  }
+}
+
+bool plan_long_kernel(const FwdArgs& a, int max_smem_optin, int sm_count, LongPlan* p) {
+  if (a.N > 512) return false;
+  p->kjmax = a.N <= 64 ? 2 : (a.N <= 128 ? 4 : (a.N <= 256 ? 8 : 16));
+  p->rs = a.S | 1;
+  p->warps_per_cta = 8;
+  const size_t floats = (size_t)2 * a.N * p->rs + 3 * a.N + 64 +
+                        (size_t)p->warps_per_cta * (2 * a.N + a.M * a.S);
+  p->smem_bytes = floats * sizeof(float);
+  if (p->smem_bytes > (size_t)max_smem_optin) return false;
+  const int64_t total = a.B * (int64_t)a.C;
+  int per_sm = (int)((228 * 1024) / (p->smem_bytes + 1024));
+  if (per_sm < 1) per_sm = 1;
+  if (per_sm > 8) per_sm = 8;
+  int64_t g = (int64_t)sm_count * per_sm;
+  p->grid = (int)(total < g ? total : g);
+  if (p->grid < 1) p->grid = 1;
+  return true;
+}
+
+template <int KJ>
+static cudaError_t launch_t(const FwdArgs& a, const LongPlan& p, cudaStream_t st) {
+  auto k = prnet_fwd_long_kernel<KJ>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)p.smem_bytes);
+  if (e != cudaSuccess) return e;
+  k<<<p.grid, 32 * p.warps_per_cta, p.smem_bytes, st>>>(a, p.rs);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_long_kernel(const FwdArgs& a, const LongPlan& p, cudaStream_t st) {
+  switch (p.kjmax) {
+    case 2: return launch_t<2>(a, p, st);
+    case 4: return launch_t<4>(a, p, st);
+    case 8: return launch_t<8>(a, p, st);
+    default: return launch_t<16>(a, p, st);
+  }
+}
+
+}  // namespace prnet

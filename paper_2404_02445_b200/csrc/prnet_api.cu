@@ -1,0 +1,395 @@
+// prnet_api.cu -- the C ABI of include/prnet.h: validation, handle state,
+// kernel-variant selection, and the host-buffer streaming runtime
+// (prnet_forward_host).  No torch types, no exceptions across the boundary.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/prnet.h"
+#include "prnet_internal.cuh"
+
+struct prnet_handle {
+  prnet_config cfg;
+  int N, r, M, Cw;
+  int sm_count, max_smem_optin;
+  float* d_ws = nullptr;
+  float* d_wt = nullptr;
+  float* d_b = nullptr;
+  double* d_err = nullptr;  // error-sum partials
+  bool loaded = false;
+  std::string err;
+  // host-forward runtime
+  int64_t host_chunk = 0;   // windows per chunk (0 = default)
+  int64_t stage_windows = 0;
+  static constexpr int kStages = 3;
+  float* d_xstage[kStages] = {nullptr, nullptr, nullptr};
+  float* d_ystage[kStages] = {nullptr, nullptr, nullptr};
+  cudaStream_t streams[kStages] = {nullptr, nullptr, nullptr};
+};
+
+namespace {
+
+thread_local std::string g_create_error;
+
+prnet_status fail(prnet_handle* h, prnet_status s, const std::string& msg) {
+  if (h) h->err = msg;
+  else g_create_error = msg;
+  return s;
+}
+
+prnet_status cuda_fail(prnet_handle* h, cudaError_t e, const char* what) {
+  std::string m = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) +
+                  ")";
+  return fail(h, e == cudaErrorMemoryAllocation ? PRNET_ERR_OOM : PRNET_ERR_CUDA, m);
+}
+
+// RAII device switch (the caller's current device is restored).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    if (cudaGetDevice(&cur) == cudaSuccess && prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+prnet::FwdArgs make_args(const prnet_handle* h, const float* x, int64_t B, float* y) {
+  prnet::FwdArgs a{};
+  const prnet_config& c = h->cfg;
+  a.x = x;
+  a.y = y;
+  a.ws = h->d_ws;
+  a.wt = h->d_wt;
+  a.bias = h->d_b;
+  a.B = B;
+  a.C = c.channels;
+  a.L = c.lookback;
+  a.S = c.seg_len;
+  a.H = c.horizon;
+  a.N = h->N;
+  a.r = h->r;
+  a.M = h->M;
+  a.head_per_channel = c.head_per_channel ? 1 : 0;
+  a.ks = prnet::kLog2e / c.tau_seasonal;
+  a.kt = prnet::kLog2e / c.tau_trend;
+  const double S = c.seg_len;
+  a.half_s = (float)(0.5 * (S - 1.0));
+  a.inv_v = (float)(12.0 / (S * (S * S - 1.0)));
+  a.vtrend = (float)((S * S - 1.0) / 12.0);
+  a.inv_s = (float)(1.0 / S);
+  a.inv_n = (float)(1.0 / h->N);
+  a.inv_ns = (float)(1.0 / ((double)h->N * S));
+  return a;
+}
+
+// Checks a device pointer lives on the handle's device.
+prnet_status check_dev_ptr(prnet_handle* h, const void* p, const char* name) {
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(h, PRNET_ERR_UNSUPPORTED, std::string(name) + " is not a CUDA pointer");
+  }
+  if (!(at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) ||
+      at.device != h->cfg.device)
+    return fail(h, PRNET_ERR_UNSUPPORTED,
+                std::string(name) + " is not device memory on device " +
+                    std::to_string(h->cfg.device));
+  return PRNET_OK;
+}
+
+bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+  uintptr_t pa = (uintptr_t)a, pb = (uintptr_t)b;
+  return pa < pb + nb && pb < pa + na;
+}
+
+int pick_variant(const prnet_handle* h) { return h->N <= 32 ? 0 : 1; }
+
+// Enqueue the forward for B windows (pointers already validated).
+prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* y, float* a_s,
+                             float* a_t, cudaStream_t st) {
+  prnet::FwdArgs a = make_args(h, x, B, y);
+  a.a_s_dbg = a_s;
+  a.a_t_dbg = a_t;
+  cudaError_t e;
+  if (pick_variant(h) == 0) {
+    prnet::WarpPlan p;
+    if (!prnet::plan_warp_kernel(a, h->max_smem_optin, &p))
+      return fail(h, PRNET_ERR_UNSUPPORTED, "shape exceeds the N<=32 kernel's shared memory");
+    e = prnet::launch_warp_kernel(a, p, st);
+  } else {
+    prnet::LongPlan p;
+    if (!prnet::plan_long_kernel(a, h->max_smem_optin, h->sm_count, &p))
+      return fail(h, PRNET_ERR_UNSUPPORTED, "shape exceeds the long-N kernel's limits");
+    e = prnet::launch_long_kernel(a, p, st);
+  }
+  if (e != cudaSuccess) return cuda_fail(h, e, "forward launch");
+  return PRNET_OK;
+}
+
+prnet_status validate_forward(prnet_handle* h, const float* x, int64_t B, const float* y,
+                              bool device_ptrs) {
+  if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
+  if (!h->loaded) return fail(h, PRNET_ERR_BAD_STATE, "forward before prnet_load_params");
+  if (B < 0) return fail(h, PRNET_ERR_INVALID_ARG, "batch < 0");
+  if (B == 0) return PRNET_OK;
+  if (!x || !y) return fail(h, PRNET_ERR_INVALID_ARG, "NULL x or y with batch > 0");
+  const int64_t C = h->cfg.channels, L = h->cfg.lookback, H = h->cfg.horizon;
+  if (B > INT64_MAX / (C * (L > H ? L : H)) / 4)
+    return fail(h, PRNET_ERR_INVALID_ARG, "batch * C * L overflows");
+  if (device_ptrs) {
+    if (((uintptr_t)x & 15) || ((uintptr_t)y & 15))
+      return fail(h, PRNET_ERR_UNSUPPORTED, "x and y must be 16-byte aligned");
+    if (overlaps(x, (size_t)(B * C * L * 4), y, (size_t)(B * C * H * 4)))
+      return fail(h, PRNET_ERR_UNSUPPORTED, "x and y overlap");
+    prnet_status s = check_dev_ptr(h, x, "x");
+    if (s != PRNET_OK) return s;
+    s = check_dev_ptr(h, y, "y");
+    if (s != PRNET_OK) return s;
+  } else if (overlaps(x, (size_t)(B * C * L * 4), y, (size_t)(B * C * H * 4))) {
+    return fail(h, PRNET_ERR_UNSUPPORTED, "x and y overlap");
+  }
+  return PRNET_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+prnet_status prnet_create(const prnet_config* cfg, prnet_handle** out) {
+  if (out) *out = nullptr;
+  if (!cfg || !out) return fail(nullptr, PRNET_ERR_INVALID_ARG, "NULL cfg or out");
+  if (cfg->abi_version != PRNET_ABI_VERSION)
+    return fail(nullptr, PRNET_ERR_INVALID_ARG, "abi_version mismatch");
+  if (cfg->channels < 1 || cfg->seg_len < 2 || cfg->lookback < cfg->seg_len || cfg->horizon < 1)
+    return fail(nullptr, PRNET_ERR_INVALID_ARG, "need C >= 1, S >= 2, L >= S, H >= 1");
+  if (!(cfg->tau_seasonal > 0.f) || !std::isfinite(cfg->tau_seasonal) ||
+      !(cfg->tau_trend > 0.f) || !std::isfinite(cfg->tau_trend))
+    return fail(nullptr, PRNET_ERR_INVALID_ARG, "temperatures must be finite and > 0");
+  if (cfg->metric_variant != 0)
+    return fail(nullptr, PRNET_ERR_INVALID_ARG, "metric_variant must be 0 (others reserved)");
+  if (cfg->channels > 65535)
+    return fail(nullptr, PRNET_ERR_UNSUPPORTED, "C > 65535 not supported");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || cfg->device < 0 || cfg->device >= ndev) {
+    cudaGetLastError();
+    return fail(nullptr, PRNET_ERR_UNSUPPORTED, "no such CUDA device");
+  }
+  cudaDeviceProp prop;
+  if ((e = cudaGetDeviceProperties(&prop, cfg->device)) != cudaSuccess)
+    return cuda_fail(nullptr, e, "cudaGetDeviceProperties");
+  if (prop.major != 10)
+    return fail(nullptr, PRNET_ERR_UNSUPPORTED,
+                "device is not compute capability 10.x (this library is built for sm_100a)");
+  prnet_handle* h = new (std::nothrow) prnet_handle();
+  if (!h) return fail(nullptr, PRNET_ERR_OOM, "host allocation failed");
+  h->cfg = *cfg;
+  h->N = cfg->lookback / cfg->seg_len;
+  h->r = cfg->lookback - h->N * cfg->seg_len;
+  h->M = (cfg->horizon + cfg->seg_len - 1) / cfg->seg_len;
+  h->Cw = cfg->head_per_channel ? cfg->channels : 1;
+  h->sm_count = prop.multiProcessorCount;
+  h->max_smem_optin = (int)prop.sharedMemPerBlockOptin;
+  if (h->N > 512 || cfg->seg_len > 4096) {
+    delete h;
+    return fail(nullptr, PRNET_ERR_UNSUPPORTED, "N > 512 segments not supported");
+  }
+  DeviceGuard g(cfg->device);
+  const size_t nw = (size_t)h->Cw * h->M * h->N, nb = (size_t)h->Cw * cfg->horizon;
+  if ((e = cudaMalloc(&h->d_ws, nw * 4)) != cudaSuccess ||
+      (e = cudaMalloc(&h->d_wt, nw * 4)) != cudaSuccess ||
+      (e = cudaMalloc(&h->d_b, nb * 4)) != cudaSuccess ||
+      (e = cudaMalloc(&h->d_err, 2 * prnet::kErrPartials * sizeof(double))) != cudaSuccess) {
+    prnet_status s = cuda_fail(nullptr, e, "cudaMalloc(params)");
+    prnet_destroy(h);
+    return s;
+  }
+  *out = h;
+  return PRNET_OK;
+}
+
+prnet_status prnet_load_params(prnet_handle* h, const float* w_seasonal, const float* w_trend,
+                               const float* bias, int64_t n_w, int64_t n_b) {
+  if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
+  const int64_t want_w = (int64_t)h->Cw * h->M * h->N, want_b = (int64_t)h->Cw * h->cfg.horizon;
+  if (!w_seasonal || !w_trend || !bias) return fail(h, PRNET_ERR_INVALID_ARG, "NULL parameter");
+  if (n_w != want_w || n_b != want_b)
+    return fail(h, PRNET_ERR_INVALID_ARG,
+                "parameter counts: want n_w=" + std::to_string(want_w) +
+                    " n_b=" + std::to_string(want_b));
+  DeviceGuard g(h->cfg.device);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(h, e, "cudaDeviceSynchronize");
+  if ((e = cudaMemcpy(h->d_ws, w_seasonal, want_w * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(h->d_wt, w_trend, want_w * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaMemcpy(h->d_b, bias, want_b * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
+    return cuda_fail(h, e, "cudaMemcpy(params)");
+  h->loaded = true;
+  return PRNET_OK;
+}
+
+prnet_status prnet_forward(prnet_handle* h, const float* x, int64_t batch, float* y,
+                           void* cuda_stream) {
+  prnet_status s = validate_forward(h, x, batch, y, true);
+  if (s != PRNET_OK || batch == 0) return s;
+  DeviceGuard g(h->cfg.device);
+  return enqueue_forward(h, x, batch, y, nullptr, nullptr, (cudaStream_t)cuda_stream);
+}
+
+prnet_status prnet_set_host_chunk(prnet_handle* h, int64_t windows_per_chunk) {
+  if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
+  if (windows_per_chunk < 1) return fail(h, PRNET_ERR_INVALID_ARG, "windows_per_chunk < 1");
+  h->host_chunk = windows_per_chunk;
+  return PRNET_OK;
+}
+
+prnet_status prnet_forward_host(prnet_handle* h, const float* x_host, int64_t batch,
+                                float* y_host) {
+  prnet_status s = validate_forward(h, x_host, batch, y_host, false);
+  if (s != PRNET_OK || batch == 0) return s;
+  DeviceGuard g(h->cfg.device);
+  const int64_t C = h->cfg.channels, L = h->cfg.lookback, H = h->cfg.horizon;
+  int64_t chunk = h->host_chunk;
+  if (chunk <= 0) {
+    chunk = (256ll << 20) / (C * L * 4);
+    if (chunk < 1) chunk = 1;
+  }
+  if (chunk > batch) chunk = batch;
+  cudaError_t e;
+  if (chunk > h->stage_windows) {  // (re)allocate the staging ring
+    for (int k = 0; k < prnet_handle::kStages; k++) {
+      cudaFree(h->d_xstage[k]);
+      cudaFree(h->d_ystage[k]);
+      h->d_xstage[k] = h->d_ystage[k] = nullptr;
+    }
+    h->stage_windows = 0;
+    for (int k = 0; k < prnet_handle::kStages; k++) {
+      if ((e = cudaMalloc(&h->d_xstage[k], chunk * C * L * 4)) != cudaSuccess ||
+          (e = cudaMalloc(&h->d_ystage[k], chunk * C * H * 4)) != cudaSuccess)
+        return cuda_fail(h, e, "cudaMalloc(staging)");
+    }
+    h->stage_windows = chunk;
+  }
+  for (int k = 0; k < prnet_handle::kStages; k++) {
+    if (!h->streams[k] &&
+        (e = cudaStreamCreateWithFlags(&h->streams[k], cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(h, e, "cudaStreamCreate");
+  }
+  // Chunk k goes to stage k % 3 on stream k % 3: H2D -> kernel -> D2H in stream
+  // order, so the copy engines overlap chunk k+1's upload, chunk k's kernel and
+  // chunk k-1's download across the three streams.
+  int64_t k = 0;
+  for (int64_t b0 = 0; b0 < batch; b0 += chunk, k++) {
+    const int64_t nb = (batch - b0) < chunk ? (batch - b0) : chunk;
+    const int st = (int)(k % prnet_handle::kStages);
+    cudaStream_t stream = h->streams[st];
+    if ((e = cudaMemcpyAsync(h->d_xstage[st], x_host + b0 * C * L, nb * C * L * 4,
+                             cudaMemcpyHostToDevice, stream)) != cudaSuccess)
+      return cuda_fail(h, e, "cudaMemcpyAsync(H2D)");
+    s = enqueue_forward(h, h->d_xstage[st], nb, h->d_ystage[st], nullptr, nullptr, stream);
+    if (s != PRNET_OK) return s;
+    if ((e = cudaMemcpyAsync(y_host + b0 * C * H, h->d_ystage[st], nb * C * H * 4,
+                             cudaMemcpyDeviceToHost, stream)) != cudaSuccess)
+      return cuda_fail(h, e, "cudaMemcpyAsync(D2H)");
+  }
+  for (int st = 0; st < prnet_handle::kStages; st++)
+    if ((e = cudaStreamSynchronize(h->streams[st])) != cudaSuccess)
+      return cuda_fail(h, e, "cudaStreamSynchronize");
+  return PRNET_OK;
+}
+
+void prnet_destroy(prnet_handle* h) {
+  if (!h) return;
+  {
+    DeviceGuard g(h->cfg.device);
+    cudaFree(h->d_ws);
+    cudaFree(h->d_wt);
+    cudaFree(h->d_b);
+    cudaFree(h->d_err);
+    for (int k = 0; k < prnet_handle::kStages; k++) {
+      cudaFree(h->d_xstage[k]);
+      cudaFree(h->d_ystage[k]);
+      if (h->streams[k]) cudaStreamDestroy(h->streams[k]);
+    }
+  }
+  delete h;
+}
+
+const char* prnet_last_error(const prnet_handle* h) {
+  return h ? h->err.c_str() : g_create_error.c_str();
+}
+
+prnet_status prnet_get_dims(const prnet_handle* h, int32_t* N, int32_t* M, int32_t* r) {
+  if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
+  if (N) *N = h->N;
+  if (M) *M = h->M;
+  if (r) *r = h->r;
+  return PRNET_OK;
+}
+
+prnet_status prnet_debug_segments(prnet_handle* h, const float* x, int64_t batch, float* seg,
+                                  void* cuda_stream) {
+  if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
+  if (batch < 0) return fail(h, PRNET_ERR_INVALID_ARG, "batch < 0");
+  if (batch == 0) return PRNET_OK;
+  if (!x || !seg) return fail(h, PRNET_ERR_INVALID_ARG, "NULL pointer");
+  prnet_status s = check_dev_ptr(h, x, "x");
+  if (s == PRNET_OK) s = check_dev_ptr(h, seg, "seg");
+  if (s != PRNET_OK) return s;
+  DeviceGuard g(h->cfg.device);
+  cudaError_t e = prnet::launch_gather_segments(x, batch, h->cfg.channels, h->cfg.lookback,
+                                                h->cfg.seg_len, h->N, h->r, seg,
+                                                (cudaStream_t)cuda_stream);
+  return e == cudaSuccess ? PRNET_OK : cuda_fail(h, e, "gather_segments launch");
+}
+
+prnet_status prnet_debug_attention(prnet_handle* h, const float* x, int64_t batch, float* a_s,
+                                   float* a_t, void* cuda_stream) {
+  if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
+  if (h->N > 32) return fail(h, PRNET_ERR_UNSUPPORTED, "debug_attention needs N <= 32");
+  if (!a_s || !a_t) return fail(h, PRNET_ERR_INVALID_ARG, "NULL attention buffer");
+  const int64_t C = h->cfg.channels, H = h->cfg.horizon;
+  prnet_status s = validate_forward(h, x, batch, a_s, true);  // x checks (a_s as dummy y)
+  if (s != PRNET_OK || batch == 0) return s;
+  s = check_dev_ptr(h, a_t, "a_t");
+  if (s != PRNET_OK) return s;
+  DeviceGuard g(h->cfg.device);
+  // the forward's own y goes to a scratch buffer
+  float* y = nullptr;
+  cudaError_t e = cudaMallocAsync(&y, batch * C * H * 4, (cudaStream_t)cuda_stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "cudaMallocAsync(scratch y)");
+  s = enqueue_forward(h, x, batch, y, a_s, a_t, (cudaStream_t)cuda_stream);
+  cudaFreeAsync(y, (cudaStream_t)cuda_stream);
+  return s;
+}
+
+prnet_status prnet_error_sums(prnet_handle* h, const float* y, const float* target,
+                              int64_t batch, double* out3, void* cuda_stream) {
+  if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
+  if (batch < 0 || !y || !target || !out3)
+    return fail(h, PRNET_ERR_INVALID_ARG, "NULL pointer or batch < 0");
+  prnet_status s = check_dev_ptr(h, y, "y");
+  if (s == PRNET_OK) s = check_dev_ptr(h, target, "target");
+  if (s == PRNET_OK) s = check_dev_ptr(h, out3, "out3");
+  if (s != PRNET_OK) return s;
+  DeviceGuard g(h->cfg.device);
+  const int64_t n = batch * h->cfg.channels * h->cfg.horizon;
+  cudaError_t e = prnet::launch_error_sums(y, target, n, h->d_err, out3, (cudaStream_t)cuda_stream);
+  return e == cudaSuccess ? PRNET_OK : cuda_fail(h, e, "error_sums launch");
+}
+
+prnet_status prnet_forward_plan(const prnet_handle* h, int64_t batch, int32_t* kernel_launches,
+                                int32_t* variant) {
+  if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
+  if (kernel_launches) *kernel_launches = batch > 0 ? 1 : 0;
+  if (variant) *variant = pick_variant(h);
+  return PRNET_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,77 @@
+"""CPU-side checks of the boundary: libprnet.so builds for sm_100a, loads, and
+exports every entry point include/prnet.h declares; without a GPU, create fails
+loudly with PRNET_ERR_UNSUPPORTED (no CPU fallback)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2404_02445_b200 import _build
+    _build.build()
+    from paper_2404_02445_b200 import load_library
+    return load_library()
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "prnet.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(prnet_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_the_abi():
+    syms = declared_symbols()
+    for s in ("prnet_create", "prnet_load_params", "prnet_forward", "prnet_destroy"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol(lib):
+    from paper_2404_02445_b200 import EXPORTS
+    syms = declared_symbols()
+    assert sorted(EXPORTS) == syms
+    for s in syms:
+        assert hasattr(lib, s), s
+    out = subprocess.check_output(["nm", "-D", "--defined-only", lib._name]).decode()
+    exported = set(re.findall(r"\bT (prnet_\w+)", out))
+    assert set(syms) <= exported
+    # C linkage: no mangled prnet symbols in the dynamic table
+    assert not re.search(r"\bT _Z\w*prnet_create", out)
+
+
+def test_library_is_sm100a_only(lib):
+    out = subprocess.check_output(["/usr/local/cuda/bin/cuobjdump", "--list-elf", lib._name]).decode()
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(8\d|90)\b", out)
+
+
+def test_create_without_gpu_fails_loudly(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    from paper_2404_02445_b200 import PRNet, PrnetError
+    with pytest.raises(PrnetError) as e:
+        PRNet(7, 96, 24, 96)
+    assert e.value.status == 3
+
+
+def test_create_validates_before_touching_the_device(lib):
+    from paper_2404_02445_b200 import PrnetConfig
+    h = ctypes.c_void_p(123)
+    for bad in [dict(seg_len=1), dict(lookback=10), dict(horizon=0), dict(channels=0),
+                dict(tau_seasonal=0.0), dict(tau_trend=float("nan")), dict(abi_version=2),
+                dict(metric_variant=1)]:
+        kw = dict(abi_version=1, channels=7, lookback=96, seg_len=24, horizon=96,
+                  head_per_channel=1, metric_variant=0, tau_seasonal=1.0, tau_trend=1.0, device=0)
+        kw.update(bad)
+        cfg = PrnetConfig(**kw)
+        assert lib.prnet_create(ctypes.byref(cfg), ctypes.byref(h)) == 1, bad
+        assert h.value is None
+        assert lib.prnet_last_error(None)
+    assert lib.prnet_forward(None, None, 0, None, None) == 2
+    lib.prnet_destroy(None)

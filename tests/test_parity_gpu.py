@@ -1,0 +1,234 @@
+"""GPU parity: libprnet.so (called through its C ABI) against the fp64 CPU oracle
+on the same seeded inputs.  Tolerance: |d| <= 1e-5 + 1e-4 |ref| (north_star);
+segment indexing bit-exact.  Run on a B200 via gpurun: pytest -m gpu."""
+import numpy as np
+import pytest
+
+import synth
+from parity_util import assert_parity, parity_report
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2404_02445_b200 import PRNet, PrnetError  # noqa: E402
+
+
+def _model(C, L, S, H, hpc=True, tau_s=1.0, tau_t=1.0, seed=synth.DEFAULT_SEED, cfg_id=0):
+    N, _, M = synth.derived_dims(L, S, H)
+    ws, wt, b = synth.make_params(C, M, N, H, hpc, seed, cfg_id)
+    m = PRNet(C, L, S, H, head_per_channel=hpc, tau_s=tau_s, tau_t=tau_t).load(ws, wt, b)
+    return m, (ws, wt, b)
+
+
+def _check_small(oracle_mod, x, S, H, hpc=True, tau_s=1.0, tau_t=1.0, scale=None):
+    B, C, L = x.shape
+    m, (ws, wt, b) = _model(C, L, S, H, hpc, tau_s, tau_t)
+    xd = torch.from_numpy(x).cuda()
+    y = m.forward(xd).cpu().numpy()
+    _, y64 = oracle_mod.forward(x, S, H, ws, wt, b, hpc, tau_s, tau_t)
+    sc = None
+    if scale is not None:
+        sc = scale
+    return assert_parity(y, y64, scale=sc)
+
+
+# ------------------------------------------------------------------ configs[0] in full
+def test_etth1_full(oracle_mod):
+    w = synth.WORKLOADS["etth1"]
+    s = synth.make_series(w)
+    x, _ = synth.window_batch(s, w, np.arange(w.windows))
+    assert x.shape == (32, 7, 96)
+    _check_small(oracle_mod, x, w.S, w.H)
+
+
+# ------------------------------------------------------------------ full-size configs, sampled
+FULL = ["weather_h96", "weather_h192", "weather_h336", "weather_h720", "electricity", "traffic"]
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_full_size_sampled(oracle_mod, name):
+    """The whole test set runs on the GPU in the bench's launch configuration; the
+    oracle checks windows {0, 1, B/2, B-1} plus a stride sample, all channels."""
+    w = synth.WORKLOADS[name]
+    s = synth.make_series(w)
+    B = w.windows
+    sd = torch.from_numpy(s).cuda()
+    x = sd.unfold(1, w.L, 1)[:, w.t0:w.t0 + B, :].permute(1, 0, 2).contiguous()
+    m, (ws, wt, b) = _model(w.C, w.L, w.S, w.H, cfg_id=w.cfg_id)
+    y = m.forward(x)
+    torch.cuda.synchronize()
+    idx = [0, 1, B // 2, B - 1]
+    if w.C <= 100:
+        idx = sorted(set(idx + list(range(0, B, max(1, B // 6)))))
+    xs, _ = synth.window_batch(s, w, idx)
+    np.testing.assert_array_equal(x[idx].cpu().numpy(), xs)
+    _, y64 = oracle_mod.forward(xs, w.S, w.H, ws, wt, b, True)
+    assert_parity(y[idx].cpu().numpy(), y64)
+    del x, y, sd
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------------ configs[4] stress sweep
+@pytest.mark.parametrize("L,S", synth.STRESS_GRID)
+def test_stress_grid(oracle_mod, L, S):
+    """Every (L, S) point of the sweep: 4 windows x 100 channels through the same kernels
+    (N = L/S from 1 to 480 covers the warp kernel's 8/16/32 variants and the long-N kernel)."""
+    w = synth.WORKLOADS[f"stress_L{L}_S{S}_H96"]
+    N = L // S
+    nwin = 4 if N <= 120 else 1
+    C = 100 if N <= 120 else 8
+    s = synth.make_series(w, channels=range(C))
+    x, _ = synth.window_batch(s, w, np.arange(nwin) * 97)
+    _check_small(oracle_mod, x, S, w.H)
+
+
+@pytest.mark.parametrize("L,S", [(5760, 12), (1440, 24), (720, 96)])
+def test_stress_full_size_sampled(oracle_mod, L, S):
+    """Full 100k-series stress batch on the GPU, sampled series checked."""
+    w = synth.WORKLOADS[f"stress_L{L}_S{S}_H96"]
+    s = synth.make_series(w)
+    sd = torch.from_numpy(s).cuda()
+    x = sd.unfold(1, w.L, 1)[:, w.t0:w.t0 + w.windows, :].permute(1, 0, 2).contiguous()
+    m, (ws, wt, b) = _model(w.C, w.L, w.S, w.H, cfg_id=w.cfg_id)
+    y = m.forward(x).cpu().numpy()
+    idx = [0, 999] if L // S > 120 else [0, 1, 500, 999]
+    chans = np.arange(0, 100, 33) if L // S > 120 else np.arange(100)
+    xs = x[idx].cpu().numpy()[:, chans]
+    _, y64 = oracle_mod.forward(np.ascontiguousarray(xs), S, w.H, ws[chans], wt[chans], b[chans])
+    assert_parity(y[idx][:, chans], y64)
+
+
+# ------------------------------------------------------------------ shapes and edge cases
+@pytest.mark.parametrize("L,S,H", [
+    (96, 24, 96), (100, 24, 90), (97, 7, 13), (50, 49, 3), (24, 24, 24), (25, 24, 1),
+    (64, 8, 64), (72, 8, 100), (128, 8, 64), (136, 8, 9), (256, 8, 40), (264, 8, 40),
+    (270, 9, 31), (33, 2, 5), (66, 2, 7), (720, 24, 720), (722, 12, 721), (1000, 3, 17)])
+def test_shapes_ragged(oracle_mod, L, S, H):
+    """N from 1 to 333 across the 8/16/32/long variants; L mod S != 0 (r > 0);
+    H mod S != 0; odd S and L (scalar load path)."""
+    x = synth.random_windows(3, 5, L, kind="mixed")
+    _check_small(oracle_mod, x, S, H)
+
+
+@pytest.mark.parametrize("tau", [0.05, 0.1, 1.0, 10.0])
+@pytest.mark.parametrize("hpc", [True, False])
+def test_temperatures_and_head_modes(oracle_mod, tau, hpc):
+    x = synth.random_windows(4, 6, 720, kind="mixed")
+    _check_small(oracle_mod, x, 24, 336, hpc=hpc, tau_s=tau, tau_t=tau * 0.7)
+
+
+@pytest.mark.parametrize("kind", ["normal", "constant", "scaled"])
+@pytest.mark.parametrize("L,S", [(720, 24), (1440, 24)])
+def test_value_distributions(oracle_mod, kind, L, S):
+    x = synth.random_windows(3, 4, L, kind=kind)
+    scale = np.abs(x).max(axis=2, keepdims=True)[..., :1] if kind == "scaled" else None
+    scale = None if scale is None else np.maximum(scale, 1.0)
+    _check_small(oracle_mod, x, S, 96, scale=scale)
+
+
+def test_batch_zero_and_one(oracle_mod):
+    m, _ = _model(3, 96, 24, 96)
+    x = torch.zeros((0, 3, 96), device="cuda")
+    assert m.forward(x).shape == (0, 3, 96)
+    xx = synth.random_windows(1, 3, 96)
+    _check_small(oracle_mod, xx, 24, 96)
+
+
+# ------------------------------------------------------------------ index map, intermediates
+@pytest.mark.parametrize("L,S", [(720, 24), (722, 24), (97, 7), (5760, 12)])
+def test_segment_gather_bit_exact(L, S):
+    x = synth.random_windows(3, 4, L, kind="normal")
+    m, _ = _model(4, L, S, 10)
+    seg = m.debug_segments(torch.from_numpy(x).cuda()).cpu().numpy()
+    N, r = L // S, L - (L // S) * S
+    idx = r + np.arange(N)[:, None] * S + np.arange(S)[None, :]
+    np.testing.assert_array_equal(seg, x[:, :, idx])
+
+
+@pytest.mark.parametrize("L,S", [(720, 24), (96, 24), (384, 24)])
+def test_attention_matrices(oracle_mod, L, S):
+    x = synth.random_windows(2, 3, L, kind="mixed")
+    m, _ = _model(3, L, S, 24, tau_s=0.5, tau_t=2.0)
+    a_s, a_t = m.debug_attention(torch.from_numpy(x).cuda())
+    a_s, a_t = a_s.cpu().numpy(), a_t.cpu().numpy()
+    np.testing.assert_allclose(a_s.sum(-1), 1.0, atol=1e-6)
+    np.testing.assert_allclose(a_t.sum(-1), 1.0, atol=1e-6)
+    N = L // S
+    for b in range(2):
+        for c in range(3):
+            r = oracle_mod.series(x[b, c], S, 24, np.zeros((1, N)), np.zeros((1, N)),
+                                  np.zeros(24), 0.5, 2.0)
+            np.testing.assert_allclose(a_s[b, c], r["a_s"], atol=2e-6)
+            np.testing.assert_allclose(a_t[b, c], r["a_t"], atol=2e-6)
+            assert np.all(np.argmax(a_s[b, c], 1) == np.arange(N))
+
+
+# ------------------------------------------------------------------ determinism, sharding, host path
+def test_deterministic_and_shard_invariant():
+    from paper_2404_02445_b200 import shard_windows
+    x = torch.from_numpy(synth.random_windows(37, 11, 720)).cuda()
+    m, _ = _model(11, 720, 24, 720)
+    y1 = m.forward(x)
+    y2 = m.forward(x)
+    assert torch.equal(y1, y2)
+    for world in (2, 3, 8):
+        parts = []
+        for rank in range(world):
+            s, n = shard_windows(37, world, rank)
+            parts.append(m.forward(x[s:s + n].contiguous()))
+        assert torch.equal(torch.cat(parts), y1)
+
+
+def test_forward_host_matches_device():
+    x = synth.random_windows(29, 7, 720)
+    m, _ = _model(7, 720, 24, 336)
+    yd = m.forward(torch.from_numpy(x).cuda()).cpu()
+    xp = torch.from_numpy(x).pin_memory()
+    for chunk in (None, 1, 5, 29, 64):
+        yh = m.forward_host(xp, chunk_windows=chunk)
+        assert torch.equal(yh, yd)
+
+
+def test_error_sums_device(oracle_mod):
+    rng = np.random.default_rng(3)
+    y = rng.normal(size=(13, 5, 96)).astype(np.float32)
+    t = rng.normal(size=(13, 5, 96)).astype(np.float32)
+    m, _ = _model(5, 96, 24, 96)
+    out = m.error_sums(torch.from_numpy(y).cuda(), torch.from_numpy(t).cuda()).cpu().numpy()
+    sse, sae, n = oracle_mod.error_sums(y, t)
+    assert n == out[2] and abs(out[0] - sse) < 1e-9 * sse and abs(out[1] - sae) < 1e-9 * sae
+
+
+# ------------------------------------------------------------------ ABI error behaviour
+def test_abi_errors():
+    from paper_2404_02445_b200.prnet import PRNet as P
+    with pytest.raises(PrnetError) as e:
+        P(3, 20, 24, 5)               # L < S
+    assert e.value.status == 1
+    with pytest.raises(PrnetError):
+        P(3, 96, 24, 96, tau_s=0.0)
+    m = P(3, 96, 24, 96)
+    x = torch.zeros((2, 3, 96), device="cuda")
+    with pytest.raises(PrnetError) as e:
+        m.forward(x)                  # before load
+    assert e.value.status == 2
+    N, M = m.N, m.M
+    w0 = np.zeros(3 * M * N, np.float32)
+    assert m._lib.prnet_load_params(m.handle, w0.ctypes.data, w0.ctypes.data, w0.ctypes.data,
+                                    w0.size, 3 * 96 - 1) == 1      # wrong bias count
+    assert m._lib.prnet_forward(m.handle, None, -1, None, None) == 2   # still not loaded
+    m.load(np.zeros((3, M, N)), np.zeros((3, M, N)), np.zeros((3, 96)))
+    buf = torch.zeros(2 * 3 * 96 + 1, device="cuda")
+    xm = buf[1:].view(2, 3, 96)       # 4-byte offset: misaligned
+    with pytest.raises(PrnetError) as e:
+        m.forward(xm)
+    assert e.value.status == 3
+    with pytest.raises(PrnetError) as e:
+        m.forward_into(x, x)          # overlap (H == L here)
+    assert e.value.status == 3
+    with pytest.raises(PrnetError) as e:
+        m.forward(torch.zeros((2, 3, 96)))   # host pointer on the device entry
+    assert e.value.status == 3
