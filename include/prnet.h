@@ -134,10 +134,19 @@ prnet_status prnet_debug_attention(prnet_handle* h, const float* x, int64_t batc
 prnet_status prnet_error_sums(prnet_handle* h, const float* y, const float* target,
                               int64_t batch, double* out3, void* cuda_stream);
 
+/* Select the forward kernel (tuning / cross-checking; default -1 = automatic):
+ *   0 = warp_f32   one warp per series, CUDA-core FP32            (N <= 32)
+ *   1 = long_f32   one CTA per series, rows streamed, FP32         (N <= 512)
+ *   2 = mma_f16x3  one warp per series, tensor cores (mma.sync m16n8k16) with
+ *                  split-fp16 hi/lo operands, 3 products, fp32 accumulation
+ *                  (N <= 32, M <= 32, S <= 128)
+ * All variants compute the same reading to within the documented tolerance. */
+prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant);
+
 /* Kernel-level accounting for the bench (host-side, no device work):
  * kernel_launches = device kernels one prnet_forward(batch) enqueues. */
 prnet_status prnet_forward_plan(const prnet_handle* h, int64_t batch, int32_t* kernel_launches,
-                                int32_t* variant);
+                                int32_t* variant);  /* variant as above */
 
 #ifdef __cplusplus
 }

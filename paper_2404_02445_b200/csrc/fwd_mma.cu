@@ -1,0 +1,575 @@
+// fwd_mma.cu -- fused PRNet pattern-attention forward on the tensor cores
+// (sm_100a mma.sync, split-fp16 "3-product" arithmetic), 9 <= N <= 32, M <= 32.
+//
+// Same per-series step map and reading as fwd_warp.cu; what
+// changes is how the three contractions run:
+//   a3 Gram      G  = Z Z^T            (N x S)(S x N)
+//   a6+a7 fold   Q  = W_s A_s + W_t A_t (M x N)(N x N) x 2
+//   a7 head      Y  = Q X               (M x N)(N x S)
+// each as m16n8k16 MMAs with fp32 accumulation, every fp32 operand v split
+// into v = hi + lo (both fp16; lo = fp16(v - hi)) and the product formed as
+// hi*hi + hi*lo + lo*hi.  The dropped lo*lo term and the rounding of lo are
+// ~2^-22 relative, i.e. fp32-class accuracy (plain fp16/tf32
+// fail the 1e-5 + 1e-4|y| bar).  Operands are pre-scaled by exact powers of
+// two (per series for X and Z, per channel for W) so fp16 never overflows;
+// the scales are divided out exactly in fp32.
+//
+// Data never leaves the SM between load and store: the Gram accumulators are
+// softmax-ed in registers (FA2-style quad reductions), the attention tiles are
+// transposed in registers with movmatrix into the B operand of the fold, and
+// the fold's accumulators are re-packed in registers as the A operand of the
+// head.  Shared memory holds only the series (fp32 staging + fp16 X, Z) and
+// the channel's head (fp16 W, fp32 b).  The next series is prefetched with
+// cp.async while the current one is in the tensor cores.
+#include <cuda_fp16.h>
+
+#include "prnet_internal.cuh"
+
+namespace prnet {
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(a, b);
+  const float2 hf = __half22float2(h);
+  const __half2 l = __floats2half2_rn(a - hf.x, b - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
+__device__ __forceinline__ void split1(float a, __half& hi, __half& lo) {
+  hi = __float2half_rn(a);
+  lo = __float2half_rn(a - __half2float(hi));
+}
+
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// hi*hi + hi*lo + lo*hi
+__device__ __forceinline__ void mma3(float (&c)[4], const uint32_t (&ah)[4],
+                                     const uint32_t (&al)[4], uint32_t bh0, uint32_t bh1,
+                                     uint32_t bl0, uint32_t bl1) {
+  mma16816(c, al, bh0, bh1);
+  mma16816(c, ah, bl0, bl1);
+  mma16816(c, ah, bh0, bh1);
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(p)));
+}
+
+__device__ __forceinline__ void ldsm_x2_t(uint32_t& r0, uint32_t& r1, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];"
+               : "=r"(r0), "=r"(r1)
+               : "r"(smem_u32(p)));
+}
+
+__device__ __forceinline__ uint32_t movm_t(uint32_t v) {
+  uint32_t r;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+// 2^-e with max|v| * 2^-e in [0.5, 1): exact power-of-two scale (1 for v == 0).
+__device__ __forceinline__ float pow2_scale(float maxabs) {
+  if (!(maxabs > 0.f) || !isfinite(maxabs)) return 1.f;
+  int e;
+  frexpf(maxabs, &e);
+  return ldexpf(1.f, -e);
+}
+
+}  // namespace
+
+
+
+template <int MT, int MMT>
+__global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLayout ly,
+                                                               int wins_per_cta) {
+  extern __shared__ float4 smem4[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(smem4);
+  constexpr int NR = 16 * MT;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int gq = lane >> 2, cq = lane & 3, q8 = lane >> 3;
+  const int c = blockIdx.y;
+  const int cw = a.head_per_channel ? c : 0;
+  const int S = a.S, N = a.N, M = a.M, H = a.H, L = a.L, C = a.C;
+
+  // ---------------- CTA-shared: W' = W * sw as fp16 hi/lo, [16*MMT][wph], cols: i (seasonal)
+  // at [0, NR), i (trend) at [NR, 2NR); zeros outside m < M, i < N.  Bias fp32.
+  __half* w_hi = reinterpret_cast<__half*>(smem);
+  __half* w_lo = reinterpret_cast<__half*>(smem + ly.off_wlo);
+  float* bS = reinterpret_cast<float*>(smem + ly.off_bias);
+  __shared__ float red[8];
+  float inv_sw;
+  {
+    const float* gws = a.ws + (int64_t)cw * M * N;
+    const float* gwt = a.wt + (int64_t)cw * M * N;
+    float mx = 0.f;
+    for (int k = threadIdx.x; k < M * N; k += blockDim.x)
+      mx = fmaxf(mx, fmaxf(fabsf(gws[k]), fabsf(gwt[k])));
+    mx = warp_max(mx);
+    if (lane == 0) red[warp] = mx;
+    __syncthreads();
+    mx = 0.f;
+    for (int w = 0; w < nwarps; w++) mx = fmaxf(mx, red[w]);
+    const float sw = pow2_scale(mx);
+    inv_sw = 1.f / sw;
+    const int rows = 16 * MMT;
+    for (int k = threadIdx.x; k < rows * ly.wph; k += blockDim.x) {
+      const int m = k / ly.wph, col = k - m * ly.wph;
+      float v = 0.f;
+      if (m < M) {
+        if (col < NR) {
+          if (col < N) v = gws[m * N + col] * sw;
+        } else if (col < 2 * NR) {
+          if (col - NR < N) v = gwt[m * N + (col - NR)] * sw;
+        }
+      }
+      split1(v, w_hi[k], w_lo[k]);
+    }
+    const float* gb = a.bias + (int64_t)cw * H;
+    for (int k = threadIdx.x; k < H; k += blockDim.x) bS[k] = gb[k];
+  }
+
+  // ---------------- per-warp: fp32 staging, X' hi/lo [NR][sph], Z' hi/lo [NR][zph]
+  unsigned char* wb = smem + ly.shared_bytes + warp * ly.per_warp_bytes;
+  float* xbuf = reinterpret_cast<float*>(wb);
+  __half* x_hi = reinterpret_cast<__half*>(wb + ly.off_xhi);
+  __half* x_lo = reinterpret_cast<__half*>(wb + ly.off_xlo);
+  __half* z_hi = reinterpret_cast<__half*>(wb + ly.off_zhi);
+  __half* z_lo = reinterpret_cast<__half*>(wb + ly.off_zlo);
+  {
+    // zero the fp16 operand tiles once: padding rows (>= N) and columns (>= S) stay 0
+    uint32_t* p = reinterpret_cast<uint32_t*>(wb + ly.off_xhi);
+    const int words = (ly.per_warp_bytes - ly.off_xhi) / 4;
+    for (int k = lane; k < words; k += 32) p[k] = 0u;
+  }
+  __syncthreads();
+
+  const bool vec_x = ((L & 3) == 0) && ((a.r & 3) == 0);
+  const int NS = N * S;
+  const int64_t b_begin = (int64_t)blockIdx.x * wins_per_cta;
+  int64_t b_end = b_begin + wins_per_cta;
+  if (b_end > a.B) b_end = a.B;
+
+  auto prefetch = [&](int64_t b) {
+    const float* xg = a.x + (b * C + c) * L + a.r;
+    if (vec_x) {
+      for (int k = lane; k < (NS >> 2); k += 32) cp_async16(xbuf + 4 * k, xg + 4 * k);
+      for (int k = (NS & ~3) + lane; k < NS; k += 32) cp_async4(xbuf + k, xg + k);
+    } else {
+      for (int k = lane; k < NS; k += 32) cp_async4(xbuf + k, xg + k);
+    }
+    cp_async_commit();
+  };
+
+  int64_t b = b_begin + warp;
+  if (b < b_end) prefetch(b);
+  for (; b < b_end; b += nwarps) {
+    const int64_t series = b * C + c;
+    cp_async_wait_all();
+    __syncwarp();
+
+    // ---------------- a2: descriptors (fp32), lane i = segment i
+    float amax = 0.f;
+    for (int k = lane; k < NS; k += 32) amax = fmaxf(amax, fabsf(xbuf[k]));
+    const float sx = pow2_scale(warp_max(amax));
+    const int i = lane;
+    float mu = 0.f, m1 = 0.f, x0 = 0.f, nu2 = 0.f, kap = 0.f, zmax = 0.f;
+    const float* xr = xbuf + i * S;
+    if (i < N) {
+      x0 = xr[0];
+      float s = 0.f;
+      for (int t = 0; t < S; t++) s += xr[t] - x0;
+      m1 = s * a.inv_s;
+      mu = x0 + m1;
+      for (int t = 0; t < S; t++) {
+        const float v = xr[t];
+        const float z = (v - x0) - m1;
+        nu2 = fmaf(z, z, nu2);
+        kap = fmaf((float)t - a.half_s, z, kap);
+        zmax = fmaxf(zmax, fabsf(z));
+        __half h, l;
+        split1(v * sx, h, l);
+        x_hi[i * ly.sph + t] = h;
+        x_lo[i * ly.sph + t] = l;
+      }
+      kap *= a.inv_v;
+    }
+    const float sz = pow2_scale(warp_max(zmax));
+    if (i < N) {
+      for (int t = 0; t < S; t++) {
+        const float z = ((xr[t] - x0) - m1) * sz;
+        __half h, l;
+        split1(z, h, l);
+        z_hi[i * ly.zph + t] = h;
+        z_lo[i * ly.zph + t] = l;
+      }
+    }
+    const float inv = i < N ? rsqrtf(nu2 + kEpsSeasonal) : 0.f;
+    const float mbar = warp_sum(i < N ? mu : 0.f) * a.inv_n;
+    const float dv = i < N ? nu2 + (float)S * (mu - mbar) * (mu - mbar) : 0.f;
+    const float inv_var = 1.0f / (warp_sum(dv) * a.inv_ns + kEpsTrend);
+    __syncwarp();
+    // xbuf is free: fetch the next series while this one is in the tensor cores
+    if (b + nwarps < b_end) prefetch(b + nwarps);
+
+    // ---------------- a3: Gram G' = Z' Z'^T (sz^2 G), fragments g[mt][nt][.]
+    float g[MT][2 * MT][4];
+#pragma unroll
+    for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+      for (int nt = 0; nt < 2 * MT; nt++)
+#pragma unroll
+        for (int e = 0; e < 4; e++) g[mt][nt][e] = 0.f;
+    for (int k0 = 0; k0 < ly.kz; k0 += 16) {
+      uint32_t ah[MT][4], al[MT][4];
+#pragma unroll
+      for (int mt = 0; mt < MT; mt++) {
+        const int off = (16 * mt + (lane & 7) + 8 * (q8 & 1)) * ly.zph + k0 + 8 * (q8 >> 1);
+        ldsm_x4(ah[mt], z_hi + off);
+        ldsm_x4(al[mt], z_lo + off);
+      }
+#pragma unroll
+      for (int np = 0; np < MT; np++) {
+        uint32_t bh[4], bl[4];
+        const int off = (16 * np + (lane & 7) + 8 * (q8 >> 1)) * ly.zph + k0 + 8 * (q8 & 1);
+        ldsm_x4(bh, z_hi + off);
+        ldsm_x4(bl, z_lo + off);
+#pragma unroll
+        for (int mt = 0; mt < MT; mt++) {
+          mma3(g[mt][2 * np], ah[mt], al[mt], bh[0], bh[1], bl[0], bl[1]);
+          mma3(g[mt][2 * np + 1], ah[mt], al[mt], bh[2], bh[3], bl[2], bl[3]);
+        }
+      }
+    }
+
+    // per-column descriptors (j = 8 nt + 2 cq + e) and per-row (i = 16 mt + 8 h + gq)
+    float cinv[2 * MT][2], cmu[2 * MT][2], ckap[2 * MT][2];
+#pragma unroll
+    for (int nt = 0; nt < 2 * MT; nt++)
+#pragma unroll
+      for (int e = 0; e < 2; e++) {
+        const int j = 8 * nt + 2 * cq + e;
+        cinv[nt][e] = __shfl_sync(0xffffffffu, inv, j);
+        cmu[nt][e] = __shfl_sync(0xffffffffu, mu, j);
+        ckap[nt][e] = __shfl_sync(0xffffffffu, kap, j);
+      }
+    const float rsz2 = 1.f / (sz * sz);
+
+    // ---------------- a5 seasonal softmax on the fragments, pack, transpose (movmatrix)
+    uint32_t bsh[MT][2 * MT][2], bsl[MT][2 * MT][2];  // B operand of the fold: [k-tile][n-tile][b0/b1]
+#pragma unroll
+    for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int ii = 16 * mt + 8 * h + gq;
+        const float ri = __shfl_sync(0xffffffffu, inv, ii) * rsz2;
+        float mx = -INFINITY;
+#pragma unroll
+        for (int nt = 0; nt < 2 * MT; nt++)
+#pragma unroll
+          for (int e = 0; e < 2; e++) {
+            const int j = 8 * nt + 2 * cq + e;
+            float v = g[mt][nt][2 * h + e] * ri * cinv[nt][e];
+            v = j < N ? v : -INFINITY;
+            g[mt][nt][2 * h + e] = v;
+            mx = fmaxf(mx, v);
+          }
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        float sum = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < 2 * MT; nt++)
+#pragma unroll
+          for (int e = 0; e < 2; e++) {
+            const int j = 8 * nt + 2 * cq + e;
+            const float p = j < N ? fast_ex2((g[mt][nt][2 * h + e] - mx) * a.ks) : 0.f;
+            g[mt][nt][2 * h + e] = p;
+            sum += p;
+          }
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        const float rs = ii < N ? 1.f / sum : 0.f;
+#pragma unroll
+        for (int nt = 0; nt < 2 * MT; nt++) {
+          const float p0 = g[mt][nt][2 * h] * rs, p1 = g[mt][nt][2 * h + 1] * rs;
+          if (a.a_s_dbg != nullptr && ii < N) {
+            const int j = 8 * nt + 2 * cq;
+            float* d = a.a_s_dbg + (series * N + ii) * N + j;
+            if (j < N) d[0] = p0;
+            if (j + 1 < N) d[1] = p1;
+          }
+          uint32_t hi, lo;
+          split2(p0, p1, hi, lo);
+          bsh[mt][nt][h] = movm_t(hi);
+          bsl[mt][nt][h] = movm_t(lo);
+        }
+      }
+
+    // ---------------- a6+a7 fold, seasonal half: Q' += W'_s A_s   (Q' = sw Q)
+    float qa[MMT][2 * MT][4];
+#pragma unroll
+    for (int mm = 0; mm < MMT; mm++)
+#pragma unroll
+      for (int nt = 0; nt < 2 * MT; nt++)
+#pragma unroll
+        for (int e = 0; e < 4; e++) qa[mm][nt][e] = 0.f;
+#pragma unroll
+    for (int kt = 0; kt < MT; kt++) {
+#pragma unroll
+      for (int mm = 0; mm < MMT; mm++) {
+        uint32_t wh[4], wl[4];
+        const int off = (16 * mm + (lane & 7) + 8 * (q8 & 1)) * ly.wph + 16 * kt + 8 * (q8 >> 1);
+        ldsm_x4(wh, w_hi + off);
+        ldsm_x4(wl, w_lo + off);
+#pragma unroll
+        for (int nt = 0; nt < 2 * MT; nt++)
+          mma3(qa[mm][nt], wh, wl, bsh[kt][nt][0], bsh[kt][nt][1], bsl[kt][nt][0],
+               bsl[kt][nt][1]);
+      }
+    }
+
+    // ---------------- a4+a5 trend distances and softmax, pack, transpose
+#pragma unroll
+    for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int ii = 16 * mt + 8 * h + gq;
+        const float mui = __shfl_sync(0xffffffffu, mu, ii);
+        const float ki = __shfl_sync(0xffffffffu, kap, ii);
+        float mx = -INFINITY;
+#pragma unroll
+        for (int nt = 0; nt < 2 * MT; nt++)
+#pragma unroll
+          for (int e = 0; e < 2; e++) {
+            const int j = 8 * nt + 2 * cq + e;
+            const float dm = mui - cmu[nt][e], dk = ki - ckap[nt][e];
+            float v = -(fmaf(a.vtrend * dk, dk, dm * dm) * inv_var);
+            v = j < N ? v : -INFINITY;
+            g[mt][nt][2 * h + e] = v;
+            mx = fmaxf(mx, v);
+          }
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        float sum = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < 2 * MT; nt++)
+#pragma unroll
+          for (int e = 0; e < 2; e++) {
+            const int j = 8 * nt + 2 * cq + e;
+            const float p = j < N ? fast_ex2((g[mt][nt][2 * h + e] - mx) * a.kt) : 0.f;
+            g[mt][nt][2 * h + e] = p;
+            sum += p;
+          }
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        const float rs = ii < N ? 1.f / sum : 0.f;
+#pragma unroll
+        for (int nt = 0; nt < 2 * MT; nt++) {
+          const float p0 = g[mt][nt][2 * h] * rs, p1 = g[mt][nt][2 * h + 1] * rs;
+          if (a.a_t_dbg != nullptr && ii < N) {
+            const int j = 8 * nt + 2 * cq;
+            float* d = a.a_t_dbg + (series * N + ii) * N + j;
+            if (j < N) d[0] = p0;
+            if (j + 1 < N) d[1] = p1;
+          }
+          uint32_t hi, lo;
+          split2(p0, p1, hi, lo);
+          bsh[mt][nt][h] = movm_t(hi);
+          bsl[mt][nt][h] = movm_t(lo);
+        }
+      }
+
+    // ---------------- fold, trend half: Q' += W'_t A_t
+#pragma unroll
+    for (int kt = 0; kt < MT; kt++) {
+#pragma unroll
+      for (int mm = 0; mm < MMT; mm++) {
+        uint32_t wh[4], wl[4];
+        const int off =
+            (16 * mm + (lane & 7) + 8 * (q8 & 1)) * ly.wph + NR + 16 * kt + 8 * (q8 >> 1);
+        ldsm_x4(wh, w_hi + off);
+        ldsm_x4(wl, w_lo + off);
+#pragma unroll
+        for (int nt = 0; nt < 2 * MT; nt++)
+          mma3(qa[mm][nt], wh, wl, bsh[kt][nt][0], bsh[kt][nt][1], bsl[kt][nt][0],
+               bsl[kt][nt][1]);
+      }
+    }
+
+    // ---------------- Q' fragments -> A operand of the head (hi/lo, in registers)
+    uint32_t qh[MMT][MT][4], ql[MMT][MT][4];
+#pragma unroll
+    for (int mm = 0; mm < MMT; mm++)
+#pragma unroll
+      for (int kj = 0; kj < MT; kj++) {
+        split2(qa[mm][2 * kj][0], qa[mm][2 * kj][1], qh[mm][kj][0], ql[mm][kj][0]);
+        split2(qa[mm][2 * kj][2], qa[mm][2 * kj][3], qh[mm][kj][1], ql[mm][kj][1]);
+        split2(qa[mm][2 * kj + 1][0], qa[mm][2 * kj + 1][1], qh[mm][kj][2], ql[mm][kj][2]);
+        split2(qa[mm][2 * kj + 1][2], qa[mm][2 * kj + 1][3], qh[mm][kj][3], ql[mm][kj][3]);
+      }
+
+    // ---------------- a7 head Y' = Q' X' (= sw sx Y), t in chunks of 4 tiles; a8 store
+    const float yscale = inv_sw / sx;
+    float* yg = a.y + series * H;
+    for (int t0 = 0; t0 < ly.ntt; t0 += 4) {
+      float ya[MMT][4][4];
+#pragma unroll
+      for (int mm = 0; mm < MMT; mm++)
+#pragma unroll
+        for (int nt = 0; nt < 4; nt++)
+#pragma unroll
+          for (int e = 0; e < 4; e++) ya[mm][nt][e] = 0.f;
+#pragma unroll
+      for (int kj = 0; kj < MT; kj++) {
+#pragma unroll
+        for (int tp = 0; tp < 2; tp++) {
+          const int nt0 = t0 + 2 * tp;
+          if (nt0 >= ly.ntt) break;
+          uint32_t xh[4], xl[4];
+          const int krow = 16 * kj + (lane & 7) + 8 * (q8 & 1);
+          if (nt0 + 1 < ly.ntt) {
+            const int off = krow * ly.sph + 8 * (nt0 + (q8 >> 1));
+            ldsm_x4_t(xh, x_hi + off);
+            ldsm_x4_t(xl, x_lo + off);
+          } else {
+            const int off = krow * ly.sph + 8 * nt0;
+            ldsm_x2_t(xh[0], xh[1], x_hi + off);
+            ldsm_x2_t(xl[0], xl[1], x_lo + off);
+            xh[2] = xh[3] = xl[2] = xl[3] = 0u;
+          }
+#pragma unroll
+          for (int mm = 0; mm < MMT; mm++) {
+            mma3(ya[mm][2 * tp], qh[mm][kj], ql[mm][kj], xh[0], xh[1], xl[0], xl[1]);
+            if (nt0 + 1 < ly.ntt)
+              mma3(ya[mm][2 * tp + 1], qh[mm][kj], ql[mm][kj], xh[2], xh[3], xl[2], xl[3]);
+          }
+        }
+      }
+#pragma unroll
+      for (int mm = 0; mm < MMT; mm++)
+#pragma unroll
+        for (int nt = 0; nt < 4; nt++) {
+          const int t = 8 * (t0 + nt) + 2 * cq;
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int m = 16 * mm + 8 * h + gq;
+            if (m < M && t < S) {
+              const int hh = m * S + t;
+              const float v0 = ya[mm][nt][2 * h] * yscale;
+              const float v1 = ya[mm][nt][2 * h + 1] * yscale;
+              if (t + 1 < S && hh + 1 < H && (((series * H + hh) & 1) == 0)) {
+                float2 o = make_float2(v0 + bS[hh], v1 + bS[hh + 1]);
+                asm volatile("st.global.cs.v2.f32 [%0], {%1,%2};" ::"l"(yg + hh), "f"(o.x),
+                             "f"(o.y)
+                             : "memory");
+              } else {
+                if (hh < H) yg[hh] = v0 + bS[hh];
+                if (t + 1 < S && hh + 1 < H) yg[hh + 1] = v1 + bS[hh + 1];
+              }
+            }
+          }
+        }
+    }
+  }
+  cp_async_wait_all();
+}
+
+static int odd8(int halves) {  // round up to a multiple of 8 halves whose /8 is odd
+  int v = (halves + 7) & ~7;
+  if (((v / 8) & 1) == 0) v += 8;
+  return v;
+}
+
+bool plan_mma_kernel(const FwdArgs& a, int max_smem_optin, MmaPlan* p) {
+  if (a.N < 1 || a.N > 32 || a.M > 32 || a.S > 128) return false;
+  MmaLayout& ly = p->ly;
+  p->mt = a.N <= 16 ? 1 : 2;
+  p->mmt = a.M <= 16 ? 1 : 2;
+  ly.nr = 16 * p->mt;
+  ly.sph = odd8(a.S);
+  ly.kz = (a.S + 15) & ~15;
+  ly.zph = odd8(ly.kz);
+  ly.wph = 2 * ly.nr + 8;
+  ly.ntt = (a.S + 7) / 8;
+  ly.xbuf_f = (a.N * a.S + 3) & ~3;
+  int off = ly.xbuf_f * 4;
+  ly.off_xhi = off;
+  off += ly.nr * ly.sph * 2;
+  ly.off_xlo = off;
+  off += ly.nr * ly.sph * 2;
+  off = (off + 15) & ~15;
+  ly.off_zhi = off;
+  off += ly.nr * ly.zph * 2;
+  ly.off_zlo = off;
+  off += ly.nr * ly.zph * 2;
+  ly.per_warp_bytes = (off + 127) & ~127;
+  const int wrows = 16 * p->mmt;
+  int so = 0;
+  so += wrows * ly.wph * 2;
+  ly.off_wlo = so;
+  so += wrows * ly.wph * 2;
+  so = (so + 15) & ~15;
+  ly.off_bias = so;
+  so += a.H * 4;
+  ly.shared_bytes = (so + 127) & ~127;
+  p->warps_per_cta = 8;
+  p->smem_bytes = (size_t)ly.shared_bytes + (size_t)p->warps_per_cta * ly.per_warp_bytes;
+  while (p->smem_bytes > (size_t)max_smem_optin && p->warps_per_cta > 1) {
+    p->warps_per_cta >>= 1;
+    p->smem_bytes = (size_t)ly.shared_bytes + (size_t)p->warps_per_cta * ly.per_warp_bytes;
+  }
+  if (p->smem_bytes > (size_t)max_smem_optin) return false;
+  p->wins_per_cta = p->warps_per_cta * 4;
+  return true;
+}
+
+template <int MT, int MMT>
+static cudaError_t launch_t(const FwdArgs& a, const MmaPlan& p, cudaStream_t st) {
+  auto k = prnet_fwd_mma_kernel<MT, MMT>;
+  cudaError_t e =
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)((a.B + p.wins_per_cta - 1) / p.wins_per_cta), (unsigned)a.C);
+  k<<<grid, 32 * p.warps_per_cta, p.smem_bytes, st>>>(a, p.ly, p.wins_per_cta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mma_kernel(const FwdArgs& a, const MmaPlan& p, cudaStream_t st) {
+  if (p.mt == 1) return p.mmt == 1 ? launch_t<1, 1>(a, p, st) : launch_t<1, 2>(a, p, st);
+  return p.mmt == 1 ? launch_t<2, 1>(a, p, st) : launch_t<2, 2>(a, p, st);
+}
+
+}  // namespace prnet

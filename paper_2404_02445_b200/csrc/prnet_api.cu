@@ -19,6 +19,7 @@ struct prnet_handle {
   float* d_b = nullptr;
   double* d_err = nullptr;  // error-sum partials
   bool loaded = false;
+  int forced_variant = -1;  // prnet_set_kernel_variant
   std::string err;
   // host-forward runtime
   int64_t host_chunk = 0;   // windows per chunk (0 = default)
@@ -108,7 +109,13 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
   return pa < pb + nb && pb < pa + na;
 }
 
-int pick_variant(const prnet_handle* h) { return h->N <= 32 ? 0 : 1; }
+// 0 = warp_f32 (N <= 32, CUDA-core FP32), 1 = long_f32 (32 < N <= 512),
+// 2 = mma_f16x3 (N <= 32, M <= 32: tensor cores, split-fp16 3-product).
+int pick_variant(const prnet_handle* h) {
+  if (h->forced_variant >= 0) return h->forced_variant;
+  if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
+  return h->N <= 32 ? 0 : 1;
+}
 
 // Enqueue the forward for B windows (pointers already validated).
 prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* y, float* a_s,
@@ -117,7 +124,14 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
   a.a_s_dbg = a_s;
   a.a_t_dbg = a_t;
   cudaError_t e;
-  if (pick_variant(h) == 0) {
+  int v = pick_variant(h);
+  if (v == 1 && a_s != nullptr) v = 0;  // the attention dump lives in the N <= 32 kernels
+  if (v == 2) {
+    prnet::MmaPlan p;
+    if (!prnet::plan_mma_kernel(a, h->max_smem_optin, &p))
+      return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the tensor-core kernel");
+    e = prnet::launch_mma_kernel(a, p, st);
+  } else if (v == 0) {
     prnet::WarpPlan p;
     if (!prnet::plan_warp_kernel(a, h->max_smem_optin, &p))
       return fail(h, PRNET_ERR_UNSUPPORTED, "shape exceeds the N<=32 kernel's shared memory");
@@ -382,6 +396,17 @@ prnet_status prnet_error_sums(prnet_handle* h, const float* y, const float* targ
   const int64_t n = batch * h->cfg.channels * h->cfg.horizon;
   cudaError_t e = prnet::launch_error_sums(y, target, n, h->d_err, out3, (cudaStream_t)cuda_stream);
   return e == cudaSuccess ? PRNET_OK : cuda_fail(h, e, "error_sums launch");
+}
+
+prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {
+  if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
+  if (variant < -1 || variant > 2) return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,0,1,2}");
+  if ((variant == 0 || variant == 2) && h->N > 32)
+    return fail(h, PRNET_ERR_UNSUPPORTED, "variant needs N <= 32");
+  if (variant == 2 && (h->M > 32 || h->cfg.seg_len > 128))
+    return fail(h, PRNET_ERR_UNSUPPORTED, "tensor-core variant needs M <= 32 and S <= 128");
+  h->forced_variant = variant;
+  return PRNET_OK;
 }
 
 prnet_status prnet_forward_plan(const prnet_handle* h, int64_t batch, int32_t* kernel_launches,

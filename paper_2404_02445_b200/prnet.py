@@ -23,7 +23,8 @@ STATUS = {0: "PRNET_OK", 1: "PRNET_ERR_INVALID_ARG", 2: "PRNET_ERR_BAD_STATE",
 EXPORTS = ("prnet_create", "prnet_load_params", "prnet_forward", "prnet_forward_host",
            "prnet_set_host_chunk", "prnet_destroy", "prnet_last_error", "prnet_get_dims",
            "prnet_debug_segments", "prnet_debug_attention", "prnet_error_sums",
-           "prnet_forward_plan")
+           "prnet_forward_plan", "prnet_set_kernel_variant")
+VARIANTS = ("warp_f32", "long_f32", "mma_f16x3")
 
 
 class PrnetError(RuntimeError):
@@ -63,6 +64,7 @@ def load_library(path: str | None = None):
         "prnet_debug_attention": ([vp, vp, i64, vp, vp, vp], ctypes.c_int),
         "prnet_error_sums": ([vp, vp, vp, i64, vp, vp], ctypes.c_int),
         "prnet_forward_plan": ([vp, i64, i32p, i32p], ctypes.c_int),
+        "prnet_set_kernel_variant": ([vp, ctypes.c_int32], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -191,4 +193,11 @@ class PRNet:
     def plan(self, batch: int):
         n, v = ctypes.c_int32(), ctypes.c_int32()
         self._check(self._lib.prnet_forward_plan(self._h, batch, ctypes.byref(n), ctypes.byref(v)))
-        return {"kernel_launches": n.value, "variant": ("warp_n32", "long_n")[v.value]}
+        return {"kernel_launches": n.value, "variant": VARIANTS[v.value]}
+
+    def set_variant(self, variant):
+        """-1/None = automatic, or one of VARIANTS (or its index)."""
+        v = -1 if variant is None else (VARIANTS.index(variant) if isinstance(variant, str)
+                                        else int(variant))
+        self._check(self._lib.prnet_set_kernel_variant(self._h, v))
+        return self

@@ -16,16 +16,33 @@ if not torch.cuda.is_available():
 from paper_2404_02445_b200 import PRNet, PrnetError  # noqa: E402
 
 
-def _model(C, L, S, H, hpc=True, tau_s=1.0, tau_t=1.0, seed=synth.DEFAULT_SEED, cfg_id=0):
+def _model(C, L, S, H, hpc=True, tau_s=1.0, tau_t=1.0, seed=synth.DEFAULT_SEED, cfg_id=0,
+           variant=None):
     N, _, M = synth.derived_dims(L, S, H)
     ws, wt, b = synth.make_params(C, M, N, H, hpc, seed, cfg_id)
     m = PRNet(C, L, S, H, head_per_channel=hpc, tau_s=tau_s, tau_t=tau_t).load(ws, wt, b)
+    if variant is not None:
+        m.set_variant(variant)
     return m, (ws, wt, b)
 
 
-def _check_small(oracle_mod, x, S, H, hpc=True, tau_s=1.0, tau_t=1.0, scale=None):
+def _applicable(variant, L, S, H):
+    N, _, M = synth.derived_dims(L, S, H)
+    if variant == "warp_f32":
+        return N <= 32
+    if variant == "mma_f16x3":
+        return N <= 32 and M <= 32 and S <= 128
+    return True
+
+
+VARIANTS = [None, "warp_f32", "mma_f16x3", "long_f32"]
+
+
+def _check_small(oracle_mod, x, S, H, hpc=True, tau_s=1.0, tau_t=1.0, scale=None, variant=None):
     B, C, L = x.shape
-    m, (ws, wt, b) = _model(C, L, S, H, hpc, tau_s, tau_t)
+    if not _applicable(variant, L, S, H):
+        pytest.skip(f"{variant} not applicable to L={L} S={S} H={H}")
+    m, (ws, wt, b) = _model(C, L, S, H, hpc, tau_s, tau_t, variant=variant)
     xd = torch.from_numpy(x).cuda()
     y = m.forward(xd).cpu().numpy()
     _, y64 = oracle_mod.forward(x, S, H, ws, wt, b, hpc, tau_s, tau_t)
@@ -48,8 +65,9 @@ def test_etth1_full(oracle_mod):
 FULL = ["weather_h96", "weather_h192", "weather_h336", "weather_h720", "electricity", "traffic"]
 
 
+@pytest.mark.parametrize("variant", [None, "warp_f32"])
 @pytest.mark.parametrize("name", FULL)
-def test_full_size_sampled(oracle_mod, name):
+def test_full_size_sampled(oracle_mod, name, variant):
     """The whole test set runs on the GPU in the bench's launch configuration; the
     oracle checks windows {0, 1, B/2, B-1} plus a stride sample, all channels."""
     w = synth.WORKLOADS[name]
@@ -57,7 +75,7 @@ def test_full_size_sampled(oracle_mod, name):
     B = w.windows
     sd = torch.from_numpy(s).cuda()
     x = sd.unfold(1, w.L, 1)[:, w.t0:w.t0 + B, :].permute(1, 0, 2).contiguous()
-    m, (ws, wt, b) = _model(w.C, w.L, w.S, w.H, cfg_id=w.cfg_id)
+    m, (ws, wt, b) = _model(w.C, w.L, w.S, w.H, cfg_id=w.cfg_id, variant=variant)
     y = m.forward(x)
     torch.cuda.synchronize()
     idx = [0, 1, B // 2, B - 1]
@@ -105,28 +123,33 @@ def test_stress_full_size_sampled(oracle_mod, L, S):
 @pytest.mark.parametrize("L,S,H", [
     (96, 24, 96), (100, 24, 90), (97, 7, 13), (50, 49, 3), (24, 24, 24), (25, 24, 1),
     (64, 8, 64), (72, 8, 100), (128, 8, 64), (136, 8, 9), (256, 8, 40), (264, 8, 40),
-    (270, 9, 31), (33, 2, 5), (66, 2, 7), (720, 24, 720), (722, 12, 721), (1000, 3, 17)])
-def test_shapes_ragged(oracle_mod, L, S, H):
-    """N from 1 to 333 across the 8/16/32/long variants; L mod S != 0 (r > 0);
-    H mod S != 0; odd S and L (scalar load path)."""
+    (270, 9, 31), (33, 2, 5), (66, 2, 7), (720, 24, 720), (722, 12, 721), (1000, 3, 17),
+    (720, 24, 769), (720, 96, 96), (768, 24, 96), (767, 24, 700), (384, 128, 200),
+    (1440, 48, 96), (160, 5, 40)])
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_shapes_ragged(oracle_mod, L, S, H, variant):
+    """N from 1 to 333 across every kernel variant; L mod S != 0 (r > 0);
+    H mod S != 0; odd S and L (scalar load path); M > 32 falls back."""
     x = synth.random_windows(3, 5, L, kind="mixed")
-    _check_small(oracle_mod, x, S, H)
+    _check_small(oracle_mod, x, S, H, variant=variant)
 
 
+@pytest.mark.parametrize("variant", VARIANTS[:3])
 @pytest.mark.parametrize("tau", [0.05, 0.1, 1.0, 10.0])
 @pytest.mark.parametrize("hpc", [True, False])
-def test_temperatures_and_head_modes(oracle_mod, tau, hpc):
+def test_temperatures_and_head_modes(oracle_mod, tau, hpc, variant):
     x = synth.random_windows(4, 6, 720, kind="mixed")
-    _check_small(oracle_mod, x, 24, 336, hpc=hpc, tau_s=tau, tau_t=tau * 0.7)
+    _check_small(oracle_mod, x, 24, 336, hpc=hpc, tau_s=tau, tau_t=tau * 0.7, variant=variant)
 
 
+@pytest.mark.parametrize("variant", VARIANTS[:3])
 @pytest.mark.parametrize("kind", ["normal", "constant", "scaled"])
 @pytest.mark.parametrize("L,S", [(720, 24), (1440, 24)])
-def test_value_distributions(oracle_mod, kind, L, S):
+def test_value_distributions(oracle_mod, kind, L, S, variant):
     x = synth.random_windows(3, 4, L, kind=kind)
     scale = np.abs(x).max(axis=2, keepdims=True)[..., :1] if kind == "scaled" else None
     scale = None if scale is None else np.maximum(scale, 1.0)
-    _check_small(oracle_mod, x, S, 96, scale=scale)
+    _check_small(oracle_mod, x, S, 96, scale=scale, variant=variant)
 
 
 def test_batch_zero_and_one(oracle_mod):
@@ -148,10 +171,11 @@ def test_segment_gather_bit_exact(L, S):
     np.testing.assert_array_equal(seg, x[:, :, idx])
 
 
+@pytest.mark.parametrize("variant", ["warp_f32", "mma_f16x3"])
 @pytest.mark.parametrize("L,S", [(720, 24), (96, 24), (384, 24)])
-def test_attention_matrices(oracle_mod, L, S):
+def test_attention_matrices(oracle_mod, L, S, variant):
     x = synth.random_windows(2, 3, L, kind="mixed")
-    m, _ = _model(3, L, S, 24, tau_s=0.5, tau_t=2.0)
+    m, _ = _model(3, L, S, 24, tau_s=0.5, tau_t=2.0, variant=variant)
     a_s, a_t = m.debug_attention(torch.from_numpy(x).cuda())
     a_s, a_t = a_s.cpu().numpy(), a_t.cpu().numpy()
     np.testing.assert_allclose(a_s.sum(-1), 1.0, atol=1e-6)
@@ -167,10 +191,11 @@ def test_attention_matrices(oracle_mod, L, S):
 
 
 # ------------------------------------------------------------------ determinism, sharding, host path
-def test_deterministic_and_shard_invariant():
+@pytest.mark.parametrize("variant", VARIANTS[:3])
+def test_deterministic_and_shard_invariant(variant):
     from paper_2404_02445_b200 import shard_windows
     x = torch.from_numpy(synth.random_windows(37, 11, 720)).cuda()
-    m, _ = _model(11, 720, 24, 720)
+    m, _ = _model(11, 720, 24, 720, variant=variant)
     y1 = m.forward(x)
     y2 = m.forward(x)
     assert torch.equal(y1, y2)
