@@ -23,6 +23,8 @@
 // cp.async while the current one is in the tensor cores.
 #include <cuda_fp16.h>
 
+#include <cmath>
+
 #include "prnet_internal.cuh"
 
 namespace prnet {
@@ -125,41 +127,19 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
   const int cw = a.head_per_channel ? c : 0;
   const int S = a.S, N = a.N, M = a.M, H = a.H, L = a.L, C = a.C;
 
-  // ---------------- CTA-shared: W' = W * sw as fp16 hi/lo, [16*MMT][wph], cols: i (seasonal)
-  // at [0, NR), i (trend) at [NR, 2NR); zeros outside m < M, i < N.  Bias fp32.
+  // ---------------- CTA-shared: the channel's pre-packed head (prnet_load_params):
+  // W' = W * sw as fp16 hi/lo [16*MMT][wph] (cols: seasonal i at [0, NR), trend i at
+  // [NR, 2NR), zeros elsewhere), 1/sw, and the fp32 bias.
   __half* w_hi = reinterpret_cast<__half*>(smem);
   __half* w_lo = reinterpret_cast<__half*>(smem + ly.off_wlo);
   float* bS = reinterpret_cast<float*>(smem + ly.off_bias);
-  __shared__ float red[8];
-  float inv_sw;
+  const float inv_sw = a.wpack_inv_sw[cw];
   {
-    const float* gws = a.ws + (int64_t)cw * M * N;
-    const float* gwt = a.wt + (int64_t)cw * M * N;
-    float mx = 0.f;
-    for (int k = threadIdx.x; k < M * N; k += blockDim.x)
-      mx = fmaxf(mx, fmaxf(fabsf(gws[k]), fabsf(gwt[k])));
-    mx = warp_max(mx);
-    if (lane == 0) red[warp] = mx;
-    __syncthreads();
-    mx = 0.f;
-    for (int w = 0; w < nwarps; w++) mx = fmaxf(mx, red[w]);
-    const float sw = pow2_scale(mx);
-    inv_sw = 1.f / sw;
-    const int rows = 16 * MMT;
-    for (int k = threadIdx.x; k < rows * ly.wph; k += blockDim.x) {
-      const int m = k / ly.wph, col = k - m * ly.wph;
-      float v = 0.f;
-      if (m < M) {
-        if (col < NR) {
-          if (col < N) v = gws[m * N + col] * sw;
-        } else if (col < 2 * NR) {
-          if (col - NR < N) v = gwt[m * N + (col - NR)] * sw;
-        }
-      }
-      split1(v, w_hi[k], w_lo[k]);
-    }
+    const uint4* src = a.wpack + (int64_t)cw * (ly.wpack_bytes / 16);
+    uint4* dst = reinterpret_cast<uint4*>(smem);
+    for (int k = threadIdx.x; k < ly.wpack_bytes / 16; k += blockDim.x) dst[k] = __ldg(src + k);
     const float* gb = a.bias + (int64_t)cw * H;
-    for (int k = threadIdx.x; k < H; k += blockDim.x) bS[k] = gb[k];
+    for (int k = threadIdx.x; k < H; k += blockDim.x) bS[k] = __ldg(gb + k);
   }
 
   // ---------------- per-warp: fp32 staging, X' hi/lo [NR][sph], Z' hi/lo [NR][zph]
@@ -169,10 +149,11 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
   __half* x_lo = reinterpret_cast<__half*>(wb + ly.off_xlo);
   __half* z_hi = reinterpret_cast<__half*>(wb + ly.off_zhi);
   __half* z_lo = reinterpret_cast<__half*>(wb + ly.off_zlo);
+  float* dsm = reinterpret_cast<float*>(wb + ly.off_diag);   // [32] Gram diagonal
   {
     // zero the fp16 operand tiles once: padding rows (>= N) and columns (>= S) stay 0
     uint32_t* p = reinterpret_cast<uint32_t*>(wb + ly.off_xhi);
-    const int words = (ly.per_warp_bytes - ly.off_xhi) / 4;
+    const int words = (ly.off_diag - ly.off_xhi) / 4;
     for (int k = lane; k < words; k += 32) p[k] = 0u;
   }
   __syncthreads();
@@ -201,51 +182,75 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
     cp_async_wait_all();
     __syncwarp();
 
-    // ---------------- a2: descriptors (fp32), lane i = segment i
-    float amax = 0.f;
-    for (int k = lane; k < NS; k += 32) amax = fmaxf(amax, fabsf(xbuf[k]));
-    const float sx = pow2_scale(warp_max(amax));
+    // ---------------- a2 pass 1 (lane i = segment i): sums of d = x - x0 (x0 = the
+    // segment's first value, so a constant segment gives exact zeros), t~ d, max|x|, max|d|
     const int i = lane;
-    float mu = 0.f, m1 = 0.f, x0 = 0.f, nu2 = 0.f, kap = 0.f, zmax = 0.f;
-    const float* xr = xbuf + i * S;
+    float x0 = 0.f, s1 = 0.f, s3 = 0.f, amx = 0.f, dmx = 0.f;
     if (i < N) {
+      const float* xr = xbuf + i * S;
       x0 = xr[0];
-      float s = 0.f;
-      for (int t = 0; t < S; t++) s += xr[t] - x0;
-      m1 = s * a.inv_s;
-      mu = x0 + m1;
-      for (int t = 0; t < S; t++) {
-        const float v = xr[t];
-        const float z = (v - x0) - m1;
-        nu2 = fmaf(z, z, nu2);
-        kap = fmaf((float)t - a.half_s, z, kap);
-        zmax = fmaxf(zmax, fabsf(z));
+      auto acc1 = [&](float v, int t) {
+        const float d = v - x0;
+        s1 += d;
+        s3 = fmaf((float)t - a.half_s, d, s3);
+        amx = fmaxf(amx, fabsf(v));
+        dmx = fmaxf(dmx, fabsf(d));
+      };
+      if ((S & 3) == 0) {
+        for (int t = 0; t < S; t += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(xr + t);
+          acc1(v.x, t);
+          acc1(v.y, t + 1);
+          acc1(v.z, t + 2);
+          acc1(v.w, t + 3);
+        }
+      } else {
+        for (int t = 0; t < S; t++) acc1(xr[t], t);
+      }
+    }
+    const float m1 = s1 * a.inv_s;        // mu - x0
+    const float mu = x0 + m1;             // Def 4: mu_i
+    const float kap = s3 * a.inv_v;       // Def 4: kappa_i (sum t~ z = sum t~ d)
+    const float sx = pow2_scale(warp_max(amx));
+    const float sz = pow2_scale(2.f * warp_max(dmx));  // |z| <= 2 max|d|
+
+    // ---------------- a2 pass 2 (coalesced over element pairs): X' = x sx, Z' = z sz as
+    // fp16 hi/lo, z = (x - x0_i) - m1_i  (Def 4)
+    if ((S & 1) == 0) {
+      for (int p = lane; p < (NS >> 1); p += 32) {
+        const int k = 2 * p;
+        const int r = (int)(((float)k + 0.5f) * a.inv_s);
+        const int t = k - r * S;
+        const float2 v = *reinterpret_cast<const float2*>(xbuf + k);
+        const float xr0 = __shfl_sync(0xffffffffu, x0, r), mr = __shfl_sync(0xffffffffu, m1, r);
+        uint32_t h, l;
+        split2(v.x * sx, v.y * sx, h, l);
+        *reinterpret_cast<uint32_t*>(x_hi + r * ly.sph + t) = h;
+        *reinterpret_cast<uint32_t*>(x_lo + r * ly.sph + t) = l;
+        split2(((v.x - xr0) - mr) * sz, ((v.y - xr0) - mr) * sz, h, l);
+        *reinterpret_cast<uint32_t*>(z_hi + r * ly.zph + t) = h;
+        *reinterpret_cast<uint32_t*>(z_lo + r * ly.zph + t) = l;
+      }
+    } else {
+      for (int k = lane; k < NS; k += 32) {
+        const int r = (int)(((float)k + 0.5f) * a.inv_s);
+        const int t = k - r * S;
+        const float v = xbuf[k];
+        const float xr0 = __shfl_sync(0xffffffffu, x0, r), mr = __shfl_sync(0xffffffffu, m1, r);
         __half h, l;
         split1(v * sx, h, l);
-        x_hi[i * ly.sph + t] = h;
-        x_lo[i * ly.sph + t] = l;
-      }
-      kap *= a.inv_v;
-    }
-    const float sz = pow2_scale(warp_max(zmax));
-    if (i < N) {
-      for (int t = 0; t < S; t++) {
-        const float z = ((xr[t] - x0) - m1) * sz;
-        __half h, l;
-        split1(z, h, l);
-        z_hi[i * ly.zph + t] = h;
-        z_lo[i * ly.zph + t] = l;
+        x_hi[r * ly.sph + t] = h;
+        x_lo[r * ly.sph + t] = l;
+        split1(((v - xr0) - mr) * sz, h, l);
+        z_hi[r * ly.zph + t] = h;
+        z_lo[r * ly.zph + t] = l;
       }
     }
-    const float inv = i < N ? rsqrtf(nu2 + kEpsSeasonal) : 0.f;
-    const float mbar = warp_sum(i < N ? mu : 0.f) * a.inv_n;
-    const float dv = i < N ? nu2 + (float)S * (mu - mbar) * (mu - mbar) : 0.f;
-    const float inv_var = 1.0f / (warp_sum(dv) * a.inv_ns + kEpsTrend);
     __syncwarp();
     // xbuf is free: fetch the next series while this one is in the tensor cores
     if (b + nwarps < b_end) prefetch(b + nwarps);
 
-    // ---------------- a3: Gram G' = Z' Z'^T (sz^2 G), fragments g[mt][nt][.]
+    // ---------------- a3: Gram G' = Z' Z'^T (= sz^2 G), fragments g[mt][nt][.]
     float g[MT][2 * MT][4];
 #pragma unroll
     for (int mt = 0; mt < MT; mt++)
@@ -274,19 +279,41 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
         }
       }
     }
+    // diagonal G'_ii = sz^2 nu2_i (Def 4) lives in lane 4 gq + gq/2: publish via smem
+    if (cq == (gq >> 1)) {
+#pragma unroll
+      for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+        for (int h = 0; h < 2; h++)
+          dsm[16 * mt + 8 * h + gq] =
+              (gq & 1) ? g[mt][2 * mt + h][2 * h + 1] : g[mt][2 * mt + h][2 * h];
+    }
+    __syncwarp();
+    const float diag = i < N ? dsm[i] : 0.f;
+    // Def 6 normaliser in sz^2 units: rho_ij = G'_ij inv_i inv_j
+    const float inv = i < N ? rsqrtf(diag + kEpsSeasonal * sz * sz) : 1.f;
+    // Def 5: sigma^2 = (1/(N S)) sum_n [nu2_n + S (mu_n - mubar)^2]
+    const float mbar = warp_sum(i < N ? mu : 0.f) * a.inv_n;
+    const float dv = i < N ? diag / (sz * sz) + (float)S * (mu - mbar) * (mu - mbar) : 0.f;
+    const float inv_var = 1.0f / (warp_sum(dv) * a.inv_ns + kEpsTrend);
+    // trend exponent -(Dhat/tau_t) log2 e = -(mu~_i - mu~_j)^2 - (k~_i - k~_j)^2 with
+    // mu~ = mu sqrt(inv_var kt), k~ = kappa sqrt(vtrend inv_var kt)   (Def 7-8)
+    const float cm = sqrtf(inv_var * a.kt), ck = sqrtf(a.vtrend * inv_var * a.kt);
+    const float mus = i < N ? mu * cm : 0.f, kas = i < N ? kap * ck : 0.f;
 
-    // per-column descriptors (j = 8 nt + 2 cq + e) and per-row (i = 16 mt + 8 h + gq)
-    float cinv[2 * MT][2], cmu[2 * MT][2], ckap[2 * MT][2];
+    // per-column quantities (j = 8 nt + 2 cq + e), masked past N
+    float cinv[2 * MT][2], cmask[2 * MT][2], cmu[2 * MT][2], ckap[2 * MT][2];
 #pragma unroll
     for (int nt = 0; nt < 2 * MT; nt++)
 #pragma unroll
       for (int e = 0; e < 2; e++) {
         const int j = 8 * nt + 2 * cq + e;
         cinv[nt][e] = __shfl_sync(0xffffffffu, inv, j);
-        cmu[nt][e] = __shfl_sync(0xffffffffu, mu, j);
-        ckap[nt][e] = __shfl_sync(0xffffffffu, kap, j);
+        cmask[nt][e] = j < N ? 0.f : -INFINITY;
+        const float mj = __shfl_sync(0xffffffffu, mus, j);
+        cmu[nt][e] = j < N ? mj : INFINITY;
+        ckap[nt][e] = __shfl_sync(0xffffffffu, kas, j);
       }
-    const float rsz2 = 1.f / (sz * sz);
 
     // ---------------- a5 seasonal softmax on the fragments, pack, transpose (movmatrix)
     uint32_t bsh[MT][2 * MT][2], bsl[MT][2 * MT][2];  // B operand of the fold: [k-tile][n-tile][b0/b1]
@@ -295,27 +322,25 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
 #pragma unroll
       for (int h = 0; h < 2; h++) {
         const int ii = 16 * mt + 8 * h + gq;
-        const float ri = __shfl_sync(0xffffffffu, inv, ii) * rsz2;
+        const float rk = __shfl_sync(0xffffffffu, inv, ii) * a.ks;
         float mx = -INFINITY;
 #pragma unroll
         for (int nt = 0; nt < 2 * MT; nt++)
 #pragma unroll
           for (int e = 0; e < 2; e++) {
-            const int j = 8 * nt + 2 * cq + e;
-            float v = g[mt][nt][2 * h + e] * ri * cinv[nt][e];
-            v = j < N ? v : -INFINITY;
-            g[mt][nt][2 * h + e] = v;
-            mx = fmaxf(mx, v);
+            const float u = fmaf(g[mt][nt][2 * h + e], cinv[nt][e], cmask[nt][e]);
+            g[mt][nt][2 * h + e] = u;
+            mx = fmaxf(mx, u);
           }
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float nb = -mx * rk;
         float sum = 0.f;
 #pragma unroll
         for (int nt = 0; nt < 2 * MT; nt++)
 #pragma unroll
           for (int e = 0; e < 2; e++) {
-            const int j = 8 * nt + 2 * cq + e;
-            const float p = j < N ? fast_ex2((g[mt][nt][2 * h + e] - mx) * a.ks) : 0.f;
+            const float p = fast_ex2(fmaf(g[mt][nt][2 * h + e], rk, nb));
             g[mt][nt][2 * h + e] = p;
             sum += p;
           }
@@ -361,35 +386,21 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
       }
     }
 
-    // ---------------- a4+a5 trend distances and softmax, pack, transpose
+    // ---------------- a4+a5 trend: exponent -Dhat_ij / tau_t (row max is 0 at j = i, D_ii = 0)
 #pragma unroll
     for (int mt = 0; mt < MT; mt++)
 #pragma unroll
       for (int h = 0; h < 2; h++) {
         const int ii = 16 * mt + 8 * h + gq;
-        const float mui = __shfl_sync(0xffffffffu, mu, ii);
-        const float ki = __shfl_sync(0xffffffffu, kap, ii);
-        float mx = -INFINITY;
-#pragma unroll
-        for (int nt = 0; nt < 2 * MT; nt++)
-#pragma unroll
-          for (int e = 0; e < 2; e++) {
-            const int j = 8 * nt + 2 * cq + e;
-            const float dm = mui - cmu[nt][e], dk = ki - ckap[nt][e];
-            float v = -(fmaf(a.vtrend * dk, dk, dm * dm) * inv_var);
-            v = j < N ? v : -INFINITY;
-            g[mt][nt][2 * h + e] = v;
-            mx = fmaxf(mx, v);
-          }
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float mui = __shfl_sync(0xffffffffu, mus, ii);
+        const float ki = __shfl_sync(0xffffffffu, kas, ii);
         float sum = 0.f;
 #pragma unroll
         for (int nt = 0; nt < 2 * MT; nt++)
 #pragma unroll
           for (int e = 0; e < 2; e++) {
-            const int j = 8 * nt + 2 * cq + e;
-            const float p = j < N ? fast_ex2((g[mt][nt][2 * h + e] - mx) * a.kt) : 0.f;
+            const float dm = mui - cmu[nt][e], dk = ki - ckap[nt][e];
+            const float p = fast_ex2(fmaf(-dk, dk, -dm * dm));
             g[mt][nt][2 * h + e] = p;
             sum += p;
           }
@@ -443,6 +454,7 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
 
     // ---------------- a7 head Y' = Q' X' (= sw sx Y), t in chunks of 4 tiles; a8 store
     const float yscale = inv_sw / sx;
+    const bool pair_store = ((S | H) & 1) == 0;   // t, hh even -> 8-byte aligned pairs
     float* yg = a.y + series * H;
     for (int t0 = 0; t0 < ly.ntt; t0 += 4) {
       float ya[MMT][4][4];
@@ -490,7 +502,7 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
               const int hh = m * S + t;
               const float v0 = ya[mm][nt][2 * h] * yscale;
               const float v1 = ya[mm][nt][2 * h + 1] * yscale;
-              if (t + 1 < S && hh + 1 < H && (((series * H + hh) & 1) == 0)) {
+              if (pair_store) {
                 float2 o = make_float2(v0 + bS[hh], v1 + bS[hh + 1]);
                 asm volatile("st.global.cs.v2.f32 [%0], {%1,%2};" ::"l"(yg + hh), "f"(o.x),
                              "f"(o.y)
@@ -505,6 +517,46 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
     }
   }
   cp_async_wait_all();
+}
+
+int mma_wpack_bytes(int N, int M) {
+  const int nr = N <= 16 ? 16 : 32, rows = M <= 16 ? 16 : 32, wph = 2 * nr + 8;
+  return ((2 * rows * wph * 2) + 15) & ~15;
+}
+
+void pack_mma_head(const float* ws, const float* wt, int Cw, int M, int N, unsigned char* out,
+                   float* inv_sw) {
+  const int nr = N <= 16 ? 16 : 32, rows = M <= 16 ? 16 : 32, wph = 2 * nr + 8;
+  const int bytes = mma_wpack_bytes(N, M);
+  for (int c = 0; c < Cw; c++) {
+    const float* s = ws + (size_t)c * M * N;
+    const float* t = wt + (size_t)c * M * N;
+    float mx = 0.f;
+    for (int k = 0; k < M * N; k++) mx = fmaxf(mx, fmaxf(fabsf(s[k]), fabsf(t[k])));
+    float sw = 1.f;
+    if (mx > 0.f && std::isfinite(mx)) {
+      int e;
+      frexpf(mx, &e);
+      sw = ldexpf(1.f, -e);
+    }
+    inv_sw[c] = 1.f / sw;
+    __half* hi = reinterpret_cast<__half*>(out + (size_t)c * bytes);
+    __half* lo = hi + rows * wph;
+    for (int m = 0; m < rows; m++)
+      for (int col = 0; col < wph; col++) {
+        float v = 0.f;
+        if (m < M) {
+          if (col < nr) {
+            if (col < N) v = s[m * N + col] * sw;
+          } else if (col < 2 * nr) {
+            if (col - nr < N) v = t[m * N + (col - nr)] * sw;
+          }
+        }
+        const __half h = __float2half_rn(v);
+        hi[m * wph + col] = h;
+        lo[m * wph + col] = __float2half_rn(v - __half2float(h));
+      }
+  }
 }
 
 static int odd8(int halves) {  // round up to a multiple of 8 halves whose /8 is odd
@@ -535,6 +587,9 @@ bool plan_mma_kernel(const FwdArgs& a, int max_smem_optin, MmaPlan* p) {
   off += ly.nr * ly.zph * 2;
   ly.off_zlo = off;
   off += ly.nr * ly.zph * 2;
+  off = (off + 15) & ~15;
+  ly.off_diag = off;
+  off += 32 * 4;
   ly.per_warp_bytes = (off + 127) & ~127;
   const int wrows = 16 * p->mmt;
   int so = 0;
@@ -542,6 +597,7 @@ bool plan_mma_kernel(const FwdArgs& a, int max_smem_optin, MmaPlan* p) {
   ly.off_wlo = so;
   so += wrows * ly.wph * 2;
   so = (so + 15) & ~15;
+  ly.wpack_bytes = so;
   ly.off_bias = so;
   so += a.H * 4;
   ly.shared_bytes = (so + 127) & ~127;
@@ -552,7 +608,7 @@ bool plan_mma_kernel(const FwdArgs& a, int max_smem_optin, MmaPlan* p) {
     p->smem_bytes = (size_t)ly.shared_bytes + (size_t)p->warps_per_cta * ly.per_warp_bytes;
   }
   if (p->smem_bytes > (size_t)max_smem_optin) return false;
-  p->wins_per_cta = p->warps_per_cta * 4;
+  p->wins_per_cta = p->warps_per_cta * 8;
   return true;
 }
 

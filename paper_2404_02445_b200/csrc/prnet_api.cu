@@ -6,6 +6,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/prnet.h"
 #include "prnet_internal.cuh"
@@ -18,6 +19,8 @@ struct prnet_handle {
   float* d_wt = nullptr;
   float* d_b = nullptr;
   double* d_err = nullptr;  // error-sum partials
+  unsigned char* d_wpack = nullptr;  // mma variant: packed fp16 hi/lo head
+  float* d_invsw = nullptr;
   bool loaded = false;
   int forced_variant = -1;  // prnet_set_kernel_variant
   std::string err;
@@ -67,6 +70,8 @@ prnet::FwdArgs make_args(const prnet_handle* h, const float* x, int64_t B, float
   a.ws = h->d_ws;
   a.wt = h->d_wt;
   a.bias = h->d_b;
+  a.wpack = reinterpret_cast<const uint4*>(h->d_wpack);
+  a.wpack_inv_sw = h->d_invsw;
   a.B = B;
   a.C = c.channels;
   a.L = c.lookback;
@@ -244,6 +249,22 @@ prnet_status prnet_load_params(prnet_handle* h, const float* w_seasonal, const f
       (e = cudaMemcpy(h->d_wt, w_trend, want_w * 4, cudaMemcpyHostToDevice)) != cudaSuccess ||
       (e = cudaMemcpy(h->d_b, bias, want_b * 4, cudaMemcpyHostToDevice)) != cudaSuccess)
     return cuda_fail(h, e, "cudaMemcpy(params)");
+  if (h->N <= 32 && h->M <= 32) {  // pre-pack the head for the tensor-core variant
+    const int bytes = prnet::mma_wpack_bytes(h->N, h->M);
+    std::vector<unsigned char> pack((size_t)h->Cw * bytes);
+    std::vector<float> inv(h->Cw);
+    prnet::pack_mma_head(w_seasonal, w_trend, h->Cw, h->M, h->N, pack.data(), inv.data());
+    if (!h->d_wpack) {
+      if ((e = cudaMalloc(&h->d_wpack, pack.size())) != cudaSuccess ||
+          (e = cudaMalloc(&h->d_invsw, inv.size() * 4)) != cudaSuccess)
+        return cuda_fail(h, e, "cudaMalloc(packed head)");
+    }
+    if ((e = cudaMemcpy(h->d_wpack, pack.data(), pack.size(), cudaMemcpyHostToDevice)) !=
+            cudaSuccess ||
+        (e = cudaMemcpy(h->d_invsw, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice)) !=
+            cudaSuccess)
+      return cuda_fail(h, e, "cudaMemcpy(packed head)");
+  }
   h->loaded = true;
   return PRNET_OK;
 }
@@ -326,6 +347,8 @@ void prnet_destroy(prnet_handle* h) {
     cudaFree(h->d_wt);
     cudaFree(h->d_b);
     cudaFree(h->d_err);
+    cudaFree(h->d_wpack);
+    cudaFree(h->d_invsw);
     for (int k = 0; k < prnet_handle::kStages; k++) {
       cudaFree(h->d_xstage[k]);
       cudaFree(h->d_ystage[k]);
