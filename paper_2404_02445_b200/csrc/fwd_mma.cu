@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
   __half* z_hi = reinterpret_cast<__half*>(wb + ly.off_zhi);
   __half* z_lo = reinterpret_cast<__half*>(wb + ly.off_zlo);
   float* dsm = reinterpret_cast<float*>(wb + ly.off_diag);   // [32] Gram diagonal
+  float* rsm = dsm + 32;                                      // [64] x0, m1 per row
   {
     // zero the fp16 operand tiles once: padding rows (>= N) and columns (>= S) stay 0
     uint32_t* p = reinterpret_cast<uint32_t*>(wb + ly.off_xhi);
@@ -213,6 +214,9 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
     const float kap = s3 * a.inv_v;       // Def 4: kappa_i (sum t~ z = sum t~ d)
     const float sx = pow2_scale(warp_max(amx));
     const float sz = pow2_scale(2.f * warp_max(dmx));  // |z| <= 2 max|d|
+    rsm[lane] = x0;        // per-row shift and mean for the coalesced pass (no shuffles in
+    rsm[32 + lane] = m1;   // its lane-divergent loop)
+    __syncwarp();
 
     // ---------------- a2 pass 2 (coalesced over element pairs): X' = x sx, Z' = z sz as
     // fp16 hi/lo, z = (x - x0_i) - m1_i  (Def 4)
@@ -222,7 +226,7 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
         const int r = (int)(((float)k + 0.5f) * a.inv_s);
         const int t = k - r * S;
         const float2 v = *reinterpret_cast<const float2*>(xbuf + k);
-        const float xr0 = __shfl_sync(0xffffffffu, x0, r), mr = __shfl_sync(0xffffffffu, m1, r);
+        const float xr0 = rsm[r], mr = rsm[32 + r];
         uint32_t h, l;
         split2(v.x * sx, v.y * sx, h, l);
         *reinterpret_cast<uint32_t*>(x_hi + r * ly.sph + t) = h;
@@ -236,7 +240,7 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
         const int r = (int)(((float)k + 0.5f) * a.inv_s);
         const int t = k - r * S;
         const float v = xbuf[k];
-        const float xr0 = __shfl_sync(0xffffffffu, x0, r), mr = __shfl_sync(0xffffffffu, m1, r);
+        const float xr0 = rsm[r], mr = rsm[32 + r];
         __half h, l;
         split1(v * sx, h, l);
         x_hi[r * ly.sph + t] = h;
@@ -589,7 +593,7 @@ bool plan_mma_kernel(const FwdArgs& a, int max_smem_optin, MmaPlan* p) {
   off += ly.nr * ly.zph * 2;
   off = (off + 15) & ~15;
   ly.off_diag = off;
-  off += 32 * 4;
+  off += 96 * 4;
   ly.per_warp_bytes = (off + 127) & ~127;
   const int wrows = 16 * p->mmt;
   int so = 0;
