@@ -221,10 +221,10 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
     // ---------------- a2 pass 2 (coalesced over element pairs): X' = x sx, Z' = z sz as
     // fp16 hi/lo, z = (x - x0_i) - m1_i  (Def 4)
     if ((S & 1) == 0) {
-      for (int p = lane; p < (NS >> 1); p += 32) {
-        const int k = 2 * p;
-        const int r = (int)(((float)k + 0.5f) * a.inv_s);
-        const int t = k - r * S;
+      // element k = 2 p walks with stride 64: (row r, col t) advance by (step_r, step_t)
+      int r = (2 * lane) / S, t = 2 * lane - r * S;
+      const int step_r = 64 / S, step_t = 64 - step_r * S;
+      for (int k = 2 * lane; k < NS; k += 64) {
         const float2 v = *reinterpret_cast<const float2*>(xbuf + k);
         const float xr0 = rsm[r], mr = rsm[32 + r];
         uint32_t h, l;
@@ -234,11 +234,17 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
         split2(((v.x - xr0) - mr) * sz, ((v.y - xr0) - mr) * sz, h, l);
         *reinterpret_cast<uint32_t*>(z_hi + r * ly.zph + t) = h;
         *reinterpret_cast<uint32_t*>(z_lo + r * ly.zph + t) = l;
+        r += step_r;
+        t += step_t;
+        if (t >= S) {
+          t -= S;
+          r++;
+        }
       }
     } else {
+      int r = lane / S, t = lane - r * S;
+      const int step_r = 32 / S, step_t = 32 - step_r * S;
       for (int k = lane; k < NS; k += 32) {
-        const int r = (int)(((float)k + 0.5f) * a.inv_s);
-        const int t = k - r * S;
         const float v = xbuf[k];
         const float xr0 = rsm[r], mr = rsm[32 + r];
         __half h, l;
@@ -248,6 +254,12 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
         split1(((v - xr0) - mr) * sz, h, l);
         z_hi[r * ly.zph + t] = h;
         z_lo[r * ly.zph + t] = l;
+        r += step_r;
+        t += step_t;
+        if (t >= S) {
+          t -= S;
+          r++;
+        }
       }
     }
     __syncwarp();
@@ -276,10 +288,21 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
         const int off = (16 * np + (lane & 7) + 8 * (q8 >> 1)) * ly.zph + k0 + 8 * (q8 & 1);
         ldsm_x4(bh, z_hi + off);
         ldsm_x4(bl, z_lo + off);
+        // product-major order: independent accumulators back to back (no MMA-latency chains)
 #pragma unroll
         for (int mt = 0; mt < MT; mt++) {
-          mma3(g[mt][2 * np], ah[mt], al[mt], bh[0], bh[1], bl[0], bl[1]);
-          mma3(g[mt][2 * np + 1], ah[mt], al[mt], bh[2], bh[3], bl[2], bl[3]);
+          mma16816(g[mt][2 * np], al[mt], bh[0], bh[1]);
+          mma16816(g[mt][2 * np + 1], al[mt], bh[2], bh[3]);
+        }
+#pragma unroll
+        for (int mt = 0; mt < MT; mt++) {
+          mma16816(g[mt][2 * np], ah[mt], bl[0], bl[1]);
+          mma16816(g[mt][2 * np + 1], ah[mt], bl[2], bl[3]);
+        }
+#pragma unroll
+        for (int mt = 0; mt < MT; mt++) {
+          mma16816(g[mt][2 * np], ah[mt], bh[0], bh[1]);
+          mma16816(g[mt][2 * np + 1], ah[mt], bh[2], bh[3]);
         }
       }
     }
@@ -384,9 +407,11 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
         ldsm_x4(wh, w_hi + off);
         ldsm_x4(wl, w_lo + off);
 #pragma unroll
-        for (int nt = 0; nt < 2 * MT; nt++)
-          mma3(qa[mm][nt], wh, wl, bsh[kt][nt][0], bsh[kt][nt][1], bsl[kt][nt][0],
-               bsl[kt][nt][1]);
+        for (int nt = 0; nt < 2 * MT; nt++) mma16816(qa[mm][nt], wl, bsh[kt][nt][0], bsh[kt][nt][1]);
+#pragma unroll
+        for (int nt = 0; nt < 2 * MT; nt++) mma16816(qa[mm][nt], wh, bsl[kt][nt][0], bsl[kt][nt][1]);
+#pragma unroll
+        for (int nt = 0; nt < 2 * MT; nt++) mma16816(qa[mm][nt], wh, bsh[kt][nt][0], bsh[kt][nt][1]);
       }
     }
 
@@ -438,9 +463,11 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
         ldsm_x4(wh, w_hi + off);
         ldsm_x4(wl, w_lo + off);
 #pragma unroll
-        for (int nt = 0; nt < 2 * MT; nt++)
-          mma3(qa[mm][nt], wh, wl, bsh[kt][nt][0], bsh[kt][nt][1], bsl[kt][nt][0],
-               bsl[kt][nt][1]);
+        for (int nt = 0; nt < 2 * MT; nt++) mma16816(qa[mm][nt], wl, bsh[kt][nt][0], bsh[kt][nt][1]);
+#pragma unroll
+        for (int nt = 0; nt < 2 * MT; nt++) mma16816(qa[mm][nt], wh, bsl[kt][nt][0], bsl[kt][nt][1]);
+#pragma unroll
+        for (int nt = 0; nt < 2 * MT; nt++) mma16816(qa[mm][nt], wh, bsh[kt][nt][0], bsh[kt][nt][1]);
       }
     }
 
@@ -486,11 +513,21 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
             ldsm_x2_t(xl[0], xl[1], x_lo + off);
             xh[2] = xh[3] = xl[2] = xl[3] = 0u;
           }
+          const bool two = nt0 + 1 < ly.ntt;
 #pragma unroll
           for (int mm = 0; mm < MMT; mm++) {
-            mma3(ya[mm][2 * tp], qh[mm][kj], ql[mm][kj], xh[0], xh[1], xl[0], xl[1]);
-            if (nt0 + 1 < ly.ntt)
-              mma3(ya[mm][2 * tp + 1], qh[mm][kj], ql[mm][kj], xh[2], xh[3], xl[2], xl[3]);
+            mma16816(ya[mm][2 * tp], ql[mm][kj], xh[0], xh[1]);
+            if (two) mma16816(ya[mm][2 * tp + 1], ql[mm][kj], xh[2], xh[3]);
+          }
+#pragma unroll
+          for (int mm = 0; mm < MMT; mm++) {
+            mma16816(ya[mm][2 * tp], qh[mm][kj], xl[0], xl[1]);
+            if (two) mma16816(ya[mm][2 * tp + 1], qh[mm][kj], xl[2], xl[3]);
+          }
+#pragma unroll
+          for (int mm = 0; mm < MMT; mm++) {
+            mma16816(ya[mm][2 * tp], qh[mm][kj], xh[0], xh[1]);
+            if (two) mma16816(ya[mm][2 * tp + 1], qh[mm][kj], xh[2], xh[3]);
           }
         }
       }
@@ -506,7 +543,8 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
               const int hh = m * S + t;
               const float v0 = ya[mm][nt][2 * h] * yscale;
               const float v1 = ya[mm][nt][2 * h + 1] * yscale;
-              if (pair_store) {
+              if (pair_store) {  // hh even, H even: hh < H implies hh + 1 < H
+                if (hh >= H) continue;
                 float2 o = make_float2(v0 + bS[hh], v1 + bS[hh + 1]);
                 asm volatile("st.global.cs.v2.f32 [%0], {%1,%2};" ::"l"(yg + hh), "f"(o.x),
                              "f"(o.y)
