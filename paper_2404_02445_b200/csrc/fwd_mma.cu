@@ -1,26 +1,32 @@
 // fwd_mma.cu -- fused PRNet pattern-attention forward on the tensor cores
-// (sm_100a mma.sync, split-fp16 "3-product" arithmetic), 9 <= N <= 32, M <= 32.
+// (sm_100a mma.sync, split-fp16 "3-product" arithmetic), N <= 32, M <= 32.
 //
 // Same per-series step map and reading as fwd_warp.cu; what
 // changes is how the three contractions run:
 //   a3 Gram      G  = Z Z^T            (N x S)(S x N)
 //   a6+a7 fold   Q  = W_s A_s + W_t A_t (M x N)(N x N) x 2
 //   a7 head      Y  = Q X               (M x N)(N x S)
-// each as m16n8k16 MMAs with fp32 accumulation, every fp32 operand v split
-// into v = hi + lo (both fp16; lo = fp16(v - hi)) and the product formed as
-// hi*hi + hi*lo + lo*hi.  The dropped lo*lo term and the rounding of lo are
-// ~2^-22 relative, i.e. fp32-class accuracy (plain fp16/tf32
-// fail the 1e-5 + 1e-4|y| bar).  Operands are pre-scaled by exact powers of
-// two (per series for X and Z, per channel for W) so fp16 never overflows;
-// the scales are divided out exactly in fp32.
+// each as m16n8k16 (and m16n8k8) MMAs with fp32 accumulation, every fp32
+// operand v split into v = hi + lo (both fp16; lo = fp16(v - hi)) and the
+// product formed as hi*hi + hi*lo + lo*hi.  The dropped lo*lo term and the
+// rounding of lo are ~2^-22 relative, i.e. fp32-class accuracy (
+// plain fp16/tf32 fail the 1e-5 + 1e-4|y| bar).  Operands are pre-scaled by
+// exact powers of two (per series for X and Z, per channel for W) so fp16
+// never overflows; the scales are divided out exactly in fp32.
 //
 // Data never leaves the SM between load and store: the Gram accumulators are
-// softmax-ed in registers (FA2-style quad reductions), the attention tiles are
-// transposed in registers with movmatrix into the B operand of the fold, and
-// the fold's accumulators are re-packed in registers as the A operand of the
-// head.  Shared memory holds only the series (fp32 staging + fp16 X, Z) and
-// the channel's head (fp16 W, fp32 b).  The next series is prefetched with
-// cp.async while the current one is in the tensor cores.
+// softmax-ed in registers (FA2-style quad reductions, packed f32x2 math), the
+// attention tiles are transposed in registers with movmatrix into the B
+// operand of the fold, and the fold's accumulators are re-packed in registers
+// as the A operand of the head.  Shared memory holds only the series (fp32
+// staging + fp16 X, Z) and the channel's head (fp16 W, fp32 b).  The next
+// series is prefetched with cp.async while the current one is in the tensor
+// cores.
+//
+// Template parameters: MT / MMT = 16-row tiles of segments / future segments;
+// SC = compile-time segment length (24: every configs[0..3] shape; dense
+// operand rows, lane-per-row register conversion, k16 + k8 Gram) or 0
+// (generic runtime S with padded rows); DBG = also dump the attention rows.
 #include <cuda_fp16.h>
 
 #include <cmath>
@@ -35,14 +41,44 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-__device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
-  const __half2 h = __floats2half2_rn(a, b);
+// ---- packed FP32 (sm_100 FFMA2 / FADD2 / FMUL2)
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("{.reg .b64 a,b,c,d; mov.b64 a,{%2,%3}; mov.b64 b,{%4,%5}; mov.b64 c,{%6,%7};"
+      " fma.rn.f32x2 d,a,b,c; mov.b64 {%0,%1},d;}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 a,b,d; mov.b64 a,{%2,%3}; mov.b64 b,{%4,%5}; add.rn.f32x2 d,a,b;"
+      " mov.b64 {%0,%1},d;}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  float2 r;
+  asm("{.reg .b64 a,b,d; mov.b64 a,{%2,%3}; mov.b64 b,{%4,%5}; mul.rn.f32x2 d,a,b;"
+      " mov.b64 {%0,%1},d;}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
+// v = hi + lo with hi = fp16(v), lo = fp16(v - hi), packed as half2 pairs
+__device__ __forceinline__ void split2(float2 v, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(v.x, v.y);
   const float2 hf = __half22float2(h);
-  const __half2 l = __floats2half2_rn(a - hf.x, b - hf.y);
+  const __half2 l = __floats2half2_rn(v.x - hf.x, v.y - hf.y);
   hi = *reinterpret_cast<const uint32_t*>(&h);
   lo = *reinterpret_cast<const uint32_t*>(&l);
 }
-
+__device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  split2(make_float2(a, b), hi, lo);
+}
 __device__ __forceinline__ void split1(float a, __half& hi, __half& lo) {
   hi = __float2half_rn(a);
   lo = __float2half_rn(a - __half2float(hi));
@@ -56,14 +92,12 @@ __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], 
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
-
-// hi*hi + hi*lo + lo*hi
-__device__ __forceinline__ void mma3(float (&c)[4], const uint32_t (&ah)[4],
-                                     const uint32_t (&al)[4], uint32_t bh0, uint32_t bh1,
-                                     uint32_t bl0, uint32_t bl1) {
-  mma16816(c, al, bh0, bh1);
-  mma16816(c, ah, bl0, bl1);
-  mma16816(c, ah, bh0, bh1);
+__device__ __forceinline__ void mma1688(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(b0));
 }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
@@ -71,19 +105,21 @@ __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(smem_u32(p)));
 }
-
+__device__ __forceinline__ void ldsm_x2(uint32_t& r0, uint32_t& r1, const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
+               : "=r"(r0), "=r"(r1)
+               : "r"(smem_u32(p)));
+}
 __device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(smem_u32(p)));
 }
-
 __device__ __forceinline__ void ldsm_x2_t(uint32_t& r0, uint32_t& r1, const void* p) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];"
                : "=r"(r0), "=r"(r1)
                : "r"(smem_u32(p)));
 }
-
 __device__ __forceinline__ uint32_t movm_t(uint32_t v) {
   uint32_t r;
   asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(r) : "r"(v));
@@ -113,9 +149,7 @@ __device__ __forceinline__ float pow2_scale(float maxabs) {
 
 }  // namespace
 
-
-
-template <int MT, int MMT>
+template <int MT, int MMT, int SC, bool DBG>
 __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLayout ly,
                                                                int wins_per_cta) {
   extern __shared__ float4 smem4[];
@@ -125,7 +159,12 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
   const int gq = lane >> 2, cq = lane & 3, q8 = lane >> 3;
   const int c = blockIdx.y;
   const int cw = a.head_per_channel ? c : 0;
-  const int S = a.S, N = a.N, M = a.M, H = a.H, L = a.L, C = a.C;
+  const int S = SC > 0 ? SC : a.S;
+  const int N = a.N, M = a.M, H = a.H, L = a.L, C = a.C;
+  // operand row strides (halves): dense rows when S is the compile-time 24
+  const int sph = SC > 0 ? SC : ly.sph;
+  const int zph = SC > 0 ? SC : ly.zph;
+  const int ntt = SC > 0 ? (SC + 7) / 8 : ly.ntt;
 
   // ---------------- CTA-shared: the channel's pre-packed head (prnet_load_params):
   // W' = W * sw as fp16 hi/lo [16*MMT][wph] (cols: seasonal i at [0, NR), trend i at
@@ -183,86 +222,111 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
     cp_async_wait_all();
     __syncwarp();
 
-    // ---------------- a2 pass 1 (lane i = segment i): sums of d = x - x0 (x0 = the
-    // segment's first value, so a constant segment gives exact zeros), t~ d, max|x|, max|d|
+    // ---------------- a2: descriptors (Def 4) from d = x - x0 (x0 = the segment's first
+    // value, so a constant segment gives exact zeros); X' = x sx, Z' = z sz as fp16 hi/lo
     const int i = lane;
-    float x0 = 0.f, s1 = 0.f, s3 = 0.f, amx = 0.f, dmx = 0.f;
-    if (i < N) {
-      const float* xr = xbuf + i * S;
-      x0 = xr[0];
-      auto acc1 = [&](float v, int t) {
-        const float d = v - x0;
-        s1 += d;
-        s3 = fmaf((float)t - a.half_s, d, s3);
-        amx = fmaxf(amx, fabsf(v));
-        dmx = fmaxf(dmx, fabsf(d));
-      };
-      if ((S & 3) == 0) {
-        for (int t = 0; t < S; t += 4) {
-          const float4 v = *reinterpret_cast<const float4*>(xr + t);
-          acc1(v.x, t);
-          acc1(v.y, t + 1);
-          acc1(v.z, t + 2);
-          acc1(v.w, t + 3);
+    float x0 = 0.f, m1 = 0.f, mu = 0.f, kap = 0.f, sx, sz;
+    if constexpr (SC == 24) {
+      // lane i holds its whole segment in registers: one read, 16-byte row stores
+      float xv[24];
+      float2 s1 = f2(0.f), s3 = f2(0.f);
+      float amx = 0.f, dmx = 0.f;
+      if (i < N) {
+        const float4* xr = reinterpret_cast<const float4*>(xbuf + i * 24);
+#pragma unroll
+        for (int q = 0; q < 6; q++) {
+          const float4 v = xr[q];
+          xv[4 * q] = v.x;
+          xv[4 * q + 1] = v.y;
+          xv[4 * q + 2] = v.z;
+          xv[4 * q + 3] = v.w;
         }
-      } else {
-        for (int t = 0; t < S; t++) acc1(xr[t], t);
+        x0 = xv[0];
+#pragma unroll
+        for (int t = 0; t < 24; t += 2) {
+          const float2 d = add2(make_float2(xv[t], xv[t + 1]), f2(-x0));
+          s1 = add2(s1, d);
+          s3 = fma2(make_float2((float)t - 11.5f, (float)t - 10.5f), d, s3);
+          amx = fmaxf(amx, fmaxf(fabsf(xv[t]), fabsf(xv[t + 1])));
+          dmx = fmaxf(dmx, fmaxf(fabsf(d.x), fabsf(d.y)));
+        }
+        m1 = (s1.x + s1.y) * (1.f / 24.f);
+        mu = x0 + m1;
+        kap = (s3.x + s3.y) * a.inv_v;
       }
-    }
-    const float m1 = s1 * a.inv_s;        // mu - x0
-    const float mu = x0 + m1;             // Def 4: mu_i
-    const float kap = s3 * a.inv_v;       // Def 4: kappa_i (sum t~ z = sum t~ d)
-    const float sx = pow2_scale(warp_max(amx));
-    const float sz = pow2_scale(2.f * warp_max(dmx));  // |z| <= 2 max|d|
-    rsm[lane] = x0;        // per-row shift and mean for the coalesced pass (no shuffles in
-    rsm[32 + lane] = m1;   // its lane-divergent loop)
-    __syncwarp();
-
-    // ---------------- a2 pass 2 (coalesced over element pairs): X' = x sx, Z' = z sz as
-    // fp16 hi/lo, z = (x - x0_i) - m1_i  (Def 4)
-    if ((S & 1) == 0) {
-      // element k = 2 p walks with stride 64: (row r, col t) advance by (step_r, step_t)
-      int r = (2 * lane) / S, t = 2 * lane - r * S;
-      const int step_r = 64 / S, step_t = 64 - step_r * S;
-      for (int k = 2 * lane; k < NS; k += 64) {
-        const float2 v = *reinterpret_cast<const float2*>(xbuf + k);
-        const float xr0 = rsm[r], mr = rsm[32 + r];
-        uint32_t h, l;
-        split2(v.x * sx, v.y * sx, h, l);
-        *reinterpret_cast<uint32_t*>(x_hi + r * ly.sph + t) = h;
-        *reinterpret_cast<uint32_t*>(x_lo + r * ly.sph + t) = l;
-        split2(((v.x - xr0) - mr) * sz, ((v.y - xr0) - mr) * sz, h, l);
-        *reinterpret_cast<uint32_t*>(z_hi + r * ly.zph + t) = h;
-        *reinterpret_cast<uint32_t*>(z_lo + r * ly.zph + t) = l;
-        r += step_r;
-        t += step_t;
-        if (t >= S) {
-          t -= S;
-          r++;
+      sx = pow2_scale(warp_max(amx));
+      sz = pow2_scale(2.f * warp_max(dmx));  // |z| <= 2 max|d|
+      if (i < N) {
+        const float2 sx2 = f2(sx), sz2 = f2(sz), nx0 = f2(-x0), nm1 = f2(-m1);
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+          uint4 xh, xl, zh, zl;
+          uint32_t* pxh = reinterpret_cast<uint32_t*>(&xh);
+          uint32_t* pxl = reinterpret_cast<uint32_t*>(&xl);
+          uint32_t* pzh = reinterpret_cast<uint32_t*>(&zh);
+          uint32_t* pzl = reinterpret_cast<uint32_t*>(&zl);
+#pragma unroll
+          for (int u = 0; u < 4; u++) {
+            const int t = 8 * q + 2 * u;
+            const float2 v = make_float2(xv[t], xv[t + 1]);
+            split2(mul2(v, sx2), pxh[u], pxl[u]);
+            split2(mul2(add2(add2(v, nx0), nm1), sz2), pzh[u], pzl[u]);
+          }
+          *reinterpret_cast<uint4*>(x_hi + i * 24 + 8 * q) = xh;
+          *reinterpret_cast<uint4*>(x_lo + i * 24 + 8 * q) = xl;
+          *reinterpret_cast<uint4*>(z_hi + i * 24 + 8 * q) = zh;
+          *reinterpret_cast<uint4*>(z_lo + i * 24 + 8 * q) = zl;
         }
       }
+      __syncwarp();
     } else {
-      int r = lane / S, t = lane - r * S;
-      const int step_r = 32 / S, step_t = 32 - step_r * S;
+      // generic S: pass 1 per lane-row, pass 2 coalesced over elements
+      float s1 = 0.f, s3 = 0.f, amx = 0.f, dmx = 0.f;
+      if (i < N) {
+        const float* xr = xbuf + i * S;
+        x0 = xr[0];
+        auto acc1 = [&](float v, int t) {
+          const float d = v - x0;
+          s1 += d;
+          s3 = fmaf((float)t - a.half_s, d, s3);
+          amx = fmaxf(amx, fabsf(v));
+          dmx = fmaxf(dmx, fabsf(d));
+        };
+        if ((S & 3) == 0) {
+          for (int t = 0; t < S; t += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(xr + t);
+            acc1(v.x, t);
+            acc1(v.y, t + 1);
+            acc1(v.z, t + 2);
+            acc1(v.w, t + 3);
+          }
+        } else {
+          for (int t = 0; t < S; t++) acc1(xr[t], t);
+        }
+        m1 = s1 * a.inv_s;
+        mu = x0 + m1;
+        kap = s3 * a.inv_v;
+      }
+      sx = pow2_scale(warp_max(amx));
+      sz = pow2_scale(2.f * warp_max(dmx));
+      rsm[lane] = x0;        // per-row shift and mean for the coalesced pass (no shuffles in
+      rsm[32 + lane] = m1;   // its lane-divergent loop)
+      __syncwarp();
       for (int k = lane; k < NS; k += 32) {
+        const int r = (int)(((float)k + 0.5f) * a.inv_s);
+        const int t = k - r * S;
         const float v = xbuf[k];
         const float xr0 = rsm[r], mr = rsm[32 + r];
         __half h, l;
         split1(v * sx, h, l);
-        x_hi[r * ly.sph + t] = h;
-        x_lo[r * ly.sph + t] = l;
+        x_hi[r * sph + t] = h;
+        x_lo[r * sph + t] = l;
         split1(((v - xr0) - mr) * sz, h, l);
-        z_hi[r * ly.zph + t] = h;
-        z_lo[r * ly.zph + t] = l;
-        r += step_r;
-        t += step_t;
-        if (t >= S) {
-          t -= S;
-          r++;
-        }
+        z_hi[r * zph + t] = h;
+        z_lo[r * zph + t] = l;
       }
+      __syncwarp();
     }
-    __syncwarp();
     // xbuf is free: fetch the next series while this one is in the tensor cores
     if (b + nwarps < b_end) prefetch(b + nwarps);
 
@@ -274,21 +338,22 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
       for (int nt = 0; nt < 2 * MT; nt++)
 #pragma unroll
         for (int e = 0; e < 4; e++) g[mt][nt][e] = 0.f;
-    for (int k0 = 0; k0 < ly.kz; k0 += 16) {
+    const int k16 = SC > 0 ? (SC / 16) * 16 : ly.kz;
+    for (int k0 = 0; k0 < k16; k0 += 16) {
       uint32_t ah[MT][4], al[MT][4];
 #pragma unroll
       for (int mt = 0; mt < MT; mt++) {
-        const int off = (16 * mt + (lane & 7) + 8 * (q8 & 1)) * ly.zph + k0 + 8 * (q8 >> 1);
+        const int off = (16 * mt + (lane & 7) + 8 * (q8 & 1)) * zph + k0 + 8 * (q8 >> 1);
         ldsm_x4(ah[mt], z_hi + off);
         ldsm_x4(al[mt], z_lo + off);
       }
 #pragma unroll
       for (int np = 0; np < MT; np++) {
         uint32_t bh[4], bl[4];
-        const int off = (16 * np + (lane & 7) + 8 * (q8 >> 1)) * ly.zph + k0 + 8 * (q8 & 1);
+        const int off = (16 * np + (lane & 7) + 8 * (q8 >> 1)) * zph + k0 + 8 * (q8 & 1);
         ldsm_x4(bh, z_hi + off);
         ldsm_x4(bl, z_lo + off);
-        // product-major order: independent accumulators back to back (no MMA-latency chains)
+        // product-major order: independent accumulators back to back
 #pragma unroll
         for (int mt = 0; mt < MT; mt++) {
           mma16816(g[mt][2 * np], al[mt], bh[0], bh[1]);
@@ -303,6 +368,39 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
         for (int mt = 0; mt < MT; mt++) {
           mma16816(g[mt][2 * np], ah[mt], bh[0], bh[1]);
           mma16816(g[mt][2 * np + 1], ah[mt], bh[2], bh[3]);
+        }
+      }
+    }
+    if constexpr (SC > 0 && (SC % 16) == 8) {
+      // K tail of 8 (S = 24: columns 16..23) with m16n8k8
+      constexpr int k0 = (SC / 16) * 16;
+      uint32_t ah[MT][2], al[MT][2];
+#pragma unroll
+      for (int mt = 0; mt < MT; mt++) {
+        const int off = (16 * mt + (lane & 7) + 8 * (q8 & 1)) * zph + k0;
+        ldsm_x2(ah[mt][0], ah[mt][1], z_hi + off);
+        ldsm_x2(al[mt][0], al[mt][1], z_lo + off);
+      }
+#pragma unroll
+      for (int np = 0; np < MT; np++) {
+        uint32_t bh[2], bl[2];  // b0 of n-tiles 2np, 2np+1 (rows j of Z', k = 16..23)
+        const int off = (16 * np + 8 * (q8 & 1) + (lane & 7)) * zph + k0;
+        ldsm_x2(bh[0], bh[1], z_hi + off);
+        ldsm_x2(bl[0], bl[1], z_lo + off);
+#pragma unroll
+        for (int mt = 0; mt < MT; mt++) {
+          mma1688(g[mt][2 * np], al[mt][0], al[mt][1], bh[0]);
+          mma1688(g[mt][2 * np + 1], al[mt][0], al[mt][1], bh[1]);
+        }
+#pragma unroll
+        for (int mt = 0; mt < MT; mt++) {
+          mma1688(g[mt][2 * np], ah[mt][0], ah[mt][1], bl[0]);
+          mma1688(g[mt][2 * np + 1], ah[mt][0], ah[mt][1], bl[1]);
+        }
+#pragma unroll
+        for (int mt = 0; mt < MT; mt++) {
+          mma1688(g[mt][2 * np], ah[mt][0], ah[mt][1], bh[0]);
+          mma1688(g[mt][2 * np + 1], ah[mt][0], ah[mt][1], bh[1]);
         }
       }
     }
@@ -328,19 +426,17 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
     const float cm = sqrtf(inv_var * a.kt), ck = sqrtf(a.vtrend * inv_var * a.kt);
     const float mus = i < N ? mu * cm : 0.f, kas = i < N ? kap * ck : 0.f;
 
-    // per-column quantities (j = 8 nt + 2 cq + e), masked past N
-    float cinv[2 * MT][2], cmask[2 * MT][2], cmu[2 * MT][2], ckap[2 * MT][2];
+    // per-column quantities (j = 8 nt + 2 cq + e) as pairs, masked past N
+    float2 cinv[2 * MT], cmask[2 * MT], cmu[2 * MT], ckap[2 * MT];
 #pragma unroll
-    for (int nt = 0; nt < 2 * MT; nt++)
-#pragma unroll
-      for (int e = 0; e < 2; e++) {
-        const int j = 8 * nt + 2 * cq + e;
-        cinv[nt][e] = __shfl_sync(0xffffffffu, inv, j);
-        cmask[nt][e] = j < N ? 0.f : -INFINITY;
-        const float mj = __shfl_sync(0xffffffffu, mus, j);
-        cmu[nt][e] = j < N ? mj : INFINITY;
-        ckap[nt][e] = __shfl_sync(0xffffffffu, kas, j);
-      }
+    for (int nt = 0; nt < 2 * MT; nt++) {
+      const int j = 8 * nt + 2 * cq;
+      cinv[nt] = make_float2(__shfl_sync(0xffffffffu, inv, j), __shfl_sync(0xffffffffu, inv, j + 1));
+      cmask[nt] = make_float2(j < N ? 0.f : -INFINITY, j + 1 < N ? 0.f : -INFINITY);
+      const float m0 = __shfl_sync(0xffffffffu, mus, j), m1v = __shfl_sync(0xffffffffu, mus, j + 1);
+      cmu[nt] = make_float2(j < N ? -m0 : -INFINITY, j + 1 < N ? -m1v : -INFINITY);
+      ckap[nt] = make_float2(-__shfl_sync(0xffffffffu, kas, j), -__shfl_sync(0xffffffffu, kas, j + 1));
+    }
 
     // ---------------- a5 seasonal softmax on the fragments, pack, transpose (movmatrix)
     uint32_t bsh[MT][2 * MT][2], bsl[MT][2 * MT][2];  // B operand of the fold: [k-tile][n-tile][b0/b1]
@@ -350,41 +446,40 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
       for (int h = 0; h < 2; h++) {
         const int ii = 16 * mt + 8 * h + gq;
         const float rk = __shfl_sync(0xffffffffu, inv, ii) * a.ks;
+        float2 u[2 * MT];
         float mx = -INFINITY;
 #pragma unroll
-        for (int nt = 0; nt < 2 * MT; nt++)
-#pragma unroll
-          for (int e = 0; e < 2; e++) {
-            const float u = fmaf(g[mt][nt][2 * h + e], cinv[nt][e], cmask[nt][e]);
-            g[mt][nt][2 * h + e] = u;
-            mx = fmaxf(mx, u);
-          }
+        for (int nt = 0; nt < 2 * MT; nt++) {
+          u[nt] = fma2(make_float2(g[mt][nt][2 * h], g[mt][nt][2 * h + 1]), cinv[nt], cmask[nt]);
+          mx = fmaxf(mx, fmaxf(u[nt].x, u[nt].y));
+        }
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        const float nb = -mx * rk;
-        float sum = 0.f;
-#pragma unroll
-        for (int nt = 0; nt < 2 * MT; nt++)
-#pragma unroll
-          for (int e = 0; e < 2; e++) {
-            const float p = fast_ex2(fmaf(g[mt][nt][2 * h + e], rk, nb));
-            g[mt][nt][2 * h + e] = p;
-            sum += p;
-          }
-        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-        const float rs = ii < N ? 1.f / sum : 0.f;
+        const float2 rk2 = f2(rk), nb2 = f2(-mx * rk);
+        float2 sum2 = f2(0.f);
 #pragma unroll
         for (int nt = 0; nt < 2 * MT; nt++) {
-          const float p0 = g[mt][nt][2 * h] * rs, p1 = g[mt][nt][2 * h + 1] * rs;
-          if (a.a_s_dbg != nullptr && ii < N) {
-            const int j = 8 * nt + 2 * cq;
-            float* d = a.a_s_dbg + (series * N + ii) * N + j;
-            if (j < N) d[0] = p0;
-            if (j + 1 < N) d[1] = p1;
+          const float2 arg = fma2(u[nt], rk2, nb2);
+          u[nt] = make_float2(fast_ex2(arg.x), fast_ex2(arg.y));
+          sum2 = add2(sum2, u[nt]);
+        }
+        float sum = sum2.x + sum2.y;
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        const float2 rs2 = f2(ii < N ? 1.f / sum : 0.f);
+#pragma unroll
+        for (int nt = 0; nt < 2 * MT; nt++) {
+          const float2 p = mul2(u[nt], rs2);
+          if constexpr (DBG) {
+            if (ii < N) {
+              const int j = 8 * nt + 2 * cq;
+              float* d = a.a_s_dbg + (series * N + ii) * N + j;
+              if (j < N) d[0] = p.x;
+              if (j + 1 < N) d[1] = p.y;
+            }
           }
           uint32_t hi, lo;
-          split2(p0, p1, hi, lo);
+          split2(p, hi, lo);
           bsh[mt][nt][h] = movm_t(hi);
           bsl[mt][nt][h] = movm_t(lo);
         }
@@ -421,32 +516,34 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
 #pragma unroll
       for (int h = 0; h < 2; h++) {
         const int ii = 16 * mt + 8 * h + gq;
-        const float mui = __shfl_sync(0xffffffffu, mus, ii);
-        const float ki = __shfl_sync(0xffffffffu, kas, ii);
-        float sum = 0.f;
-#pragma unroll
-        for (int nt = 0; nt < 2 * MT; nt++)
-#pragma unroll
-          for (int e = 0; e < 2; e++) {
-            const float dm = mui - cmu[nt][e], dk = ki - ckap[nt][e];
-            const float p = fast_ex2(fmaf(-dk, dk, -dm * dm));
-            g[mt][nt][2 * h + e] = p;
-            sum += p;
-          }
-        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-        const float rs = ii < N ? 1.f / sum : 0.f;
+        const float2 mui = f2(__shfl_sync(0xffffffffu, mus, ii));
+        const float2 ki = f2(__shfl_sync(0xffffffffu, kas, ii));
+        float2 u[2 * MT];
+        float2 sum2 = f2(0.f);
 #pragma unroll
         for (int nt = 0; nt < 2 * MT; nt++) {
-          const float p0 = g[mt][nt][2 * h] * rs, p1 = g[mt][nt][2 * h + 1] * rs;
-          if (a.a_t_dbg != nullptr && ii < N) {
-            const int j = 8 * nt + 2 * cq;
-            float* d = a.a_t_dbg + (series * N + ii) * N + j;
-            if (j < N) d[0] = p0;
-            if (j + 1 < N) d[1] = p1;
+          const float2 dm = add2(mui, cmu[nt]), dk = add2(ki, ckap[nt]);
+          const float2 e = fma2(make_float2(-dk.x, -dk.y), dk, mul2(make_float2(-dm.x, -dm.y), dm));
+          u[nt] = make_float2(fast_ex2(e.x), fast_ex2(e.y));
+          sum2 = add2(sum2, u[nt]);
+        }
+        float sum = sum2.x + sum2.y;
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        const float2 rs2 = f2(ii < N ? 1.f / sum : 0.f);
+#pragma unroll
+        for (int nt = 0; nt < 2 * MT; nt++) {
+          const float2 p = mul2(u[nt], rs2);
+          if constexpr (DBG) {
+            if (ii < N) {
+              const int j = 8 * nt + 2 * cq;
+              float* d = a.a_t_dbg + (series * N + ii) * N + j;
+              if (j < N) d[0] = p.x;
+              if (j + 1 < N) d[1] = p.y;
+            }
           }
           uint32_t hi, lo;
-          split2(p0, p1, hi, lo);
+          split2(p, hi, lo);
           bsh[mt][nt][h] = movm_t(hi);
           bsl[mt][nt][h] = movm_t(lo);
         }
@@ -484,10 +581,10 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
       }
 
     // ---------------- a7 head Y' = Q' X' (= sw sx Y), t in chunks of 4 tiles; a8 store
-    const float yscale = inv_sw / sx;
+    const float2 ys2 = f2(inv_sw / sx);
     const bool pair_store = ((S | H) & 1) == 0;   // t, hh even -> 8-byte aligned pairs
     float* yg = a.y + series * H;
-    for (int t0 = 0; t0 < ly.ntt; t0 += 4) {
+    for (int t0 = 0; t0 < ntt; t0 += 4) {
       float ya[MMT][4][4];
 #pragma unroll
       for (int mm = 0; mm < MMT; mm++)
@@ -500,20 +597,20 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
 #pragma unroll
         for (int tp = 0; tp < 2; tp++) {
           const int nt0 = t0 + 2 * tp;
-          if (nt0 >= ly.ntt) break;
+          if (nt0 >= ntt) break;
           uint32_t xh[4], xl[4];
           const int krow = 16 * kj + (lane & 7) + 8 * (q8 & 1);
-          if (nt0 + 1 < ly.ntt) {
-            const int off = krow * ly.sph + 8 * (nt0 + (q8 >> 1));
+          const bool two = nt0 + 1 < ntt;
+          if (two) {
+            const int off = krow * sph + 8 * (nt0 + (q8 >> 1));
             ldsm_x4_t(xh, x_hi + off);
             ldsm_x4_t(xl, x_lo + off);
           } else {
-            const int off = krow * ly.sph + 8 * nt0;
+            const int off = krow * sph + 8 * nt0;
             ldsm_x2_t(xh[0], xh[1], x_hi + off);
             ldsm_x2_t(xl[0], xl[1], x_lo + off);
             xh[2] = xh[3] = xl[2] = xl[3] = 0u;
           }
-          const bool two = nt0 + 1 < ly.ntt;
 #pragma unroll
           for (int mm = 0; mm < MMT; mm++) {
             mma16816(ya[mm][2 * tp], ql[mm][kj], xh[0], xh[1]);
@@ -541,17 +638,16 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
             const int m = 16 * mm + 8 * h + gq;
             if (m < M && t < S) {
               const int hh = m * S + t;
-              const float v0 = ya[mm][nt][2 * h] * yscale;
-              const float v1 = ya[mm][nt][2 * h + 1] * yscale;
+              const float2 v = mul2(make_float2(ya[mm][nt][2 * h], ya[mm][nt][2 * h + 1]), ys2);
               if (pair_store) {  // hh even, H even: hh < H implies hh + 1 < H
                 if (hh >= H) continue;
-                float2 o = make_float2(v0 + bS[hh], v1 + bS[hh + 1]);
+                const float2 o = add2(v, *reinterpret_cast<const float2*>(bS + hh));
                 asm volatile("st.global.cs.v2.f32 [%0], {%1,%2};" ::"l"(yg + hh), "f"(o.x),
                              "f"(o.y)
                              : "memory");
               } else {
-                if (hh < H) yg[hh] = v0 + bS[hh];
-                if (t + 1 < S && hh + 1 < H) yg[hh + 1] = v1 + bS[hh + 1];
+                if (hh < H) yg[hh] = v.x + bS[hh];
+                if (t + 1 < S && hh + 1 < H) yg[hh + 1] = v.y + bS[hh + 1];
               }
             }
           }
@@ -612,21 +708,31 @@ bool plan_mma_kernel(const FwdArgs& a, int max_smem_optin, MmaPlan* p) {
   MmaLayout& ly = p->ly;
   p->mt = a.N <= 16 ? 1 : 2;
   p->mmt = a.M <= 16 ? 1 : 2;
+  p->sc = a.S == 24 ? 24 : 0;
   ly.nr = 16 * p->mt;
-  ly.sph = odd8(a.S);
-  ly.kz = (a.S + 15) & ~15;
-  ly.zph = odd8(ly.kz);
+  if (p->sc == 24) {  // dense rows of 24 halves (48 B: 16-byte aligned, conflict-free ldmatrix)
+    ly.sph = 24;
+    ly.kz = 24;
+    ly.zph = 24;
+  } else {
+    ly.sph = odd8(a.S);
+    ly.kz = (a.S + 15) & ~15;
+    ly.zph = odd8(ly.kz);
+  }
   ly.wph = 2 * ly.nr + 8;
   ly.ntt = (a.S + 7) / 8;
   ly.xbuf_f = (a.N * a.S + 3) & ~3;
   int off = ly.xbuf_f * 4;
+  off = (off + 15) & ~15;
   ly.off_xhi = off;
   off += ly.nr * ly.sph * 2;
+  off = (off + 15) & ~15;
   ly.off_xlo = off;
   off += ly.nr * ly.sph * 2;
   off = (off + 15) & ~15;
   ly.off_zhi = off;
   off += ly.nr * ly.zph * 2;
+  off = (off + 15) & ~15;
   ly.off_zlo = off;
   off += ly.nr * ly.zph * 2;
   off = (off + 15) & ~15;
@@ -654,9 +760,9 @@ bool plan_mma_kernel(const FwdArgs& a, int max_smem_optin, MmaPlan* p) {
   return true;
 }
 
-template <int MT, int MMT>
+template <int MT, int MMT, int SC, bool DBG>
 static cudaError_t launch_t(const FwdArgs& a, const MmaPlan& p, cudaStream_t st) {
-  auto k = prnet_fwd_mma_kernel<MT, MMT>;
+  auto k = prnet_fwd_mma_kernel<MT, MMT, SC, DBG>;
   cudaError_t e =
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
@@ -665,9 +771,17 @@ static cudaError_t launch_t(const FwdArgs& a, const MmaPlan& p, cudaStream_t st)
   return cudaGetLastError();
 }
 
+template <int SC, bool DBG>
+static cudaError_t launch_sc(const FwdArgs& a, const MmaPlan& p, cudaStream_t st) {
+  if (p.mt == 1)
+    return p.mmt == 1 ? launch_t<1, 1, SC, DBG>(a, p, st) : launch_t<1, 2, SC, DBG>(a, p, st);
+  return p.mmt == 1 ? launch_t<2, 1, SC, DBG>(a, p, st) : launch_t<2, 2, SC, DBG>(a, p, st);
+}
+
 cudaError_t launch_mma_kernel(const FwdArgs& a, const MmaPlan& p, cudaStream_t st) {
-  if (p.mt == 1) return p.mmt == 1 ? launch_t<1, 1>(a, p, st) : launch_t<1, 2>(a, p, st);
-  return p.mmt == 1 ? launch_t<2, 1>(a, p, st) : launch_t<2, 2>(a, p, st);
+  const bool dbg = a.a_s_dbg != nullptr;
+  if (p.sc == 24) return dbg ? launch_sc<24, true>(a, p, st) : launch_sc<24, false>(a, p, st);
+  return dbg ? launch_sc<0, true>(a, p, st) : launch_sc<0, false>(a, p, st);
 }
 
 }  // namespace prnet
