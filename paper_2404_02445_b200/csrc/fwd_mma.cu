@@ -69,10 +69,12 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
 // v = hi + lo with hi = fp16(v), lo = fp16(v - hi), packed as half2 pairs
+__device__ __forceinline__ float2 add2(float2 a, float2 b);
 __device__ __forceinline__ void split2(float2 v, uint32_t& hi, uint32_t& lo) {
   const __half2 h = __floats2half2_rn(v.x, v.y);
   const float2 hf = __half22float2(h);
-  const __half2 l = __floats2half2_rn(v.x - hf.x, v.y - hf.y);
+  const float2 d = add2(v, make_float2(-hf.x, -hf.y));
+  const __half2 l = __floats2half2_rn(d.x, d.y);
   hi = *reinterpret_cast<const uint32_t*>(&h);
   lo = *reinterpret_cast<const uint32_t*>(&l);
 }
@@ -139,6 +141,31 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
+// ---- 1-D TMA bulk copy global -> shared with mbarrier completion (UBLKCP)
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // 2^-e with max|v| * 2^-e in [0.5, 1): exact power-of-two scale (1 for v == 0).
 __device__ __forceinline__ float pow2_scale(float maxabs) {
   if (!(maxabs > 0.f) || !isfinite(maxabs)) return 1.f;
@@ -190,6 +217,9 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
   __half* z_lo = reinterpret_cast<__half*>(wb + ly.off_zlo);
   float* dsm = reinterpret_cast<float*>(wb + ly.off_diag);   // [32] Gram diagonal
   float* rsm = dsm + 32;                                      // [64] x0, m1 per row
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(dsm + 96);     // TMA completion barrier
+  if (lane == 0) mbar_init(xbar, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   {
     // zero the fp16 operand tiles once: padding rows (>= N) and columns (>= S) stay 0
     uint32_t* p = reinterpret_cast<uint32_t*>(wb + ly.off_xhi);
@@ -200,12 +230,19 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
 
   const bool vec_x = ((L & 3) == 0) && ((a.r & 3) == 0);
   const int NS = N * S;
+  // one bulk TMA per series when its segmented span is 16-byte aligned and sized
+  const bool bulk = vec_x && ((NS & 3) == 0);
+  uint32_t xphase = 0;
   const int64_t b_begin = (int64_t)blockIdx.x * wins_per_cta;
   int64_t b_end = b_begin + wins_per_cta;
   if (b_end > a.B) b_end = a.B;
 
   auto prefetch = [&](int64_t b) {
     const float* xg = a.x + (b * C + c) * L + a.r;
+    if (bulk) {
+      if (lane == 0) bulk_load(xbuf, xg, (uint32_t)NS * 4u, xbar);
+      return;
+    }
     if (vec_x) {
       for (int k = lane; k < (NS >> 2); k += 32) cp_async16(xbuf + 4 * k, xg + 4 * k);
       for (int k = (NS & ~3) + lane; k < NS; k += 32) cp_async4(xbuf + k, xg + k);
@@ -219,7 +256,12 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
   if (b < b_end) prefetch(b);
   for (; b < b_end; b += nwarps) {
     const int64_t series = b * C + c;
-    cp_async_wait_all();
+    if (bulk) {
+      mbar_wait(xbar, xphase);
+      xphase ^= 1u;
+    } else {
+      cp_async_wait_all();
+    }
     __syncwarp();
 
     // ---------------- a2: descriptors (Def 4) from d = x - x0 (x0 = the segment's first
@@ -737,7 +779,7 @@ bool plan_mma_kernel(const FwdArgs& a, int max_smem_optin, MmaPlan* p) {
   off += ly.nr * ly.zph * 2;
   off = (off + 15) & ~15;
   ly.off_diag = off;
-  off += 96 * 4;
+  off += 96 * 4 + 16;   // diag[32], x0/m1[64], TMA mbarrier
   ly.per_warp_bytes = (off + 127) & ~127;
   const int wrows = 16 * p->mmt;
   int so = 0;
