@@ -103,47 +103,75 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU oracle leg
+_ORACLE_CACHE = {}
+
+
 def _oracle_chunk(args):
+    """Worker: oracle.forward (as it stands, 1 thread) on whole windows of a channel block."""
     name, seed, widx, chans = args
     import oracle
-    w = synth.WORKLOADS[name]
-    N, _, M = synth.derived_dims(w.L, w.S, w.H)
-    s = synth.make_series(w, seed, channels=chans)
-    x, _ = synth.window_batch(s, w, widx)
-    ws, wt, b = synth.make_params(w.C, M, N, w.H, True, seed, w.cfg_id)
+    key = (name, seed, tuple(widx), tuple(chans))
+    if key not in _ORACLE_CACHE:
+        w = synth.WORKLOADS[name]
+        N, _, M = synth.derived_dims(w.L, w.S, w.H)
+        s = synth.make_series(w, seed, channels=chans)
+        x, _ = synth.window_batch(s, w, widx)
+        ws, wt, b = synth.make_params(w.C, M, N, w.H, True, seed, w.cfg_id)
+        _ORACLE_CACHE.clear()
+        _ORACLE_CACHE[key] = (x, ws[chans], wt[chans], b[chans], w.S, w.H)
+    x, ws, wt, b, S, H = _ORACLE_CACHE[key]
     t0 = time.perf_counter()
-    oracle.forward(x, w.S, w.H, ws[chans], wt[chans], b[chans], True)
-    return time.perf_counter() - t0, len(widx) * len(chans)
+    oracle.forward(x, S, H, ws, wt, b, True)
+    return time.perf_counter() - t0, x.shape[0] * x.shape[1]
+
+
+class CpuOracleBench:
+    """The oracle timed on the host cores on a bounded, fixed sample of the workload:
+    whole windows (all channels) spread evenly over the test set, split by channel
+    blocks over one single-threaded process per core.  step() returns windows/s."""
+
+    def __init__(self, name, seed, budget_s=3.0, cores=None):
+        import multiprocessing as mp
+        import oracle
+        oracle.build()
+        self.w = w = synth.WORKLOADS[name]
+        self.cores = cores or len(os.sched_getaffinity(0))
+        dt, n = _oracle_chunk((name, seed, [0], list(range(min(w.C, 8)))))
+        per_series = dt / n
+        n_series = max(w.C, int(budget_s * self.cores / per_series))
+        n_win = max(1, min(w.windows, n_series // w.C))
+        self.widx = np.unique(np.linspace(0, w.windows - 1, n_win).astype(int)).tolist()
+        blocks = [b.tolist() for b in np.array_split(np.arange(w.C), min(self.cores, w.C)) if len(b)]
+        self.jobs = [(name, seed, self.widx, blk) for blk in blocks]
+        self.pool = mp.get_context("fork").Pool(len(self.jobs))
+        self.pool.map(_oracle_chunk, self.jobs)          # build the inputs in the workers
+
+    def step(self):
+        t0 = time.perf_counter()
+        res = self.pool.map(_oracle_chunk, self.jobs)
+        self.wall = time.perf_counter() - t0
+        self.compute = max(r[0] for r in res)
+        self.series = sum(r[1] for r in res)
+        return self.series / self.compute / self.w.C
+
+    def describe(self):
+        w = self.w
+        return (f"{len(self.widx)} of {w.windows} windows x {w.C} channels ({self.series} series) "
+                f"per step, {len(self.jobs)} processes x 1 thread, {self.compute:.2f} s compute "
+                f"(wall {self.wall:.2f} s)")
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
 
 
 def cpu_oracle_rate(name, seed, budget_s=12.0, cores=None):
-    """Time the oracle on a bounded sample: whole windows (all channels) spread over
-    the test set, split by channel blocks over `cores` processes.  Returns
-    (windows/s, series/s, cores, sample description)."""
-    import multiprocessing as mp
-    import oracle
-    oracle.build()
-    w = synth.WORKLOADS[name]
-    N, _, M = synth.derived_dims(w.L, w.S, w.H)
-    cores = cores or len(os.sched_getaffinity(0))
-    # calibrate on one window's first few channels
-    dt, n = _oracle_chunk((name, seed, [0], list(range(min(w.C, 8)))))
-    per_series = dt / n
-    n_series = max(w.C, int(budget_s * cores / per_series))
-    n_win = max(1, min(w.windows, n_series // w.C))
-    widx = np.unique(np.linspace(0, w.windows - 1, n_win).astype(int)).tolist()
-    blocks = np.array_split(np.arange(w.C), min(cores, w.C))
-    jobs = [(name, seed, widx, blk.tolist()) for blk in blocks if len(blk)]
-    t0 = time.perf_counter()
-    with mp.get_context("fork").Pool(len(jobs)) as pool:
-        res = pool.map(_oracle_chunk, jobs)
-    wall = time.perf_counter() - t0
-    series = sum(r[1] for r in res)
-    compute = max(r[0] for r in res)
-    rate_series = series / compute
-    return (rate_series / w.C, rate_series, len(jobs),
-            f"{len(widx)} of {w.windows} windows x {w.C} channels ({series} series), "
-            f"{len(jobs)} processes x 1 thread, {compute:.1f} s (wall {wall:.1f} s)")
+    """One timed pass of the oracle over a ~budget_s sample: (windows/s, series/s, cores, sample)."""
+    b = CpuOracleBench(name, seed, budget_s, cores)
+    wps = b.step()
+    desc = b.describe()
+    b.close()
+    return wps, wps * b.w.C, len(b.jobs), desc
 
 
 # ------------------------------------------------------------------ distributed helpers
@@ -181,13 +209,16 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        times = []
-        for _ in range(args.warmup + args.steps):
-            wps, sps, cores, sample = cpu_oracle_rate(w.name, args.seed,
-                                                      budget_s=max(1.0, args.cpu_budget / 4))
-            times.append(1.0 / wps)
-        t = times[args.warmup:]
-        value = 1.0 / statistics.mean(t)
+        # each step: one oracle pass over a fixed sample sized so the whole run takes minutes
+        per_step = max(0.3, min(3.0, 150.0 / max(1, args.steps + args.warmup)))
+        ob = CpuOracleBench(w.name, args.seed, budget_s=per_step)
+        for _ in range(args.warmup):
+            ob.step()
+        rates = [ob.step() for _ in range(args.steps)]
+        value = len(rates) / sum(1.0 / r for r in rates)      # windows / total time
+        sample = ob.describe()
+        cores = len(ob.jobs)
+        ob.close()
         print(json.dumps({
             "impl": "reference", "metric": METRIC, "value": value, "unit": "windows/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,

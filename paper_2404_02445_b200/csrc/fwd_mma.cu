@@ -176,12 +176,43 @@ __device__ __forceinline__ float pow2_scale(float maxabs) {
 
 }  // namespace
 
+// Shared-memory layout, identical on host (plan) and device (compile-time for SC = 24):
+// [W' hi | W' lo]  [per-warp regions x nwarps]  [bias fp32 [H]]
+// per-warp: xbuf fp32 [nr*S] | X' hi, lo [nr][sph] | Z' hi, lo [nr][zph] | misc (diag[32],
+// x0/m1[64], mbarrier)
+struct MmaOffsets {
+  int xhi, xlo, zhi, zlo, misc, pw;   // per-warp
+  int wlo, wpack;                     // CTA-shared head
+};
+__host__ __device__ constexpr int r16(int v) { return (v + 15) & ~15; }
+__host__ __device__ constexpr MmaOffsets mma_offsets(int nr, int S, int sph, int zph, int mmt) {
+  MmaOffsets o{};
+  int off = r16(nr * S * 4);
+  o.xhi = off;
+  off = r16(off + nr * sph * 2);
+  o.xlo = off;
+  off = r16(off + nr * sph * 2);
+  o.zhi = off;
+  off = r16(off + nr * zph * 2);
+  o.zlo = off;
+  off = r16(off + nr * zph * 2);
+  o.misc = off;
+  off += 96 * 4 + 16;
+  o.pw = (off + 127) & ~127;
+  const int wph = 2 * nr + 8, rows = 16 * mmt;
+  o.wlo = rows * wph * 2;
+  o.wpack = r16(2 * rows * wph * 2);
+  return o;
+}
+
 template <int MT, int MMT, int SC, bool DBG>
 __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLayout ly,
                                                                int wins_per_cta) {
   extern __shared__ float4 smem4[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(smem4);
   constexpr int NR = 16 * MT;
+  constexpr int WPH = 2 * NR + 8;
+  constexpr MmaOffsets KO = mma_offsets(NR, SC > 0 ? SC : 8, SC > 0 ? SC : 8, SC > 0 ? SC : 8, MMT);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int gq = lane >> 2, cq = lane & 3, q8 = lane >> 3;
   const int c = blockIdx.y;
@@ -192,38 +223,40 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
   const int sph = SC > 0 ? SC : ly.sph;
   const int zph = SC > 0 ? SC : ly.zph;
   const int ntt = SC > 0 ? (SC + 7) / 8 : ly.ntt;
+  const int pw = SC > 0 ? KO.pw : ly.per_warp_bytes;
 
   // ---------------- CTA-shared: the channel's pre-packed head (prnet_load_params):
-  // W' = W * sw as fp16 hi/lo [16*MMT][wph] (cols: seasonal i at [0, NR), trend i at
+  // W' = W * sw as fp16 hi/lo [16*MMT][WPH] (cols: seasonal i at [0, NR), trend i at
   // [NR, 2NR), zeros elsewhere), 1/sw, and the fp32 bias.
-  __half* w_hi = reinterpret_cast<__half*>(smem);
-  __half* w_lo = reinterpret_cast<__half*>(smem + ly.off_wlo);
-  float* bS = reinterpret_cast<float*>(smem + ly.off_bias);
+  const __half* w_hi = reinterpret_cast<const __half*>(smem);
+  const __half* w_lo = reinterpret_cast<const __half*>(smem + KO.wlo);
+  float* bS = reinterpret_cast<float*>(smem + KO.wpack + nwarps * pw);
   const float inv_sw = a.wpack_inv_sw[cw];
   {
-    const uint4* src = a.wpack + (int64_t)cw * (ly.wpack_bytes / 16);
+    const uint4* src = a.wpack + (int64_t)cw * (KO.wpack / 16);
     uint4* dst = reinterpret_cast<uint4*>(smem);
-    for (int k = threadIdx.x; k < ly.wpack_bytes / 16; k += blockDim.x) dst[k] = __ldg(src + k);
+    for (int k = threadIdx.x; k < KO.wpack / 16; k += blockDim.x) dst[k] = __ldg(src + k);
     const float* gb = a.bias + (int64_t)cw * H;
     for (int k = threadIdx.x; k < H; k += blockDim.x) bS[k] = __ldg(gb + k);
   }
 
   // ---------------- per-warp: fp32 staging, X' hi/lo [NR][sph], Z' hi/lo [NR][zph]
-  unsigned char* wb = smem + ly.shared_bytes + warp * ly.per_warp_bytes;
+  unsigned char* wb = smem + KO.wpack + warp * pw;
   float* xbuf = reinterpret_cast<float*>(wb);
-  __half* x_hi = reinterpret_cast<__half*>(wb + ly.off_xhi);
-  __half* x_lo = reinterpret_cast<__half*>(wb + ly.off_xlo);
-  __half* z_hi = reinterpret_cast<__half*>(wb + ly.off_zhi);
-  __half* z_lo = reinterpret_cast<__half*>(wb + ly.off_zlo);
-  float* dsm = reinterpret_cast<float*>(wb + ly.off_diag);   // [32] Gram diagonal
+  __half* x_hi = reinterpret_cast<__half*>(wb + (SC > 0 ? KO.xhi : ly.off_xhi));
+  __half* x_lo = reinterpret_cast<__half*>(wb + (SC > 0 ? KO.xlo : ly.off_xlo));
+  __half* z_hi = reinterpret_cast<__half*>(wb + (SC > 0 ? KO.zhi : ly.off_zhi));
+  __half* z_lo = reinterpret_cast<__half*>(wb + (SC > 0 ? KO.zlo : ly.off_zlo));
+  float* dsm = reinterpret_cast<float*>(wb + (SC > 0 ? KO.misc : ly.off_diag));  // [32] diag
   float* rsm = dsm + 32;                                      // [64] x0, m1 per row
   uint64_t* xbar = reinterpret_cast<uint64_t*>(dsm + 96);     // TMA completion barrier
   if (lane == 0) mbar_init(xbar, 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   {
     // zero the fp16 operand tiles once: padding rows (>= N) and columns (>= S) stay 0
-    uint32_t* p = reinterpret_cast<uint32_t*>(wb + ly.off_xhi);
-    const int words = (ly.off_diag - ly.off_xhi) / 4;
+    uint32_t* p = reinterpret_cast<uint32_t*>(x_hi);
+    const int words = (int)(reinterpret_cast<unsigned char*>(dsm) -
+                            reinterpret_cast<unsigned char*>(x_hi)) / 4;
     for (int k = lane; k < words; k += 32) p[k] = 0u;
   }
   __syncthreads();
@@ -252,6 +285,24 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
     cp_async_commit();
   };
 
+  // fold helper: Q' += W'[:, col0 + 16 kt ...] * B  for one k-tile (B = attention tile kt)
+  auto fold_tile = [&](float (&qa)[MMT][2 * MT][4], int col0, int kt,
+                       const uint32_t (&bh)[2 * MT][2], const uint32_t (&bl)[2 * MT][2]) {
+#pragma unroll
+    for (int mm = 0; mm < MMT; mm++) {
+      uint32_t wh[4], wl[4];
+      const int off = (16 * mm + (lane & 7) + 8 * (q8 & 1)) * WPH + col0 + 16 * kt + 8 * (q8 >> 1);
+      ldsm_x4(wh, w_hi + off);
+      ldsm_x4(wl, w_lo + off);
+#pragma unroll
+      for (int nt = 0; nt < 2 * MT; nt++) mma16816(qa[mm][nt], wl, bh[nt][0], bh[nt][1]);
+#pragma unroll
+      for (int nt = 0; nt < 2 * MT; nt++) mma16816(qa[mm][nt], wh, bl[nt][0], bl[nt][1]);
+#pragma unroll
+      for (int nt = 0; nt < 2 * MT; nt++) mma16816(qa[mm][nt], wh, bh[nt][0], bh[nt][1]);
+    }
+  };
+
   int64_t b = b_begin + warp;
   if (b < b_end) prefetch(b);
   for (; b < b_end; b += nwarps) {
@@ -264,10 +315,10 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
     }
     __syncwarp();
 
-    // ---------------- a2: descriptors (Def 4) from d = x - x0 (x0 = the segment's first
+    // ---------------- a2: descriptors (Def 4-5) from d = x - x0 (x0 = the segment's first
     // value, so a constant segment gives exact zeros); X' = x sx, Z' = z sz as fp16 hi/lo
     const int i = lane;
-    float x0 = 0.f, m1 = 0.f, mu = 0.f, kap = 0.f, sx, sz;
+    float x0 = 0.f, m1 = 0.f, mu = 0.f, kap = 0.f, nu2 = 0.f, sx, sz;
     if constexpr (SC == 24) {
       // lane i holds its whole segment in registers: one read, 16-byte row stores
       float xv[24];
@@ -300,6 +351,7 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
       sz = pow2_scale(2.f * warp_max(dmx));  // |z| <= 2 max|d|
       if (i < N) {
         const float2 sx2 = f2(sx), sz2 = f2(sz), nx0 = f2(-x0), nm1 = f2(-m1);
+        float2 q2 = f2(0.f);
 #pragma unroll
         for (int q = 0; q < 3; q++) {
           uint4 xh, xl, zh, zl;
@@ -311,14 +363,17 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
           for (int u = 0; u < 4; u++) {
             const int t = 8 * q + 2 * u;
             const float2 v = make_float2(xv[t], xv[t + 1]);
+            const float2 z = add2(add2(v, nx0), nm1);
+            q2 = fma2(z, z, q2);
             split2(mul2(v, sx2), pxh[u], pxl[u]);
-            split2(mul2(add2(add2(v, nx0), nm1), sz2), pzh[u], pzl[u]);
+            split2(mul2(z, sz2), pzh[u], pzl[u]);
           }
           *reinterpret_cast<uint4*>(x_hi + i * 24 + 8 * q) = xh;
           *reinterpret_cast<uint4*>(x_lo + i * 24 + 8 * q) = xl;
           *reinterpret_cast<uint4*>(z_hi + i * 24 + 8 * q) = zh;
           *reinterpret_cast<uint4*>(z_lo + i * 24 + 8 * q) = zl;
         }
+        nu2 = q2.x + q2.y;
       }
       __syncwarp();
     } else {
@@ -348,6 +403,10 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
         m1 = s1 * a.inv_s;
         mu = x0 + m1;
         kap = s3 * a.inv_v;
+        for (int t = 0; t < S; t++) {
+          const float z = (xr[t] - x0) - m1;
+          nu2 = fmaf(z, z, nu2);
+        }
       }
       sx = pow2_scale(warp_max(amx));
       sz = pow2_scale(2.f * warp_max(dmx));
@@ -371,6 +430,74 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
     }
     // xbuf is free: fetch the next series while this one is in the tensor cores
     if (b + nwarps < b_end) prefetch(b + nwarps);
+    // Def 5: sigma^2 = (1/(N S)) sum_n [nu2_n + S (mu_n - mubar)^2]
+    const float mbar = warp_sum(i < N ? mu : 0.f) * a.inv_n;
+    const float dv = i < N ? nu2 + (float)S * (mu - mbar) * (mu - mbar) : 0.f;
+    const float inv_var = 1.0f / (warp_sum(dv) * a.inv_ns + kEpsTrend);
+
+    float qa[MMT][2 * MT][4];  // Q' = sw (W_s A_s + W_t A_t)
+#pragma unroll
+    for (int mm = 0; mm < MMT; mm++)
+#pragma unroll
+      for (int nt = 0; nt < 2 * MT; nt++)
+#pragma unroll
+        for (int e = 0; e < 4; e++) qa[mm][nt][e] = 0.f;
+
+    // ---------------- a4+a5 trend: exponent -Dhat_ij / tau_t (row max is 0 at j = i,
+    // D_ii = 0) = -(mu~_i - mu~_j)^2 - (k~_i - k~_j)^2 with mu~ = mu sqrt(inv_var kt),
+    // k~ = kappa sqrt(vtrend inv_var kt) (Def 7-8); then fold Q' += W'_t A_t per k-tile
+    {
+      const float cm = sqrtf(inv_var * a.kt), ck = sqrtf(a.vtrend * inv_var * a.kt);
+      const float mus = i < N ? mu * cm : 0.f, kas = i < N ? kap * ck : 0.f;
+      float2 cmu[2 * MT], ckap[2 * MT];
+#pragma unroll
+      for (int nt = 0; nt < 2 * MT; nt++) {
+        const int j = 8 * nt + 2 * cq;
+        const float m0 = __shfl_sync(0xffffffffu, mus, j), m1v = __shfl_sync(0xffffffffu, mus, j + 1);
+        cmu[nt] = make_float2(j < N ? -m0 : -INFINITY, j + 1 < N ? -m1v : -INFINITY);
+        ckap[nt] = make_float2(-__shfl_sync(0xffffffffu, kas, j), -__shfl_sync(0xffffffffu, kas, j + 1));
+      }
+#pragma unroll
+      for (int mt = 0; mt < MT; mt++) {
+        uint32_t bh[2 * MT][2], bl[2 * MT][2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int ii = 16 * mt + 8 * h + gq;
+          const float2 mui = f2(__shfl_sync(0xffffffffu, mus, ii));
+          const float2 ki = f2(__shfl_sync(0xffffffffu, kas, ii));
+          float2 u[2 * MT];
+          float2 sum2 = f2(0.f);
+#pragma unroll
+          for (int nt = 0; nt < 2 * MT; nt++) {
+            const float2 dm = add2(mui, cmu[nt]), dk = add2(ki, ckap[nt]);
+            const float2 e = fma2(make_float2(-dk.x, -dk.y), dk, mul2(make_float2(-dm.x, -dm.y), dm));
+            u[nt] = make_float2(fast_ex2(e.x), fast_ex2(e.y));
+            sum2 = add2(sum2, u[nt]);
+          }
+          float sum = sum2.x + sum2.y;
+          sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+          sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+          const float2 rs2 = f2(ii < N ? 1.f / sum : 0.f);
+#pragma unroll
+          for (int nt = 0; nt < 2 * MT; nt++) {
+            const float2 p = mul2(u[nt], rs2);
+            if constexpr (DBG) {
+              if (ii < N) {
+                const int j = 8 * nt + 2 * cq;
+                float* d = a.a_t_dbg + (series * N + ii) * N + j;
+                if (j < N) d[0] = p.x;
+                if (j + 1 < N) d[1] = p.y;
+              }
+            }
+            uint32_t hi, lo;
+            split2(p, hi, lo);
+            bh[nt][h] = movm_t(hi);
+            bl[nt][h] = movm_t(lo);
+          }
+        }
+        fold_tile(qa, NR, mt, bh, bl);
+      }
+    }
 
     // ---------------- a3: Gram G' = Z' Z'^T (= sz^2 G), fragments g[mt][nt][.]
     float g[MT][2 * MT][4];
@@ -415,18 +542,18 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
     }
     if constexpr (SC > 0 && (SC % 16) == 8) {
       // K tail of 8 (S = 24: columns 16..23) with m16n8k8
-      constexpr int k0 = (SC / 16) * 16;
+      constexpr int kt0 = (SC / 16) * 16;
       uint32_t ah[MT][2], al[MT][2];
 #pragma unroll
       for (int mt = 0; mt < MT; mt++) {
-        const int off = (16 * mt + (lane & 7) + 8 * (q8 & 1)) * zph + k0;
+        const int off = (16 * mt + (lane & 7) + 8 * (q8 & 1)) * zph + kt0;
         ldsm_x2(ah[mt][0], ah[mt][1], z_hi + off);
         ldsm_x2(al[mt][0], al[mt][1], z_lo + off);
       }
 #pragma unroll
       for (int np = 0; np < MT; np++) {
         uint32_t bh[2], bl[2];  // b0 of n-tiles 2np, 2np+1 (rows j of Z', k = 16..23)
-        const int off = (16 * np + 8 * (q8 & 1) + (lane & 7)) * zph + k0;
+        const int off = (16 * np + 8 * (q8 & 1) + (lane & 7)) * zph + kt0;
         ldsm_x2(bh[0], bh[1], z_hi + off);
         ldsm_x2(bl[0], bl[1], z_lo + off);
 #pragma unroll
@@ -446,7 +573,7 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
         }
       }
     }
-    // diagonal G'_ii = sz^2 nu2_i (Def 4) lives in lane 4 gq + gq/2: publish via smem
+    // diagonal G'_ii = sz^2 nu2_i lives in lane 4 gq + gq/2: publish via smem
     if (cq == (gq >> 1)) {
 #pragma unroll
       for (int mt = 0; mt < MT; mt++)
@@ -456,157 +583,64 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
               (gq & 1) ? g[mt][2 * mt + h][2 * h + 1] : g[mt][2 * mt + h][2 * h];
     }
     __syncwarp();
-    const float diag = i < N ? dsm[i] : 0.f;
-    // Def 6 normaliser in sz^2 units: rho_ij = G'_ij inv_i inv_j
-    const float inv = i < N ? rsqrtf(diag + kEpsSeasonal * sz * sz) : 1.f;
-    // Def 5: sigma^2 = (1/(N S)) sum_n [nu2_n + S (mu_n - mubar)^2]
-    const float mbar = warp_sum(i < N ? mu : 0.f) * a.inv_n;
-    const float dv = i < N ? diag / (sz * sz) + (float)S * (mu - mbar) * (mu - mbar) : 0.f;
-    const float inv_var = 1.0f / (warp_sum(dv) * a.inv_ns + kEpsTrend);
-    // trend exponent -(Dhat/tau_t) log2 e = -(mu~_i - mu~_j)^2 - (k~_i - k~_j)^2 with
-    // mu~ = mu sqrt(inv_var kt), k~ = kappa sqrt(vtrend inv_var kt)   (Def 7-8)
-    const float cm = sqrtf(inv_var * a.kt), ck = sqrtf(a.vtrend * inv_var * a.kt);
-    const float mus = i < N ? mu * cm : 0.f, kas = i < N ? kap * ck : 0.f;
 
-    // per-column quantities (j = 8 nt + 2 cq + e) as pairs, masked past N
-    float2 cinv[2 * MT], cmask[2 * MT], cmu[2 * MT], ckap[2 * MT];
+    // ---------------- a5 seasonal: rho_ij = G'_ij inv_i inv_j (Def 6, normaliser from the
+    // same contraction's diagonal), row softmax on the fragments, fold Q' += W'_s A_s
+    {
+      const float inv = i < N ? rsqrtf(dsm[i] + kEpsSeasonal * sz * sz) : 1.f;
+      float2 cinv[2 * MT], cmask[2 * MT];
 #pragma unroll
-    for (int nt = 0; nt < 2 * MT; nt++) {
-      const int j = 8 * nt + 2 * cq;
-      cinv[nt] = make_float2(__shfl_sync(0xffffffffu, inv, j), __shfl_sync(0xffffffffu, inv, j + 1));
-      cmask[nt] = make_float2(j < N ? 0.f : -INFINITY, j + 1 < N ? 0.f : -INFINITY);
-      const float m0 = __shfl_sync(0xffffffffu, mus, j), m1v = __shfl_sync(0xffffffffu, mus, j + 1);
-      cmu[nt] = make_float2(j < N ? -m0 : -INFINITY, j + 1 < N ? -m1v : -INFINITY);
-      ckap[nt] = make_float2(-__shfl_sync(0xffffffffu, kas, j), -__shfl_sync(0xffffffffu, kas, j + 1));
-    }
-
-    // ---------------- a5 seasonal softmax on the fragments, pack, transpose (movmatrix)
-    uint32_t bsh[MT][2 * MT][2], bsl[MT][2 * MT][2];  // B operand of the fold: [k-tile][n-tile][b0/b1]
+      for (int nt = 0; nt < 2 * MT; nt++) {
+        const int j = 8 * nt + 2 * cq;
+        cinv[nt] = make_float2(__shfl_sync(0xffffffffu, inv, j), __shfl_sync(0xffffffffu, inv, j + 1));
+        cmask[nt] = make_float2(j < N ? 0.f : -INFINITY, j + 1 < N ? 0.f : -INFINITY);
+      }
 #pragma unroll
-    for (int mt = 0; mt < MT; mt++)
+      for (int mt = 0; mt < MT; mt++) {
+        uint32_t bh[2 * MT][2], bl[2 * MT][2];
 #pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int ii = 16 * mt + 8 * h + gq;
-        const float rk = __shfl_sync(0xffffffffu, inv, ii) * a.ks;
-        float2 u[2 * MT];
-        float mx = -INFINITY;
+        for (int h = 0; h < 2; h++) {
+          const int ii = 16 * mt + 8 * h + gq;
+          const float rk = __shfl_sync(0xffffffffu, inv, ii) * a.ks;
+          float2 u[2 * MT];
+          float mx = -INFINITY;
 #pragma unroll
-        for (int nt = 0; nt < 2 * MT; nt++) {
-          u[nt] = fma2(make_float2(g[mt][nt][2 * h], g[mt][nt][2 * h + 1]), cinv[nt], cmask[nt]);
-          mx = fmaxf(mx, fmaxf(u[nt].x, u[nt].y));
-        }
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        const float2 rk2 = f2(rk), nb2 = f2(-mx * rk);
-        float2 sum2 = f2(0.f);
-#pragma unroll
-        for (int nt = 0; nt < 2 * MT; nt++) {
-          const float2 arg = fma2(u[nt], rk2, nb2);
-          u[nt] = make_float2(fast_ex2(arg.x), fast_ex2(arg.y));
-          sum2 = add2(sum2, u[nt]);
-        }
-        float sum = sum2.x + sum2.y;
-        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-        const float2 rs2 = f2(ii < N ? 1.f / sum : 0.f);
-#pragma unroll
-        for (int nt = 0; nt < 2 * MT; nt++) {
-          const float2 p = mul2(u[nt], rs2);
-          if constexpr (DBG) {
-            if (ii < N) {
-              const int j = 8 * nt + 2 * cq;
-              float* d = a.a_s_dbg + (series * N + ii) * N + j;
-              if (j < N) d[0] = p.x;
-              if (j + 1 < N) d[1] = p.y;
-            }
+          for (int nt = 0; nt < 2 * MT; nt++) {
+            u[nt] = fma2(make_float2(g[mt][nt][2 * h], g[mt][nt][2 * h + 1]), cinv[nt], cmask[nt]);
+            mx = fmaxf(mx, fmaxf(u[nt].x, u[nt].y));
           }
-          uint32_t hi, lo;
-          split2(p, hi, lo);
-          bsh[mt][nt][h] = movm_t(hi);
-          bsl[mt][nt][h] = movm_t(lo);
-        }
-      }
-
-    // ---------------- a6+a7 fold, seasonal half: Q' += W'_s A_s   (Q' = sw Q)
-    float qa[MMT][2 * MT][4];
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+          const float2 rk2 = f2(rk), nb2 = f2(-mx * rk);
+          float2 sum2 = f2(0.f);
 #pragma unroll
-    for (int mm = 0; mm < MMT; mm++)
-#pragma unroll
-      for (int nt = 0; nt < 2 * MT; nt++)
-#pragma unroll
-        for (int e = 0; e < 4; e++) qa[mm][nt][e] = 0.f;
-#pragma unroll
-    for (int kt = 0; kt < MT; kt++) {
-#pragma unroll
-      for (int mm = 0; mm < MMT; mm++) {
-        uint32_t wh[4], wl[4];
-        const int off = (16 * mm + (lane & 7) + 8 * (q8 & 1)) * ly.wph + 16 * kt + 8 * (q8 >> 1);
-        ldsm_x4(wh, w_hi + off);
-        ldsm_x4(wl, w_lo + off);
-#pragma unroll
-        for (int nt = 0; nt < 2 * MT; nt++) mma16816(qa[mm][nt], wl, bsh[kt][nt][0], bsh[kt][nt][1]);
-#pragma unroll
-        for (int nt = 0; nt < 2 * MT; nt++) mma16816(qa[mm][nt], wh, bsl[kt][nt][0], bsl[kt][nt][1]);
-#pragma unroll
-        for (int nt = 0; nt < 2 * MT; nt++) mma16816(qa[mm][nt], wh, bsh[kt][nt][0], bsh[kt][nt][1]);
-      }
-    }
-
-    // ---------------- a4+a5 trend: exponent -Dhat_ij / tau_t (row max is 0 at j = i, D_ii = 0)
-#pragma unroll
-    for (int mt = 0; mt < MT; mt++)
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int ii = 16 * mt + 8 * h + gq;
-        const float2 mui = f2(__shfl_sync(0xffffffffu, mus, ii));
-        const float2 ki = f2(__shfl_sync(0xffffffffu, kas, ii));
-        float2 u[2 * MT];
-        float2 sum2 = f2(0.f);
-#pragma unroll
-        for (int nt = 0; nt < 2 * MT; nt++) {
-          const float2 dm = add2(mui, cmu[nt]), dk = add2(ki, ckap[nt]);
-          const float2 e = fma2(make_float2(-dk.x, -dk.y), dk, mul2(make_float2(-dm.x, -dm.y), dm));
-          u[nt] = make_float2(fast_ex2(e.x), fast_ex2(e.y));
-          sum2 = add2(sum2, u[nt]);
-        }
-        float sum = sum2.x + sum2.y;
-        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-        const float2 rs2 = f2(ii < N ? 1.f / sum : 0.f);
-#pragma unroll
-        for (int nt = 0; nt < 2 * MT; nt++) {
-          const float2 p = mul2(u[nt], rs2);
-          if constexpr (DBG) {
-            if (ii < N) {
-              const int j = 8 * nt + 2 * cq;
-              float* d = a.a_t_dbg + (series * N + ii) * N + j;
-              if (j < N) d[0] = p.x;
-              if (j + 1 < N) d[1] = p.y;
-            }
+          for (int nt = 0; nt < 2 * MT; nt++) {
+            const float2 arg = fma2(u[nt], rk2, nb2);
+            u[nt] = make_float2(fast_ex2(arg.x), fast_ex2(arg.y));
+            sum2 = add2(sum2, u[nt]);
           }
-          uint32_t hi, lo;
-          split2(p, hi, lo);
-          bsh[mt][nt][h] = movm_t(hi);
-          bsl[mt][nt][h] = movm_t(lo);
+          float sum = sum2.x + sum2.y;
+          sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+          sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+          const float2 rs2 = f2(ii < N ? 1.f / sum : 0.f);
+#pragma unroll
+          for (int nt = 0; nt < 2 * MT; nt++) {
+            const float2 p = mul2(u[nt], rs2);
+            if constexpr (DBG) {
+              if (ii < N) {
+                const int j = 8 * nt + 2 * cq;
+                float* d = a.a_s_dbg + (series * N + ii) * N + j;
+                if (j < N) d[0] = p.x;
+                if (j + 1 < N) d[1] = p.y;
+              }
+            }
+            uint32_t hi, lo;
+            split2(p, hi, lo);
+            bh[nt][h] = movm_t(hi);
+            bl[nt][h] = movm_t(lo);
+          }
         }
-      }
-
-    // ---------------- fold, trend half: Q' += W'_t A_t
-#pragma unroll
-    for (int kt = 0; kt < MT; kt++) {
-#pragma unroll
-      for (int mm = 0; mm < MMT; mm++) {
-        uint32_t wh[4], wl[4];
-        const int off =
-            (16 * mm + (lane & 7) + 8 * (q8 & 1)) * ly.wph + NR + 16 * kt + 8 * (q8 >> 1);
-        ldsm_x4(wh, w_hi + off);
-        ldsm_x4(wl, w_lo + off);
-#pragma unroll
-        for (int nt = 0; nt < 2 * MT; nt++) mma16816(qa[mm][nt], wl, bsh[kt][nt][0], bsh[kt][nt][1]);
-#pragma unroll
-        for (int nt = 0; nt < 2 * MT; nt++) mma16816(qa[mm][nt], wh, bsl[kt][nt][0], bsl[kt][nt][1]);
-#pragma unroll
-        for (int nt = 0; nt < 2 * MT; nt++) mma16816(qa[mm][nt], wh, bsh[kt][nt][0], bsh[kt][nt][1]);
+        fold_tile(qa, 0, mt, bh, bl);
       }
     }
 
@@ -763,41 +797,25 @@ bool plan_mma_kernel(const FwdArgs& a, int max_smem_optin, MmaPlan* p) {
   }
   ly.wph = 2 * ly.nr + 8;
   ly.ntt = (a.S + 7) / 8;
-  ly.xbuf_f = (a.N * a.S + 3) & ~3;
-  int off = ly.xbuf_f * 4;
-  off = (off + 15) & ~15;
-  ly.off_xhi = off;
-  off += ly.nr * ly.sph * 2;
-  off = (off + 15) & ~15;
-  ly.off_xlo = off;
-  off += ly.nr * ly.sph * 2;
-  off = (off + 15) & ~15;
-  ly.off_zhi = off;
-  off += ly.nr * ly.zph * 2;
-  off = (off + 15) & ~15;
-  ly.off_zlo = off;
-  off += ly.nr * ly.zph * 2;
-  off = (off + 15) & ~15;
-  ly.off_diag = off;
-  off += 96 * 4 + 16;   // diag[32], x0/m1[64], TMA mbarrier
-  ly.per_warp_bytes = (off + 127) & ~127;
-  const int wrows = 16 * p->mmt;
-  int so = 0;
-  so += wrows * ly.wph * 2;
-  ly.off_wlo = so;
-  so += wrows * ly.wph * 2;
-  so = (so + 15) & ~15;
-  ly.wpack_bytes = so;
-  ly.off_bias = so;
-  so += a.H * 4;
-  ly.shared_bytes = (so + 127) & ~127;
+  const MmaOffsets o = mma_offsets(ly.nr, a.S, ly.sph, ly.zph, p->mmt);
+  ly.xbuf_f = ly.nr * a.S;
+  ly.off_xhi = o.xhi;
+  ly.off_xlo = o.xlo;
+  ly.off_zhi = o.zhi;
+  ly.off_zlo = o.zlo;
+  ly.off_diag = o.misc;
+  ly.per_warp_bytes = o.pw;
+  ly.off_wlo = o.wlo;
+  ly.wpack_bytes = o.wpack;
+  ly.off_bias = -1;  // after the per-warp regions (depends on warps per CTA)
+  ly.shared_bytes = o.wpack;
   p->warps_per_cta = 8;
-  p->smem_bytes = (size_t)ly.shared_bytes + (size_t)p->warps_per_cta * ly.per_warp_bytes;
-  while (p->smem_bytes > (size_t)max_smem_optin && p->warps_per_cta > 1) {
+  auto total = [&](int w) { return (size_t)o.wpack + (size_t)w * o.pw + (size_t)a.H * 4; };
+  while (total(p->warps_per_cta) > (size_t)max_smem_optin && p->warps_per_cta > 1)
     p->warps_per_cta >>= 1;
-    p->smem_bytes = (size_t)ly.shared_bytes + (size_t)p->warps_per_cta * ly.per_warp_bytes;
-  }
+  p->smem_bytes = total(p->warps_per_cta);
   if (p->smem_bytes > (size_t)max_smem_optin) return false;
+  if (p->sc == 24 && mma_wpack_bytes(a.N, a.M) != o.wpack) return false;
   p->wins_per_cta = p->warps_per_cta * 8;
   return true;
 }
