@@ -499,95 +499,12 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
       }
     }
 
-    // ---------------- a3: Gram G' = Z' Z'^T (= sz^2 G), fragments g[mt][nt][.]
-    float g[MT][2 * MT][4];
-#pragma unroll
-    for (int mt = 0; mt < MT; mt++)
-#pragma unroll
-      for (int nt = 0; nt < 2 * MT; nt++)
-#pragma unroll
-        for (int e = 0; e < 4; e++) g[mt][nt][e] = 0.f;
-    const int k16 = SC > 0 ? (SC / 16) * 16 : ly.kz;
-    for (int k0 = 0; k0 < k16; k0 += 16) {
-      uint32_t ah[MT][4], al[MT][4];
-#pragma unroll
-      for (int mt = 0; mt < MT; mt++) {
-        const int off = (16 * mt + (lane & 7) + 8 * (q8 & 1)) * zph + k0 + 8 * (q8 >> 1);
-        ldsm_x4(ah[mt], z_hi + off);
-        ldsm_x4(al[mt], z_lo + off);
-      }
-#pragma unroll
-      for (int np = 0; np < MT; np++) {
-        uint32_t bh[4], bl[4];
-        const int off = (16 * np + (lane & 7) + 8 * (q8 >> 1)) * zph + k0 + 8 * (q8 & 1);
-        ldsm_x4(bh, z_hi + off);
-        ldsm_x4(bl, z_lo + off);
-        // product-major order: independent accumulators back to back
-#pragma unroll
-        for (int mt = 0; mt < MT; mt++) {
-          mma16816(g[mt][2 * np], al[mt], bh[0], bh[1]);
-          mma16816(g[mt][2 * np + 1], al[mt], bh[2], bh[3]);
-        }
-#pragma unroll
-        for (int mt = 0; mt < MT; mt++) {
-          mma16816(g[mt][2 * np], ah[mt], bl[0], bl[1]);
-          mma16816(g[mt][2 * np + 1], ah[mt], bl[2], bl[3]);
-        }
-#pragma unroll
-        for (int mt = 0; mt < MT; mt++) {
-          mma16816(g[mt][2 * np], ah[mt], bh[0], bh[1]);
-          mma16816(g[mt][2 * np + 1], ah[mt], bh[2], bh[3]);
-        }
-      }
-    }
-    if constexpr (SC > 0 && (SC % 16) == 8) {
-      // K tail of 8 (S = 24: columns 16..23) with m16n8k8
-      constexpr int kt0 = (SC / 16) * 16;
-      uint32_t ah[MT][2], al[MT][2];
-#pragma unroll
-      for (int mt = 0; mt < MT; mt++) {
-        const int off = (16 * mt + (lane & 7) + 8 * (q8 & 1)) * zph + kt0;
-        ldsm_x2(ah[mt][0], ah[mt][1], z_hi + off);
-        ldsm_x2(al[mt][0], al[mt][1], z_lo + off);
-      }
-#pragma unroll
-      for (int np = 0; np < MT; np++) {
-        uint32_t bh[2], bl[2];  // b0 of n-tiles 2np, 2np+1 (rows j of Z', k = 16..23)
-        const int off = (16 * np + 8 * (q8 & 1) + (lane & 7)) * zph + kt0;
-        ldsm_x2(bh[0], bh[1], z_hi + off);
-        ldsm_x2(bl[0], bl[1], z_lo + off);
-#pragma unroll
-        for (int mt = 0; mt < MT; mt++) {
-          mma1688(g[mt][2 * np], al[mt][0], al[mt][1], bh[0]);
-          mma1688(g[mt][2 * np + 1], al[mt][0], al[mt][1], bh[1]);
-        }
-#pragma unroll
-        for (int mt = 0; mt < MT; mt++) {
-          mma1688(g[mt][2 * np], ah[mt][0], ah[mt][1], bl[0]);
-          mma1688(g[mt][2 * np + 1], ah[mt][0], ah[mt][1], bl[1]);
-        }
-#pragma unroll
-        for (int mt = 0; mt < MT; mt++) {
-          mma1688(g[mt][2 * np], ah[mt][0], ah[mt][1], bh[0]);
-          mma1688(g[mt][2 * np + 1], ah[mt][0], ah[mt][1], bh[1]);
-        }
-      }
-    }
-    // diagonal G'_ii = sz^2 nu2_i lives in lane 4 gq + gq/2: publish via smem
-    if (cq == (gq >> 1)) {
-#pragma unroll
-      for (int mt = 0; mt < MT; mt++)
-#pragma unroll
-        for (int h = 0; h < 2; h++)
-          dsm[16 * mt + 8 * h + gq] =
-              (gq & 1) ? g[mt][2 * mt + h][2 * h + 1] : g[mt][2 * mt + h][2 * h];
-    }
-    __syncwarp();
-
-    // ---------------- a5 seasonal: rho_ij = G'_ij inv_i inv_j (Def 6, normaliser from the
-    // same contraction's diagonal), row softmax on the fragments, fold Q' += W'_s A_s
+    // ---------------- a3 + a5 seasonal, one 16-row tile of query segments at a time:
+    // Gram rows G'[16 mt .. 16 mt + 15][:] = Z' Z'^T (= sz^2 G), rho_ij = G'_ij inv_i inv_j / sz^2
+    // with inv = 1/sqrt(nu2 + eps_s) (Def 6), row softmax on the fragments, fold Q' += W'_s A_s
     {
-      const float inv = i < N ? rsqrtf(dsm[i] + kEpsSeasonal * sz * sz) : 1.f;
+      const float inv = i < N ? rsqrtf(nu2 + kEpsSeasonal) : 1.f;
+      const float ks_z = a.ks / (sz * sz);
       float2 cinv[2 * MT], cmask[2 * MT];
 #pragma unroll
       for (int nt = 0; nt < 2 * MT; nt++) {
@@ -595,18 +512,69 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
         cinv[nt] = make_float2(__shfl_sync(0xffffffffu, inv, j), __shfl_sync(0xffffffffu, inv, j + 1));
         cmask[nt] = make_float2(j < N ? 0.f : -INFINITY, j + 1 < N ? 0.f : -INFINITY);
       }
+      const int k16 = SC > 0 ? (SC / 16) * 16 : ly.kz;
 #pragma unroll
       for (int mt = 0; mt < MT; mt++) {
+        float g[2 * MT][4];
+#pragma unroll
+        for (int nt = 0; nt < 2 * MT; nt++)
+#pragma unroll
+          for (int e = 0; e < 4; e++) g[nt][e] = 0.f;
+        for (int k0 = 0; k0 < k16; k0 += 16) {
+          uint32_t ah[4], al[4];
+          {
+            const int off = (16 * mt + (lane & 7) + 8 * (q8 & 1)) * zph + k0 + 8 * (q8 >> 1);
+            ldsm_x4(ah, z_hi + off);
+            ldsm_x4(al, z_lo + off);
+          }
+#pragma unroll
+          for (int np = 0; np < MT; np++) {
+            uint32_t bh[4], bl[4];
+            const int off = (16 * np + (lane & 7) + 8 * (q8 >> 1)) * zph + k0 + 8 * (q8 & 1);
+            ldsm_x4(bh, z_hi + off);
+            ldsm_x4(bl, z_lo + off);
+            // product-major order: independent accumulators back to back
+            mma16816(g[2 * np], al, bh[0], bh[1]);
+            mma16816(g[2 * np + 1], al, bh[2], bh[3]);
+            mma16816(g[2 * np], ah, bl[0], bl[1]);
+            mma16816(g[2 * np + 1], ah, bl[2], bl[3]);
+            mma16816(g[2 * np], ah, bh[0], bh[1]);
+            mma16816(g[2 * np + 1], ah, bh[2], bh[3]);
+          }
+        }
+        if constexpr (SC > 0 && (SC % 16) == 8) {
+          // K tail of 8 (S = 24: columns 16..23) with m16n8k8
+          constexpr int kt0 = (SC / 16) * 16;
+          uint32_t ah[2], al[2];
+          {
+            const int off = (16 * mt + (lane & 7) + 8 * (q8 & 1)) * zph + kt0;
+            ldsm_x2(ah[0], ah[1], z_hi + off);
+            ldsm_x2(al[0], al[1], z_lo + off);
+          }
+#pragma unroll
+          for (int np = 0; np < MT; np++) {
+            uint32_t bh[2], bl[2];  // b0 of n-tiles 2np, 2np+1 (rows j of Z', k = 16..23)
+            const int off = (16 * np + 8 * (q8 & 1) + (lane & 7)) * zph + kt0;
+            ldsm_x2(bh[0], bh[1], z_hi + off);
+            ldsm_x2(bl[0], bl[1], z_lo + off);
+            mma1688(g[2 * np], al[0], al[1], bh[0]);
+            mma1688(g[2 * np + 1], al[0], al[1], bh[1]);
+            mma1688(g[2 * np], ah[0], ah[1], bl[0]);
+            mma1688(g[2 * np + 1], ah[0], ah[1], bl[1]);
+            mma1688(g[2 * np], ah[0], ah[1], bh[0]);
+            mma1688(g[2 * np + 1], ah[0], ah[1], bh[1]);
+          }
+        }
         uint32_t bh[2 * MT][2], bl[2 * MT][2];
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           const int ii = 16 * mt + 8 * h + gq;
-          const float rk = __shfl_sync(0xffffffffu, inv, ii) * a.ks;
+          const float rk = __shfl_sync(0xffffffffu, inv, ii) * ks_z;
           float2 u[2 * MT];
           float mx = -INFINITY;
 #pragma unroll
           for (int nt = 0; nt < 2 * MT; nt++) {
-            u[nt] = fma2(make_float2(g[mt][nt][2 * h], g[mt][nt][2 * h + 1]), cinv[nt], cmask[nt]);
+            u[nt] = fma2(make_float2(g[nt][2 * h], g[nt][2 * h + 1]), cinv[nt], cmask[nt]);
             mx = fmaxf(mx, fmaxf(u[nt].x, u[nt].y));
           }
           mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
@@ -644,68 +612,55 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
       }
     }
 
-    // ---------------- Q' fragments -> A operand of the head (hi/lo, in registers)
-    uint32_t qh[MMT][MT][4], ql[MMT][MT][4];
-#pragma unroll
-    for (int mm = 0; mm < MMT; mm++)
-#pragma unroll
-      for (int kj = 0; kj < MT; kj++) {
-        split2(qa[mm][2 * kj][0], qa[mm][2 * kj][1], qh[mm][kj][0], ql[mm][kj][0]);
-        split2(qa[mm][2 * kj][2], qa[mm][2 * kj][3], qh[mm][kj][1], ql[mm][kj][1]);
-        split2(qa[mm][2 * kj + 1][0], qa[mm][2 * kj + 1][1], qh[mm][kj][2], ql[mm][kj][2]);
-        split2(qa[mm][2 * kj + 1][2], qa[mm][2 * kj + 1][3], qh[mm][kj][3], ql[mm][kj][3]);
-      }
-
-    // ---------------- a7 head Y' = Q' X' (= sw sx Y), t in chunks of 4 tiles; a8 store
+    // ---------------- a7 head Y' = Q' X' (= sw sx Y), one 16-row tile of future segments
+    // at a time, t in chunks of 4 tiles; a8 store y = Y + b
     const float2 ys2 = f2(inv_sw / sx);
     const bool pair_store = ((S | H) & 1) == 0;   // t, hh even -> 8-byte aligned pairs
     float* yg = a.y + series * H;
-    for (int t0 = 0; t0 < ntt; t0 += 4) {
-      float ya[MMT][4][4];
 #pragma unroll
-      for (int mm = 0; mm < MMT; mm++)
+    for (int mm = 0; mm < MMT; mm++) {
+      if (16 * mm >= M) break;
+      uint32_t qh[MT][4], ql[MT][4];   // Q' fragments -> A operand (hi/lo, in registers)
+#pragma unroll
+      for (int kj = 0; kj < MT; kj++) {
+        split2(qa[mm][2 * kj][0], qa[mm][2 * kj][1], qh[kj][0], ql[kj][0]);
+        split2(qa[mm][2 * kj][2], qa[mm][2 * kj][3], qh[kj][1], ql[kj][1]);
+        split2(qa[mm][2 * kj + 1][0], qa[mm][2 * kj + 1][1], qh[kj][2], ql[kj][2]);
+        split2(qa[mm][2 * kj + 1][2], qa[mm][2 * kj + 1][3], qh[kj][3], ql[kj][3]);
+      }
+      for (int t0 = 0; t0 < ntt; t0 += 4) {
+        float ya[4][4];
 #pragma unroll
         for (int nt = 0; nt < 4; nt++)
 #pragma unroll
-          for (int e = 0; e < 4; e++) ya[mm][nt][e] = 0.f;
+          for (int e = 0; e < 4; e++) ya[nt][e] = 0.f;
 #pragma unroll
-      for (int kj = 0; kj < MT; kj++) {
+        for (int kj = 0; kj < MT; kj++) {
 #pragma unroll
-        for (int tp = 0; tp < 2; tp++) {
-          const int nt0 = t0 + 2 * tp;
-          if (nt0 >= ntt) break;
-          uint32_t xh[4], xl[4];
-          const int krow = 16 * kj + (lane & 7) + 8 * (q8 & 1);
-          const bool two = nt0 + 1 < ntt;
-          if (two) {
-            const int off = krow * sph + 8 * (nt0 + (q8 >> 1));
-            ldsm_x4_t(xh, x_hi + off);
-            ldsm_x4_t(xl, x_lo + off);
-          } else {
-            const int off = krow * sph + 8 * nt0;
-            ldsm_x2_t(xh[0], xh[1], x_hi + off);
-            ldsm_x2_t(xl[0], xl[1], x_lo + off);
-            xh[2] = xh[3] = xl[2] = xl[3] = 0u;
-          }
-#pragma unroll
-          for (int mm = 0; mm < MMT; mm++) {
-            mma16816(ya[mm][2 * tp], ql[mm][kj], xh[0], xh[1]);
-            if (two) mma16816(ya[mm][2 * tp + 1], ql[mm][kj], xh[2], xh[3]);
-          }
-#pragma unroll
-          for (int mm = 0; mm < MMT; mm++) {
-            mma16816(ya[mm][2 * tp], qh[mm][kj], xl[0], xl[1]);
-            if (two) mma16816(ya[mm][2 * tp + 1], qh[mm][kj], xl[2], xl[3]);
-          }
-#pragma unroll
-          for (int mm = 0; mm < MMT; mm++) {
-            mma16816(ya[mm][2 * tp], qh[mm][kj], xh[0], xh[1]);
-            if (two) mma16816(ya[mm][2 * tp + 1], qh[mm][kj], xh[2], xh[3]);
+          for (int tp = 0; tp < 2; tp++) {
+            const int nt0 = t0 + 2 * tp;
+            if (nt0 >= ntt) break;
+            uint32_t xh[4], xl[4];
+            const int krow = 16 * kj + (lane & 7) + 8 * (q8 & 1);
+            const bool two = nt0 + 1 < ntt;
+            if (two) {
+              const int off = krow * sph + 8 * (nt0 + (q8 >> 1));
+              ldsm_x4_t(xh, x_hi + off);
+              ldsm_x4_t(xl, x_lo + off);
+            } else {
+              const int off = krow * sph + 8 * nt0;
+              ldsm_x2_t(xh[0], xh[1], x_hi + off);
+              ldsm_x2_t(xl[0], xl[1], x_lo + off);
+              xh[2] = xh[3] = xl[2] = xl[3] = 0u;
+            }
+            mma16816(ya[2 * tp], ql[kj], xh[0], xh[1]);
+            if (two) mma16816(ya[2 * tp + 1], ql[kj], xh[2], xh[3]);
+            mma16816(ya[2 * tp], qh[kj], xl[0], xl[1]);
+            if (two) mma16816(ya[2 * tp + 1], qh[kj], xl[2], xl[3]);
+            mma16816(ya[2 * tp], qh[kj], xh[0], xh[1]);
+            if (two) mma16816(ya[2 * tp + 1], qh[kj], xh[2], xh[3]);
           }
         }
-      }
-#pragma unroll
-      for (int mm = 0; mm < MMT; mm++)
 #pragma unroll
         for (int nt = 0; nt < 4; nt++) {
           const int t = 8 * (t0 + nt) + 2 * cq;
@@ -714,7 +669,7 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
             const int m = 16 * mm + 8 * h + gq;
             if (m < M && t < S) {
               const int hh = m * S + t;
-              const float2 v = mul2(make_float2(ya[mm][nt][2 * h], ya[mm][nt][2 * h + 1]), ys2);
+              const float2 v = mul2(make_float2(ya[nt][2 * h], ya[nt][2 * h + 1]), ys2);
               if (pair_store) {  // hh even, H even: hh < H implies hh + 1 < H
                 if (hh >= H) continue;
                 const float2 o = add2(v, *reinterpret_cast<const float2*>(bS + hh));
@@ -728,6 +683,7 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
             }
           }
         }
+      }
     }
   }
   cp_async_wait_all();
