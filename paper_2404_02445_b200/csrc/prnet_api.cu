@@ -21,6 +21,7 @@ struct prnet_handle {
   double* d_err = nullptr;  // error-sum partials
   unsigned char* d_wpack = nullptr;  // mma variant: packed fp16 hi/lo head
   float* d_invsw = nullptr;
+  unsigned char* d_wpack_tc = nullptr;  // tc variant: head as the tcgen05 B operand
   bool loaded = false;
   int forced_variant = -1;  // prnet_set_kernel_variant
   std::string err;
@@ -72,6 +73,7 @@ prnet::FwdArgs make_args(const prnet_handle* h, const float* x, int64_t B, float
   a.bias = h->d_b;
   a.wpack = reinterpret_cast<const uint4*>(h->d_wpack);
   a.wpack_inv_sw = h->d_invsw;
+  a.wpack_tc = reinterpret_cast<const uint4*>(h->d_wpack_tc);
   a.B = B;
   a.C = c.channels;
   a.L = c.lookback;
@@ -115,9 +117,14 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
 }
 
 // 0 = warp_f32 (N <= 32, CUDA-core FP32), 1 = long_f32 (32 < N <= 512),
-// 2 = mma_f16x3 (N <= 32, M <= 32: tensor cores, split-fp16 3-product).
+// 2 = mma_f16x3 (N <= 32, M <= 32: mma.sync tensor cores, split-fp16 3-product),
+// 3 = tc_fold (S = 24, 16 < N <= 32, M <= 32: fold on tcgen05 / TMEM, rest as 2).
+bool tc_applicable(const prnet_handle* h) {
+  return h->cfg.seg_len == 24 && h->N > 16 && h->N <= 32 && h->M <= 32;
+}
 int pick_variant(const prnet_handle* h) {
   if (h->forced_variant >= 0) return h->forced_variant;
+  if (tc_applicable(h)) return 3;
   if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
   return h->N <= 32 ? 0 : 1;
 }
@@ -131,7 +138,12 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
   cudaError_t e;
   int v = pick_variant(h);
   if (v == 1 && a_s != nullptr) v = 0;  // the attention dump lives in the N <= 32 kernels
-  if (v == 2) {
+  if (v == 3) {
+    prnet::TcPlan p;
+    if (!prnet::plan_tc_kernel(a, h->max_smem_optin, &p))
+      return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the tcgen05 kernel");
+    e = prnet::launch_tc_kernel(a, p, st);
+  } else if (v == 2) {
     prnet::MmaPlan p;
     if (!prnet::plan_mma_kernel(a, h->max_smem_optin, &p))
       return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the tensor-core kernel");
@@ -265,6 +277,17 @@ prnet_status prnet_load_params(prnet_handle* h, const float* w_seasonal, const f
             cudaSuccess)
       return cuda_fail(h, e, "cudaMemcpy(packed head)");
   }
+  if (tc_applicable(h)) {  // the same head as the tcgen05 B operand (K-major core matrices)
+    const int bytes = prnet::tc_wpack_bytes();
+    std::vector<unsigned char> pack((size_t)h->Cw * bytes);
+    std::vector<float> inv(h->Cw);
+    prnet::pack_tc_head(w_seasonal, w_trend, h->Cw, h->M, h->N, pack.data(), inv.data());
+    if (!h->d_wpack_tc && (e = cudaMalloc(&h->d_wpack_tc, pack.size())) != cudaSuccess)
+      return cuda_fail(h, e, "cudaMalloc(tc head)");
+    if ((e = cudaMemcpy(h->d_wpack_tc, pack.data(), pack.size(), cudaMemcpyHostToDevice)) !=
+        cudaSuccess)
+      return cuda_fail(h, e, "cudaMemcpy(tc head)");
+  }
   h->loaded = true;
   return PRNET_OK;
 }
@@ -349,6 +372,7 @@ void prnet_destroy(prnet_handle* h) {
     cudaFree(h->d_err);
     cudaFree(h->d_wpack);
     cudaFree(h->d_invsw);
+    cudaFree(h->d_wpack_tc);
     for (int k = 0; k < prnet_handle::kStages; k++) {
       cudaFree(h->d_xstage[k]);
       cudaFree(h->d_ystage[k]);
@@ -423,7 +447,10 @@ prnet_status prnet_error_sums(prnet_handle* h, const float* y, const float* targ
 
 prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {
   if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
-  if (variant < -1 || variant > 2) return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,0,1,2}");
+  if (variant < -1 || variant > 3)
+    return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,0,1,2,3}");
+  if (variant == 3 && !tc_applicable(h))
+    return fail(h, PRNET_ERR_UNSUPPORTED, "tc_fold variant needs S = 24, 16 < N <= 32, M <= 32");
   if ((variant == 0 || variant == 2) && h->N > 32)
     return fail(h, PRNET_ERR_UNSUPPORTED, "variant needs N <= 32");
   if (variant == 2 && (h->M > 32 || h->cfg.seg_len > 128))
