@@ -195,6 +195,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no extras)")
+    ap.add_argument("--variant", default=None, help="force a kernel variant (tuning)")
     args = ap.parse_args()
 
     rank, world, local = dist_env()
@@ -249,6 +250,8 @@ def main():
     del sd
     ws, wt, b = synth.make_params(w.C, M, N, w.H, True, args.seed, w.cfg_id)
     model = PRNet(w.C, w.L, w.S, w.H, device=local).load(ws, wt, b)
+    if args.variant:
+        model.set_variant(args.variant)
     y = torch.empty((count, w.C, w.H), dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
     plan = model.plan(count)

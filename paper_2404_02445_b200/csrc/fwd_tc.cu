@@ -180,7 +180,7 @@ void pack_tc_head(const float* ws, const float* wt, int Cw, int M, int N, unsign
 template <int MMT, bool DBG>
 __global__ void __launch_bounds__(128, 4) prnet_fwd_tc_kernel(FwdArgs a, int wins_per_cta) {
   extern __shared__ __align__(1024) unsigned char smem[];
-  constexpr int MT = 2, NR = 32, S = 24;
+  constexpr int MT = 2, S = 24;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gq = lane >> 2, cq = lane & 3, q8 = lane >> 3;
   const int c = blockIdx.y;
@@ -634,7 +634,7 @@ bool plan_tc_kernel(const FwdArgs& a, int max_smem_optin, TcPlan* p) {
   p->mmt = a.M <= 16 ? 1 : 2;
   p->smem_bytes = (size_t)kTcOffBias + (size_t)a.H * 4;
   if (p->smem_bytes > (size_t)max_smem_optin) return false;
-  p->wins_per_cta = 32;
+  p->wins_per_cta = 128;
   return true;
 }
 

@@ -3,6 +3,7 @@
 // (prnet_forward_host).  No torch types, no exceptions across the boundary.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -138,15 +139,21 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
   cudaError_t e;
   int v = pick_variant(h);
   if (v == 1 && a_s != nullptr) v = 0;  // the attention dump lives in the N <= 32 kernels
+  static const int wpc_env = [] {  // tuning knob: windows per CTA (0 = plan default)
+    const char* e = getenv("PRNET_WINDOWS_PER_CTA");
+    return e ? atoi(e) : 0;
+  }();
   if (v == 3) {
     prnet::TcPlan p;
     if (!prnet::plan_tc_kernel(a, h->max_smem_optin, &p))
       return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the tcgen05 kernel");
+    if (wpc_env > 0) p.wins_per_cta = (wpc_env + 3) & ~3;
     e = prnet::launch_tc_kernel(a, p, st);
   } else if (v == 2) {
     prnet::MmaPlan p;
     if (!prnet::plan_mma_kernel(a, h->max_smem_optin, &p))
       return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the tensor-core kernel");
+    if (wpc_env > 0) p.wins_per_cta = wpc_env;
     e = prnet::launch_mma_kernel(a, p, st);
   } else if (v == 0) {
     prnet::WarpPlan p;
