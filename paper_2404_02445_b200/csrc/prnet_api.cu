@@ -123,6 +123,10 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
 bool tc_applicable(const prnet_handle* h) {
   return h->cfg.seg_len == 24 && h->N > 16 && h->N <= 32 && h->M <= 32;
 }
+// 4 = tc_full (S = 24, N <= 32, M <= 32: Gram, fold and head on tcgen05 / TMEM)
+bool tc2_applicable(const prnet_handle* h) {
+  return h->cfg.seg_len == 24 && h->N <= 32 && h->M <= 32;
+}
 int pick_variant(const prnet_handle* h) {
   if (h->forced_variant >= 0) return h->forced_variant;
   if (tc_applicable(h)) return 3;
@@ -143,7 +147,13 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
     const char* e = getenv("PRNET_WINDOWS_PER_CTA");
     return e ? atoi(e) : 0;
   }();
-  if (v == 3) {
+  if (v == 4) {
+    prnet::Tc2Plan p;
+    if (!prnet::plan_tc2_kernel(a, h->max_smem_optin, &p))
+      return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the tcgen05 kernel");
+    if (wpc_env > 0) p.wins_per_group = (wpc_env + 3) & ~3;
+    e = prnet::launch_tc2_kernel(a, p, st);
+  } else if (v == 3) {
     prnet::TcPlan p;
     if (!prnet::plan_tc_kernel(a, h->max_smem_optin, &p))
       return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the tcgen05 kernel");
@@ -284,7 +294,7 @@ prnet_status prnet_load_params(prnet_handle* h, const float* w_seasonal, const f
             cudaSuccess)
       return cuda_fail(h, e, "cudaMemcpy(packed head)");
   }
-  if (tc_applicable(h)) {  // the same head as the tcgen05 B operand (K-major core matrices)
+  if (tc2_applicable(h)) {  // the same head as the tcgen05 B operand (K-major core matrices)
     const int bytes = prnet::tc_wpack_bytes();
     std::vector<unsigned char> pack((size_t)h->Cw * bytes);
     std::vector<float> inv(h->Cw);
@@ -454,8 +464,10 @@ prnet_status prnet_error_sums(prnet_handle* h, const float* y, const float* targ
 
 prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {
   if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
-  if (variant < -1 || variant > 3)
-    return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,0,1,2,3}");
+  if (variant < -1 || variant > 4)
+    return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,0,1,2,3,4}");
+  if (variant == 4 && !tc2_applicable(h))
+    return fail(h, PRNET_ERR_UNSUPPORTED, "tc_full variant needs S = 24, N <= 32, M <= 32");
   if (variant == 3 && !tc_applicable(h))
     return fail(h, PRNET_ERR_UNSUPPORTED, "tc_fold variant needs S = 24, 16 < N <= 32, M <= 32");
   if ((variant == 0 || variant == 2) && h->N > 32)

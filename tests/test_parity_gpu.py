@@ -36,10 +36,12 @@ def _applicable(variant, L, S, H):
         return N <= 32 and M <= 32 and S <= 128
     if variant == "tc_fold":
         return S == 24 and 16 < N <= 32 and M <= 32
+    if variant == "tc_full":
+        return S == 24 and N <= 32 and M <= 32
     return True
 
 
-VARIANTS = [None, "warp_f32", "mma_f16x3", "tc_fold", "long_f32"]
+VARIANTS = [None, "warp_f32", "mma_f16x3", "tc_fold", "tc_full", "long_f32"]
 
 
 def _check_small(oracle_mod, x, S, H, hpc=True, tau_s=1.0, tau_t=1.0, scale=None, variant=None):
@@ -69,7 +71,7 @@ def test_etth1_full(oracle_mod):
 FULL = ["weather_h96", "weather_h192", "weather_h336", "weather_h720", "electricity", "traffic"]
 
 
-@pytest.mark.parametrize("variant", [None, "warp_f32", "mma_f16x3"])
+@pytest.mark.parametrize("variant", [None, "warp_f32", "mma_f16x3", "tc_fold", "tc_full"])
 @pytest.mark.parametrize("name", FULL)
 def test_full_size_sampled(oracle_mod, name, variant):
     """The whole test set runs on the GPU in the bench's launch configuration; the
@@ -138,7 +140,7 @@ def test_shapes_ragged(oracle_mod, L, S, H, variant):
     _check_small(oracle_mod, x, S, H, variant=variant)
 
 
-@pytest.mark.parametrize("variant", VARIANTS[:4])
+@pytest.mark.parametrize("variant", VARIANTS[:5])
 @pytest.mark.parametrize("tau", [0.05, 0.1, 1.0, 10.0])
 @pytest.mark.parametrize("hpc", [True, False])
 def test_temperatures_and_head_modes(oracle_mod, tau, hpc, variant):
@@ -146,7 +148,7 @@ def test_temperatures_and_head_modes(oracle_mod, tau, hpc, variant):
     _check_small(oracle_mod, x, 24, 336, hpc=hpc, tau_s=tau, tau_t=tau * 0.7, variant=variant)
 
 
-@pytest.mark.parametrize("variant", VARIANTS[:4])
+@pytest.mark.parametrize("variant", VARIANTS[:5])
 @pytest.mark.parametrize("kind", ["normal", "constant", "scaled"])
 @pytest.mark.parametrize("L,S", [(720, 24), (1440, 24)])
 def test_value_distributions(oracle_mod, kind, L, S, variant):
@@ -175,7 +177,7 @@ def test_segment_gather_bit_exact(L, S):
     np.testing.assert_array_equal(seg, x[:, :, idx])
 
 
-@pytest.mark.parametrize("variant", ["warp_f32", "mma_f16x3", "tc_fold"])
+@pytest.mark.parametrize("variant", ["warp_f32", "mma_f16x3", "tc_fold", "tc_full"])
 @pytest.mark.parametrize("L,S", [(720, 24), (96, 24), (384, 24), (480, 24)])
 def test_attention_matrices(oracle_mod, L, S, variant):
     x = synth.random_windows(2, 3, L, kind="mixed")
@@ -195,7 +197,7 @@ def test_attention_matrices(oracle_mod, L, S, variant):
 
 
 # ------------------------------------------------------------------ determinism, sharding, host path
-@pytest.mark.parametrize("variant", VARIANTS[:4])
+@pytest.mark.parametrize("variant", VARIANTS[:5])
 def test_deterministic_and_shard_invariant(variant):
     from paper_2404_02445_b200 import shard_windows
     x = torch.from_numpy(synth.random_windows(37, 11, 720)).cuda()
