@@ -632,7 +632,7 @@ bool plan_mma_kernel(const FwdArgs& a, int max_smem_optin, MmaPlan* p) {
   p->smem_bytes = total(p->warps_per_cta);
   if (p->smem_bytes > (size_t)max_smem_optin) return false;
   if (p->sc == 24 && mma_wpack_bytes(a.N, a.M) != o.wpack) return false;
-  p->wins_per_cta = p->warps_per_cta * 8;
+  p->wins_per_cta = p->warps_per_cta * 16;
   return true;
 }
 

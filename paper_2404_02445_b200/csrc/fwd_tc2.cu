@@ -107,13 +107,13 @@ __device__ __forceinline__ void mbar_wait_to(uint64_t* bar, uint32_t parity) {
   uint64_t t0 = 0;
   for (uint32_t it = 0;; it++) {
     asm volatile(
-        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
         "selp.u32 %0, 1, 0, p;\n}"
         : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(20000u)   // suspend up to 20 us, no spinning
         : "memory");
     if (done) return;
-    if ((it & 1023u) == 0) {
+    if ((it & 63u) == 0) {
       uint64_t now;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
       if (it == 0) t0 = now;

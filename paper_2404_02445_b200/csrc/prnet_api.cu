@@ -129,7 +129,8 @@ bool tc2_applicable(const prnet_handle* h) {
 }
 int pick_variant(const prnet_handle* h) {
   if (h->forced_variant >= 0) return h->forced_variant;
-  if (tc_applicable(h)) return 3;
+  // measured on B200 (profiles/r01_variants.md): mma_f16x3 is the fastest N <= 32 path;
+  // tc_fold (-1.6 %) and tc_full (-30 %) are selectable with prnet_set_kernel_variant
   if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
   return h->N <= 32 ? 0 : 1;
 }
