@@ -65,7 +65,7 @@ __host__ __device__ constexpr MmaOffsets mma_offsets(int nr, int S, int sph, int
   return o;
 }
 
-template <int MT, int MMT, int SC, bool DBG>
+template <int MT, int MMT, int SC, bool DBG, int NC = 0>
 __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLayout ly,
                                                                int wins_per_cta) {
   extern __shared__ float4 smem4[];
@@ -78,7 +78,10 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
   const int c = blockIdx.y;
   const int cw = a.head_per_channel ? c : 0;
   const int S = SC > 0 ? SC : a.S;
-  const int N = a.N, M = a.M, H = a.H, L = a.L, C = a.C;
+  // NC > 0: compile-time segment count (30: every L = 720, S = 24 config), so the
+  // j < N / i < N masks fold away
+  const int N = NC > 0 ? NC : a.N;
+  const int M = a.M, H = a.H, L = a.L, C = a.C;
   // operand row strides (halves): dense rows when S is the compile-time 24
   const int sph = SC > 0 ? SC : ly.sph;
   const int zph = SC > 0 ? SC : ly.zph;
@@ -636,9 +639,9 @@ bool plan_mma_kernel(const FwdArgs& a, int max_smem_optin, MmaPlan* p) {
   return true;
 }
 
-template <int MT, int MMT, int SC, bool DBG>
+template <int MT, int MMT, int SC, bool DBG, int NC = 0>
 static cudaError_t launch_t(const FwdArgs& a, const MmaPlan& p, cudaStream_t st) {
-  auto k = prnet_fwd_mma_kernel<MT, MMT, SC, DBG>;
+  auto k = prnet_fwd_mma_kernel<MT, MMT, SC, DBG, NC>;
   cudaError_t e =
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
@@ -656,6 +659,9 @@ static cudaError_t launch_sc(const FwdArgs& a, const MmaPlan& p, cudaStream_t st
 
 cudaError_t launch_mma_kernel(const FwdArgs& a, const MmaPlan& p, cudaStream_t st) {
   const bool dbg = a.a_s_dbg != nullptr;
+  if (p.sc == 24 && a.N == 30 && !dbg)   // L = 720, S = 24: configs[1..3]
+    return p.mmt == 1 ? launch_t<2, 1, 24, false, 30>(a, p, st)
+                      : launch_t<2, 2, 24, false, 30>(a, p, st);
   if (p.sc == 24) return dbg ? launch_sc<24, true>(a, p, st) : launch_sc<24, false>(a, p, st);
   return dbg ? launch_sc<0, true>(a, p, st) : launch_sc<0, false>(a, p, st);
 }
