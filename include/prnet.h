@@ -134,13 +134,20 @@ prnet_status prnet_debug_attention(prnet_handle* h, const float* x, int64_t batc
 prnet_status prnet_error_sums(prnet_handle* h, const float* y, const float* target,
                               int64_t batch, double* out3, void* cuda_stream);
 
-/* Select the forward kernel (tuning / cross-checking; default -1 = automatic):
- *   0 = warp_f32   one warp per series, CUDA-core FP32            (N <= 32)
- *   1 = long_f32   one CTA per series, rows streamed, FP32         (N <= 512)
- *   2 = mma_f16x3  one warp per series, tensor cores (mma.sync m16n8k16) with
- *                  split-fp16 hi/lo operands, 3 products, fp32 accumulation
- *                  (N <= 32, M <= 32, S <= 128)
- * All variants compute the same reading to within the documented tolerance. */
+/* Select the forward kernel (tuning / cross-checking; default -1 = automatic).
+ * All variants compute the same reading to within the documented tolerance:
+ *   0 = warp_f32     one warp per series, CUDA-core FP32                  (N <= 32)
+ *   1 = long_f32     one CTA per series, rows streamed, FP32              (N <= 512)
+ *   2 = mma_f16x3    one warp per series, mma.sync m16n8k16 with split-fp16
+ *                    hi/lo operands, 3 products, fp32 accumulation
+ *                    (N <= 32, M <= 32, S <= 128)             [auto: N <= 32]
+ *   3 = tc_fold      as 2, fold Q = W A on tcgen05.mma with a TMEM accumulator
+ *                    (S = 24, 16 < N <= 32, M <= 32)
+ *   4 = tc_full      Gram, fold and head on tcgen05 / TMEM, lane-per-row softmax
+ *                    (S = 24, N <= 32, M <= 32)
+ *   5 = flash_f16x3  one CTA per series, 16-key tiles streamed, mma.sync
+ *                    split-fp16 (16 < N <= 512, S <= 48, M <= 32)  [auto: N > 32]
+ * Returns PRNET_ERR_UNSUPPORTED when the variant does not cover the handle's shape. */
 prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant);
 
 /* Kernel-level accounting for the bench (host-side, no device work):

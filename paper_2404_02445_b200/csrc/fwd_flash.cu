@@ -1,0 +1,449 @@
+// fwd_flash.cu -- PRNet pattern-attention forward for long lookbacks (32 < N <= 512
+// segments; the stress sweep of BASELINE.json configs[4], L up to 5760) on the
+// tensor cores, flash-attention style.
+//
+// Same reading and split-fp16 3-product arithmetic as
+// fwd_mma.cu.  The N x N similarity matrices are never materialised: one CTA owns
+// one series, warps take 16-row query tiles, and for each 16-key tile
+//   a3  Gram tile      G' = Z'_i Z'_j^T                      (mma.sync m16n8k16)
+//   a4  trend logits   -(mu~_i - mu~_j)^2 - (k~_i - k~_j)^2  (FP32, packed f32x2)
+//   a5  exponentials with a KNOWN row maximum -- 0 for the trend row (D_ii = 0) and
+//       f_i = nu_i / sqrt(nu2_i + eps_s) >= rho_ij for the seasonal row (Cauchy-Schwarz)
+//       -- so no online rescaling is needed; the row sums accumulate
+//   a6  P_s += E_s X_j,  P_t += E_t X_j   (E straight from the accumulator fragments
+//       to the A operand, FA2 style; X_j from shared memory)      (mma.sync)
+// then the 16 pattern rows are normalised and folded into the head accumulator
+//   a7  Y += W'_s[:, tile] P_s + W'_t[:, tile] P_t     (P transposed with movmatrix)
+// and a fixed-order reduction over the warps adds the bias (a8).
+#include <cuda_fp16.h>
+
+#include <cmath>
+
+#include "mma_common.cuh"
+
+namespace prnet {
+
+namespace {
+
+__device__ __forceinline__ float block_reduce(float v, float* scratch, bool is_max) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = is_max ? warp_max(v) : warp_sum(v);
+  __syncthreads();
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  float r = is_max ? 0.f : 0.f;
+  for (int w = 0; w < nw; w++) r = is_max ? fmaxf(r, scratch[w]) : r + scratch[w];
+  return r;
+}
+
+// A-fragment (16 x 16, rows r0.., cols c0..) of a row-major global fp16 matrix
+__device__ __forceinline__ void ldg_afrag(const __half* base, int ld, int r0, int c0, int lane,
+                                          uint32_t (&f)[4]) {
+  const int g = lane >> 2, c = lane & 3;
+  const __half* p = base + (size_t)(r0 + g) * ld + c0 + 2 * c;
+  f[0] = __ldg(reinterpret_cast<const unsigned int*>(p));
+  f[1] = __ldg(reinterpret_cast<const unsigned int*>(p + 8 * ld));
+  f[2] = __ldg(reinterpret_cast<const unsigned int*>(p + 8));
+  f[3] = __ldg(reinterpret_cast<const unsigned int*>(p + 8 * ld + 8));
+}
+
+}  // namespace
+
+static int flash_npad(int N) { return (N + 15) & ~15; }
+
+int flash_wpack_bytes(int N, int M) {
+  const int rows = M <= 16 ? 16 : 32;
+  return 2 * rows * 2 * flash_npad(N) * 2;   // hi + lo, [rows][2 Npad] halves
+}
+
+// W' = W sw as fp16 hi/lo, row-major [16 MMT][2 Npad]: seasonal i at [0, Npad),
+// trend i at [Npad, 2 Npad); hi block then lo block.
+void pack_flash_head(const float* ws, const float* wt, int Cw, int M, int N, unsigned char* out,
+                     float* inv_sw) {
+  const int rows = M <= 16 ? 16 : 32, np = flash_npad(N), ld = 2 * np;
+  const int bytes = flash_wpack_bytes(N, M);
+  for (int c = 0; c < Cw; c++) {
+    const float* s = ws + (size_t)c * M * N;
+    const float* t = wt + (size_t)c * M * N;
+    float mx = 0.f;
+    for (int k = 0; k < M * N; k++) mx = fmaxf(mx, fmaxf(fabsf(s[k]), fabsf(t[k])));
+    float sw = 1.f;
+    if (mx > 0.f && std::isfinite(mx)) {
+      int e;
+      frexpf(mx, &e);
+      sw = ldexpf(1.f, -e);
+    }
+    inv_sw[c] = 1.f / sw;
+    __half* hi = reinterpret_cast<__half*>(out + (size_t)c * bytes);
+    __half* lo = hi + rows * ld;
+    for (int m = 0; m < rows; m++)
+      for (int k = 0; k < ld; k++) {
+        float v = 0.f;
+        if (m < M) {
+          if (k < np) {
+            if (k < N) v = s[m * N + k] * sw;
+          } else if (k - np < N) {
+            v = t[m * N + (k - np)] * sw;
+          }
+        }
+        const __half h = __float2half_rn(v);
+        hi[m * ld + k] = h;
+        lo[m * ld + k] = __float2half_rn(v - __half2float(h));
+      }
+  }
+}
+
+template <int KS, int NTT, int MMT>
+__global__ void __launch_bounds__(256, 1) prnet_fwd_flash_kernel(FwdArgs a, FlashLayout ly,
+                                                                 int wins_per_cta) {
+  extern __shared__ float4 smem4[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(smem4);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int gq = lane >> 2, cq = lane & 3, q8 = lane >> 3;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int c = blockIdx.y;
+  const int cw = a.head_per_channel ? c : 0;
+  const int S = a.S, N = a.N, M = a.M, H = a.H, L = a.L, C = a.C;
+  const int NP = ly.npad, NT = NP / 16, ZP = ly.zph, XP = ly.xph;
+
+  float* xbuf = reinterpret_cast<float*>(smem);
+  __half* z_hi = reinterpret_cast<__half*>(smem + ly.off_zhi);
+  __half* z_lo = reinterpret_cast<__half*>(smem + ly.off_zlo);
+  __half* x_hi = reinterpret_cast<__half*>(smem + ly.off_xhi);
+  __half* x_lo = reinterpret_cast<__half*>(smem + ly.off_xlo);
+  float* c_inv = reinterpret_cast<float*>(smem + ly.off_col);   // [NP] 0 past N
+  float* c_max = c_inv + NP;                                    // [NP] f_i
+  float* c_mu = c_max + NP;                                     // [NP] mu~ (+inf past N)
+  float* c_ka = c_mu + NP;                                      // [NP] kappa~
+  float* c_nu = c_ka + NP;                                      // [NP] scratch: mu, nu2
+  float* yred = reinterpret_cast<float*>(smem + ly.off_yred);   // [nwarps][16 MMT][8 NTT]
+  float* scr = reinterpret_cast<float*>(smem + ly.off_scr);     // [32]
+  const __half* w_hi = reinterpret_cast<const __half*>(
+      reinterpret_cast<const unsigned char*>(a.wpack_flash) + (size_t)cw * ly.wpack_bytes);
+  const int WLD = 2 * NP;
+  const __half* w_lo = w_hi + (16 * MMT) * WLD;
+  const float inv_sw = a.wpack_flash_inv_sw[cw];
+
+  // operand tiles start at zero: rows >= N and columns >= S stay zero
+  for (int k = tid; k < (ly.off_col - ly.off_zhi) / 16; k += nthr)
+    reinterpret_cast<uint4*>(smem + ly.off_zhi)[k] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+
+  const int64_t b_begin = (int64_t)blockIdx.x * wins_per_cta;
+  int64_t b_end = b_begin + wins_per_cta;
+  if (b_end > a.B) b_end = a.B;
+  const float half_s = a.half_s;
+  for (int64_t b = b_begin; b < b_end; b++) {
+    const int64_t series = b * C + c;
+    // ---------------- a1: load the segmented span
+    {
+      const float* xg = a.x + series * L + a.r;
+      for (int k = tid; k < N * S; k += nthr) xbuf[k] = __ldg(xg + k);
+    }
+    __syncthreads();
+    // ---------------- a2: descriptors (Def 4-5), thread per segment
+    float amx = 0.f, dmx = 0.f;
+    for (int n = tid; n < N; n += nthr) {
+      const float* xr = xbuf + n * S;
+      const float x0 = xr[0];
+      float s1 = 0.f, s3 = 0.f;
+      for (int t = 0; t < S; t++) {
+        const float d = xr[t] - x0;
+        s1 += d;
+        s3 = fmaf((float)t - half_s, d, s3);
+        amx = fmaxf(amx, fabsf(xr[t]));
+        dmx = fmaxf(dmx, fabsf(d));
+      }
+      c_nu[n] = s1 * a.inv_s;          // m1 (mu - x0)
+      c_ka[n] = s3 * a.inv_v;          // kappa
+    }
+    const float sx = pow2_scale(block_reduce(amx, scr, true));
+    const float sz = pow2_scale(2.f * block_reduce(dmx, scr, true));
+    float musum = 0.f;
+    for (int n = tid; n < N; n += nthr) {
+      const float* xr = xbuf + n * S;
+      const float x0 = xr[0], m1 = c_nu[n];
+      float q = 0.f;
+      for (int t = 0; t < S; t++) {
+        const float v = xr[t];
+        const float z = (v - x0) - m1;
+        q = fmaf(z, z, q);
+        __half h, l;
+        split1(v * sx, h, l);
+        x_hi[n * XP + t] = h;
+        x_lo[n * XP + t] = l;
+        split1(z * sz, h, l);
+        z_hi[n * ZP + t] = h;
+        z_lo[n * ZP + t] = l;
+      }
+      const float mu = x0 + m1;
+      c_mu[n] = mu;        // temporarily mu
+      c_inv[n] = q;        // temporarily nu2
+      musum += mu;
+    }
+    const float mbar = block_reduce(musum, scr, false) * a.inv_n;
+    float dsum = 0.f;
+    for (int n = tid; n < N; n += nthr) {
+      const float d = c_mu[n] - mbar;
+      dsum += c_inv[n] + (float)S * d * d;
+    }
+    const float inv_var = 1.0f / (block_reduce(dsum, scr, false) * a.inv_ns + kEpsTrend);
+    const float cmt = sqrtf(inv_var * a.kt), ckt = sqrtf(a.vtrend * inv_var * a.kt);
+    for (int n = tid; n < NP; n += nthr) {
+      if (n < N) {
+        const float nu2 = c_inv[n];
+        const float inv = rsqrtf(nu2 + kEpsSeasonal);
+        c_inv[n] = inv;
+        c_max[n] = sqrtf(nu2) * inv;   // f_n: known row maximum of rho (Cauchy-Schwarz)
+        c_mu[n] = c_mu[n] * cmt;
+        c_ka[n] = c_ka[n] * ckt;
+      } else {
+        c_inv[n] = 0.f;
+        c_max[n] = 0.f;
+        c_mu[n] = INFINITY;            // exponent -inf: masked key
+        c_ka[n] = 0.f;
+      }
+    }
+    __syncthreads();
+
+    // ---------------- a3..a7 per 16-row query tile
+    float yacc[MMT][NTT][4];
+#pragma unroll
+    for (int mm = 0; mm < MMT; mm++)
+#pragma unroll
+      for (int nt = 0; nt < NTT; nt++)
+#pragma unroll
+        for (int e = 0; e < 4; e++) yacc[mm][nt][e] = 0.f;
+    const float rsz2 = a.ks / (sz * sz);
+    for (int qt = warp; qt < NT; qt += nwarps) {
+      uint32_t zah[KS][4], zal[KS][4];
+#pragma unroll
+      for (int ks = 0; ks < KS; ks++) {
+        const int off = (16 * qt + (lane & 7) + 8 * (q8 & 1)) * ZP + 16 * ks + 8 * (q8 >> 1);
+        ldsm_x4(zah[ks], z_hi + off);
+        ldsm_x4(zal[ks], z_lo + off);
+      }
+      float rk[2], nb[2], mi[2], ki[2];
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int ii = 16 * qt + 8 * h + gq;
+        rk[h] = (ii < N ? c_inv[ii] : 1.f) * rsz2;
+        nb[h] = -c_max[ii] * a.ks;
+        mi[h] = ii < N ? c_mu[ii] : 0.f;
+        ki[h] = c_ka[ii];
+      }
+      float as_[NTT][4], at_[NTT][4];
+#pragma unroll
+      for (int nt = 0; nt < NTT; nt++)
+#pragma unroll
+        for (int e = 0; e < 4; e++) as_[nt][e] = at_[nt][e] = 0.f;
+      float ssum[2] = {0.f, 0.f}, tsum[2] = {0.f, 0.f};
+
+      for (int jt = 0; jt < NT; jt++) {
+        // a3: Gram tile (16 query rows x 16 keys)
+        float g[2][4];
+#pragma unroll
+        for (int nt = 0; nt < 2; nt++)
+#pragma unroll
+          for (int e = 0; e < 4; e++) g[nt][e] = 0.f;
+#pragma unroll
+        for (int ks = 0; ks < KS; ks++) {
+          uint32_t bh[4], bl[4];
+          const int off = (16 * jt + (lane & 7) + 8 * (q8 >> 1)) * ZP + 16 * ks + 8 * (q8 & 1);
+          ldsm_x4(bh, z_hi + off);
+          ldsm_x4(bl, z_lo + off);
+          mma16816(g[0], zal[ks], bh[0], bh[1]);
+          mma16816(g[1], zal[ks], bh[2], bh[3]);
+          mma16816(g[0], zah[ks], bl[0], bl[1]);
+          mma16816(g[1], zah[ks], bl[2], bl[3]);
+          mma16816(g[0], zah[ks], bh[0], bh[1]);
+          mma16816(g[1], zah[ks], bh[2], bh[3]);
+        }
+        // a4/a5: exponentials with known maxima, row sums, E as A fragments (hi/lo)
+        uint32_t esh[4], esl[4], eth[4], etl[4];
+#pragma unroll
+        for (int nt = 0; nt < 2; nt++) {
+          const int j = 16 * jt + 8 * nt + 2 * cq;
+          const float2 cinv = *reinterpret_cast<const float2*>(c_inv + j);
+          const float2 cmu = *reinterpret_cast<const float2*>(c_mu + j);
+          const float2 cka = *reinterpret_cast<const float2*>(c_ka + j);
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const float2 u = mul2(make_float2(g[nt][2 * h], g[nt][2 * h + 1]), cinv);
+            const float2 arg = fma2(u, f2(rk[h]), f2(nb[h]));
+            float2 es = make_float2(fast_ex2(arg.x), fast_ex2(arg.y));
+            if (j >= N) es.x = 0.f;
+            if (j + 1 >= N) es.y = 0.f;
+            const float2 dm = add2(f2(mi[h]), make_float2(-cmu.x, -cmu.y));
+            const float2 dk = add2(f2(ki[h]), make_float2(-cka.x, -cka.y));
+            const float2 ea = fma2(make_float2(-dk.x, -dk.y), dk, mul2(make_float2(-dm.x, -dm.y), dm));
+            const float2 et = make_float2(fast_ex2(ea.x), fast_ex2(ea.y));
+            ssum[h] += es.x + es.y;
+            tsum[h] += et.x + et.y;
+            // A fragment register index: a0 (h0, nt0), a1 (h1, nt0), a2 (h0, nt1), a3 (h1, nt1)
+            split2(es, esh[2 * nt + h], esl[2 * nt + h]);
+            split2(et, eth[2 * nt + h], etl[2 * nt + h]);
+          }
+        }
+        // a6: P += E X_j  (X_j rows of this key tile, t tiles)
+#pragma unroll
+        for (int tp = 0; tp < (NTT + 1) / 2; tp++) {
+          uint32_t xh[4], xl[4];
+          const int krow = 16 * jt + (lane & 7) + 8 * (q8 & 1);
+          if (2 * tp + 1 < NTT) {
+            const int off = krow * XP + 8 * (2 * tp + (q8 >> 1));
+            ldsm_x4_t(xh, x_hi + off);
+            ldsm_x4_t(xl, x_lo + off);
+          } else {
+            const int off = krow * XP + 8 * (2 * tp);
+            ldsm_x2_t(xh[0], xh[1], x_hi + off);
+            ldsm_x2_t(xl[0], xl[1], x_lo + off);
+          }
+#pragma unroll
+          for (int u2 = 0; u2 < 2; u2++) {
+            const int nt = 2 * tp + u2;
+            if (nt < NTT) {
+              mma16816(as_[nt], esl, xh[2 * u2], xh[2 * u2 + 1]);
+              mma16816(at_[nt], etl, xh[2 * u2], xh[2 * u2 + 1]);
+              mma16816(as_[nt], esh, xl[2 * u2], xl[2 * u2 + 1]);
+              mma16816(at_[nt], eth, xl[2 * u2], xl[2 * u2 + 1]);
+              mma16816(as_[nt], esh, xh[2 * u2], xh[2 * u2 + 1]);
+              mma16816(at_[nt], eth, xh[2 * u2], xh[2 * u2 + 1]);
+            }
+          }
+        }
+      }
+      // row sums over the quad, normalise: P rows of this tile
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        ssum[h] += __shfl_xor_sync(0xffffffffu, ssum[h], 1);
+        ssum[h] += __shfl_xor_sync(0xffffffffu, ssum[h], 2);
+        tsum[h] += __shfl_xor_sync(0xffffffffu, tsum[h], 1);
+        tsum[h] += __shfl_xor_sync(0xffffffffu, tsum[h], 2);
+        const int ii = 16 * qt + 8 * h + gq;
+        ssum[h] = ii < N ? 1.f / ssum[h] : 0.f;
+        tsum[h] = ii < N ? 1.f / tsum[h] : 0.f;
+      }
+      // a7: P fragments -> B operand (k = i, n = t) via movmatrix; Y += W'_s P_s + W'_t P_t
+      uint32_t psh[NTT][2], psl[NTT][2], pth[NTT][2], ptl[NTT][2];
+#pragma unroll
+      for (int nt = 0; nt < NTT; nt++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          uint32_t hi, lo;
+          split2(mul2(make_float2(as_[nt][2 * h], as_[nt][2 * h + 1]), f2(ssum[h])), hi, lo);
+          psh[nt][h] = movm_t(hi);
+          psl[nt][h] = movm_t(lo);
+          split2(mul2(make_float2(at_[nt][2 * h], at_[nt][2 * h + 1]), f2(tsum[h])), hi, lo);
+          pth[nt][h] = movm_t(hi);
+          ptl[nt][h] = movm_t(lo);
+        }
+#pragma unroll
+      for (int mm = 0; mm < MMT; mm++) {
+        uint32_t wsh[4], wsl[4], wth[4], wtl[4];
+        ldg_afrag(w_hi, WLD, 16 * mm, 16 * qt, lane, wsh);
+        ldg_afrag(w_lo, WLD, 16 * mm, 16 * qt, lane, wsl);
+        ldg_afrag(w_hi, WLD, 16 * mm, NP + 16 * qt, lane, wth);
+        ldg_afrag(w_lo, WLD, 16 * mm, NP + 16 * qt, lane, wtl);
+#pragma unroll
+        for (int nt = 0; nt < NTT; nt++) {
+          mma16816(yacc[mm][nt], wsl, psh[nt][0], psh[nt][1]);
+          mma16816(yacc[mm][nt], wsh, psl[nt][0], psl[nt][1]);
+          mma16816(yacc[mm][nt], wsh, psh[nt][0], psh[nt][1]);
+          mma16816(yacc[mm][nt], wtl, pth[nt][0], pth[nt][1]);
+          mma16816(yacc[mm][nt], wth, ptl[nt][0], ptl[nt][1]);
+          mma16816(yacc[mm][nt], wth, pth[nt][0], pth[nt][1]);
+        }
+      }
+    }
+    // ---------------- a8: fixed-order reduction over warps, scale, bias, store
+    {
+      constexpr int YR = 8 * NTT;
+      float* yw = yred + warp * (16 * MMT) * YR;
+#pragma unroll
+      for (int mm = 0; mm < MMT; mm++)
+#pragma unroll
+        for (int nt = 0; nt < NTT; nt++)
+#pragma unroll
+          for (int h = 0; h < 2; h++)
+            *reinterpret_cast<float2*>(yw + (16 * mm + 8 * h + gq) * YR + 8 * nt + 2 * cq) =
+                make_float2(yacc[mm][nt][2 * h], yacc[mm][nt][2 * h + 1]);
+      __syncthreads();
+      const float ysc = inv_sw / sx;
+      const float* gb = a.bias + (int64_t)cw * H;
+      float* yg = a.y + series * H;
+      for (int h = tid; h < H; h += nthr) {
+        const int m = h / S, t = h - m * S;
+        float v = 0.f;
+        for (int w = 0; w < nwarps; w++) v += yred[(w * (16 * MMT) + m) * YR + t];
+        yg[h] = v * ysc + __ldg(gb + h);
+      }
+      __syncthreads();
+    }
+  }
+}
+
+bool plan_flash_kernel(const FwdArgs& a, int max_smem_optin, FlashPlan* p) {
+  if (a.N <= 16 || a.N > 512 || a.M > 32 || a.S > 48) return false;
+  FlashLayout& ly = p->ly;
+  p->ks = (a.S + 15) / 16;
+  p->ntt = (a.S + 7) / 8;
+  if (p->ntt == 5) p->ntt = 6;
+  if (p->ntt == 1) p->ntt = 2;
+  p->mmt = a.M <= 16 ? 1 : 2;
+  ly.npad = flash_npad(a.N);
+  auto odd8 = [](int v) { v = (v + 7) & ~7; if (((v / 8) & 1) == 0) v += 8; return v; };
+  ly.zph = odd8(16 * p->ks);
+  ly.xph = odd8(8 * p->ntt);
+  int off = ((a.N * a.S * 4) + 15) & ~15;
+  ly.off_zhi = off;
+  off += ly.npad * ly.zph * 2;
+  ly.off_zlo = off;
+  off += ly.npad * ly.zph * 2;
+  ly.off_xhi = off;
+  off += ly.npad * ly.xph * 2;
+  ly.off_xlo = off;
+  off += ly.npad * ly.xph * 2;
+  off = (off + 15) & ~15;
+  ly.off_col = off;
+  off += 5 * ly.npad * 4;
+  off = (off + 15) & ~15;
+  ly.off_yred = off;
+  p->warps = 8;
+  off += p->warps * (16 * p->mmt) * (8 * p->ntt) * 4;
+  ly.off_scr = off;
+  off += 32 * 4;
+  p->smem_bytes = (size_t)((off + 127) & ~127);
+  ly.wpack_bytes = flash_wpack_bytes(a.N, a.M);
+  if (p->smem_bytes > (size_t)max_smem_optin) return false;
+  p->wins_per_cta = 4;
+  return true;
+}
+
+template <int KS, int NTT, int MMT>
+static cudaError_t launch_flash_t(const FwdArgs& a, const FlashPlan& p, cudaStream_t st) {
+  auto k = prnet_fwd_flash_kernel<KS, NTT, MMT>;
+  cudaError_t e =
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)((a.B + p.wins_per_cta - 1) / p.wins_per_cta), (unsigned)a.C);
+  k<<<grid, 32 * p.warps, p.smem_bytes, st>>>(a, p.ly, p.wins_per_cta);
+  return cudaGetLastError();
+}
+
+template <int KS, int NTT>
+static cudaError_t launch_flash_m(const FwdArgs& a, const FlashPlan& p, cudaStream_t st) {
+  return p.mmt == 1 ? launch_flash_t<KS, NTT, 1>(a, p, st) : launch_flash_t<KS, NTT, 2>(a, p, st);
+}
+
+cudaError_t launch_flash_kernel(const FwdArgs& a, const FlashPlan& p, cudaStream_t st) {
+  switch (p.ks * 10 + p.ntt) {
+    case 12: return launch_flash_m<1, 2>(a, p, st);   // S <= 16
+    case 23: return launch_flash_m<2, 3>(a, p, st);   // S in (16, 24]
+    case 24: return launch_flash_m<2, 4>(a, p, st);   // S in (24, 32]
+    case 36: return launch_flash_m<3, 6>(a, p, st);   // S in (32, 48]
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace prnet

@@ -367,6 +367,11 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
     // with inv = 1/sqrt(nu2 + eps_s) (Def 6), row softmax on the fragments, fold Q' += W'_s A_s
     {
       const float inv = i < N ? rsqrtf(nu2 + kEpsSeasonal) : 1.f;
+      // Known row maximum: rho_ij <= f_i f_j <= f_i with f = nu / sqrt(nu2 + eps_s) (Cauchy-
+      // Schwarz), and rho_ii = f_i^2 is within f_i (1 - f_i) <= 1/4 of it, so exp((rho_ij -
+      // f_i) / tau_s) never overflows and its largest term never underflows for tau_s > 0.003.
+      // Softmax is shift-invariant: same result as subtracting the searched max (Def 8).
+      const float cself = i < N ? sqrtf(nu2) * inv : 0.f;
       const float ks_z = a.ks / (sz * sz);
       float2 cinv[2 * MT], cmask[2 * MT];
 #pragma unroll
@@ -434,15 +439,10 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
           const int ii = 16 * mt + 8 * h + gq;
           const float rk = __shfl_sync(0xffffffffu, inv, ii) * ks_z;
           float2 u[2 * MT];
-          float mx = -INFINITY;
 #pragma unroll
-          for (int nt = 0; nt < 2 * MT; nt++) {
+          for (int nt = 0; nt < 2 * MT; nt++)
             u[nt] = fma2(make_float2(g[nt][2 * h], g[nt][2 * h + 1]), cinv[nt], cmask[nt]);
-            mx = fmaxf(mx, fmaxf(u[nt].x, u[nt].y));
-          }
-          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-          const float2 rk2 = f2(rk), nb2 = f2(-mx * rk);
+          const float2 rk2 = f2(rk), nb2 = f2(-__shfl_sync(0xffffffffu, cself, ii) * a.ks);
           float2 sum2 = f2(0.f);
 #pragma unroll
           for (int nt = 0; nt < 2 * MT; nt++) {

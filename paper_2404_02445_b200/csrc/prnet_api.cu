@@ -23,6 +23,8 @@ struct prnet_handle {
   unsigned char* d_wpack = nullptr;  // mma variant: packed fp16 hi/lo head
   float* d_invsw = nullptr;
   unsigned char* d_wpack_tc = nullptr;  // tc variant: head as the tcgen05 B operand
+  unsigned char* d_wpack_fl = nullptr;  // flash variant: head [16 MMT][2 Npad] hi/lo
+  float* d_invsw_fl = nullptr;
   bool loaded = false;
   int forced_variant = -1;  // prnet_set_kernel_variant
   std::string err;
@@ -75,6 +77,8 @@ prnet::FwdArgs make_args(const prnet_handle* h, const float* x, int64_t B, float
   a.wpack = reinterpret_cast<const uint4*>(h->d_wpack);
   a.wpack_inv_sw = h->d_invsw;
   a.wpack_tc = reinterpret_cast<const uint4*>(h->d_wpack_tc);
+  a.wpack_flash = h->d_wpack_fl;
+  a.wpack_flash_inv_sw = h->d_invsw_fl;
   a.B = B;
   a.C = c.channels;
   a.L = c.lookback;
@@ -123,6 +127,10 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
 bool tc_applicable(const prnet_handle* h) {
   return h->cfg.seg_len == 24 && h->N > 16 && h->N <= 32 && h->M <= 32;
 }
+// 5 = flash_f16x3 (16 < N <= 512, S <= 48, M <= 32: key-streaming mma.sync, long lookbacks)
+bool flash_applicable(const prnet_handle* h) {
+  return h->N > 16 && h->N <= 512 && h->cfg.seg_len <= 48 && h->M <= 32;
+}
 // 4 = tc_full (S = 24, N <= 32, M <= 32: Gram, fold and head on tcgen05 / TMEM)
 bool tc2_applicable(const prnet_handle* h) {
   return h->cfg.seg_len == 24 && h->N <= 32 && h->M <= 32;
@@ -132,6 +140,7 @@ int pick_variant(const prnet_handle* h) {
   // measured on B200 (profiles/r01_variants.md): mma_f16x3 is the fastest N <= 32 path;
   // tc_fold (-1.6 %) and tc_full (-30 %) are selectable with prnet_set_kernel_variant
   if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
+  if (h->N > 32 && flash_applicable(h)) return 5;
   return h->N <= 32 ? 0 : 1;
 }
 
@@ -148,7 +157,12 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
     const char* e = getenv("PRNET_WINDOWS_PER_CTA");
     return e ? atoi(e) : 0;
   }();
-  if (v == 4) {
+  if (v == 5) {
+    prnet::FlashPlan p;
+    if (!prnet::plan_flash_kernel(a, h->max_smem_optin, &p))
+      return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the flash kernel");
+    e = prnet::launch_flash_kernel(a, p, st);
+  } else if (v == 4) {
     prnet::Tc2Plan p;
     if (!prnet::plan_tc2_kernel(a, h->max_smem_optin, &p))
       return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the tcgen05 kernel");
@@ -295,6 +309,20 @@ prnet_status prnet_load_params(prnet_handle* h, const float* w_seasonal, const f
             cudaSuccess)
       return cuda_fail(h, e, "cudaMemcpy(packed head)");
   }
+  if (flash_applicable(h)) {  // head for the key-streaming kernel
+    const int bytes = prnet::flash_wpack_bytes(h->N, h->M);
+    std::vector<unsigned char> pack((size_t)h->Cw * bytes);
+    std::vector<float> inv(h->Cw);
+    prnet::pack_flash_head(w_seasonal, w_trend, h->Cw, h->M, h->N, pack.data(), inv.data());
+    if (!h->d_wpack_fl && ((e = cudaMalloc(&h->d_wpack_fl, pack.size())) != cudaSuccess ||
+                           (e = cudaMalloc(&h->d_invsw_fl, inv.size() * 4)) != cudaSuccess))
+      return cuda_fail(h, e, "cudaMalloc(flash head)");
+    if ((e = cudaMemcpy(h->d_wpack_fl, pack.data(), pack.size(), cudaMemcpyHostToDevice)) !=
+            cudaSuccess ||
+        (e = cudaMemcpy(h->d_invsw_fl, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice)) !=
+            cudaSuccess)
+      return cuda_fail(h, e, "cudaMemcpy(flash head)");
+  }
   if (tc2_applicable(h)) {  // the same head as the tcgen05 B operand (K-major core matrices)
     const int bytes = prnet::tc_wpack_bytes();
     std::vector<unsigned char> pack((size_t)h->Cw * bytes);
@@ -391,6 +419,8 @@ void prnet_destroy(prnet_handle* h) {
     cudaFree(h->d_wpack);
     cudaFree(h->d_invsw);
     cudaFree(h->d_wpack_tc);
+    cudaFree(h->d_wpack_fl);
+    cudaFree(h->d_invsw_fl);
     for (int k = 0; k < prnet_handle::kStages; k++) {
       cudaFree(h->d_xstage[k]);
       cudaFree(h->d_ystage[k]);
@@ -465,8 +495,10 @@ prnet_status prnet_error_sums(prnet_handle* h, const float* y, const float* targ
 
 prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {
   if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
-  if (variant < -1 || variant > 4)
-    return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,0,1,2,3,4}");
+  if (variant < -1 || variant > 5)
+    return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,...,5}");
+  if (variant == 5 && !flash_applicable(h))
+    return fail(h, PRNET_ERR_UNSUPPORTED, "flash variant needs 16 < N <= 512, S <= 48, M <= 32");
   if (variant == 4 && !tc2_applicable(h))
     return fail(h, PRNET_ERR_UNSUPPORTED, "tc_full variant needs S = 24, N <= 32, M <= 32");
   if (variant == 3 && !tc_applicable(h))
