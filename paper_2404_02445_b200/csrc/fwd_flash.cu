@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(256, 1) prnet_fwd_flash_kernel(FwdArgs a, Flas
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int c = blockIdx.y;
   const int cw = a.head_per_channel ? c : 0;
-  const int S = a.S, N = a.N, M = a.M, H = a.H, L = a.L, C = a.C;
+  const int S = a.S, N = a.N, H = a.H, L = a.L, C = a.C;
   const int NP = ly.npad, NT = NP / 16, ZP = ly.zph, XP = ly.xph;
 
   float* xbuf = reinterpret_cast<float*>(smem);
