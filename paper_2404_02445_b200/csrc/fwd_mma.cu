@@ -183,14 +183,12 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
     const int i = lane;
     float x0 = 0.f, m1 = 0.f, mu = 0.f, kap = 0.f, nu2 = 0.f, sx, sz;
     if constexpr (SC == 24) {
-      // lane i holds its whole segment in registers: one read, 16-byte row stores.
-      // Lanes past N mirror row N-1 (no divergence); their results are masked below.
+      // lane i holds its whole segment in registers: one read, 16-byte row stores
       float xv[24];
       float2 s1 = f2(0.f), s3 = f2(0.f);
       float amx = 0.f, dmx = 0.f;
-      const int row = i < N ? i : N - 1;
-      {
-        const float4* xr = reinterpret_cast<const float4*>(xbuf + row * 24);
+      if (i < N) {
+        const float4* xr = reinterpret_cast<const float4*>(xbuf + i * 24);
 #pragma unroll
         for (int q = 0; q < 6; q++) {
           const float4 v = xr[q];
@@ -214,10 +212,9 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
       }
       sx = pow2_scale(warp_max(amx));
       sz = pow2_scale(2.f * warp_max(dmx));  // |z| <= 2 max|d|
-      {
+      if (i < N) {
         const float2 sx2 = f2(sx), sz2 = f2(sz), nx0 = f2(-x0), nm1 = f2(-m1);
         float2 q2 = f2(0.f);
-        const bool own = i < N;   // rows >= N of the operand tiles stay zero
 #pragma unroll
         for (int q = 0; q < 3; q++) {
           uint4 xh, xl, zh, zl;
@@ -234,12 +231,10 @@ __global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLay
             split2(mul2(v, sx2), pxh[u], pxl[u]);
             split2(mul2(z, sz2), pzh[u], pzl[u]);
           }
-          if (own) {
-            *reinterpret_cast<uint4*>(x_hi + i * 24 + 8 * q) = xh;
-            *reinterpret_cast<uint4*>(x_lo + i * 24 + 8 * q) = xl;
-            *reinterpret_cast<uint4*>(z_hi + i * 24 + 8 * q) = zh;
-            *reinterpret_cast<uint4*>(z_lo + i * 24 + 8 * q) = zl;
-          }
+          *reinterpret_cast<uint4*>(x_hi + i * 24 + 8 * q) = xh;
+          *reinterpret_cast<uint4*>(x_lo + i * 24 + 8 * q) = xl;
+          *reinterpret_cast<uint4*>(z_hi + i * 24 + 8 * q) = zh;
+          *reinterpret_cast<uint4*>(z_lo + i * 24 + 8 * q) = zl;
         }
         nu2 = q2.x + q2.y;
       }

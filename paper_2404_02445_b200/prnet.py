@@ -46,7 +46,7 @@ def load_library(path: str | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = path or _LIB_PATH
+    p = path or os.environ.get("PRNET_LIB") or _LIB_PATH   # PRNET_LIB: A/B a second build
     if not os.path.exists(p):
         raise ImportError(f"{p} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
     lib = ctypes.CDLL(p)
