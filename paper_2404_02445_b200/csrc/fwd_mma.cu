@@ -33,6 +33,13 @@
 
 #include "mma_common.cuh"
 
+#ifndef PRNET_MMA_THREADS
+#define PRNET_MMA_THREADS 256
+#endif
+#ifndef PRNET_MMA_MINB
+#define PRNET_MMA_MINB 2
+#endif
+
 namespace prnet {
 
 
@@ -66,7 +73,7 @@ __host__ __device__ constexpr MmaOffsets mma_offsets(int nr, int S, int sph, int
 }
 
 template <int MT, int MMT, int SC, bool DBG, int NC = 0>
-__global__ void __launch_bounds__(256, 2) prnet_fwd_mma_kernel(FwdArgs a, MmaLayout ly,
+__global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_mma_kernel(FwdArgs a, MmaLayout ly,
                                                                int wins_per_cta) {
   extern __shared__ float4 smem4[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(smem4);
@@ -628,7 +635,7 @@ bool plan_mma_kernel(const FwdArgs& a, int max_smem_optin, MmaPlan* p) {
   ly.wpack_bytes = o.wpack;
   ly.off_bias = -1;  // after the per-warp regions (depends on warps per CTA)
   ly.shared_bytes = o.wpack;
-  p->warps_per_cta = 8;
+  p->warps_per_cta = PRNET_MMA_THREADS / 32;
   auto total = [&](int w) { return (size_t)o.wpack + (size_t)w * o.pw + (size_t)a.H * 4; };
   while (total(p->warps_per_cta) > (size_t)max_smem_optin && p->warps_per_cta > 1)
     p->warps_per_cta >>= 1;
