@@ -409,7 +409,10 @@ bool plan_flash_kernel(const FwdArgs& a, int max_smem_optin, FlashPlan* p) {
   off += 5 * ly.npad * 4;
   off = (off + 15) & ~15;
   ly.off_yred = off;
-  p->warps = 8;
+  // one warp per 16-row query tile, up to 8: short series (N <= 64) run 4-warp CTAs so
+  // two of them share an SM instead of leaving half an 8-warp CTA idle
+  const int nt = ly.npad / 16;
+  p->warps = nt >= 8 ? 8 : (nt >= 4 ? 4 : 2);
   off += p->warps * (16 * p->mmt) * (8 * p->ntt) * 4;
   ly.off_scr = off;
   off += 32 * 4;
