@@ -196,6 +196,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no extras)")
     ap.add_argument("--variant", default=None, help="force a kernel variant (tuning)")
+    ap.add_argument("--host-chunk", type=int, default=0,
+                    help="windows per chunk of the host-buffer pipeline (0 = library default)")
     args = ap.parse_args()
 
     rank, world, local = dist_env()
@@ -299,7 +301,7 @@ def main():
             xh = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
             xh.copy_(x)
             yh = torch.empty(y.shape, dtype=torch.float32, pin_memory=True)
-            model.forward_host(xh, yh)          # warm-up (allocates the staging ring)
+            model.forward_host(xh, yh, chunk_windows=args.host_chunk or None)   # warm-up
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()

@@ -1,0 +1,30 @@
+"""Small forwards of every kernel variant, for compute-sanitizer (memcheck / racecheck /
+synccheck / initcheck).  Usage: compute-sanitizer --tool memcheck python tools/sanitize.py"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+from paper_2404_02445_b200 import PRNet  # noqa: E402
+
+CASES = [  # (L, S, H, variants)
+    (720, 24, 720, ["mma_f16x3", "tc_fold", "tc_full", "warp_f32"]),
+    (96, 24, 96, ["mma_f16x3", "tc_full", "warp_f32"]),
+    (97, 7, 13, ["mma_f16x3", "warp_f32", "long_f32"]),
+    (1440, 24, 96, ["flash_f16x3", "long_f32"]),
+    (1440, 12, 100, ["flash_f16x3"]),
+]
+for L, S, H, variants in CASES:
+    x = torch.from_numpy(synth.random_windows(5, 3, L)).cuda()
+    N, _, M = synth.derived_dims(L, S, H)
+    ws, wt, b = synth.make_params(3, M, N, H)
+    for v in variants:
+        m = PRNet(3, L, S, H).load(ws, wt, b).set_variant(v)
+        y = m.forward(x)
+        torch.cuda.synchronize()
+        assert torch.isfinite(y).all(), (L, S, H, v)
+        print("ok", L, S, H, v, flush=True)
+print("sanitize cases done")
