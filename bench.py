@@ -237,9 +237,20 @@ def main():
     import torch.distributed as dist
     from paper_2404_02445_b200 import PRNet, all_reduce_error_sums, shard_windows
 
-    torch.cuda.set_device(local)
+    # one process per GPU; NCCL for the collectives.  (world > GPUs only happens in the
+    # single-GPU multi-rank smoke test: ranks then share a device and collectives use gloo
+    # on host tensors -- a functional check of the sharding/reduction path, not a timing.)
+    ndev = torch.cuda.device_count()
+    dev = local % ndev
+    torch.cuda.set_device(dev)
+    use_nccl = world > 1 and ndev >= world
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if use_nccl:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
+    coll = "cuda" if (use_nccl or world == 1) else "cpu"
+    cfg["collectives"] = "nccl" if use_nccl else ("gloo (shared-GPU smoke test)" if world > 1 else "none")
     start, count = shard_windows(B, world, rank)
     peaks, peak_src = measured_peaks()
 
@@ -251,7 +262,7 @@ def main():
         .permute(1, 0, 2).contiguous()
     del sd
     ws, wt, b = synth.make_params(w.C, M, N, w.H, True, args.seed, w.cfg_id)
-    model = PRNet(w.C, w.L, w.S, w.H, device=local).load(ws, wt, b)
+    model = PRNet(w.C, w.L, w.S, w.H, device=dev).load(ws, wt, b)
     if args.variant:
         model.set_variant(args.variant)
     y = torch.empty((count, w.C, w.H), dtype=torch.float32, device="cuda")
@@ -266,7 +277,7 @@ def main():
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         t_wall = time.perf_counter()
         for e0, e1 in ev:
             e0.record(stream)
@@ -279,14 +290,14 @@ def main():
     torch.cuda.synchronize()
     per_launch = [e0.elapsed_time(e1) for e0, e1 in ev]          # ms, on the launching stream
     total_ms = ev[0][0].elapsed_time(ev[-1][1])
-    tt = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    tt = torch.tensor([total_ms], dtype=torch.float64, device=coll)
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     total_ms_max = float(tt.item())
     ms_per_step = total_ms_max / args.steps
 
     # ---- accuracy metric of this forward (K6 error sums + the one NCCL all-reduce)
-    sums = model.error_sums(y, tgt)
+    sums = model.error_sums(y, tgt).to(coll)
     mse, mae = all_reduce_error_sums(sums)
 
     if args.profile:
@@ -308,7 +319,7 @@ def main():
             for _ in range(args.e2e_steps):
                 model.forward_host(xh, yh)
             dt = torch.tensor([(time.perf_counter() - t0) / args.e2e_steps], dtype=torch.float64,
-                              device="cuda")
+                              device=coll)
             if world > 1:
                 dist.all_reduce(dt, op=dist.ReduceOp.MAX)
             assert torch.equal(yh, y.cpu()), "host path disagrees with the device path"
