@@ -150,6 +150,24 @@ def test_temperatures_and_head_modes(oracle_mod, tau, hpc, variant):
     _check_small(oracle_mod, x, 24, 336, hpc=hpc, tau_s=tau, tau_t=tau * 0.7, variant=variant)
 
 
+@pytest.mark.parametrize("tau", [0.05, 1.0, 10.0])
+@pytest.mark.parametrize("hpc", [True, False])
+@pytest.mark.parametrize("L,S,H", [(1440, 24, 96), (1536, 12, 200), (2880, 48, 96)])
+def test_long_lookback_temperatures_and_head_modes(oracle_mod, L, S, H, tau, hpc):
+    """The long-N (flash) path under both head modes and several temperatures."""
+    x = synth.random_windows(2, 3, L, kind="mixed")
+    _check_small(oracle_mod, x, S, H, hpc=hpc, tau_s=tau, tau_t=tau * 0.7)
+
+
+@pytest.mark.parametrize("variant", [None, "flash_f16x3", "long_f32"])
+@pytest.mark.parametrize("kind", ["normal", "constant", "scaled"])
+def test_long_lookback_value_distributions(oracle_mod, kind, variant):
+    x = synth.random_windows(2, 3, 1440, kind=kind)
+    scale = np.abs(x).max(axis=2, keepdims=True)[..., :1] if kind == "scaled" else None
+    scale = None if scale is None else np.maximum(scale, 1.0)
+    _check_small(oracle_mod, x, 24, 96, scale=scale, variant=variant)
+
+
 @pytest.mark.parametrize("variant", VARIANTS[:5])
 @pytest.mark.parametrize("kind", ["normal", "constant", "scaled"])
 @pytest.mark.parametrize("L,S", [(720, 24), (1440, 24)])
