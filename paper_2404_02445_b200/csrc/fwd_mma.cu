@@ -45,10 +45,11 @@ namespace prnet {
 
 // Shared-memory layout, identical on host (plan) and device (compile-time for SC = 24):
 // [W' hi | W' lo]  [per-warp regions x nwarps]  [bias fp32 [H]]
-// per-warp: xbuf fp32 [nr*S] | X' hi, lo [nr][sph] | Z' hi, lo [nr][zph] | misc (diag[32],
-// x0/m1[64], mbarrier)
+// per-warp: xbuf fp32 [nr*S] | X' hi, lo [nr][sph] | Z' hi, lo [nr][zph] | misc (row
+// descriptors float4[32], x0/m1[64], mbarrier)
 struct MmaOffsets {
   int xhi, xlo, zhi, zlo, misc, pw;   // per-warp
+  int zhi_bytes;                      // bytes of one Z' plane (Z' hi, lo are contiguous)
   int wlo, wpack;                     // CTA-shared head
 };
 __host__ __device__ constexpr int r16(int v) { return (v + 15) & ~15; }
@@ -60,11 +61,12 @@ __host__ __device__ constexpr MmaOffsets mma_offsets(int nr, int S, int sph, int
   o.xlo = off;
   off = r16(off + nr * sph * 2);
   o.zhi = off;
+  o.zhi_bytes = r16(nr * zph * 2);
   off = r16(off + nr * zph * 2);
   o.zlo = off;
   off = r16(off + nr * zph * 2);
   o.misc = off;
-  off += 96 * 4 + 16;
+  off += 512 + 256 + 16;
   o.pw = (off + 127) & ~127;
   const int wph = 2 * nr + 8, rows = 16 * mmt;
   o.wlo = rows * wph * 2;
@@ -117,15 +119,16 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
   __half* x_lo = reinterpret_cast<__half*>(wb + (SC > 0 ? KO.xlo : ly.off_xlo));
   __half* z_hi = reinterpret_cast<__half*>(wb + (SC > 0 ? KO.zhi : ly.off_zhi));
   __half* z_lo = reinterpret_cast<__half*>(wb + (SC > 0 ? KO.zlo : ly.off_zlo));
-  float* dsm = reinterpret_cast<float*>(wb + (SC > 0 ? KO.misc : ly.off_diag));  // [32] diag
-  float* rsm = dsm + 32;                                      // [64] x0, m1 per row
-  uint64_t* xbar = reinterpret_cast<uint64_t*>(dsm + 96);     // TMA completion barrier
+  // per-row descriptors (mu~, kappa~, 1/sqrt(nu2 + eps_s), f) broadcast through shared memory
+  float4* dsc = reinterpret_cast<float4*>(wb + (SC > 0 ? KO.misc : ly.off_diag));
+  float* rsm = reinterpret_cast<float*>(dsc + 32);            // [64] x0, m1 per row
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(rsm + 64);     // TMA completion barrier
   if (lane == 0) mbar_init(xbar, 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   {
     // zero the fp16 operand tiles once: padding rows (>= N) and columns (>= S) stay 0
     uint32_t* p = reinterpret_cast<uint32_t*>(x_hi);
-    const int words = (int)(reinterpret_cast<unsigned char*>(dsm) -
+    const int words = (int)(reinterpret_cast<unsigned char*>(dsc) -
                             reinterpret_cast<unsigned char*>(x_hi)) / 4;
     for (int k = lane; k < words; k += 32) p[k] = 0u;
   }
@@ -135,6 +138,9 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
   const int NS = N * S;
   // one bulk TMA per series when its segmented span is 16-byte aligned and sized
   const bool bulk = vec_x && ((NS & 3) == 0);
+  // S = 24: the output row is staged in the Z' region (free after the Gram) and written
+  // by one 1-D TMA bulk store when it is whole float4s (y is 16-byte aligned by contract)
+  const bool bstore = SC == 24 && (H & 3) == 0 && H * 4 <= 2 * KO.zhi_bytes;
   uint32_t xphase = 0;
   const int64_t b_begin = (int64_t)blockIdx.x * wins_per_cta;
   int64_t b_end = b_begin + wins_per_cta;
@@ -217,8 +223,12 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
         mu = x0 + m1;
         kap = (s3.x + s3.y) * a.inv_v;
       }
-      sx = pow2_scale(warp_max(amx));
-      sz = pow2_scale(2.f * warp_max(dmx));  // |z| <= 2 max|d|
+      sx = pow2_scale(warp_max_nonneg(amx));
+      sz = pow2_scale(2.f * warp_max_nonneg(dmx));  // |z| <= 2 max|d|
+      if (bstore) {  // the previous series' output store has left the Z' region
+        if (lane == 0) bulk_wait_read();
+        __syncwarp();
+      }
       if (i < N) {
         const float2 sx2 = f2(sx), sz2 = f2(sz), nx0 = f2(-x0), nm1 = f2(-m1);
         float2 q2 = f2(0.f);
@@ -244,6 +254,13 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
           *reinterpret_cast<uint4*>(z_lo + i * 24 + 8 * q) = zl;
         }
         nu2 = q2.x + q2.y;
+      } else if (bstore && i < NR) {
+        // padding rows of Z' must read 0 in the Gram: the output staging overwrote them
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+          *reinterpret_cast<uint4*>(z_hi + i * 24 + 8 * q) = make_uint4(0u, 0u, 0u, 0u);
+          *reinterpret_cast<uint4*>(z_lo + i * 24 + 8 * q) = make_uint4(0u, 0u, 0u, 0u);
+        }
       }
       __syncwarp();
     } else {
@@ -278,8 +295,8 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
           nu2 = fmaf(z, z, nu2);
         }
       }
-      sx = pow2_scale(warp_max(amx));
-      sz = pow2_scale(2.f * warp_max(dmx));
+      sx = pow2_scale(warp_max_nonneg(amx));
+      sz = pow2_scale(2.f * warp_max_nonneg(dmx));
       rsm[lane] = x0;        // per-row shift and mean for the coalesced pass (no shuffles in
       rsm[32 + lane] = m1;   // its lane-divergent loop)
       __syncwarp();
@@ -304,6 +321,19 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
     const float mbar = warp_sum(i < N ? mu : 0.f) * a.inv_n;
     const float dv = i < N ? nu2 + (float)S * (mu - mbar) * (mu - mbar) : 0.f;
     const float inv_var = 1.0f / (warp_sum(dv) * a.inv_ns + kEpsTrend);
+    {
+      // trend: mu~ = mu sqrt(inv_var kt), k~ = kappa sqrt(vtrend inv_var kt) (Def 7-8);
+      // seasonal: inv = 1/sqrt(nu2 + eps_s) (Def 6) and the known row maximum f = nu inv:
+      // rho_ij <= f_i f_j <= f_i (Cauchy-Schwarz), rho_ii = f_i^2 within f_i (1 - f_i) <= 1/4
+      // of it, so exp((rho_ij - f_i) / tau_s) never overflows and its largest term never
+      // underflows for tau_s > 0.003; softmax is shift-invariant, so this is the same result
+      // as subtracting the searched max (Def 8).
+      const float cm = sqrtf(inv_var * a.kt), ck = sqrtf(a.vtrend * inv_var * a.kt);
+      const float inv = rsqrtf(nu2 + kEpsSeasonal);
+      dsc[lane] = i < N ? make_float4(mu * cm, kap * ck, inv, sqrtf(nu2) * inv)
+                        : make_float4(0.f, 0.f, 1.f, 0.f);
+      __syncwarp();
+    }
 
     float qa[MMT][2 * MT][4];  // Q' = sw (W_s A_s + W_t A_t)
 #pragma unroll
@@ -317,15 +347,13 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
     // D_ii = 0) = -(mu~_i - mu~_j)^2 - (k~_i - k~_j)^2 with mu~ = mu sqrt(inv_var kt),
     // k~ = kappa sqrt(vtrend inv_var kt) (Def 7-8); then fold Q' += W'_t A_t per k-tile
     {
-      const float cm = sqrtf(inv_var * a.kt), ck = sqrtf(a.vtrend * inv_var * a.kt);
-      const float mus = i < N ? mu * cm : 0.f, kas = i < N ? kap * ck : 0.f;
       float2 cmu[2 * MT], ckap[2 * MT];
 #pragma unroll
       for (int nt = 0; nt < 2 * MT; nt++) {
         const int j = 8 * nt + 2 * cq;
-        const float m0 = __shfl_sync(0xffffffffu, mus, j), m1v = __shfl_sync(0xffffffffu, mus, j + 1);
-        cmu[nt] = make_float2(j < N ? -m0 : -INFINITY, j + 1 < N ? -m1v : -INFINITY);
-        ckap[nt] = make_float2(-__shfl_sync(0xffffffffu, kas, j), -__shfl_sync(0xffffffffu, kas, j + 1));
+        const float4 d0 = dsc[j], d1 = dsc[j + 1];
+        cmu[nt] = make_float2(j < N ? -d0.x : -INFINITY, j + 1 < N ? -d1.x : -INFINITY);
+        ckap[nt] = make_float2(-d0.y, -d1.y);
       }
 #pragma unroll
       for (int mt = 0; mt < MT; mt++) {
@@ -333,8 +361,8 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           const int ii = 16 * mt + 8 * h + gq;
-          const float2 mui = f2(__shfl_sync(0xffffffffu, mus, ii));
-          const float2 ki = f2(__shfl_sync(0xffffffffu, kas, ii));
+          const float4 di = dsc[ii];
+          const float2 mui = f2(di.x), ki = f2(di.y);
           float2 u[2 * MT];
           float2 sum2 = f2(0.f);
 #pragma unroll
@@ -347,7 +375,7 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
           float sum = sum2.x + sum2.y;
           sum += __shfl_xor_sync(0xffffffffu, sum, 1);
           sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-          const float2 rs2 = f2(ii < N ? 1.f / sum : 0.f);
+          const float2 rs2 = f2(ii < N ? fast_rcp(sum) : 0.f);
 #pragma unroll
           for (int nt = 0; nt < 2 * MT; nt++) {
             const float2 p = mul2(u[nt], rs2);
@@ -373,18 +401,12 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
     // Gram rows G'[16 mt .. 16 mt + 15][:] = Z' Z'^T (= sz^2 G), rho_ij = G'_ij inv_i inv_j / sz^2
     // with inv = 1/sqrt(nu2 + eps_s) (Def 6), row softmax on the fragments, fold Q' += W'_s A_s
     {
-      const float inv = i < N ? rsqrtf(nu2 + kEpsSeasonal) : 1.f;
-      // Known row maximum: rho_ij <= f_i f_j <= f_i with f = nu / sqrt(nu2 + eps_s) (Cauchy-
-      // Schwarz), and rho_ii = f_i^2 is within f_i (1 - f_i) <= 1/4 of it, so exp((rho_ij -
-      // f_i) / tau_s) never overflows and its largest term never underflows for tau_s > 0.003.
-      // Softmax is shift-invariant: same result as subtracting the searched max (Def 8).
-      const float cself = i < N ? sqrtf(nu2) * inv : 0.f;
       const float ks_z = a.ks / (sz * sz);
       float2 cinv[2 * MT], cmask[2 * MT];
 #pragma unroll
       for (int nt = 0; nt < 2 * MT; nt++) {
         const int j = 8 * nt + 2 * cq;
-        cinv[nt] = make_float2(__shfl_sync(0xffffffffu, inv, j), __shfl_sync(0xffffffffu, inv, j + 1));
+        cinv[nt] = make_float2(dsc[j].z, dsc[j + 1].z);
         cmask[nt] = make_float2(j < N ? 0.f : -INFINITY, j + 1 < N ? 0.f : -INFINITY);
       }
       const int k16 = SC > 0 ? (SC / 16) * 16 : ly.kz;
@@ -444,12 +466,13 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           const int ii = 16 * mt + 8 * h + gq;
-          const float rk = __shfl_sync(0xffffffffu, inv, ii) * ks_z;
+          const float4 di = dsc[ii];
+          const float rk = di.z * ks_z;
           float2 u[2 * MT];
 #pragma unroll
           for (int nt = 0; nt < 2 * MT; nt++)
             u[nt] = fma2(make_float2(g[nt][2 * h], g[nt][2 * h + 1]), cinv[nt], cmask[nt]);
-          const float2 rk2 = f2(rk), nb2 = f2(-__shfl_sync(0xffffffffu, cself, ii) * a.ks);
+          const float2 rk2 = f2(rk), nb2 = f2(-di.w * a.ks);
           float2 sum2 = f2(0.f);
 #pragma unroll
           for (int nt = 0; nt < 2 * MT; nt++) {
@@ -460,7 +483,7 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
           float sum = sum2.x + sum2.y;
           sum += __shfl_xor_sync(0xffffffffu, sum, 1);
           sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-          const float2 rs2 = f2(ii < N ? 1.f / sum : 0.f);
+          const float2 rs2 = f2(ii < N ? fast_rcp(sum) : 0.f);
 #pragma unroll
           for (int nt = 0; nt < 2 * MT; nt++) {
             const float2 p = mul2(u[nt], rs2);
@@ -487,6 +510,7 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
     const float2 ys2 = f2(inv_sw / sx);
     const bool pair_store = ((S | H) & 1) == 0;   // t, hh even -> 8-byte aligned pairs
     float* yg = a.y + series * H;
+    float* ystage = reinterpret_cast<float*>(z_hi);
 #pragma unroll
     for (int mm = 0; mm < MMT; mm++) {
       if (16 * mm >= M) break;
@@ -540,7 +564,11 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
             if (m < M && t < S) {
               const int hh = m * S + t;
               const float2 v = mul2(make_float2(ya[nt][2 * h], ya[nt][2 * h + 1]), ys2);
-              if (pair_store) {  // hh even, H even: hh < H implies hh + 1 < H
+              if (bstore) {  // H % 4 == 0, hh even: hh < H implies hh + 1 < H
+                if (hh >= H) continue;
+                *reinterpret_cast<float2*>(ystage + hh) =
+                    add2(v, *reinterpret_cast<const float2*>(bS + hh));
+              } else if (pair_store) {  // hh even, H even: hh < H implies hh + 1 < H
                 if (hh >= H) continue;
                 const float2 o = add2(v, *reinterpret_cast<const float2*>(bS + hh));
                 asm volatile("st.global.cs.v2.f32 [%0], {%1,%2};" ::"l"(yg + hh), "f"(o.x),
@@ -555,8 +583,14 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
         }
       }
     }
+    if (bstore) {
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) bulk_store(yg, ystage, (uint32_t)H * 4u);
+    }
   }
   cp_async_wait_all();
+  if (bstore && lane == 0) bulk_wait_all();
 }
 
 int mma_wpack_bytes(int N, int M) {

@@ -41,15 +41,21 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
 }
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
-// v = hi + lo with hi = fp16(v), lo = fp16(v - hi), packed as half2 pairs
-__device__ __forceinline__ float2 add2(float2 a, float2 b);
+// v = hi + lo with hi = fp16(v), lo = fp16(v - hi), packed as half2 pairs.  v - hi is
+// formed by the sm_100 mixed-precision FMA (f16 x f16 + f32 -> f32, SASS FHFMA) as
+// hi * -1 + v: exact (v - hi fits in fp32), one instruction per element instead of an
+// f16 -> f32 unpack plus a subtract.
 __device__ __forceinline__ void split2(float2 v, uint32_t& hi, uint32_t& lo) {
-  const __half2 h = __floats2half2_rn(v.x, v.y);
-  const float2 hf = __half22float2(h);
-  const float2 d = add2(v, make_float2(-hf.x, -hf.y));
-  const __half2 l = __floats2half2_rn(d.x, d.y);
-  hi = *reinterpret_cast<const uint32_t*>(&h);
-  lo = *reinterpret_cast<const uint32_t*>(&l);
+  asm("{.reg .b16 h0, h1, m1; .reg .b32 hh; .reg .f32 d0, d1;\n\t"
+      "cvt.rn.f16x2.f32 hh, %3, %2;\n\t"
+      "mov.b32 {h0, h1}, hh;\n\t"
+      "mov.b16 m1, 0xBC00;\n\t"
+      "fma.rn.f32.f16 d0, h0, m1, %2;\n\t"
+      "fma.rn.f32.f16 d1, h1, m1, %3;\n\t"
+      "cvt.rn.f16x2.f32 %1, d1, d0;\n\t"
+      "mov.b32 %0, hh;}"
+      : "=r"(hi), "=r"(lo)
+      : "f"(v.x), "f"(v.y));
 }
 __device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
   split2(make_float2(a, b), hi, lo);
@@ -130,6 +136,24 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// ---- 1-D TMA bulk copy shared -> global (bulk-group completion)
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// the issuing thread's bulk stores have finished reading shared memory
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+// make this thread's generic-proxy shared-memory writes visible to the async proxy (TMA)
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n.reg .pred p;\nWAIT_%=:\n"
@@ -139,12 +163,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// 2^-e with max|v| * 2^-e in [0.5, 1): exact power-of-two scale (1 for v == 0).
+// 2^-e with max|v| * 2^-e in [0.5, 1): exact power-of-two scale (1 for v == 0 or
+// non-finite).  From the exponent bits: maxabs in [2^(E-127), 2^(E-126)) -> 2^(126-E),
+// clamped to a normal float (maxabs >= 2^126 gets 2^-126; denormal maxabs gets 2^126).
 __device__ __forceinline__ float pow2_scale(float maxabs) {
-  if (!(maxabs > 0.f) || !isfinite(maxabs)) return 1.f;
-  int e;
-  frexpf(maxabs, &e);
-  return ldexpf(1.f, -e);
+  const uint32_t u = __float_as_uint(maxabs);   // maxabs >= 0
+  const uint32_t E = min(u >> 23, 252u);
+  return (u == 0u || u >= 0x7f800000u) ? 1.f : __uint_as_float((253u - E) << 23);
+}
+
+// max over the warp of a non-negative float: non-negative IEEE floats order like their
+// bit patterns, so one integer redux (REDUX) replaces a 5-step shuffle tree.
+__device__ __forceinline__ float warp_max_nonneg(float v) {
+  uint32_t r;
+  asm volatile("redux.sync.max.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(__float_as_uint(v)));
+  return __uint_as_float(r);
+}
+
+// 1/v via MUFU.RCP (approximate, <= 1 ulp; v a normal softmax row sum >= 2^-126)
+__device__ __forceinline__ float fast_rcp(float v) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
 }
 
 }  // namespace mmah
