@@ -109,7 +109,8 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
     uint4* dst = reinterpret_cast<uint4*>(smem);
     for (int k = threadIdx.x; k < KO.wpack / 16; k += blockDim.x) dst[k] = __ldg(src + k);
     const float* gb = a.bias + (int64_t)cw * H;
-    for (int k = threadIdx.x; k < H; k += blockDim.x) bS[k] = __ldg(gb + k);
+    const int hb = max(H, 16 * MMT * S);   // zero-padded to the epilogue's whole tiles
+    for (int k = threadIdx.x; k < hb; k += blockDim.x) bS[k] = k < H ? __ldg(gb + k) : 0.f;
   }
 
   // ---------------- per-warp: fp32 staging, X' hi/lo [NR][sph], Z' hi/lo [NR][zph]
@@ -131,6 +132,10 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
     const int words = (int)(reinterpret_cast<unsigned char*>(dsc) -
                             reinterpret_cast<unsigned char*>(x_hi)) / 4;
     for (int k = lane; k < words; k += 32) p[k] = 0u;
+    // S = 24: fp32 staging rows >= N are never loaded and stay 0, so the descriptor phase
+    // runs on all lanes without a branch (padding rows give zero X', Z' rows)
+    if (SC == 24)
+      for (int k = N * S + lane; k < NR * S; k += 32) xbuf[k] = 0.f;
   }
   __syncthreads();
 
@@ -140,7 +145,8 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
   const bool bulk = vec_x && ((NS & 3) == 0);
   // S = 24: the output row is staged in the Z' region (free after the Gram) and written
   // by one 1-D TMA bulk store when it is whole float4s (y is 16-byte aligned by contract)
-  const bool bstore = SC == 24 && (H & 3) == 0 && H * 4 <= 2 * KO.zhi_bytes;
+  // (the epilogue writes whole 16-row tiles there: rows >= M land past H and are not stored)
+  const bool bstore = SC == 24 && (H & 3) == 0 && 16 * MMT * SC * 4 <= 2 * KO.zhi_bytes;
   uint32_t xphase = 0;
   const int64_t b_begin = (int64_t)blockIdx.x * wins_per_cta;
   int64_t b_end = b_begin + wins_per_cta;
@@ -200,7 +206,8 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
       float xv[24];
       float2 s1 = f2(0.f), s3 = f2(0.f);
       float amx = 0.f, dmx = 0.f;
-      if (i < N) {
+      const bool row_ok = MT == 2 || i < NR;   // lanes past NR own no row (MT = 1)
+      if (row_ok) {
         const float4* xr = reinterpret_cast<const float4*>(xbuf + i * 24);
 #pragma unroll
         for (int q = 0; q < 6; q++) {
@@ -229,7 +236,7 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
         if (lane == 0) bulk_wait_read();
         __syncwarp();
       }
-      if (i < N) {
+      if (row_ok) {
         const float2 sx2 = f2(sx), sz2 = f2(sz), nx0 = f2(-x0), nm1 = f2(-m1);
         float2 q2 = f2(0.f);
 #pragma unroll
@@ -254,13 +261,6 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
           *reinterpret_cast<uint4*>(z_lo + i * 24 + 8 * q) = zl;
         }
         nu2 = q2.x + q2.y;
-      } else if (bstore && i < NR) {
-        // padding rows of Z' must read 0 in the Gram: the output staging overwrote them
-#pragma unroll
-        for (int q = 0; q < 3; q++) {
-          *reinterpret_cast<uint4*>(z_hi + i * 24 + 8 * q) = make_uint4(0u, 0u, 0u, 0u);
-          *reinterpret_cast<uint4*>(z_lo + i * 24 + 8 * q) = make_uint4(0u, 0u, 0u, 0u);
-        }
       }
       __syncwarp();
     } else {
@@ -555,6 +555,21 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
             if (two) mma16816(ya[2 * tp + 1], qh[kj], xh[2], xh[3]);
           }
         }
+        if (bstore) {
+          // whole tiles into the staging row (bias zero-padded): no masks, no branches
+#pragma unroll
+          for (int nt = 0; nt < (SC + 7) / 8; nt++) {
+            if (nt >= 4) break;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              const int hh = (16 * mm + 8 * h + gq) * SC + 8 * (t0 + nt) + 2 * cq;
+              const float2 v = mul2(make_float2(ya[nt][2 * h], ya[nt][2 * h + 1]), ys2);
+              *reinterpret_cast<float2*>(ystage + hh) =
+                  add2(v, *reinterpret_cast<const float2*>(bS + hh));
+            }
+          }
+          continue;
+        }
 #pragma unroll
         for (int nt = 0; nt < 4; nt++) {
           const int t = 8 * (t0 + nt) + 2 * cq;
@@ -564,11 +579,7 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
             if (m < M && t < S) {
               const int hh = m * S + t;
               const float2 v = mul2(make_float2(ya[nt][2 * h], ya[nt][2 * h + 1]), ys2);
-              if (bstore) {  // H % 4 == 0, hh even: hh < H implies hh + 1 < H
-                if (hh >= H) continue;
-                *reinterpret_cast<float2*>(ystage + hh) =
-                    add2(v, *reinterpret_cast<const float2*>(bS + hh));
-              } else if (pair_store) {  // hh even, H even: hh < H implies hh + 1 < H
+              if (pair_store) {  // hh even, H even: hh < H implies hh + 1 < H
                 if (hh >= H) continue;
                 const float2 o = add2(v, *reinterpret_cast<const float2*>(bS + hh));
                 asm volatile("st.global.cs.v2.f32 [%0], {%1,%2};" ::"l"(yg + hh), "f"(o.x),
@@ -670,7 +681,8 @@ bool plan_mma_kernel(const FwdArgs& a, int max_smem_optin, MmaPlan* p) {
   ly.off_bias = -1;  // after the per-warp regions (depends on warps per CTA)
   ly.shared_bytes = o.wpack;
   p->warps_per_cta = PRNET_MMA_THREADS / 32;
-  auto total = [&](int w) { return (size_t)o.wpack + (size_t)w * o.pw + (size_t)a.H * 4; };
+  const int hb = a.H > 16 * p->mmt * a.S ? a.H : 16 * p->mmt * a.S;  // zero-padded bias
+  auto total = [&](int w) { return (size_t)o.wpack + (size_t)w * o.pw + (size_t)hb * 4; };
   while (total(p->warps_per_cta) > (size_t)max_smem_optin && p->warps_per_cta > 1)
     p->warps_per_cta >>= 1;
   p->smem_bytes = total(p->warps_per_cta);
