@@ -1,0 +1,511 @@
+// fwd_tcq.cu -- fused PRNet pattern-attention forward, "tc_quad" variant: every
+// contraction on the 5th-gen tensor cores (tcgen05.mma, TMEM accumulators), every
+// element-wise step lane-per-row on the CUDA cores; S = 24, N <= 32, M <= 32.
+//
+// Same reading (SURVEY §8(c) Definition steps 1-11) and split-fp16
+// 3-product arithmetic as the other variants.  What is different is the
+// work decomposition, chosen to minimise CUDA-core instructions and shared-memory
+// traffic per series:
+//
+//  * a CTA holds 4 groups of 4 warps; a group processes a QUAD of 4 series (4
+//    consecutive windows of one channel) per round, warp s <-> series s <-> TMEM lanes
+//    32s..32s+31, lane i <-> segment i.  No shuffles in the softmaxes, compile-time
+//    column masks (N = 30 instantiation), no fragment bookkeeping.
+//  * the seasonal Gram is taken of the row-NORMALISED centred segments
+//    zhat_i = z_i / sqrt(nu2_i + eps_s), so the tensor core returns rho_ij itself
+//    (Def 6 regrouped: <z_i, z_j> inv_i inv_j = <z_i inv_i, z_j inv_j>); |zhat| <= 1, so
+//    no fp16 range scale is needed for it.
+//  * the fold needs the attention TRANSPOSED (M = column j, K = row i) as its A operand.
+//    Both logit matrices are symmetric (rho_ij = rho_ji; Dhat_ij = Dhat_ji), so lane j
+//    computing "its" logit row ell_j. also holds column j; only the row-dependent
+//    normalisers must be exchanged (one 32-float vector per branch through shared
+//    memory).  Trend: A_t[i][j] = E_ji / l_i with E = 2^(-Dhat kt) (shift 0 = the row max,
+//    attained at j = i) and l_i = sum_j E_ij.  Seasonal: the same with the symmetric
+//    E_ij = 2^((rho_ij - 1) ks), i.e. the shift 1 >= rho_ij (|rho| <= 1) for every row;
+//    softmax is shift-invariant (Def 8), E <= 1, and the row maximum rho_ii = f_i^2 keeps
+//    the largest term >= 2^-ks: normal for tau_s >= 1/80.  Each lane writes
+//    its row of A^T (fp16 hi/lo) straight into its own TMEM lane with tcgen05.st, and the
+//    fold reads A from TMEM: no shared-memory tile for the attention at all.
+//  * one 128-column TMEM block per group is reused by every product of a round:
+//      Gram  D[0,128)  = Z' Z'^T                (smem x smem, diagonal blocks used)
+//      A^T         [0,64)  hi_s | hi_t | lo_s | lo_t  (tcgen05.st, after the Gram is read)
+//      fold  D[64,96)  = A^T W'^T  = Q'^T       (tmem x smem, all 128 rows useful)
+//      head  D[0,96)   = Q' [X'_0..X'_3]        (smem x smem, diagonal blocks used)
+//    issued by one elected thread of the group, completion through tcgen05.commit.
+//  * shared memory per group: the Z' tile (K-major; reused as the head's Q' tile), the
+//    head's X' tile (MN-major), 4 TMA staging rows and the column vectors; the
+//    channel's head W' (K-major, packed at load time by pack_tc_head) and bias are
+//    CTA-shared.  4 x 43 KB + 11 KB per CTA, 16 warps per SM.
+//
+// Layouts (byte offsets; core matrix = 8 rows x 16 bytes, no swizzle):
+//   Z' (K-major, row r = 32 s + i, K = t; hi t 0..31 | lo t 0..31, t >= 24 zero):
+//       (r/8)*1024 + (k/8)*128 + (r%8)*16 + (k%8)*2               LBO 128, SBO 1024
+//   Q' (MN-major, M = (s, m), K = j; hi j 0..31 | lo):  (4s + m/8)*1024 + (k/8)*128 +
+//       (k%8)*16 + (m%8)*2                                          LBO 128, SBO 1024
+//   X' (MN-major, N = 24 s + t, K = j; hi | lo): (n/8)*1024 + (k/8)*128 + (k%8)*16 +
+//       (n%8)*2                                                     LBO 128, SBO 1024
+//   W' (K-major, N = m, K: W_s hi i | W_t hi i | W_s lo | W_t lo):
+//       (m/8)*2048 + (k/8)*128 + (m%8)*16 + (k%8)*2                 LBO 128, SBO 2048
+//
+// Numerical domain: tau_s >= 1/80 (prnet_api.cu routes smaller seasonal temperatures to
+// the mma_f16x3 kernel, whose known-max shift covers tau_s > 0.003).
+#include <cuda_fp16.h>
+
+#include <cmath>
+
+#include "tc_common.cuh"
+
+namespace prnet {
+using namespace tcq;
+
+namespace {
+
+constexpr int kQGroups = 4;
+constexpr int kQZQ = 16384;        // Z' tile, then Q' tile
+constexpr int kQXT = 12288;        // X' tile
+constexpr int kQStage = 3072;      // TMA staging per warp: N S fp32, N <= 32, S = 24
+constexpr int kQColW = 160;        // per warp column vectors [5][32] fp32
+constexpr int kQGroup = kQZQ + kQXT + 4 * kQStage + 4 * kQColW * 4;
+constexpr int kQOffW = kQGroups * kQGroup;
+constexpr int kQOffBar = kQOffW + 8192;            // 4 x 3 MMA barriers + 16 TMA barriers
+constexpr int kQOffTmem = kQOffBar + 256;
+constexpr int kQOffBias = kQOffTmem + 16;
+constexpr int kQBiasRow = 28;                      // bias row stride (floats): conflict-free
+constexpr int kQBias = 32 * kQBiasRow;             // bias rows m < 32, zero-padded
+constexpr int kQSmem = kQOffBias + kQBias * 4;
+static_assert(kQGroup % 16 == 0, "16-byte aligned tiles");
+
+constexpr uint32_t kIdGram = idesc_f16(128, 128, false, false);
+constexpr uint32_t kIdFold = idesc_f16(128, 32, false, false);
+constexpr uint32_t kIdHead = idesc_f16(128, 96, true, true);
+
+// 8 consecutive fp32 -> 16-byte fp16 hi and lo rows (v = hi + lo)
+__device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
+  uint32_t* h = reinterpret_cast<uint32_t*>(&hi);
+  uint32_t* l = reinterpret_cast<uint32_t*>(&lo);
+#pragma unroll
+  for (int u = 0; u < 4; u++) split2(make_float2(v[2 * u], v[2 * u + 1]), h[u], l[u]);
+}
+__device__ __forceinline__ void sts128(unsigned char* p, uint4 v) {
+  *reinterpret_cast<uint4*>(p) = v;
+}
+
+}  // namespace
+
+// NC > 0: compile-time segment count (30: every L = 720, S = 24 config) -> no column
+// masks; NC = 0: runtime N <= 32 with masks.
+template <int NC>
+__global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ctas_per_channel) {
+  static_assert(NC % 2 == 0 && NC <= 32, "NC");
+  extern __shared__ __align__(1024) unsigned char smem[];
+  constexpr int S = 24;
+  constexpr int NJ = NC > 0 ? NC : 32;   // columns computed per row
+  const int lane = threadIdx.x & 31;
+  // warp index made provably warp-uniform (shfl from lane 0), so the MMA issue path
+  // below runs on uniform registers without a per-thread waterfall loop
+  const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x >> 5, 0);
+  const int grp = warp >> 2, s = warp & 3;
+  const int c = blockIdx.y;
+  const int cw = a.head_per_channel ? c : 0;
+  const int N = NC > 0 ? NC : a.N;
+  const int M = a.M, H = a.H, L = a.L, C = a.C;
+  const int i = lane;
+  const bool valid = i < N;
+
+  unsigned char* gbase = smem + grp * kQGroup;
+  unsigned char* zq = gbase;
+  unsigned char* xt = gbase + kQZQ;
+  float* xstage = reinterpret_cast<float*>(gbase + kQZQ + kQXT + s * kQStage);
+  // column vectors: [0] mu~, [1] kappa~, [2] 1/l_t, [3] 1/l_s, [4] seasonal mask (NC = 0)
+  float* colv = reinterpret_cast<float*>(gbase + kQZQ + kQXT + 4 * kQStage) + s * kQColW;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kQOffBar);
+  uint64_t* mbar = bars + 3 * grp;                  // +0 Gram, +1 fold, +2 head done
+  uint64_t* xbar = bars + 3 * kQGroups + warp;      // this warp's TMA load
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kQOffTmem);
+  const float* bS = reinterpret_cast<const float*>(smem + kQOffBias);
+
+  // ---------------- prologue: channel head W' and bias, barriers, TMEM.  The operand
+  // tiles need no zero fill: every row an active series reads is written each round
+  // (padding rows / columns with explicit zeros); stale rows of idle slots only reach
+  // discarded off-diagonal blocks and idle rows.
+  {
+    const uint4* src = a.wpack_tc + (int64_t)cw * (8192 / 16);
+    uint4* dst = reinterpret_cast<uint4*>(smem + kQOffW);
+    for (int k = threadIdx.x; k < 8192 / 16; k += blockDim.x) dst[k] = __ldg(src + k);
+    const float* gb = a.bias + (int64_t)cw * H;
+    float* bw = reinterpret_cast<float*>(smem + kQOffBias);
+    for (int k = threadIdx.x; k < kQBias; k += blockDim.x) {
+      const int h = (k / kQBiasRow) * 24 + k % kQBiasRow;
+      bw[k] = (k % kQBiasRow < 24 && h < H) ? __ldg(gb + h) : 0.f;
+    }
+  }
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 3 * kQGroups + 4 * kQGroups; k++) mbar_init(bars + k, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, 512);
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem0 = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  const uint32_t tcol = tmem0 + 128u * (uint32_t)grp;   // the group's 128 columns
+  const uint32_t tlane = (uint32_t)(32 * s) << 16;        // this warp's 32 lanes
+  const bool mma_warp = s == 0;
+  const uint32_t zq_s = smem_u32(zq), xt_s = smem_u32(xt), w_s = smem_u32(smem + kQOffW);
+  const float inv_sw = __ldg(a.wpack_inv_sw + cw);
+
+  // windows of channel c: CTA k of the channel takes [B k / K, B (k+1) / K), split into
+  // near-equal runs of whole quads over the groups
+  const int64_t cb0 = a.B * blockIdx.x / ctas_per_channel;
+  const int64_t cb1 = a.B * (blockIdx.x + 1) / ctas_per_channel;
+  const int64_t quads = (cb1 - cb0 + 3) / 4;
+  const int64_t g0 = cb0 + 4 * (quads * grp / kQGroups);
+  const int64_t g1 = min(cb0 + 4 * (quads * (grp + 1) / kQGroups), cb1);
+  const int rounds = g1 > g0 ? (int)((g1 - g0 + 3) / 4) : 0;
+  const int NS = N * S;
+  const bool bulk = ((L & 3) == 0) && ((a.r & 3) == 0);
+  auto issue_load = [&](int64_t bb) {
+    const float* xg = a.x + (bb * C + c) * L + a.r;
+    if (bulk) {
+      if (lane == 0) bulk_load(xstage, xg, (uint32_t)NS * 4u, xbar);
+    } else {
+      for (int k = lane; k < NS; k += 32) cp_async4(xstage + k, xg + k);
+      cp_async_commit();
+    }
+  };
+
+  uint32_t xph = 0, ph = 0;
+  if (rounds > 0 && g0 + s < g1) issue_load(g0 + s);
+  for (int rd = 0; rd < rounds; rd++) {
+    const int64_t b = g0 + 4 * rd + s;
+    const bool active = b < g1;
+    const int64_t series = b * C + c;
+    float sx = 1.f, mi = 0.f, ki = 0.f;
+
+    // ---------------- a1+a2: segment row i (Def 2) from the TMA staging, descriptors
+    // (Def 4-5) from d = x - x0 (a constant segment gives exact zeros), Z' = z inv and
+    // X' = x sx as fp16 hi/lo rows of the Gram / head operand tiles
+    if (active) {
+      if (bulk) {
+        mbar_wait_bounded(xbar, xph);
+        xph ^= 1u;
+      } else {
+        cp_async_wait_all();
+      }
+      __syncwarp();
+      float xv[24], dv[24];
+      {
+        const float4* xr = reinterpret_cast<const float4*>(xstage + (valid ? i : N - 1) * 24);
+#pragma unroll
+        for (int q = 0; q < 6; q++) {
+          const float4 v = xr[q];
+          xv[4 * q] = v.x;
+          xv[4 * q + 1] = v.y;
+          xv[4 * q + 2] = v.z;
+          xv[4 * q + 3] = v.w;
+        }
+      }
+      __syncwarp();
+      // the staging row is in registers: fetch this warp's next series now
+      if (b + 4 < g1) issue_load(b + 4);
+      const float x0 = xv[0];
+      float2 s1 = f2(0.f), s3 = f2(0.f);
+#pragma unroll
+      for (int t = 0; t < 24; t += 2) {
+        const float2 d = add2(make_float2(xv[t], xv[t + 1]), f2(-x0));
+        dv[t] = d.x;
+        dv[t + 1] = d.y;
+        s1 = add2(s1, d);
+        s3 = fma2(make_float2((float)t - 11.5f, (float)t - 10.5f), d, s3);
+      }
+      const float m1 = (s1.x + s1.y) * (1.f / 24.f);
+      const float mu = x0 + m1;
+      const float kap = (s3.x + s3.y) * a.inv_v;
+      float2 q2 = f2(0.f);
+      const float2 nm1 = f2(-m1);
+#pragma unroll
+      for (int t = 0; t < 24; t += 2) {
+        const float2 z = add2(make_float2(dv[t], dv[t + 1]), nm1);
+        dv[t] = z.x;
+        dv[t + 1] = z.y;
+        q2 = fma2(z, z, q2);
+      }
+      const float nu2 = q2.x + q2.y;
+      const float inv = rsqrtf(nu2 + kEpsSeasonal);
+      const float nu = sqrtf(nu2);
+      // |x_t| <= |mu| + |z_t| <= |mu| + nu: an exact power-of-two scale for X' from it
+      sx = pow2_scale(warp_max_nonneg(valid ? fabsf(mu) + nu : 0.f));
+      {
+        const float2 zs2 = f2(valid ? inv : 0.f), xs2 = f2(valid ? sx : 0.f);
+#pragma unroll
+        for (int t = 0; t < 24; t += 2) {
+          const float2 zz = mul2(make_float2(dv[t], dv[t + 1]), zs2);
+          const float2 xx = mul2(make_float2(xv[t], xv[t + 1]), xs2);
+          dv[t] = zz.x;
+          dv[t + 1] = zz.y;
+          xv[t] = xx.x;
+          xv[t + 1] = xx.y;
+        }
+      }
+      unsigned char* zr = zq + (4 * s + (i >> 3)) * 1024 + (i & 7) * 16;
+      unsigned char* xr = xt + 3 * s * 1024 + (i >> 3) * 128 + (i & 7) * 16;
+#pragma unroll
+      for (int q = 0; q < 3; q++) {
+        uint4 h, l;
+        split8(dv + 8 * q, h, l);
+        sts128(zr + q * 128, h);
+        sts128(zr + (4 + q) * 128, l);
+        split8(xv + 8 * q, h, l);
+        sts128(xr + q * 1024, h);
+        sts128(xr + q * 1024 + 512, l);
+      }
+      sts128(zr + 3 * 128, make_uint4(0u, 0u, 0u, 0u));   // K padding t = 24..31 (the tile
+      sts128(zr + 7 * 128, make_uint4(0u, 0u, 0u, 0u));   // held Q' last round)
+      // Def 5: sigma^2 = (1/(N S)) sum_n [nu2_n + S (mu_n - mubar)^2]
+      const float mbar_ = warp_sum(valid ? mu : 0.f) * a.inv_n;
+      const float dm = mu - mbar_;
+      const float inv_var =
+          1.0f / (warp_sum(valid ? fmaf(24.f * dm, dm, nu2) : 0.f) * a.inv_ns + kEpsTrend);
+      // trend (Def 7-8): exponent -(mu~_i - mu~_j)^2 - (k~_i - k~_j)^2, mu~ = mu sqrt(kt/var'),
+      // k~ = kappa sqrt(vtrend kt/var')
+      mi = mu * sqrtf(inv_var * a.kt);
+      ki = kap * sqrtf(a.vtrend * inv_var * a.kt);
+      colv[i] = (NC > 0 || valid) ? mi : INFINITY;   // -> exponent -inf past N
+      colv[32 + i] = ki;
+      if constexpr (NC == 0) colv[128 + i] = valid ? 0.f : -INFINITY;
+      __syncwarp();
+    }
+
+    // ---------------- a3 Gram on tcgen05: rho = Z' Z'^T (4 series, diagonal blocks used)
+    fence_proxy_async();
+    tc_fence_before();
+    named_bar(1 + grp, 128);
+    tc_fence_after();
+    if (mma_warp && elect_one()) {
+#pragma unroll
+      for (int ks = 0; ks < 2; ks++) {
+        const uint64_t ah = sdesc(zq_s + ks * 256, 128, 1024);
+        const uint64_t al = sdesc(zq_s + (4 + 2 * ks) * 128, 128, 1024);
+        umma(tcol, ah, ah, kIdGram, ks > 0);
+        umma(tcol, ah, al, kIdGram, true);
+        umma(tcol, al, ah, kIdGram, true);
+      }
+      umma_commit(mbar);
+    }
+
+    // ---------------- a4+a5 trend softmax (overlaps the Gram): lane j -> column j of A_t,
+    // A_t[i][j] = E_ji / l_i (E symmetric), as fp16 hi/lo pairs held for the TMEM store
+    uint32_t th[16], tl[16];
+    if (active) {
+      float e[32];
+      const float2 mi2 = f2(mi), ki2 = f2(ki);
+      float2 sum2 = f2(0.f);
+      const float4* cm4 = reinterpret_cast<const float4*>(colv);
+      const float4* ck4 = reinterpret_cast<const float4*>(colv + 32);
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        if (4 * q >= NJ) break;
+        const float4 mj = cm4[q], kj = ck4[q];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int j = 4 * q + 2 * h;
+          if (j >= NJ) break;
+          const float2 dmj = add2(mi2, h ? make_float2(-mj.z, -mj.w) : make_float2(-mj.x, -mj.y));
+          const float2 dkj = add2(ki2, h ? make_float2(-kj.z, -kj.w) : make_float2(-kj.x, -kj.y));
+          const float2 ex =
+              fma2(make_float2(-dkj.x, -dkj.y), dkj, mul2(make_float2(-dmj.x, -dmj.y), dmj));
+          e[j] = fast_ex2(ex.x);
+          e[j + 1] = fast_ex2(ex.y);
+          sum2 = add2(sum2, make_float2(e[j], e[j + 1]));
+        }
+      }
+      colv[64 + i] = valid ? fast_rcp(sum2.x + sum2.y) : 0.f;
+      __syncwarp();
+      const float4* cr4 = reinterpret_cast<const float4*>(colv + 64);
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        const float4 r = cr4[q];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int j = 4 * q + 2 * h;
+          if (j >= NJ) {
+            th[j / 2] = 0u;
+            tl[j / 2] = 0u;
+            continue;
+          }
+          const float2 v = mul2(make_float2(e[j], e[j + 1]), h ? make_float2(r.z, r.w) : make_float2(r.x, r.y));
+          split2(v, th[j / 2], tl[j / 2]);
+        }
+      }
+    }
+
+    // ---------------- a5 seasonal softmax from the Gram row in TMEM: lane j -> column j of
+    // A_s, A_s[i][j] = F_ji u_i / sum_i, F_ji = 2^(rho_ji ks - g_i - C)
+    mbar_wait_bounded(mbar, ph);
+    tc_fence_after();
+    if (active) {
+      uint32_t sh[16], sl[16];
+      {
+        uint32_t gr[32];
+        tld_x32(tcol + tlane + 32u * s, gr);
+        tld_wait();
+        float e[32];
+        const float2 ks2 = f2(a.ks), nks2 = f2(-a.ks);
+        const float4* cx4 = reinterpret_cast<const float4*>(colv + 128);
+        float2 sum2 = f2(0.f);
+#pragma unroll
+        for (int j = 0; j < NJ; j += 2) {
+          float2 arg = fma2(make_float2(__uint_as_float(gr[j]), __uint_as_float(gr[j + 1])), ks2,
+                            nks2);
+          if constexpr (NC == 0) {
+            const float4 mk = cx4[j >> 2];
+            arg = add2(arg, (j & 2) ? make_float2(mk.z, mk.w) : make_float2(mk.x, mk.y));
+          }
+          e[j] = fast_ex2(arg.x);
+          e[j + 1] = fast_ex2(arg.y);
+          sum2 = add2(sum2, make_float2(e[j], e[j + 1]));
+        }
+        colv[96 + i] = valid ? fast_rcp(sum2.x + sum2.y) : 0.f;
+        __syncwarp();
+        const float4* cr4 = reinterpret_cast<const float4*>(colv + 96);
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          const float4 r = cr4[q];
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int j = 4 * q + 2 * h;
+            if (j >= NJ) {
+              sh[j / 2] = 0u;
+              sl[j / 2] = 0u;
+              continue;
+            }
+            const float2 v = mul2(make_float2(e[j], e[j + 1]), h ? make_float2(r.z, r.w) : make_float2(r.x, r.y));
+            split2(v, sh[j / 2], sl[j / 2]);
+          }
+        }
+      }
+      // A^T rows into this warp's TMEM lanes (the Gram block is read): K = i packed in
+      // pairs, columns [0,16) A_s hi, [16,32) A_t hi, [32,48) A_s lo, [48,64) A_t lo
+      tst_x16(tcol + tlane, sh);
+      tst_x16(tcol + tlane + 16u, th);
+      tst_x16(tcol + tlane + 32u, sl);
+      tst_x16(tcol + tlane + 48u, tl);
+      tst_wait();
+    }
+
+    // ---------------- a6+a7 fold on tcgen05: Q'^T = [A_s^T | A_t^T] W'^T (Def 9-10 folded),
+    // A from TMEM, W' from shared memory, D in columns [64, 96)
+    tc_fence_before();
+    named_bar(1 + grp, 128);
+    tc_fence_after();
+    if (mma_warp && elect_one()) {
+#pragma unroll
+      for (int ks = 0; ks < 4; ks++) {
+        const uint64_t bh = sdesc(w_s + ks * 256, 128, 2048);
+        const uint64_t bl = sdesc(w_s + (8 + 2 * ks) * 128, 128, 2048);
+        umma_ts(tcol + 64u, tcol + 8u * ks, bh, kIdFold, ks > 0);
+        umma_ts(tcol + 64u, tcol + 8u * ks, bl, kIdFold, true);
+        umma_ts(tcol + 64u, tcol + 32u + 8u * ks, bh, kIdFold, true);
+      }
+      umma_commit(mbar + 1);
+    }
+    mbar_wait_bounded(mbar + 1, ph);
+    tc_fence_after();
+    if (active) {
+      uint32_t qv[32];
+      tld_x32(tcol + tlane + 64u, qv);   // lane j: Q'[m][j], m = 0..31
+      tld_wait();
+      unsigned char* qr = zq + 4 * s * 1024 + (i >> 3) * 128 + (i & 7) * 16;
+#pragma unroll
+      for (int mc = 0; mc < 4; mc++) {
+        uint4 h, l;
+        split8(reinterpret_cast<const float*>(qv) + 8 * mc, h, l);
+        sts128(qr + mc * 1024, h);
+        sts128(qr + mc * 1024 + 512, l);
+      }
+    }
+
+    // ---------------- a7 head on tcgen05: Y' = Q' X' (4 series, diagonal blocks used)
+    fence_proxy_async();
+    tc_fence_before();
+    named_bar(1 + grp, 128);
+    tc_fence_after();
+    if (mma_warp && elect_one()) {
+#pragma unroll
+      for (int ks = 0; ks < 2; ks++) {
+        const uint64_t ah = sdesc(zq_s + ks * 256, 128, 1024);
+        const uint64_t al = sdesc(zq_s + (4 + 2 * ks) * 128, 128, 1024);
+        const uint64_t bh = sdesc(xt_s + ks * 256, 128, 1024);
+        const uint64_t bl = sdesc(xt_s + (4 + 2 * ks) * 128, 128, 1024);
+        umma(tcol, ah, bh, kIdHead, ks > 0);
+        umma(tcol, ah, bl, kIdHead, true);
+        umma(tcol, al, bh, kIdHead, true);
+      }
+      umma_commit(mbar + 2);
+    }
+    mbar_wait_bounded(mbar + 2, ph);
+    tc_fence_after();
+
+    // ---------------- a8 store: lane m holds Y'[m][0..23]; y = Y' / (sw sx) + b (Def 11)
+    if (active) {
+      uint32_t yv[24];
+      tld_x24(tcol + tlane + 24u * s, yv);
+      tld_wait();
+      const int m = lane;
+      if (m < M) {
+        const float2 ys2 = f2(inv_sw / sx);
+        float* yg = a.y + series * H + m * 24;
+        const float* bm = bS + m * kQBiasRow;
+        if ((H & 3) == 0 && m * 24 + 24 <= H) {
+#pragma unroll
+          for (int q = 0; q < 6; q++) {
+            const float4 bb = *reinterpret_cast<const float4*>(bm + 4 * q);
+            const float2 o0 = fma2(make_float2(__uint_as_float(yv[4 * q]), __uint_as_float(yv[4 * q + 1])),
+                                   ys2, make_float2(bb.x, bb.y));
+            const float2 o1 = fma2(make_float2(__uint_as_float(yv[4 * q + 2]), __uint_as_float(yv[4 * q + 3])),
+                                   ys2, make_float2(bb.z, bb.w));
+            stg_stream4(yg + 4 * q, make_float4(o0.x, o0.y, o1.x, o1.y));
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < 24; t++)
+            if (m * 24 + t < H) yg[t] = fmaf(__uint_as_float(yv[t]), ys2.x, bm[t]);
+        }
+      }
+    }
+    ph ^= 1u;
+  }
+  cp_async_wait_all();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc(tmem0, 512);
+}
+
+bool plan_tcq_kernel(const FwdArgs& a, int max_smem_optin, TcqPlan* p) {
+  if (a.S != 24 || a.N < 1 || a.N > 32 || a.M > 32) return false;
+  p->smem_bytes = (size_t)kQSmem;
+  if (p->smem_bytes > (size_t)max_smem_optin) return false;
+  p->wins_per_group = 128;
+  return true;
+}
+
+template <int NC>
+static cudaError_t launch_tcq_t(const FwdArgs& a, const TcqPlan& p, cudaStream_t st) {
+  auto k = prnet_fwd_tcq_kernel<NC>;
+  cudaError_t e =
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+  if (e != cudaSuccess) return e;
+  const int64_t per_cta = (int64_t)kQGroups * p.wins_per_group;
+  const int ctas = (int)((a.B + per_cta - 1) / per_cta);
+  dim3 grid((unsigned)ctas, (unsigned)a.C);
+  k<<<grid, 32 * 4 * kQGroups, p.smem_bytes, st>>>(a, ctas);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tcq_kernel(const FwdArgs& a, const TcqPlan& p, cudaStream_t st) {
+  return a.N == 30 ? launch_tcq_t<30>(a, p, st) : launch_tcq_t<0>(a, p, st);
+}
+
+}  // namespace prnet

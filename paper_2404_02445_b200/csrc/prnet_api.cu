@@ -135,6 +135,11 @@ bool flash_applicable(const prnet_handle* h) {
 bool tc2_applicable(const prnet_handle* h) {
   return h->cfg.seg_len == 24 && h->N <= 32 && h->M <= 32;
 }
+// 6 = tc_quad (S = 24, N <= 32, M <= 32, tau_s >= 1/80: quads of series on tcgen05 / TMEM,
+// seasonal shift 1 >= rho keeps the diagonal term normal only down to tau_s = 1/80)
+bool tcq_applicable(const prnet_handle* h) {
+  return h->cfg.seg_len == 24 && h->N <= 32 && h->M <= 32 && h->cfg.tau_seasonal >= 0.0125f;
+}
 int pick_variant(const prnet_handle* h) {
   if (h->forced_variant >= 0) return h->forced_variant;
   // measured on B200 (profiles/r01_variants.md): mma_f16x3 is the fastest N <= 32 path;
@@ -153,11 +158,18 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
   cudaError_t e;
   int v = pick_variant(h);
   if (v == 1 && a_s != nullptr) v = 0;  // the attention dump lives in the N <= 32 kernels
+  if (v == 6 && a_s != nullptr) v = 2;
   static const int wpc_env = [] {  // tuning knob: windows per CTA (0 = plan default)
     const char* e = getenv("PRNET_WINDOWS_PER_CTA");
     return e ? atoi(e) : 0;
   }();
-  if (v == 5) {
+  if (v == 6) {
+    prnet::TcqPlan p;
+    if (!prnet::plan_tcq_kernel(a, h->max_smem_optin, &p))
+      return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the tc_quad kernel");
+    if (wpc_env > 0) p.wins_per_group = (wpc_env + 3) & ~3;
+    e = prnet::launch_tcq_kernel(a, p, st);
+  } else if (v == 5) {
     prnet::FlashPlan p;
     if (!prnet::plan_flash_kernel(a, h->max_smem_optin, &p))
       return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the flash kernel");
@@ -495,8 +507,11 @@ prnet_status prnet_error_sums(prnet_handle* h, const float* y, const float* targ
 
 prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {
   if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
-  if (variant < -1 || variant > 5)
-    return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,...,5}");
+  if (variant < -1 || variant > 6)
+    return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,...,6}");
+  if (variant == 6 && !tcq_applicable(h))
+    return fail(h, PRNET_ERR_UNSUPPORTED,
+                "tc_quad variant needs S = 24, N <= 32, M <= 32, tau_seasonal >= 1/80");
   if (variant == 5 && !flash_applicable(h))
     return fail(h, PRNET_ERR_UNSUPPORTED, "flash variant needs 16 < N <= 512, S <= 48, M <= 32");
   if (variant == 4 && !tc2_applicable(h))

@@ -24,7 +24,7 @@ EXPORTS = ("prnet_create", "prnet_load_params", "prnet_forward", "prnet_forward_
            "prnet_set_host_chunk", "prnet_destroy", "prnet_last_error", "prnet_get_dims",
            "prnet_debug_segments", "prnet_debug_attention", "prnet_error_sums",
            "prnet_forward_plan", "prnet_set_kernel_variant")
-VARIANTS = ("warp_f32", "long_f32", "mma_f16x3", "tc_fold", "tc_full", "flash_f16x3")
+VARIANTS = ("warp_f32", "long_f32", "mma_f16x3", "tc_fold", "tc_full", "flash_f16x3", "tc_quad")
 
 
 class PrnetError(RuntimeError):

@@ -36,14 +36,16 @@ def _applicable(variant, L, S, H):
         return N <= 32 and M <= 32 and S <= 128
     if variant == "tc_fold":
         return S == 24 and 16 < N <= 32 and M <= 32
-    if variant == "tc_full":
+    if variant in ("tc_full", "tc_quad"):
         return S == 24 and N <= 32 and M <= 32
     if variant == "flash_f16x3":
         return 16 < N <= 512 and S <= 48 and M <= 32
     return True
 
 
-VARIANTS = [None, "warp_f32", "mma_f16x3", "tc_fold", "tc_full", "long_f32", "flash_f16x3"]
+VARIANTS = [None, "warp_f32", "mma_f16x3", "tc_fold", "tc_full", "long_f32", "flash_f16x3",
+            "tc_quad"]
+SHORT_VARIANTS = [None, "warp_f32", "mma_f16x3", "tc_fold", "tc_full", "tc_quad"]   # N <= 32
 
 
 def _check_small(oracle_mod, x, S, H, hpc=True, tau_s=1.0, tau_t=1.0, scale=None, variant=None):
@@ -73,7 +75,8 @@ def test_etth1_full(oracle_mod):
 FULL = ["weather_h96", "weather_h192", "weather_h336", "weather_h720", "electricity", "traffic"]
 
 
-@pytest.mark.parametrize("variant", [None, "warp_f32", "mma_f16x3", "tc_fold", "tc_full"])
+@pytest.mark.parametrize("variant", [None, "warp_f32", "mma_f16x3", "tc_fold", "tc_full",
+                                     "tc_quad"])
 @pytest.mark.parametrize("name", FULL)
 def test_full_size_sampled(oracle_mod, name, variant):
     """The whole test set runs on the GPU in the bench's launch configuration; the
@@ -142,7 +145,7 @@ def test_shapes_ragged(oracle_mod, L, S, H, variant):
     _check_small(oracle_mod, x, S, H, variant=variant)
 
 
-@pytest.mark.parametrize("variant", VARIANTS[:5])
+@pytest.mark.parametrize("variant", SHORT_VARIANTS)
 @pytest.mark.parametrize("tau", [0.05, 0.1, 1.0, 10.0])
 @pytest.mark.parametrize("hpc", [True, False])
 def test_temperatures_and_head_modes(oracle_mod, tau, hpc, variant):
@@ -168,7 +171,7 @@ def test_long_lookback_value_distributions(oracle_mod, kind, variant):
     _check_small(oracle_mod, x, 24, 96, scale=scale, variant=variant)
 
 
-@pytest.mark.parametrize("variant", VARIANTS[:5])
+@pytest.mark.parametrize("variant", SHORT_VARIANTS)
 @pytest.mark.parametrize("kind", ["normal", "constant", "scaled"])
 @pytest.mark.parametrize("L,S", [(720, 24), (1440, 24)])
 def test_value_distributions(oracle_mod, kind, L, S, variant):
@@ -217,7 +220,7 @@ def test_attention_matrices(oracle_mod, L, S, variant):
 
 
 # ------------------------------------------------------------------ determinism, sharding, host path
-@pytest.mark.parametrize("variant", VARIANTS[:5])
+@pytest.mark.parametrize("variant", SHORT_VARIANTS)
 def test_deterministic_and_shard_invariant(variant):
     from paper_2404_02445_b200 import shard_windows
     x = torch.from_numpy(synth.random_windows(37, 11, 720)).cuda()
