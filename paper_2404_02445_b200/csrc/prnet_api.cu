@@ -142,8 +142,10 @@ bool tcq_applicable(const prnet_handle* h) {
 }
 int pick_variant(const prnet_handle* h) {
   if (h->forced_variant >= 0) return h->forced_variant;
-  // measured on B200 (profiles/r01_variants.md): mma_f16x3 is the fastest N <= 32 path;
-  // tc_fold (-1.6 %) and tc_full (-30 %) are selectable with prnet_set_kernel_variant
+  // measured on B200 (profiles/README.md): tc_quad is the fastest S = 24 path (Traffic
+  // 6.37 ms vs 6.60 ms for mma_f16x3), mma_f16x3 the fastest other N <= 32 path;
+  // tc_fold and tc_full are selectable with prnet_set_kernel_variant
+  if (tcq_applicable(h)) return 6;
   if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
   if (h->N > 32 && flash_applicable(h)) return 5;
   return h->N <= 32 ? 0 : 1;
