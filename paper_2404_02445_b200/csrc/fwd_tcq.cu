@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
     const bool active = b < g1;
     const int64_t series = b * C + c;
     float sx = 1.f, mi = 0.f, ki = 0.f;
+    float xv[24];   // the segment row, then X' = x sx (stored after the Gram issue)
 
     // ---------------- a1+a2: segment row i (Def 2) from the TMA staging, descriptors
     // (Def 4-5) from d = x - x0 (a constant segment gives exact zeros), Z' = z inv and
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
         cp_async_wait_all();
       }
       __syncwarp();
-      float xv[24], dv[24];
+      float dv[24];
       {
         const float4* xr = reinterpret_cast<const float4*>(xstage + (valid ? i : N - 1) * 24);
 #pragma unroll
@@ -249,24 +250,28 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
         }
       }
       unsigned char* zr = zq + (4 * s + (i >> 3)) * 1024 + (i & 7) * 16;
-      unsigned char* xr = xt + 3 * s * 1024 + (i >> 3) * 128 + (i & 7) * 16;
 #pragma unroll
       for (int q = 0; q < 3; q++) {
         uint4 h, l;
         split8(dv + 8 * q, h, l);
         sts128(zr + q * 128, h);
         sts128(zr + (4 + q) * 128, l);
-        split8(xv + 8 * q, h, l);
-        sts128(xr + q * 1024, h);
-        sts128(xr + q * 1024 + 512, l);
       }
       sts128(zr + 3 * 128, make_uint4(0u, 0u, 0u, 0u));   // K padding t = 24..31 (the tile
       sts128(zr + 7 * 128, make_uint4(0u, 0u, 0u, 0u));   // held Q' last round)
-      // Def 5: sigma^2 = (1/(N S)) sum_n [nu2_n + S (mu_n - mubar)^2]
-      const float mbar_ = warp_sum(valid ? mu : 0.f) * a.inv_n;
-      const float dm = mu - mbar_;
+      // Def 5: sigma^2 = (1/(N S)) sum_n [nu2_n + S (mu_n - mubar)^2], both sums in one
+      // shuffle tree about the reference m0 = mu_0: with d = mu - m0,
+      // sum_n (mu_n - mubar)^2 = sum d^2 - (sum d)^2 / N (exact; no cancellation against
+      // the level of the series, only against the spread of the segment means)
+      const float m0 = __shfl_sync(0xffffffffu, mu, 0);
+      const float dd = valid ? mu - m0 : 0.f;
+      float2 acc = make_float2(dd, valid ? fmaf(24.f * dd, dd, nu2) : 0.f);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+        acc = add2(acc, make_float2(__shfl_xor_sync(0xffffffffu, acc.x, o),
+                                    __shfl_xor_sync(0xffffffffu, acc.y, o)));
       const float inv_var =
-          1.0f / (warp_sum(valid ? fmaf(24.f * dm, dm, nu2) : 0.f) * a.inv_ns + kEpsTrend);
+          1.0f / (fmaf(-24.f * acc.x, acc.x * a.inv_n, acc.y) * a.inv_ns + kEpsTrend);
       // trend (Def 7-8): exponent -(mu~_i - mu~_j)^2 - (k~_i - k~_j)^2, mu~ = mu sqrt(kt/var'),
       // k~ = kappa sqrt(vtrend kt/var')
       mi = mu * sqrtf(inv_var * a.kt);
@@ -292,6 +297,17 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
         umma(tcol, al, ah, kIdGram, true);
       }
       umma_commit(mbar);
+    }
+    // X' rows -> head B tile (read only by the head, after the next barrier)
+    if (active) {
+      unsigned char* xr = xt + 3 * s * 1024 + (i >> 3) * 128 + (i & 7) * 16;
+#pragma unroll
+      for (int q = 0; q < 3; q++) {
+        uint4 h, l;
+        split8(xv + 8 * q, h, l);
+        sts128(xr + q * 1024, h);
+        sts128(xr + q * 1024 + 512, l);
+      }
     }
 
     // ---------------- a4+a5 trend softmax (overlaps the Gram): lane j -> column j of A_t,
