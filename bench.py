@@ -59,7 +59,7 @@ class ClockSampler:
            "hw_power_brake": 0x80, "display_clocks": 0x100}
 
     def __init__(self, device_index, period_s=0.005):
-        self.samples, self.reasons = [], 0
+        self.samples, self.reasons, self.power = [], 0, []
         self._stop = threading.Event()
         self.ok = False
         try:
@@ -79,6 +79,7 @@ class ClockSampler:
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
                 self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.power.append(nv.nvmlDeviceGetPowerUsage(self._h) / 1000.0)
             except Exception:
                 pass
             time.sleep(self.period)
@@ -99,7 +100,8 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml_unavailable"]}
         reasons = [k for k, v in self.ALL.items() if self.reasons & v]
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
-                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples)}
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples),
+                "power_w_median": statistics.median(self.power) if self.power else None}
 
 
 # ------------------------------------------------------------------ CPU oracle leg

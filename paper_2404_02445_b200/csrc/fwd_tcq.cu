@@ -60,6 +60,9 @@ using namespace tcq;
 
 namespace {
 
+#ifndef PRNET_TCQ_HEAD_SYNC
+#define PRNET_TCQ_HEAD_SYNC 1   // head on per-warp mma.sync (1) or on tcgen05 per quad (0)
+#endif
 constexpr int kQGroups = 4;
 constexpr int kQZQ = 16384;        // Z' tile, then Q' tile
 constexpr int kQXT = 12288;        // X' tile
@@ -77,7 +80,9 @@ static_assert(kQGroup % 16 == 0, "16-byte aligned tiles");
 
 constexpr uint32_t kIdGram = idesc_f16(128, 128, false, false);
 constexpr uint32_t kIdFold = idesc_f16(128, 32, false, false);
+#if !PRNET_TCQ_HEAD_SYNC
 constexpr uint32_t kIdHead = idesc_f16(128, 96, true, true);
+#endif
 
 // 8 consecutive fp32 -> 16-byte fp16 hi and lo rows (v = hi + lo)
 __device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
@@ -441,7 +446,79 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
         sts128(qr + mc * 1024 + 512, l);
       }
     }
-
+#if PRNET_TCQ_HEAD_SYNC
+    // ---------------- a7 head on mma.sync, per warp (its own series only, so no group
+    // barrier and no block-diagonal waste): Y' = Q' X' with m16n8k16 split-fp16 MMAs,
+    // A = Q' and B = X' fragments by ldmatrix.trans from the core-matrix tiles
+    if (active) {
+      __syncwarp();
+      const int l8 = lane & 7, g4 = lane >> 3;
+      const unsigned char* qs = zq + 4 * s * 1024;
+      const unsigned char* xs = xt + 3 * s * 1024;
+      float acc[2][3][4];
+#pragma unroll
+      for (int mt = 0; mt < 2; mt++)
+#pragma unroll
+        for (int nt = 0; nt < 3; nt++)
+#pragma unroll
+          for (int e = 0; e < 4; e++) acc[mt][nt][e] = 0.f;
+#pragma unroll
+      for (int kt = 0; kt < 2; kt++) {
+        // B = X'[j][t]: (j-block 2kt + (g4 & 1), t-block nt + (g4 >> 1)) for the x4 pair
+        uint32_t xh[3][2], xl[3][2];
+        {
+          uint32_t r[4];
+          const unsigned char* p = xs + (g4 >> 1) * 1024 + (2 * kt + (g4 & 1)) * 128 + l8 * 16;
+          ldsm_x4_t(r, p);
+          xh[0][0] = r[0]; xh[0][1] = r[1]; xh[1][0] = r[2]; xh[1][1] = r[3];
+          ldsm_x4_t(r, p + 512);
+          xl[0][0] = r[0]; xl[0][1] = r[1]; xl[1][0] = r[2]; xl[1][1] = r[3];
+          const unsigned char* p2 = xs + 2 * 1024 + (2 * kt + (g4 & 1)) * 128 + l8 * 16;
+          ldsm_x2_t(xh[2][0], xh[2][1], p2);
+          ldsm_x2_t(xl[2][0], xl[2][1], p2 + 512);
+        }
+#pragma unroll
+        for (int mt = 0; mt < 2; mt++) {
+          // A = Q'[m][j]: blocks (m-block 2mt + (g4 & 1), j-block 2kt + (g4 >> 1))
+          uint32_t ah[4], al[4];
+          const unsigned char* p = qs + (2 * mt + (g4 & 1)) * 1024 + (2 * kt + (g4 >> 1)) * 128 + l8 * 16;
+          ldsm_x4_t(ah, p);
+          ldsm_x4_t(al, p + 512);
+#pragma unroll
+          for (int nt = 0; nt < 3; nt++) mma16816(acc[mt][nt], al, xh[nt][0], xh[nt][1]);
+#pragma unroll
+          for (int nt = 0; nt < 3; nt++) mma16816(acc[mt][nt], ah, xl[nt][0], xl[nt][1]);
+#pragma unroll
+          for (int nt = 0; nt < 3; nt++) mma16816(acc[mt][nt], ah, xh[nt][0], xh[nt][1]);
+        }
+      }
+      // ---------------- a8 store: y = Y' / (sw sx) + b (Def 11), pairs (m, t..t+1)
+      const float2 ys2 = f2(inv_sw / sx);
+      float* yg = a.y + series * H;
+      const bool pairs = (H & 1) == 0;
+#pragma unroll
+      for (int mt = 0; mt < 2; mt++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int m = 16 * mt + 8 * h + (lane >> 2);
+          if (m >= M) continue;
+#pragma unroll
+          for (int nt = 0; nt < 3; nt++) {
+            const int t = 8 * nt + 2 * (lane & 3);
+            const int hh = m * 24 + t;
+            const float2 bb = *reinterpret_cast<const float2*>(bS + m * kQBiasRow + t);
+            const float2 o = fma2(make_float2(acc[mt][nt][2 * h], acc[mt][nt][2 * h + 1]), ys2, bb);
+            if (pairs && hh + 1 < H) {
+              asm volatile("st.global.cs.v2.f32 [%0], {%1,%2};" ::"l"(yg + hh), "f"(o.x), "f"(o.y)
+                           : "memory");
+            } else {
+              if (hh < H) yg[hh] = o.x;
+              if (hh + 1 < H) yg[hh + 1] = o.y;
+            }
+          }
+        }
+    }
+#else
     // ---------------- a7 head on tcgen05: Y' = Q' X' (4 series, diagonal blocks used)
     fence_proxy_async();
     tc_fence_before();
@@ -490,6 +567,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
         }
       }
     }
+#endif
     ph ^= 1u;
   }
   cp_async_wait_all();
