@@ -159,6 +159,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
   const bool mma_warp = s == 0;
   const uint32_t zq_s = smem_u32(zq), xt_s = smem_u32(xt), w_s = smem_u32(smem + kQOffW);
   const float inv_sw = __ldg(a.wpack_inv_sw + cw);
+  const bool full_rows = H == 24 * M && (H & 1) == 0;   // the output rows tile H exactly
 
   // windows of channel c: CTA k of the channel takes [B k / K, B (k+1) / K), split into
   // near-equal runs of whole quads over the groups
@@ -494,29 +495,44 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
       }
       // ---------------- a8 store: y = Y' / (sw sx) + b (Def 11), pairs (m, t..t+1)
       const float2 ys2 = f2(inv_sw / sx);
-      float* yg = a.y + series * H;
-      const bool pairs = (H & 1) == 0;
+      float* yg = a.y + series * H + 2 * (lane & 3);
+      const float* bq = bS + 2 * (lane & 3);
+      if (full_rows) {   // H = 24 M, H even: every (m < M, t) pair is stored, no tail
 #pragma unroll
-      for (int mt = 0; mt < 2; mt++)
+        for (int mt = 0; mt < 2; mt++)
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const int m = 16 * mt + 8 * h + (lane >> 2);
-          if (m >= M) continue;
+          for (int h = 0; h < 2; h++) {
+            const int m = 16 * mt + 8 * h + (lane >> 2);
+            if (m < M) {
+              float* yr = yg + m * 24;
+              const float* br = bq + m * kQBiasRow;
 #pragma unroll
-          for (int nt = 0; nt < 3; nt++) {
-            const int t = 8 * nt + 2 * (lane & 3);
-            const int hh = m * 24 + t;
-            const float2 bb = *reinterpret_cast<const float2*>(bS + m * kQBiasRow + t);
-            const float2 o = fma2(make_float2(acc[mt][nt][2 * h], acc[mt][nt][2 * h + 1]), ys2, bb);
-            if (pairs && hh + 1 < H) {
-              asm volatile("st.global.cs.v2.f32 [%0], {%1,%2};" ::"l"(yg + hh), "f"(o.x), "f"(o.y)
-                           : "memory");
-            } else {
-              if (hh < H) yg[hh] = o.x;
-              if (hh + 1 < H) yg[hh + 1] = o.y;
+              for (int nt = 0; nt < 3; nt++) {
+                const float2 bb = *reinterpret_cast<const float2*>(br + 8 * nt);
+                const float2 o = fma2(make_float2(acc[mt][nt][2 * h], acc[mt][nt][2 * h + 1]), ys2, bb);
+                asm volatile("st.global.cs.v2.f32 [%0], {%1,%2};" ::"l"(yr + 8 * nt), "f"(o.x),
+                             "f"(o.y)
+                             : "memory");
+              }
             }
           }
-        }
+      } else {
+#pragma unroll
+        for (int mt = 0; mt < 2; mt++)
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int m = 16 * mt + 8 * h + (lane >> 2);
+            if (m >= M) continue;
+#pragma unroll
+            for (int nt = 0; nt < 3; nt++) {
+              const int hh = m * 24 + 8 * nt + 2 * (lane & 3);
+              const float2 bb = *reinterpret_cast<const float2*>(bq + m * kQBiasRow + 8 * nt);
+              const float2 o = fma2(make_float2(acc[mt][nt][2 * h], acc[mt][nt][2 * h + 1]), ys2, bb);
+              if (hh < H) yg[m * 24 + 8 * nt] = o.x;
+              if (hh + 1 < H) yg[m * 24 + 8 * nt + 1] = o.y;
+            }
+          }
+      }
     }
 #else
     // ---------------- a7 head on tcgen05: Y' = Q' X' (4 series, diagonal blocks used)
