@@ -27,7 +27,8 @@
 //    its row of A^T (fp16 hi/lo) straight into its own TMEM lane with tcgen05.st, and the
 //    fold reads A from TMEM: no shared-memory tile for the attention at all.
 //  * one 128-column TMEM block per group is reused by every product of a round:
-//      Gram  D[0,128)  = Z' Z'^T                (smem x smem, diagonal blocks used)
+//      Gram  D[0,128)  = Z' Z'^T                (smem x smem, diagonal blocks used;
+//                                                5 K-steps, see the Z' chunk order)
 //      A^T         [0,64)  hi_s | hi_t | lo_s | lo_t  (tcgen05.st, after the Gram is read)
 //      fold  D[64,96)  = A^T W'^T  = Q'^T       (tmem x smem, all 128 rows useful)
 //      head  D[0,96)   = Q' [X'_0..X'_3]        (smem x smem, diagonal blocks used)
@@ -38,7 +39,7 @@
 //    CTA-shared.  4 x 43 KB + 11 KB per CTA, 16 warps per SM.
 //
 // Layouts (byte offsets; core matrix = 8 rows x 16 bytes, no swizzle):
-//   Z' (K-major, row r = 32 s + i, K = t; hi t 0..31 | lo t 0..31, t >= 24 zero):
+//   Z' (K-major, row r = 32 s + i; K chunks of 8 t: h0 h1 h2 l0 l1 l2 h2 0, see the Gram):
 //       (r/8)*1024 + (k/8)*128 + (r%8)*16 + (k%8)*2               LBO 128, SBO 1024
 //   Q' (MN-major, M = (s, m), K = j; hi j 0..31 | lo):  (4s + m/8)*1024 + (k/8)*128 +
 //       (k%8)*16 + (m%8)*2                                          LBO 128, SBO 1024
@@ -60,6 +61,9 @@ using namespace tcq;
 
 namespace {
 
+#ifndef PRNET_TCQ_FRAG
+#define PRNET_TCQ_FRAG 0        // softmaxes in the mma accumulator (16x256b) layout (1) or
+#endif                          // lane-per-row (0)
 #ifndef PRNET_TCQ_HEAD_SYNC
 #define PRNET_TCQ_HEAD_SYNC 1   // head on per-warp mma.sync (1) or on tcgen05 per quad (0)
 #endif
@@ -84,6 +88,17 @@ constexpr uint32_t kIdFold = idesc_f16(128, 32, false, false);
 constexpr uint32_t kIdHead = idesc_f16(128, 96, true, true);
 #endif
 
+// Gram row / column POSITION p <-> segment pi(p).  With p = 8k + 2c + e the 16x256b
+// fragment of thread c holds, for k = 0..3, the segments 16(k/2) + 4c + 2(k%2) + e: four
+// consecutive segments per 16-segment chunk, i.e. exactly the packed fp16 K pairs the
+// same thread must store for the fold's A operand (TMEM columns 8(k/2) + 2c + k%2).
+__device__ __forceinline__ constexpr int pi_pos(int p) {
+  return 16 * (p >> 4) + 4 * ((p >> 1) & 3) + 2 * ((p >> 3) & 1) + (p & 1);
+}
+__device__ __forceinline__ constexpr int pi_inv(int i) {
+  return 8 * (2 * (i >> 4) + ((i >> 1) & 1)) + 2 * ((i >> 2) & 3) + (i & 1);
+}
+
 // 8 consecutive fp32 -> 16-byte fp16 hi and lo rows (v = hi + lo)
 __device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
   uint32_t* h = reinterpret_cast<uint32_t*>(&hi);
@@ -104,7 +119,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
   static_assert(NC % 2 == 0 && NC <= 32, "NC");
   extern __shared__ __align__(1024) unsigned char smem[];
   constexpr int S = 24;
-  constexpr int NJ = NC > 0 ? NC : 32;   // columns computed per row
+  [[maybe_unused]] constexpr int NJ = NC > 0 ? NC : 32;   // columns per row (lane-per-row)
   const int lane = threadIdx.x & 31;
   // warp index made provably warp-uniform (shfl from lane 0), so the MMA issue path
   // below runs on uniform registers without a per-thread waterfall loop
@@ -255,16 +270,17 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
           xv[t + 1] = xx.y;
         }
       }
-      unsigned char* zr = zq + (4 * s + (i >> 3)) * 1024 + (i & 7) * 16;
+      const int zrow = PRNET_TCQ_FRAG ? pi_inv(i) : i;   // Gram position of segment i
+      unsigned char* zr = zq + (4 * s + (zrow >> 3)) * 1024 + (zrow & 7) * 16;
 #pragma unroll
       for (int q = 0; q < 3; q++) {
         uint4 h, l;
         split8(dv + 8 * q, h, l);
-        sts128(zr + q * 128, h);
-        sts128(zr + (4 + q) * 128, l);
+        sts128(zr + q * 128, h);          // K chunks: h0 h1 h2 | l0 l1 l2 | h2 | 0
+        sts128(zr + (3 + q) * 128, l);
+        if (q == 2) sts128(zr + 6 * 128, h);
       }
-      sts128(zr + 3 * 128, make_uint4(0u, 0u, 0u, 0u));   // K padding t = 24..31 (the tile
-      sts128(zr + 7 * 128, make_uint4(0u, 0u, 0u, 0u));   // held Q' last round)
+      sts128(zr + 7 * 128, make_uint4(0u, 0u, 0u, 0u));   // (the tile held Q' last round)
       // Def 5: sigma^2 = (1/(N S)) sum_n [nu2_n + S (mu_n - mubar)^2], both sums in one
       // shuffle tree about the reference m0 = mu_0: with d = mu - m0,
       // sum_n (mu_n - mubar)^2 = sum d^2 - (sum d)^2 / N (exact; no cancellation against
@@ -282,9 +298,14 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
       // k~ = kappa sqrt(vtrend kt/var')
       mi = mu * sqrtf(inv_var * a.kt);
       ki = kap * sqrtf(a.vtrend * inv_var * a.kt);
+#if PRNET_TCQ_FRAG
+      // (mu~, k~) pairs; past N a far-away but finite mu~ (exponent -1e36 -> 0, no inf - inf)
+      reinterpret_cast<float2*>(colv)[i] = make_float2(valid ? mi : 1e18f, ki);
+#else
       colv[i] = (NC > 0 || valid) ? mi : INFINITY;   // -> exponent -inf past N
       colv[32 + i] = ki;
       if constexpr (NC == 0) colv[128 + i] = valid ? 0.f : -INFINITY;
+#endif
       __syncwarp();
     }
 
@@ -294,14 +315,13 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
     named_bar(1 + grp, 128);
     tc_fence_after();
     if (mma_warp && elect_one()) {
-#pragma unroll
-      for (int ks = 0; ks < 2; ks++) {
-        const uint64_t ah = sdesc(zq_s + ks * 256, 128, 1024);
-        const uint64_t al = sdesc(zq_s + (4 + 2 * ks) * 128, 128, 1024);
-        umma(tcol, ah, ah, kIdGram, ks > 0);
-        umma(tcol, ah, al, kIdGram, true);
-        umma(tcol, al, ah, kIdGram, true);
-      }
+      // 5 K-steps of 2 chunks (c, c + LBO/128) cover hh + hl + lh with no zero K-step:
+      // (h0 h1)(h0 h1), (h2 0)(h2 0), (h0 h1)(l0 l1), (l0 l1)(h0 h1), (h2 l2)(l2 h2')
+      umma(tcol, sdesc(zq_s, 128, 1024), sdesc(zq_s, 128, 1024), kIdGram, false);
+      umma(tcol, sdesc(zq_s + 256, 640, 1024), sdesc(zq_s + 256, 640, 1024), kIdGram, true);
+      umma(tcol, sdesc(zq_s, 128, 1024), sdesc(zq_s + 384, 128, 1024), kIdGram, true);
+      umma(tcol, sdesc(zq_s + 384, 128, 1024), sdesc(zq_s, 128, 1024), kIdGram, true);
+      umma(tcol, sdesc(zq_s + 256, 384, 1024), sdesc(zq_s + 640, 128, 1024), kIdGram, true);
       umma_commit(mbar);
     }
     // X' rows -> head B tile (read only by the head, after the next barrier)
@@ -316,6 +336,134 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
       }
     }
 
+#if PRNET_TCQ_FRAG
+    // ---------------- a4+a5 / a5 softmaxes in the mma accumulator layout: thread
+    // (g = lane/4, c = lane%4) owns the row positions P = 16 mt + 8 v + g (segments pi(P))
+    // and the column segments 16(k/2) + 4c + 2(k%2) + e, k = 0..3, e = 0, 1.  A row of A^T
+    // (= column of A, symmetric logits) is E[pi(P)][i] / l_i; the row sums are quad
+    // reductions, the 1/l_i exchange is 8 values per thread.
+    const int gq = lane >> 2, cq = lane & 3;
+    uint32_t th[2][8], tl[2][8];   // [mt][4(k/2) + 2v + k%2] packed fp16 pairs
+    // column masks (segments >= N), per pair k
+    float2 madd[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int sg = 16 * (k >> 1) + 4 * cq + 2 * (k & 1);
+      madd[k] = make_float2(sg < N ? 0.f : -INFINITY, sg + 1 < N ? 0.f : -INFINITY);
+    }
+    // ---------------- a4+a5 trend softmax (overlaps the Gram): E = 2^(-Dhat kt), shift 0
+    if (active) {
+      const float4* cp4 = reinterpret_cast<const float4*>(colv);
+      const float2* cp2 = reinterpret_cast<const float2*>(colv);
+      float2 cm[4], ck[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const float4 v = cp4[(16 * (k >> 1) + 4 * cq + 2 * (k & 1)) >> 1];
+        cm[k] = make_float2(-v.x, -v.z);
+        ck[k] = make_float2(-v.y, -v.w);
+      }
+      float e[2][2][8];
+#pragma unroll
+      for (int mt = 0; mt < 2; mt++)
+#pragma unroll
+        for (int v = 0; v < 2; v++) {
+          const int sr = pi_pos(16 * mt + 8 * v + gq);
+          const float2 rp = cp2[sr];
+          const float2 rm = f2(rp.x), rk = f2(rp.y);
+          float2 sum2 = f2(0.f);
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            const float2 dm = add2(rm, cm[k]), dk = add2(rk, ck[k]);
+            const float2 ex = fma2(make_float2(-dk.x, -dk.y), dk, mul2(make_float2(-dm.x, -dm.y), dm));
+            e[mt][v][2 * k] = fast_ex2(ex.x);
+            e[mt][v][2 * k + 1] = fast_ex2(ex.y);
+            sum2 = add2(sum2, make_float2(e[mt][v][2 * k], e[mt][v][2 * k + 1]));
+          }
+          float sm = sum2.x + sum2.y;
+          sm += __shfl_xor_sync(0xffffffffu, sm, 1);
+          sm += __shfl_xor_sync(0xffffffffu, sm, 2);
+          if (cq == 0) colv[64 + sr] = sr < N ? fast_rcp(sm) : 0.f;
+        }
+      __syncwarp();
+      const float4 r0 = reinterpret_cast<const float4*>(colv + 64)[cq];
+      const float4 r1 = reinterpret_cast<const float4*>(colv + 80)[cq];
+      const float2 rc[4] = {make_float2(r0.x, r0.y), make_float2(r0.z, r0.w), make_float2(r1.x, r1.y),
+                            make_float2(r1.z, r1.w)};
+#pragma unroll
+      for (int mt = 0; mt < 2; mt++)
+#pragma unroll
+        for (int v = 0; v < 2; v++)
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            const float2 p = mul2(make_float2(e[mt][v][2 * k], e[mt][v][2 * k + 1]), rc[k]);
+            const int ri = 4 * (k >> 1) + 2 * v + (k & 1);
+            split2(p, th[mt][ri], tl[mt][ri]);
+          }
+    }
+
+    // ---------------- a5 seasonal softmax from the Gram fragments in TMEM:
+    // E = 2^((rho - 1) ks), the same row exchange
+    mbar_wait_bounded(mbar, ph);
+    tc_fence_after();
+    if (active) {
+      uint32_t sh[2][8], sl[2][8];
+      {
+        uint32_t gr[2][16];
+        tld16_x4(tcol + ((uint32_t)(32 * s) << 16) + 32u * s, gr[0]);
+        tld16_x4(tcol + ((uint32_t)(32 * s + 16) << 16) + 32u * s, gr[1]);
+        tld_wait();
+        const float2 ks2 = f2(a.ks), nks2 = f2(-a.ks);
+        float e[2][2][8];
+#pragma unroll
+        for (int mt = 0; mt < 2; mt++)
+#pragma unroll
+          for (int v = 0; v < 2; v++) {
+            float2 sum2 = f2(0.f);
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+              float2 arg = fma2(make_float2(__uint_as_float(gr[mt][4 * k + 2 * v]),
+                                            __uint_as_float(gr[mt][4 * k + 2 * v + 1])),
+                                ks2, nks2);
+              if (NC == 0 || k == 3) arg = add2(arg, madd[k]);
+              e[mt][v][2 * k] = fast_ex2(arg.x);
+              e[mt][v][2 * k + 1] = fast_ex2(arg.y);
+              sum2 = add2(sum2, make_float2(e[mt][v][2 * k], e[mt][v][2 * k + 1]));
+            }
+            float sm = sum2.x + sum2.y;
+            sm += __shfl_xor_sync(0xffffffffu, sm, 1);
+            sm += __shfl_xor_sync(0xffffffffu, sm, 2);
+            const int sr = pi_pos(16 * mt + 8 * v + gq);
+            if (cq == 0) colv[96 + sr] = sr < N ? fast_rcp(sm) : 0.f;
+          }
+        __syncwarp();
+        const float4 r0 = reinterpret_cast<const float4*>(colv + 96)[cq];
+        const float4 r1 = reinterpret_cast<const float4*>(colv + 112)[cq];
+        const float2 rc[4] = {make_float2(r0.x, r0.y), make_float2(r0.z, r0.w),
+                              make_float2(r1.x, r1.y), make_float2(r1.z, r1.w)};
+#pragma unroll
+        for (int mt = 0; mt < 2; mt++)
+#pragma unroll
+          for (int v = 0; v < 2; v++)
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+              const float2 p = mul2(make_float2(e[mt][v][2 * k], e[mt][v][2 * k + 1]), rc[k]);
+              const int ri = 4 * (k >> 1) + 2 * v + (k & 1);
+              split2(p, sh[mt][ri], sl[mt][ri]);
+            }
+      }
+      // A^T rows (positions) into this warp's TMEM lanes: K = segment i packed in pairs,
+      // columns [0,16) A_s hi, [16,32) A_t hi, [32,48) A_s lo, [48,64) A_t lo
+#pragma unroll
+      for (int mt = 0; mt < 2; mt++) {
+        const uint32_t ta = tcol + ((uint32_t)(32 * s + 16 * mt) << 16);
+        tst16_x2(ta, sh[mt]);
+        tst16_x2(ta + 16u, th[mt]);
+        tst16_x2(ta + 32u, sl[mt]);
+        tst16_x2(ta + 48u, tl[mt]);
+      }
+      tst_wait();
+    }
+#else
     // ---------------- a4+a5 trend softmax (overlaps the Gram): lane j -> column j of A_t,
     // A_t[i][j] = E_ji / l_i (E symmetric), as fp16 hi/lo pairs held for the TMEM store
     uint32_t th[16], tl[16];
@@ -416,6 +564,8 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
       tst_wait();
     }
 
+#endif
+
     // ---------------- a6+a7 fold on tcgen05: Q'^T = [A_s^T | A_t^T] W'^T (Def 9-10 folded),
     // A from TMEM, W' from shared memory, D in columns [64, 96)
     tc_fence_before();
@@ -438,7 +588,8 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
       uint32_t qv[32];
       tld_x32(tcol + tlane + 64u, qv);   // lane j: Q'[m][j], m = 0..31
       tld_wait();
-      unsigned char* qr = zq + 4 * s * 1024 + (i >> 3) * 128 + (i & 7) * 16;
+      const int qj = PRNET_TCQ_FRAG ? pi_pos(i) : i;   // fold row (TMEM lane) -> segment
+      unsigned char* qr = zq + 4 * s * 1024 + (qj >> 3) * 128 + (qj & 7) * 16;
 #pragma unroll
       for (int mc = 0; mc < 4; mc++) {
         uint4 h, l;

@@ -72,6 +72,21 @@ __device__ __forceinline__ void tld_x24(uint32_t taddr, uint32_t (&r)[24]) {
                : PRNET_TLD_R8(r, 16)
                : "r"(taddr + 16u));
 }
+// 16x256b shape (the mma.sync accumulator layout): thread t <-> TMEM lanes base + t/4 and
+// base + 8 + t/4; r[4k + 2v + e] = lane (base + t/4 + 8v), column 8k + 2(t%4) + e
+__device__ __forceinline__ void tld16_x4(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : PRNET_TLD_R8(r, 0), PRNET_TLD_R8(r, 8)
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tst16_x2(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x256b.x2.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+      : "memory");
+}
 // TMEM lane (base lane + t) <- thread t: 16 consecutive 32-bit columns
 __device__ __forceinline__ void tst_x16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
