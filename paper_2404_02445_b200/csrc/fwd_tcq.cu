@@ -68,6 +68,10 @@ namespace {
 #define PRNET_TCQ_HEAD_SYNC 1   // head on per-warp mma.sync (1) or on tcgen05 per quad (0)
 #endif
 constexpr int kQGroups = 4;
+// (t - 11.5, t + 1 - 11.5) pairs: the centred positions t~ of Def 3 for S = 24
+__constant__ float2 c_ttilde[12] = {{-11.5f, -10.5f}, {-9.5f, -8.5f}, {-7.5f, -6.5f}, {-5.5f, -4.5f},
+                                    {-3.5f, -2.5f},   {-1.5f, -0.5f}, {0.5f, 1.5f},   {2.5f, 3.5f},
+                                    {4.5f, 5.5f},     {6.5f, 7.5f},   {8.5f, 9.5f},   {10.5f, 11.5f}};
 constexpr int kQZQ = 16384;        // Z' tile, then Q' tile
 constexpr int kQXT = 12288;        // X' tile
 constexpr int kQStage = 3072;      // TMA staging per warp: N S fp32, N <= 32, S = 24
@@ -186,8 +190,12 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
   const int rounds = g1 > g0 ? (int)((g1 - g0 + 3) / 4) : 0;
   const int NS = N * S;
   const bool bulk = ((L & 3) == 0) && ((a.r & 3) == 0);
-  auto issue_load = [&](int64_t bb) {
-    const float* xg = a.x + (bb * C + c) * L + a.r;
+  // per-warp running pointers (window b = g0 + 4 rd + s): no 64-bit index math per round
+  const int64_t win0 = g0 + s;
+  const float* xnext = a.x + (win0 * C + c) * L + a.r;
+  float* ycur = a.y + (win0 * C + c) * H;
+  const int64_t xstep = 4 * (int64_t)C * L, ystep = 4 * (int64_t)C * H;
+  auto issue_load = [&](const float* xg) {
     if (bulk) {
       if (lane == 0) bulk_load(xstage, xg, (uint32_t)NS * 4u, xbar);
     } else {
@@ -197,11 +205,10 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
   };
 
   uint32_t xph = 0, ph = 0;
-  if (rounds > 0 && g0 + s < g1) issue_load(g0 + s);
+  if (rounds > 0 && win0 < g1) issue_load(xnext);
   for (int rd = 0; rd < rounds; rd++) {
     const int64_t b = g0 + 4 * rd + s;
     const bool active = b < g1;
-    const int64_t series = b * C + c;
     float sx = 1.f, mi = 0.f, ki = 0.f;
     float xv[24];   // the segment row, then X' = x sx (stored after the Gram issue)
 
@@ -230,7 +237,8 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
       }
       __syncwarp();
       // the staging row is in registers: fetch this warp's next series now
-      if (b + 4 < g1) issue_load(b + 4);
+      xnext += xstep;
+      if (b + 4 < g1) issue_load(xnext);
       const float x0 = xv[0];
       float2 s1 = f2(0.f), s3 = f2(0.f);
 #pragma unroll
@@ -239,7 +247,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
         dv[t] = d.x;
         dv[t + 1] = d.y;
         s1 = add2(s1, d);
-        s3 = fma2(make_float2((float)t - 11.5f, (float)t - 10.5f), d, s3);
+        s3 = fma2(c_ttilde[t / 2], d, s3);
       }
       const float m1 = (s1.x + s1.y) * (1.f / 24.f);
       const float mu = x0 + m1;
@@ -646,7 +654,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
       }
       // ---------------- a8 store: y = Y' / (sw sx) + b (Def 11), pairs (m, t..t+1)
       const float2 ys2 = f2(inv_sw / sx);
-      float* yg = a.y + series * H + 2 * (lane & 3);
+      float* yg = ycur + 2 * (lane & 3);
       const float* bq = bS + 2 * (lane & 3);
       if (full_rows) {   // H = 24 M, H even: every (m < M, t) pair is stored, no tail
 #pragma unroll
@@ -715,7 +723,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
       const int m = lane;
       if (m < M) {
         const float2 ys2 = f2(inv_sw / sx);
-        float* yg = a.y + series * H + m * 24;
+        float* yg = ycur + m * 24;
         const float* bm = bS + m * kQBiasRow;
         if ((H & 3) == 0 && m * 24 + 24 <= H) {
 #pragma unroll
@@ -736,6 +744,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
     }
 #endif
     ph ^= 1u;
+    ycur += ystep;
   }
   cp_async_wait_all();
   tc_fence_before();

@@ -114,17 +114,30 @@ __host__ __device__ constexpr uint32_t idesc_f16(int M, int N, bool a_mn, bool b
   return (1u << 4) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
-// mbarrier phase wait (try_wait suspends in hardware between polls); traps after ~2^26
-// polls instead of hanging the GPU if a phase never completes
+// mbarrier phase wait: try_wait may suspend the thread until the phase completes or the
+// time hint (ns) elapses; traps after ~2^26 polls instead of hanging the GPU if a phase
+// never completes
+#ifndef PRNET_MBAR_SUSPEND_NS
+#define PRNET_MBAR_SUSPEND_NS 0u   // 0: no hint (A/B: a 100 us hint was 1 % slower)
+#endif
 __device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity) {
   uint32_t done;
   for (uint32_t it = 0;; it++) {
+#if PRNET_MBAR_SUSPEND_NS
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(PRNET_MBAR_SUSPEND_NS)
+        : "memory");
+#else
     asm volatile(
         "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
         "selp.u32 %0, 1, 0, p;\n}"
         : "=r"(done)
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
+#endif
     if (done) return;
     if (it > (1u << 26)) __trap();
   }
