@@ -66,6 +66,17 @@ def _load():
                                        ctypes.c_int32, ctypes.c_double, ctypes.c_double,
                                        _f32p, _f64p]
         lib.oracle_forward.restype = ctypes.c_int
+        lib.oracle_series_ex.argtypes = [_f32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                         _f32p, _f32p, _f32p, ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
+                                         _f64p, ctypes.POINTER(_Debug)]
+        lib.oracle_series_ex.restype = ctypes.c_int
+        lib.oracle_forward_ex.argtypes = [_f32p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                          ctypes.c_int32, ctypes.c_int32, _f32p, _f32p, _f32p,
+                                          ctypes.c_int32, ctypes.c_double, ctypes.c_double,
+                                          ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
+                                          _f32p, _f64p]
+        lib.oracle_forward_ex.restype = ctypes.c_int
         lib.oracle_error_sums.argtypes = [_f32p, _f32p, ctypes.c_int64, _f64p]
         lib.oracle_error_sums.restype = None
         _lib = lib
@@ -80,8 +91,14 @@ def dims(L: int, S: int, H: int):
     return n.value, r.value, m.value
 
 
-def series(x, S, H, ws, wt, bias, tau_s=1.0, tau_t=1.0):
-    """One series; returns a dict with y and every intermediate (fp64)."""
+EPS_REVIN = 1e-5   # RevIN epsilon of the product (R-f1)
+
+
+def series(x, S, H, ws, wt, bias, tau_s=1.0, tau_t=1.0, metric_variant=0, instance_norm=False,
+           eps_r=EPS_REVIN):
+    """One series; returns a dict with y and every intermediate (fp64).
+    metric_variant bit 0 = level-only trend, bit 1 = detrended seasonal; instance_norm =
+    RevIN-style normalisation."""
     x = np.ascontiguousarray(x, dtype=np.float32).ravel()
     L = x.size
     N, r, M = dims(L, S, H)
@@ -96,8 +113,9 @@ def series(x, S, H, ws, wt, bias, tau_s=1.0, tau_t=1.0):
     }
     dbg = _Debug(**{k: v.ctypes.data for k, v in out.items()})
     y = np.zeros(H)
-    if _load().oracle_series(x, L, S, H, ws, wt, bias, float(tau_s), float(tau_t), y,
-                             ctypes.byref(dbg)) != 0:
+    if _load().oracle_series_ex(x, L, S, H, ws, wt, bias, float(tau_s), float(tau_t),
+                                int(metric_variant), int(bool(instance_norm)), float(eps_r), y,
+                                ctypes.byref(dbg)) != 0:
         raise ValueError("oracle_series rejected its arguments")
     out["sigma2"] = float(out["sigma2"][0])
     out["y"] = y
@@ -105,7 +123,8 @@ def series(x, S, H, ws, wt, bias, tau_s=1.0, tau_t=1.0):
     return out
 
 
-def forward(x, S, H, ws, wt, bias, head_per_channel=True, tau_s=1.0, tau_t=1.0):
+def forward(x, S, H, ws, wt, bias, head_per_channel=True, tau_s=1.0, tau_t=1.0,
+            metric_variant=0, instance_norm=False, eps_r=EPS_REVIN):
     """x [B, C, L] fp32 -> (y fp32 [B, C, H], y64 fp64 [B, C, H])."""
     x = np.ascontiguousarray(x, dtype=np.float32)
     B, C, L = x.shape
@@ -116,8 +135,9 @@ def forward(x, S, H, ws, wt, bias, head_per_channel=True, tau_s=1.0, tau_t=1.0):
     bias = np.ascontiguousarray(bias, dtype=np.float32).reshape(Cw, H)
     y = np.zeros((B, C, H), np.float32)
     y64 = np.zeros((B, C, H), np.float64)
-    if _load().oracle_forward(x, B, C, L, S, H, ws, wt, bias, int(bool(head_per_channel)),
-                              float(tau_s), float(tau_t), y, y64) != 0:
+    if _load().oracle_forward_ex(x, B, C, L, S, H, ws, wt, bias, int(bool(head_per_channel)),
+                                 float(tau_s), float(tau_t), int(metric_variant),
+                                 int(bool(instance_norm)), float(eps_r), y, y64) != 0:
         raise ValueError("oracle_forward rejected its arguments")
     return y, y64
 

@@ -68,6 +68,37 @@ static void oracle_descriptors(const double* X, int N, int S, double* mu, double
   }
 }
 
+/* SURVEY §8(f) f3, A4 variant "linear detrending before the correlation"
+ * (metric_variant bit 1): the seasonal metric sees the residual of each segment
+ * about its least-squares line, e_n[t] = z_n[t] - kappa_n ttilde_t, and its
+ * squared norm; Def 6 is then applied to (e, |e|^2) in place of (z, nu2). */
+static void oracle_detrend(const double* z, const double* kappa, int N, int S, double* e,
+                           double* e2) {
+  for (int n = 0; n < N; n++) {
+    double q = 0.0;
+    for (int t = 0; t < S; t++) {
+      double tt = (double)t - 0.5 * (double)(S - 1);
+      e[n * S + t] = z[n * S + t] - kappa[n] * tt;
+      q += e[n * S + t] * e[n * S + t];
+    }
+    e2[n] = q;
+  }
+}
+
+/* SURVEY §8(f) f1 (RevIN-style instance normalisation, reading R-f1 in DESIGN.md
+ * §3): statistics of the N*S segmented points the method consumes,
+ *   mu_r = (1/(N S)) sum X,  var_r = (1/(N S)) sum (X - mu_r)^2,
+ * Xhat = (X - mu_r) / sqrt(var_r + eps_r); the forecast is de-normalised as
+ * y = yhat sqrt(var_r + eps_r) + mu_r. */
+static void oracle_instance_stats(const double* X, int N, int S, double* mu_r, double* var_r) {
+  double s = 0.0;
+  for (int k = 0; k < N * S; k++) s += X[k];
+  *mu_r = s / ((double)N * (double)S);
+  double q = 0.0;
+  for (int k = 0; k < N * S; k++) q += (X[k] - *mu_r) * (X[k] - *mu_r);
+  *var_r = q / ((double)N * (double)S);
+}
+
 /* Def 5: sigma^2 = (1/(N S)) sum_n [nu2_n + S (mu_n - mubar)^2], mubar = mean_n mu_n:
  * the population variance of the N*S segmented points (A5 normaliser). */
 static double oracle_series_variance(const double* mu, const double* nu2, int N, int S) {
@@ -96,8 +127,10 @@ static void oracle_seasonal_similarity(const double* z, const double* nu2, int N
  * which equals (1/S) ||T_i - T_j||^2 for the least-squares lines
  * T_n[t] = mu_n + kappa_n ttilde_t. */
 static void oracle_trend_distance(const double* mu, const double* kappa, int N, int S,
-                                  double* D) {
-  double c = ((double)S * (double)S - 1.0) / 12.0;
+                                  int level_only, double* D) {
+  /* level_only (metric_variant bit 0, SURVEY §8(f) f3 / A5 variant "level only"):
+   * D_ij = (mu_i - mu_j)^2 */
+  double c = level_only ? 0.0 : ((double)S * (double)S - 1.0) / 12.0;
   for (int i = 0; i < N; i++)
     for (int j = 0; j < N; j++) {
       double dm = mu[i] - mu[j];
@@ -154,9 +187,17 @@ static void oracle_head(const double* Ps, const double* Pt, const float* ws, con
 int oracle_series(const float* x, int32_t L, int32_t S, int32_t H, const float* ws,
                   const float* wt, const float* bias, double tau_s, double tau_t, double* y,
                   const oracle_debug* dbg) {
+  return oracle_series_ex(x, L, S, H, ws, wt, bias, tau_s, tau_t, 0, 0, 0.0, y, dbg);
+}
+
+int oracle_series_ex(const float* x, int32_t L, int32_t S, int32_t H, const float* ws,
+                     const float* wt, const float* bias, double tau_s, double tau_t,
+                     int32_t metric_variant, int32_t instance_norm, double eps_r, double* y,
+                     const oracle_debug* dbg) {
   int32_t N, r, M;
   if (oracle_dims(L, S, H, &N, &r, &M) != 0) return -1;
   if (!(tau_s > 0.0) || !(tau_t > 0.0)) return -1;
+  if (metric_variant < 0 || metric_variant > 3 || !(eps_r >= 0.0)) return -1;
   size_t nS = (size_t)N * S, nN = (size_t)N * N, mS = (size_t)M * S;
   double* X = (double*)malloc(nS * sizeof(double));
   double* z = (double*)malloc(nS * sizeof(double));
@@ -173,16 +214,34 @@ int oracle_series(const float* x, int32_t L, int32_t S, int32_t H, const float* 
   double* Yf = (double*)malloc(mS * sizeof(double));
 
   oracle_segment(x, N, S, r, X);                                   /* Def 2   */
+  double mu_r = 0.0, s_r = 1.0;
+  if (instance_norm) {                                             /* f1      */
+    double var_r;
+    oracle_instance_stats(X, N, S, &mu_r, &var_r);
+    s_r = sqrt(var_r + eps_r);
+    for (size_t k = 0; k < nS; k++) X[k] = (X[k] - mu_r) / s_r;
+  }
   oracle_descriptors(X, N, S, mu, z, nu2, kap);                    /* Def 3-4 */
   double sigma2 = oracle_series_variance(mu, nu2, N, S);           /* Def 5   */
-  oracle_seasonal_similarity(z, nu2, N, S, rho);                   /* Def 6   */
-  oracle_trend_distance(mu, kap, N, S, D);                         /* Def 7   */
+  if (metric_variant & 2) {                                        /* f3      */
+    double* e = (double*)malloc(nS * sizeof(double));
+    double* e2 = (double*)malloc(N * sizeof(double));
+    oracle_detrend(z, kap, N, S, e, e2);
+    oracle_seasonal_similarity(e, e2, N, S, rho);                  /* Def 6 on e */
+    free(e);
+    free(e2);
+  } else {
+    oracle_seasonal_similarity(z, nu2, N, S, rho);                 /* Def 6   */
+  }
+  oracle_trend_distance(mu, kap, N, S, metric_variant & 1, D);     /* Def 7   */
   for (size_t k = 0; k < nN; k++) Dh[k] = D[k] / (sigma2 + ORACLE_EPS_T);
   oracle_softmax_rows(rho, N, +1.0, 1.0 / tau_s, As);              /* Def 8   */
   oracle_softmax_rows(Dh, N, -1.0, 1.0 / tau_t, At);               /* Def 8   */
   oracle_aggregate(As, X, N, S, Ps);                               /* Def 9   */
   oracle_aggregate(At, X, N, S, Pt);                               /* Def 9   */
   oracle_head(Ps, Pt, ws, wt, bias, N, S, M, H, Yf, y);            /* Def 10-11 */
+  if (instance_norm)                                               /* f1      */
+    for (int32_t h = 0; h < H; h++) y[h] = y[h] * s_r + mu_r;
 
   if (dbg) {
     if (dbg->seg) memcpy(dbg->seg, X, nS * sizeof(double));
@@ -207,6 +266,15 @@ int oracle_forward(const float* x, int64_t B, int32_t C, int32_t L, int32_t S, i
                    const float* ws, const float* wt, const float* bias,
                    int32_t head_per_channel, double tau_s, double tau_t, float* y,
                    double* y64) {
+  return oracle_forward_ex(x, B, C, L, S, H, ws, wt, bias, head_per_channel, tau_s, tau_t, 0, 0,
+                           0.0, y, y64);
+}
+
+int oracle_forward_ex(const float* x, int64_t B, int32_t C, int32_t L, int32_t S, int32_t H,
+                      const float* ws, const float* wt, const float* bias,
+                      int32_t head_per_channel, double tau_s, double tau_t,
+                      int32_t metric_variant, int32_t instance_norm, double eps_r, float* y,
+                      double* y64) {
   int32_t N, r, M;
   if (B < 0 || C < 1 || oracle_dims(L, S, H, &N, &r, &M) != 0) return -1;
   double* yy = (double*)malloc((size_t)H * sizeof(double));
@@ -214,8 +282,9 @@ int oracle_forward(const float* x, int64_t B, int32_t C, int32_t L, int32_t S, i
     for (int32_t c = 0; c < C; c++) {
       int64_t cw = head_per_channel ? c : 0;
       const float* xs = x + (b * C + c) * (int64_t)L;
-      if (oracle_series(xs, L, S, H, ws + cw * M * N, wt + cw * M * N, bias + cw * H, tau_s,
-                        tau_t, yy, NULL) != 0) {
+      if (oracle_series_ex(xs, L, S, H, ws + cw * M * N, wt + cw * M * N, bias + cw * H,
+                           tau_s, tau_t, metric_variant, instance_norm, eps_r, yy,
+                           NULL) != 0) {
         free(yy);
         return -1;
       }

@@ -62,6 +62,18 @@ int oracle_series(const float* x, int32_t L, int32_t S, int32_t H,
                   const float* ws, const float* wt, const float* bias,
                   double tau_s, double tau_t, double* y, const oracle_debug* dbg);
 
+/* As oracle_series, with the SURVEY §8(f) widening (DESIGN.md §3 readings R-f1, R-f3):
+ * metric_variant bit 0: level-only trend distance D_ij = (mu_i - mu_j)^2;
+ * metric_variant bit 1: seasonal metric on the residuals about each segment's
+ *                       least-squares line;
+ * instance_norm != 0:   RevIN-style normalisation of the segmented points with
+ *                       eps_r, de-normalised forecast.
+ * Returns -1 also for metric_variant outside [0, 3] or eps_r < 0. */
+int oracle_series_ex(const float* x, int32_t L, int32_t S, int32_t H,
+                     const float* ws, const float* wt, const float* bias,
+                     double tau_s, double tau_t, int32_t metric_variant,
+                     int32_t instance_norm, double eps_r, double* y, const oracle_debug* dbg);
+
 /* A batch x[B][C][L] -> y[B][C][H] (fp32, rounded from the fp64 result) and
  * optionally y64 (fp64).  head_per_channel: 1 -> ws/wt are [C][M][N], bias
  * [C][H]; 0 -> [1][M][N], [1][H].  Series are processed in (b, c) order,
@@ -70,6 +82,12 @@ int oracle_forward(const float* x, int64_t B, int32_t C, int32_t L, int32_t S,
                    int32_t H, const float* ws, const float* wt, const float* bias,
                    int32_t head_per_channel, double tau_s, double tau_t,
                    float* y, double* y64);
+
+int oracle_forward_ex(const float* x, int64_t B, int32_t C, int32_t L, int32_t S,
+                      int32_t H, const float* ws, const float* wt, const float* bias,
+                      int32_t head_per_channel, double tau_s, double tau_t,
+                      int32_t metric_variant, int32_t instance_norm, double eps_r,
+                      float* y, double* y64);
 
 /* Sum of squared and absolute errors of y against target (n values), fp64,
  * in index order: out[0] = SSE, out[1] = SAE, out[2] = n.  (Bench metric,
