@@ -198,6 +198,10 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no extras)")
     ap.add_argument("--variant", default=None, help="force a kernel variant (tuning)")
+    ap.add_argument("--metric-variant", type=int, default=0,
+                    help="SURVEY 8(f) f3: bit 0 level-only trend, bit 1 detrended seasonal")
+    ap.add_argument("--instance-norm", action="store_true",
+                    help="SURVEY 8(f) f1: RevIN-style instance normalisation")
     ap.add_argument("--host-chunk", type=int, default=0,
                     help="windows per chunk of the host-buffer pipeline (0 = library default)")
     args = ap.parse_args()
@@ -210,6 +214,8 @@ def main():
            "M": M, "series_per_step": B * w.C, "head": "per-channel",
            "l2": f"inputs larger than L2 ({B * w.C * w.L * 4 / 1e9:.2f} GB read per step)",
            "parallelism": f"dp{world}", "seed": args.seed}
+    if args.metric_variant or args.instance_norm:
+        cfg.update(metric_variant=args.metric_variant, instance_norm=bool(args.instance_norm))
 
     if args.impl == "reference":
         if rank != 0:
@@ -264,7 +270,8 @@ def main():
         .permute(1, 0, 2).contiguous()
     del sd
     ws, wt, b = synth.make_params(w.C, M, N, w.H, True, args.seed, w.cfg_id)
-    model = PRNet(w.C, w.L, w.S, w.H, device=dev).load(ws, wt, b)
+    model = PRNet(w.C, w.L, w.S, w.H, device=dev, metric_variant=args.metric_variant,
+                  instance_norm=args.instance_norm).load(ws, wt, b)
     if args.variant:
         model.set_variant(args.variant)
     y = torch.empty((count, w.C, w.H), dtype=torch.float32, device="cuda")
@@ -357,7 +364,7 @@ def main():
             traffic = None
 
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and not (args.metric_variant or args.instance_norm):
         try:
             wps, sps, cores, sample = cpu_oracle_rate(w.name, args.seed, args.cpu_budget)
             cpu = {"value": wps, "unit": "windows/s", "cores": cores, "kind": "oracle",

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define PRNET_ABI_VERSION 1
+#define PRNET_ABI_VERSION 2
 
 typedef struct prnet_handle prnet_handle; /* opaque; owned by the library */
 
@@ -43,27 +43,37 @@ typedef enum {
   PRNET_OK = 0,
   PRNET_ERR_INVALID_ARG = 1, /* NULL pointer with B > 0, C < 1, S < 2, L < S, H < 1,
                                 tau <= 0 or non-finite, wrong parameter counts, B < 0,
-                                size overflow, wrong abi_version                       */
+                                size overflow, abi_version not 1 or 2, metric_variant
+                                outside [0, 3], instance_norm not 0/1                  */
   PRNET_ERR_BAD_STATE = 2,   /* forward before load_params; NULL handle                  */
   PRNET_ERR_UNSUPPORTED = 3, /* device is not sm_100 (cc 10.x); x/y not 16-byte aligned;
                                 x and y overlap; pointer not on the handle's device;
-                                shape beyond the compiled limits (N > 512, S > 128)    */
+                                shape beyond the compiled limits (N > 512, S > 128);
+                                metric_variant != 0 or instance_norm with N > 32       */
   PRNET_ERR_CUDA = 4,        /* CUDA runtime or launch error (text: prnet_last_error)    */
   PRNET_ERR_OOM = 5          /* device or pinned-host allocation failed                  */
 } prnet_status;
 
 typedef struct {
-  int32_t abi_version;      /* must equal PRNET_ABI_VERSION                               */
+  int32_t abi_version;      /* PRNET_ABI_VERSION (2); 1 = the v1 layout (no fields past device) */
   int32_t channels;         /* C >= 1                                                     */
   int32_t lookback;         /* L >= seg_len                                               */
   int32_t seg_len;          /* S >= 2 (A1: S is an input, e.g. the dominant period)      */
   int32_t horizon;          /* H >= 1                                                     */
   int32_t head_per_channel; /* 1: ws/wt are [C][M][N], bias [C][H] (A7, NS "per-channel
                                linear head"); 0: one shared head [1][M][N], [1][H]       */
-  int32_t metric_variant;   /* 0 = the DESIGN.md §3 reading; other values reserved       */
+  int32_t metric_variant;   /* bit flags, 0 = the DESIGN.md §3 reading; SURVEY §8(f) f3:
+                               bit 0 = level-only trend distance D = (mu_i - mu_j)^2;
+                               bit 1 = seasonal metric on the residuals about each
+                                       segment's least-squares line.  Values > 3 invalid. */
   float tau_seasonal;       /* tau_s > 0: softmax temperature of the seasonal branch (A6) */
   float tau_trend;          /* tau_t > 0: softmax temperature of the trend branch (A6)    */
   int32_t device;           /* CUDA device ordinal the handle is bound to                 */
+  /* ---- ABI 2 (a caller passing abi_version = 1 gets 0 for every field below) ---- */
+  int32_t instance_norm;    /* 1 = RevIN-style normalisation of the N*S
+                               segmented points (mean, population variance, eps 1e-5)
+                               before the method and de-normalisation of the forecast
+                               (R-f1); 0 = off                              */
 } prnet_config;
 
 /* Create a handle: validates cfg, checks the device is compute capability 10.x,

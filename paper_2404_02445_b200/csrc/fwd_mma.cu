@@ -66,7 +66,7 @@ __host__ __device__ constexpr MmaOffsets mma_offsets(int nr, int S, int sph, int
   o.zlo = off;
   off = r16(off + nr * zph * 2);
   o.misc = off;
-  off += 512 + 256 + 16;
+  off += 512 + 384 + 16;
   o.pw = (off + 127) & ~127;
   const int wph = 2 * nr + 8, rows = 16 * mmt;
   o.wlo = rows * wph * 2;
@@ -122,8 +122,8 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
   __half* z_lo = reinterpret_cast<__half*>(wb + (SC > 0 ? KO.zlo : ly.off_zlo));
   // per-row descriptors (mu~, kappa~, 1/sqrt(nu2 + eps_s), f) broadcast through shared memory
   float4* dsc = reinterpret_cast<float4*>(wb + (SC > 0 ? KO.misc : ly.off_diag));
-  float* rsm = reinterpret_cast<float*>(dsc + 32);            // [64] x0, m1 per row
-  uint64_t* xbar = reinterpret_cast<uint64_t*>(rsm + 64);     // TMA completion barrier
+  float* rsm = reinterpret_cast<float*>(dsc + 32);            // [96] x0, m1, kappa per row
+  uint64_t* xbar = reinterpret_cast<uint64_t*>(rsm + 96);     // TMA completion barrier
   if (lane == 0) mbar_init(xbar, 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   {
@@ -201,6 +201,9 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
     // value, so a constant segment gives exact zeros); X' = x sx, Z' = z sz as fp16 hi/lo
     const int i = lane;
     float x0 = 0.f, m1 = 0.f, mu = 0.f, kap = 0.f, nu2 = 0.f, sx, sz;
+    // generic path only: Def 5 pieces computed before pass 2, and the instance-norm map
+    // (rr = 1, sr = 1, mr = 0 when off; the S = 24 instantiations never see the widening)
+    float gen_mbar = 0.f, gen_var = 0.f, rr = 1.f, sr = 1.f, mr = 0.f;
     if constexpr (SC == 24) {
       // lane i holds its whole segment in registers: one read, 16-byte row stores
       float xv[24];
@@ -290,26 +293,44 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
         m1 = s1 * a.inv_s;
         mu = x0 + m1;
         kap = s3 * a.inv_v;
+        // nu2: |z|^2, or with metric_variant bit 1 the residual |e|^2, e = z - kappa t~
+        // (SURVEY §8(f) f3); Def 5 below uses |z|^2 = |e|^2 + kappa^2 V
+        const float kd = a.detrend ? kap : 0.f;
         for (int t = 0; t < S; t++) {
-          const float z = (xr[t] - x0) - m1;
+          const float z = fmaf(-kd, (float)t - a.half_s, (xr[t] - x0) - m1);
           nu2 = fmaf(z, z, nu2);
         }
       }
-      sx = pow2_scale(warp_max_nonneg(amx));
-      sz = pow2_scale(2.f * warp_max_nonneg(dmx));
-      rsm[lane] = x0;        // per-row shift and mean for the coalesced pass (no shuffles in
-      rsm[32 + lane] = m1;   // its lane-divergent loop)
+      // sigma^2 (Def 5) and, with instance_norm (f1, R-f1), the RevIN map xhat = (x - mu_r) rr
+      gen_mbar = warp_sum(i < N ? mu : 0.f) * a.inv_n;
+      {
+        const float nz2 = a.detrend ? fmaf(s3, kap, nu2) : nu2;
+        gen_var = warp_sum(i < N ? nz2 + (float)S * (mu - gen_mbar) * (mu - gen_mbar) : 0.f) *
+                  a.inv_ns;
+      }
+      if (a.revin) {
+        rr = rsqrtf(gen_var + kEpsRevin);
+        sr = (gen_var + kEpsRevin) * rr;
+        mr = gen_mbar;
+      }
+      sx = pow2_scale((warp_max_nonneg(amx) + fabsf(mr)) * rr);
+      // |e| <= |z| + |kappa| max|t~| <= 2 max|d| + |kappa| (S-1)/2
+      sz = pow2_scale(warp_max_nonneg(2.f * dmx + (a.detrend ? fabsf(kap) * a.half_s : 0.f)));
+      rsm[lane] = x0;        // per-row shift, mean and slope for the coalesced pass (no
+      rsm[32 + lane] = m1;   // shuffles in its lane-divergent loop)
+      rsm[64 + lane] = a.detrend ? kap : 0.f;
       __syncwarp();
+      const float xsc = rr * sx, xoff = -mr * rr * sx;
       for (int k = lane; k < NS; k += 32) {
         const int r = (int)(((float)k + 0.5f) * a.inv_s);
         const int t = k - r * S;
         const float v = xbuf[k];
-        const float xr0 = rsm[r], mr = rsm[32 + r];
+        const float xr0 = rsm[r], mrow = rsm[32 + r], krow = rsm[64 + r];
         __half h, l;
-        split1(v * sx, h, l);
+        split1(fmaf(v, xsc, xoff), h, l);
         x_hi[r * sph + t] = h;
         x_lo[r * sph + t] = l;
-        split1(((v - xr0) - mr) * sz, h, l);
+        split1(fmaf(-krow, (float)t - a.half_s, (v - xr0) - mrow) * sz, h, l);
         z_hi[r * zph + t] = h;
         z_lo[r * zph + t] = l;
       }
@@ -318,9 +339,15 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
     // xbuf is free: fetch the next series while this one is in the tensor cores
     if (b + nwarps < b_end) prefetch(b + nwarps);
     // Def 5: sigma^2 = (1/(N S)) sum_n [nu2_n + S (mu_n - mubar)^2]
-    const float mbar = warp_sum(i < N ? mu : 0.f) * a.inv_n;
-    const float dv = i < N ? nu2 + (float)S * (mu - mbar) * (mu - mbar) : 0.f;
-    const float inv_var = 1.0f / (warp_sum(dv) * a.inv_ns + kEpsTrend);
+    float inv_var;
+    if constexpr (SC > 0) {
+      const float mbar = warp_sum(i < N ? mu : 0.f) * a.inv_n;
+      const float dv = i < N ? nu2 + (float)S * (mu - mbar) * (mu - mbar) : 0.f;
+      inv_var = 1.0f / (warp_sum(dv) * a.inv_ns + kEpsTrend);
+    } else {
+      // of the (normalised) input: var rr^2
+      inv_var = 1.0f / fmaf(gen_var * rr, rr, kEpsTrend);
+    }
     {
       // trend: mu~ = mu sqrt(inv_var kt), k~ = kappa sqrt(vtrend inv_var kt) (Def 7-8);
       // seasonal: inv = 1/sqrt(nu2 + eps_s) (Def 6) and the known row maximum f = nu inv:
@@ -328,9 +355,12 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
       // of it, so exp((rho_ij - f_i) / tau_s) never overflows and its largest term never
       // underflows for tau_s > 0.003; softmax is shift-invariant, so this is the same result
       // as subtracting the searched max (Def 8).
-      const float cm = sqrtf(inv_var * a.kt), ck = sqrtf(a.vtrend * inv_var * a.kt);
-      const float inv = rsqrtf(nu2 + kEpsSeasonal);
-      dsc[lane] = i < N ? make_float4(mu * cm, kap * ck, inv, sqrtf(nu2) * inv)
+      const float cm = sqrtf(inv_var * a.kt) * rr, ck = sqrtf(a.vtrend * inv_var * a.kt) * rr;
+      // seasonal normaliser of the normalised input: 1/sqrt(nu2 rr^2 + eps_s); the Gram is of
+      // z sz (unnormalised), so the column factor carries one rr and rk the other
+      const float nh2 = nu2 * rr * rr;
+      const float invh = rsqrtf(nh2 + kEpsSeasonal);
+      dsc[lane] = i < N ? make_float4((mu - mr) * cm, kap * ck, invh * rr, sqrtf(nh2) * invh)
                         : make_float4(0.f, 0.f, 1.f, 0.f);
       __syncwarp();
     }
@@ -507,7 +537,7 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
 
     // ---------------- a7 head Y' = Q' X' (= sw sx Y), one 16-row tile of future segments
     // at a time, t in chunks of 4 tiles; a8 store y = Y + b
-    const float2 ys2 = f2(inv_sw / sx);
+    const float2 ys2 = f2(inv_sw * sr / sx);
     const bool pair_store = ((S | H) & 1) == 0;   // t, hh even -> 8-byte aligned pairs
     float* yg = a.y + series * H;
     float* ystage = reinterpret_cast<float*>(z_hi);
@@ -581,13 +611,15 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
               const float2 v = mul2(make_float2(ya[nt][2 * h], ya[nt][2 * h + 1]), ys2);
               if (pair_store) {  // hh even, H even: hh < H implies hh + 1 < H
                 if (hh >= H) continue;
-                const float2 o = add2(v, *reinterpret_cast<const float2*>(bS + hh));
+                float2 bb = *reinterpret_cast<const float2*>(bS + hh);
+                if (SC == 0 && a.revin) bb = fma2(bb, f2(sr), f2(mr));   // y = yhat sr + mr
+                const float2 o = add2(v, bb);
                 asm volatile("st.global.cs.v2.f32 [%0], {%1,%2};" ::"l"(yg + hh), "f"(o.x),
                              "f"(o.y)
                              : "memory");
               } else {
-                if (hh < H) yg[hh] = v.x + bS[hh];
-                if (t + 1 < S && hh + 1 < H) yg[hh + 1] = v.y + bS[hh + 1];
+                if (hh < H) yg[hh] = v.x + fmaf(bS[hh], sr, mr);
+                if (t + 1 < S && hh + 1 < H) yg[hh + 1] = v.y + fmaf(bS[hh + 1], sr, mr);
               }
             }
           }
@@ -655,7 +687,8 @@ bool plan_mma_kernel(const FwdArgs& a, int max_smem_optin, MmaPlan* p) {
   MmaLayout& ly = p->ly;
   p->mt = a.N <= 16 ? 1 : 2;
   p->mmt = a.M <= 16 ? 1 : 2;
-  p->sc = a.S == 24 ? 24 : 0;
+  // the S = 24 instantiations implement the plain reading only (the widening runs generic)
+  p->sc = (a.S == 24 && !a.detrend && !a.revin) ? 24 : 0;
   ly.nr = 16 * p->mt;
   if (p->sc == 24) {  // dense rows of 24 halves (48 B: 16-byte aligned, conflict-free ldmatrix)
     ly.sph = 24;
@@ -712,7 +745,7 @@ static cudaError_t launch_sc(const FwdArgs& a, const MmaPlan& p, cudaStream_t st
 
 cudaError_t launch_mma_kernel(const FwdArgs& a, const MmaPlan& p, cudaStream_t st) {
   const bool dbg = a.a_s_dbg != nullptr;
-  if (p.sc == 24 && a.N == 30 && !dbg)   // L = 720, S = 24: configs[1..3]
+  if (p.sc == 24 && a.N == 30 && !dbg)   // L = 720, S = 24: configs[1..3], plain reading
     return p.mmt == 1 ? launch_t<2, 1, 24, false, 30>(a, p, st)
                       : launch_t<2, 2, 24, false, 30>(a, p, st);
   if (p.sc == 24) return dbg ? launch_sc<24, true>(a, p, st) : launch_sc<24, false>(a, p, st);

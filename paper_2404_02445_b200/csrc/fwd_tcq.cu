@@ -118,8 +118,11 @@ __device__ __forceinline__ void sts128(unsigned char* p, uint4 v) {
 
 // NC > 0: compile-time segment count (30: every L = 720, S = 24 config) -> no column
 // masks; NC = 0: runtime N <= 32 with masks.
-template <int NC>
+template <int NC, bool WIDE>
 __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ctas_per_channel) {
+  // WIDE: the SURVEY §8(f) widening (detrended seasonal metric, instance normalisation) is
+  // compiled in; the plain instantiation is exactly the reading's kernel
+  const bool detrend = WIDE && a.detrend, revin = WIDE && a.revin;
   static_assert(NC % 2 == 0 && NC <= 32, "NC");
   extern __shared__ __align__(1024) unsigned char smem[];
   constexpr int S = 24;
@@ -210,6 +213,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
     const int64_t b = g0 + 4 * rd + s;
     const bool active = b < g1;
     float sx = 1.f, mi = 0.f, ki = 0.f;
+    float sr = 1.f, mr = 0.f;   // forecast de-normalisation y = yhat sr + mr (instance_norm)
     float xv[24];   // the segment row, then X' = x sx (stored after the Gram issue)
 
     // ---------------- a1+a2: segment row i (Def 2) from the TMA staging, descriptors
@@ -251,44 +255,67 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
       }
       const float m1 = (s1.x + s1.y) * (1.f / 24.f);
       const float mu = x0 + m1;
-      const float kap = (s3.x + s3.y) * a.inv_v;
+      const float s3s = s3.x + s3.y;
+      const float kap = s3s * a.inv_v;
       float2 q2 = f2(0.f);
       const float2 nm1 = f2(-m1);
+      if (!detrend) {
 #pragma unroll
-      for (int t = 0; t < 24; t += 2) {
-        const float2 z = add2(make_float2(dv[t], dv[t + 1]), nm1);
-        dv[t] = z.x;
-        dv[t + 1] = z.y;
-        q2 = fma2(z, z, q2);
+        for (int t = 0; t < 24; t += 2) {
+          const float2 z = add2(make_float2(dv[t], dv[t + 1]), nm1);
+          dv[t] = z.x;
+          dv[t + 1] = z.y;
+          q2 = fma2(z, z, q2);
+        }
+      } else {
+        // metric_variant bit 1: the seasonal metric sees the residual
+        // e = z - kappa t~ about the segment's least-squares line
+        const float2 nk2 = f2(-kap);
+#pragma unroll
+        for (int t = 0; t < 24; t += 2) {
+          const float2 e = fma2(nk2, c_ttilde[t / 2], add2(make_float2(dv[t], dv[t + 1]), nm1));
+          dv[t] = e.x;
+          dv[t + 1] = e.y;
+          q2 = fma2(e, e, q2);
+        }
       }
-      const float nu2 = q2.x + q2.y;
-      const float inv = rsqrtf(nu2 + kEpsSeasonal);
-      const float nu = sqrtf(nu2);
-      // |x_t| <= |mu| + |z_t| <= |mu| + nu: an exact power-of-two scale for X' from it
-      sx = pow2_scale(warp_max_nonneg(valid ? fabsf(mu) + nu : 0.f));
-      {
-        const float2 zs2 = f2(valid ? inv : 0.f), xs2 = f2(valid ? sx : 0.f);
+      const float nu2s = q2.x + q2.y;                        // |z|^2, or |e|^2 (detrended)
+      // Def 4: nu2 = |z|^2 = |e|^2 + kappa^2 V (e orthogonal to t~) for Def 5
+      const float nu2 = detrend ? fmaf(s3s, kap, nu2s) : nu2s;
+      // Z' = (e or z) rr / sqrt(nu2 rr^2 + eps_s) and X' = (x - mu_r) rr sx as split-fp16 rows
+      // of the Gram / head operand tiles.  Plain path (rr = 1, mu_r = 0): written before the
+      // sigma^2 shuffle tree, off its dependency chain; instance_norm: after it.
+      auto write_operands = [&](float mu_r, float rr) {
+        const float zsc = rr * rsqrtf(nu2s * rr * rr + kEpsSeasonal);
+        // |xhat_t| <= (|mu - mu_r| + |kappa| 11.5 [detrended] + |e or z|) rr: an exact
+        // power-of-two scale for X' from it
+        const float bnd =
+            (fabsf(mu - mu_r) + (detrend ? 11.5f * fabsf(kap) : 0.f) + sqrtf(nu2s)) * rr;
+        sx = pow2_scale(warp_max_nonneg(valid ? bnd : 0.f));
+        const float2 zs2 = f2(valid ? zsc : 0.f), xs2 = f2(valid ? rr * sx : 0.f);
+        const float2 xo2 = f2(valid ? -mu_r * rr * sx : 0.f);
 #pragma unroll
         for (int t = 0; t < 24; t += 2) {
           const float2 zz = mul2(make_float2(dv[t], dv[t + 1]), zs2);
-          const float2 xx = mul2(make_float2(xv[t], xv[t + 1]), xs2);
+          const float2 xx = fma2(make_float2(xv[t], xv[t + 1]), xs2, xo2);
           dv[t] = zz.x;
           dv[t + 1] = zz.y;
           xv[t] = xx.x;
           xv[t + 1] = xx.y;
         }
-      }
-      const int zrow = PRNET_TCQ_FRAG ? pi_inv(i) : i;   // Gram position of segment i
-      unsigned char* zr = zq + (4 * s + (zrow >> 3)) * 1024 + (zrow & 7) * 16;
+        const int zrow = PRNET_TCQ_FRAG ? pi_inv(i) : i;   // Gram position of segment i
+        unsigned char* zr = zq + (4 * s + (zrow >> 3)) * 1024 + (zrow & 7) * 16;
 #pragma unroll
-      for (int q = 0; q < 3; q++) {
-        uint4 h, l;
-        split8(dv + 8 * q, h, l);
-        sts128(zr + q * 128, h);          // K chunks: h0 h1 h2 | l0 l1 l2 | h2 | 0
-        sts128(zr + (3 + q) * 128, l);
-        if (q == 2) sts128(zr + 6 * 128, h);
-      }
-      sts128(zr + 7 * 128, make_uint4(0u, 0u, 0u, 0u));   // (the tile held Q' last round)
+        for (int q = 0; q < 3; q++) {
+          uint4 h, l;
+          split8(dv + 8 * q, h, l);
+          sts128(zr + q * 128, h);          // K chunks: h0 h1 h2 | l0 l1 l2 | h2 | 0
+          sts128(zr + (3 + q) * 128, l);
+          if (q == 2) sts128(zr + 6 * 128, h);
+        }
+        sts128(zr + 7 * 128, make_uint4(0u, 0u, 0u, 0u));   // (the tile held Q' last round)
+      };
+      if (!revin) write_operands(0.f, 1.f);
       // Def 5: sigma^2 = (1/(N S)) sum_n [nu2_n + S (mu_n - mubar)^2], both sums in one
       // shuffle tree about the reference m0 = mu_0: with d = mu - m0,
       // sum_n (mu_n - mubar)^2 = sum d^2 - (sum d)^2 / N (exact; no cancellation against
@@ -300,12 +327,24 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
       for (int o = 16; o > 0; o >>= 1)
         acc = add2(acc, make_float2(__shfl_xor_sync(0xffffffffu, acc.x, o),
                                     __shfl_xor_sync(0xffffffffu, acc.y, o)));
-      const float inv_var =
-          1.0f / (fmaf(-24.f * acc.x, acc.x * a.inv_n, acc.y) * a.inv_ns + kEpsTrend);
-      // trend (Def 7-8): exponent -(mu~_i - mu~_j)^2 - (k~_i - k~_j)^2, mu~ = mu sqrt(kt/var'),
-      // k~ = kappa sqrt(vtrend kt/var')
-      mi = mu * sqrtf(inv_var * a.kt);
-      ki = kap * sqrtf(a.vtrend * inv_var * a.kt);
+      const float var = fmaf(-24.f * acc.x, acc.x * a.inv_n, acc.y) * a.inv_ns;
+      // instance normalisation: xhat = (x - mu_r) rr with the mean
+      // mu_r and variance var of the segmented points; every descriptor of xhat is the
+      // descriptor of x mapped affinely (mu -> (mu - mu_r) rr, z, e, kappa -> * rr), so only
+      // scalars change.  Off: mu_r = 0, rr = sr = 1 exactly (bitwise the plain path).
+      float mu_r = 0.f, rr = 1.f;
+      if (revin) {
+        mu_r = fmaf(acc.x, a.inv_n, m0);
+        rr = rsqrtf(var + kEpsRevin);
+        sr = (var + kEpsRevin) * rr;
+        mr = mu_r;
+        write_operands(mu_r, rr);
+      }
+      const float inv_var = 1.0f / fmaf(var * rr, rr, kEpsTrend);
+      // trend (Def 7-8): exponent -(mu~_i - mu~_j)^2 - (k~_i - k~_j)^2, mu~ = muhat sqrt(kt/var'),
+      // k~ = kappahat sqrt(vtrend kt/var')
+      mi = (mu - mu_r) * rr * sqrtf(inv_var * a.kt);
+      ki = kap * rr * sqrtf(a.vtrend * inv_var * a.kt);
 #if PRNET_TCQ_FRAG
       // (mu~, k~) pairs; past N a far-away but finite mu~ (exponent -1e36 -> 0, no inf - inf)
       reinterpret_cast<float2*>(colv)[i] = make_float2(valid ? mi : 1e18f, ki);
@@ -653,7 +692,8 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
         }
       }
       // ---------------- a8 store: y = Y' / (sw sx) + b (Def 11), pairs (m, t..t+1)
-      const float2 ys2 = f2(inv_sw / sx);
+      const float2 ys2 = f2(inv_sw * sr / sx);
+      const float2 sr2 = f2(sr), mr2 = f2(mr);
       float* yg = ycur + 2 * (lane & 3);
       const float* bq = bS + 2 * (lane & 3);
       if (full_rows) {   // H = 24 M, H even: every (m < M, t) pair is stored, no tail
@@ -667,7 +707,8 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
               const float* br = bq + m * kQBiasRow;
 #pragma unroll
               for (int nt = 0; nt < 3; nt++) {
-                const float2 bb = *reinterpret_cast<const float2*>(br + 8 * nt);
+                float2 bb = *reinterpret_cast<const float2*>(br + 8 * nt);
+                if (revin) bb = fma2(bb, sr2, mr2);   // y = yhat sr + mr
                 const float2 o = fma2(make_float2(acc[mt][nt][2 * h], acc[mt][nt][2 * h + 1]), ys2, bb);
                 asm volatile("st.global.cs.v2.f32 [%0], {%1,%2};" ::"l"(yr + 8 * nt), "f"(o.x),
                              "f"(o.y)
@@ -685,7 +726,8 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
 #pragma unroll
             for (int nt = 0; nt < 3; nt++) {
               const int hh = m * 24 + 8 * nt + 2 * (lane & 3);
-              const float2 bb = *reinterpret_cast<const float2*>(bq + m * kQBiasRow + 8 * nt);
+              float2 bb = *reinterpret_cast<const float2*>(bq + m * kQBiasRow + 8 * nt);
+              if (revin) bb = fma2(bb, sr2, mr2);
               const float2 o = fma2(make_float2(acc[mt][nt][2 * h], acc[mt][nt][2 * h + 1]), ys2, bb);
               if (hh < H) yg[m * 24 + 8 * nt] = o.x;
               if (hh + 1 < H) yg[m * 24 + 8 * nt + 1] = o.y;
@@ -722,13 +764,17 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
       tld_wait();
       const int m = lane;
       if (m < M) {
-        const float2 ys2 = f2(inv_sw / sx);
+        const float2 ys2 = f2(inv_sw * sr / sx);
         float* yg = ycur + m * 24;
         const float* bm = bS + m * kQBiasRow;
         if ((H & 3) == 0 && m * 24 + 24 <= H) {
 #pragma unroll
           for (int q = 0; q < 6; q++) {
-            const float4 bb = *reinterpret_cast<const float4*>(bm + 4 * q);
+            float4 bb = *reinterpret_cast<const float4*>(bm + 4 * q);
+            if (revin) {
+              bb.x = fmaf(bb.x, sr, mr); bb.y = fmaf(bb.y, sr, mr);
+              bb.z = fmaf(bb.z, sr, mr); bb.w = fmaf(bb.w, sr, mr);
+            }
             const float2 o0 = fma2(make_float2(__uint_as_float(yv[4 * q]), __uint_as_float(yv[4 * q + 1])),
                                    ys2, make_float2(bb.x, bb.y));
             const float2 o1 = fma2(make_float2(__uint_as_float(yv[4 * q + 2]), __uint_as_float(yv[4 * q + 3])),
@@ -738,7 +784,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
         } else {
 #pragma unroll
           for (int t = 0; t < 24; t++)
-            if (m * 24 + t < H) yg[t] = fmaf(__uint_as_float(yv[t]), ys2.x, bm[t]);
+            if (m * 24 + t < H) yg[t] = fmaf(__uint_as_float(yv[t]), ys2.x, fmaf(bm[t], sr, mr));
         }
       }
     }
@@ -761,9 +807,9 @@ bool plan_tcq_kernel(const FwdArgs& a, int max_smem_optin, TcqPlan* p) {
   return true;
 }
 
-template <int NC>
+template <int NC, bool WIDE>
 static cudaError_t launch_tcq_t(const FwdArgs& a, const TcqPlan& p, cudaStream_t st) {
-  auto k = prnet_fwd_tcq_kernel<NC>;
+  auto k = prnet_fwd_tcq_kernel<NC, WIDE>;
   cudaError_t e =
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
@@ -775,7 +821,9 @@ static cudaError_t launch_tcq_t(const FwdArgs& a, const TcqPlan& p, cudaStream_t
 }
 
 cudaError_t launch_tcq_kernel(const FwdArgs& a, const TcqPlan& p, cudaStream_t st) {
-  return a.N == 30 ? launch_tcq_t<30>(a, p, st) : launch_tcq_t<0>(a, p, st);
+  const bool wide = a.detrend || a.revin;
+  if (a.N == 30) return wide ? launch_tcq_t<30, true>(a, p, st) : launch_tcq_t<30, false>(a, p, st);
+  return wide ? launch_tcq_t<0, true>(a, p, st) : launch_tcq_t<0, false>(a, p, st);
 }
 
 }  // namespace prnet

@@ -2,6 +2,7 @@
 // kernel-variant selection, and the host-buffer streaming runtime
 // (prnet_forward_host).  No torch types, no exceptions across the boundary.
 #include <cmath>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -93,7 +94,10 @@ prnet::FwdArgs make_args(const prnet_handle* h, const float* x, int64_t B, float
   const double S = c.seg_len;
   a.half_s = (float)(0.5 * (S - 1.0));
   a.inv_v = (float)(12.0 / (S * (S * S - 1.0)));
-  a.vtrend = (float)((S * S - 1.0) / 12.0);
+  // metric_variant bit 0 (level-only trend): the kappa term of Def 7 drops
+  a.vtrend = (c.metric_variant & 1) ? 0.f : (float)((S * S - 1.0) / 12.0);
+  a.detrend = (c.metric_variant >> 1) & 1;
+  a.revin = c.instance_norm;
   a.inv_s = (float)(1.0 / S);
   a.inv_n = (float)(1.0 / h->N);
   a.inv_ns = (float)(1.0 / ((double)h->N * S));
@@ -140,8 +144,20 @@ bool tc2_applicable(const prnet_handle* h) {
 bool tcq_applicable(const prnet_handle* h) {
   return h->cfg.seg_len == 24 && h->N <= 32 && h->M <= 32 && h->cfg.tau_seasonal >= 0.0125f;
 }
+// Variants that implement the SURVEY §8(f) widening: the level-only trend runs in every
+// kernel (a.vtrend = 0); the detrended seasonal metric and instance normalisation only in
+// tc_quad and mma_f16x3 (N <= 32).
+bool widening_on(const prnet_handle* h) {
+  return (h->cfg.metric_variant & 2) != 0 || h->cfg.instance_norm != 0;
+}
+bool variant_supports_widening(int v) { return v == 2 || v == 6; }
 int pick_variant(const prnet_handle* h) {
   if (h->forced_variant >= 0) return h->forced_variant;
+  if (widening_on(h)) {
+    if (tcq_applicable(h)) return 6;
+    if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
+    return -1;   // no kernel implements it for this shape
+  }
   // measured on B200 (profiles/README.md): tc_quad is the fastest S = 24 path (Traffic
   // 6.37 ms vs 6.60 ms for mma_f16x3), mma_f16x3 the fastest other N <= 32 path;
   // tc_fold and tc_full are selectable with prnet_set_kernel_variant
@@ -159,6 +175,10 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
   a.a_t_dbg = a_t;
   cudaError_t e;
   int v = pick_variant(h);
+  if (v < 0 || (widening_on(h) && !variant_supports_widening(v)))
+    return fail(h, PRNET_ERR_UNSUPPORTED,
+                "metric_variant bit 1 / instance_norm are implemented for N <= 32, M <= 32, "
+                "S <= 128 (kernels tc_quad, mma_f16x3)");
   if (v == 1 && a_s != nullptr) v = 0;  // the attention dump lives in the N <= 32 kernels
   if (v == 6 && a_s != nullptr) v = 2;
   static const int wpc_env = [] {  // tuning knob: windows per CTA (0 = plan default)
@@ -241,15 +261,26 @@ extern "C" {
 prnet_status prnet_create(const prnet_config* cfg, prnet_handle** out) {
   if (out) *out = nullptr;
   if (!cfg || !out) return fail(nullptr, PRNET_ERR_INVALID_ARG, "NULL cfg or out");
-  if (cfg->abi_version != PRNET_ABI_VERSION)
-    return fail(nullptr, PRNET_ERR_INVALID_ARG, "abi_version mismatch");
+  if (cfg->abi_version != 1 && cfg->abi_version != PRNET_ABI_VERSION)
+    return fail(nullptr, PRNET_ERR_INVALID_ARG, "abi_version must be 1 or 2");
+  // a v1 caller's struct ends at `device`: copy only what it owns
+  prnet_config c2{};
+  if (cfg->abi_version == 1)
+    std::memcpy(&c2, cfg, offsetof(prnet_config, instance_norm));
+  else
+    c2 = *cfg;
+  c2.abi_version = PRNET_ABI_VERSION;
+  cfg = &c2;
   if (cfg->channels < 1 || cfg->seg_len < 2 || cfg->lookback < cfg->seg_len || cfg->horizon < 1)
     return fail(nullptr, PRNET_ERR_INVALID_ARG, "need C >= 1, S >= 2, L >= S, H >= 1");
   if (!(cfg->tau_seasonal > 0.f) || !std::isfinite(cfg->tau_seasonal) ||
       !(cfg->tau_trend > 0.f) || !std::isfinite(cfg->tau_trend))
     return fail(nullptr, PRNET_ERR_INVALID_ARG, "temperatures must be finite and > 0");
-  if (cfg->metric_variant != 0)
-    return fail(nullptr, PRNET_ERR_INVALID_ARG, "metric_variant must be 0 (others reserved)");
+  if (cfg->metric_variant < 0 || cfg->metric_variant > 3)
+    return fail(nullptr, PRNET_ERR_INVALID_ARG,
+                "metric_variant must be in [0, 3] (bit 0 level trend, bit 1 detrended seasonal)");
+  if (cfg->instance_norm != 0 && cfg->instance_norm != 1)
+    return fail(nullptr, PRNET_ERR_INVALID_ARG, "instance_norm must be 0 or 1");
   if (cfg->channels > 65535)
     return fail(nullptr, PRNET_ERR_UNSUPPORTED, "C > 65535 not supported");
   int ndev = 0;
@@ -524,6 +555,9 @@ prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {
     return fail(h, PRNET_ERR_UNSUPPORTED, "variant needs N <= 32");
   if (variant == 2 && (h->M > 32 || h->cfg.seg_len > 128))
     return fail(h, PRNET_ERR_UNSUPPORTED, "tensor-core variant needs M <= 32 and S <= 128");
+  if (variant >= 0 && widening_on(h) && !variant_supports_widening(variant))
+    return fail(h, PRNET_ERR_UNSUPPORTED,
+                "metric_variant bit 1 / instance_norm need tc_quad or mma_f16x3");
   h->forced_variant = variant;
   return PRNET_OK;
 }

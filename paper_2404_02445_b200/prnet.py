@@ -15,7 +15,7 @@ import numpy as np
 _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libprnet.so")
 _lib = None
 
-PRNET_ABI_VERSION = 1
+PRNET_ABI_VERSION = 2
 STATUS = {0: "PRNET_OK", 1: "PRNET_ERR_INVALID_ARG", 2: "PRNET_ERR_BAD_STATE",
           3: "PRNET_ERR_UNSUPPORTED", 4: "PRNET_ERR_CUDA", 5: "PRNET_ERR_OOM"}
 
@@ -38,7 +38,8 @@ class PrnetConfig(ctypes.Structure):
                 ("lookback", ctypes.c_int32), ("seg_len", ctypes.c_int32),
                 ("horizon", ctypes.c_int32), ("head_per_channel", ctypes.c_int32),
                 ("metric_variant", ctypes.c_int32), ("tau_seasonal", ctypes.c_float),
-                ("tau_trend", ctypes.c_float), ("device", ctypes.c_int32)]
+                ("tau_trend", ctypes.c_float), ("device", ctypes.c_int32),
+                ("instance_norm", ctypes.c_int32)]        # ABI 2
 
 
 def load_library(path: str | None = None):
@@ -85,10 +86,13 @@ class PRNet:
 
     def __init__(self, channels: int, lookback: int, seg_len: int, horizon: int,
                  head_per_channel: bool = True, tau_s: float = 1.0, tau_t: float = 1.0,
-                 device: int = 0):
+                 device: int = 0, metric_variant: int = 0, instance_norm: bool = False):
+        """metric_variant: bit 0 level-only trend, bit 1 detrended seasonal metric;
+        instance_norm: RevIN-style normalisation (include/prnet.h)."""
         self._lib = load_library()
         cfg = PrnetConfig(PRNET_ABI_VERSION, channels, lookback, seg_len, horizon,
-                          int(bool(head_per_channel)), 0, tau_s, tau_t, device)
+                          int(bool(head_per_channel)), int(metric_variant), tau_s, tau_t, device,
+                          int(bool(instance_norm)))
         h = ctypes.c_void_p()
         st = self._lib.prnet_create(ctypes.byref(cfg), ctypes.byref(h))
         if st != 0:

@@ -286,3 +286,74 @@ def test_abi_errors():
     with pytest.raises(PrnetError) as e:
         m.forward(torch.zeros((2, 3, 96)))   # host pointer on the device entry
     assert e.value.status == 3
+
+
+# ------------------------------------------------------------ SURVEY §8(f) widening (f1, f3)
+def _check_widening(oracle_mod, x, S, H, mv, rev, variant=None, tau_s=1.0, tau_t=1.0, hpc=True):
+    B, C, L = x.shape
+    N, _, M = synth.derived_dims(L, S, H)
+    ws, wt, b = synth.make_params(C, M, N, H, hpc, synth.DEFAULT_SEED, 0)
+    m = PRNet(C, L, S, H, head_per_channel=hpc, tau_s=tau_s, tau_t=tau_t, metric_variant=mv,
+              instance_norm=rev).load(ws, wt, b)
+    if variant is not None:
+        m.set_variant(variant)
+    y = m.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+    _, y64 = oracle_mod.forward(x, S, H, ws, wt, b, hpc, tau_s, tau_t, metric_variant=mv,
+                                instance_norm=rev)
+    scale = None
+    if rev:   # the de-normalised forecast carries the input's level and scale
+        scale = np.maximum(np.abs(x).max(axis=2, keepdims=True)[..., :1], 1.0)
+    return assert_parity(y, y64, scale=scale)
+
+
+@pytest.mark.parametrize("variant", [None, "tc_quad", "mma_f16x3"])
+@pytest.mark.parametrize("mv,rev", [(1, False), (2, False), (3, False), (0, True), (3, True)])
+@pytest.mark.parametrize("L,S,H", [(720, 24, 720), (720, 24, 336), (100, 24, 90), (96, 24, 96),
+                                   (97, 7, 13), (128, 8, 64), (270, 9, 31)])
+def test_widening_parity(oracle_mod, L, S, H, mv, rev, variant):
+    if variant == "tc_quad" and S != 24:
+        pytest.skip("tc_quad needs S = 24")
+    x = synth.random_windows(3, 5, L, kind="mixed")
+    _check_widening(oracle_mod, x, S, H, mv, rev, variant)
+
+
+@pytest.mark.parametrize("kind", ["normal", "constant", "scaled"])
+@pytest.mark.parametrize("rev", [False, True])
+def test_widening_value_distributions(oracle_mod, kind, rev):
+    x = synth.random_windows(3, 4, 720, kind=kind)
+    if kind == "scaled" and not rev:
+        pytest.skip("covered by test_value_distributions")
+    _check_widening(oracle_mod, x, 24, 96, 3 if not rev else 2, rev)
+
+
+@pytest.mark.parametrize("tau", [0.05, 1.0, 10.0])
+@pytest.mark.parametrize("hpc", [True, False])
+def test_widening_temperatures_and_head_modes(oracle_mod, tau, hpc):
+    x = synth.random_windows(4, 6, 720, kind="mixed")
+    _check_widening(oracle_mod, x, 24, 336, 3, True, tau_s=tau, tau_t=tau * 0.7, hpc=hpc)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_level_trend_every_variant(oracle_mod, variant):
+    """metric_variant bit 0 only changes a scalar (vtrend = 0): every kernel implements it."""
+    for L, S, H in [(720, 24, 96), (1440, 24, 96), (97, 7, 13)]:
+        N, _, M = synth.derived_dims(L, S, H)
+        if not _applicable(variant, L, S, H):
+            continue
+        x = synth.random_windows(2, 3, L, kind="mixed")
+        _check_widening(oracle_mod, x, S, H, 1, False, variant)
+
+
+def test_widening_unsupported_paths():
+    m = PRNet(3, 1440, 24, 96, metric_variant=2)        # N = 60: no kernel implements bit 1
+    N, _, M = m.N, m.M, m.M
+    m.load(np.zeros((3, m.M, m.N)), np.zeros((3, m.M, m.N)), np.zeros((3, 96)))
+    with pytest.raises(PrnetError) as e:
+        m.forward(torch.zeros((2, 3, 1440), device="cuda"))
+    assert e.value.status == 3
+    m2 = PRNet(3, 720, 24, 96, instance_norm=True)
+    with pytest.raises(PrnetError) as e:
+        m2.set_variant("warp_f32")
+    assert e.value.status == 3
+    m3 = PRNet(3, 720, 24, 96, metric_variant=1)         # level-only: any variant
+    m3.set_variant("warp_f32")
