@@ -77,3 +77,24 @@ def test_create_validates_before_touching_the_device(lib):
         assert lib.prnet_last_error(None)
     assert lib.prnet_forward(None, None, 0, None, None) == 2
     lib.prnet_destroy(None)
+
+
+def test_abi_v1_struct_still_accepted(lib):
+    """An ABI-1 caller (struct ending at `device`) is validated and then reaches the device
+    check (no GPU here: UNSUPPORTED), i.e. not rejected as a wrong abi_version."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+
+    class ConfigV1(ctypes.Structure):
+        _fields_ = [("abi_version", ctypes.c_int32), ("channels", ctypes.c_int32),
+                    ("lookback", ctypes.c_int32), ("seg_len", ctypes.c_int32),
+                    ("horizon", ctypes.c_int32), ("head_per_channel", ctypes.c_int32),
+                    ("metric_variant", ctypes.c_int32), ("tau_seasonal", ctypes.c_float),
+                    ("tau_trend", ctypes.c_float), ("device", ctypes.c_int32)]
+    h = ctypes.c_void_p(123)
+    cfg = ConfigV1(1, 7, 96, 24, 96, 1, 0, 1.0, 1.0, 0)
+    from paper_2404_02445_b200 import PrnetConfig
+    assert lib.prnet_create(ctypes.cast(ctypes.pointer(cfg), ctypes.POINTER(PrnetConfig)),
+                            ctypes.byref(h)) == 3
+    assert h.value is None
