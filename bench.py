@@ -202,6 +202,9 @@ def main():
                     help="SURVEY 8(f) f3: bit 0 level-only trend, bit 1 detrended seasonal")
     ap.add_argument("--instance-norm", action="store_true",
                     help="SURVEY 8(f) f1: RevIN-style instance normalisation")
+    ap.add_argument("--sliding", action="store_true",
+                    help="SURVEY 8(f) f2: forecast the test windows straight from the [C][T] "
+                         "series (prnet_forward_sliding); e2e uploads the series span once")
     ap.add_argument("--host-chunk", type=int, default=0,
                     help="windows per chunk of the host-buffer pipeline (0 = library default)")
     args = ap.parse_args()
@@ -216,6 +219,10 @@ def main():
            "parallelism": f"dp{world}", "seed": args.seed}
     if args.metric_variant or args.instance_norm:
         cfg.update(metric_variant=args.metric_variant, instance_norm=bool(args.instance_norm))
+    if args.sliding:
+        cfg.update(input="sliding windows of the [C][T] series (prnet_forward_sliding)",
+                   l2=f"series span {w.C * (B + w.L - 1) * 4 / 1e6:.1f} MB (L2-resident); "
+                      f"outputs {B * w.C * w.H * 4 / 1e9:.2f} GB written per step")
 
     if args.impl == "reference":
         if rank != 0:
@@ -268,7 +275,8 @@ def main():
     x = sd.unfold(1, w.L, 1)[:, w.t0 + start:w.t0 + start + count, :].permute(1, 0, 2).contiguous()
     tgt = sd[:, w.L:].unfold(1, w.H, 1)[:, w.t0 + start:w.t0 + start + count, :] \
         .permute(1, 0, 2).contiguous()
-    del sd
+    if not args.sliding:
+        del sd
     ws, wt, b = synth.make_params(w.C, M, N, w.H, True, args.seed, w.cfg_id)
     model = PRNet(w.C, w.L, w.S, w.H, device=dev, metric_variant=args.metric_variant,
                   instance_norm=args.instance_norm).load(ws, wt, b)
@@ -278,8 +286,19 @@ def main():
     stream = torch.cuda.current_stream()
     plan = model.plan(count)
 
+    if args.sliding:
+        t0s = w.t0 + start
+        y_ref = model.forward(x)
+        del x
+        fwd = lambda: model.forward_sliding_into(sd, t0s, count, y, stream)  # noqa: E731
+        fwd()
+        torch.cuda.synchronize()
+        assert torch.equal(y, y_ref), "sliding forward disagrees with the materialised windows"
+        del y_ref
+    else:
+        fwd = lambda: model.forward_into(x, y, stream)  # noqa: E731
     for _ in range(args.warmup):
-        model.forward_into(x, y, stream)
+        fwd()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -290,7 +309,7 @@ def main():
         t_wall = time.perf_counter()
         for e0, e1 in ev:
             e0.record(stream)
-            model.forward_into(x, y, stream)
+            fwd()
             e1.record(stream)
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall
@@ -316,7 +335,32 @@ def main():
 
     # ---- end to end through the public API with HOST buffers (H2D + kernel + D2H timed)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.sliding:
+        try:
+            sh = torch.empty(sd.shape, dtype=torch.float32, pin_memory=True)
+            sh.copy_(sd)
+            yh = torch.empty(y.shape, dtype=torch.float32, pin_memory=True)
+            model.forward_sliding_host(sh, t0s, count, yh,
+                                       chunk_windows=args.host_chunk or None)   # warm-up
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            for _ in range(args.e2e_steps):
+                model.forward_sliding_host(sh, t0s, count, yh)
+            dt = torch.tensor([(time.perf_counter() - t0) / args.e2e_steps], dtype=torch.float64,
+                              device=coll)
+            if world > 1:
+                dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            assert torch.equal(yh, y.cpu()), "host sliding path disagrees with the device path"
+            e2e = {"value": B / float(dt.item()), "unit": "windows/s",
+                   "h2d_bytes_per_step": int(w.C * (count + w.L - 1) * 4) * world,
+                   "d2h_bytes_per_step": int(yh.numel() * 4) * world,
+                   "steps": args.e2e_steps,
+                   "path": "prnet_forward_sliding_host (pinned host series, span uploaded once)"}
+            del sh, yh
+        except Exception as ex:  # report, never fake
+            e2e = {"value": None, "unit": "windows/s", "error": str(ex)[:200]}
+    elif not args.no_e2e:
         try:
             xh = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
             xh.copy_(x)
@@ -347,8 +391,12 @@ def main():
 
     value = B / (ms_per_step / 1e3)
     bytes_per_series = 4 * (w.L + w.H)
+    launch_bytes = count * w.C * bytes_per_series
+    if args.sliding:   # the series span is read once, the outputs written once
+        bytes_per_series = 4 * w.H + 4 * (count + w.L - 1) / count
+        launch_bytes = 4 * w.C * (count + w.L - 1) + 4 * count * w.C * w.H
     launch_ms = statistics.mean(per_launch)
-    achieved_gbs = count * w.C * bytes_per_series / (launch_ms / 1e3) / 1e9
+    achieved_gbs = launch_bytes / (launch_ms / 1e3) / 1e9
     peak_gbs = float(peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"]))
     fl = flops_per_series(N, w.S, M)
     achieved_tf = count * w.C * fl / (launch_ms / 1e3) / 1e12
@@ -359,7 +407,7 @@ def main():
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(w.name)
+            traffic = None if args.sliding else json.load(open(prof)).get(w.name)
         except Exception:
             traffic = None
 
@@ -383,7 +431,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak_gbs, "unit": "GB/s",
                      "frac": achieved_gbs / peak_gbs, "traffic": traffic,
                      "kernel": f"prnet_fwd_{plan['variant']}", "launch_ms": launch_ms,
-                     "bytes_per_launch": count * w.C * bytes_per_series, "peak_source": peak_src},
+                     "bytes_per_launch": launch_bytes, "peak_source": peak_src},
         "roofline_alu": {"bound": "alu", "achieved": achieved_tf, "unit": "TFLOP/s",
                          "peak": fp32_peak, "frac": achieved_tf / fp32_peak,
                          "flops_per_series": fl,

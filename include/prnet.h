@@ -112,6 +112,24 @@ prnet_status prnet_forward(prnet_handle* h, const float* x, int64_t batch, float
 prnet_status prnet_forward_host(prnet_handle* h, const float* x_host, int64_t batch,
                                 float* y_host);
 
+/* Sliding-window input mode (NS: "full sliding-window test set").
+ * series: DEVICE, [C][T] fp32 row-major (channel c's T time steps contiguous),
+ * 16-byte aligned.  Window b (0 <= b < batch) is x[b][c][l] = series[c][t0 + b + l],
+ * l < L, so the B windows of a test set are read from C (B + L - 1) floats instead of
+ * B C L.  Requires 0 <= t0 and t0 + batch - 1 + L <= T (PRNET_ERR_INVALID_ARG otherwise).
+ * y: DEVICE [batch][C][H] as prnet_forward.  The result is bitwise the prnet_forward
+ * result on the materialised windows.  Enqueue-only, no workspace, like prnet_forward. */
+prnet_status prnet_forward_sliding(prnet_handle* h, const float* series, int64_t T,
+                                   int64_t t0, int64_t batch, float* y, void* cuda_stream);
+
+/* As prnet_forward_sliding with HOST buffers (end-to-end entry): the series span
+ * [t0, t0 + batch - 1 + L) of every channel is copied to the device once (pitched),
+ * then the windows are forecast in chunks whose device->host copies overlap the next
+ * chunk's kernel (three streams, workspace owned by the handle).  Blocking.  Pinned
+ * host memory gets full PCIe bandwidth. */
+prnet_status prnet_forward_sliding_host(prnet_handle* h, const float* series, int64_t T,
+                                        int64_t t0, int64_t batch, float* y_host);
+
 /* Windows per chunk for prnet_forward_host (default: ~256 MiB of input per
  * chunk).  windows_per_chunk >= 1. */
 prnet_status prnet_set_host_chunk(prnet_handle* h, int64_t windows_per_chunk);

@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(256, 1) prnet_fwd_flash_kernel(FwdArgs a, Flas
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int c = blockIdx.y;
   const int cw = a.head_per_channel ? c : 0;
-  const int S = a.S, N = a.N, H = a.H, L = a.L, C = a.C;
+  const int S = a.S, N = a.N, H = a.H, C = a.C;
   const int NP = ly.npad, NT = NP / 16, ZP = ly.zph, XP = ly.xph;
 
   float* xbuf = reinterpret_cast<float*>(smem);
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(256, 1) prnet_fwd_flash_kernel(FwdArgs a, Flas
     const int64_t series = b * C + c;
     // ---------------- a1: load the segmented span
     {
-      const float* xg = a.x + series * L + a.r;
+      const float* xg = a.x + b * a.xsb + c * a.xsc + a.r;
       for (int k = tid; k < N * S; k += nthr) xbuf[k] = __ldg(xg + k);
     }
     __syncthreads();

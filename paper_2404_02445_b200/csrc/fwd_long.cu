@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(256) prnet_fwd_long_kernel(FwdArgs a, int rs) 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
-  const int S = a.S, N = a.N, M = a.M, H = a.H, L = a.L, C = a.C;
+  const int S = a.S, N = a.N, M = a.M, H = a.H, C = a.C;
   const int MS = M * S;
 
   float* xr = smem;               // [N][rs]  segments, odd row stride
@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(256) prnet_fwd_long_kernel(FwdArgs a, int rs) 
     const float* gwt = a.wt + (int64_t)cw * M * N;
 
     // ---- a1: load + segment
-    const float* xg = a.x + series * L + a.r;
+    const float* xg = a.x + (series / C) * a.xsb + c * a.xsc + a.r;
     for (int k = threadIdx.x; k < N * S; k += blockDim.x) {
       const int n = k / S, t = k - n * S;
       xr[n * rs + t] = __ldg(xg + k);

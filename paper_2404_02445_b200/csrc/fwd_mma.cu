@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
   // NC > 0: compile-time segment count (30: every L = 720, S = 24 config), so the
   // j < N / i < N masks fold away
   const int N = NC > 0 ? NC : a.N;
-  const int M = a.M, H = a.H, L = a.L, C = a.C;
+  const int M = a.M, H = a.H, C = a.C;
   // operand row strides (halves): dense rows when S is the compile-time 24
   const int sph = SC > 0 ? SC : ly.sph;
   const int zph = SC > 0 ? SC : ly.zph;
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
   }
   __syncthreads();
 
-  const bool vec_x = ((L & 3) == 0) && ((a.r & 3) == 0);
+  const bool vec_x = a.x_vec;
   const int NS = N * S;
   // one bulk TMA per series when its segmented span is 16-byte aligned and sized
   const bool bulk = vec_x && ((NS & 3) == 0);
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
   if (b_end > a.B) b_end = a.B;
 
   auto prefetch = [&](int64_t b) {
-    const float* xg = a.x + (b * C + c) * L + a.r;
+    const float* xg = a.x + b * a.xsb + c * a.xsc + a.r;
     if (bulk) {
       if (lane == 0) bulk_load(xbuf, xg, (uint32_t)NS * 4u, xbar);
       return;

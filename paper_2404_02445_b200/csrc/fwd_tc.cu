@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(128, 4) prnet_fwd_tc_kernel(FwdArgs a, int win
   const int gq = lane >> 2, cq = lane & 3, q8 = lane >> 3;
   const int c = blockIdx.y;
   const int cw = a.head_per_channel ? c : 0;
-  const int N = a.N, M = a.M, H = a.H, L = a.L, C = a.C;
+  const int N = a.N, M = a.M, H = a.H, C = a.C;
   const int NS = N * S;
 
   unsigned char* atile = smem;
@@ -235,11 +235,11 @@ __global__ void __launch_bounds__(128, 4) prnet_fwd_tc_kernel(FwdArgs a, int win
   int64_t b_end = b_begin + wins_per_cta;
   if (b_end > a.B) b_end = a.B;
   const int rounds = (int)((b_end - b_begin + 3) / 4);
-  const bool vec_x = ((L & 3) == 0) && ((a.r & 3) == 0) && ((NS & 3) == 0);
+  const bool vec_x = a.x_vec && ((NS & 3) == 0);
   uint32_t xphase = 0, mphase = 0;
 
   auto issue_load = [&](int64_t bb) {
-    const float* xg = a.x + (bb * C + c) * L + a.r;
+    const float* xg = a.x + bb * a.xsb + c * a.xsc + a.r;
     if (vec_x) {
       if (lane == 0) bulk_load(xbuf, xg, (uint32_t)NS * 4u, xbar);
     } else {

@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(384, 1) prnet_fwd_tc2_kernel(FwdArgs a, int wi
   const int grp = warp >> 2, w = warp & 3;   // group, series slot in the group
   const int c = blockIdx.y;
   const int cw = a.head_per_channel ? c : 0;
-  const int N = a.N, M = a.M, H = a.H, L = a.L, C = a.C;
+  const int N = a.N, M = a.M, H = a.H, C = a.C;
   const int NS = N * S;
   const int i = lane;
 
@@ -212,11 +212,11 @@ __global__ void __launch_bounds__(384, 1) prnet_fwd_tc2_kernel(FwdArgs a, int wi
   int64_t g_end = g_begin + wins_per_group;
   if (g_end > a.B) g_end = a.B;
   const int rounds = g_end > g_begin ? (int)((g_end - g_begin + 3) / 4) : 0;
-  const bool vec_x = ((L & 3) == 0) && ((a.r & 3) == 0) && ((NS & 3) == 0);
+  const bool vec_x = a.x_vec && ((NS & 3) == 0);
   uint32_t xphase = 0, rphase = 0;
 
   auto issue_load = [&](int64_t bb) {
-    const float* xg = a.x + (bb * C + c) * L + a.r;
+    const float* xg = a.x + bb * a.xsb + c * a.xsc + a.r;
     if (vec_x) {
       if (lane == 0) bulk_load(xbuf, xg, (uint32_t)NS * 4u, xbar);
     } else {

@@ -74,7 +74,8 @@ __constant__ float2 c_ttilde[12] = {{-11.5f, -10.5f}, {-9.5f, -8.5f}, {-7.5f, -6
                                     {4.5f, 5.5f},     {6.5f, 7.5f},   {8.5f, 9.5f},   {10.5f, 11.5f}};
 constexpr int kQZQ = 16384;        // Z' tile, then Q' tile
 constexpr int kQXT = 12288;        // X' tile
-constexpr int kQStage = 3072;      // TMA staging per warp: N S fp32, N <= 32, S = 24
+constexpr int kQStage = 3104;      // TMA staging per warp: N S fp32 (N <= 32, S = 24) + the
+                                   // sliding mode's alignment slack (up to 3 + 3 floats)
 constexpr int kQColW = 160;        // per warp column vectors [5][32] fp32
 constexpr int kQGroup = kQZQ + kQXT + 4 * kQStage + 4 * kQColW * 4;
 constexpr int kQOffW = kQGroups * kQGroup;
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
   const int c = blockIdx.y;
   const int cw = a.head_per_channel ? c : 0;
   const int N = NC > 0 ? NC : a.N;
-  const int M = a.M, H = a.H, L = a.L, C = a.C;
+  const int M = a.M, H = a.H, C = a.C;
   const int i = lane;
   const bool valid = i < N;
 
@@ -192,17 +193,31 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
   const int64_t g1 = min(cb0 + 4 * (quads * (grp + 1) / kQGroups), cb1);
   const int rounds = g1 > g0 ? (int)((g1 - g0 + 3) / 4) : 0;
   const int NS = N * S;
-  const bool bulk = ((L & 3) == 0) && ((a.r & 3) == 0);
+  const bool bulk = a.x_vec;
   // per-warp running pointers (window b = g0 + 4 rd + s): no 64-bit index math per round
   const int64_t win0 = g0 + s;
-  const float* xnext = a.x + (win0 * C + c) * L + a.r;
+  const float* xnext = a.x + win0 * a.xsb + c * a.xsc + a.r;
   float* ycur = a.y + (win0 * C + c) * H;
-  const int64_t xstep = 4 * (int64_t)C * L, ystep = 4 * (int64_t)C * H;
+  const int64_t xstep = 4 * a.xsb, ystep = 4 * (int64_t)C * H;
+  // sliding windows (prnet_forward_sliding, window starts not 16-byte aligned): one 1-D bulk
+  // copy of the aligned superset [floor4(start), ceil4(start + NS)) when it stays inside the
+  // series buffer; the window then starts o = start mod 4 floats into the staging row
+  const bool slide = !bulk && a.x_end != nullptr;
+  auto slide_o = [&](const float* xg) { return (int)(((uintptr_t)xg >> 2) & 3u); };
+  auto slide_bytes = [&](const float* xg) { return (uint32_t)((slide_o(xg) + NS + 3) & ~3) * 4u; };
+  auto slide_bulk = [&](const float* xg) {
+    return slide && ((uintptr_t)xg & ~(uintptr_t)15) + slide_bytes(xg) <= (uintptr_t)a.x_end;
+  };
   auto issue_load = [&](const float* xg) {
     if (bulk) {
       if (lane == 0) bulk_load(xstage, xg, (uint32_t)NS * 4u, xbar);
+    } else if (slide_bulk(xg)) {
+      if (lane == 0)
+        bulk_load(xstage, reinterpret_cast<const float*>((uintptr_t)xg & ~(uintptr_t)15),
+                  slide_bytes(xg), xbar);
     } else {
-      for (int k = lane; k < NS; k += 32) cp_async4(xstage + k, xg + k);
+      const int o = slide ? slide_o(xg) : 0;
+      for (int k = lane; k < NS; k += 32) cp_async4(xstage + o + k, xg + k);
       cp_async_commit();
     }
   };
@@ -220,7 +235,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
     // (Def 4-5) from d = x - x0 (a constant segment gives exact zeros), Z' = z inv and
     // X' = x sx as fp16 hi/lo rows of the Gram / head operand tiles
     if (active) {
-      if (bulk) {
+      if (bulk || slide_bulk(xnext)) {
         mbar_wait_bounded(xbar, xph);
         xph ^= 1u;
       } else {
@@ -229,14 +244,38 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
       __syncwarp();
       float dv[24];
       {
+        const int o = slide ? slide_o(xnext) : 0;   // warp-uniform
         const float4* xr = reinterpret_cast<const float4*>(xstage + (valid ? i : N - 1) * 24);
+        if (o == 0) {
 #pragma unroll
-        for (int q = 0; q < 6; q++) {
-          const float4 v = xr[q];
-          xv[4 * q] = v.x;
-          xv[4 * q + 1] = v.y;
-          xv[4 * q + 2] = v.z;
-          xv[4 * q + 3] = v.w;
+          for (int q = 0; q < 6; q++) {
+            const float4 v = xr[q];
+            xv[4 * q] = v.x;
+            xv[4 * q + 1] = v.y;
+            xv[4 * q + 2] = v.z;
+            xv[4 * q + 3] = v.w;
+          }
+        } else {
+          // the row starts o floats past an aligned address: 7 aligned loads, static shift
+          float w[28];
+#pragma unroll
+          for (int q = 0; q < 7; q++) {
+            const float4 v = xr[q];
+            w[4 * q] = v.x;
+            w[4 * q + 1] = v.y;
+            w[4 * q + 2] = v.z;
+            w[4 * q + 3] = v.w;
+          }
+          if (o == 1) {
+#pragma unroll
+            for (int t = 0; t < 24; t++) xv[t] = w[t + 1];
+          } else if (o == 2) {
+#pragma unroll
+            for (int t = 0; t < 24; t++) xv[t] = w[t + 2];
+          } else {
+#pragma unroll
+            for (int t = 0; t < 24; t++) xv[t] = w[t + 3];
+          }
         }
       }
       __syncwarp();

@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(256) prnet_fwd_warp_kernel(FwdArgs a, int wins
   const int nwarps = blockDim.x >> 5;
   const int c = blockIdx.y;
   const int cw = a.head_per_channel ? c : 0;
-  const int S = a.S, N = a.N, M = a.M, H = a.H, L = a.L, C = a.C;
+  const int S = a.S, N = a.N, M = a.M, H = a.H, C = a.C;
   const int SP = (S + 3) & ~3;       // padded row stride of xs (16-byte rows)
   constexpr int AP = NMAX + 1;       // odd stride: conflict-free row writes / column reads
   constexpr int QP = NMAX + 1;
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256) prnet_fwd_warp_kernel(FwdArgs a, int wins
   for (int k = lane; k < NMAX * SP; k += 32) xs[k] = 0.f;
   __syncthreads();
 
-  const bool vec_x = ((S & 3) == 0) && ((L & 3) == 0) && ((a.r & 3) == 0);
+  const bool vec_x = ((S & 3) == 0) && a.x_vec;
   const bool vec_y = ((S & 3) == 0) && ((H & 3) == 0);
   const int64_t b_begin = (int64_t)blockIdx.x * wins_per_cta;
   int64_t b_end = b_begin + wins_per_cta;
@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(256) prnet_fwd_warp_kernel(FwdArgs a, int wins
   for (int64_t b = b_begin + warp; b < b_end; b += nwarps) {
     const int64_t series = b * C + c;
     // ---------------- a1: load + segment (each element read once)
-    const float* xg = a.x + series * L + a.r;
+    const float* xg = a.x + b * a.xsb + c * a.xsc + a.r;
     if (vec_x) {
       const int n4 = (N * S) >> 2;  // SP == S: rows are contiguous
       for (int k = lane; k < n4; k += 32)

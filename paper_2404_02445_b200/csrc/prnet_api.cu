@@ -36,6 +36,8 @@ struct prnet_handle {
   float* d_xstage[kStages] = {nullptr, nullptr, nullptr};
   float* d_ystage[kStages] = {nullptr, nullptr, nullptr};
   cudaStream_t streams[kStages] = {nullptr, nullptr, nullptr};
+  float* d_series = nullptr;   // prnet_forward_sliding_host: device copy of the series span
+  int64_t series_floats = 0;
 };
 
 namespace {
@@ -81,6 +83,9 @@ prnet::FwdArgs make_args(const prnet_handle* h, const float* x, int64_t B, float
   a.wpack_flash = h->d_wpack_fl;
   a.wpack_flash_inv_sw = h->d_invsw_fl;
   a.B = B;
+  a.xsb = (int64_t)c.channels * c.lookback;   // [B][C][L]; prnet_forward_sliding overrides
+  a.xsc = c.lookback;
+  a.x_vec = ((c.lookback & 3) == 0) && ((h->r & 3) == 0);
   a.C = c.channels;
   a.L = c.lookback;
   a.S = c.seg_len;
@@ -169,8 +174,15 @@ int pick_variant(const prnet_handle* h) {
 
 // Enqueue the forward for B windows (pointers already validated).
 prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* y, float* a_s,
-                             float* a_t, cudaStream_t st) {
+                             float* a_t, cudaStream_t st, int64_t slide_T = 0,
+                             const float* slide_end = nullptr) {
   prnet::FwdArgs a = make_args(h, x, B, y);
+  if (slide_T > 0) {  // sliding windows of a [C][T] series: window b starts at x + b
+    a.xsb = 1;
+    a.xsc = slide_T;
+    a.x_vec = 0;
+    a.x_end = slide_end;
+  }
   a.a_s_dbg = a_s;
   a.a_t_dbg = a_t;
   cudaError_t e;
@@ -453,10 +465,117 @@ prnet_status prnet_forward_host(prnet_handle* h, const float* x_host, int64_t ba
   return PRNET_OK;
 }
 
+// ---- sliding-window input mode
+static prnet_status validate_sliding(prnet_handle* h, const float* series, int64_t T, int64_t t0,
+                              int64_t B, const float* y, bool device_ptrs) {
+  if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
+  if (!h->loaded) return fail(h, PRNET_ERR_BAD_STATE, "forward before prnet_load_params");
+  if (B < 0) return fail(h, PRNET_ERR_INVALID_ARG, "batch < 0");
+  if (B == 0) return PRNET_OK;
+  if (!series || !y) return fail(h, PRNET_ERR_INVALID_ARG, "NULL series or y with batch > 0");
+  const int64_t C = h->cfg.channels, L = h->cfg.lookback, H = h->cfg.horizon;
+  if (t0 < 0 || T < L || B > T - L - t0 + 1)
+    return fail(h, PRNET_ERR_INVALID_ARG, "need 0 <= t0 and t0 + batch - 1 + L <= T");
+  if (T > INT64_MAX / C / 4 || B > INT64_MAX / (C * H) / 4)
+    return fail(h, PRNET_ERR_INVALID_ARG, "size overflows");
+  if (overlaps(series, (size_t)(C * T * 4), y, (size_t)(B * C * H * 4)))
+    return fail(h, PRNET_ERR_UNSUPPORTED, "series and y overlap");
+  if (device_ptrs) {
+    if (((uintptr_t)series & 15) || ((uintptr_t)y & 15))
+      return fail(h, PRNET_ERR_UNSUPPORTED, "series and y must be 16-byte aligned");
+    prnet_status s = check_dev_ptr(h, series, "series");
+    if (s != PRNET_OK) return s;
+    s = check_dev_ptr(h, y, "y");
+    if (s != PRNET_OK) return s;
+  }
+  return PRNET_OK;
+}
+
+prnet_status prnet_forward_sliding(prnet_handle* h, const float* series, int64_t T, int64_t t0,
+                                   int64_t batch, float* y, void* cuda_stream) {
+  prnet_status s = validate_sliding(h, series, T, t0, batch, y, true);
+  if (s != PRNET_OK || batch == 0) return s;
+  DeviceGuard g(h->cfg.device);
+  return enqueue_forward(h, series + t0, batch, y, nullptr, nullptr, (cudaStream_t)cuda_stream,
+                         T, series + h->cfg.channels * T);
+}
+
+prnet_status prnet_forward_sliding_host(prnet_handle* h, const float* series, int64_t T,
+                                        int64_t t0, int64_t batch, float* y_host) {
+  prnet_status s = validate_sliding(h, series, T, t0, batch, y_host, false);
+  if (s != PRNET_OK || batch == 0) return s;
+  DeviceGuard g(h->cfg.device);
+  const int64_t C = h->cfg.channels, L = h->cfg.lookback, H = h->cfg.horizon;
+  const int64_t span = batch - 1 + L;          // the time steps every window touches
+  const int64_t Tp = (span + 3) & ~int64_t(3);  // 16-byte pitch of the device copy
+  cudaError_t e;
+  if (C * Tp > h->series_floats) {
+    cudaFree(h->d_series);
+    h->d_series = nullptr;
+    h->series_floats = 0;
+    if ((e = cudaMalloc(&h->d_series, C * Tp * 4)) != cudaSuccess)
+      return cuda_fail(h, e, "cudaMalloc(series)");
+    h->series_floats = C * Tp;
+  }
+  int64_t chunk = h->host_chunk;
+  if (chunk <= 0) {
+    chunk = (128ll << 20) / (C * H * 4);
+    if (chunk < 1) chunk = 1;
+  }
+  if (chunk > batch) chunk = batch;
+  if (chunk > h->stage_windows) {  // (re)allocate the output staging ring
+    for (int k = 0; k < prnet_handle::kStages; k++) {
+      cudaFree(h->d_xstage[k]);
+      cudaFree(h->d_ystage[k]);
+      h->d_xstage[k] = h->d_ystage[k] = nullptr;
+    }
+    h->stage_windows = 0;
+    for (int k = 0; k < prnet_handle::kStages; k++) {
+      if ((e = cudaMalloc(&h->d_xstage[k], chunk * C * L * 4)) != cudaSuccess ||
+          (e = cudaMalloc(&h->d_ystage[k], chunk * C * H * 4)) != cudaSuccess)
+        return cuda_fail(h, e, "cudaMalloc(staging)");
+    }
+    h->stage_windows = chunk;
+  }
+  for (int k = 0; k < prnet_handle::kStages; k++) {
+    if (!h->streams[k] &&
+        (e = cudaStreamCreateWithFlags(&h->streams[k], cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(h, e, "cudaStreamCreate");
+  }
+  // the series span goes up once (C rows of `span` floats, pitched); windows are then
+  // forecast in chunks on three streams so chunk k's D2H overlaps chunk k+1's kernel
+  if ((e = cudaMemcpy2DAsync(h->d_series, Tp * 4, series + t0, T * 4, span * 4, C,
+                             cudaMemcpyHostToDevice, h->streams[0])) != cudaSuccess)
+    return cuda_fail(h, e, "cudaMemcpy2DAsync(series)");
+  cudaEvent_t up;
+  if ((e = cudaEventCreateWithFlags(&up, cudaEventDisableTiming)) != cudaSuccess)
+    return cuda_fail(h, e, "cudaEventCreate");
+  cudaEventRecord(up, h->streams[0]);
+  for (int k = 1; k < prnet_handle::kStages; k++) cudaStreamWaitEvent(h->streams[k], up, 0);
+  cudaEventDestroy(up);
+  int64_t k = 0;
+  for (int64_t b0 = 0; b0 < batch; b0 += chunk, k++) {
+    const int64_t nb = (batch - b0) < chunk ? (batch - b0) : chunk;
+    const int st = (int)(k % prnet_handle::kStages);
+    cudaStream_t stream = h->streams[st];
+    s = enqueue_forward(h, h->d_series + b0, nb, h->d_ystage[st], nullptr, nullptr, stream, Tp,
+                        h->d_series + C * Tp);
+    if (s != PRNET_OK) return s;
+    if ((e = cudaMemcpyAsync(y_host + b0 * C * H, h->d_ystage[st], nb * C * H * 4,
+                             cudaMemcpyDeviceToHost, stream)) != cudaSuccess)
+      return cuda_fail(h, e, "cudaMemcpyAsync(D2H)");
+  }
+  for (int st = 0; st < prnet_handle::kStages; st++)
+    if ((e = cudaStreamSynchronize(h->streams[st])) != cudaSuccess)
+      return cuda_fail(h, e, "cudaStreamSynchronize");
+  return PRNET_OK;
+}
+
 void prnet_destroy(prnet_handle* h) {
   if (!h) return;
   {
     DeviceGuard g(h->cfg.device);
+    cudaFree(h->d_series);
     cudaFree(h->d_ws);
     cudaFree(h->d_wt);
     cudaFree(h->d_b);

@@ -23,7 +23,8 @@ STATUS = {0: "PRNET_OK", 1: "PRNET_ERR_INVALID_ARG", 2: "PRNET_ERR_BAD_STATE",
 EXPORTS = ("prnet_create", "prnet_load_params", "prnet_forward", "prnet_forward_host",
            "prnet_set_host_chunk", "prnet_destroy", "prnet_last_error", "prnet_get_dims",
            "prnet_debug_segments", "prnet_debug_attention", "prnet_error_sums",
-           "prnet_forward_plan", "prnet_set_kernel_variant")
+           "prnet_forward_plan", "prnet_set_kernel_variant", "prnet_forward_sliding",
+           "prnet_forward_sliding_host")
 VARIANTS = ("warp_f32", "long_f32", "mma_f16x3", "tc_fold", "tc_full", "flash_f16x3", "tc_quad")
 
 
@@ -57,6 +58,8 @@ def load_library(path: str | None = None):
         "prnet_load_params": ([vp, vp, vp, vp, i64, i64], ctypes.c_int),
         "prnet_forward": ([vp, vp, i64, vp, vp], ctypes.c_int),
         "prnet_forward_host": ([vp, vp, i64, vp], ctypes.c_int),
+        "prnet_forward_sliding": ([vp, vp, i64, i64, i64, vp, vp], ctypes.c_int),
+        "prnet_forward_sliding_host": ([vp, vp, i64, i64, i64, vp], ctypes.c_int),
         "prnet_set_host_chunk": ([vp, i64], ctypes.c_int),
         "prnet_destroy": ([vp], None),
         "prnet_last_error": ([vp], ctypes.c_char_p),
@@ -163,6 +166,39 @@ class PRNet:
             self._check(self._lib.prnet_set_host_chunk(self._h, int(chunk_windows)))
         self._check(self._lib.prnet_forward_host(self._h, ctypes.c_void_p(xt.data_ptr()), B,
                                                  ctypes.c_void_p(yt.data_ptr())))
+        return y
+
+    def forward_sliding_into(self, series, t0: int, batch: int, y, stream=None):
+        """Sliding windows: series cuda fp32 [C, T] contiguous; window b is
+        series[:, t0 + b : t0 + b + L]; y cuda fp32 [batch, C, H] (written)."""
+        assert series.is_contiguous() and series.shape[0] == self.C and y.is_contiguous()
+        assert tuple(y.shape) == (batch, self.C, self.H)
+        self._check(self._lib.prnet_forward_sliding(
+            self._h, ctypes.c_void_p(series.data_ptr()), int(series.shape[1]), int(t0),
+            int(batch), ctypes.c_void_p(y.data_ptr()), _stream_ptr(stream)))
+        return y
+
+    def forward_sliding(self, series, t0: int, batch: int, stream=None):
+        import torch
+        y = torch.empty((batch, self.C, self.H), dtype=torch.float32, device=series.device)
+        return self.forward_sliding_into(series, t0, batch, y, stream)
+
+    def forward_sliding_host(self, series, t0: int, batch: int, y=None,
+                             chunk_windows: int | None = None):
+        """Sliding windows, host buffers end to end: series [C, T] (numpy / CPU tensor,
+        ideally pinned) -> y [batch, C, H]."""
+        import torch
+        st = torch.as_tensor(series)
+        assert st.dtype == torch.float32 and st.is_contiguous() and st.device.type == "cpu"
+        if y is None:
+            y = torch.empty((batch, self.C, self.H), dtype=torch.float32,
+                            pin_memory=st.is_pinned())
+        yt = torch.as_tensor(y)
+        if chunk_windows:
+            self._check(self._lib.prnet_set_host_chunk(self._h, int(chunk_windows)))
+        self._check(self._lib.prnet_forward_sliding_host(
+            self._h, ctypes.c_void_p(st.data_ptr()), int(st.shape[1]), int(t0), int(batch),
+            ctypes.c_void_p(yt.data_ptr())))
         return y
 
     def debug_segments(self, x, stream=None):

@@ -357,3 +357,68 @@ def test_widening_unsupported_paths():
     assert e.value.status == 3
     m3 = PRNet(3, 720, 24, 96, metric_variant=1)         # level-only: any variant
     m3.set_variant("warp_f32")
+
+
+# ------------------------------------------------------------ sliding windows
+def _series_and_windows(C, T, L, t0, B, seed=5):
+    g = np.random.default_rng(seed)
+    t = np.arange(T)[None, :]
+    s = (np.sin(2 * np.pi * t / g.integers(6, 30, (C, 1))) + 0.3 * g.standard_normal((C, T))
+         + g.uniform(-1, 1, (C, 1)) * t / T).astype(np.float32)
+    x = np.stack([s[:, t0 + b:t0 + b + L] for b in range(B)])      # [B, C, L]
+    return s, np.ascontiguousarray(x)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("L,S,H", [(720, 24, 96), (96, 24, 96), (100, 24, 90), (97, 7, 13),
+                                   (1440, 24, 96), (270, 9, 31)])
+@pytest.mark.parametrize("t0", [0, 1, 2, 3, 6])
+def test_sliding_equals_materialised_windows(L, S, H, t0, variant):
+    """prnet_forward_sliding is bitwise prnet_forward on the materialised windows, for every
+    kernel and every window alignment (t0 + b mod 4)."""
+    if not _applicable(variant, L, S, H):
+        pytest.skip("variant not applicable")
+    C, B = 5, 11
+    T = t0 + B - 1 + L + 3
+    s, x = _series_and_windows(C, T, L, t0, B)
+    m, _ = _model(C, L, S, H, variant=variant)
+    y_win = m.forward(torch.from_numpy(x).cuda())
+    y_sl = m.forward_sliding(torch.from_numpy(s).cuda(), t0, B)
+    assert torch.equal(y_sl, y_win)
+
+
+@pytest.mark.parametrize("t0", [0, 3])
+def test_sliding_window_at_the_end_of_the_series(oracle_mod, t0):
+    """The last window ends exactly at T (the aligned-superset load must not run past the
+    buffer), checked against the oracle."""
+    C, L, S, H, B = 4, 720, 24, 336, 9
+    T = t0 + B - 1 + L
+    s, x = _series_and_windows(C, T, L, t0, B, seed=9)
+    m, (ws, wt, b) = _model(C, L, S, H)
+    y = m.forward_sliding(torch.from_numpy(s).cuda(), t0, B).cpu().numpy()
+    _, y64 = oracle_mod.forward(x, S, H, ws, wt, b, True)
+    assert_parity(y, y64)
+
+
+@pytest.mark.parametrize("chunk", [None, 1, 4, 64])
+def test_sliding_host_matches_device(chunk):
+    C, L, S, H, B, t0 = 6, 720, 24, 720, 37, 5
+    T = t0 + B - 1 + L + 11
+    s, _ = _series_and_windows(C, T, L, t0, B, seed=3)
+    m, _ = _model(C, L, S, H)
+    yd = m.forward_sliding(torch.from_numpy(s).cuda(), t0, B).cpu()
+    sp = torch.from_numpy(s).pin_memory()
+    yh = m.forward_sliding_host(sp, t0, B, chunk_windows=chunk)
+    assert torch.equal(yh, yd)
+
+
+def test_sliding_argument_errors():
+    m, _ = _model(3, 96, 24, 96)
+    s = torch.zeros((3, 200), device="cuda")
+    with pytest.raises(PrnetError) as e:
+        m.forward_sliding(s, 100, 10)              # t0 + B - 1 + L = 205 > 200
+    assert e.value.status == 1
+    with pytest.raises(PrnetError) as e:
+        m.forward_sliding(s, -1, 2)
+    assert e.value.status == 1
+    assert m.forward_sliding(s, 104, 1).shape == (1, 3, 96)   # ends exactly at T
