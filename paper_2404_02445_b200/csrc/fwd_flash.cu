@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(256, 1) prnet_fwd_flash_kernel(FwdArgs a, Flas
   float* c_nu = c_ka + NP;                                      // [NP] scratch: mu, nu2
   float* yred = reinterpret_cast<float*>(smem + ly.off_yred);   // [nwarps][16 MMT][8 NTT]
   float* scr = reinterpret_cast<float*>(smem + ly.off_scr);     // [32]
+  float* w1 = scr + 32;   // [32] row sums of W_s + W_t (instance normalisation, see a8)
   const __half* w_hi = reinterpret_cast<const __half*>(
       reinterpret_cast<const unsigned char*>(a.wpack_flash) + (size_t)cw * ly.wpack_bytes);
   const int WLD = 2 * NP;
@@ -127,6 +128,15 @@ __global__ void __launch_bounds__(256, 1) prnet_fwd_flash_kernel(FwdArgs a, Flas
   // operand tiles start at zero: rows >= N and columns >= S stay zero
   for (int k = tid; k < (ly.off_col - ly.off_zhi) / 16; k += nthr)
     reinterpret_cast<uint4*>(smem + ly.off_zhi)[k] = make_uint4(0, 0, 0, 0);
+  if (a.revin) {   // w1[m] = sum_n W_s[m][n] + W_t[m][n] (the head applied to a constant row)
+    const float* gs = a.ws + (int64_t)cw * a.M * N;
+    const float* gt = a.wt + (int64_t)cw * a.M * N;
+    for (int m = tid; m < a.M; m += nthr) {
+      float acc = 0.f;
+      for (int n = 0; n < N; n++) acc += __ldg(gs + m * N + n) + __ldg(gt + m * N + n);
+      w1[m] = acc;
+    }
+  }
   __syncthreads();
 
   const int64_t b_begin = (int64_t)blockIdx.x * wins_per_cta;
@@ -146,27 +156,30 @@ __global__ void __launch_bounds__(256, 1) prnet_fwd_flash_kernel(FwdArgs a, Flas
     for (int n = tid; n < N; n += nthr) {
       const float* xr = xbuf + n * S;
       const float x0 = xr[0];
-      float s1 = 0.f, s3 = 0.f;
+      float s1 = 0.f, s3 = 0.f, dm = 0.f;
       for (int t = 0; t < S; t++) {
         const float d = xr[t] - x0;
         s1 += d;
         s3 = fmaf((float)t - half_s, d, s3);
         amx = fmaxf(amx, fabsf(xr[t]));
-        dmx = fmaxf(dmx, fabsf(d));
+        dm = fmaxf(dm, fabsf(d));
       }
       c_nu[n] = s1 * a.inv_s;          // m1 (mu - x0)
       c_ka[n] = s3 * a.inv_v;          // kappa
+      // |z| <= 2 max|d|; detrended (metric_variant bit 1): |e| <= |z| + |kappa| (S-1)/2
+      dmx = fmaxf(dmx, 2.f * dm + (a.detrend ? fabsf(c_ka[n]) * half_s : 0.f));
     }
     const float sx = pow2_scale(block_reduce(amx, scr, true));
-    const float sz = pow2_scale(2.f * block_reduce(dmx, scr, true));
+    const float sz = pow2_scale(block_reduce(dmx, scr, true));
     float musum = 0.f;
     for (int n = tid; n < N; n += nthr) {
       const float* xr = xbuf + n * S;
       const float x0 = xr[0], m1 = c_nu[n];
+      const float kd = a.detrend ? c_ka[n] : 0.f;   // e = z - kappa t~
       float q = 0.f;
       for (int t = 0; t < S; t++) {
         const float v = xr[t];
-        const float z = (v - x0) - m1;
+        const float z = fmaf(-kd, (float)t - half_s, (v - x0) - m1);
         q = fmaf(z, z, q);
         __half h, l;
         split1(v * sx, h, l);
@@ -185,17 +198,28 @@ __global__ void __launch_bounds__(256, 1) prnet_fwd_flash_kernel(FwdArgs a, Flas
     float dsum = 0.f;
     for (int n = tid; n < N; n += nthr) {
       const float d = c_mu[n] - mbar;
-      dsum += c_inv[n] + (float)S * d * d;
+      // Def 5 uses |z|^2 = |e|^2 + kappa^2 V when the seasonal metric is detrended
+      const float nz2 = a.detrend ? fmaf(c_ka[n] * c_ka[n], 1.f / a.inv_v, c_inv[n]) : c_inv[n];
+      dsum += nz2 + (float)S * d * d;
     }
-    const float inv_var = 1.0f / (block_reduce(dsum, scr, false) * a.inv_ns + kEpsTrend);
-    const float cmt = sqrtf(inv_var * a.kt), ckt = sqrtf(a.vtrend * inv_var * a.kt);
+    const float var = block_reduce(dsum, scr, false) * a.inv_ns;
+    // instance normalisation: descriptors of xhat = (x - mu_r) rr are
+    // affine images of those of x; the head runs on x and a8 adds mu_r (1 - w1[m]) + sr b
+    float mu_r = 0.f, rr = 1.f, sr = 1.f;
+    if (a.revin) {
+      mu_r = mbar;
+      rr = rsqrtf(var + kEpsRevin);
+      sr = (var + kEpsRevin) * rr;
+    }
+    const float inv_var = 1.0f / fmaf(var * rr, rr, kEpsTrend);
+    const float cmt = sqrtf(inv_var * a.kt) * rr, ckt = sqrtf(a.vtrend * inv_var * a.kt) * rr;
     for (int n = tid; n < NP; n += nthr) {
       if (n < N) {
-        const float nu2 = c_inv[n];
+        const float nu2 = c_inv[n] * rr * rr;
         const float inv = rsqrtf(nu2 + kEpsSeasonal);
-        c_inv[n] = inv;
+        c_inv[n] = inv * rr;           // the Gram is of the un-normalised z sz
         c_max[n] = sqrtf(nu2) * inv;   // f_n: known row maximum of rho (Cauchy-Schwarz)
-        c_mu[n] = c_mu[n] * cmt;
+        c_mu[n] = (c_mu[n] - mu_r) * cmt;
         c_ka[n] = c_ka[n] * ckt;
       } else {
         c_inv[n] = 0.f;
@@ -376,7 +400,8 @@ __global__ void __launch_bounds__(256, 1) prnet_fwd_flash_kernel(FwdArgs a, Flas
         const int m = h / S, t = h - m * S;
         float v = 0.f;
         for (int w = 0; w < nwarps; w++) v += yred[(w * (16 * MMT) + m) * YR + t];
-        yg[h] = v * ysc + __ldg(gb + h);
+        yg[h] = a.revin ? v * ysc + fmaf(__ldg(gb + h), sr, mu_r * (1.f - w1[m]))
+                        : v * ysc + __ldg(gb + h);
       }
       __syncthreads();
     }
@@ -415,7 +440,7 @@ bool plan_flash_kernel(const FwdArgs& a, int max_smem_optin, FlashPlan* p) {
   p->warps = nt >= 8 ? 8 : (nt >= 4 ? 4 : 2);
   off += p->warps * (16 * p->mmt) * (8 * p->ntt) * 4;
   ly.off_scr = off;
-  off += 32 * 4;
+  off += 64 * 4;   // block-reduce scratch [32] + w1 [32]
   p->smem_bytes = (size_t)((off + 127) & ~127);
   ly.wpack_bytes = flash_wpack_bytes(a.N, a.M);
   if (p->smem_bytes > (size_t)max_smem_optin) return false;

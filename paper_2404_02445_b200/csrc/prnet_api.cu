@@ -150,17 +150,18 @@ bool tcq_applicable(const prnet_handle* h) {
   return h->cfg.seg_len == 24 && h->N <= 32 && h->M <= 32 && h->cfg.tau_seasonal >= 0.0125f;
 }
 // Variants that implement the SURVEY §8(f) widening: the level-only trend runs in every
-// kernel (a.vtrend = 0); the detrended seasonal metric and instance normalisation only in
-// tc_quad and mma_f16x3 (N <= 32).
+// kernel (a.vtrend = 0); the detrended seasonal metric and instance normalisation in
+// tc_quad, mma_f16x3 (N <= 32) and flash_f16x3 (16 < N <= 512, S <= 48).
 bool widening_on(const prnet_handle* h) {
   return (h->cfg.metric_variant & 2) != 0 || h->cfg.instance_norm != 0;
 }
-bool variant_supports_widening(int v) { return v == 2 || v == 6; }
+bool variant_supports_widening(int v) { return v == 2 || v == 5 || v == 6; }
 int pick_variant(const prnet_handle* h) {
   if (h->forced_variant >= 0) return h->forced_variant;
   if (widening_on(h)) {
     if (tcq_applicable(h)) return 6;
     if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
+    if (flash_applicable(h)) return 5;
     return -1;   // no kernel implements it for this shape
   }
   // measured on B200 (profiles/README.md): tc_quad is the fastest S = 24 path (Traffic
@@ -189,8 +190,8 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
   int v = pick_variant(h);
   if (v < 0 || (widening_on(h) && !variant_supports_widening(v)))
     return fail(h, PRNET_ERR_UNSUPPORTED,
-                "metric_variant bit 1 / instance_norm are implemented for N <= 32, M <= 32, "
-                "S <= 128 (kernels tc_quad, mma_f16x3)");
+                "metric_variant bit 1 / instance_norm need tc_quad, mma_f16x3 (N <= 32) or "
+                "flash_f16x3 (16 < N <= 512, S <= 48, M <= 32)");
   if (v == 1 && a_s != nullptr) v = 0;  // the attention dump lives in the N <= 32 kernels
   if (v == 6 && a_s != nullptr) v = 2;
   static const int wpc_env = [] {  // tuning knob: windows per CTA (0 = plan default)
@@ -676,7 +677,7 @@ prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {
     return fail(h, PRNET_ERR_UNSUPPORTED, "tensor-core variant needs M <= 32 and S <= 128");
   if (variant >= 0 && widening_on(h) && !variant_supports_widening(variant))
     return fail(h, PRNET_ERR_UNSUPPORTED,
-                "metric_variant bit 1 / instance_norm need tc_quad or mma_f16x3");
+                "metric_variant bit 1 / instance_norm need tc_quad, mma_f16x3 or flash_f16x3");
   h->forced_variant = variant;
   return PRNET_OK;
 }

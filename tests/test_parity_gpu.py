@@ -344,12 +344,19 @@ def test_level_trend_every_variant(oracle_mod, variant):
         _check_widening(oracle_mod, x, S, H, 1, False, variant)
 
 
+@pytest.mark.parametrize("mv,rev", [(2, False), (0, True), (3, True)])
+@pytest.mark.parametrize("L,S,H", [(1440, 24, 96), (1536, 12, 200), (2880, 48, 96)])
+def test_widening_parity_long_lookback(oracle_mod, L, S, H, mv, rev):
+    """N > 32: the flash kernel implements the widening."""
+    x = synth.random_windows(2, 3, L, kind="mixed")
+    _check_widening(oracle_mod, x, S, H, mv, rev)
+
+
 def test_widening_unsupported_paths():
-    m = PRNet(3, 1440, 24, 96, metric_variant=2)        # N = 60: no kernel implements bit 1
-    N, _, M = m.N, m.M, m.M
+    m = PRNet(3, 3840, 96, 96, metric_variant=2)        # N = 40, S = 96: no kernel for bit 1
     m.load(np.zeros((3, m.M, m.N)), np.zeros((3, m.M, m.N)), np.zeros((3, 96)))
     with pytest.raises(PrnetError) as e:
-        m.forward(torch.zeros((2, 3, 1440), device="cuda"))
+        m.forward(torch.zeros((2, 3, 3840), device="cuda"))
     assert e.value.status == 3
     m2 = PRNet(3, 720, 24, 96, instance_norm=True)
     with pytest.raises(PrnetError) as e:
