@@ -64,6 +64,9 @@ namespace {
 #ifndef PRNET_TCQ_FRAG
 #define PRNET_TCQ_FRAG 0        // softmaxes in the mma accumulator (16x256b) layout (1) or
 #endif                          // lane-per-row (0)
+#ifndef PRNET_TCQ_QREG
+#define PRNET_TCQ_QREG 1        // head A fragments from TMEM via 16x256b + movmatrix (1) or
+#endif                          // through a shared-memory Q' tile and ldmatrix (0)
 #ifndef PRNET_TCQ_HEAD_SYNC
 #define PRNET_TCQ_HEAD_SYNC 1   // head on per-warp mma.sync (1) or on tcgen05 per quad (0)
 #endif
@@ -97,10 +100,10 @@ constexpr uint32_t kIdHead = idesc_f16(128, 96, true, true);
 // fragment of thread c holds, for k = 0..3, the segments 16(k/2) + 4c + 2(k%2) + e: four
 // consecutive segments per 16-segment chunk, i.e. exactly the packed fp16 K pairs the
 // same thread must store for the fold's A operand (TMEM columns 8(k/2) + 2c + k%2).
-__device__ __forceinline__ constexpr int pi_pos(int p) {
+[[maybe_unused]] __device__ __forceinline__ constexpr int pi_pos(int p) {
   return 16 * (p >> 4) + 4 * ((p >> 1) & 3) + 2 * ((p >> 3) & 1) + (p & 1);
 }
-__device__ __forceinline__ constexpr int pi_inv(int i) {
+[[maybe_unused]] __device__ __forceinline__ constexpr int pi_inv(int i) {
   return 8 * (2 * (i >> 4) + ((i >> 1) & 1)) + 2 * ((i >> 2) & 3) + (i & 1);
 }
 
@@ -670,6 +673,32 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
     }
     mbar_wait_bounded(mbar + 1, ph);
     tc_fence_after();
+#if PRNET_TCQ_QREG
+    // Q'^T straight into the head's A fragments: 16x256b loads give 8x8 blocks of Q'^T
+    // (rows j, columns m) in the mma accumulator layout; split to fp16 hi/lo and transposed
+    // in registers (movmatrix), block (j-half h, j-octet v, m-octet k) is A-fragment
+    // register (k & 1) + 2v of tile (m-tile k / 2, k-tile h).  No shared-memory round trip.
+    uint32_t qah[2][2][4], qal[2][2][4];   // [mt][kt][reg]
+    if (active) {
+      uint32_t r0[16], r1[16];
+      tld16_x4(tcol + ((uint32_t)(32 * s) << 16) + 64u, r0);
+      tld16_x4(tcol + ((uint32_t)(32 * s + 16) << 16) + 64u, r1);
+      tld_wait();
+#pragma unroll
+      for (int h = 0; h < 2; h++)
+#pragma unroll
+        for (int v = 0; v < 2; v++)
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            const uint32_t* r = h ? r1 : r0;
+            uint32_t hi, lo;
+            split2(make_float2(__uint_as_float(r[4 * k + 2 * v]), __uint_as_float(r[4 * k + 2 * v + 1])),
+                   hi, lo);
+            qah[k >> 1][h][(k & 1) + 2 * v] = movm_t(hi);
+            qal[k >> 1][h][(k & 1) + 2 * v] = movm_t(lo);
+          }
+    }
+#else
     if (active) {
       uint32_t qv[32];
       tld_x32(tcol + tlane + 64u, qv);   // lane j: Q'[m][j], m = 0..31
@@ -684,6 +713,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
         sts128(qr + mc * 1024 + 512, l);
       }
     }
+#endif
 #if PRNET_TCQ_HEAD_SYNC
     // ---------------- a7 head on mma.sync, per warp (its own series only, so no group
     // barrier and no block-diagonal waste): Y' = Q' X' with m16n8k16 split-fp16 MMAs,
@@ -691,7 +721,9 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
     if (active) {
       __syncwarp();
       const int l8 = lane & 7, g4 = lane >> 3;
+#if !PRNET_TCQ_QREG
       const unsigned char* qs = zq + 4 * s * 1024;
+#endif
       const unsigned char* xs = xt + 3 * s * 1024;
       float acc[2][3][4];
 #pragma unroll
@@ -717,11 +749,16 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
         }
 #pragma unroll
         for (int mt = 0; mt < 2; mt++) {
+#if PRNET_TCQ_QREG
+          const uint32_t(&ah)[4] = qah[mt][kt];
+          const uint32_t(&al)[4] = qal[mt][kt];
+#else
           // A = Q'[m][j]: blocks (m-block 2mt + (g4 & 1), j-block 2kt + (g4 >> 1))
           uint32_t ah[4], al[4];
           const unsigned char* p = qs + (2 * mt + (g4 & 1)) * 1024 + (2 * kt + (g4 >> 1)) * 128 + l8 * 16;
           ldsm_x4_t(ah, p);
           ldsm_x4_t(al, p + 512);
+#endif
 #pragma unroll
           for (int nt = 0; nt < 3; nt++) mma16816(acc[mt][nt], al, xh[nt][0], xh[nt][1]);
 #pragma unroll
