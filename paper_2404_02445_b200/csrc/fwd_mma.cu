@@ -537,6 +537,9 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
 
     // ---------------- a7 head Y' = Q' X' (= sw sx Y), one 16-row tile of future segments
     // at a time, t in chunks of 4 tiles; a8 store y = Y + b
+    // the output staging row (bstore) overwrites the Z' tiles the Gram's ldmatrix just read
+    // (other lanes' rows): order the two explicitly
+    if (bstore) __syncwarp();
     const float2 ys2 = f2(inv_sw * sr / sx);
     const bool pair_store = ((S | H) & 1) == 0;   // t, hh even -> 8-byte aligned pairs
     float* yg = a.y + series * H;

@@ -11,8 +11,9 @@ import synth  # noqa: E402
 from paper_2404_02445_b200 import PRNet  # noqa: E402
 
 CASES = [  # (L, S, H, variants)
-    (720, 24, 720, ["mma_f16x3", "tc_fold", "tc_full", "warp_f32"]),
-    (96, 24, 96, ["mma_f16x3", "tc_full", "warp_f32"]),
+    (720, 24, 720, ["tc_quad", "mma_f16x3", "tc_fold", "tc_full", "warp_f32"]),
+    (96, 24, 96, ["tc_quad", "mma_f16x3", "tc_full", "warp_f32"]),
+    (100, 24, 90, ["tc_quad"]),
     (97, 7, 13, ["mma_f16x3", "warp_f32", "long_f32"]),
     (1440, 24, 96, ["flash_f16x3", "long_f32"]),
     (1440, 12, 100, ["flash_f16x3"]),
@@ -27,4 +28,22 @@ for L, S, H, variants in CASES:
         torch.cuda.synchronize()
         assert torch.isfinite(y).all(), (L, S, H, v)
         print("ok", L, S, H, v, flush=True)
+# SURVEY §8(f) widening and the sliding-window mode
+for L, S, H, mv, rev in [(720, 24, 720, 3, True), (97, 7, 13, 2, True), (1440, 24, 96, 3, True)]:
+    x = torch.from_numpy(synth.random_windows(5, 3, L)).cuda()
+    N, _, M = synth.derived_dims(L, S, H)
+    ws, wt, b = synth.make_params(3, M, N, H)
+    y = PRNet(3, L, S, H, metric_variant=mv, instance_norm=rev).load(ws, wt, b).forward(x)
+    torch.cuda.synchronize()
+    assert torch.isfinite(y).all(), (L, S, H, mv, rev)
+    print("ok widening", L, S, H, mv, rev, flush=True)
+for L, S, H, t0 in [(720, 24, 720, 1), (720, 24, 96, 0), (97, 7, 13, 3)]:
+    T = t0 + 7 - 1 + L
+    ser = torch.from_numpy(synth.random_windows(1, 3, T)[0]).cuda()
+    N, _, M = synth.derived_dims(L, S, H)
+    ws, wt, b = synth.make_params(3, M, N, H)
+    y = PRNet(3, L, S, H).load(ws, wt, b).forward_sliding(ser, t0, 7)
+    torch.cuda.synchronize()
+    assert torch.isfinite(y).all(), (L, S, H, t0)
+    print("ok sliding", L, S, H, t0, flush=True)
 print("sanitize cases done")
