@@ -93,8 +93,10 @@ void pack_flash_head(const float* ws, const float* wt, int Cw, int M, int N, uns
   }
 }
 
+// S <= 32 (KS <= 2): registers capped at 128 so two 8-warp (or four 4-warp) CTAs fit an SM
+// (A/B, stress L = 1440, S = 24: 1.84 vs 2.91 ms); S in (32, 48] would spill, keeps 1
 template <int KS, int NTT, int MMT>
-__global__ void __launch_bounds__(256, 1) prnet_fwd_flash_kernel(FwdArgs a, FlashLayout ly,
+__global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel(FwdArgs a, FlashLayout ly,
                                                                  int wins_per_cta) {
   extern __shared__ float4 smem4[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(smem4);
