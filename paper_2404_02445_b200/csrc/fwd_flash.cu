@@ -108,7 +108,6 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
   const int S = a.S, N = a.N, H = a.H, C = a.C;
   const int NP = ly.npad, NT = NP / 16, ZP = ly.zph, XP = ly.xph;
 
-  float* xbuf = reinterpret_cast<float*>(smem);
   __half* z_hi = reinterpret_cast<__half*>(smem + ly.off_zhi);
   __half* z_lo = reinterpret_cast<__half*>(smem + ly.off_zlo);
   __half* x_hi = reinterpret_cast<__half*>(smem + ly.off_xhi);
@@ -147,12 +146,10 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
   const float half_s = a.half_s;
   for (int64_t b = b_begin; b < b_end; b++) {
     const int64_t series = b * C + c;
-    // ---------------- a1: load the segmented span
-    {
-      const float* xg = a.x + b * a.xsb + c * a.xsc + a.r;
-      for (int k = tid; k < N * S; k += nthr) xbuf[k] = __ldg(xg + k);
-    }
-    __syncthreads();
+    // ---------------- a1: the segmented span is read straight from global memory by the two
+    // descriptor passes (the second hits L1/L2): no shared staging, so a 480-segment series
+    // fits two CTAs per SM
+    const float* xbuf = a.x + b * a.xsb + c * a.xsc + a.r;
     // ---------------- a2: descriptors (Def 4-5), thread per segment
     float amx = 0.f, dmx = 0.f;
     for (int n = tid; n < N; n += nthr) {
@@ -422,7 +419,7 @@ bool plan_flash_kernel(const FwdArgs& a, int max_smem_optin, FlashPlan* p) {
   auto odd8 = [](int v) { v = (v + 7) & ~7; if (((v / 8) & 1) == 0) v += 8; return v; };
   ly.zph = odd8(16 * p->ks);
   ly.xph = odd8(8 * p->ntt);
-  int off = ((a.N * a.S * 4) + 15) & ~15;
+  int off = 0;   // (no fp32 staging of the series: the descriptor passes read global memory)
   ly.off_zhi = off;
   off += ly.npad * ly.zph * 2;
   ly.off_zlo = off;
