@@ -64,6 +64,9 @@ namespace {
 #ifndef PRNET_TCQ_FRAG
 #define PRNET_TCQ_FRAG 0        // softmaxes in the mma accumulator (16x256b) layout (1) or
 #endif                          // lane-per-row (0)
+#ifndef PRNET_TCQ_ROT
+#define PRNET_TCQ_ROT 1         // conflict-free staging row reads (rotated float4 order)
+#endif
 #ifndef PRNET_TCQ_QREG
 #define PRNET_TCQ_QREG 1        // head A fragments from TMEM via 16x256b + movmatrix (1) or
 #endif                          // through a shared-memory Q' tile and ldmatrix (0)
@@ -250,6 +253,23 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
         const int o = slide ? slide_o(xnext) : 0;   // warp-uniform
         const float4* xr = reinterpret_cast<const float4*>(xstage + (valid ? i : N - 1) * 24);
         if (o == 0) {
+#if PRNET_TCQ_ROT
+          // rows are 96 B apart, so lanes i and i + 4 of a quarter-warp hit the same banks:
+          // lanes with (i / 4) odd read the float4s in rotated order (q + 1) mod 6 and the
+          // registers are rotated back with selects (no bank conflicts)
+          const bool rot = (i >> 2) & 1;
+          float4 v[6];
+#pragma unroll
+          for (int q = 0; q < 6; q++) v[q] = xr[rot ? (q + 1) % 6 : q];
+#pragma unroll
+          for (int q = 0; q < 6; q++) {
+            const float4 u = rot ? v[(q + 5) % 6] : v[q];
+            xv[4 * q] = u.x;
+            xv[4 * q + 1] = u.y;
+            xv[4 * q + 2] = u.z;
+            xv[4 * q + 3] = u.w;
+          }
+#else
 #pragma unroll
           for (int q = 0; q < 6; q++) {
             const float4 v = xr[q];
@@ -258,6 +278,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
             xv[4 * q + 2] = v.z;
             xv[4 * q + 3] = v.w;
           }
+#endif
         } else {
           // the row starts o floats past an aligned address: 7 aligned loads, static shift
           float w[28];
