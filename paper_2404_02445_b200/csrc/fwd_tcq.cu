@@ -88,7 +88,9 @@ constexpr int kQOffW = kQGroups * kQGroup;
 constexpr int kQOffBar = kQOffW + 8192;            // 4 x 3 MMA barriers + 16 TMA barriers
 constexpr int kQOffTmem = kQOffBar + 256;
 constexpr int kQOffBias = kQOffTmem + 16;
-constexpr int kQBiasRow = 28;                      // bias row stride (floats): conflict-free
+// bias row stride (floats), conflict-free for the epilogue's reads: 8-byte pair reads of the
+// mma.sync head (lanes (g, c) -> 24 g + 2 c) or 16-byte row reads of the tcgen05 head
+constexpr int kQBiasRow = PRNET_TCQ_HEAD_SYNC ? 24 : 28;
 constexpr int kQBias = 32 * kQBiasRow;             // bias rows m < 32, zero-padded
 constexpr int kQSmem = kQOffBias + kQBias * 4;
 static_assert(kQGroup % 16 == 0, "16-byte aligned tiles");
