@@ -178,7 +178,9 @@ prnet_status prnet_error_sums(prnet_handle* h, const float* y, const float* targ
  *   6 = tc_quad      groups of 4 warps take quads of 4 series; Gram of the
  *                    row-normalised segments, fold and head on tcgen05 / TMEM,
  *                    lane-per-row softmaxes (S = 24, N <= 32, M <= 32,
- *                    tau_seasonal >= 1/80)                           [auto]
+ *                    tau_seasonal >= 1/80)               [auto: N > 8]
+ *   7 = small_f32    one warp per series with lanes over TIME, FP32, warp
+ *                    butterfly reductions (N <= 8, S <= 128, M <= 32)     [auto]
  * Returns PRNET_ERR_UNSUPPORTED when the variant does not cover the handle's shape. */
 prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant);
 

@@ -156,6 +156,10 @@ bool widening_on(const prnet_handle* h) {
   return (h->cfg.metric_variant & 2) != 0 || h->cfg.instance_norm != 0;
 }
 bool variant_supports_widening(int v) { return v == 2 || v == 5 || v == 6; }
+// 7 = small_f32 (N <= 8, S <= 128, M <= 32: lanes over time, FP32)
+bool small_applicable(const prnet_handle* h) {
+  return h->N <= 8 && h->cfg.seg_len <= 128 && h->M <= 32;
+}
 int pick_variant(const prnet_handle* h) {
   if (h->forced_variant >= 0) return h->forced_variant;
   if (widening_on(h)) {
@@ -164,9 +168,11 @@ int pick_variant(const prnet_handle* h) {
     if (flash_applicable(h)) return 5;
     return -1;   // no kernel implements it for this shape
   }
-  // measured on B200 (profiles/README.md): tc_quad is the fastest S = 24 path (Traffic
-  // 6.37 ms vs 6.60 ms for mma_f16x3), mma_f16x3 the fastest other N <= 32 path;
-  // tc_fold and tc_full are selectable with prnet_set_kernel_variant
+  // measured on B200 (profiles/README.md): small_f32 is the fastest N <= 8 path (stress
+  // sweep 2-9x over tc_quad / mma_f16x3), tc_quad the fastest S = 24 path (Traffic 5.4 ms vs
+  // 6.6 ms for mma_f16x3), mma_f16x3 the fastest other N <= 32 path; tc_fold and tc_full are
+  // selectable with prnet_set_kernel_variant
+  if (small_applicable(h)) return 7;
   if (tcq_applicable(h)) return 6;
   if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
   if (h->N > 32 && flash_applicable(h)) return 5;
@@ -193,12 +199,19 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
                 "metric_variant bit 1 / instance_norm need tc_quad, mma_f16x3 (N <= 32) or "
                 "flash_f16x3 (16 < N <= 512, S <= 48, M <= 32)");
   if (v == 1 && a_s != nullptr) v = 0;  // the attention dump lives in the N <= 32 kernels
+  if (v == 7 && a_s != nullptr) v = 2;
   if (v == 6 && a_s != nullptr) v = 2;
   static const int wpc_env = [] {  // tuning knob: windows per CTA (0 = plan default)
     const char* e = getenv("PRNET_WINDOWS_PER_CTA");
     return e ? atoi(e) : 0;
   }();
-  if (v == 6) {
+  if (v == 7) {
+    prnet::SmallPlan p;
+    if (!prnet::plan_small_kernel(a, h->max_smem_optin, &p))
+      return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the small_f32 kernel");
+    if (wpc_env > 0) p.wins_per_cta = wpc_env;
+    e = prnet::launch_small_kernel(a, p, st);
+  } else if (v == 6) {
     prnet::TcqPlan p;
     if (!prnet::plan_tcq_kernel(a, h->max_smem_optin, &p))
       return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the tc_quad kernel");
@@ -660,8 +673,10 @@ prnet_status prnet_error_sums(prnet_handle* h, const float* y, const float* targ
 
 prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {
   if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
-  if (variant < -1 || variant > 6)
-    return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,...,6}");
+  if (variant < -1 || variant > 7)
+    return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,...,7}");
+  if (variant == 7 && !small_applicable(h))
+    return fail(h, PRNET_ERR_UNSUPPORTED, "small_f32 variant needs N <= 8, S <= 128, M <= 32");
   if (variant == 6 && !tcq_applicable(h))
     return fail(h, PRNET_ERR_UNSUPPORTED,
                 "tc_quad variant needs S = 24, N <= 32, M <= 32, tau_seasonal >= 1/80");

@@ -38,14 +38,16 @@ def _applicable(variant, L, S, H):
         return S == 24 and 16 < N <= 32 and M <= 32
     if variant in ("tc_full", "tc_quad"):
         return S == 24 and N <= 32 and M <= 32
+    if variant == "small_f32":
+        return N <= 8 and S <= 128 and M <= 32
     if variant == "flash_f16x3":
         return 16 < N <= 512 and S <= 48 and M <= 32
     return True
 
 
 VARIANTS = [None, "warp_f32", "mma_f16x3", "tc_fold", "tc_full", "long_f32", "flash_f16x3",
-            "tc_quad"]
-SHORT_VARIANTS = [None, "warp_f32", "mma_f16x3", "tc_fold", "tc_full", "tc_quad"]   # N <= 32
+            "tc_quad", "small_f32"]
+SHORT_VARIANTS = [None, "warp_f32", "mma_f16x3", "tc_fold", "tc_full", "tc_quad", "small_f32"]
 
 
 def _check_small(oracle_mod, x, S, H, hpc=True, tau_s=1.0, tau_t=1.0, scale=None, variant=None):
