@@ -168,7 +168,7 @@ prnet_status prnet_error_sums(prnet_handle* h, const float* y, const float* targ
  *   1 = long_f32     one CTA per series, rows streamed, FP32              (N <= 512)
  *   2 = mma_f16x3    one warp per series, mma.sync m16n8k16 with split-fp16
  *                    hi/lo operands, 3 products, fp32 accumulation
- *                    (N <= 32, M <= 32, S <= 128)  [auto: N <= 32 unless 6 applies]
+ *                    (N <= 32, M <= 32, S <= 128)  [auto: N <= 32 unless 6, 7 apply]
  *   3 = tc_fold      as 2, fold Q = W A on tcgen05.mma with a TMEM accumulator
  *                    (S = 24, 16 < N <= 32, M <= 32)
  *   4 = tc_full      Gram, fold and head on tcgen05 / TMEM, lane-per-row softmax
@@ -178,9 +178,10 @@ prnet_status prnet_error_sums(prnet_handle* h, const float* y, const float* targ
  *   6 = tc_quad      groups of 4 warps take quads of 4 series; Gram of the
  *                    row-normalised segments, fold and head on tcgen05 / TMEM,
  *                    lane-per-row softmaxes (S = 24, N <= 32, M <= 32,
- *                    tau_seasonal >= 1/80)               [auto: N > 8]
+ *                    tau_seasonal >= 1/80)              [auto: N > 16]
  *   7 = small_f32    one warp per series with lanes over TIME, FP32, warp
- *                    butterfly reductions (N <= 8, S <= 128, M <= 32)     [auto]
+ *                    butterfly reductions (N <= 16, S <= 128, M <= 32)
+ *                    [auto: N <= 8, or S > 64]
  * Returns PRNET_ERR_UNSUPPORTED when the variant does not cover the handle's shape. */
 prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant);
 

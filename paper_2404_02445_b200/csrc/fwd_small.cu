@@ -1,4 +1,4 @@
-// fwd_small.cu -- fused PRNet pattern-attention forward for SHORT series (N <= 8 segments,
+// fwd_small.cu -- fused PRNet pattern-attention forward for SHORT series (N <= 16 segments,
 // S <= 128): "small_f32" variant, FP32 throughout (the warp_f32 arithmetic), with the
 // lanes of a warp over TIME instead of over segments.
 //
@@ -62,12 +62,42 @@ __device__ __forceinline__ void warp_reduce_to(float (&v)[P], float* out, int la
 }  // namespace
 
 // NP: padded segment count (power of two >= N, <= 8); TS: time slots per lane (S <= 32 TS)
+// Gram partial sums for the pairs e in [LO, LO + P) (e = i NP - i (i - 1) / 2 + j - i, i <= j),
+// reduced across the warp into red[LO..LO + P)
+template <int NP, int TS, int LO, int P>
+__device__ __forceinline__ void gram_batch(const float (&zv)[NP][TS], float* red, int lane) {
+  float g[P];
+#pragma unroll
+  for (int q = 0; q < P; q++) g[q] = 0.f;
+#pragma unroll
+  for (int i = 0; i < NP; i++)
+#pragma unroll
+    for (int j = 0; j < NP; j++) {
+      if (j < i) continue;
+      const int e = i * NP - i * (i - 1) / 2 + (j - i);   // compile-time after unrolling
+      if (e < LO || e >= LO + P) continue;
+      float sacc = 0.f;
+#pragma unroll
+      for (int k = 0; k < TS; k++) sacc = fmaf(zv[i][k], zv[j][k], sacc);
+      g[e - LO] = sacc;
+    }
+  warp_reduce_to<P>(g, red + LO, lane);
+}
+template <int NP, int TS, int LO>
+__device__ __forceinline__ void gram_all(const float (&zv)[NP][TS], float* red, int lane) {
+  constexpr int NG = NP * (NP + 1) / 2;
+  if constexpr (LO < NG) {
+    constexpr int R = NG - LO;
+    constexpr int P = R >= 32 ? 32 : (R > 8 ? 16 : (R > 4 ? 8 : (R > 2 ? 4 : 2)));
+    gram_batch<NP, TS, LO, P>(zv, red, lane);
+    gram_all<NP, TS, LO + P>(zv, red, lane);
+  }
+}
+
 template <int NP, int TS>
 __global__ void __launch_bounds__(256) prnet_fwd_small_kernel(FwdArgs a, int wins_per_cta) {
   constexpr int NG = NP * (NP + 1) / 2;                      // Gram entries i <= j
-  constexpr int PG = NG <= 4 ? 4 : (NG <= 8 ? 8 : (NG <= 16 ? 16 : 32));
-  constexpr int NG2 = NG > 32 ? NG - 32 : 0;                  // second batch (NP = 8: 4)
-  constexpr int PG2 = NG2 <= 1 ? 1 : (NG2 <= 2 ? 2 : (NG2 <= 4 ? 4 : 8));
+  constexpr int RED = (NG + 31) / 32 * 32 + 32;               // reduced sums (+ slack)
   constexpr int PD = 2 * NP;                                  // s1, s3 per segment
   constexpr int NE = (NP * NP + 31) / 32;                     // attention elements per lane
   extern __shared__ float4 smem4[];
@@ -93,9 +123,11 @@ __global__ void __launch_bounds__(256) prnet_fwd_small_kernel(FwdArgs a, int win
     for (int k = threadIdx.x; k < H; k += blockDim.x) bS[k] = __ldg(gb + k);
   }
   __syncthreads();
-  // per-warp scratch: reduced sums [64], A_s, A_t [NP][NP], Q [M][NP]
-  float* red = bS + ((a.H + 3) & ~3) + warp * (64 + 2 * NP * NP + 32 * NP);
-  float* as_ = red + 64;
+  // per-warp scratch: reduced sums [RED], mu / kappa table [2 NP], A_s, A_t [NP][NP],
+  // Q [M][NP]
+  float* red = bS + ((a.H + 3) & ~3) + warp * (RED + 2 * NP + 2 * NP * NP + 32 * NP);
+  float* dtab = red + RED;
+  float* as_ = dtab + 2 * NP;
   float* at_ = as_ + NP * NP;
   float* qs = at_ + NP * NP;
 
@@ -132,12 +164,15 @@ __global__ void __launch_bounds__(256) prnet_fwd_small_kernel(FwdArgs a, int win
     }
     warp_reduce_to<PD>(dsum, red, lane);
     __syncwarp();
-    float m1[NP], mu[NP], kap[NP];
+    float m1[NP];
 #pragma unroll
-    for (int n = 0; n < NP; n++) {
-      m1[n] = red[n] * a.inv_s;
-      mu[n] = x0[n] + m1[n];
-      kap[n] = red[NP + n] * a.inv_v;
+    for (int n = 0; n < NP; n++) m1[n] = red[n] * a.inv_s;
+    if (lane == 0) {   // segment means and slopes, read by index below
+#pragma unroll
+      for (int n = 0; n < NP; n++) {
+        dtab[n] = x0[n] + m1[n];
+        dtab[NP + n] = red[NP + n] * a.inv_v;
+      }
     }
     // z = d - m1 (zero past S), then the Gram entries G_ij = <z_i, z_j> (i <= j)
 #pragma unroll
@@ -147,29 +182,9 @@ __global__ void __launch_bounds__(256) prnet_fwd_small_kernel(FwdArgs a, int win
         const int t = lane + 32 * k;
         xv[n][k] = (n < N && t < S) ? xv[n][k] - m1[n] : 0.f;
       }
-    {
-      float g1[PG], g2[PG2];
-#pragma unroll
-      for (int q = 0; q < PG; q++) g1[q] = 0.f;
-#pragma unroll
-      for (int q = 0; q < PG2; q++) g2[q] = 0.f;
-#pragma unroll
-      for (int i = 0; i < NP; i++)
-#pragma unroll
-        for (int j = 0; j < NP; j++) {
-          if (j < i) continue;
-          const int e = i * NP - i * (i - 1) / 2 + (j - i);   // compile-time after unrolling
-          float s = 0.f;
-#pragma unroll
-          for (int k = 0; k < TS; k++) s = fmaf(xv[i][k], xv[j][k], s);
-          if (e < 32) g1[e < PG ? e : 0] += e < PG ? s : 0.f;
-          else g2[(e - 32) < PG2 ? e - 32 : 0] += (e - 32) < PG2 ? s : 0.f;
-        }
-      __syncwarp();   // red[] (the descriptor sums) was read above
-      warp_reduce_to<PG>(g1, red, lane);
-      if constexpr (NG2 > 0) warp_reduce_to<PG2>(g2, red + 32, lane);
-      __syncwarp();
-    }
+    __syncwarp();   // red[] (the descriptor sums) was read above
+    gram_all<NP, TS, 0>(xv, red, lane);
+    __syncwarp();
     auto gram = [&](int i, int j) {   // G_ij, i, j < NP
       const int lo = i < j ? i : j, hi = i < j ? j : i;
       return red[lo * NP - lo * (lo - 1) / 2 + (hi - lo)];
@@ -177,12 +192,12 @@ __global__ void __launch_bounds__(256) prnet_fwd_small_kernel(FwdArgs a, int win
     // ---------------- Def 5: sigma^2 = (1/(N S)) sum_n [nu2_n + S (mu_n - mubar)^2]
     float mbar = 0.f;
 #pragma unroll
-    for (int n = 0; n < NP; n++) mbar += n < N ? mu[n] : 0.f;
+    for (int n = 0; n < NP; n++) mbar += n < N ? dtab[n] : 0.f;
     mbar *= a.inv_n;
     float var = 0.f;
 #pragma unroll
     for (int n = 0; n < NP; n++)
-      var += n < N ? gram(n, n) + (float)S * (mu[n] - mbar) * (mu[n] - mbar) : 0.f;
+      var += n < N ? gram(n, n) + (float)S * (dtab[n] - mbar) * (dtab[n] - mbar) : 0.f;
     const float inv_var = 1.0f / (var * a.inv_ns + kEpsTrend);
     const float cm = sqrtf(inv_var * a.kt), ck = sqrtf(a.vtrend * inv_var * a.kt);
 
@@ -197,14 +212,7 @@ __global__ void __launch_bounds__(256) prnet_fwd_small_kernel(FwdArgs a, int win
       const float rho = gram(i, j) * invi * invj;
       const float fi = sqrtf(nui) * invi;             // rho_ij <= f_i (Cauchy-Schwarz)
       float es = ok ? fast_ex2((rho - fi) * a.ks) : 0.f;
-      float mui = 0.f, muj = 0.f, ki = 0.f, kj = 0.f;
-#pragma unroll
-      for (int n = 0; n < NP; n++) {
-        mui = n == i ? mu[n] : mui;
-        muj = n == j ? mu[n] : muj;
-        ki = n == i ? kap[n] : ki;
-        kj = n == j ? kap[n] : kj;
-      }
+      const float mui = dtab[i], muj = dtab[j], ki = dtab[NP + i], kj = dtab[NP + j];
       const float dm = (mui - muj) * cm, dk = (ki - kj) * ck;
       float et = ok ? fast_ex2(-fmaf(dm, dm, dk * dk)) : 0.f;   // row max 0 at j = i
       float ss = es, st = et;
@@ -236,7 +244,7 @@ __global__ void __launch_bounds__(256) prnet_fwd_small_kernel(FwdArgs a, int win
 #pragma unroll
       for (int j = 0; j < NP; j++) {
         qm[j] = qs[m * NP + j];
-        qmu = fmaf(qm[j], mu[j], qmu);
+        qmu = fmaf(qm[j], dtab[j], qmu);
       }
 #pragma unroll
       for (int k = 0; k < TS; k++) {
@@ -255,11 +263,12 @@ __global__ void __launch_bounds__(256) prnet_fwd_small_kernel(FwdArgs a, int win
 }
 
 bool plan_small_kernel(const FwdArgs& a, int max_smem_optin, SmallPlan* p) {
-  if (a.N > 8 || a.S > 128 || a.M > 32) return false;
-  p->np = a.N <= 2 ? 2 : (a.N <= 4 ? 4 : 8);
+  if (a.N > 16 || a.S > 128 || a.M > 32) return false;
+  p->np = a.N <= 2 ? 2 : (a.N <= 4 ? 4 : (a.N <= 8 ? 8 : 16));
   p->ts = a.S <= 32 ? 1 : (a.S <= 64 ? 2 : 4);
   p->warps_per_cta = 8;
-  const int per_warp = 64 + 2 * p->np * p->np + 32 * p->np;
+  const int ng = p->np * (p->np + 1) / 2;
+  const int per_warp = (ng + 31) / 32 * 32 + 32 + 2 * p->np + 2 * p->np * p->np + 32 * p->np;
   p->smem_bytes =
       (size_t)(2 * 32 * p->np + ((a.H + 3) & ~3) + p->warps_per_cta * per_warp) * sizeof(float);
   if (p->smem_bytes > (size_t)max_smem_optin) return false;
@@ -291,7 +300,8 @@ cudaError_t launch_small_kernel(const FwdArgs& a, const SmallPlan& p, cudaStream
   switch (p.np) {
     case 2: return launch_small_n<2>(a, p, st);
     case 4: return launch_small_n<4>(a, p, st);
-    default: return launch_small_n<8>(a, p, st);
+    case 8: return launch_small_n<8>(a, p, st);
+    default: return launch_small_n<16>(a, p, st);
   }
 }
 

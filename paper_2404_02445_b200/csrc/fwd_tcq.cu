@@ -898,11 +898,26 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
   if (warp == 0) tmem_dealloc(tmem0, 512);
 }
 
-bool plan_tcq_kernel(const FwdArgs& a, int max_smem_optin, TcqPlan* p) {
+bool plan_tcq_kernel(const FwdArgs& a, int max_smem_optin, int sm_count, TcqPlan* p) {
   if (a.S != 24 || a.N < 1 || a.N > 32 || a.M > 32) return false;
   p->smem_bytes = (size_t)kQSmem;
   if (p->smem_bytes > (size_t)max_smem_optin) return false;
   p->wins_per_group = 128;
+  // one CTA per SM: a small launch (few channels x few windows) ends in a partial wave.
+  // Split each channel into k CTAs, k >= B / (4 x 128), minimising
+  //   waves(k) x (windows per CTA + kQPrologue)
+  // where kQPrologue ~ the per-CTA setup (W' and bias loads, TMEM allocation) in windows
+  constexpr int64_t kQPrologue = 32;
+  const int64_t per_cta = (int64_t)kQGroups * p->wins_per_group;
+  const int64_t k0 = a.B > 0 ? (a.B + per_cta - 1) / per_cta : 1;
+  const int64_t sms = sm_count > 0 ? sm_count : 148;
+  int64_t best_k = k0, best = -1;
+  for (int64_t k = k0; k <= 4 * k0 && k <= (a.B + 63) / 64 + 1; k++) {
+    const int64_t waves = ((int64_t)a.C * k + sms - 1) / sms;
+    const int64_t cost = waves * ((a.B + k - 1) / k + kQPrologue);
+    if (best < 0 || cost < best) best = cost, best_k = k;
+  }
+  p->ctas_per_channel = (int)best_k;
   return true;
 }
 
@@ -913,7 +928,8 @@ static cudaError_t launch_tcq_t(const FwdArgs& a, const TcqPlan& p, cudaStream_t
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
   const int64_t per_cta = (int64_t)kQGroups * p.wins_per_group;
-  const int ctas = (int)((a.B + per_cta - 1) / per_cta);
+  const int ctas =
+      p.ctas_per_channel > 0 ? p.ctas_per_channel : (int)((a.B + per_cta - 1) / per_cta);
   dim3 grid((unsigned)ctas, (unsigned)a.C);
   k<<<grid, 32 * 4 * kQGroups, p.smem_bytes, st>>>(a, ctas);
   return cudaGetLastError();

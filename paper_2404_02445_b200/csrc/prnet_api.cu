@@ -156,24 +156,26 @@ bool widening_on(const prnet_handle* h) {
   return (h->cfg.metric_variant & 2) != 0 || h->cfg.instance_norm != 0;
 }
 bool variant_supports_widening(int v) { return v == 2 || v == 5 || v == 6; }
-// 7 = small_f32 (N <= 8, S <= 128, M <= 32: lanes over time, FP32)
+// 7 = small_f32 (N <= 16, S <= 128, M <= 32: lanes over time, FP32)
 bool small_applicable(const prnet_handle* h) {
-  return h->N <= 8 && h->cfg.seg_len <= 128 && h->M <= 32;
+  return h->N <= 16 && h->cfg.seg_len <= 128 && h->M <= 32;
 }
 int pick_variant(const prnet_handle* h) {
   if (h->forced_variant >= 0) return h->forced_variant;
   if (widening_on(h)) {
-    if (tcq_applicable(h)) return 6;
+    if (tcq_applicable(h) && h->N > 16) return 6;
     if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
     if (flash_applicable(h)) return 5;
     return -1;   // no kernel implements it for this shape
   }
   // measured on B200 (profiles/README.md): small_f32 is the fastest N <= 8 path (stress
-  // sweep 2-9x over tc_quad / mma_f16x3), tc_quad the fastest S = 24 path (Traffic 5.4 ms vs
-  // 6.6 ms for mma_f16x3), mma_f16x3 the fastest other N <= 32 path; tc_fold and tc_full are
-  // selectable with prnet_set_kernel_variant
-  if (small_applicable(h)) return 7;
-  if (tcq_applicable(h)) return 6;
+  // sweep 2-9x over tc_quad / mma_f16x3) and the fastest N <= 16 path for S > 64 (2.3x);
+  // tc_quad the fastest S = 24 path for N > 16 (Traffic 5.4 ms vs 6.6 ms for mma_f16x3; its
+  // MMA tiles pad N to 32, so mma_f16x3 wins at N = 14: 0.166 vs 0.255 ms); mma_f16x3 the
+  // fastest other N <= 32 path; tc_fold and tc_full are selectable with
+  // prnet_set_kernel_variant
+  if (small_applicable(h) && (h->N <= 8 || h->cfg.seg_len > 64)) return 7;
+  if (tcq_applicable(h) && h->N > 16) return 6;
   if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
   if (h->N > 32 && flash_applicable(h)) return 5;
   return h->N <= 32 ? 0 : 1;
@@ -213,9 +215,12 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
     e = prnet::launch_small_kernel(a, p, st);
   } else if (v == 6) {
     prnet::TcqPlan p;
-    if (!prnet::plan_tcq_kernel(a, h->max_smem_optin, &p))
+    if (!prnet::plan_tcq_kernel(a, h->max_smem_optin, h->sm_count, &p))
       return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the tc_quad kernel");
-    if (wpc_env > 0) p.wins_per_group = (wpc_env + 3) & ~3;
+    if (wpc_env > 0) {
+      p.wins_per_group = (wpc_env + 3) & ~3;
+      p.ctas_per_channel = 0;
+    }
     e = prnet::launch_tcq_kernel(a, p, st);
   } else if (v == 5) {
     prnet::FlashPlan p;
@@ -676,7 +681,7 @@ prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {
   if (variant < -1 || variant > 7)
     return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,...,7}");
   if (variant == 7 && !small_applicable(h))
-    return fail(h, PRNET_ERR_UNSUPPORTED, "small_f32 variant needs N <= 8, S <= 128, M <= 32");
+    return fail(h, PRNET_ERR_UNSUPPORTED, "small_f32 variant needs N <= 16, S <= 128, M <= 32");
   if (variant == 6 && !tcq_applicable(h))
     return fail(h, PRNET_ERR_UNSUPPORTED,
                 "tc_quad variant needs S = 24, N <= 32, M <= 32, tau_seasonal >= 1/80");

@@ -39,7 +39,7 @@ def _applicable(variant, L, S, H):
     if variant in ("tc_full", "tc_quad"):
         return S == 24 and N <= 32 and M <= 32
     if variant == "small_f32":
-        return N <= 8 and S <= 128 and M <= 32
+        return N <= 16 and S <= 128 and M <= 32
     if variant == "flash_f16x3":
         return 16 < N <= 512 and S <= 48 and M <= 32
     return True
