@@ -97,7 +97,8 @@ EPS_REVIN = 1e-5   # RevIN epsilon of the product (R-f1)
 def series(x, S, H, ws, wt, bias, tau_s=1.0, tau_t=1.0, metric_variant=0, instance_norm=False,
            eps_r=EPS_REVIN):
     """One series; returns a dict with y and every intermediate (fp64).
-    metric_variant bit 0 = level-only trend, bit 1 = detrended seasonal; instance_norm =
+    metric_variant bit 0 = level-only trend, bit 1 = detrended seasonal, bit 2 = component
+    values (each branch aggregates its own component, reading R-f4); instance_norm =
     RevIN-style normalisation."""
     x = np.ascontiguousarray(x, dtype=np.float32).ravel()
     L = x.size

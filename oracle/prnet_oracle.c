@@ -167,6 +167,24 @@ static void oracle_aggregate(const double* A, const double* X, int N, int S, dou
     }
 }
 
+/* SURVEY §8(f) f3 / A10 variant "each branch aggregates its component (T_n or z_n)"
+ * (metric_variant bit 2, reading R-f4 in DESIGN.md §3): the values each branch
+ * aggregates are the component its metric measures,
+ *   seasonal  Vs_n[t] = z_n[t]                      (plain, bit 1 = 0)
+ *             Vs_n[t] = z_n[t] - kappa_n ttilde_t   (detrended metric, bit 1 = 1)
+ *   trend     Vt_n[t] = mu_n + kappa_n ttilde_t     (the least-squares line T_n, bit 0 = 0)
+ *             Vt_n[t] = mu_n                        (level-only trend metric, bit 0 = 1)
+ * and Def 9 becomes P_s = A_s Vs, P_t = A_t Vt. */
+static void oracle_components(const double* z, const double* mu, const double* kappa, int N,
+                              int S, int level_only, int detrended, double* Vs, double* Vt) {
+  for (int n = 0; n < N; n++)
+    for (int t = 0; t < S; t++) {
+      double tt = (double)t - 0.5 * (double)(S - 1);
+      Vs[n * S + t] = detrended ? z[n * S + t] - kappa[n] * tt : z[n * S + t];
+      Vt[n * S + t] = level_only ? mu[n] : mu[n] + kappa[n] * tt;
+    }
+}
+
 /* Def 10-11 (linear head, NS "the per-channel linear head maps to the
  * forecast horizon"; A7, A8, A11, A3):
  * Y[m][t] = sum_n ws[m][n] P_s[n][t] + wt[m][n] P_t[n][t];
@@ -197,7 +215,7 @@ int oracle_series_ex(const float* x, int32_t L, int32_t S, int32_t H, const floa
   int32_t N, r, M;
   if (oracle_dims(L, S, H, &N, &r, &M) != 0) return -1;
   if (!(tau_s > 0.0) || !(tau_t > 0.0)) return -1;
-  if (metric_variant < 0 || metric_variant > 3 || !(eps_r >= 0.0)) return -1;
+  if (metric_variant < 0 || metric_variant > 7 || !(eps_r >= 0.0)) return -1;
   size_t nS = (size_t)N * S, nN = (size_t)N * N, mS = (size_t)M * S;
   double* X = (double*)malloc(nS * sizeof(double));
   double* z = (double*)malloc(nS * sizeof(double));
@@ -237,8 +255,18 @@ int oracle_series_ex(const float* x, int32_t L, int32_t S, int32_t H, const floa
   for (size_t k = 0; k < nN; k++) Dh[k] = D[k] / (sigma2 + ORACLE_EPS_T);
   oracle_softmax_rows(rho, N, +1.0, 1.0 / tau_s, As);              /* Def 8   */
   oracle_softmax_rows(Dh, N, -1.0, 1.0 / tau_t, At);               /* Def 8   */
-  oracle_aggregate(As, X, N, S, Ps);                               /* Def 9   */
-  oracle_aggregate(At, X, N, S, Pt);                               /* Def 9   */
+  if (metric_variant & 4) {                                        /* f3, A10 */
+    double* Vs = (double*)malloc(nS * sizeof(double));
+    double* Vt = (double*)malloc(nS * sizeof(double));
+    oracle_components(z, mu, kap, N, S, metric_variant & 1, metric_variant & 2, Vs, Vt);
+    oracle_aggregate(As, Vs, N, S, Ps);                            /* Def 9 on Vs */
+    oracle_aggregate(At, Vt, N, S, Pt);                            /* Def 9 on Vt */
+    free(Vs);
+    free(Vt);
+  } else {
+    oracle_aggregate(As, X, N, S, Ps);                             /* Def 9   */
+    oracle_aggregate(At, X, N, S, Pt);                             /* Def 9   */
+  }
   oracle_head(Ps, Pt, ws, wt, bias, N, S, M, H, Yf, y);            /* Def 10-11 */
   if (instance_norm)                                               /* f1      */
     for (int32_t h = 0; h < H; h++) y[h] = y[h] * s_r + mu_r;

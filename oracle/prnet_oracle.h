@@ -66,9 +66,12 @@ int oracle_series(const float* x, int32_t L, int32_t S, int32_t H,
  * metric_variant bit 0: level-only trend distance D_ij = (mu_i - mu_j)^2;
  * metric_variant bit 1: seasonal metric on the residuals about each segment's
  *                       least-squares line;
+ * metric_variant bit 2: component values (A10 variant, reading R-f4): the seasonal
+ *                       branch aggregates z_n (bit 1: z_n - kappa_n ttilde), the trend
+ *                       branch the line T_n (bit 0: the level mu_n);
  * instance_norm != 0:   RevIN-style normalisation of the segmented points with
  *                       eps_r, de-normalised forecast.
- * Returns -1 also for metric_variant outside [0, 3] or eps_r < 0. */
+ * Returns -1 also for metric_variant outside [0, 7] or eps_r < 0. */
 int oracle_series_ex(const float* x, int32_t L, int32_t S, int32_t H,
                      const float* ws, const float* wt, const float* bias,
                      double tau_s, double tau_t, int32_t metric_variant,

@@ -108,11 +108,12 @@ def test_metric_bits_compose(oracle_mod):
 def test_metric_variant_rejected_out_of_range(oracle_mod):
     with pytest.raises(ValueError):
         _run(oracle_mod, np.zeros(48), 24, 24, np.zeros((1, 2)), np.zeros((1, 2)),
-             np.zeros(24), mv=4)
+             np.zeros(24), mv=8)
 
 
 # ------------------------------------------------------------ f1: instance normalisation
-def test_revin_affine_equivariance_without_eps(oracle_mod):
+@pytest.mark.parametrize("mv", [0, 6, 7])
+def test_revin_affine_equivariance_without_eps(oracle_mod, mv):
     """With eps_r = 0 the normalised input of a x + b (a > 0) is that of x, so
     f(a x + b) = a f(x) + b exactly (up to fp64 rounding): pins the normalise /
     de-normalise pair, its sign and its placement around the whole method."""
@@ -123,12 +124,13 @@ def test_revin_affine_equivariance_without_eps(oracle_mod):
     a, b = 4.0, -3.0
     x32 = x.astype(np.float32)
     assert np.array_equal((a * x32 + b).astype(np.float64), a * x + b)
-    y0 = _run(oracle_mod, x32, S, H, *p, rev=True, eps_r=0.0)["y"]
-    y1 = _run(oracle_mod, (a * x32 + b).astype(np.float32), S, H, *p, rev=True, eps_r=0.0)["y"]
+    y0 = _run(oracle_mod, x32, S, H, *p, mv=mv, rev=True, eps_r=0.0)["y"]
+    y1 = _run(oracle_mod, (a * x32 + b).astype(np.float32), S, H, *p, mv=mv, rev=True,
+              eps_r=0.0)["y"]
     np.testing.assert_allclose(y1, a * y0 + b, atol=1e-9)
     # without RevIN the same map does not commute (the bias and the level are not rescaled)
-    z0 = _run(oracle_mod, x32, S, H, *p)["y"]
-    z1 = _run(oracle_mod, (a * x32 + b).astype(np.float32), S, H, *p)["y"]
+    z0 = _run(oracle_mod, x32, S, H, *p, mv=mv)["y"]
+    z1 = _run(oracle_mod, (a * x32 + b).astype(np.float32), S, H, *p, mv=mv)["y"]
     assert np.abs(z1 - (a * z0 + b)).max() > 1e-2
 
 
@@ -168,3 +170,73 @@ def test_revin_on_standardised_input_is_identity_map(oracle_mod):
     p = _params(rng, 1, N, H)
     np.testing.assert_allclose(_run(oracle_mod, x, S, H, *p, rev=True)["y"],
                                _run(oracle_mod, x, S, H, *p)["y"], atol=2e-6)
+
+
+# ------------------------------------------------------------ f3: component values (A10)
+def _lines(seg):
+    """Least-squares line of each segment (library polyfit) and its residual."""
+    S = seg.shape[1]
+    t = np.arange(S, dtype=np.float64)
+    T = np.array([np.polyval(np.polyfit(t, row, 1), t) for row in seg])
+    return T, seg - T
+
+
+@pytest.mark.parametrize("mv", [4, 5, 6, 7])
+def test_component_values_seasonal_branch(oracle_mod, mv):
+    """W_t = 0: Y = W_s A_s V_s with V_s the mean-centred segments (np.mean), or with
+    bit 1 the residuals about the np.polyfit line."""
+    rng = np.random.default_rng(20 + mv)
+    S, N, H = 12, 6, 36
+    x = rng.normal(size=N * S).astype(np.float32) + np.linspace(0, 3, N * S, dtype=np.float32)
+    ws, wt, b = _params(rng, 3, N, H)
+    r = _run(oracle_mod, x, S, H, ws, np.zeros_like(wt), b, mv=mv)
+    seg = x.astype(np.float64).reshape(N, S)
+    vs = _lines(seg)[1] if mv & 2 else seg - seg.mean(axis=1, keepdims=True)
+    np.testing.assert_allclose(r["y_full"], ws.astype(np.float64) @ r["a_s"] @ vs, atol=1e-12)
+
+
+@pytest.mark.parametrize("mv", [4, 5, 6, 7])
+def test_component_values_trend_branch(oracle_mod, mv):
+    """W_s = 0: Y = W_t A_t V_t with V_t the np.polyfit line of each segment, or with
+    bit 0 (level-only trend) its mean: every output segment is a line / a constant."""
+    rng = np.random.default_rng(30 + mv)
+    S, N, H = 12, 6, 36
+    x = rng.normal(size=N * S).astype(np.float32)
+    ws, wt, b = _params(rng, 3, N, H)
+    r = _run(oracle_mod, x, S, H, np.zeros_like(ws), wt, b, mv=mv)
+    seg = x.astype(np.float64).reshape(N, S)
+    vt = np.repeat(seg.mean(axis=1, keepdims=True), S, axis=1) if mv & 1 else _lines(seg)[0]
+    np.testing.assert_allclose(r["y_full"], wt.astype(np.float64) @ r["a_t"] @ vt, atol=1e-12)
+    d2 = np.diff(r["y_full"], n=2, axis=1)            # lines: zero second differences
+    np.testing.assert_allclose(d2, 0.0, atol=1e-12)
+    if mv & 1:
+        np.testing.assert_allclose(np.diff(r["y_full"], axis=1), 0.0, atol=1e-12)
+
+
+def test_component_values_detrended_split_sums_to_the_series(oracle_mod):
+    """mv = 6: residual + line = the segment.  With uniform attention (tau -> inf) and
+    W_s = W_t = W, the component forecast is half the plain one (which aggregates X in
+    both branches)."""
+    rng = np.random.default_rng(40)
+    S, N, H = 8, 5, 16
+    x = rng.normal(size=N * S).astype(np.float32)
+    w, _, b = _params(rng, 2, N, H)
+    big = 1e12
+    yc = _run(oracle_mod, x, S, H, w, w, b, tau_s=big, tau_t=big, mv=6)["y"]
+    yp = _run(oracle_mod, x, S, H, w, w, b, tau_s=big, tau_t=big, mv=0)["y"]
+    np.testing.assert_allclose(yc - b, (yp - b) / 2, atol=1e-9)
+    # plain component split (mv = 4) does not sum to X: z_n + T_n = X_n + kappa_n t~
+    y4 = _run(oracle_mod, x, S, H, w, w, b, tau_s=big, tau_t=big, mv=4)["y"]
+    assert np.abs((y4 - b) - (yp - b) / 2).max() > 1e-3
+
+
+def test_component_values_leave_attention_unchanged(oracle_mod):
+    """Bit 2 changes only the aggregated values, never the attention weights."""
+    rng = np.random.default_rng(41)
+    x = rng.normal(size=96).astype(np.float32)
+    p = _params(rng, 2, 4, 48)
+    for mv in range(4):
+        a = _run(oracle_mod, x, 24, 48, *p, mv=mv)
+        c = _run(oracle_mod, x, 24, 48, *p, mv=mv | 4)
+        np.testing.assert_array_equal(a["a_s"], c["a_s"])
+        np.testing.assert_array_equal(a["a_t"], c["a_t"])
