@@ -44,12 +44,14 @@ typedef enum {
   PRNET_ERR_INVALID_ARG = 1, /* NULL pointer with B > 0, C < 1, S < 2, L < S, H < 1,
                                 tau <= 0 or non-finite, wrong parameter counts, B < 0,
                                 size overflow, abi_version not 1 or 2, metric_variant
-                                outside [0, 3], instance_norm not 0/1                  */
+                                outside [0, 7], instance_norm not 0/1                  */
   PRNET_ERR_BAD_STATE = 2,   /* forward before load_params; NULL handle                  */
   PRNET_ERR_UNSUPPORTED = 3, /* device is not sm_100 (cc 10.x); x/y not 16-byte aligned;
                                 x and y overlap; pointer not on the handle's device;
                                 shape beyond the compiled limits (N > 512, S > 128);
-                                metric_variant != 0 or instance_norm with N > 32       */
+                                widening (metric_variant bits 1-2, instance_norm) on a
+                                shape no kernel implements it for (see
+                                prnet_set_kernel_variant)                               */
   PRNET_ERR_CUDA = 4,        /* CUDA runtime or launch error (text: prnet_last_error)    */
   PRNET_ERR_OOM = 5          /* device or pinned-host allocation failed                  */
 } prnet_status;
@@ -65,7 +67,13 @@ typedef struct {
   int32_t metric_variant;   /* bit flags, 0 = the DESIGN.md §3 reading; SURVEY §8(f) f3:
                                bit 0 = level-only trend distance D = (mu_i - mu_j)^2;
                                bit 1 = seasonal metric on the residuals about each
-                                       segment's least-squares line.  Values > 3 invalid. */
+                                       segment's least-squares line;
+                               bit 2 = component values (A10 variant, DESIGN.md §3 R-f4):
+                                       the seasonal branch aggregates z_n (bit 1: the
+                                       residual z_n - kappa_n t~), the trend branch the
+                                       line mu_n + kappa_n t~ (bit 0: the level mu_n)
+                                       instead of the raw segments; N <= 32, M <= 32,
+                                       S <= 128 (mma_f16x3).  Values > 7 invalid.        */
   float tau_seasonal;       /* tau_s > 0: softmax temperature of the seasonal branch (A6) */
   float tau_trend;          /* tau_t > 0: softmax temperature of the trend branch (A6)    */
   int32_t device;           /* CUDA device ordinal the handle is bound to                 */

@@ -46,14 +46,19 @@ namespace prnet {
 // Shared-memory layout, identical on host (plan) and device (compile-time for SC = 24):
 // [W' hi | W' lo]  [per-warp regions x nwarps]  [bias fp32 [H]]
 // per-warp: xbuf fp32 [nr*S] | X' hi, lo [nr][sph] | Z' hi, lo [nr][zph] | misc (row
-// descriptors float4[32], x0/m1[64], mbarrier)
+// descriptors float4[32], x0/m1/kappa[96], mbarrier, and with `extra` = kCompBytes the
+// component-value vectors of the generic path)
 struct MmaOffsets {
   int xhi, xlo, zhi, zlo, misc, pw;   // per-warp
   int zhi_bytes;                      // bytes of one Z' plane (Z' hi, lo are contiguous)
   int wlo, wpack;                     // CTA-shared head
 };
 __host__ __device__ constexpr int r16(int v) { return (v + 15) & ~15; }
-__host__ __device__ constexpr MmaOffsets mma_offsets(int nr, int S, int sph, int zph, int mmt) {
+// generic path, metric_variant bit 2: mu^, kappa^, A_s mu^, A_s kappa^, A_t mu^, A_t kappa^,
+// alpha, beta  [8][32] floats
+constexpr int kCompBytes = 8 * 32 * 4;
+__host__ __device__ constexpr MmaOffsets mma_offsets(int nr, int S, int sph, int zph, int mmt,
+                                                     int extra = 0) {
   MmaOffsets o{};
   int off = r16(nr * S * 4);
   o.xhi = off;
@@ -66,7 +71,7 @@ __host__ __device__ constexpr MmaOffsets mma_offsets(int nr, int S, int sph, int
   o.zlo = off;
   off = r16(off + nr * zph * 2);
   o.misc = off;
-  off += 512 + 384 + 16;
+  off += 512 + 384 + 16 + extra;
   o.pw = (off + 127) & ~127;
   const int wph = 2 * nr + 8, rows = 16 * mmt;
   o.wlo = rows * wph * 2;
@@ -124,6 +129,7 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
   float4* dsc = reinterpret_cast<float4*>(wb + (SC > 0 ? KO.misc : ly.off_diag));
   float* rsm = reinterpret_cast<float*>(dsc + 32);            // [96] x0, m1, kappa per row
   uint64_t* xbar = reinterpret_cast<uint64_t*>(rsm + 96);     // TMA completion barrier
+  float* cvec = rsm + 100;   // generic path, component values: [8][32] (kCompBytes)
   if (lane == 0) mbar_init(xbar, 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   {
@@ -362,10 +368,36 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
       const float invh = rsqrtf(nh2 + kEpsSeasonal);
       dsc[lane] = i < N ? make_float4((mu - mr) * cm, kap * ck, invh * rr, sqrtf(nh2) * invh)
                         : make_float4(0.f, 0.f, 1.f, 0.f);
+      if (SC == 0 && a.comp) {   // the (normalised) segment level and slope, by column
+        cvec[lane] = i < N ? (mu - mr) * rr : 0.f;
+        cvec[32 + lane] = i < N ? kap * rr : 0.f;
+      }
       __syncwarp();
     }
 
-    float qa[MMT][2 * MT][4];  // Q' = sw (W_s A_s + W_t A_t)
+    // component values (generic path): row ii of A times mu^ and kappa^, reduced over the
+    // quad's 4 lanes, into cvec[dst + ii], cvec[dst + 32 + ii]
+    const bool comp = SC == 0 && a.comp;
+    auto comp_rows = [&](const float2 (&p)[2 * MT], int ii, int dst) {
+      float2 am = f2(0.f), ak = f2(0.f);
+#pragma unroll
+      for (int nt = 0; nt < 2 * MT; nt++) {
+        const int j = 8 * nt + 2 * cq;
+        am = fma2(p[nt], make_float2(cvec[j], cvec[j + 1]), am);
+        ak = fma2(p[nt], make_float2(cvec[32 + j], cvec[33 + j]), ak);
+      }
+      float sm = am.x + am.y, sk = ak.x + ak.y;
+      sm += __shfl_xor_sync(0xffffffffu, sm, 1);
+      sk += __shfl_xor_sync(0xffffffffu, sk, 1);
+      sm += __shfl_xor_sync(0xffffffffu, sm, 2);
+      sk += __shfl_xor_sync(0xffffffffu, sk, 2);
+      if (cq == 0) {
+        cvec[dst + ii] = ii < N ? sm : 0.f;
+        cvec[dst + 32 + ii] = ii < N ? sk : 0.f;
+      }
+    };
+
+    float qa[MMT][2 * MT][4];  // Q' = sw (W_s A_s + W_t A_t)   (component values: sw W_s A_s)
 #pragma unroll
     for (int mm = 0; mm < MMT; mm++)
 #pragma unroll
@@ -406,6 +438,12 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
           sum += __shfl_xor_sync(0xffffffffu, sum, 1);
           sum += __shfl_xor_sync(0xffffffffu, sum, 2);
           const float2 rs2 = f2(ii < N ? fast_rcp(sum) : 0.f);
+          if (comp) {
+            float2 pr[2 * MT];
+#pragma unroll
+            for (int nt = 0; nt < 2 * MT; nt++) pr[nt] = mul2(u[nt], rs2);
+            comp_rows(pr, ii, 128);
+          }
 #pragma unroll
           for (int nt = 0; nt < 2 * MT; nt++) {
             const float2 p = mul2(u[nt], rs2);
@@ -423,7 +461,7 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
             bl[nt][h] = movm_t(lo);
           }
         }
-        fold_tile(qa, NR, mt, bh, bl);
+        if (!comp) fold_tile(qa, NR, mt, bh, bl);
       }
     }
 
@@ -514,6 +552,12 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
           sum += __shfl_xor_sync(0xffffffffu, sum, 1);
           sum += __shfl_xor_sync(0xffffffffu, sum, 2);
           const float2 rs2 = f2(ii < N ? fast_rcp(sum) : 0.f);
+          if (comp) {
+            float2 pr[2 * MT];
+#pragma unroll
+            for (int nt = 0; nt < 2 * MT; nt++) pr[nt] = mul2(u[nt], rs2);
+            comp_rows(pr, ii, 64);
+          }
 #pragma unroll
           for (int nt = 0; nt < 2 * MT; nt++) {
             const float2 p = mul2(u[nt], rs2);
@@ -540,6 +584,28 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
     // the output staging row (bstore) overwrites the Z' tiles the Gram's ldmatrix just read
     // (other lanes' rows): order the two explicitly
     if (bstore) __syncwarp();
+    if (comp) {
+      // Y = W_s A_s V_s + W_t A_t V_t with V_s = X^ - mu^ - d1 kappa^ t~, V_t = mu^ + d0 kappa^ t~
+      //   = (W_s A_s) X^ + alpha_m + beta_m t~      (d1 = bit 1, d0 = 1 - bit 0)
+      // alpha = W_t (A_t mu^) - W_s (A_s mu^), beta = d0 W_t (A_t kappa^) - d1 W_s (A_s kappa^);
+      // W from the packed head (W' = W sw as fp16 hi + lo), stored times sr (de-normalised)
+      __syncwarp();
+      const int m = lane;
+      float al = 0.f, be = 0.f;
+      if (m < M) {
+        const float d0 = a.vtrend != 0.f ? 1.f : 0.f, d1 = a.detrend ? 1.f : 0.f;
+        for (int n = 0; n < N; n++) {
+          const float ws_ = __half2float(w_hi[m * WPH + n]) + __half2float(w_lo[m * WPH + n]);
+          const float wt_ =
+              __half2float(w_hi[m * WPH + NR + n]) + __half2float(w_lo[m * WPH + NR + n]);
+          al = fmaf(wt_, cvec[128 + n], fmaf(-ws_, cvec[64 + n], al));
+          be = fmaf(d0 * wt_, cvec[160 + n], fmaf(-d1 * ws_, cvec[96 + n], be));
+        }
+      }
+      cvec[192 + lane] = al * inv_sw * sr;
+      cvec[224 + lane] = be * inv_sw * sr;
+      __syncwarp();
+    }
     const float2 ys2 = f2(inv_sw * sr / sx);
     const bool pair_store = ((S | H) & 1) == 0;   // t, hh even -> 8-byte aligned pairs
     float* yg = a.y + series * H;
@@ -616,13 +682,22 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
                 if (hh >= H) continue;
                 float2 bb = *reinterpret_cast<const float2*>(bS + hh);
                 if (SC == 0 && a.revin) bb = fma2(bb, f2(sr), f2(mr));   // y = yhat sr + mr
+                if (comp)
+                  bb = add2(bb, fma2(f2(cvec[224 + m]),
+                                     make_float2((float)t - a.half_s, (float)t + 1.f - a.half_s),
+                                     f2(cvec[192 + m])));
                 const float2 o = add2(v, bb);
                 asm volatile("st.global.cs.v2.f32 [%0], {%1,%2};" ::"l"(yg + hh), "f"(o.x),
                              "f"(o.y)
                              : "memory");
               } else {
-                if (hh < H) yg[hh] = v.x + fmaf(bS[hh], sr, mr);
-                if (t + 1 < S && hh + 1 < H) yg[hh + 1] = v.y + fmaf(bS[hh + 1], sr, mr);
+                float c0 = 0.f, c1 = 0.f;
+                if (comp) {
+                  c0 = fmaf(cvec[224 + m], (float)t - a.half_s, cvec[192 + m]);
+                  c1 = fmaf(cvec[224 + m], (float)t + 1.f - a.half_s, cvec[192 + m]);
+                }
+                if (hh < H) yg[hh] = v.x + fmaf(bS[hh], sr, mr) + c0;
+                if (t + 1 < S && hh + 1 < H) yg[hh + 1] = v.y + fmaf(bS[hh + 1], sr, mr) + c1;
               }
             }
           }
@@ -691,7 +766,7 @@ bool plan_mma_kernel(const FwdArgs& a, int max_smem_optin, MmaPlan* p) {
   p->mt = a.N <= 16 ? 1 : 2;
   p->mmt = a.M <= 16 ? 1 : 2;
   // the S = 24 instantiations implement the plain reading only (the widening runs generic)
-  p->sc = (a.S == 24 && !a.detrend && !a.revin) ? 24 : 0;
+  p->sc = (a.S == 24 && !a.detrend && !a.revin && !a.comp) ? 24 : 0;
   ly.nr = 16 * p->mt;
   if (p->sc == 24) {  // dense rows of 24 halves (48 B: 16-byte aligned, conflict-free ldmatrix)
     ly.sph = 24;
@@ -704,7 +779,7 @@ bool plan_mma_kernel(const FwdArgs& a, int max_smem_optin, MmaPlan* p) {
   }
   ly.wph = 2 * ly.nr + 8;
   ly.ntt = (a.S + 7) / 8;
-  const MmaOffsets o = mma_offsets(ly.nr, a.S, ly.sph, ly.zph, p->mmt);
+  const MmaOffsets o = mma_offsets(ly.nr, a.S, ly.sph, ly.zph, p->mmt, p->sc == 0 ? kCompBytes : 0);
   ly.xbuf_f = ly.nr * a.S;
   ly.off_xhi = o.xhi;
   ly.off_xlo = o.xlo;

@@ -103,6 +103,7 @@ prnet::FwdArgs make_args(const prnet_handle* h, const float* x, int64_t B, float
   a.vtrend = (c.metric_variant & 1) ? 0.f : (float)((S * S - 1.0) / 12.0);
   a.detrend = (c.metric_variant >> 1) & 1;
   a.revin = c.instance_norm;
+  a.comp = (c.metric_variant >> 2) & 1;
   a.inv_s = (float)(1.0 / S);
   a.inv_n = (float)(1.0 / h->N);
   a.inv_ns = (float)(1.0 / ((double)h->N * S));
@@ -151,11 +152,20 @@ bool tcq_applicable(const prnet_handle* h) {
 }
 // Variants that implement the SURVEY §8(f) widening: the level-only trend runs in every
 // kernel (a.vtrend = 0); the detrended seasonal metric and instance normalisation in
-// tc_quad, mma_f16x3 (N <= 32) and flash_f16x3 (16 < N <= 512, S <= 48).
+// tc_quad, mma_f16x3 (N <= 32) and flash_f16x3 (16 < N <= 512, S <= 48); component values
+// (bit 2) in mma_f16x3.
 bool widening_on(const prnet_handle* h) {
-  return (h->cfg.metric_variant & 2) != 0 || h->cfg.instance_norm != 0;
+  return (h->cfg.metric_variant & 6) != 0 || h->cfg.instance_norm != 0;
 }
-bool variant_supports_widening(int v) { return v == 2 || v == 5 || v == 6; }
+bool comp_on(const prnet_handle* h) { return (h->cfg.metric_variant & 4) != 0; }
+bool variant_supports_widening(const prnet_handle* h, int v) {
+  if (comp_on(h)) return v == 2;
+  return v == 2 || v == 5 || v == 6;
+}
+const char* kWideningMsg =
+    "metric_variant bit 1 / instance_norm need tc_quad, mma_f16x3 (N <= 32) or flash_f16x3 "
+    "(16 < N <= 512, S <= 48, M <= 32); metric_variant bit 2 needs mma_f16x3 (N <= 32, "
+    "M <= 32, S <= 128)";
 // 7 = small_f32 (N <= 16, S <= 128, M <= 32: lanes over time, FP32)
 bool small_applicable(const prnet_handle* h) {
   return h->N <= 16 && h->cfg.seg_len <= 128 && h->M <= 32;
@@ -163,6 +173,7 @@ bool small_applicable(const prnet_handle* h) {
 int pick_variant(const prnet_handle* h) {
   if (h->forced_variant >= 0) return h->forced_variant;
   if (widening_on(h)) {
+    if (comp_on(h)) return h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128 ? 2 : -1;
     if (tcq_applicable(h) && h->N > 16) return 6;
     if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
     if (flash_applicable(h)) return 5;
@@ -196,10 +207,8 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
   a.a_t_dbg = a_t;
   cudaError_t e;
   int v = pick_variant(h);
-  if (v < 0 || (widening_on(h) && !variant_supports_widening(v)))
-    return fail(h, PRNET_ERR_UNSUPPORTED,
-                "metric_variant bit 1 / instance_norm need tc_quad, mma_f16x3 (N <= 32) or "
-                "flash_f16x3 (16 < N <= 512, S <= 48, M <= 32)");
+  if (v < 0 || (widening_on(h) && !variant_supports_widening(h, v)))
+    return fail(h, PRNET_ERR_UNSUPPORTED, kWideningMsg);
   if (v == 1 && a_s != nullptr) v = 0;  // the attention dump lives in the N <= 32 kernels
   if (v == 7 && a_s != nullptr) v = 2;
   if (v == 6 && a_s != nullptr) v = 2;
@@ -307,9 +316,10 @@ prnet_status prnet_create(const prnet_config* cfg, prnet_handle** out) {
   if (!(cfg->tau_seasonal > 0.f) || !std::isfinite(cfg->tau_seasonal) ||
       !(cfg->tau_trend > 0.f) || !std::isfinite(cfg->tau_trend))
     return fail(nullptr, PRNET_ERR_INVALID_ARG, "temperatures must be finite and > 0");
-  if (cfg->metric_variant < 0 || cfg->metric_variant > 3)
+  if (cfg->metric_variant < 0 || cfg->metric_variant > 7)
     return fail(nullptr, PRNET_ERR_INVALID_ARG,
-                "metric_variant must be in [0, 3] (bit 0 level trend, bit 1 detrended seasonal)");
+                "metric_variant must be in [0, 7] (bit 0 level trend, bit 1 detrended seasonal, "
+                "bit 2 component values)");
   if (cfg->instance_norm != 0 && cfg->instance_norm != 1)
     return fail(nullptr, PRNET_ERR_INVALID_ARG, "instance_norm must be 0 or 1");
   if (cfg->channels > 65535)
@@ -695,9 +705,8 @@ prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {
     return fail(h, PRNET_ERR_UNSUPPORTED, "variant needs N <= 32");
   if (variant == 2 && (h->M > 32 || h->cfg.seg_len > 128))
     return fail(h, PRNET_ERR_UNSUPPORTED, "tensor-core variant needs M <= 32 and S <= 128");
-  if (variant >= 0 && widening_on(h) && !variant_supports_widening(variant))
-    return fail(h, PRNET_ERR_UNSUPPORTED,
-                "metric_variant bit 1 / instance_norm need tc_quad, mma_f16x3 or flash_f16x3");
+  if (variant >= 0 && widening_on(h) && !variant_supports_widening(h, variant))
+    return fail(h, PRNET_ERR_UNSUPPORTED, kWideningMsg);
   h->forced_variant = variant;
   return PRNET_OK;
 }

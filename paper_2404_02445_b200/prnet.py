@@ -90,7 +90,8 @@ class PRNet:
     def __init__(self, channels: int, lookback: int, seg_len: int, horizon: int,
                  head_per_channel: bool = True, tau_s: float = 1.0, tau_t: float = 1.0,
                  device: int = 0, metric_variant: int = 0, instance_norm: bool = False):
-        """metric_variant: bit 0 level-only trend, bit 1 detrended seasonal metric;
+        """metric_variant: bit 0 level-only trend, bit 1 detrended seasonal metric, bit 2
+        component values (reading R-f4);
         instance_norm: RevIN-style normalisation (include/prnet.h)."""
         self._lib = load_library()
         cfg = PrnetConfig(PRNET_ABI_VERSION, channels, lookback, seg_len, horizon,

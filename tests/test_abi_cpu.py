@@ -65,7 +65,7 @@ def test_create_validates_before_touching_the_device(lib):
     h = ctypes.c_void_p(123)
     for bad in [dict(seg_len=1), dict(lookback=10), dict(horizon=0), dict(channels=0),
                 dict(tau_seasonal=0.0), dict(tau_trend=float("nan")), dict(abi_version=3),
-                dict(abi_version=0), dict(metric_variant=4), dict(metric_variant=-1),
+                dict(abi_version=0), dict(metric_variant=8), dict(metric_variant=-1),
                 dict(instance_norm=2)]:
         kw = dict(abi_version=2, channels=7, lookback=96, seg_len=24, horizon=96,
                   head_per_channel=1, metric_variant=0, tau_seasonal=1.0, tau_trend=1.0, device=0,

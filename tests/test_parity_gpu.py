@@ -354,6 +354,38 @@ def test_widening_parity_long_lookback(oracle_mod, L, S, H, mv, rev):
     _check_widening(oracle_mod, x, S, H, mv, rev)
 
 
+@pytest.mark.parametrize("mv,rev", [(4, False), (5, False), (6, False), (7, False), (4, True),
+                                    (7, True)])
+@pytest.mark.parametrize("L,S,H", [(720, 24, 720), (720, 24, 336), (100, 24, 90), (96, 24, 96),
+                                   (97, 7, 13), (128, 8, 64), (270, 9, 31), (384, 128, 200)])
+def test_component_values_parity(oracle_mod, L, S, H, mv, rev):
+    """metric_variant bit 2 (component values, reading R-f4): mma_f16x3's generic path."""
+    x = synth.random_windows(3, 5, L, kind="mixed")
+    _check_widening(oracle_mod, x, S, H, mv, rev)
+
+
+@pytest.mark.parametrize("kind", ["normal", "constant", "scaled"])
+@pytest.mark.parametrize("tau,hpc", [(0.05, True), (1.0, False), (10.0, True)])
+def test_component_values_distributions(oracle_mod, kind, tau, hpc):
+    x = synth.random_windows(3, 4, 720, kind=kind)
+    _check_widening(oracle_mod, x, 24, 336, 6, kind == "scaled", tau_s=tau, tau_t=tau * 0.7,
+                    hpc=hpc)
+
+
+def test_component_values_unsupported_paths():
+    m = PRNet(3, 1440, 24, 96, metric_variant=4)        # N = 60: only mma_f16x3 has bit 2
+    m.load(np.zeros((3, m.M, m.N)), np.zeros((3, m.M, m.N)), np.zeros((3, 96)))
+    with pytest.raises(PrnetError) as e:
+        m.forward(torch.zeros((2, 3, 1440), device="cuda"))
+    assert e.value.status == 3
+    m2 = PRNet(3, 720, 24, 96, metric_variant=4)
+    for v in ("tc_quad", "flash_f16x3", "small_f32", "warp_f32"):
+        with pytest.raises(PrnetError) as e:
+            m2.set_variant(v)
+        assert e.value.status == 3
+    m2.set_variant("mma_f16x3")
+
+
 def test_widening_unsupported_paths():
     m = PRNet(3, 3840, 96, 96, metric_variant=2)        # N = 40, S = 96: no kernel for bit 1
     m.load(np.zeros((3, m.M, m.N)), np.zeros((3, m.M, m.N)), np.zeros((3, 96)))
