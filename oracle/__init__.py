@@ -69,13 +69,13 @@ def _load():
         lib.oracle_series_ex.argtypes = [_f32p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                          _f32p, _f32p, _f32p, ctypes.c_double, ctypes.c_double,
                                          ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
-                                         _f64p, ctypes.POINTER(_Debug)]
+                                         ctypes.c_int32, _f64p, ctypes.POINTER(_Debug)]
         lib.oracle_series_ex.restype = ctypes.c_int
         lib.oracle_forward_ex.argtypes = [_f32p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                           ctypes.c_int32, ctypes.c_int32, _f32p, _f32p, _f32p,
                                           ctypes.c_int32, ctypes.c_double, ctypes.c_double,
                                           ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
-                                          _f32p, _f64p]
+                                          ctypes.c_int32, _f32p, _f64p]
         lib.oracle_forward_ex.restype = ctypes.c_int
         lib.oracle_error_sums.argtypes = [_f32p, _f32p, ctypes.c_int64, _f64p]
         lib.oracle_error_sums.restype = None
@@ -95,11 +95,12 @@ EPS_REVIN = 1e-5   # RevIN epsilon of the product (R-f1)
 
 
 def series(x, S, H, ws, wt, bias, tau_s=1.0, tau_t=1.0, metric_variant=0, instance_norm=False,
-           eps_r=EPS_REVIN):
+           eps_r=EPS_REVIN, ma_kernel=0):
     """One series; returns a dict with y and every intermediate (fp64).
     metric_variant bit 0 = level-only trend, bit 1 = detrended seasonal, bit 2 = component
     values (each branch aggregates its own component, reading R-f4); instance_norm =
-    RevIN-style normalisation."""
+    RevIN-style normalisation; ma_kernel = odd k > 0: moving-average decomposition feeding
+    each branch (reading R-f5)."""
     x = np.ascontiguousarray(x, dtype=np.float32).ravel()
     L = x.size
     N, r, M = dims(L, S, H)
@@ -115,8 +116,8 @@ def series(x, S, H, ws, wt, bias, tau_s=1.0, tau_t=1.0, metric_variant=0, instan
     dbg = _Debug(**{k: v.ctypes.data for k, v in out.items()})
     y = np.zeros(H)
     if _load().oracle_series_ex(x, L, S, H, ws, wt, bias, float(tau_s), float(tau_t),
-                                int(metric_variant), int(bool(instance_norm)), float(eps_r), y,
-                                ctypes.byref(dbg)) != 0:
+                                int(metric_variant), int(bool(instance_norm)), float(eps_r),
+                                int(ma_kernel), y, ctypes.byref(dbg)) != 0:
         raise ValueError("oracle_series rejected its arguments")
     out["sigma2"] = float(out["sigma2"][0])
     out["y"] = y
@@ -125,7 +126,7 @@ def series(x, S, H, ws, wt, bias, tau_s=1.0, tau_t=1.0, metric_variant=0, instan
 
 
 def forward(x, S, H, ws, wt, bias, head_per_channel=True, tau_s=1.0, tau_t=1.0,
-            metric_variant=0, instance_norm=False, eps_r=EPS_REVIN):
+            metric_variant=0, instance_norm=False, eps_r=EPS_REVIN, ma_kernel=0):
     """x [B, C, L] fp32 -> (y fp32 [B, C, H], y64 fp64 [B, C, H])."""
     x = np.ascontiguousarray(x, dtype=np.float32)
     B, C, L = x.shape
@@ -138,7 +139,8 @@ def forward(x, S, H, ws, wt, bias, head_per_channel=True, tau_s=1.0, tau_t=1.0,
     y64 = np.zeros((B, C, H), np.float64)
     if _load().oracle_forward_ex(x, B, C, L, S, H, ws, wt, bias, int(bool(head_per_channel)),
                                  float(tau_s), float(tau_t), int(metric_variant),
-                                 int(bool(instance_norm)), float(eps_r), y, y64) != 0:
+                                 int(bool(instance_norm)), float(eps_r), int(ma_kernel), y,
+                                 y64) != 0:
         raise ValueError("oracle_forward rejected its arguments")
     return y, y64
 

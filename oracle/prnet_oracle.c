@@ -202,26 +202,53 @@ static void oracle_head(const double* Ps, const double* Pt, const float* ws, con
   for (int h = 0; h < H; h++) y[h] = Yfull[(h / S) * S + (h % S)] + (double)bias[h];
 }
 
+/* SURVEY §8(f) f3 "moving-average seasonal/trend decomposition feeding each branch"
+ * (reading R-f5 in DESIGN.md §3; the series decomposition of the decomposition-based LTSF
+ * models): over the N*S segmented points p_0..p_{NS-1} (after RevIN when on), with an
+ * odd kernel k = 2h + 1 and the ends padded by repeating the first / last point,
+ *   trend_i = (1/k) sum_{d=-h..h} p_{clamp(i+d, 0, NS-1)},   seasonal_i = p_i - trend_i. */
+static void oracle_decompose(const double* X, int NS, int k, double* Xs, double* Xt) {
+  int h = (k - 1) / 2;
+  for (int i = 0; i < NS; i++) {
+    double s = 0.0;
+    for (int d = -h; d <= h; d++) {
+      int j = i + d;
+      if (j < 0) j = 0;
+      if (j > NS - 1) j = NS - 1;
+      s += X[j];
+    }
+    Xt[i] = s / (double)k;
+    Xs[i] = X[i] - Xt[i];
+  }
+}
+
 int oracle_series(const float* x, int32_t L, int32_t S, int32_t H, const float* ws,
                   const float* wt, const float* bias, double tau_s, double tau_t, double* y,
                   const oracle_debug* dbg) {
-  return oracle_series_ex(x, L, S, H, ws, wt, bias, tau_s, tau_t, 0, 0, 0.0, y, dbg);
+  return oracle_series_ex(x, L, S, H, ws, wt, bias, tau_s, tau_t, 0, 0, 0.0, 0, y, dbg);
 }
 
 int oracle_series_ex(const float* x, int32_t L, int32_t S, int32_t H, const float* ws,
                      const float* wt, const float* bias, double tau_s, double tau_t,
-                     int32_t metric_variant, int32_t instance_norm, double eps_r, double* y,
-                     const oracle_debug* dbg) {
+                     int32_t metric_variant, int32_t instance_norm, double eps_r,
+                     int32_t ma_kernel, double* y, const oracle_debug* dbg) {
   int32_t N, r, M;
   if (oracle_dims(L, S, H, &N, &r, &M) != 0) return -1;
   if (!(tau_s > 0.0) || !(tau_t > 0.0)) return -1;
   if (metric_variant < 0 || metric_variant > 7 || !(eps_r >= 0.0)) return -1;
+  if (ma_kernel < 0 || (ma_kernel > 0 && ma_kernel % 2 == 0)) return -1;
   size_t nS = (size_t)N * S, nN = (size_t)N * N, mS = (size_t)M * S;
   double* X = (double*)malloc(nS * sizeof(double));
-  double* z = (double*)malloc(nS * sizeof(double));
-  double* mu = (double*)malloc(N * sizeof(double));
-  double* nu2 = (double*)malloc(N * sizeof(double));
-  double* kap = (double*)malloc(N * sizeof(double));
+  double* Xs = (double*)malloc(nS * sizeof(double));   /* seasonal branch input */
+  double* Xt = (double*)malloc(nS * sizeof(double));   /* trend branch input    */
+  double* zs = (double*)malloc(nS * sizeof(double));
+  double* zt = (double*)malloc(nS * sizeof(double));
+  double* mus = (double*)malloc(N * sizeof(double));
+  double* nu2s = (double*)malloc(N * sizeof(double));
+  double* kaps = (double*)malloc(N * sizeof(double));
+  double* mut = (double*)malloc(N * sizeof(double));
+  double* nu2t = (double*)malloc(N * sizeof(double));
+  double* kapt = (double*)malloc(N * sizeof(double));
   double* rho = (double*)malloc(nN * sizeof(double));
   double* D = (double*)malloc(nN * sizeof(double));
   double* Dh = (double*)malloc(nN * sizeof(double));
@@ -239,33 +266,44 @@ int oracle_series_ex(const float* x, int32_t L, int32_t S, int32_t H, const floa
     s_r = sqrt(var_r + eps_r);
     for (size_t k = 0; k < nS; k++) X[k] = (X[k] - mu_r) / s_r;
   }
-  oracle_descriptors(X, N, S, mu, z, nu2, kap);                    /* Def 3-4 */
-  double sigma2 = oracle_series_variance(mu, nu2, N, S);           /* Def 5   */
+  if (ma_kernel > 0) {                                             /* f3, R-f5 */
+    oracle_decompose(X, (int)nS, ma_kernel, Xs, Xt);
+  } else {                                    /* both branches see the segments */
+    memcpy(Xs, X, nS * sizeof(double));
+    memcpy(Xt, X, nS * sizeof(double));
+  }
+  oracle_descriptors(Xs, N, S, mus, zs, nu2s, kaps);               /* Def 3-4, seasonal */
+  oracle_descriptors(Xt, N, S, mut, zt, nu2t, kapt);               /* Def 3-4, trend    */
+  double sigma2 = oracle_series_variance(mut, nu2t, N, S);         /* Def 5   */
   if (metric_variant & 2) {                                        /* f3      */
     double* e = (double*)malloc(nS * sizeof(double));
     double* e2 = (double*)malloc(N * sizeof(double));
-    oracle_detrend(z, kap, N, S, e, e2);
+    oracle_detrend(zs, kaps, N, S, e, e2);
     oracle_seasonal_similarity(e, e2, N, S, rho);                  /* Def 6 on e */
     free(e);
     free(e2);
   } else {
-    oracle_seasonal_similarity(z, nu2, N, S, rho);                 /* Def 6   */
+    oracle_seasonal_similarity(zs, nu2s, N, S, rho);               /* Def 6   */
   }
-  oracle_trend_distance(mu, kap, N, S, metric_variant & 1, D);     /* Def 7   */
+  oracle_trend_distance(mut, kapt, N, S, metric_variant & 1, D);   /* Def 7   */
   for (size_t k = 0; k < nN; k++) Dh[k] = D[k] / (sigma2 + ORACLE_EPS_T);
   oracle_softmax_rows(rho, N, +1.0, 1.0 / tau_s, As);              /* Def 8   */
   oracle_softmax_rows(Dh, N, -1.0, 1.0 / tau_t, At);               /* Def 8   */
   if (metric_variant & 4) {                                        /* f3, A10 */
     double* Vs = (double*)malloc(nS * sizeof(double));
     double* Vt = (double*)malloc(nS * sizeof(double));
-    oracle_components(z, mu, kap, N, S, metric_variant & 1, metric_variant & 2, Vs, Vt);
+    double* dummy = (double*)malloc(nS * sizeof(double));
+    /* seasonal component of the seasonal input, trend component of the trend input */
+    oracle_components(zs, mus, kaps, N, S, metric_variant & 1, metric_variant & 2, Vs, dummy);
+    oracle_components(zt, mut, kapt, N, S, metric_variant & 1, metric_variant & 2, dummy, Vt);
     oracle_aggregate(As, Vs, N, S, Ps);                            /* Def 9 on Vs */
     oracle_aggregate(At, Vt, N, S, Pt);                            /* Def 9 on Vt */
     free(Vs);
     free(Vt);
+    free(dummy);
   } else {
-    oracle_aggregate(As, X, N, S, Ps);                             /* Def 9   */
-    oracle_aggregate(At, X, N, S, Pt);                             /* Def 9   */
+    oracle_aggregate(As, Xs, N, S, Ps);                            /* Def 9   */
+    oracle_aggregate(At, Xt, N, S, Pt);                            /* Def 9   */
   }
   oracle_head(Ps, Pt, ws, wt, bias, N, S, M, H, Yf, y);            /* Def 10-11 */
   if (instance_norm)                                               /* f1      */
@@ -273,9 +311,9 @@ int oracle_series_ex(const float* x, int32_t L, int32_t S, int32_t H, const floa
 
   if (dbg) {
     if (dbg->seg) memcpy(dbg->seg, X, nS * sizeof(double));
-    if (dbg->mu) memcpy(dbg->mu, mu, N * sizeof(double));
-    if (dbg->nu2) memcpy(dbg->nu2, nu2, N * sizeof(double));
-    if (dbg->kappa) memcpy(dbg->kappa, kap, N * sizeof(double));
+    if (dbg->mu) memcpy(dbg->mu, mut, N * sizeof(double));
+    if (dbg->nu2) memcpy(dbg->nu2, nu2s, N * sizeof(double));
+    if (dbg->kappa) memcpy(dbg->kappa, kapt, N * sizeof(double));
     if (dbg->sigma2) dbg->sigma2[0] = sigma2;
     if (dbg->rho) memcpy(dbg->rho, rho, nN * sizeof(double));
     if (dbg->dist) memcpy(dbg->dist, D, nN * sizeof(double));
@@ -285,7 +323,8 @@ int oracle_series_ex(const float* x, int32_t L, int32_t S, int32_t H, const floa
     if (dbg->p_t) memcpy(dbg->p_t, Pt, nS * sizeof(double));
     if (dbg->y_full) memcpy(dbg->y_full, Yf, mS * sizeof(double));
   }
-  free(X); free(z); free(mu); free(nu2); free(kap); free(rho); free(D); free(Dh);
+  free(X); free(Xs); free(Xt); free(zs); free(zt); free(mus); free(nu2s); free(kaps);
+  free(mut); free(nu2t); free(kapt); free(rho); free(D); free(Dh);
   free(As); free(At); free(Ps); free(Pt); free(Yf);
   return 0;
 }
@@ -295,14 +334,14 @@ int oracle_forward(const float* x, int64_t B, int32_t C, int32_t L, int32_t S, i
                    int32_t head_per_channel, double tau_s, double tau_t, float* y,
                    double* y64) {
   return oracle_forward_ex(x, B, C, L, S, H, ws, wt, bias, head_per_channel, tau_s, tau_t, 0, 0,
-                           0.0, y, y64);
+                           0.0, 0, y, y64);
 }
 
 int oracle_forward_ex(const float* x, int64_t B, int32_t C, int32_t L, int32_t S, int32_t H,
                       const float* ws, const float* wt, const float* bias,
                       int32_t head_per_channel, double tau_s, double tau_t,
-                      int32_t metric_variant, int32_t instance_norm, double eps_r, float* y,
-                      double* y64) {
+                      int32_t metric_variant, int32_t instance_norm, double eps_r,
+                      int32_t ma_kernel, float* y, double* y64) {
   int32_t N, r, M;
   if (B < 0 || C < 1 || oracle_dims(L, S, H, &N, &r, &M) != 0) return -1;
   double* yy = (double*)malloc((size_t)H * sizeof(double));
@@ -311,7 +350,7 @@ int oracle_forward_ex(const float* x, int64_t B, int32_t C, int32_t L, int32_t S
       int64_t cw = head_per_channel ? c : 0;
       const float* xs = x + (b * C + c) * (int64_t)L;
       if (oracle_series_ex(xs, L, S, H, ws + cw * M * N, wt + cw * M * N, bias + cw * H,
-                           tau_s, tau_t, metric_variant, instance_norm, eps_r, yy,
+                           tau_s, tau_t, metric_variant, instance_norm, eps_r, ma_kernel, yy,
                            NULL) != 0) {
         free(yy);
         return -1;

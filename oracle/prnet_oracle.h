@@ -70,12 +70,18 @@ int oracle_series(const float* x, int32_t L, int32_t S, int32_t H,
  *                       branch aggregates z_n (bit 1: z_n - kappa_n ttilde), the trend
  *                       branch the line T_n (bit 0: the level mu_n);
  * instance_norm != 0:   RevIN-style normalisation of the segmented points with
- *                       eps_r, de-normalised forecast.
- * Returns -1 also for metric_variant outside [0, 7] or eps_r < 0. */
+ *                       eps_r, de-normalised forecast;
+ * ma_kernel = k > 0:    moving-average decomposition (odd k, edge-replicate padding) of
+ *                       the segmented points (reading R-f5): the seasonal branch (Def 3-4,
+ *                       6, 9) runs on x - MA(x), the trend branch (Def 3-5, 7, 9) on MA(x).
+ *                       dbg->mu, kappa, sigma2 are then the trend branch's, dbg->nu2 the
+ *                       seasonal branch's, dbg->seg the segments before the split.
+ * Returns -1 also for metric_variant outside [0, 7], eps_r < 0, ma_kernel < 0 or even. */
 int oracle_series_ex(const float* x, int32_t L, int32_t S, int32_t H,
                      const float* ws, const float* wt, const float* bias,
                      double tau_s, double tau_t, int32_t metric_variant,
-                     int32_t instance_norm, double eps_r, double* y, const oracle_debug* dbg);
+                     int32_t instance_norm, double eps_r, int32_t ma_kernel, double* y,
+                     const oracle_debug* dbg);
 
 /* A batch x[B][C][L] -> y[B][C][H] (fp32, rounded from the fp64 result) and
  * optionally y64 (fp64).  head_per_channel: 1 -> ws/wt are [C][M][N], bias
@@ -90,7 +96,7 @@ int oracle_forward_ex(const float* x, int64_t B, int32_t C, int32_t L, int32_t S
                       int32_t H, const float* ws, const float* wt, const float* bias,
                       int32_t head_per_channel, double tau_s, double tau_t,
                       int32_t metric_variant, int32_t instance_norm, double eps_r,
-                      float* y, double* y64);
+                      int32_t ma_kernel, float* y, double* y64);
 
 /* Sum of squared and absolute errors of y against target (n values), fp64,
  * in index order: out[0] = SSE, out[1] = SAE, out[2] = n.  (Bench metric,

@@ -13,8 +13,9 @@ import numpy as np
 import pytest
 
 
-def _run(o, x, S, H, ws, wt, b, tau_s=1.0, tau_t=1.0, mv=0, rev=False, eps_r=None):
+def _run(o, x, S, H, ws, wt, b, tau_s=1.0, tau_t=1.0, mv=0, rev=False, eps_r=None, ma=0):
     kw = {} if eps_r is None else {"eps_r": eps_r}
+    kw["ma_kernel"] = ma
     return o.series(np.asarray(x, np.float32), S, H, np.asarray(ws, np.float32),
                     np.asarray(wt, np.float32), np.asarray(b, np.float32), tau_s, tau_t,
                     metric_variant=mv, instance_norm=rev, **kw)
@@ -240,3 +241,90 @@ def test_component_values_leave_attention_unchanged(oracle_mod):
         c = _run(oracle_mod, x, 24, 48, *p, mv=mv | 4)
         np.testing.assert_array_equal(a["a_s"], c["a_s"])
         np.testing.assert_array_equal(a["a_t"], c["a_t"])
+
+
+# ------------------------------------------------------------ f3: moving-average decomposition
+def _ma_split(seg_flat, k):
+    """Library moving average: np.pad (edge) + np.convolve, and the remainder."""
+    h = (k - 1) // 2
+    t = np.convolve(np.pad(seg_flat, h, mode="edge"), np.ones(k) / k, mode="valid")
+    return seg_flat - t, t
+
+
+def test_ma_kernel_one_is_all_trend(oracle_mod):
+    """k = 1: the trend is the series and the seasonal part is 0 (uniform A_s, P_s = 0), so
+    the forecast is the plain one with W_s = 0."""
+    rng = np.random.default_rng(50)
+    S, N, H = 12, 5, 30
+    x = rng.normal(size=N * S).astype(np.float32)
+    ws, wt, b = _params(rng, 3, N, H)
+    r = _run(oracle_mod, x, S, H, ws, wt, b, ma=1)
+    np.testing.assert_allclose(r["a_s"], 1.0 / N, atol=1e-12)
+    np.testing.assert_allclose(r["y"], _run(oracle_mod, x, S, H, np.zeros_like(ws), wt, b)["y"],
+                               atol=1e-12)
+
+
+@pytest.mark.parametrize("k", [3, 25])
+def test_ma_components_match_library_convolution(oracle_mod, k):
+    """Uniform attention (tau -> inf) makes each pattern the segment mean of its branch's
+    input: W_t = 0 exposes mean_n Xs_n, W_s = 0 mean_n Xt_n, with Xt = np.convolve of the
+    edge-padded segmented points."""
+    rng = np.random.default_rng(51 + k)
+    S, N, H = 12, 6, 24
+    x = rng.normal(size=N * S + 5).astype(np.float32)   # r = 5 dropped points
+    ws, wt, b = _params(rng, 2, N, H)
+    big = 1e12
+    xs, xt = _ma_split(x[5:].astype(np.float64), k)
+    ys = _run(oracle_mod, x, S, H, ws, np.zeros_like(wt), b, tau_s=big, tau_t=big, ma=k)
+    np.testing.assert_allclose(ys["y_full"], ws.astype(np.float64) @ np.tile(
+        xs.reshape(N, S).mean(axis=0), (N, 1)), atol=1e-9)
+    yt = _run(oracle_mod, x, S, H, np.zeros_like(ws), wt, b, tau_s=big, tau_t=big, ma=k)
+    np.testing.assert_allclose(yt["y_full"], wt.astype(np.float64) @ np.tile(
+        xt.reshape(N, S).mean(axis=0), (N, 1)), atol=1e-9)
+
+
+def test_ma_branch_metrics_on_their_components(oracle_mod):
+    """rho is np.corrcoef of the seasonal component's segments; D is (1/S)|T_i - T_j|^2 of
+    the np.polyfit lines of the trend component's segments; sigma^2 is np.var of the trend
+    component."""
+    rng = np.random.default_rng(53)
+    S, N, k = 16, 5, 7
+    x = (rng.normal(size=N * S) + np.sin(np.arange(N * S) / 3.0)).astype(np.float32)
+    r = _run(oracle_mod, x, S, S, *_params(rng, 1, N, S), ma=k)
+    xs, xt = _ma_split(x.astype(np.float64), k)
+    np.testing.assert_allclose(r["rho"], np.corrcoef(xs.reshape(N, S)), atol=1e-9)
+    T = _lines(xt.reshape(N, S))[0]
+    D = ((T[:, None, :] - T[None, :, :]) ** 2).sum(axis=2) / S
+    np.testing.assert_allclose(r["dist"], D, atol=1e-10)
+    np.testing.assert_allclose(r["sigma2"], xt.var(), atol=1e-12)
+
+
+def test_ma_constant_series_closed_form(oracle_mod):
+    """x = c: trend = c, seasonal = 0, both attentions uniform: y = c W_t 1 + b."""
+    S, N, H = 8, 4, 16
+    rng = np.random.default_rng(54)
+    ws, wt, b = _params(rng, 2, N, H)
+    c = -1.75
+    r = _run(oracle_mod, np.full(N * S, c), S, H, ws, wt, b, ma=5)
+    yf = c * wt.astype(np.float64).sum(axis=1)[:, None] * np.ones((1, S))
+    np.testing.assert_allclose(r["y"], yf.ravel()[:H] + b, atol=1e-12)
+
+
+@pytest.mark.parametrize("mv", [0, 7])
+def test_ma_revin_affine_equivariance(oracle_mod, mv):
+    rng = np.random.default_rng(55)
+    S, N, H = 12, 6, 30
+    x = (np.round(rng.normal(size=N * S) * 1024) / 1024).astype(np.float32)
+    p = _params(rng, 3, N, H)
+    a, b = 2.0, 5.0
+    y0 = _run(oracle_mod, x, S, H, *p, mv=mv, rev=True, eps_r=0.0, ma=9)["y"]
+    y1 = _run(oracle_mod, (a * x + b).astype(np.float32), S, H, *p, mv=mv, rev=True, eps_r=0.0,
+              ma=9)["y"]
+    np.testing.assert_allclose(y1, a * y0 + b, atol=1e-9)
+
+
+@pytest.mark.parametrize("k", [-1, 2, 24])
+def test_ma_kernel_rejected(oracle_mod, k):
+    with pytest.raises(ValueError):
+        _run(oracle_mod, np.zeros(48), 24, 24, np.zeros((1, 2)), np.zeros((1, 2)), np.zeros(24),
+             ma=k)
