@@ -199,7 +199,10 @@ def main():
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no extras)")
     ap.add_argument("--variant", default=None, help="force a kernel variant (tuning)")
     ap.add_argument("--metric-variant", type=int, default=0,
-                    help="SURVEY 8(f) f3: bit 0 level-only trend, bit 1 detrended seasonal")
+                    help="SURVEY 8(f) f3: bit 0 level-only trend, bit 1 detrended seasonal, "
+                         "bit 2 component values")
+    ap.add_argument("--ma-kernel", type=int, default=0,
+                    help="SURVEY 8(f) f3: moving-average decomposition kernel (odd, 0 = off)")
     ap.add_argument("--instance-norm", action="store_true",
                     help="SURVEY 8(f) f1: RevIN-style instance normalisation")
     ap.add_argument("--sliding", action="store_true",
@@ -217,8 +220,9 @@ def main():
            "M": M, "series_per_step": B * w.C, "head": "per-channel",
            "l2": f"inputs larger than L2 ({B * w.C * w.L * 4 / 1e9:.2f} GB read per step)",
            "parallelism": f"dp{world}", "seed": args.seed}
-    if args.metric_variant or args.instance_norm:
-        cfg.update(metric_variant=args.metric_variant, instance_norm=bool(args.instance_norm))
+    if args.metric_variant or args.instance_norm or args.ma_kernel:
+        cfg.update(metric_variant=args.metric_variant, instance_norm=bool(args.instance_norm),
+                   ma_kernel=args.ma_kernel)
     if args.sliding:
         cfg.update(input="sliding windows of the [C][T] series (prnet_forward_sliding)",
                    l2=f"series span {w.C * (B + w.L - 1) * 4 / 1e6:.1f} MB (L2-resident); "
@@ -279,7 +283,7 @@ def main():
         del sd
     ws, wt, b = synth.make_params(w.C, M, N, w.H, True, args.seed, w.cfg_id)
     model = PRNet(w.C, w.L, w.S, w.H, device=dev, metric_variant=args.metric_variant,
-                  instance_norm=args.instance_norm).load(ws, wt, b)
+                  instance_norm=args.instance_norm, ma_kernel=args.ma_kernel).load(ws, wt, b)
     if args.variant:
         model.set_variant(args.variant)
     y = torch.empty((count, w.C, w.H), dtype=torch.float32, device="cuda")
@@ -412,7 +416,8 @@ def main():
             traffic = None
 
     cpu = None
-    if world == 1 and not args.no_cpu_baseline and not (args.metric_variant or args.instance_norm):
+    if world == 1 and not args.no_cpu_baseline and not (args.metric_variant or args.instance_norm
+                                                        or args.ma_kernel):
         try:
             wps, sps, cores, sample = cpu_oracle_rate(w.name, args.seed, args.cpu_budget)
             cpu = {"value": wps, "unit": "windows/s", "cores": cores, "kind": "oracle",

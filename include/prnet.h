@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define PRNET_ABI_VERSION 2
+#define PRNET_ABI_VERSION 3
 
 typedef struct prnet_handle prnet_handle; /* opaque; owned by the library */
 
@@ -43,8 +43,9 @@ typedef enum {
   PRNET_OK = 0,
   PRNET_ERR_INVALID_ARG = 1, /* NULL pointer with B > 0, C < 1, S < 2, L < S, H < 1,
                                 tau <= 0 or non-finite, wrong parameter counts, B < 0,
-                                size overflow, abi_version not 1 or 2, metric_variant
-                                outside [0, 7], instance_norm not 0/1                  */
+                                size overflow, abi_version not in [1, 3], metric_variant
+                                outside [0, 7], instance_norm not 0/1, ma_kernel not 0
+                                or odd in [1, 4095]                                     */
   PRNET_ERR_BAD_STATE = 2,   /* forward before load_params; NULL handle                  */
   PRNET_ERR_UNSUPPORTED = 3, /* device is not sm_100 (cc 10.x); x/y not 16-byte aligned;
                                 x and y overlap; pointer not on the handle's device;
@@ -57,7 +58,8 @@ typedef enum {
 } prnet_status;
 
 typedef struct {
-  int32_t abi_version;      /* PRNET_ABI_VERSION (2); 1 = the v1 layout (no fields past device) */
+  int32_t abi_version;      /* PRNET_ABI_VERSION (3); 1, 2 = the older layouts (ending at
+                               device / instance_norm)                                    */
   int32_t channels;         /* C >= 1                                                     */
   int32_t lookback;         /* L >= seg_len                                               */
   int32_t seg_len;          /* S >= 2 (A1: S is an input, e.g. the dominant period)      */
@@ -82,6 +84,13 @@ typedef struct {
                                segmented points (mean, population variance, eps 1e-5)
                                before the method and de-normalisation of the forecast
                                (R-f1); 0 = off                              */
+  /* ---- ABI 3 (abi_version 1 or 2 callers get 0 here) ---- */
+  int32_t ma_kernel;        /* 0 = off; odd k in [1, 4095] = moving-average
+                               decomposition of the segmented points (edge-replicated ends,
+                               after instance_norm): the seasonal branch (Def 3-4, 6, 9)
+                               runs on x - MA_k(x), the trend branch (Def 3-5, 7, 9) on
+                               MA_k(x) (R-f5).  N <= 32, M <= 32, S <= 128
+                               (mma_f16x3); other shapes: PRNET_ERR_UNSUPPORTED           */
 } prnet_config;
 
 /* Create a handle: validates cfg, checks the device is compute capability 10.x,

@@ -54,9 +54,10 @@ struct MmaOffsets {
   int wlo, wpack;                     // CTA-shared head
 };
 __host__ __device__ constexpr int r16(int v) { return (v + 15) & ~15; }
-// generic path, metric_variant bit 2: mu^, kappa^, A_s mu^, A_s kappa^, A_t mu^, A_t kappa^,
-// alpha, beta  [8][32] floats
-constexpr int kCompBytes = 8 * 32 * 4;
+// generic path, metric_variant bit 2: [10][32] floats: mu^_s, kappa^_s, A_s mu^_s,
+// A_s kappa^_s, A_t mu^_t, A_t kappa^_t, alpha, beta, mu^_t, kappa^_t (the _s and _t inputs
+// differ only under the moving-average decomposition)
+constexpr int kCompBytes = 10 * 32 * 4;
 __host__ __device__ constexpr MmaOffsets mma_offsets(int nr, int S, int sph, int zph, int mmt,
                                                      int extra = 0) {
   MmaOffsets o{};
@@ -79,7 +80,9 @@ __host__ __device__ constexpr MmaOffsets mma_offsets(int nr, int S, int sph, int
   return o;
 }
 
-template <int MT, int MMT, int SC, bool DBG, int NC = 0>
+// DEC: moving-average decomposition (ma_kernel, reading R-f5; generic path only): the
+// seasonal branch runs on x - MA(x), the trend branch on MA(x), the head on both
+template <int MT, int MMT, int SC, bool DBG, int NC = 0, bool DEC = false>
 __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_mma_kernel(FwdArgs a, MmaLayout ly,
                                                                int wins_per_cta) {
   extern __shared__ float4 smem4[];
@@ -129,7 +132,11 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
   float4* dsc = reinterpret_cast<float4*>(wb + (SC > 0 ? KO.misc : ly.off_diag));
   float* rsm = reinterpret_cast<float*>(dsc + 32);            // [96] x0, m1, kappa per row
   uint64_t* xbar = reinterpret_cast<uint64_t*>(rsm + 96);     // TMA completion barrier
-  float* cvec = rsm + 100;   // generic path, component values: [8][32] (kCompBytes)
+  float* cvec = rsm + 100;   // generic path, component values: [10][32] (kCompBytes)
+  // DEC: fp32 trend of the staged series, trend values X_t' as fp16 hi / lo
+  float* tbuf = DEC ? reinterpret_cast<float*>(wb + ly.off_tbuf) : nullptr;
+  __half* xt_hi = DEC ? reinterpret_cast<__half*>(wb + ly.off_xthi) : nullptr;
+  __half* xt_lo = DEC ? reinterpret_cast<__half*>(wb + ly.off_xtlo) : nullptr;
   if (lane == 0) mbar_init(xbar, 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   {
@@ -138,6 +145,11 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
     const int words = (int)(reinterpret_cast<unsigned char*>(dsc) -
                             reinterpret_cast<unsigned char*>(x_hi)) / 4;
     for (int k = lane; k < words; k += 32) p[k] = 0u;
+    if constexpr (DEC) {
+      uint32_t* pt = reinterpret_cast<uint32_t*>(xt_hi);
+      const int wt_ = (ly.per_warp_bytes - ly.off_xthi) / 4;
+      for (int k = lane; k < wt_; k += 32) pt[k] = 0u;
+    }
     // S = 24: fp32 staging rows >= N are never loaded and stay 0, so the descriptor phase
     // runs on all lanes without a branch (padding rows give zero X', Z' rows)
     if (SC == 24)
@@ -210,6 +222,8 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
     // generic path only: Def 5 pieces computed before pass 2, and the instance-norm map
     // (rr = 1, sr = 1, mr = 0 when off; the S = 24 instantiations never see the widening)
     float gen_mbar = 0.f, gen_var = 0.f, rr = 1.f, sr = 1.f, mr = 0.f;
+    // trend-branch level and slope (differ from mu, kap only under DEC)
+    float mu_t = 0.f, kap_t = 0.f;
     if constexpr (SC == 24) {
       // lane i holds its whole segment in registers: one read, 16-byte row stores
       float xv[24];
@@ -270,6 +284,97 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
           *reinterpret_cast<uint4*>(z_lo + i * 24 + 8 * q) = zl;
         }
         nu2 = q2.x + q2.y;
+      }
+      __syncwarp();
+    } else if constexpr (DEC) {
+      // ---- R-f5: trend = moving average of the N S segmented points with the ends
+      // repeated, lane-chunked running sums; seasonal = x - trend.  (RevIN commutes with the
+      // average: both components are mapped affinely below.)
+      {
+        const int hk = (a.ma_k - 1) >> 1;
+        const int cnk = (NS + 31) >> 5;
+        const int i0 = lane * cnk, i1 = min(i0 + cnk, NS);
+        if (i0 < i1) {
+          float sacc = 0.f;
+          for (int d = -hk; d <= hk; d++) sacc += xbuf[min(max(i0 + d, 0), NS - 1)];
+          tbuf[i0] = sacc * a.ma_inv;
+          for (int q = i0 + 1; q < i1; q++) {
+            sacc += xbuf[min(q + hk, NS - 1)] - xbuf[max(q - 1 - hk, 0)];
+            tbuf[q] = sacc * a.ma_inv;
+          }
+        }
+      }
+      __syncwarp();
+      float s1 = 0.f, s3 = 0.f, s1t = 0.f, s3t = 0.f, amx = 0.f, dmx = 0.f, nu2t = 0.f;
+      if (i < N) {
+        const float* xr = xbuf + i * S;
+        const float* tr = tbuf + i * S;
+        x0 = xr[0] - tr[0];
+        const float x0t = tr[0];
+        for (int t = 0; t < S; t++) {
+          const float vt = tr[t], vs = xr[t] - vt;
+          const float ds = vs - x0, dt = vt - x0t;
+          s1 += ds;
+          s3 = fmaf((float)t - a.half_s, ds, s3);
+          s1t += dt;
+          s3t = fmaf((float)t - a.half_s, dt, s3t);
+          amx = fmaxf(amx, fmaxf(fabsf(vs), fabsf(vt)));
+          dmx = fmaxf(dmx, fabsf(ds));
+        }
+        m1 = s1 * a.inv_s;
+        mu = x0 + m1;
+        kap = s3 * a.inv_v;
+        const float m1t = s1t * a.inv_s;
+        mu_t = x0t + m1t;
+        kap_t = s3t * a.inv_v;
+        const float kd = a.detrend ? kap : 0.f;
+        for (int t = 0; t < S; t++) {
+          const float vt = tr[t], vs = xr[t] - vt;
+          const float z = fmaf(-kd, (float)t - a.half_s, (vs - x0) - m1);
+          nu2 = fmaf(z, z, nu2);
+          const float zt = (vt - x0t) - m1t;
+          nu2t = fmaf(zt, zt, nu2t);
+        }
+      }
+      if (a.revin) {   // R-f1 statistics of the segmented points themselves
+        float sm = 0.f;
+        for (int k = lane; k < NS; k += 32) sm += xbuf[k];
+        mr = warp_sum(sm) * a.inv_ns;
+        float q = 0.f;
+        for (int k = lane; k < NS; k += 32) {
+          const float d = xbuf[k] - mr;
+          q = fmaf(d, d, q);
+        }
+        const float vr = warp_sum(q) * a.inv_ns;
+        rr = rsqrtf(vr + kEpsRevin);
+        sr = (vr + kEpsRevin) * rr;
+      }
+      // Def 5 on the trend branch's input
+      gen_mbar = warp_sum(i < N ? mu_t : 0.f) * a.inv_n;
+      gen_var = warp_sum(i < N ? nu2t + (float)S * (mu_t - gen_mbar) * (mu_t - gen_mbar) : 0.f) *
+                a.inv_ns;
+      sx = pow2_scale((warp_max_nonneg(amx) + fabsf(mr)) * rr);
+      sz = pow2_scale(warp_max_nonneg(2.f * dmx + (a.detrend ? fabsf(kap) * a.half_s : 0.f)));
+      rsm[lane] = x0;
+      rsm[32 + lane] = m1;
+      rsm[64 + lane] = a.detrend ? kap : 0.f;
+      __syncwarp();
+      const float xsc = rr * sx, xoff = -mr * rr * sx;
+      for (int k = lane; k < NS; k += 32) {
+        const int r = (int)(((float)k + 0.5f) * a.inv_s);
+        const int t = k - r * S;
+        const float tv = tbuf[k], vs = xbuf[k] - tv;
+        const float xr0 = rsm[r], mrow = rsm[32 + r], krow = rsm[64 + r];
+        __half h, l;
+        split1(vs * xsc, h, l);
+        x_hi[r * sph + t] = h;
+        x_lo[r * sph + t] = l;
+        split1(fmaf(tv, xsc, xoff), h, l);
+        xt_hi[r * sph + t] = h;
+        xt_lo[r * sph + t] = l;
+        split1(fmaf(-krow, (float)t - a.half_s, (vs - xr0) - mrow) * sz, h, l);
+        z_hi[r * zph + t] = h;
+        z_lo[r * zph + t] = l;
       }
       __syncwarp();
     } else {
@@ -342,6 +447,10 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
       }
       __syncwarp();
     }
+    if constexpr (!DEC) {
+      mu_t = mu;
+      kap_t = kap;
+    }
     // xbuf is free: fetch the next series while this one is in the tensor cores
     if (b + nwarps < b_end) prefetch(b + nwarps);
     // Def 5: sigma^2 = (1/(N S)) sum_n [nu2_n + S (mu_n - mubar)^2]
@@ -366,11 +475,13 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
       // z sz (unnormalised), so the column factor carries one rr and rk the other
       const float nh2 = nu2 * rr * rr;
       const float invh = rsqrtf(nh2 + kEpsSeasonal);
-      dsc[lane] = i < N ? make_float4((mu - mr) * cm, kap * ck, invh * rr, sqrtf(nh2) * invh)
+      dsc[lane] = i < N ? make_float4((mu_t - mr) * cm, kap_t * ck, invh * rr, sqrtf(nh2) * invh)
                         : make_float4(0.f, 0.f, 1.f, 0.f);
-      if (SC == 0 && a.comp) {   // the (normalised) segment level and slope, by column
-        cvec[lane] = i < N ? (mu - mr) * rr : 0.f;
+      if (SC == 0 && a.comp) {   // the (normalised) segment levels and slopes, by column
+        cvec[lane] = i < N ? (DEC ? mu : mu - mr) * rr : 0.f;
         cvec[32 + lane] = i < N ? kap * rr : 0.f;
+        cvec[256 + lane] = i < N ? (mu_t - mr) * rr : 0.f;
+        cvec[288 + lane] = i < N ? kap_t * rr : 0.f;
       }
       __syncwarp();
     }
@@ -378,13 +489,13 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
     // component values (generic path): row ii of A times mu^ and kappa^, reduced over the
     // quad's 4 lanes, into cvec[dst + ii], cvec[dst + 32 + ii]
     const bool comp = SC == 0 && a.comp;
-    auto comp_rows = [&](const float2 (&p)[2 * MT], int ii, int dst) {
+    auto comp_rows = [&](const float2 (&p)[2 * MT], int ii, int dst, int src) {
       float2 am = f2(0.f), ak = f2(0.f);
 #pragma unroll
       for (int nt = 0; nt < 2 * MT; nt++) {
         const int j = 8 * nt + 2 * cq;
-        am = fma2(p[nt], make_float2(cvec[j], cvec[j + 1]), am);
-        ak = fma2(p[nt], make_float2(cvec[32 + j], cvec[33 + j]), ak);
+        am = fma2(p[nt], make_float2(cvec[src + j], cvec[src + j + 1]), am);
+        ak = fma2(p[nt], make_float2(cvec[src + 32 + j], cvec[src + 33 + j]), ak);
       }
       float sm = am.x + am.y, sk = ak.x + ak.y;
       sm += __shfl_xor_sync(0xffffffffu, sm, 1);
@@ -398,12 +509,21 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
     };
 
     float qa[MMT][2 * MT][4];  // Q' = sw (W_s A_s + W_t A_t)   (component values: sw W_s A_s)
+    float qa2[DEC ? MMT : 1][2 * MT][4];   // DEC: Q_t' = sw W_t A_t (its own head operand)
 #pragma unroll
     for (int mm = 0; mm < MMT; mm++)
 #pragma unroll
       for (int nt = 0; nt < 2 * MT; nt++)
 #pragma unroll
         for (int e = 0; e < 4; e++) qa[mm][nt][e] = 0.f;
+    if constexpr (DEC) {
+#pragma unroll
+      for (int mm = 0; mm < MMT; mm++)
+#pragma unroll
+        for (int nt = 0; nt < 2 * MT; nt++)
+#pragma unroll
+          for (int e = 0; e < 4; e++) qa2[mm][nt][e] = 0.f;
+    }
 
     // ---------------- a4+a5 trend: exponent -Dhat_ij / tau_t (row max is 0 at j = i,
     // D_ii = 0) = -(mu~_i - mu~_j)^2 - (k~_i - k~_j)^2 with mu~ = mu sqrt(inv_var kt),
@@ -442,7 +562,7 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
             float2 pr[2 * MT];
 #pragma unroll
             for (int nt = 0; nt < 2 * MT; nt++) pr[nt] = mul2(u[nt], rs2);
-            comp_rows(pr, ii, 128);
+            comp_rows(pr, ii, 128, 256);
           }
 #pragma unroll
           for (int nt = 0; nt < 2 * MT; nt++) {
@@ -461,7 +581,10 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
             bl[nt][h] = movm_t(lo);
           }
         }
-        if (!comp) fold_tile(qa, NR, mt, bh, bl);
+        if (!comp) {
+          if constexpr (DEC) fold_tile(qa2, NR, mt, bh, bl);
+          else fold_tile(qa, NR, mt, bh, bl);
+        }
       }
     }
 
@@ -556,7 +679,7 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
             float2 pr[2 * MT];
 #pragma unroll
             for (int nt = 0; nt < 2 * MT; nt++) pr[nt] = mul2(u[nt], rs2);
-            comp_rows(pr, ii, 64);
+            comp_rows(pr, ii, 64, 0);
           }
 #pragma unroll
           for (int nt = 0; nt < 2 * MT; nt++) {
@@ -621,6 +744,16 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
         split2(qa[mm][2 * kj + 1][0], qa[mm][2 * kj + 1][1], qh[kj][2], ql[kj][2]);
         split2(qa[mm][2 * kj + 1][2], qa[mm][2 * kj + 1][3], qh[kj][3], ql[kj][3]);
       }
+      uint32_t qh2[DEC ? MT : 1][4], ql2[DEC ? MT : 1][4];   // DEC: Q_t' fragments
+      if constexpr (DEC) {
+#pragma unroll
+        for (int kj = 0; kj < MT; kj++) {
+          split2(qa2[mm][2 * kj][0], qa2[mm][2 * kj][1], qh2[kj][0], ql2[kj][0]);
+          split2(qa2[mm][2 * kj][2], qa2[mm][2 * kj][3], qh2[kj][1], ql2[kj][1]);
+          split2(qa2[mm][2 * kj + 1][0], qa2[mm][2 * kj + 1][1], qh2[kj][2], ql2[kj][2]);
+          split2(qa2[mm][2 * kj + 1][2], qa2[mm][2 * kj + 1][3], qh2[kj][3], ql2[kj][3]);
+        }
+      }
       for (int t0 = 0; t0 < ntt; t0 += 4) {
         float ya[4][4];
 #pragma unroll
@@ -652,6 +785,25 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
             if (two) mma16816(ya[2 * tp + 1], qh[kj], xl[2], xl[3]);
             mma16816(ya[2 * tp], qh[kj], xh[0], xh[1]);
             if (two) mma16816(ya[2 * tp + 1], qh[kj], xh[2], xh[3]);
+            if constexpr (DEC) {
+              if (!comp) {   // + Q_t' X_t'
+                if (two) {
+                  const int off = krow * sph + 8 * (nt0 + (q8 >> 1));
+                  ldsm_x4_t(xh, xt_hi + off);
+                  ldsm_x4_t(xl, xt_lo + off);
+                } else {
+                  const int off = krow * sph + 8 * nt0;
+                  ldsm_x2_t(xh[0], xh[1], xt_hi + off);
+                  ldsm_x2_t(xl[0], xl[1], xt_lo + off);
+                }
+                mma16816(ya[2 * tp], ql2[kj], xh[0], xh[1]);
+                if (two) mma16816(ya[2 * tp + 1], ql2[kj], xh[2], xh[3]);
+                mma16816(ya[2 * tp], qh2[kj], xl[0], xl[1]);
+                if (two) mma16816(ya[2 * tp + 1], qh2[kj], xl[2], xl[3]);
+                mma16816(ya[2 * tp], qh2[kj], xh[0], xh[1]);
+                if (two) mma16816(ya[2 * tp + 1], qh2[kj], xh[2], xh[3]);
+              }
+            }
           }
         }
         if (bstore) {
@@ -766,7 +918,8 @@ bool plan_mma_kernel(const FwdArgs& a, int max_smem_optin, MmaPlan* p) {
   p->mt = a.N <= 16 ? 1 : 2;
   p->mmt = a.M <= 16 ? 1 : 2;
   // the S = 24 instantiations implement the plain reading only (the widening runs generic)
-  p->sc = (a.S == 24 && !a.detrend && !a.revin && !a.comp) ? 24 : 0;
+  p->sc = (a.S == 24 && !a.detrend && !a.revin && !a.comp && a.ma_k == 0) ? 24 : 0;
+  p->dec = a.ma_k > 0;
   ly.nr = 16 * p->mt;
   if (p->sc == 24) {  // dense rows of 24 halves (48 B: 16-byte aligned, conflict-free ldmatrix)
     ly.sph = 24;
@@ -790,10 +943,19 @@ bool plan_mma_kernel(const FwdArgs& a, int max_smem_optin, MmaPlan* p) {
   ly.off_wlo = o.wlo;
   ly.wpack_bytes = o.wpack;
   ly.off_bias = -1;  // after the per-warp regions (depends on warps per CTA)
+  ly.off_tbuf = ly.off_xthi = ly.off_xtlo = -1;
+  if (p->dec) {   // trend staging and X_t' tiles after the misc region
+    ly.off_tbuf = ly.per_warp_bytes;
+    ly.off_xthi = r16(ly.off_tbuf + ly.nr * a.S * 4);
+    ly.off_xtlo = r16(ly.off_xthi + ly.nr * ly.sph * 2);
+    ly.per_warp_bytes = (r16(ly.off_xtlo + ly.nr * ly.sph * 2) + 127) & ~127;
+  }
   ly.shared_bytes = o.wpack;
   p->warps_per_cta = PRNET_MMA_THREADS / 32;
   const int hb = a.H > 16 * p->mmt * a.S ? a.H : 16 * p->mmt * a.S;  // zero-padded bias
-  auto total = [&](int w) { return (size_t)o.wpack + (size_t)w * o.pw + (size_t)hb * 4; };
+  auto total = [&](int w) {
+    return (size_t)o.wpack + (size_t)w * ly.per_warp_bytes + (size_t)hb * 4;
+  };
   while (total(p->warps_per_cta) > (size_t)max_smem_optin && p->warps_per_cta > 1)
     p->warps_per_cta >>= 1;
   p->smem_bytes = total(p->warps_per_cta);
@@ -803,9 +965,9 @@ bool plan_mma_kernel(const FwdArgs& a, int max_smem_optin, MmaPlan* p) {
   return true;
 }
 
-template <int MT, int MMT, int SC, bool DBG, int NC = 0>
+template <int MT, int MMT, int SC, bool DBG, int NC = 0, bool DEC = false>
 static cudaError_t launch_t(const FwdArgs& a, const MmaPlan& p, cudaStream_t st) {
-  auto k = prnet_fwd_mma_kernel<MT, MMT, SC, DBG, NC>;
+  auto k = prnet_fwd_mma_kernel<MT, MMT, SC, DBG, NC, DEC>;
   cudaError_t e =
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
@@ -814,11 +976,13 @@ static cudaError_t launch_t(const FwdArgs& a, const MmaPlan& p, cudaStream_t st)
   return cudaGetLastError();
 }
 
-template <int SC, bool DBG>
+template <int SC, bool DBG, bool DEC = false>
 static cudaError_t launch_sc(const FwdArgs& a, const MmaPlan& p, cudaStream_t st) {
   if (p.mt == 1)
-    return p.mmt == 1 ? launch_t<1, 1, SC, DBG>(a, p, st) : launch_t<1, 2, SC, DBG>(a, p, st);
-  return p.mmt == 1 ? launch_t<2, 1, SC, DBG>(a, p, st) : launch_t<2, 2, SC, DBG>(a, p, st);
+    return p.mmt == 1 ? launch_t<1, 1, SC, DBG, 0, DEC>(a, p, st)
+                      : launch_t<1, 2, SC, DBG, 0, DEC>(a, p, st);
+  return p.mmt == 1 ? launch_t<2, 1, SC, DBG, 0, DEC>(a, p, st)
+                    : launch_t<2, 2, SC, DBG, 0, DEC>(a, p, st);
 }
 
 cudaError_t launch_mma_kernel(const FwdArgs& a, const MmaPlan& p, cudaStream_t st) {
@@ -827,6 +991,7 @@ cudaError_t launch_mma_kernel(const FwdArgs& a, const MmaPlan& p, cudaStream_t s
     return p.mmt == 1 ? launch_t<2, 1, 24, false, 30>(a, p, st)
                       : launch_t<2, 2, 24, false, 30>(a, p, st);
   if (p.sc == 24) return dbg ? launch_sc<24, true>(a, p, st) : launch_sc<24, false>(a, p, st);
+  if (p.dec) return dbg ? launch_sc<0, true, true>(a, p, st) : launch_sc<0, false, true>(a, p, st);
   return dbg ? launch_sc<0, true>(a, p, st) : launch_sc<0, false>(a, p, st);
 }
 

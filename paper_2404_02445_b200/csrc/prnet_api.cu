@@ -104,6 +104,8 @@ prnet::FwdArgs make_args(const prnet_handle* h, const float* x, int64_t B, float
   a.detrend = (c.metric_variant >> 1) & 1;
   a.revin = c.instance_norm;
   a.comp = (c.metric_variant >> 2) & 1;
+  a.ma_k = c.ma_kernel;
+  a.ma_inv = c.ma_kernel > 0 ? 1.0f / (float)c.ma_kernel : 0.f;
   a.inv_s = (float)(1.0 / S);
   a.inv_n = (float)(1.0 / h->N);
   a.inv_ns = (float)(1.0 / ((double)h->N * S));
@@ -155,17 +157,20 @@ bool tcq_applicable(const prnet_handle* h) {
 // tc_quad, mma_f16x3 (N <= 32) and flash_f16x3 (16 < N <= 512, S <= 48); component values
 // (bit 2) in mma_f16x3.
 bool widening_on(const prnet_handle* h) {
-  return (h->cfg.metric_variant & 6) != 0 || h->cfg.instance_norm != 0;
+  return (h->cfg.metric_variant & 6) != 0 || h->cfg.instance_norm != 0 || h->cfg.ma_kernel > 0;
 }
-bool comp_on(const prnet_handle* h) { return (h->cfg.metric_variant & 4) != 0; }
+// component values and the moving-average decomposition: mma_f16x3's generic path only
+bool comp_on(const prnet_handle* h) {
+  return (h->cfg.metric_variant & 4) != 0 || h->cfg.ma_kernel > 0;
+}
 bool variant_supports_widening(const prnet_handle* h, int v) {
   if (comp_on(h)) return v == 2;
   return v == 2 || v == 5 || v == 6;
 }
 const char* kWideningMsg =
     "metric_variant bit 1 / instance_norm need tc_quad, mma_f16x3 (N <= 32) or flash_f16x3 "
-    "(16 < N <= 512, S <= 48, M <= 32); metric_variant bit 2 needs mma_f16x3 (N <= 32, "
-    "M <= 32, S <= 128)";
+    "(16 < N <= 512, S <= 48, M <= 32); metric_variant bit 2 and ma_kernel need mma_f16x3 "
+    "(N <= 32, M <= 32, S <= 128)";
 // 7 = small_f32 (N <= 16, S <= 128, M <= 32: lanes over time, FP32)
 bool small_applicable(const prnet_handle* h) {
   return h->N <= 16 && h->cfg.seg_len <= 128 && h->M <= 32;
@@ -301,12 +306,15 @@ extern "C" {
 prnet_status prnet_create(const prnet_config* cfg, prnet_handle** out) {
   if (out) *out = nullptr;
   if (!cfg || !out) return fail(nullptr, PRNET_ERR_INVALID_ARG, "NULL cfg or out");
-  if (cfg->abi_version != 1 && cfg->abi_version != PRNET_ABI_VERSION)
-    return fail(nullptr, PRNET_ERR_INVALID_ARG, "abi_version must be 1 or 2");
-  // a v1 caller's struct ends at `device`: copy only what it owns
+  if (cfg->abi_version < 1 || cfg->abi_version > PRNET_ABI_VERSION)
+    return fail(nullptr, PRNET_ERR_INVALID_ARG, "abi_version must be 1, 2 or 3");
+  // a v1 caller's struct ends at `device`, a v2 caller's at `instance_norm`: copy only what
+  // the caller owns
   prnet_config c2{};
   if (cfg->abi_version == 1)
     std::memcpy(&c2, cfg, offsetof(prnet_config, instance_norm));
+  else if (cfg->abi_version == 2)
+    std::memcpy(&c2, cfg, offsetof(prnet_config, ma_kernel));
   else
     c2 = *cfg;
   c2.abi_version = PRNET_ABI_VERSION;
@@ -322,6 +330,9 @@ prnet_status prnet_create(const prnet_config* cfg, prnet_handle** out) {
                 "bit 2 component values)");
   if (cfg->instance_norm != 0 && cfg->instance_norm != 1)
     return fail(nullptr, PRNET_ERR_INVALID_ARG, "instance_norm must be 0 or 1");
+  if (cfg->ma_kernel < 0 || cfg->ma_kernel > 4095 ||
+      (cfg->ma_kernel > 0 && (cfg->ma_kernel & 1) == 0))
+    return fail(nullptr, PRNET_ERR_INVALID_ARG, "ma_kernel must be 0 or odd in [1, 4095]");
   if (cfg->channels > 65535)
     return fail(nullptr, PRNET_ERR_UNSUPPORTED, "C > 65535 not supported");
   int ndev = 0;

@@ -15,7 +15,7 @@ import numpy as np
 _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libprnet.so")
 _lib = None
 
-PRNET_ABI_VERSION = 2
+PRNET_ABI_VERSION = 3
 STATUS = {0: "PRNET_OK", 1: "PRNET_ERR_INVALID_ARG", 2: "PRNET_ERR_BAD_STATE",
           3: "PRNET_ERR_UNSUPPORTED", 4: "PRNET_ERR_CUDA", 5: "PRNET_ERR_OOM"}
 
@@ -40,7 +40,8 @@ class PrnetConfig(ctypes.Structure):
                 ("horizon", ctypes.c_int32), ("head_per_channel", ctypes.c_int32),
                 ("metric_variant", ctypes.c_int32), ("tau_seasonal", ctypes.c_float),
                 ("tau_trend", ctypes.c_float), ("device", ctypes.c_int32),
-                ("instance_norm", ctypes.c_int32)]        # ABI 2
+                ("instance_norm", ctypes.c_int32),         # ABI 2
+                ("ma_kernel", ctypes.c_int32)]             # ABI 3
 
 
 def load_library(path: str | None = None):
@@ -89,14 +90,17 @@ class PRNet:
 
     def __init__(self, channels: int, lookback: int, seg_len: int, horizon: int,
                  head_per_channel: bool = True, tau_s: float = 1.0, tau_t: float = 1.0,
-                 device: int = 0, metric_variant: int = 0, instance_norm: bool = False):
+                 device: int = 0, metric_variant: int = 0, instance_norm: bool = False,
+                 ma_kernel: int = 0):
         """metric_variant: bit 0 level-only trend, bit 1 detrended seasonal metric, bit 2
         component values (reading R-f4);
-        instance_norm: RevIN-style normalisation (include/prnet.h)."""
+        instance_norm: RevIN-style normalisation;
+        ma_kernel: odd k > 0 = moving-average decomposition feeding each branch (R-f5)
+        (include/prnet.h)."""
         self._lib = load_library()
         cfg = PrnetConfig(PRNET_ABI_VERSION, channels, lookback, seg_len, horizon,
                           int(bool(head_per_channel)), int(metric_variant), tau_s, tau_t, device,
-                          int(bool(instance_norm)))
+                          int(bool(instance_norm)), int(ma_kernel))
         h = ctypes.c_void_p()
         st = self._lib.prnet_create(ctypes.byref(cfg), ctypes.byref(h))
         if st != 0:

@@ -64,12 +64,13 @@ def test_create_validates_before_touching_the_device(lib):
     from paper_2404_02445_b200 import PrnetConfig
     h = ctypes.c_void_p(123)
     for bad in [dict(seg_len=1), dict(lookback=10), dict(horizon=0), dict(channels=0),
-                dict(tau_seasonal=0.0), dict(tau_trend=float("nan")), dict(abi_version=3),
+                dict(tau_seasonal=0.0), dict(tau_trend=float("nan")), dict(abi_version=4),
                 dict(abi_version=0), dict(metric_variant=8), dict(metric_variant=-1),
-                dict(instance_norm=2)]:
-        kw = dict(abi_version=2, channels=7, lookback=96, seg_len=24, horizon=96,
+                dict(instance_norm=2), dict(ma_kernel=2), dict(ma_kernel=-1),
+                dict(ma_kernel=4097)]:
+        kw = dict(abi_version=3, channels=7, lookback=96, seg_len=24, horizon=96,
                   head_per_channel=1, metric_variant=0, tau_seasonal=1.0, tau_trend=1.0, device=0,
-                  instance_norm=0)
+                  instance_norm=0, ma_kernel=0)
         kw.update(bad)
         cfg = PrnetConfig(**kw)
         assert lib.prnet_create(ctypes.byref(cfg), ctypes.byref(h)) == 1, bad
@@ -94,6 +95,27 @@ def test_abi_v1_struct_still_accepted(lib):
                     ("tau_trend", ctypes.c_float), ("device", ctypes.c_int32)]
     h = ctypes.c_void_p(123)
     cfg = ConfigV1(1, 7, 96, 24, 96, 1, 0, 1.0, 1.0, 0)
+    from paper_2404_02445_b200 import PrnetConfig
+    assert lib.prnet_create(ctypes.cast(ctypes.pointer(cfg), ctypes.POINTER(PrnetConfig)),
+                            ctypes.byref(h)) == 3
+    assert h.value is None
+
+
+def test_abi_v2_struct_still_accepted(lib):
+    """An ABI-2 caller (struct ending at `instance_norm`) reaches the device check."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+
+    class ConfigV2(ctypes.Structure):
+        _fields_ = [("abi_version", ctypes.c_int32), ("channels", ctypes.c_int32),
+                    ("lookback", ctypes.c_int32), ("seg_len", ctypes.c_int32),
+                    ("horizon", ctypes.c_int32), ("head_per_channel", ctypes.c_int32),
+                    ("metric_variant", ctypes.c_int32), ("tau_seasonal", ctypes.c_float),
+                    ("tau_trend", ctypes.c_float), ("device", ctypes.c_int32),
+                    ("instance_norm", ctypes.c_int32)]
+    h = ctypes.c_void_p(123)
+    cfg = ConfigV2(2, 7, 96, 24, 96, 1, 0, 1.0, 1.0, 0, 1)
     from paper_2404_02445_b200 import PrnetConfig
     assert lib.prnet_create(ctypes.cast(ctypes.pointer(cfg), ctypes.POINTER(PrnetConfig)),
                             ctypes.byref(h)) == 3

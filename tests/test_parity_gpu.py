@@ -291,17 +291,18 @@ def test_abi_errors():
 
 
 # ------------------------------------------------------------ SURVEY §8(f) widening (f1, f3)
-def _check_widening(oracle_mod, x, S, H, mv, rev, variant=None, tau_s=1.0, tau_t=1.0, hpc=True):
+def _check_widening(oracle_mod, x, S, H, mv, rev, variant=None, tau_s=1.0, tau_t=1.0, hpc=True,
+                    ma=0):
     B, C, L = x.shape
     N, _, M = synth.derived_dims(L, S, H)
     ws, wt, b = synth.make_params(C, M, N, H, hpc, synth.DEFAULT_SEED, 0)
     m = PRNet(C, L, S, H, head_per_channel=hpc, tau_s=tau_s, tau_t=tau_t, metric_variant=mv,
-              instance_norm=rev).load(ws, wt, b)
+              instance_norm=rev, ma_kernel=ma).load(ws, wt, b)
     if variant is not None:
         m.set_variant(variant)
     y = m.forward(torch.from_numpy(x).cuda()).cpu().numpy()
     _, y64 = oracle_mod.forward(x, S, H, ws, wt, b, hpc, tau_s, tau_t, metric_variant=mv,
-                                instance_norm=rev)
+                                instance_norm=rev, ma_kernel=ma)
     scale = None
     if rev:   # the de-normalised forecast carries the input's level and scale
         scale = np.maximum(np.abs(x).max(axis=2, keepdims=True)[..., :1], 1.0)
@@ -370,6 +371,36 @@ def test_component_values_distributions(oracle_mod, kind, tau, hpc):
     x = synth.random_windows(3, 4, 720, kind=kind)
     _check_widening(oracle_mod, x, 24, 336, 6, kind == "scaled", tau_s=tau, tau_t=tau * 0.7,
                     hpc=hpc)
+
+
+@pytest.mark.parametrize("ma", [1, 3, 25, 101])
+@pytest.mark.parametrize("mv,rev", [(0, False), (3, False), (4, False), (7, False), (0, True),
+                                    (6, True)])
+@pytest.mark.parametrize("L,S,H", [(720, 24, 720), (720, 24, 96), (100, 24, 90), (97, 7, 13),
+                                   (270, 9, 31), (384, 128, 200)])
+def test_ma_decomposition_parity(oracle_mod, L, S, H, mv, rev, ma):
+    """ma_kernel (moving-average decomposition feeding each branch, reading R-f5)."""
+    x = synth.random_windows(2, 4, L, kind="mixed")
+    _check_widening(oracle_mod, x, S, H, mv, rev, ma=ma)
+
+
+@pytest.mark.parametrize("kind", ["normal", "constant", "scaled"])
+@pytest.mark.parametrize("tau,hpc", [(0.05, True), (1.0, False), (10.0, True)])
+def test_ma_decomposition_distributions(oracle_mod, kind, tau, hpc):
+    x = synth.random_windows(3, 4, 720, kind=kind)
+    _check_widening(oracle_mod, x, 24, 336, 0, kind == "scaled", tau_s=tau, tau_t=tau * 0.7,
+                    hpc=hpc, ma=25)
+
+
+def test_ma_decomposition_attention_dump():
+    """debug_attention on a decomposition handle dumps rows that sum to 1."""
+    m = PRNet(3, 720, 24, 96, ma_kernel=25)
+    ws, wt, b = synth.make_params(3, m.M, m.N, 96, True, synth.DEFAULT_SEED, 0)
+    m.load(ws, wt, b)
+    x = torch.from_numpy(synth.random_windows(2, 3, 720, kind="mixed")).cuda()
+    a_s, a_t = m.debug_attention(x)
+    for a in (a_s, a_t):
+        np.testing.assert_allclose(a.sum(-1).cpu().numpy(), 1.0, atol=1e-5)
 
 
 def test_component_values_unsupported_paths():
