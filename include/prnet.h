@@ -191,7 +191,7 @@ prnet_status prnet_error_sums(prnet_handle* h, const float* y, const float* targ
  *   4 = tc_full      Gram, fold and head on tcgen05 / TMEM, lane-per-row softmax
  *                    (S = 24, N <= 32, M <= 32)
  *   5 = flash_f16x3  one CTA per series, 16-key tiles streamed, mma.sync
- *                    split-fp16 (16 < N <= 512, S <= 48, M <= 32)  [auto: N > 32]
+ *                    split-fp16 (16 < N <= 512, S <= 96, M <= 32)  [auto: N > 32]
  *   6 = tc_quad      groups of 4 warps take quads of 4 series; Gram of the
  *                    row-normalised segments, fold and head on tcgen05 / TMEM,
  *                    lane-per-row softmaxes (S = 24, N <= 32, M <= 32,

@@ -95,6 +95,9 @@ void pack_flash_head(const float* ws, const float* wt, int Cw, int M, int N, uns
 
 // S <= 32 (KS <= 2): registers capped at 128 so two 8-warp (or four 4-warp) CTAs fit an SM
 // (A/B, stress L = 1440, S = 24: 1.84 vs 2.91 ms); S in (32, 48] would spill, keeps 1
+// NTT = t tiles of 8 per chunk: S <= 48 in one chunk; longer segments (S <= 96) in
+// ly.nch chunks of NTT tiles, the Gram and exponentials recomputed per chunk (the P, Y
+// accumulators of all of S would not fit the register file)
 template <int KS, int NTT, int MMT>
 __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel(FwdArgs a, FlashLayout ly,
                                                                  int wins_per_cta) {
@@ -229,6 +232,10 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
     }
     __syncthreads();
 
+    // (KS <= 3: one chunk, compile-time, so the loop and the offsets fold away)
+    const int nch = KS >= 4 ? ly.nch : 1;
+    for (int tc = 0; tc < nch; tc++) {
+    const int tb = KS >= 4 ? tc * NTT : 0;   // first t tile of this chunk
     // ---------------- a3..a7 per 16-row query tile
     float yacc[MMT][NTT][4];
 #pragma unroll
@@ -314,11 +321,11 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
           uint32_t xh[4], xl[4];
           const int krow = 16 * jt + (lane & 7) + 8 * (q8 & 1);
           if (2 * tp + 1 < NTT) {
-            const int off = krow * XP + 8 * (2 * tp + (q8 >> 1));
+            const int off = krow * XP + 8 * (tb + 2 * tp + (q8 >> 1));
             ldsm_x4_t(xh, x_hi + off);
             ldsm_x4_t(xl, x_lo + off);
           } else {
-            const int off = krow * XP + 8 * (2 * tp);
+            const int off = krow * XP + 8 * (tb + 2 * tp);
             ldsm_x2_t(xh[0], xh[1], x_hi + off);
             ldsm_x2_t(xl[0], xl[1], x_lo + off);
           }
@@ -396,7 +403,8 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
       const float* gb = a.bias + (int64_t)cw * H;
       float* yg = a.y + series * H;
       for (int h = tid; h < H; h += nthr) {
-        const int m = h / S, t = h - m * S;
+        const int m = h / S, t = h - m * S - 8 * tb;
+        if (t < 0 || t >= YR) continue;   // another chunk's columns
         float v = 0.f;
         for (int w = 0; w < nwarps; w++) v += yred[(w * (16 * MMT) + m) * YR + t];
         yg[h] = a.revin ? v * ysc + fmaf(__ldg(gb + h), sr, mu_r * (1.f - w1[m]))
@@ -404,21 +412,29 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
       }
       __syncthreads();
     }
+    }   // t chunks
   }
 }
 
 bool plan_flash_kernel(const FwdArgs& a, int max_smem_optin, FlashPlan* p) {
-  if (a.N <= 16 || a.N > 512 || a.M > 32 || a.S > 48) return false;
+  if (a.N <= 16 || a.N > 512 || a.M > 32 || a.S > 96) return false;
   FlashLayout& ly = p->ly;
   p->ks = (a.S + 15) / 16;
   p->ntt = (a.S + 7) / 8;
   if (p->ntt == 5) p->ntt = 6;
   if (p->ntt == 1) p->ntt = 2;
+  ly.nch = 1;
+  if (a.S > 48) {   // chunks of 4 (S <= 64) or 6 (S <= 96) t tiles
+    p->ks = a.S <= 64 ? 4 : 6;
+    ly.nch = 2;
+    p->ntt = (((a.S + 7) / 8) + 1) / 2;
+    p->ntt = p->ntt <= 4 ? 4 : 6;
+  }
   p->mmt = a.M <= 16 ? 1 : 2;
   ly.npad = flash_npad(a.N);
   auto odd8 = [](int v) { v = (v + 7) & ~7; if (((v / 8) & 1) == 0) v += 8; return v; };
   ly.zph = odd8(16 * p->ks);
-  ly.xph = odd8(8 * p->ntt);
+  ly.xph = odd8(8 * p->ntt * ly.nch);   // whole chunks (zero columns past S)
   int off = 0;   // (no fp32 staging of the series: the descriptor passes read global memory)
   ly.off_zhi = off;
   off += ly.npad * ly.zph * 2;
@@ -469,6 +485,8 @@ cudaError_t launch_flash_kernel(const FwdArgs& a, const FlashPlan& p, cudaStream
     case 23: return launch_flash_m<2, 3>(a, p, st);   // S in (16, 24]
     case 24: return launch_flash_m<2, 4>(a, p, st);   // S in (24, 32]
     case 36: return launch_flash_m<3, 6>(a, p, st);   // S in (32, 48]
+    case 44: return launch_flash_m<4, 4>(a, p, st);   // S in (48, 64], 2 chunks
+    case 66: return launch_flash_m<6, 6>(a, p, st);   // S in (64, 96], 2 chunks
     default: return cudaErrorInvalidValue;
   }
 }

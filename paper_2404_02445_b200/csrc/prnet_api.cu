@@ -139,9 +139,9 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
 bool tc_applicable(const prnet_handle* h) {
   return h->cfg.seg_len == 24 && h->N > 16 && h->N <= 32 && h->M <= 32;
 }
-// 5 = flash_f16x3 (16 < N <= 512, S <= 48, M <= 32: key-streaming mma.sync, long lookbacks)
+// 5 = flash_f16x3 (16 < N <= 512, S <= 96, M <= 32: key-streaming mma.sync, long lookbacks)
 bool flash_applicable(const prnet_handle* h) {
-  return h->N > 16 && h->N <= 512 && h->cfg.seg_len <= 48 && h->M <= 32;
+  return h->N > 16 && h->N <= 512 && h->cfg.seg_len <= 96 && h->M <= 32;
 }
 // 4 = tc_full (S = 24, N <= 32, M <= 32: Gram, fold and head on tcgen05 / TMEM)
 bool tc2_applicable(const prnet_handle* h) {
@@ -154,7 +154,7 @@ bool tcq_applicable(const prnet_handle* h) {
 }
 // Variants that implement the SURVEY §8(f) widening: the level-only trend runs in every
 // kernel (a.vtrend = 0); the detrended seasonal metric and instance normalisation in
-// tc_quad, mma_f16x3 (N <= 32) and flash_f16x3 (16 < N <= 512, S <= 48); component values
+// tc_quad, mma_f16x3 (N <= 32) and flash_f16x3 (16 < N <= 512, S <= 96); component values
 // (bit 2) in mma_f16x3.
 bool widening_on(const prnet_handle* h) {
   return (h->cfg.metric_variant & 6) != 0 || h->cfg.instance_norm != 0 || h->cfg.ma_kernel > 0;
@@ -169,7 +169,7 @@ bool variant_supports_widening(const prnet_handle* h, int v) {
 }
 const char* kWideningMsg =
     "metric_variant bit 1 / instance_norm need tc_quad, mma_f16x3 (N <= 32) or flash_f16x3 "
-    "(16 < N <= 512, S <= 48, M <= 32); metric_variant bit 2 and ma_kernel need mma_f16x3 "
+    "(16 < N <= 512, S <= 96, M <= 32); metric_variant bit 2 and ma_kernel need mma_f16x3 "
     "(N <= 32, M <= 32, S <= 128)";
 // 7 = small_f32 (N <= 16, S <= 128, M <= 32: lanes over time, FP32)
 bool small_applicable(const prnet_handle* h) {
@@ -707,7 +707,7 @@ prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {
     return fail(h, PRNET_ERR_UNSUPPORTED,
                 "tc_quad variant needs S = 24, N <= 32, M <= 32, tau_seasonal >= 1/80");
   if (variant == 5 && !flash_applicable(h))
-    return fail(h, PRNET_ERR_UNSUPPORTED, "flash variant needs 16 < N <= 512, S <= 48, M <= 32");
+    return fail(h, PRNET_ERR_UNSUPPORTED, "flash variant needs 16 < N <= 512, S <= 96, M <= 32");
   if (variant == 4 && !tc2_applicable(h))
     return fail(h, PRNET_ERR_UNSUPPORTED, "tc_full variant needs S = 24, N <= 32, M <= 32");
   if (variant == 3 && !tc_applicable(h))

@@ -41,7 +41,7 @@ def _applicable(variant, L, S, H):
     if variant == "small_f32":
         return N <= 16 and S <= 128 and M <= 32
     if variant == "flash_f16x3":
-        return 16 < N <= 512 and S <= 48 and M <= 32
+        return 16 < N <= 512 and S <= 96 and M <= 32
     return True
 
 
@@ -116,7 +116,7 @@ def test_stress_grid(oracle_mod, L, S):
     _check_small(oracle_mod, x, S, w.H)
 
 
-@pytest.mark.parametrize("L,S", [(5760, 12), (1440, 24), (720, 96)])
+@pytest.mark.parametrize("L,S", [(5760, 12), (1440, 24), (720, 96), (5760, 96)])
 def test_stress_full_size_sampled(oracle_mod, L, S):
     """Full 100k-series stress batch on the GPU, sampled series checked."""
     w = synth.WORKLOADS[f"stress_L{L}_S{S}_H96"]
@@ -138,7 +138,8 @@ def test_stress_full_size_sampled(oracle_mod, L, S):
     (64, 8, 64), (72, 8, 100), (128, 8, 64), (136, 8, 9), (256, 8, 40), (264, 8, 40),
     (270, 9, 31), (33, 2, 5), (66, 2, 7), (720, 24, 720), (722, 12, 721), (1000, 3, 17),
     (720, 24, 769), (720, 96, 96), (768, 24, 96), (767, 24, 700), (384, 128, 200),
-    (1440, 48, 96), (160, 5, 40)])
+    (1440, 48, 96), (160, 5, 40), (3840, 96, 96), (2000, 72, 150), (1700, 50, 120),
+    (1290, 64, 400)])
 @pytest.mark.parametrize("variant", VARIANTS)
 def test_shapes_ragged(oracle_mod, L, S, H, variant):
     """N from 1 to 333 across every kernel variant; L mod S != 0 (r > 0);
@@ -157,7 +158,8 @@ def test_temperatures_and_head_modes(oracle_mod, tau, hpc, variant):
 
 @pytest.mark.parametrize("tau", [0.05, 1.0, 10.0])
 @pytest.mark.parametrize("hpc", [True, False])
-@pytest.mark.parametrize("L,S,H", [(1440, 24, 96), (1536, 12, 200), (2880, 48, 96)])
+@pytest.mark.parametrize("L,S,H", [(1440, 24, 96), (1536, 12, 200), (2880, 48, 96),
+                                   (5760, 96, 96), (3200, 64, 700)])
 def test_long_lookback_temperatures_and_head_modes(oracle_mod, L, S, H, tau, hpc):
     """The long-N (flash) path under both head modes and several temperatures."""
     x = synth.random_windows(2, 3, L, kind="mixed")
@@ -348,7 +350,8 @@ def test_level_trend_every_variant(oracle_mod, variant):
 
 
 @pytest.mark.parametrize("mv,rev", [(2, False), (0, True), (3, True)])
-@pytest.mark.parametrize("L,S,H", [(1440, 24, 96), (1536, 12, 200), (2880, 48, 96)])
+@pytest.mark.parametrize("L,S,H", [(1440, 24, 96), (1536, 12, 200), (2880, 48, 96),
+                                   (3840, 96, 96), (3250, 65, 130)])
 def test_widening_parity_long_lookback(oracle_mod, L, S, H, mv, rev):
     """N > 32: the flash kernel implements the widening."""
     x = synth.random_windows(2, 3, L, kind="mixed")
@@ -418,10 +421,10 @@ def test_component_values_unsupported_paths():
 
 
 def test_widening_unsupported_paths():
-    m = PRNet(3, 3840, 96, 96, metric_variant=2)        # N = 40, S = 96: no kernel for bit 1
+    m = PRNet(3, 3000, 150, 96, metric_variant=2)       # N = 20, S = 150: no kernel for bit 1
     m.load(np.zeros((3, m.M, m.N)), np.zeros((3, m.M, m.N)), np.zeros((3, 96)))
     with pytest.raises(PrnetError) as e:
-        m.forward(torch.zeros((2, 3, 3840), device="cuda"))
+        m.forward(torch.zeros((2, 3, 3000), device="cuda"))
     assert e.value.status == 3
     m2 = PRNet(3, 720, 24, 96, instance_norm=True)
     with pytest.raises(PrnetError) as e:
