@@ -390,7 +390,12 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
           amx = fmaxf(amx, fabsf(v));
           dmx = fmaxf(dmx, fabsf(d));
         };
-        if ((S & 3) == 0) {
+        // rows are S floats apart: for S a multiple of 8 the lanes share banks (8-way at
+        // S = 24, 32-way at S = 96), so lane i walks its row from column (i mod S) on,
+        // wrapping, which spreads the lanes over the banks (A/B: S = 48 1.20 -> 1.00 ms,
+        // S = 96 3.30 -> 2.41 ms; at S = 12 the wrap bookkeeping measured slower)
+        const bool rot = (S & 7) == 0 && S >= 24;
+        if ((S & 3) == 0 && !rot) {
           for (int t = 0; t < S; t += 4) {
             const float4 v = *reinterpret_cast<const float4*>(xr + t);
             acc1(v.x, t);
@@ -398,8 +403,25 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
             acc1(v.z, t + 2);
             acc1(v.w, t + 3);
           }
-        } else {
+        } else if ((S & 3) == 0) {
+          const int S4 = S >> 2;
+          int tq = i % S4;
+          for (int q = 0; q < S4; q++) {
+            const float4 v = *reinterpret_cast<const float4*>(xr + 4 * tq);
+            acc1(v.x, 4 * tq);
+            acc1(v.y, 4 * tq + 1);
+            acc1(v.z, 4 * tq + 2);
+            acc1(v.w, 4 * tq + 3);
+            if (++tq == S4) tq = 0;
+          }
+        } else if (!rot) {
           for (int t = 0; t < S; t++) acc1(xr[t], t);
+        } else {
+          int t = i % S;
+          for (int q = 0; q < S; q++) {
+            acc1(xr[t], t);
+            if (++t == S) t = 0;
+          }
         }
         m1 = s1 * a.inv_s;
         mu = x0 + m1;
@@ -407,9 +429,18 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
         // nu2: |z|^2, or with metric_variant bit 1 the residual |e|^2, e = z - kappa t~
         // (SURVEY §8(f) f3); Def 5 below uses |z|^2 = |e|^2 + kappa^2 V
         const float kd = a.detrend ? kap : 0.f;
-        for (int t = 0; t < S; t++) {
-          const float z = fmaf(-kd, (float)t - a.half_s, (xr[t] - x0) - m1);
-          nu2 = fmaf(z, z, nu2);
+        if (rot) {
+          int t = i % S;
+          for (int q = 0; q < S; q++) {
+            const float z = fmaf(-kd, (float)t - a.half_s, (xr[t] - x0) - m1);
+            nu2 = fmaf(z, z, nu2);
+            if (++t == S) t = 0;
+          }
+        } else {
+          for (int t = 0; t < S; t++) {
+            const float z = fmaf(-kd, (float)t - a.half_s, (xr[t] - x0) - m1);
+            nu2 = fmaf(z, z, nu2);
+          }
         }
       }
       // sigma^2 (Def 5) and, with instance_norm (f1, R-f1), the RevIN map xhat = (x - mu_r) rr
