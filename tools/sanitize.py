@@ -17,6 +17,11 @@ CASES = [  # (L, S, H, variants)
     (97, 7, 13, ["mma_f16x3", "warp_f32", "long_f32"]),
     (1440, 24, 96, ["flash_f16x3", "long_f32"]),
     (1440, 12, 100, ["flash_f16x3"]),
+    (96, 24, 96, ["small_f32"]),
+    (192, 12, 96, ["small_f32", "mma_f16x3"]),
+    (1440, 96, 96, ["small_f32", "mma_f16x3"]),
+    (3840, 96, 96, ["flash_f16x3"]),
+    (1290, 64, 400, ["flash_f16x3"]),
 ]
 for L, S, H, variants in CASES:
     x = torch.from_numpy(synth.random_windows(5, 3, L)).cuda()
@@ -37,6 +42,18 @@ for L, S, H, mv, rev in [(720, 24, 720, 3, True), (97, 7, 13, 2, True), (1440, 2
     torch.cuda.synchronize()
     assert torch.isfinite(y).all(), (L, S, H, mv, rev)
     print("ok widening", L, S, H, mv, rev, flush=True)
+# component values and the moving-average decomposition (generic mma_f16x3)
+for L, S, H, mv, rev, ma in [(720, 24, 336, 4, False, 0), (720, 24, 336, 7, True, 0),
+                             (720, 24, 336, 0, False, 25), (97, 7, 13, 6, True, 3),
+                             (384, 128, 200, 7, True, 9)]:
+    x = torch.from_numpy(synth.random_windows(5, 3, L)).cuda()
+    N, _, M = synth.derived_dims(L, S, H)
+    ws, wt, b = synth.make_params(3, M, N, H)
+    y = PRNet(3, L, S, H, metric_variant=mv, instance_norm=rev, ma_kernel=ma).load(
+        ws, wt, b).forward(x)
+    torch.cuda.synchronize()
+    assert torch.isfinite(y).all(), (L, S, H, mv, rev, ma)
+    print("ok component/decomposition", L, S, H, mv, rev, ma, flush=True)
 for L, S, H, t0 in [(720, 24, 720, 1), (720, 24, 96, 0), (97, 7, 13, 3)]:
     T = t0 + 7 - 1 + L
     ser = torch.from_numpy(synth.random_windows(1, 3, T)[0]).cuda()
