@@ -82,14 +82,16 @@ __host__ __device__ constexpr MmaOffsets mma_offsets(int nr, int S, int sph, int
 
 // DEC: moving-average decomposition (ma_kernel, reading R-f5; generic path only): the
 // seasonal branch runs on x - MA(x), the trend branch on MA(x), the head on both
-template <int MT, int MMT, int SC, bool DBG, int NC = 0, bool DEC = false>
+// COMP: the S = 24 instantiation with component values (the generic one has them at run time)
+template <int MT, int MMT, int SC, bool DBG, int NC = 0, bool DEC = false, bool COMP = false>
 __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_mma_kernel(FwdArgs a, MmaLayout ly,
                                                                int wins_per_cta) {
   extern __shared__ float4 smem4[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(smem4);
   constexpr int NR = 16 * MT;
   constexpr int WPH = 2 * NR + 8;
-  constexpr MmaOffsets KO = mma_offsets(NR, SC > 0 ? SC : 8, SC > 0 ? SC : 8, SC > 0 ? SC : 8, MMT);
+  constexpr MmaOffsets KO =
+      mma_offsets(NR, SC > 0 ? SC : 8, SC > 0 ? SC : 8, SC > 0 ? SC : 8, MMT, COMP ? kCompBytes : 0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int gq = lane >> 2, cq = lane & 3, q8 = lane >> 3;
   const int c = blockIdx.y;
@@ -508,7 +510,7 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
       const float invh = rsqrtf(nh2 + kEpsSeasonal);
       dsc[lane] = i < N ? make_float4((mu_t - mr) * cm, kap_t * ck, invh * rr, sqrtf(nh2) * invh)
                         : make_float4(0.f, 0.f, 1.f, 0.f);
-      if (SC == 0 && a.comp) {   // the (normalised) segment levels and slopes, by column
+      if ((SC == 0 || COMP) && a.comp) {   // the (normalised) segment levels and slopes
         cvec[lane] = i < N ? (DEC ? mu : mu - mr) * rr : 0.f;
         cvec[32 + lane] = i < N ? kap * rr : 0.f;
         cvec[256 + lane] = i < N ? (mu_t - mr) * rr : 0.f;
@@ -519,7 +521,7 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
 
     // component values (generic path): row ii of A times mu^ and kappa^, reduced over the
     // quad's 4 lanes, into cvec[dst + ii], cvec[dst + 32 + ii]
-    const bool comp = SC == 0 && a.comp;
+    const bool comp = (SC == 0 || COMP) && a.comp != 0;
     auto comp_rows = [&](const float2 (&p)[2 * MT], int ii, int dst, int src) {
       float2 am = f2(0.f), ak = f2(0.f);
 #pragma unroll
@@ -846,8 +848,13 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
             for (int h = 0; h < 2; h++) {
               const int hh = (16 * mm + 8 * h + gq) * SC + 8 * (t0 + nt) + 2 * cq;
               const float2 v = mul2(make_float2(ya[nt][2 * h], ya[nt][2 * h + 1]), ys2);
-              *reinterpret_cast<float2*>(ystage + hh) =
-                  add2(v, *reinterpret_cast<const float2*>(bS + hh));
+              float2 bb = *reinterpret_cast<const float2*>(bS + hh);
+              if (comp) {   // + alpha_m + beta_m t~ (component values)
+                const int m = 16 * mm + 8 * h + gq;
+                const float t = (float)(8 * (t0 + nt) + 2 * cq) - a.half_s;
+                bb = add2(bb, fma2(f2(cvec[224 + m]), make_float2(t, t + 1.f), f2(cvec[192 + m])));
+              }
+              *reinterpret_cast<float2*>(ystage + hh) = add2(v, bb);
             }
           }
           continue;
@@ -949,7 +956,7 @@ bool plan_mma_kernel(const FwdArgs& a, int max_smem_optin, MmaPlan* p) {
   p->mt = a.N <= 16 ? 1 : 2;
   p->mmt = a.M <= 16 ? 1 : 2;
   // the S = 24 instantiations implement the plain reading only (the widening runs generic)
-  p->sc = (a.S == 24 && !a.detrend && !a.revin && !a.comp && a.ma_k == 0) ? 24 : 0;
+  p->sc = (a.S == 24 && !a.detrend && !a.revin && a.ma_k == 0) ? 24 : 0;
   p->dec = a.ma_k > 0;
   ly.nr = 16 * p->mt;
   if (p->sc == 24) {  // dense rows of 24 halves (48 B: 16-byte aligned, conflict-free ldmatrix)
@@ -963,7 +970,8 @@ bool plan_mma_kernel(const FwdArgs& a, int max_smem_optin, MmaPlan* p) {
   }
   ly.wph = 2 * ly.nr + 8;
   ly.ntt = (a.S + 7) / 8;
-  const MmaOffsets o = mma_offsets(ly.nr, a.S, ly.sph, ly.zph, p->mmt, p->sc == 0 ? kCompBytes : 0);
+  const MmaOffsets o =
+      mma_offsets(ly.nr, a.S, ly.sph, ly.zph, p->mmt, (p->sc == 0 || a.comp) ? kCompBytes : 0);
   ly.xbuf_f = ly.nr * a.S;
   ly.off_xhi = o.xhi;
   ly.off_xlo = o.xlo;
@@ -996,9 +1004,9 @@ bool plan_mma_kernel(const FwdArgs& a, int max_smem_optin, MmaPlan* p) {
   return true;
 }
 
-template <int MT, int MMT, int SC, bool DBG, int NC = 0, bool DEC = false>
+template <int MT, int MMT, int SC, bool DBG, int NC = 0, bool DEC = false, bool COMP = false>
 static cudaError_t launch_t(const FwdArgs& a, const MmaPlan& p, cudaStream_t st) {
-  auto k = prnet_fwd_mma_kernel<MT, MMT, SC, DBG, NC, DEC>;
+  auto k = prnet_fwd_mma_kernel<MT, MMT, SC, DBG, NC, DEC, COMP>;
   cudaError_t e =
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
@@ -1007,17 +1015,20 @@ static cudaError_t launch_t(const FwdArgs& a, const MmaPlan& p, cudaStream_t st)
   return cudaGetLastError();
 }
 
-template <int SC, bool DBG, bool DEC = false>
+template <int SC, bool DBG, bool DEC = false, bool COMP = false>
 static cudaError_t launch_sc(const FwdArgs& a, const MmaPlan& p, cudaStream_t st) {
   if (p.mt == 1)
-    return p.mmt == 1 ? launch_t<1, 1, SC, DBG, 0, DEC>(a, p, st)
-                      : launch_t<1, 2, SC, DBG, 0, DEC>(a, p, st);
-  return p.mmt == 1 ? launch_t<2, 1, SC, DBG, 0, DEC>(a, p, st)
-                    : launch_t<2, 2, SC, DBG, 0, DEC>(a, p, st);
+    return p.mmt == 1 ? launch_t<1, 1, SC, DBG, 0, DEC, COMP>(a, p, st)
+                      : launch_t<1, 2, SC, DBG, 0, DEC, COMP>(a, p, st);
+  return p.mmt == 1 ? launch_t<2, 1, SC, DBG, 0, DEC, COMP>(a, p, st)
+                    : launch_t<2, 2, SC, DBG, 0, DEC, COMP>(a, p, st);
 }
 
 cudaError_t launch_mma_kernel(const FwdArgs& a, const MmaPlan& p, cudaStream_t st) {
   const bool dbg = a.a_s_dbg != nullptr;
+  if (p.sc == 24 && a.comp && !dbg)   // component values at S = 24 (the attention dump
+    // does not depend on them: it runs the plain debug instantiation)
+    return launch_sc<24, false, false, true>(a, p, st);
   if (p.sc == 24 && a.N == 30 && !dbg)   // L = 720, S = 24: configs[1..3], plain reading
     return p.mmt == 1 ? launch_t<2, 1, 24, false, 30>(a, p, st)
                       : launch_t<2, 2, 24, false, 30>(a, p, st);
