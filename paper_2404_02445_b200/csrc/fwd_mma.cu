@@ -313,7 +313,10 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
         const float* tr = tbuf + i * S;
         x0 = xr[0] - tr[0];
         const float x0t = tr[0];
-        for (int t = 0; t < S; t++) {
+        // lane-rotated row walks (bank conflicts for S a multiple of 8, as in the plain path)
+        const int t_start = ((S & 7) == 0 && S >= 24) ? i % S : 0;
+        int t = t_start;
+        for (int q = 0; q < S; q++, t = (t + 1 == S) ? 0 : t + 1) {
           const float vt = tr[t], vs = xr[t] - vt;
           const float ds = vs - x0, dt = vt - x0t;
           s1 += ds;
@@ -330,7 +333,8 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
         mu_t = x0t + m1t;
         kap_t = s3t * a.inv_v;
         const float kd = a.detrend ? kap : 0.f;
-        for (int t = 0; t < S; t++) {
+        t = t_start;
+        for (int q = 0; q < S; q++, t = (t + 1 == S) ? 0 : t + 1) {
           const float vt = tr[t], vs = xr[t] - vt;
           const float z = fmaf(-kd, (float)t - a.half_s, (vs - x0) - m1);
           nu2 = fmaf(z, z, nu2);
