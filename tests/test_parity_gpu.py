@@ -462,6 +462,24 @@ def test_sliding_equals_materialised_windows(L, S, H, t0, variant):
     assert torch.equal(y_sl, y_win)
 
 
+@pytest.mark.parametrize("t0", [0, 1, 3])
+@pytest.mark.parametrize("L,S,H,mv,rev,ma", [(720, 24, 336, 3, True, 0), (720, 24, 336, 4, False, 0),
+                                             (720, 24, 96, 7, True, 25), (97, 7, 13, 6, False, 3),
+                                             (1440, 24, 96, 2, True, 0)])
+def test_sliding_widening_equals_materialised(L, S, H, mv, rev, ma, t0):
+    """The sliding mode under every widening flag (f1, f3) is bitwise the materialised
+    forward (the generic paths load unaligned windows element-wise)."""
+    C, B = 4, 9
+    T = t0 + B - 1 + L + 2
+    s, x = _series_and_windows(C, T, L, t0, B, seed=11)
+    N, _, M = synth.derived_dims(L, S, H)
+    ws, wt, b = synth.make_params(C, M, N, H, True, synth.DEFAULT_SEED, 0)
+    m = PRNet(C, L, S, H, metric_variant=mv, instance_norm=rev, ma_kernel=ma).load(ws, wt, b)
+    y_win = m.forward(torch.from_numpy(x).cuda())
+    y_sl = m.forward_sliding(torch.from_numpy(s).cuda(), t0, B)
+    assert torch.equal(y_sl, y_win)
+
+
 @pytest.mark.parametrize("t0", [0, 3])
 def test_sliding_window_at_the_end_of_the_series(oracle_mod, t0):
     """The last window ends exactly at T (the aligned-superset load must not run past the
