@@ -77,6 +77,12 @@ def _load():
                                           ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
                                           ctypes.c_int32, _f32p, _f64p]
         lib.oracle_forward_ex.restype = ctypes.c_int
+        lib.oracle_backward_head_ex.argtypes = [
+            _f32p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+            ctypes.c_int32, _f32p, _f32p, _f32p, ctypes.c_int32, ctypes.c_double,
+            ctypes.c_double, ctypes.c_int32, ctypes.c_int32, ctypes.c_double, ctypes.c_int32,
+            _f32p, _f64p, _f64p, _f64p]
+        lib.oracle_backward_head_ex.restype = ctypes.c_int
         lib.oracle_error_sums.argtypes = [_f32p, _f32p, ctypes.c_int64, _f64p]
         lib.oracle_error_sums.restype = None
         _lib = lib
@@ -143,6 +149,29 @@ def forward(x, S, H, ws, wt, bias, head_per_channel=True, tau_s=1.0, tau_t=1.0,
                                  y64) != 0:
         raise ValueError("oracle_forward rejected its arguments")
     return y, y64
+
+
+def backward_head(x, S, H, ws, wt, bias, dy, head_per_channel=True, tau_s=1.0, tau_t=1.0,
+                  metric_variant=0, instance_norm=False, eps_r=EPS_REVIN, ma_kernel=0):
+    """Gradients (dws, dwt, db), fp64, of sum(dy * y) with respect to the head (SURVEY §8(f)
+    f4, reading R-f6); x, dy [B, C, L] / [B, C, H] fp32."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    B, C, L = x.shape
+    N, r, M = dims(L, S, H)
+    Cw = C if head_per_channel else 1
+    ws = np.ascontiguousarray(ws, dtype=np.float32).reshape(Cw, M, N)
+    wt = np.ascontiguousarray(wt, dtype=np.float32).reshape(Cw, M, N)
+    bias = np.ascontiguousarray(bias, dtype=np.float32).reshape(Cw, H)
+    dy = np.ascontiguousarray(dy, dtype=np.float32).reshape(B, C, H)
+    dws = np.zeros((Cw, M, N))
+    dwt = np.zeros((Cw, M, N))
+    db = np.zeros((Cw, H))
+    if _load().oracle_backward_head_ex(x, B, C, L, S, H, ws, wt, bias,
+                                       int(bool(head_per_channel)), float(tau_s), float(tau_t),
+                                       int(metric_variant), int(bool(instance_norm)),
+                                       float(eps_r), int(ma_kernel), dy, dws, dwt, db) != 0:
+        raise ValueError("oracle_backward_head rejected its arguments")
+    return dws, dwt, db
 
 
 def error_sums(y, target):

@@ -376,3 +376,69 @@ void oracle_error_sums(const float* y, const float* target, int64_t n, double* o
   out3[1] = sae;
   out3[2] = (double)n;
 }
+
+/* SURVEY §8(f) f4, the backward pass of the head (reading R-f6 in DESIGN.md §3): for an
+ * upstream gradient dy = dL/dy of one series, with y[h] = (Y[h div S][h mod S] + b[h]) s_r
+ * + mu_r (s_r = 1, mu_r = 0 without instance_norm) and Def 10
+ * Y[m][t] = sum_n ws[m][n] P_s[n][t] + wt[m][n] P_t[n][t]:
+ *   dY[m][t] = dy[m S + t] s_r  (0 for m S + t >= H),
+ *   dws[m][n] += sum_t dY[m][t] P_s[n][t],   dwt[m][n] += sum_t dY[m][t] P_t[n][t],
+ *   db[h] += dy[h] s_r.
+ * The patterns P_s, P_t come from oracle_series_ex (Def 2-9 with every widening flag). */
+int oracle_backward_head_ex(const float* x, int64_t B, int32_t C, int32_t L, int32_t S,
+                            int32_t H, const float* ws, const float* wt, const float* bias,
+                            int32_t head_per_channel, double tau_s, double tau_t,
+                            int32_t metric_variant, int32_t instance_norm, double eps_r,
+                            int32_t ma_kernel, const float* dy, double* dws, double* dwt,
+                            double* db) {
+  int32_t N, r, M;
+  if (B < 0 || C < 1 || oracle_dims(L, S, H, &N, &r, &M) != 0) return -1;
+  int32_t Cw = head_per_channel ? C : 1;
+  memset(dws, 0, (size_t)Cw * M * N * sizeof(double));
+  memset(dwt, 0, (size_t)Cw * M * N * sizeof(double));
+  memset(db, 0, (size_t)Cw * H * sizeof(double));
+  size_t nS = (size_t)N * S;
+  double* Ps = (double*)malloc(nS * sizeof(double));
+  double* Pt = (double*)malloc(nS * sizeof(double));
+  double* X = (double*)malloc(nS * sizeof(double));
+  double* yy = (double*)malloc((size_t)H * sizeof(double));
+  int rc = 0;
+  for (int64_t b = 0; b < B && rc == 0; b++)
+    for (int32_t c = 0; c < C; c++) {
+      int64_t cw = head_per_channel ? c : 0;
+      const float* xs = x + (b * C + c) * (int64_t)L;
+      oracle_debug dbg;
+      memset(&dbg, 0, sizeof(dbg));
+      dbg.p_s = Ps;
+      dbg.p_t = Pt;
+      if (oracle_series_ex(xs, L, S, H, ws + cw * M * N, wt + cw * M * N, bias + cw * H,
+                           tau_s, tau_t, metric_variant, instance_norm, eps_r, ma_kernel, yy,
+                           &dbg) != 0) {
+        rc = -1;
+        break;
+      }
+      double s_r = 1.0;
+      if (instance_norm) {                                         /* f1 scale */
+        double mu_r, var_r;
+        oracle_segment(xs, N, S, r, X);
+        oracle_instance_stats(X, N, S, &mu_r, &var_r);
+        s_r = sqrt(var_r + eps_r);
+      }
+      const float* g = dy + (b * C + c) * (int64_t)H;
+      for (int32_t m = 0; m < M; m++)
+        for (int32_t n = 0; n < N; n++) {
+          double as = 0.0, at = 0.0;
+          for (int32_t t = 0; t < S; t++) {
+            int32_t h = m * S + t;
+            double dY = h < H ? (double)g[h] * s_r : 0.0;
+            as += dY * Ps[n * S + t];
+            at += dY * Pt[n * S + t];
+          }
+          dws[(cw * M + m) * N + n] += as;
+          dwt[(cw * M + m) * N + n] += at;
+        }
+      for (int32_t h = 0; h < H; h++) db[cw * H + h] += (double)g[h] * s_r;
+    }
+  free(Ps); free(Pt); free(X); free(yy);
+  return rc;
+}

@@ -98,6 +98,17 @@ int oracle_forward_ex(const float* x, int64_t B, int32_t C, int32_t L, int32_t S
                       int32_t metric_variant, int32_t instance_norm, double eps_r,
                       int32_t ma_kernel, float* y, double* y64);
 
+/* SURVEY §8(f) f4 (reading R-f6): gradients of L = sum dy * y with respect to the head
+ * (ws, wt: [Cw][M][N]; bias: [Cw][H]) for the upstream gradient dy [B][C][H], summed over
+ * the batch (and over the channels when head_per_channel = 0).  Outputs are fp64 and
+ * overwritten.  Returns 0 or -1. */
+int oracle_backward_head_ex(const float* x, int64_t B, int32_t C, int32_t L, int32_t S,
+                            int32_t H, const float* ws, const float* wt, const float* bias,
+                            int32_t head_per_channel, double tau_s, double tau_t,
+                            int32_t metric_variant, int32_t instance_norm, double eps_r,
+                            int32_t ma_kernel, const float* dy, double* dws, double* dwt,
+                            double* db);
+
 /* Sum of squared and absolute errors of y against target (n values), fp64,
  * in index order: out[0] = SSE, out[1] = SAE, out[2] = n.  (Bench metric,
  * PAPER.md:22 "accuracy"; MSE = SSE/n, MAE = SAE/n.) */
