@@ -179,6 +179,25 @@ prnet_status prnet_debug_attention(prnet_handle* h, const float* x, int64_t batc
 prnet_status prnet_error_sums(prnet_handle* h, const float* y, const float* target,
                               int64_t batch, double* out3, void* cuda_stream);
 
+/* Backward pass of the head (DESIGN.md §3 reading R-f6): the gradients of
+ * L = sum(dy * y) with respect to w_seasonal, w_trend and bias, for the forward of x:
+ *   dws[cw][m][n] = sum_{b, c -> cw, t} dY[m][t] P_s[n][t],  dwt likewise with P_t,
+ *   db[cw][h] = sum_{b, c -> cw} dy[b][c][h] s_r,   dY[m][t] = dy[b][c][m S + t] s_r,
+ * where P_s, P_t are the series' patterns (Def 9, after instance normalisation when on),
+ * s_r the instance-normalisation scale (1 when off), and c -> cw the head of channel c
+ * (all channels -> 0 for a shared head).  The gradients do not depend on the loaded head, so
+ * prnet_load_params is not required.
+ *   x   device [B][C][L] fp32 (as prnet_forward);  dy  device [B][C][H] fp32
+ *   dws, dwt  device [Cw][M][N] fp32, db device [Cw][H] fp32: overwritten (B = 0 -> zeros)
+ * FP32 recomputation of the attention, fixed-order reductions (fp64 across CTAs): the result
+ * is deterministic.  Uses a per-handle device workspace (grown on demand, which synchronises
+ * the stream once).  Errors: INVALID_ARG (B < 0, NULL pointers), UNSUPPORTED (N, M > 32,
+ * S > 128, metric_variant bit 2, ma_kernel > 0, pointers not on the handle's device), CUDA,
+ * OOM. */
+prnet_status prnet_backward_head(prnet_handle* h, const float* x, int64_t batch,
+                                 const float* dy, float* dws, float* dwt, float* db,
+                                 void* cuda_stream);
+
 /* Select the forward kernel (tuning / cross-checking; default -1 = automatic).
  * All variants compute the same reading to within the documented tolerance:
  *   0 = warp_f32     one warp per series, CUDA-core FP32                  (N <= 32)

@@ -1,0 +1,257 @@
+// bwd_head.cu -- backward pass of the PRNet head (reading R-f6 in
+// DESIGN.md §3): for an upstream gradient dy = dL/dy,
+//   dY[m][t] = dy[m S + t] s_r (0 past H),  dW_s[m][n] = sum_{series, t} dY[m][t] P_s[n][t],
+//   dW_t likewise with P_t,  db[h] = sum_series dy[h] s_r,
+// summed over the batch (and over the channels for a shared head).  The head enters y
+// linearly, so the gradients need the patterns P = A X̂ of every series but not W: the
+// kernel recomputes descriptors, both attentions and the patterns in FP32 (same reading as
+// the forward kernels, with every flag but component values and the decomposition).
+//
+// Layout: one warp per series, lane i = segment i (N <= 32), 8 warps (fewer for long
+// segments) per CTA, one channel per CTA.  Per-warp shared memory: X [N][S|1] and Z [N][S|1]
+// (odd pitch: conflict-free row walks), dY [M S], the bias gradient [H].  Lane i keeps its
+// column of dW_s, dW_t ([M] each) in registers over all the warp's series; at the end the
+// warps are reduced in a fixed order into one partial per CTA, and prnet_bwd_reduce sums the
+// partials in fp64 in a fixed order.  Deterministic, no atomics.
+#include <algorithm>
+
+#include "prnet_internal.cuh"
+
+namespace prnet {
+
+namespace {
+
+__device__ __forceinline__ float shfl(float v, int src) {
+  return __shfl_sync(0xffffffffu, v, src);
+}
+
+__global__ void __launch_bounds__(256) prnet_bwd_head_kernel(FwdArgs a, const float* __restrict__ dy,
+                                                          float* __restrict__ part,
+                                                          BwdLayout ly) {
+  extern __shared__ float4 smem4[];
+  float* smem = reinterpret_cast<float*>(smem4);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int c = blockIdx.y, C = a.C;
+  const int N = a.N, S = a.S, M = a.M, H = a.H;
+  const int P = ly.pitch;
+  float* wbase = smem + warp * ly.per_warp;
+  float* X = wbase;                      // [N][P]
+  float* Z = X + N * P;                  // [N][P]
+  float* dYs = wbase + ly.off_dy;        // [M S]
+  float* accB = wbase + ly.off_db;       // [H]
+  for (int k = lane; k < H; k += 32) accB[k] = 0.f;
+
+  const int i = lane;
+  float accS[32], accT[32];   // lane i: dW_s[m][i], dW_t[m][i]
+#pragma unroll
+  for (int m = 0; m < 32; m++) accS[m] = accT[m] = 0.f;
+
+  const int64_t b0 = (int64_t)blockIdx.x * ly.wins_per_cta;
+  int64_t b1 = b0 + ly.wins_per_cta;
+  if (b1 > a.B) b1 = a.B;
+  for (int64_t b = b0 + warp; b < b1; b += nwarps) {
+    const int64_t series = b * C + c;
+    const float* xg = a.x + b * a.xsb + c * a.xsc + a.r;
+    __syncwarp();
+    for (int k = lane; k < N * S; k += 32) {
+      const int n = k / S;
+      X[n * P + (k - n * S)] = __ldg(xg + k);
+    }
+    const float* g = dy + series * H;
+    for (int k = lane; k < M * S; k += 32) dYs[k] = k < H ? __ldg(g + k) : 0.f;
+    __syncwarp();
+
+    // a2: descriptors from d = x - x0 (Def 3-4), residual norm with metric_variant bit 1
+    float x0 = 0.f, m1 = 0.f, mu = 0.f, kap = 0.f, nu2 = 0.f;
+    if (i < N) {
+      const float* xr = X + i * P;
+      x0 = xr[0];
+      float s1 = 0.f, s3 = 0.f;
+      for (int t = 0; t < S; t++) {
+        const float d = xr[t] - x0;
+        s1 += d;
+        s3 = fmaf((float)t - a.half_s, d, s3);
+      }
+      m1 = s1 * a.inv_s;
+      mu = x0 + m1;
+      kap = s3 * a.inv_v;
+      const float kd = a.detrend ? kap : 0.f;
+      float* zr = Z + i * P;
+      for (int t = 0; t < S; t++) {
+        const float z = fmaf(-kd, (float)t - a.half_s, (xr[t] - x0) - m1);
+        zr[t] = z;
+        nu2 = fmaf(z, z, nu2);
+      }
+    }
+    // Def 5 (|z|^2 = |e|^2 + kappa^2 V when detrended) and the RevIN map (R-f1)
+    const float mbar = warp_sum(i < N ? mu : 0.f) * a.inv_n;
+    const float nz2 = a.detrend ? fmaf(kap * kap, 1.f / a.inv_v, nu2) : nu2;
+    const float var =
+        warp_sum(i < N ? nz2 + (float)S * (mu - mbar) * (mu - mbar) : 0.f) * a.inv_ns;
+    float mr = 0.f, rr = 1.f, sr = 1.f;
+    if (a.revin) {
+      mr = mbar;
+      rr = rsqrtf(var + kEpsRevin);
+      sr = (var + kEpsRevin) * rr;
+    }
+    const float inv_var = 1.f / fmaf(var * rr, rr, kEpsTrend);
+    const float cm = sqrtf(inv_var * a.kt) * rr, ck = sqrtf(a.vtrend * inv_var * a.kt) * rr;
+    const float mt = (mu - mr) * cm, kt = kap * ck;                 // trend coordinates
+    const float inv = rsqrtf(nu2 * rr * rr + kEpsSeasonal) * rr;    // seasonal normaliser
+    __syncwarp();   // Z rows written
+
+    // a3: Gram row i, a4: trend exponents, a5: both softmaxes (row max searched)
+    float as[32], at[32];
+#pragma unroll
+    for (int j = 0; j < 32; j++) as[j] = 0.f;
+    if (i < N) {
+      const float* zi = Z + i * P;
+      for (int t = 0; t < S; t++) {
+        const float v = zi[t];
+#pragma unroll
+        for (int j = 0; j < 32; j++)
+          if (j < N) as[j] = fmaf(v, Z[j * P + t], as[j]);
+      }
+    }
+    float smax = -INFINITY, tmax = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 32; j++) {
+      const float invj = shfl(inv, j), mtj = shfl(mt, j), ktj = shfl(kt, j);
+      if (j < N) {
+        as[j] = as[j] * inv * invj * a.ks;
+        const float dm = mt - mtj, dk = kt - ktj;
+        at[j] = -fmaf(dm, dm, dk * dk);
+        smax = fmaxf(smax, as[j]);
+        tmax = fmaxf(tmax, at[j]);
+      } else {
+        at[j] = 0.f;
+      }
+    }
+    float ssum = 0.f, tsum = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; j++) {
+      if (j < N) {
+        as[j] = exp2f(as[j] - smax);
+        at[j] = exp2f(at[j] - tmax);
+        ssum += as[j];
+        tsum += at[j];
+      }
+    }
+    const float rs = 1.f / ssum, rt = 1.f / tsum;
+#pragma unroll
+    for (int j = 0; j < 32; j++) {
+      as[j] *= rs;
+      at[j] *= rt;
+    }
+
+    // a6: pattern rows P^ = rr (A X - mr) (rows of A sum to 1), and the head gradient
+    // dW[m][i] += sum_t dY[m][t] s_r P^[i][t]
+    if (i < N) {
+      for (int t = 0; t < S; t++) {
+        float ps = 0.f, pt = 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; j++) {
+          if (j < N) {
+            const float xv = X[j * P + t];
+            ps = fmaf(as[j], xv, ps);
+            pt = fmaf(at[j], xv, pt);
+          }
+        }
+        ps = (ps - mr) * rr * sr;
+        pt = (pt - mr) * rr * sr;
+#pragma unroll
+        for (int m = 0; m < 32; m++) {
+          if (m < M) {
+            const float gy = dYs[m * S + t];
+            accS[m] = fmaf(gy, ps, accS[m]);
+            accT[m] = fmaf(gy, pt, accT[m]);
+          }
+        }
+      }
+    }
+    for (int k = lane; k < H; k += 32) accB[k] = fmaf(dYs[k], sr, accB[k]);
+  }
+
+  // fixed-order reduction over the warps into this CTA's partial [dW_s | dW_t | db]
+  __syncthreads();
+  float* red = smem + warp * ly.per_warp;   // reuse the X region: [2][M][32]
+#pragma unroll
+  for (int m = 0; m < 32; m++) {
+    if (m < M) {
+      red[m * 32 + lane] = accS[m];
+      red[(M + m) * 32 + lane] = accT[m];
+    }
+  }
+  __syncthreads();
+  const int MN = M * N, E = 2 * MN + H;
+  float* out = part + ((int64_t)c * gridDim.x + blockIdx.x) * E;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    float v = 0.f;
+    if (e < 2 * MN) {
+      const int br = e / MN, mn = e - br * MN, m = mn / N, n = mn - m * N;
+      for (int w = 0; w < nwarps; w++) v += smem[w * ly.per_warp + (br * M + m) * 32 + n];
+    } else {
+      const int hh = e - 2 * MN;
+      for (int w = 0; w < nwarps; w++) v += smem[w * ly.per_warp + ly.off_db + hh];
+    }
+    out[e] = v;
+  }
+}
+
+// out[cw][e] = sum over the channels of cw (all of them for a shared head) and the CTA
+// partials, in fp64, in a fixed order
+__global__ void prnet_bwd_reduce_kernel(const float* __restrict__ part, int C, int nblk, int E,
+                                        int MN, int H, int hpc, float* dws, float* dwt,
+                                        float* db) {
+  const int cw = blockIdx.y;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+    double v = 0.0;
+    const int c0 = hpc ? cw : 0, c1 = hpc ? cw + 1 : C;
+    for (int c = c0; c < c1; c++)
+      for (int k = 0; k < nblk; k++) v += (double)part[((int64_t)c * nblk + k) * E + e];
+    if (e < MN) dws[(int64_t)cw * MN + e] = (float)v;
+    else if (e < 2 * MN) dwt[(int64_t)cw * MN + e - MN] = (float)v;
+    else db[(int64_t)cw * H + e - 2 * MN] = (float)v;
+  }
+}
+
+}  // namespace
+
+bool plan_bwd_head(const FwdArgs& a, int max_smem_optin, BwdPlan* p) {
+  if (a.N < 1 || a.N > 32 || a.M > 32 || a.S > 128) return false;
+  BwdLayout& ly = p->ly;
+  ly.pitch = a.S | 1;
+  const int xz = std::max(2 * a.N * ly.pitch, 2 * a.M * 32);
+  ly.off_dy = (xz + 3) & ~3;
+  ly.off_db = (ly.off_dy + a.M * a.S + 3) & ~3;
+  ly.per_warp = (ly.off_db + a.H + 3) & ~3;
+  int w = 8;
+  while (w > 1 && (size_t)w * ly.per_warp * 4 > (size_t)max_smem_optin) w--;
+  if ((size_t)w * ly.per_warp * 4 > (size_t)max_smem_optin) return false;
+  p->warps = w;
+  ly.wins_per_cta = 32 * w;
+  p->nblk = (int)((a.B + ly.wins_per_cta - 1) / ly.wins_per_cta);
+  p->smem_bytes = (size_t)w * ly.per_warp * 4;
+  p->elems = 2 * a.M * a.N + a.H;
+  return true;
+}
+
+cudaError_t launch_bwd_head(const FwdArgs& a, const BwdPlan& p, const float* dy, float* part,
+                            float* dws, float* dwt, float* db, int Cw, cudaStream_t st) {
+  if (p.nblk > 0) {
+    cudaError_t e = cudaFuncSetAttribute(prnet_bwd_head_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)p.smem_bytes);
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)p.nblk, (unsigned)a.C);
+    prnet_bwd_head_kernel<<<grid, 32 * p.warps, p.smem_bytes, st>>>(a, dy, part, p.ly);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  dim3 rg((unsigned)((p.elems + 255) / 256), (unsigned)Cw);
+  prnet_bwd_reduce_kernel<<<rg, 256, 0, st>>>(part, a.C, p.nblk, p.elems, a.M * a.N, a.H,
+                                               a.head_per_channel, dws, dwt, db);
+  return cudaGetLastError();
+}
+
+}  // namespace prnet

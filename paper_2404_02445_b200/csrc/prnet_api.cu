@@ -38,6 +38,8 @@ struct prnet_handle {
   cudaStream_t streams[kStages] = {nullptr, nullptr, nullptr};
   float* d_series = nullptr;   // prnet_forward_sliding_host: device copy of the series span
   int64_t series_floats = 0;
+  float* d_bwd = nullptr;      // prnet_backward_head: per-CTA partials
+  int64_t bwd_floats = 0;
 };
 
 namespace {
@@ -616,6 +618,7 @@ void prnet_destroy(prnet_handle* h) {
   {
     DeviceGuard g(h->cfg.device);
     cudaFree(h->d_series);
+    cudaFree(h->d_bwd);
     cudaFree(h->d_ws);
     cudaFree(h->d_wt);
     cudaFree(h->d_b);
@@ -695,6 +698,46 @@ prnet_status prnet_error_sums(prnet_handle* h, const float* y, const float* targ
   const int64_t n = batch * h->cfg.channels * h->cfg.horizon;
   cudaError_t e = prnet::launch_error_sums(y, target, n, h->d_err, out3, (cudaStream_t)cuda_stream);
   return e == cudaSuccess ? PRNET_OK : cuda_fail(h, e, "error_sums launch");
+}
+
+prnet_status prnet_backward_head(prnet_handle* h, const float* x, int64_t batch,
+                                 const float* dy, float* dws, float* dwt, float* db,
+                                 void* cuda_stream) {
+  if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
+  if (batch < 0) return fail(h, PRNET_ERR_INVALID_ARG, "batch < 0");
+  if (!dws || !dwt || !db || (batch > 0 && (!x || !dy)))
+    return fail(h, PRNET_ERR_INVALID_ARG, "NULL pointer");
+  if ((h->cfg.metric_variant & 4) != 0 || h->cfg.ma_kernel > 0)
+    return fail(h, PRNET_ERR_UNSUPPORTED,
+                "backward_head: component values and the decomposition are forward-only");
+  prnet_status s = PRNET_OK;
+  if (batch > 0) {
+    s = check_dev_ptr(h, x, "x");
+    if (s == PRNET_OK) s = check_dev_ptr(h, dy, "dy");
+  }
+  if (s == PRNET_OK) s = check_dev_ptr(h, dws, "dws");
+  if (s == PRNET_OK) s = check_dev_ptr(h, dwt, "dwt");
+  if (s == PRNET_OK) s = check_dev_ptr(h, db, "db");
+  if (s != PRNET_OK) return s;
+  DeviceGuard g(h->cfg.device);
+  prnet::FwdArgs a = make_args(h, x, batch, nullptr);
+  prnet::BwdPlan p;
+  if (!prnet::plan_bwd_head(a, h->max_smem_optin, &p))
+    return fail(h, PRNET_ERR_UNSUPPORTED, "backward_head needs N <= 32, M <= 32, S <= 128");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int64_t need = (int64_t)h->cfg.channels * p.nblk * p.elems;
+  if (need > h->bwd_floats) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(h, e, "backward_head sync");
+    cudaFree(h->d_bwd);
+    h->d_bwd = nullptr;
+    h->bwd_floats = 0;
+    e = cudaMalloc(&h->d_bwd, (size_t)need * sizeof(float));
+    if (e != cudaSuccess) return cuda_fail(h, e, "backward_head workspace");
+    h->bwd_floats = need;
+  }
+  cudaError_t e = prnet::launch_bwd_head(a, p, dy, h->d_bwd, dws, dwt, db, h->Cw, st);
+  return e == cudaSuccess ? PRNET_OK : cuda_fail(h, e, "backward_head launch");
 }
 
 prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {

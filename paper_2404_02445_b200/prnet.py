@@ -24,7 +24,7 @@ EXPORTS = ("prnet_create", "prnet_load_params", "prnet_forward", "prnet_forward_
            "prnet_set_host_chunk", "prnet_destroy", "prnet_last_error", "prnet_get_dims",
            "prnet_debug_segments", "prnet_debug_attention", "prnet_error_sums",
            "prnet_forward_plan", "prnet_set_kernel_variant", "prnet_forward_sliding",
-           "prnet_forward_sliding_host")
+           "prnet_forward_sliding_host", "prnet_backward_head")
 VARIANTS = ("warp_f32", "long_f32", "mma_f16x3", "tc_fold", "tc_full", "flash_f16x3", "tc_quad", "small_f32")
 
 
@@ -70,6 +70,7 @@ def load_library(path: str | None = None):
         "prnet_error_sums": ([vp, vp, vp, i64, vp, vp], ctypes.c_int),
         "prnet_forward_plan": ([vp, i64, i32p, i32p], ctypes.c_int),
         "prnet_set_kernel_variant": ([vp, ctypes.c_int32], ctypes.c_int),
+        "prnet_backward_head": ([vp, vp, i64, vp, vp, vp, vp, vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -234,6 +235,20 @@ class PRNet:
             self._h, ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(target.data_ptr()),
             y.shape[0], ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)))
         return out
+
+    def backward_head(self, x, dy, stream=None):
+        """Gradients (dws [Cw,M,N], dwt [Cw,M,N], db [Cw,H]) of sum(dy * y) with respect to
+        the head, for the forward of x (include/prnet.h)."""
+        import torch
+        cw = self.C if self.head_per_channel else 1
+        dws = torch.empty((cw, self.M, self.N), dtype=torch.float32, device=x.device)
+        dwt = torch.empty_like(dws)
+        db = torch.empty((cw, self.H), dtype=torch.float32, device=x.device)
+        self._check(self._lib.prnet_backward_head(
+            self._h, ctypes.c_void_p(x.data_ptr()), x.shape[0], ctypes.c_void_p(dy.data_ptr()),
+            ctypes.c_void_p(dws.data_ptr()), ctypes.c_void_p(dwt.data_ptr()),
+            ctypes.c_void_p(db.data_ptr()), _stream_ptr(stream)))
+        return dws, dwt, db
 
     def plan(self, batch: int):
         n, v = ctypes.c_int32(), ctypes.c_int32()

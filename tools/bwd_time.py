@@ -1,0 +1,31 @@
+"""Time prnet_backward_head on a workload's windows (CUDA events, after warm-up)."""
+import json
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import synth  # noqa: E402
+from paper_2404_02445_b200 import PRNet  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "traffic"
+w = synth.WORKLOADS[name]
+s = synth.make_series(w)
+sd = torch.from_numpy(s).cuda()
+x = sd.unfold(1, w.L, 1)[:, w.t0:w.t0 + w.windows, :].permute(1, 0, 2).contiguous()
+dy = torch.randn((w.windows, w.C, w.H), device="cuda")
+m = PRNet(w.C, w.L, w.S, w.H)
+for _ in range(2):
+    m.backward_head(x, dy)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(5):
+    m.backward_head(x, dy)
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / 5
+byts = (w.windows * w.C * (w.L + w.H)) * 4
+print(json.dumps({"workload": name, "ms": ms, "windows_per_s": w.windows / ms * 1e3,
+                  "hbm_frac": byts / (ms / 1e3) / 6552.3e9}))
