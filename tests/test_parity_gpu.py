@@ -515,3 +515,26 @@ def test_sliding_argument_errors():
         m.forward_sliding(s, -1, 2)
     assert e.value.status == 1
     assert m.forward_sliding(s, 104, 1).shape == (1, 3, 96)   # ends exactly at T
+
+
+# ------------------------------------------------------------------ every output element written
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("L,S,H,mv", [(720, 24, 336, 0), (720, 24, 96, 0), (720, 24, 720, 4),
+                                      (96, 24, 96, 0), (97, 7, 13, 0), (1440, 24, 100, 0)])
+def test_every_output_element_written(L, S, H, mv, variant):
+    """Forward into a NaN-filled y: no element may stay unwritten (the mma_f16x3 S = 24
+    epilogue writes y with TMA bulk stores, which compute-sanitizer initcheck does not see)."""
+    if not _applicable(variant, L, S, H):
+        pytest.skip("variant not applicable")
+    if mv and variant not in (None, "mma_f16x3"):
+        pytest.skip("component values run in mma_f16x3")
+    x = torch.from_numpy(synth.random_windows(5, 3, L)).cuda()
+    N, _, M = synth.derived_dims(L, S, H)
+    ws, wt, b = synth.make_params(3, M, N, H)
+    m = PRNet(3, L, S, H, metric_variant=mv).load(ws, wt, b)
+    if variant is not None:
+        m.set_variant(variant)
+    y = torch.full((5, 3, H), float("nan"), device="cuda")
+    m.forward_into(x, y)
+    torch.cuda.synchronize()
+    assert torch.isfinite(y).all()
