@@ -8,8 +8,8 @@
 // the forward kernels, with every flag but component values and the decomposition).
 //
 // Layout: one warp per series, lane i = segment i (N <= 32), 8 warps (fewer for long
-// segments) per CTA, one channel per CTA.  Per-warp shared memory: X [N][S|1] and Z [N][S|1]
-// (odd pitch: conflict-free row walks), dY [M S], the bias gradient [H].  Lane i keeps its
+// segments) per CTA, one channel per CTA.  Per-warp shared memory: X, Z [S][NP] and dY
+// [S][MP] (transposed, zero-padded), the bias gradient [H].  Lane i keeps its
 // column of dW_s, dW_t ([M] each) in registers over all the warp's series; at the end the
 // warps are reduced in a fixed order into one partial per CTA, and prnet_bwd_reduce sums the
 // partials in fp64 in a fixed order.  Deterministic, no atomics.
@@ -25,6 +25,11 @@ __device__ __forceinline__ float shfl(float v, int src) {
   return __shfl_sync(0xffffffffu, v, src);
 }
 
+// NP / MP: segment / future-segment counts padded to 8, 16 or 32.  X, Z and dY are stored
+// transposed ([t][NP], [t][MP]) with zero padding rows, so every inner loop is unguarded,
+// a row of all segments at one t is NP/4 broadcast float4 loads, and lane i's own element
+// at t is conflict-free.
+template <int NP, int MP>
 __global__ void __launch_bounds__(256) prnet_bwd_head_kernel(FwdArgs a, const float* __restrict__ dy,
                                                           float* __restrict__ part,
                                                           BwdLayout ly) {
@@ -33,18 +38,19 @@ __global__ void __launch_bounds__(256) prnet_bwd_head_kernel(FwdArgs a, const fl
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int c = blockIdx.y, C = a.C;
   const int N = a.N, S = a.S, M = a.M, H = a.H;
-  const int P = ly.pitch;
   float* wbase = smem + warp * ly.per_warp;
-  float* X = wbase;                      // [N][P]
-  float* Z = X + N * P;                  // [N][P]
-  float* dYs = wbase + ly.off_dy;        // [M S]
+  float* X = wbase;                      // [S][NP]
+  float* Z = X + S * NP;                 // [S][NP]
+  float* dYs = wbase + ly.off_dy;        // [S][MP]
   float* accB = wbase + ly.off_db;       // [H]
   for (int k = lane; k < H; k += 32) accB[k] = 0.f;
+  for (int k = lane; k < 2 * S * NP; k += 32) X[k] = 0.f;   // padding rows stay 0
+  for (int k = lane; k < S * MP; k += 32) dYs[k] = 0.f;
 
   const int i = lane;
-  float accS[32], accT[32];   // lane i: dW_s[m][i], dW_t[m][i]
+  float accS[MP], accT[MP];   // lane i: dW_s[m][i], dW_t[m][i]
 #pragma unroll
-  for (int m = 0; m < 32; m++) accS[m] = accT[m] = 0.f;
+  for (int m = 0; m < MP; m++) accS[m] = accT[m] = 0.f;
 
   const int64_t b0 = (int64_t)blockIdx.x * ly.wins_per_cta;
   int64_t b1 = b0 + ly.wins_per_cta;
@@ -52,23 +58,25 @@ __global__ void __launch_bounds__(256) prnet_bwd_head_kernel(FwdArgs a, const fl
   for (int64_t b = b0 + warp; b < b1; b += nwarps) {
     const int64_t series = b * C + c;
     const float* xg = a.x + b * a.xsb + c * a.xsc + a.r;
-    __syncwarp();
-    for (int k = lane; k < N * S; k += 32) {
-      const int n = k / S;
-      X[n * P + (k - n * S)] = __ldg(xg + k);
-    }
     const float* g = dy + series * H;
-    for (int k = lane; k < M * S; k += 32) dYs[k] = k < H ? __ldg(g + k) : 0.f;
+    __syncwarp();
+    // lane = segment row (global reads are L1-served), transposed conflict-free stores
+    for (int t = 0; t < S; t++) {
+      if (i < N) X[t * NP + i] = __ldg(xg + i * S + t);
+      if (i < M) {
+        const int h = i * S + t;
+        dYs[t * MP + i] = h < H ? __ldg(g + h) : 0.f;
+      }
+    }
     __syncwarp();
 
     // a2: descriptors from d = x - x0 (Def 3-4), residual norm with metric_variant bit 1
     float x0 = 0.f, m1 = 0.f, mu = 0.f, kap = 0.f, nu2 = 0.f;
     if (i < N) {
-      const float* xr = X + i * P;
-      x0 = xr[0];
+      x0 = X[i];
       float s1 = 0.f, s3 = 0.f;
       for (int t = 0; t < S; t++) {
-        const float d = xr[t] - x0;
+        const float d = X[t * NP + i] - x0;
         s1 += d;
         s3 = fmaf((float)t - a.half_s, d, s3);
       }
@@ -76,10 +84,9 @@ __global__ void __launch_bounds__(256) prnet_bwd_head_kernel(FwdArgs a, const fl
       mu = x0 + m1;
       kap = s3 * a.inv_v;
       const float kd = a.detrend ? kap : 0.f;
-      float* zr = Z + i * P;
       for (int t = 0; t < S; t++) {
-        const float z = fmaf(-kd, (float)t - a.half_s, (xr[t] - x0) - m1);
-        zr[t] = z;
+        const float z = fmaf(-kd, (float)t - a.half_s, (X[t * NP + i] - x0) - m1);
+        Z[t * NP + i] = z;
         nu2 = fmaf(z, z, nu2);
       }
     }
@@ -98,85 +105,90 @@ __global__ void __launch_bounds__(256) prnet_bwd_head_kernel(FwdArgs a, const fl
     const float cm = sqrtf(inv_var * a.kt) * rr, ck = sqrtf(a.vtrend * inv_var * a.kt) * rr;
     const float mt = (mu - mr) * cm, kt = kap * ck;                 // trend coordinates
     const float inv = rsqrtf(nu2 * rr * rr + kEpsSeasonal) * rr;    // seasonal normaliser
-    __syncwarp();   // Z rows written
+    __syncwarp();   // Z written
 
-    // a3: Gram row i, a4: trend exponents, a5: both softmaxes (row max searched)
-    float as[32], at[32];
+    // a3: Gram row i (padding rows of Z are 0)
+    float as[NP], at[NP];
 #pragma unroll
-    for (int j = 0; j < 32; j++) as[j] = 0.f;
-    if (i < N) {
-      const float* zi = Z + i * P;
-      for (int t = 0; t < S; t++) {
-        const float v = zi[t];
+    for (int j = 0; j < NP; j++) as[j] = 0.f;
+    for (int t = 0; t < S; t++) {
+      const float v = Z[t * NP + i];
+      const float4* zr = reinterpret_cast<const float4*>(Z + t * NP);
 #pragma unroll
-        for (int j = 0; j < 32; j++)
-          if (j < N) as[j] = fmaf(v, Z[j * P + t], as[j]);
+      for (int q = 0; q < NP / 4; q++) {
+        const float4 z4 = zr[q];
+        as[4 * q] = fmaf(v, z4.x, as[4 * q]);
+        as[4 * q + 1] = fmaf(v, z4.y, as[4 * q + 1]);
+        as[4 * q + 2] = fmaf(v, z4.z, as[4 * q + 2]);
+        as[4 * q + 3] = fmaf(v, z4.w, as[4 * q + 3]);
       }
     }
+    // a4 + a5: exponents (masked past N), searched row maxima, both softmaxes
     float smax = -INFINITY, tmax = -INFINITY;
 #pragma unroll
-    for (int j = 0; j < 32; j++) {
+    for (int j = 0; j < NP; j++) {
       const float invj = shfl(inv, j), mtj = shfl(mt, j), ktj = shfl(kt, j);
-      if (j < N) {
-        as[j] = as[j] * inv * invj * a.ks;
-        const float dm = mt - mtj, dk = kt - ktj;
-        at[j] = -fmaf(dm, dm, dk * dk);
-        smax = fmaxf(smax, as[j]);
-        tmax = fmaxf(tmax, at[j]);
-      } else {
-        at[j] = 0.f;
-      }
+      const float dm = mt - mtj, dk = kt - ktj;
+      as[j] = j < N ? as[j] * inv * invj * a.ks : -INFINITY;
+      at[j] = j < N ? -fmaf(dm, dm, dk * dk) : -INFINITY;
+      smax = fmaxf(smax, as[j]);
+      tmax = fmaxf(tmax, at[j]);
     }
     float ssum = 0.f, tsum = 0.f;
 #pragma unroll
-    for (int j = 0; j < 32; j++) {
-      if (j < N) {
-        as[j] = exp2f(as[j] - smax);
-        at[j] = exp2f(at[j] - tmax);
-        ssum += as[j];
-        tsum += at[j];
-      }
+    for (int j = 0; j < NP; j++) {
+      as[j] = exp2f(as[j] - smax);
+      at[j] = exp2f(at[j] - tmax);
+      ssum += as[j];
+      tsum += at[j];
     }
-    const float rs = 1.f / ssum, rt = 1.f / tsum;
-#pragma unroll
-    for (int j = 0; j < 32; j++) {
-      as[j] *= rs;
-      at[j] *= rt;
-    }
+    // rows of A sum to 1: P^ = rr (A X - mr); the s_r of dY folded into the row scale
+    const float rs = rr * sr / ssum, rt = rr * sr / tsum, off = mr * rr * sr;
 
-    // a6: pattern rows P^ = rr (A X - mr) (rows of A sum to 1), and the head gradient
-    // dW[m][i] += sum_t dY[m][t] s_r P^[i][t]
-    if (i < N) {
-      for (int t = 0; t < S; t++) {
-        float ps = 0.f, pt = 0.f;
+    // a6 + gradient: dW[m][i] += sum_t dY[m][t] s_r P^[i][t]
+    for (int t = 0; t < S; t++) {
+      float ps = 0.f, pt = 0.f;
+      const float4* xr = reinterpret_cast<const float4*>(X + t * NP);
 #pragma unroll
-        for (int j = 0; j < 32; j++) {
-          if (j < N) {
-            const float xv = X[j * P + t];
-            ps = fmaf(as[j], xv, ps);
-            pt = fmaf(at[j], xv, pt);
-          }
-        }
-        ps = (ps - mr) * rr * sr;
-        pt = (pt - mr) * rr * sr;
+      for (int q = 0; q < NP / 4; q++) {
+        const float4 x4 = xr[q];
+        ps = fmaf(as[4 * q], x4.x, ps);
+        pt = fmaf(at[4 * q], x4.x, pt);
+        ps = fmaf(as[4 * q + 1], x4.y, ps);
+        pt = fmaf(at[4 * q + 1], x4.y, pt);
+        ps = fmaf(as[4 * q + 2], x4.z, ps);
+        pt = fmaf(at[4 * q + 2], x4.z, pt);
+        ps = fmaf(as[4 * q + 3], x4.w, ps);
+        pt = fmaf(at[4 * q + 3], x4.w, pt);
+      }
+      ps = fmaf(ps, rs, -off);
+      pt = fmaf(pt, rt, -off);
+      const float4* gr = reinterpret_cast<const float4*>(dYs + t * MP);
 #pragma unroll
-        for (int m = 0; m < 32; m++) {
-          if (m < M) {
-            const float gy = dYs[m * S + t];
-            accS[m] = fmaf(gy, ps, accS[m]);
-            accT[m] = fmaf(gy, pt, accT[m]);
-          }
-        }
+      for (int q = 0; q < MP / 4; q++) {
+        const float4 g4 = gr[q];
+        accS[4 * q] = fmaf(g4.x, ps, accS[4 * q]);
+        accT[4 * q] = fmaf(g4.x, pt, accT[4 * q]);
+        accS[4 * q + 1] = fmaf(g4.y, ps, accS[4 * q + 1]);
+        accT[4 * q + 1] = fmaf(g4.y, pt, accT[4 * q + 1]);
+        accS[4 * q + 2] = fmaf(g4.z, ps, accS[4 * q + 2]);
+        accT[4 * q + 2] = fmaf(g4.z, pt, accT[4 * q + 2]);
+        accS[4 * q + 3] = fmaf(g4.w, ps, accS[4 * q + 3]);
+        accT[4 * q + 3] = fmaf(g4.w, pt, accT[4 * q + 3]);
       }
     }
-    for (int k = lane; k < H; k += 32) accB[k] = fmaf(dYs[k], sr, accB[k]);
+    for (int k = lane; k < H; k += 32) {
+      const int m = k / S;
+      accB[k] = fmaf(dYs[(k - m * S) * MP + m], sr, accB[k]);
+    }
   }
 
   // fixed-order reduction over the warps into this CTA's partial [dW_s | dW_t | db]
+  // (lanes past N hold padding columns and are not read)
   __syncthreads();
   float* red = smem + warp * ly.per_warp;   // reuse the X region: [2][M][32]
 #pragma unroll
-  for (int m = 0; m < 32; m++) {
+  for (int m = 0; m < MP; m++) {
     if (m < M) {
       red[m * 32 + lane] = accS[m];
       red[(M + m) * 32 + lane] = accT[m];
@@ -220,10 +232,11 @@ __global__ void prnet_bwd_reduce_kernel(const float* __restrict__ part, int C, i
 bool plan_bwd_head(const FwdArgs& a, int max_smem_optin, BwdPlan* p) {
   if (a.N < 1 || a.N > 32 || a.M > 32 || a.S > 128) return false;
   BwdLayout& ly = p->ly;
-  ly.pitch = a.S | 1;
-  const int xz = std::max(2 * a.N * ly.pitch, 2 * a.M * 32);
+  ly.np = a.N <= 8 ? 8 : (a.N <= 16 ? 16 : 32);
+  ly.mp = a.M <= 8 ? 8 : (a.M <= 16 ? 16 : 32);
+  const int xz = std::max(2 * a.S * ly.np, 2 * a.M * 32);
   ly.off_dy = (xz + 3) & ~3;
-  ly.off_db = (ly.off_dy + a.M * a.S + 3) & ~3;
+  ly.off_db = (ly.off_dy + a.S * ly.mp + 3) & ~3;
   ly.per_warp = (ly.off_db + a.H + 3) & ~3;
   int w = 8;
   while (w > 1 && (size_t)w * ly.per_warp * 4 > (size_t)max_smem_optin) w--;
@@ -236,16 +249,36 @@ bool plan_bwd_head(const FwdArgs& a, int max_smem_optin, BwdPlan* p) {
   return true;
 }
 
+template <int NP, int MP>
+static cudaError_t launch_bwd_t(const FwdArgs& a, const BwdPlan& p, const float* dy,
+                                float* part, cudaStream_t st) {
+  auto k = prnet_bwd_head_kernel<NP, MP>;
+  cudaError_t e =
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)p.nblk, (unsigned)a.C);
+  k<<<grid, 32 * p.warps, p.smem_bytes, st>>>(a, dy, part, p.ly);
+  return cudaGetLastError();
+}
+template <int NP>
+static cudaError_t launch_bwd_n(const FwdArgs& a, const BwdPlan& p, const float* dy,
+                                float* part, cudaStream_t st) {
+  switch (p.ly.mp) {
+    case 8: return launch_bwd_t<NP, 8>(a, p, dy, part, st);
+    case 16: return launch_bwd_t<NP, 16>(a, p, dy, part, st);
+    default: return launch_bwd_t<NP, 32>(a, p, dy, part, st);
+  }
+}
+
 cudaError_t launch_bwd_head(const FwdArgs& a, const BwdPlan& p, const float* dy, float* part,
                             float* dws, float* dwt, float* db, int Cw, cudaStream_t st) {
   if (p.nblk > 0) {
-    cudaError_t e = cudaFuncSetAttribute(prnet_bwd_head_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)p.smem_bytes);
-    if (e != cudaSuccess) return e;
-    dim3 grid((unsigned)p.nblk, (unsigned)a.C);
-    prnet_bwd_head_kernel<<<grid, 32 * p.warps, p.smem_bytes, st>>>(a, dy, part, p.ly);
-    e = cudaGetLastError();
+    cudaError_t e;
+    switch (p.ly.np) {
+      case 8: e = launch_bwd_n<8>(a, p, dy, part, st); break;
+      case 16: e = launch_bwd_n<16>(a, p, dy, part, st); break;
+      default: e = launch_bwd_n<32>(a, p, dy, part, st); break;
+    }
     if (e != cudaSuccess) return e;
   }
   dim3 rg((unsigned)((p.elems + 255) / 256), (unsigned)Cw);
