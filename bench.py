@@ -411,7 +411,11 @@ def main():
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = None if args.sliding else json.load(open(prof)).get(w.name)
+            # measured for one full-workload launch of the plain path: scaled to this rank's
+            # share of the windows; not applicable to the sliding or widened modes
+            t_full = json.load(open(prof)).get(w.name)
+            widened = args.sliding or args.metric_variant or args.instance_norm or args.ma_kernel
+            traffic = None if (widened or t_full is None) else t_full * count / w.windows
         except Exception:
             traffic = None
 
