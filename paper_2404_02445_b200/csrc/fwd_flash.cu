@@ -187,9 +187,6 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
         split1(v * sx, h, l);
         x_hi[n * XP + t] = h;
         x_lo[n * XP + t] = l;
-        split1(z * sz, h, l);
-        z_hi[n * ZP + t] = h;
-        z_lo[n * ZP + t] = l;
       }
       const float mu = x0 + m1;
       c_mu[n] = mu;        // temporarily mu
@@ -219,7 +216,21 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
       if (n < N) {
         const float nu2 = c_inv[n] * rr * rr;
         const float inv = rsqrtf(nu2 + kEpsSeasonal);
-        c_inv[n] = inv * rr;           // the Gram is of the un-normalised z sz
+        // row-normalised Gram operand Z'_n = z_n rr / sqrt(nu2_n rr^2 + eps_s) (|Z'_n| <= 1):
+        // the split keeps ~22 bits relative to every row, and the Gram is rho itself
+        {
+          const float* xr = xbuf + n * S;
+          const float x0 = xr[0], m1 = c_nu[n], q = inv * rr;
+          const float kd = a.detrend ? c_ka[n] : 0.f;
+          for (int t = 0; t < S; t++) {
+            const float z = fmaf(-kd, (float)t - half_s, (xr[t] - x0) - m1);
+            __half h, l;
+            split1(z * q, h, l);
+            z_hi[n * ZP + t] = h;
+            z_lo[n * ZP + t] = l;
+          }
+        }
+        c_inv[n] = 1.f;                // column factor of rho: 1 (row-normalised Gram)
         c_max[n] = sqrtf(nu2) * inv;   // f_n: known row maximum of rho (Cauchy-Schwarz)
         c_mu[n] = (c_mu[n] - mu_r) * cmt;
         c_ka[n] = c_ka[n] * ckt;
@@ -244,7 +255,7 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
       for (int nt = 0; nt < NTT; nt++)
 #pragma unroll
         for (int e = 0; e < 4; e++) yacc[mm][nt][e] = 0.f;
-    const float rsz2 = a.ks / (sz * sz);
+    const float rsz2 = a.ks;   // the Gram of the row-normalised Z' is rho
     for (int qt = warp; qt < NT; qt += nwarps) {
       uint32_t zah[KS][4], zal[KS][4];
 #pragma unroll

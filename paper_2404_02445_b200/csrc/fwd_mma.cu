@@ -361,16 +361,20 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
                 a.inv_ns;
       sx = pow2_scale((warp_max_nonneg(amx) + fabsf(mr)) * rr);
       sz = pow2_scale(warp_max_nonneg(2.f * dmx + (a.detrend ? fabsf(kap) * a.half_s : 0.f)));
-      rsm[lane] = x0;
-      rsm[32 + lane] = m1;
-      rsm[64 + lane] = a.detrend ? kap : 0.f;
+      // per-row shift, mean, slope and Z' scale for the coalesced pass, one float4 per row in
+      // the (not yet written) descriptor array.  Row-normalised Gram operand:
+      // Z'_i = z_i rr / sqrt(nu2_i rr^2 + eps_s), |Z'_i| <= 1, so the split keeps ~22 bits
+      // relative to every row (not to the series' largest row)
+      dsc[lane] = make_float4(x0, m1, a.detrend ? kap : 0.f,
+                              rsqrtf(nu2 * rr * rr + kEpsSeasonal) * rr);
       __syncwarp();
       const float xsc = rr * sx, xoff = -mr * rr * sx;
       for (int k = lane; k < NS; k += 32) {
         const int r = (int)(((float)k + 0.5f) * a.inv_s);
         const int t = k - r * S;
         const float tv = tbuf[k], vs = xbuf[k] - tv;
-        const float xr0 = rsm[r], mrow = rsm[32 + r], krow = rsm[64 + r];
+        const float4 ri = dsc[r];
+        const float xr0 = ri.x, mrow = ri.y, krow = ri.z;
         __half h, l;
         split1(vs * xsc, h, l);
         x_hi[r * sph + t] = h;
@@ -378,7 +382,7 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
         split1(fmaf(tv, xsc, xoff), h, l);
         xt_hi[r * sph + t] = h;
         xt_lo[r * sph + t] = l;
-        split1(fmaf(-krow, (float)t - a.half_s, (vs - xr0) - mrow) * sz, h, l);
+        split1(fmaf(-krow, (float)t - a.half_s, (vs - xr0) - mrow) * ri.w, h, l);
         z_hi[r * zph + t] = h;
         z_lo[r * zph + t] = l;
       }
@@ -464,21 +468,23 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
       sx = pow2_scale((warp_max_nonneg(amx) + fabsf(mr)) * rr);
       // |e| <= |z| + |kappa| max|t~| <= 2 max|d| + |kappa| (S-1)/2
       sz = pow2_scale(warp_max_nonneg(2.f * dmx + (a.detrend ? fabsf(kap) * a.half_s : 0.f)));
-      rsm[lane] = x0;        // per-row shift, mean and slope for the coalesced pass (no
-      rsm[32 + lane] = m1;   // shuffles in its lane-divergent loop)
-      rsm[64 + lane] = a.detrend ? kap : 0.f;
+      // per-row shift, mean, slope and row-normalised Z' scale for the coalesced pass (no
+      // shuffles in its lane-divergent loop), one float4 per row in the descriptor array
+      dsc[lane] = make_float4(x0, m1, a.detrend ? kap : 0.f,
+                              rsqrtf(nu2 * rr * rr + kEpsSeasonal) * rr);
       __syncwarp();
       const float xsc = rr * sx, xoff = -mr * rr * sx;
       for (int k = lane; k < NS; k += 32) {
         const int r = (int)(((float)k + 0.5f) * a.inv_s);
         const int t = k - r * S;
         const float v = xbuf[k];
-        const float xr0 = rsm[r], mrow = rsm[32 + r], krow = rsm[64 + r];
+        const float4 ri = dsc[r];
+        const float xr0 = ri.x, mrow = ri.y, krow = ri.z;
         __half h, l;
         split1(fmaf(v, xsc, xoff), h, l);
         x_hi[r * sph + t] = h;
         x_lo[r * sph + t] = l;
-        split1(fmaf(-krow, (float)t - a.half_s, (v - xr0) - mrow) * sz, h, l);
+        split1(fmaf(-krow, (float)t - a.half_s, (v - xr0) - mrow) * ri.w, h, l);
         z_hi[r * zph + t] = h;
         z_lo[r * zph + t] = l;
       }
@@ -512,7 +518,9 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
       // z sz (unnormalised), so the column factor carries one rr and rk the other
       const float nh2 = nu2 * rr * rr;
       const float invh = rsqrtf(nh2 + kEpsSeasonal);
-      dsc[lane] = i < N ? make_float4((mu_t - mr) * cm, kap_t * ck, invh * rr, sqrtf(nh2) * invh)
+      // generic path: the Gram of the row-normalised Z' is rho itself (column factor 1)
+      dsc[lane] = i < N ? make_float4((mu_t - mr) * cm, kap_t * ck, SC == 0 ? 1.f : invh * rr,
+                                      sqrtf(nh2) * invh)
                         : make_float4(0.f, 0.f, 1.f, 0.f);
       if ((SC == 0 || COMP) && a.comp) {   // the (normalised) segment levels and slopes
         cvec[lane] = i < N ? (DEC ? mu : mu - mr) * rr : 0.f;
@@ -629,7 +637,7 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
     // Gram rows G'[16 mt .. 16 mt + 15][:] = Z' Z'^T (= sz^2 G), rho_ij = G'_ij inv_i inv_j / sz^2
     // with inv = 1/sqrt(nu2 + eps_s) (Def 6), row softmax on the fragments, fold Q' += W'_s A_s
     {
-      const float ks_z = a.ks / (sz * sz);
+      const float ks_z = SC == 0 ? a.ks : a.ks / (sz * sz);
       float2 cinv[2 * MT], cmask[2 * MT];
 #pragma unroll
       for (int nt = 0; nt < 2 * MT; nt++) {
