@@ -538,3 +538,36 @@ def test_every_output_element_written(L, S, H, mv, variant):
     m.forward_into(x, y)
     torch.cuda.synchronize()
     assert torch.isfinite(y).all()
+
+
+# ------------------------------------------------------------------ heterogeneous segment scales
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("L,S,H", [(720, 24, 336), (336, 24, 96), (1440, 24, 96), (97, 7, 13),
+                                   (576, 48, 96)])
+@pytest.mark.parametrize("mv", [0, 2])
+def test_heterogeneous_segment_scales(oracle_mod, L, S, H, mv, variant):
+    """Segments whose amplitudes differ by up to 1e3 within one series (quiet and busy
+    periods), at a sharp seasonal temperature: the Gram operand's precision must hold
+    relative to every row, not only to the largest."""
+    if not _applicable(variant, L, S, H):
+        pytest.skip("variant not applicable")
+    g = np.random.default_rng(L + S + mv)
+    B, C = 3, 4
+    N = L // S
+    x = synth.random_windows(B, C, L, kind="normal").astype(np.float64)
+    r = L - N * S
+    amp = 10.0 ** g.uniform(-3, 0, (B, C, N))
+    x[:, :, r:] = (x[:, :, r:].reshape(B, C, N, S) * amp[..., None]).reshape(B, C, N * S)
+    x = x.astype(np.float32)
+    N_, _, M = synth.derived_dims(L, S, H)
+    ws, wt, b = synth.make_params(C, M, N_, H, True, synth.DEFAULT_SEED, 0)
+    try:
+        m = PRNet(C, L, S, H, tau_s=0.05, metric_variant=mv).load(ws, wt, b)
+        if variant is not None:
+            m.set_variant(variant)
+        y = m.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+    except PrnetError as e:
+        assert e.status == 3
+        pytest.skip(str(e))
+    _, y64 = oracle_mod.forward(x, S, H, ws, wt, b, True, 0.05, 1.0, metric_variant=mv)
+    assert_parity(y, y64)
