@@ -132,7 +132,8 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
   __half* z_lo = reinterpret_cast<__half*>(wb + (SC > 0 ? KO.zlo : ly.off_zlo));
   // per-row descriptors (mu~, kappa~, 1/sqrt(nu2 + eps_s), f) broadcast through shared memory
   float4* dsc = reinterpret_cast<float4*>(wb + (SC > 0 ? KO.misc : ly.off_diag));
-  float* rsm = reinterpret_cast<float*>(dsc + 32);            // [96] x0, m1, kappa per row
+  // (the generic path stages its per-row shift / mean / slope / Z' scale in dsc itself)
+  float* rsm = reinterpret_cast<float*>(dsc + 32);            // [96] spare
   uint64_t* xbar = reinterpret_cast<uint64_t*>(rsm + 96);     // TMA completion barrier
   float* cvec = rsm + 100;   // generic path, component values: [10][32] (kCompBytes)
   // DEC: fp32 trend of the staged series, trend values X_t' as fp16 hi / lo
@@ -360,7 +361,7 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
       gen_var = warp_sum(i < N ? nu2t + (float)S * (mu_t - gen_mbar) * (mu_t - gen_mbar) : 0.f) *
                 a.inv_ns;
       sx = pow2_scale((warp_max_nonneg(amx) + fabsf(mr)) * rr);
-      sz = pow2_scale(warp_max_nonneg(2.f * dmx + (a.detrend ? fabsf(kap) * a.half_s : 0.f)));
+      sz = 1.f;   // Z' is row-normalised (per-row scale in the descriptor array)
       // per-row shift, mean, slope and Z' scale for the coalesced pass, one float4 per row in
       // the (not yet written) descriptor array.  Row-normalised Gram operand:
       // Z'_i = z_i rr / sqrt(nu2_i rr^2 + eps_s), |Z'_i| <= 1, so the split keeps ~22 bits
@@ -467,7 +468,7 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
       }
       sx = pow2_scale((warp_max_nonneg(amx) + fabsf(mr)) * rr);
       // |e| <= |z| + |kappa| max|t~| <= 2 max|d| + |kappa| (S-1)/2
-      sz = pow2_scale(warp_max_nonneg(2.f * dmx + (a.detrend ? fabsf(kap) * a.half_s : 0.f)));
+      sz = 1.f;   // Z' is row-normalised (per-row scale in the descriptor array)
       // per-row shift, mean, slope and row-normalised Z' scale for the coalesced pass (no
       // shuffles in its lane-divergent loop), one float4 per row in the descriptor array
       dsc[lane] = make_float4(x0, m1, a.detrend ? kap : 0.f,
