@@ -50,6 +50,9 @@ def flops_per_series(N, S, M):
     return 2 * N * N * S + 4 * M * N * N + 2 * M * N * S
 
 
+# inputs up to this size get an L2 flush between timed steps (B200 L2: 126 MB)
+L2_FLUSH_BELOW = 256 << 20
+
 # ------------------------------------------------------------------ clocks (NVML, sampled in a thread)
 class ClockSampler:
     BAD = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
@@ -201,6 +204,8 @@ def main():
     ap.add_argument("--metric-variant", type=int, default=0,
                     help="SURVEY 8(f) f3: bit 0 level-only trend, bit 1 detrended seasonal, "
                          "bit 2 component values")
+    ap.add_argument("--graph", action="store_true",
+                    help="time replays of a CUDA graph of the forward call (launch-bound configs)")
     ap.add_argument("--ma-kernel", type=int, default=0,
                     help="SURVEY 8(f) f3: moving-average decomposition kernel (odd, 0 = off)")
     ap.add_argument("--instance-norm", action="store_true",
@@ -218,15 +223,19 @@ def main():
     B = w.windows
     cfg = {"workload": w.name, "windows": B, "C": w.C, "L": w.L, "S": w.S, "H": w.H, "N": N,
            "M": M, "series_per_step": B * w.C, "head": "per-channel",
-           "l2": f"inputs larger than L2 ({B * w.C * w.L * 4 / 1e9:.2f} GB read per step)",
+           "l2": (f"inputs larger than L2 ({B * w.C * w.L * 4 / 1e9:.2f} GB read per step)"
+                  if B * w.C * w.L * 4 > L2_FLUSH_BELOW else
+                  f"L2 flushed between timed steps (512 MB write; inputs {B * w.C * w.L * 4 / 1e6:.1f}"
+                  f" MB < L2)"),
            "parallelism": f"dp{world}", "seed": args.seed}
     if args.metric_variant or args.instance_norm or args.ma_kernel:
         cfg.update(metric_variant=args.metric_variant, instance_norm=bool(args.instance_norm),
                    ma_kernel=args.ma_kernel)
     if args.sliding:
         cfg.update(input="sliding windows of the [C][T] series (prnet_forward_sliding)",
-                   l2=f"series span {w.C * (B + w.L - 1) * 4 / 1e6:.1f} MB (L2-resident); "
-                      f"outputs {B * w.C * w.H * 4 / 1e9:.2f} GB written per step")
+                   l2=f"series span {w.C * (B + w.L - 1) * 4 / 1e6:.1f} MB < L2: L2 flushed "
+                      f"between timed steps (512 MB write); outputs "
+                      f"{B * w.C * w.H * 4 / 1e9:.2f} GB written per step")
 
     if args.impl == "reference":
         if rank != 0:
@@ -304,14 +313,30 @@ def main():
     for _ in range(args.warmup):
         fwd()
     torch.cuda.synchronize()
+    if args.graph and not args.sliding:
+        # launch-bound workloads (configs[0]): the step is one replay of a captured CUDA graph
+        # of the same prnet_forward call, so host launch overhead leaves the timed region
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            model.forward_into(x, y)
+        graph.replay()
+        torch.cuda.synchronize()
+        fwd = graph.replay
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
+    # inputs smaller than L2 (126 MB): flush it between timed steps (outside the brackets) and
+    # time the steps by their own event pairs
+    flush = None
+    if count * w.C * w.L * 4 <= L2_FLUSH_BELOW or args.sliding:
+        flush = torch.empty(512 << 18, dtype=torch.float32, device=dev)   # 512 MB
     with ClockSampler(dev) as clk:
         t_wall = time.perf_counter()
         for e0, e1 in ev:
+            if flush is not None:
+                flush.zero_()
             e0.record(stream)
             fwd()
             e1.record(stream)
@@ -321,7 +346,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     per_launch = [e0.elapsed_time(e1) for e0, e1 in ev]          # ms, on the launching stream
-    total_ms = ev[0][0].elapsed_time(ev[-1][1])
+    total_ms = ev[0][0].elapsed_time(ev[-1][1]) if flush is None else sum(per_launch)
     tt = torch.tensor([total_ms], dtype=torch.float64, device=coll)
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
