@@ -98,7 +98,10 @@ void pack_flash_head(const float* ws, const float* wt, int Cw, int M, int N, uns
 // NTT = t tiles of 8 per chunk: S <= 48 in one chunk; longer segments (S <= 96) in
 // ly.nch chunks of NTT tiles, the Gram and exponentials recomputed per chunk (the P, Y
 // accumulators of all of S would not fit the register file)
-template <int KS, int NTT, int MMT>
+// COMP: component values (metric_variant bit 2, reading R-f4): P_s = A_s X - (A_s mu) 1^T -
+// d1 (A_s kappa) t~^T and P_t = (A_t mu) 1^T + d0 (A_t kappa) t~^T, from four row sums
+// accumulated with the exponentials (no A_t X product)
+template <int KS, int NTT, int MMT, bool COMP = false>
 __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel(FwdArgs a, FlashLayout ly,
                                                                  int wins_per_cta) {
   extern __shared__ float4 smem4[];
@@ -120,6 +123,8 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
   float* c_mu = c_max + NP;                                     // [NP] mu~ (+inf past N)
   float* c_ka = c_mu + NP;                                      // [NP] kappa~
   float* c_nu = c_ka + NP;                                      // [NP] scratch: mu, nu2
+  float* c_vm = c_nu + NP;                                      // [NP] raw mu (COMP), 0 past N
+  float* c_vk = c_vm + NP;                                      // [NP] raw kappa (COMP)
   float* yred = reinterpret_cast<float*>(smem + ly.off_yred);   // [nwarps][16 MMT][8 NTT]
   float* scr = reinterpret_cast<float*>(smem + ly.off_scr);     // [32]
   float* w1 = scr + 32;   // [32] row sums of W_s + W_t (instance normalisation, see a8)
@@ -137,7 +142,8 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
     const float* gt = a.wt + (int64_t)cw * a.M * N;
     for (int m = tid; m < a.M; m += nthr) {
       float acc = 0.f;
-      for (int n = 0; n < N; n++) acc += __ldg(gs + m * N + n) + __ldg(gt + m * N + n);
+      // (component values: only the trend branch carries the normalised level)
+      for (int n = 0; n < N; n++) acc += (COMP ? 0.f : __ldg(gs + m * N + n)) + __ldg(gt + m * N + n);
       w1[m] = acc;
     }
   }
@@ -232,6 +238,10 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
         }
         c_inv[n] = 1.f;                // column factor of rho: 1 (row-normalised Gram)
         c_max[n] = sqrtf(nu2) * inv;   // f_n: known row maximum of rho (Cauchy-Schwarz)
+        if (COMP) {
+          c_vm[n] = c_mu[n];
+          c_vk[n] = c_ka[n];
+        }
         c_mu[n] = (c_mu[n] - mu_r) * cmt;
         c_ka[n] = c_ka[n] * ckt;
       } else {
@@ -239,6 +249,7 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
         c_max[n] = 0.f;
         c_mu[n] = INFINITY;            // exponent -inf: masked key
         c_ka[n] = 0.f;
+        if (COMP) c_vm[n] = c_vk[n] = 0.f;
       }
     }
     __syncthreads();
@@ -279,6 +290,8 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
 #pragma unroll
         for (int e = 0; e < 4; e++) as_[nt][e] = at_[nt][e] = 0.f;
       float ssum[2] = {0.f, 0.f}, tsum[2] = {0.f, 0.f};
+      // COMP: sum_j E_ij mu_j, E_ij kappa_j for both branches (raw descriptors)
+      float csm[2] = {0.f, 0.f}, csk[2] = {0.f, 0.f}, ctm[2] = {0.f, 0.f}, ctk[2] = {0.f, 0.f};
 
       for (int jt = 0; jt < NT; jt++) {
         // a3: Gram tile (16 query rows x 16 keys)
@@ -308,6 +321,11 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
           const float2 cinv = *reinterpret_cast<const float2*>(c_inv + j);
           const float2 cmu = *reinterpret_cast<const float2*>(c_mu + j);
           const float2 cka = *reinterpret_cast<const float2*>(c_ka + j);
+          float2 vm = f2(0.f), vk = f2(0.f);
+          if (COMP) {
+            vm = *reinterpret_cast<const float2*>(c_vm + j);
+            vk = *reinterpret_cast<const float2*>(c_vk + j);
+          }
 #pragma unroll
           for (int h = 0; h < 2; h++) {
             const float2 u = mul2(make_float2(g[nt][2 * h], g[nt][2 * h + 1]), cinv);
@@ -321,6 +339,12 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
             const float2 et = make_float2(fast_ex2(ea.x), fast_ex2(ea.y));
             ssum[h] += es.x + es.y;
             tsum[h] += et.x + et.y;
+            if (COMP) {
+              csm[h] = fmaf(es.x, vm.x, fmaf(es.y, vm.y, csm[h]));
+              csk[h] = fmaf(es.x, vk.x, fmaf(es.y, vk.y, csk[h]));
+              ctm[h] = fmaf(et.x, vm.x, fmaf(et.y, vm.y, ctm[h]));
+              ctk[h] = fmaf(et.x, vk.x, fmaf(et.y, vk.y, ctk[h]));
+            }
             // A fragment register index: a0 (h0, nt0), a1 (h1, nt0), a2 (h0, nt1), a3 (h1, nt1)
             split2(es, esh[2 * nt + h], esl[2 * nt + h]);
             split2(et, eth[2 * nt + h], etl[2 * nt + h]);
@@ -345,11 +369,11 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
             const int nt = 2 * tp + u2;
             if (nt < NTT) {
               mma16816(as_[nt], esl, xh[2 * u2], xh[2 * u2 + 1]);
-              mma16816(at_[nt], etl, xh[2 * u2], xh[2 * u2 + 1]);
+              if constexpr (!COMP) mma16816(at_[nt], etl, xh[2 * u2], xh[2 * u2 + 1]);
               mma16816(as_[nt], esh, xl[2 * u2], xl[2 * u2 + 1]);
-              mma16816(at_[nt], eth, xl[2 * u2], xl[2 * u2 + 1]);
+              if constexpr (!COMP) mma16816(at_[nt], eth, xl[2 * u2], xl[2 * u2 + 1]);
               mma16816(as_[nt], esh, xh[2 * u2], xh[2 * u2 + 1]);
-              mma16816(at_[nt], eth, xh[2 * u2], xh[2 * u2 + 1]);
+              if constexpr (!COMP) mma16816(at_[nt], eth, xh[2 * u2], xh[2 * u2 + 1]);
             }
           }
         }
@@ -364,6 +388,20 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
         const int ii = 16 * qt + 8 * h + gq;
         ssum[h] = ii < N ? 1.f / ssum[h] : 0.f;
         tsum[h] = ii < N ? 1.f / tsum[h] : 0.f;
+        if (COMP) {
+#pragma unroll
+          for (int o = 1; o <= 2; o <<= 1) {
+            csm[h] += __shfl_xor_sync(0xffffffffu, csm[h], o);
+            csk[h] += __shfl_xor_sync(0xffffffffu, csk[h], o);
+            ctm[h] += __shfl_xor_sync(0xffffffffu, ctm[h], o);
+            ctk[h] += __shfl_xor_sync(0xffffffffu, ctk[h], o);
+          }
+          // in the X' = x sx units of the accumulators; d1 = bit 1, d0 = 1 - bit 0
+          csm[h] *= ssum[h] * sx;
+          csk[h] *= ssum[h] * sx * (a.detrend ? 1.f : 0.f);
+          ctm[h] *= tsum[h] * sx;
+          ctk[h] *= tsum[h] * sx * (a.vtrend != 0.f ? 1.f : 0.f);
+        }
       }
       // a7: P fragments -> B operand (k = i, n = t) via movmatrix; Y += W'_s P_s + W'_t P_t
       uint32_t psh[NTT][2], psl[NTT][2], pth[NTT][2], ptl[NTT][2];
@@ -372,10 +410,18 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           uint32_t hi, lo;
-          split2(mul2(make_float2(as_[nt][2 * h], as_[nt][2 * h + 1]), f2(ssum[h])), hi, lo);
+          float2 ps = mul2(make_float2(as_[nt][2 * h], as_[nt][2 * h + 1]), f2(ssum[h]));
+          float2 pt = mul2(make_float2(at_[nt][2 * h], at_[nt][2 * h + 1]), f2(tsum[h]));
+          if (COMP) {   // component values: subtract / substitute the rank-2 parts
+            const float t0 = (float)(8 * (tb + nt) + 2 * cq) - half_s;
+            const float2 tt = make_float2(t0, t0 + 1.f);
+            ps = add2(ps, make_float2(-fmaf(csk[h], tt.x, csm[h]), -fmaf(csk[h], tt.y, csm[h])));
+            pt = make_float2(fmaf(ctk[h], tt.x, ctm[h]), fmaf(ctk[h], tt.y, ctm[h]));
+          }
+          split2(ps, hi, lo);
           psh[nt][h] = movm_t(hi);
           psl[nt][h] = movm_t(lo);
-          split2(mul2(make_float2(at_[nt][2 * h], at_[nt][2 * h + 1]), f2(tsum[h])), hi, lo);
+          split2(pt, hi, lo);
           pth[nt][h] = movm_t(hi);
           ptl[nt][h] = movm_t(lo);
         }
@@ -457,7 +503,7 @@ bool plan_flash_kernel(const FwdArgs& a, int max_smem_optin, FlashPlan* p) {
   off += ly.npad * ly.xph * 2;
   off = (off + 15) & ~15;
   ly.off_col = off;
-  off += 5 * ly.npad * 4;
+  off += 7 * ly.npad * 4;   // c_inv, c_max, c_mu, c_ka, c_nu, c_vm, c_vk
   off = (off + 15) & ~15;
   ly.off_yred = off;
   // one warp per 16-row query tile, up to 8: short series (N <= 64) run 4-warp CTAs so
@@ -474,9 +520,9 @@ bool plan_flash_kernel(const FwdArgs& a, int max_smem_optin, FlashPlan* p) {
   return true;
 }
 
-template <int KS, int NTT, int MMT>
+template <int KS, int NTT, int MMT, bool COMP>
 static cudaError_t launch_flash_t(const FwdArgs& a, const FlashPlan& p, cudaStream_t st) {
-  auto k = prnet_fwd_flash_kernel<KS, NTT, MMT>;
+  auto k = prnet_fwd_flash_kernel<KS, NTT, MMT, COMP>;
   cudaError_t e =
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
@@ -487,7 +533,11 @@ static cudaError_t launch_flash_t(const FwdArgs& a, const FlashPlan& p, cudaStre
 
 template <int KS, int NTT>
 static cudaError_t launch_flash_m(const FwdArgs& a, const FlashPlan& p, cudaStream_t st) {
-  return p.mmt == 1 ? launch_flash_t<KS, NTT, 1>(a, p, st) : launch_flash_t<KS, NTT, 2>(a, p, st);
+  if (a.comp)
+    return p.mmt == 1 ? launch_flash_t<KS, NTT, 1, true>(a, p, st)
+                      : launch_flash_t<KS, NTT, 2, true>(a, p, st);
+  return p.mmt == 1 ? launch_flash_t<KS, NTT, 1, false>(a, p, st)
+                    : launch_flash_t<KS, NTT, 2, false>(a, p, st);
 }
 
 cudaError_t launch_flash_kernel(const FwdArgs& a, const FlashPlan& p, cudaStream_t st) {

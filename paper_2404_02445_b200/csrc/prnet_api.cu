@@ -161,18 +161,19 @@ bool tcq_applicable(const prnet_handle* h) {
 bool widening_on(const prnet_handle* h) {
   return (h->cfg.metric_variant & 6) != 0 || h->cfg.instance_norm != 0 || h->cfg.ma_kernel > 0;
 }
-// component values and the moving-average decomposition: mma_f16x3's generic path only
+// component values: mma_f16x3 and flash_f16x3; the moving-average decomposition: mma_f16x3
 bool comp_on(const prnet_handle* h) {
   return (h->cfg.metric_variant & 4) != 0 || h->cfg.ma_kernel > 0;
 }
 bool variant_supports_widening(const prnet_handle* h, int v) {
-  if (comp_on(h)) return v == 2;
+  if (h->cfg.ma_kernel > 0) return v == 2;
+  if (comp_on(h)) return v == 2 || v == 5;
   return v == 2 || v == 5 || v == 6;
 }
 const char* kWideningMsg =
     "metric_variant bit 1 / instance_norm need tc_quad, mma_f16x3 (N <= 32) or flash_f16x3 "
-    "(16 < N <= 512, S <= 96, M <= 32); metric_variant bit 2 and ma_kernel need mma_f16x3 "
-    "(N <= 32, M <= 32, S <= 128)";
+    "(16 < N <= 512, S <= 96, M <= 32); metric_variant bit 2 needs mma_f16x3 (N <= 32, "
+    "M <= 32, S <= 128) or flash_f16x3; ma_kernel needs mma_f16x3";
 // 7 = small_f32 (N <= 16, S <= 128, M <= 32: lanes over time, FP32)
 bool small_applicable(const prnet_handle* h) {
   return h->N <= 16 && h->cfg.seg_len <= 128 && h->M <= 32;
@@ -180,7 +181,10 @@ bool small_applicable(const prnet_handle* h) {
 int pick_variant(const prnet_handle* h) {
   if (h->forced_variant >= 0) return h->forced_variant;
   if (widening_on(h)) {
-    if (comp_on(h)) return h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128 ? 2 : -1;
+    if (comp_on(h)) {
+      if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
+      return h->cfg.ma_kernel == 0 && flash_applicable(h) ? 5 : -1;
+    }
     if (tcq_applicable(h) && h->N > 16) return 6;
     if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
     if (flash_applicable(h)) return 5;

@@ -361,9 +361,12 @@ def test_widening_parity_long_lookback(oracle_mod, L, S, H, mv, rev):
 @pytest.mark.parametrize("mv,rev", [(4, False), (5, False), (6, False), (7, False), (4, True),
                                     (7, True)])
 @pytest.mark.parametrize("L,S,H", [(720, 24, 720), (720, 24, 336), (100, 24, 90), (96, 24, 96),
-                                   (97, 7, 13), (128, 8, 64), (270, 9, 31), (384, 128, 200)])
+                                   (97, 7, 13), (128, 8, 64), (270, 9, 31), (384, 128, 200),
+                                   (1440, 24, 96), (1536, 12, 200), (2880, 48, 96),
+                                   (3840, 96, 96), (5760, 12, 96)])
 def test_component_values_parity(oracle_mod, L, S, H, mv, rev):
-    """metric_variant bit 2 (component values, reading R-f4): mma_f16x3's generic path."""
+    """metric_variant bit 2 (component values, reading R-f4): mma_f16x3 (N <= 32), the
+    flash_f16x3 COMP instantiation (N > 32)."""
     x = synth.random_windows(3, 5, L, kind="mixed")
     _check_widening(oracle_mod, x, S, H, mv, rev)
 
@@ -407,17 +410,18 @@ def test_ma_decomposition_attention_dump():
 
 
 def test_component_values_unsupported_paths():
-    m = PRNet(3, 1440, 24, 96, metric_variant=4)        # N = 60: only mma_f16x3 has bit 2
+    m = PRNet(3, 1440, 24, 96, ma_kernel=5)             # N = 60: the decomposition is N <= 32
     m.load(np.zeros((3, m.M, m.N)), np.zeros((3, m.M, m.N)), np.zeros((3, 96)))
     with pytest.raises(PrnetError) as e:
         m.forward(torch.zeros((2, 3, 1440), device="cuda"))
     assert e.value.status == 3
     m2 = PRNet(3, 720, 24, 96, metric_variant=4)
-    for v in ("tc_quad", "flash_f16x3", "small_f32", "warp_f32"):
+    for v in ("tc_quad", "small_f32", "warp_f32"):
         with pytest.raises(PrnetError) as e:
             m2.set_variant(v)
         assert e.value.status == 3
     m2.set_variant("mma_f16x3")
+    m2.set_variant("flash_f16x3")
 
 
 def test_widening_unsupported_paths():
