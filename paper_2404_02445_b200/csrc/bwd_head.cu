@@ -30,7 +30,7 @@ __device__ __forceinline__ float shfl(float v, int src) {
 // a row of all segments at one t is NP/4 broadcast float4 loads, and lane i's own element
 // at t is conflict-free.
 template <int NP, int MP>
-__global__ void __launch_bounds__(256) prnet_bwd_head_kernel(FwdArgs a, const float* __restrict__ dy,
+__global__ void __launch_bounds__(384, 1) prnet_bwd_head_kernel(FwdArgs a, const float* __restrict__ dy,
                                                           float* __restrict__ part,
                                                           BwdLayout ly) {
   extern __shared__ float4 smem4[];
@@ -238,11 +238,11 @@ bool plan_bwd_head(const FwdArgs& a, int max_smem_optin, BwdPlan* p) {
   ly.off_dy = (xz + 3) & ~3;
   ly.off_db = (ly.off_dy + a.S * ly.mp + 3) & ~3;
   ly.per_warp = (ly.off_db + a.H + 3) & ~3;
-  int w = 8;
+  int w = 12;
   while (w > 1 && (size_t)w * ly.per_warp * 4 > (size_t)max_smem_optin) w--;
   if ((size_t)w * ly.per_warp * 4 > (size_t)max_smem_optin) return false;
   p->warps = w;
-  ly.wins_per_cta = 32 * w;
+  ly.wins_per_cta = 256;   // ~21 series per warp at 12 warps
   p->nblk = (int)((a.B + ly.wins_per_cta - 1) / ly.wins_per_cta);
   p->smem_bytes = (size_t)w * ly.per_warp * 4;
   p->elems = 2 * a.M * a.N + a.H;
