@@ -185,7 +185,9 @@ int pick_variant(const prnet_handle* h) {
       if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
       return h->cfg.ma_kernel == 0 && flash_applicable(h) ? 5 : -1;
     }
-    if (tcq_applicable(h) && h->N > 16) return 6;
+    // (widened, the generic mma_f16x3 path is slower than tc_quad's WIDE instantiation from
+    // N = 14 on: stress L336/S24 0.278 vs 0.259 ms; equal at N = 8)
+    if (tcq_applicable(h) && h->N > 8) return 6;
     if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
     if (flash_applicable(h)) return 5;
     return -1;   // no kernel implements it for this shape
