@@ -203,6 +203,7 @@ prnet_status prnet_backward_head(prnet_handle* h, const float* x, int64_t batch,
  * All variants compute the same reading to within the documented tolerance:
  *   0 = warp_f32     one warp per series, CUDA-core FP32                  (N <= 32)
  *   1 = long_f32     one CTA per series, rows streamed, FP32              (N <= 512)
+ *                    [auto: N > 32 when flash_f16x3 does not apply]
  *   2 = mma_f16x3    one warp per series, mma.sync m16n8k16 with split-fp16
  *                    hi/lo operands, 3 products, fp32 accumulation
  *                    (N <= 32, M <= 32, S <= 128)  [auto: N <= 32 unless 6, 7 apply]

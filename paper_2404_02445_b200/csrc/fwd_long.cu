@@ -51,25 +51,32 @@ __global__ void __launch_bounds__(256) prnet_fwd_long_kernel(FwdArgs a, int rs) 
     for (int k = lane; k < MS; k += 32) yw[warp * MS + k] = 0.f;
     __syncthreads();
 
-    // ---- a2: descriptors, one thread per segment (shifted by the first value)
+    // ---- a2: descriptors, one thread per segment (shifted by the first value); with
+    // metric_variant bit 1 the seasonal rows are the residuals e = z - kappa t~ (R-f3)
     for (int n = threadIdx.x; n < N; n += blockDim.x) {
       const float* row = xr + n * rs;
       const float x0 = row[0];
-      float s = 0.f;
-      for (int t = 0; t < S; t++) s += row[t] - x0;
-      const float m1 = s * a.inv_s;
-      float nu2 = 0.f, kap = 0.f;
+      float s = 0.f, s3 = 0.f;
       for (int t = 0; t < S; t++) {
-        const float z = (row[t] - x0) - m1;
+        const float d = row[t] - x0;
+        s += d;
+        s3 = fmaf((float)t - a.half_s, d, s3);
+      }
+      const float m1 = s * a.inv_s;
+      const float kap = s3 * a.inv_v;
+      const float kd = a.detrend ? kap : 0.f;
+      float nu2 = 0.f;
+      for (int t = 0; t < S; t++) {
+        const float z = fmaf(-kd, (float)t - a.half_s, (row[t] - x0) - m1);
         nu2 = fmaf(z, z, nu2);
-        kap = fmaf((float)t - a.half_s, z, kap);
         zr[n * rs + t] = z;
       }
       muS[n] = x0 + m1;
-      kapS[n] = kap * a.inv_v;
-      invS[n] = rsqrtf(nu2 + kEpsSeasonal);
-      // stash nu2 for sigma^2 in the wrow scratch (free until phase 2)
-      wrow[n] = nu2;
+      kapS[n] = kap;
+      invS[n] = nu2;   // seasonal |z|^2 (|e|^2); the normaliser follows the RevIN scale below
+      // |z|^2 for sigma^2 (= |e|^2 + kappa^2 V when detrended) in the wrow scratch (free until
+      // phase 2)
+      wrow[n] = a.detrend ? fmaf(kap * kap, 1.f / a.inv_v, nu2) : nu2;
     }
     __syncthreads();
     // sigma^2: fixed-order block reduction (deterministic)
@@ -92,8 +99,21 @@ __global__ void __launch_bounds__(256) prnet_fwd_long_kernel(FwdArgs a, int rs) 
     __syncthreads();
     float sig = 0.f;
     for (int w = 0; w < nwarps; w++) sig += red[32 + w];
-    const float inv_var = 1.0f / (sig * a.inv_ns + kEpsTrend);
+    // instance normalisation (R-f1): every descriptor of xhat = (x - mr) rr is an affine image
+    // of the one of x; the patterns are mapped back in a6 (P - mr) and a8 adds sr b + mr
+    float mr = 0.f, rr = 1.f, sr = 1.f;
+    if (a.revin) {
+      const float vr = sig * a.inv_ns;
+      mr = mbar;
+      rr = rsqrtf(vr + kEpsRevin);
+      sr = (vr + kEpsRevin) * rr;
+    }
+    // trend: D^ of xhat = rr^2 D / (var rr^2 + eps_t)
+    const float inv_var = rr * rr / fmaf(sig * a.inv_ns * rr, rr, kEpsTrend);
     __syncthreads();  // wrow scratch is reused below
+    for (int n = threadIdx.x; n < N; n += blockDim.x)
+      invS[n] = rsqrtf(invS[n] * rr * rr + kEpsSeasonal) * rr;   // rho of xhat
+    __syncthreads();
 
     // ---- a3..a7 streamed over query rows
     float* wr = wrow + warp * 2 * N;
@@ -141,7 +161,7 @@ __global__ void __launch_bounds__(256) prnet_fwd_long_kernel(FwdArgs a, int rs) 
         float v = -INFINITY;
         if (j < N) {
           const float dm = mu_i - muS[j], dk = k_i - kapS[j];
-          v = -(fmaf(a.vtrend * dk, dk, dm * dm) * inv_var);
+          v = -(fmaf(a.vtrend * dk, dk, dm * dm) * inv_var);   // kapS: slope (x units)
         }
         g[k] = v;
         mx = fmaxf(mx, v);
@@ -169,6 +189,8 @@ __global__ void __launch_bounds__(256) prnet_fwd_long_kernel(FwdArgs a, int rs) 
           ps = fmaf(wr[j], xv, ps);
           pt = fmaf(wr[N + j], xv, pt);
         }
+        ps -= mr;   // RevIN: rows of A sum to 1, so A xhat = rr (A x - mr); rr sr = 1
+        pt -= mr;
         float* yr = yw + warp * MS + t;
         for (int m = 0; m < M; m++)
           yr[m * S] = fmaf(__ldg(gws + m * N + i), ps, fmaf(__ldg(gwt + m * N + i), pt, yr[m * S]));
@@ -182,7 +204,7 @@ __global__ void __launch_bounds__(256) prnet_fwd_long_kernel(FwdArgs a, int rs) 
     for (int h = threadIdx.x; h < H; h += blockDim.x) {
       float v = 0.f;
       for (int w = 0; w < nwarps; w++) v += yw[w * MS + h];
-      yg[h] = v + gb[h];
+      yg[h] = v + fmaf(gb[h], sr, mr);
     }
     __syncthreads();
   }

@@ -351,11 +351,20 @@ def test_level_trend_every_variant(oracle_mod, variant):
 
 @pytest.mark.parametrize("mv,rev", [(2, False), (0, True), (3, True)])
 @pytest.mark.parametrize("L,S,H", [(1440, 24, 96), (1536, 12, 200), (2880, 48, 96),
-                                   (3840, 96, 96), (3250, 65, 130)])
+                                   (3840, 96, 96), (3250, 65, 130), (4000, 120, 100),
+                                   (5000, 100, 1100)])
 def test_widening_parity_long_lookback(oracle_mod, L, S, H, mv, rev):
-    """N > 32: the flash kernel implements the widening."""
+    """N > 32: the flash kernel implements the widening (S <= 96), long_f32 beyond."""
     x = synth.random_windows(2, 3, L, kind="mixed")
     _check_widening(oracle_mod, x, S, H, mv, rev)
+
+
+@pytest.mark.parametrize("mv,rev", [(1, False), (2, False), (3, True), (0, True)])
+@pytest.mark.parametrize("L,S,H", [(1440, 24, 96), (1536, 12, 200), (97, 7, 13)])
+def test_widening_parity_long_f32(oracle_mod, L, S, H, mv, rev):
+    """The FP32 row-streaming kernel under every detrend / RevIN flag (forced)."""
+    x = synth.random_windows(2, 3, L, kind="mixed")
+    _check_widening(oracle_mod, x, S, H, mv, rev, variant="long_f32")
 
 
 @pytest.mark.parametrize("mv,rev", [(4, False), (5, False), (6, False), (7, False), (4, True),
