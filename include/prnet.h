@@ -76,7 +76,8 @@ typedef struct {
                                        line mu_n + kappa_n t~ (bit 0: the level mu_n)
                                        instead of the raw segments; N <= 32, M <= 32,
                                        S <= 128 (mma_f16x3) or 16 < N <= 512, S <= 96
-                                       (flash_f16x3).  Values > 7 invalid.               */
+                                       (flash_f16x3) or N <= 512 (long_f32).  Values > 7
+                                       invalid.                                          */
   float tau_seasonal;       /* tau_s > 0: softmax temperature of the seasonal branch (A6) */
   float tau_trend;          /* tau_t > 0: softmax temperature of the trend branch (A6)    */
   int32_t device;           /* CUDA device ordinal the handle is bound to                 */

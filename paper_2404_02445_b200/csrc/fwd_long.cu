@@ -181,6 +181,20 @@ __global__ void __launch_bounds__(256) prnet_fwd_long_kernel(FwdArgs a, int rs) 
         if (j < N) wr[N + j] = g[k] * rsum;
       }
       __syncwarp();
+      // component values (metric_variant bit 2, R-f4): row sums A mu, A kappa of both branches
+      float asm_ = 0.f, ask = 0.f, atm = 0.f, atk = 0.f;
+      if (a.comp) {
+        for (int j = lane; j < N; j += 32) {
+          asm_ = fmaf(wr[j], muS[j], asm_);
+          ask = fmaf(wr[j], kapS[j], ask);
+          atm = fmaf(wr[N + j], muS[j], atm);
+          atk = fmaf(wr[N + j], kapS[j], atk);
+        }
+        asm_ = warp_sum(asm_);
+        ask = warp_sum(ask) * (a.detrend ? 1.f : 0.f);
+        atm = warp_sum(atm);
+        atk = warp_sum(atk) * (a.vtrend != 0.f ? 1.f : 0.f);
+      }
       // a6: P_s[i][t], P_t[i][t] by lane t; a7: fold row i into Y
       for (int t = lane; t < S; t += 32) {
         float ps = 0.f, pt = 0.f;
@@ -188,6 +202,13 @@ __global__ void __launch_bounds__(256) prnet_fwd_long_kernel(FwdArgs a, int rs) 
           const float xv = xr[j * rs + t];
           ps = fmaf(wr[j], xv, ps);
           pt = fmaf(wr[N + j], xv, pt);
+        }
+        if (a.comp) {
+          // P_s = A (x - mu - d1 kappa t~) carries no level; P_t = A (mu + d0 kappa t~) the
+          // level (its RevIN shift below)
+          const float tt = (float)t - a.half_s;
+          ps = ps - fmaf(ask, tt, asm_) + mr;
+          pt = fmaf(atk, tt, atm);
         }
         ps -= mr;   // RevIN: rows of A sum to 1, so A xhat = rr (A x - mr); rr sr = 1
         pt -= mr;

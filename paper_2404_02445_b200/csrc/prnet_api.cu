@@ -167,14 +167,14 @@ bool comp_on(const prnet_handle* h) {
 }
 bool variant_supports_widening(const prnet_handle* h, int v) {
   if (h->cfg.ma_kernel > 0) return v == 2;
-  if (comp_on(h)) return v == 2 || v == 5;
+  if (comp_on(h)) return v == 1 || v == 2 || v == 5;
   return v == 1 || v == 2 || v == 5 || v == 6;
 }
 const char* kWideningMsg =
     "metric_variant bit 1 / instance_norm need tc_quad, mma_f16x3 (N <= 32) or flash_f16x3 "
     "(16 < N <= 512, S <= 96, M <= 32) or long_f32 (N <= 512); metric_variant bit 2 needs "
-    "mma_f16x3 (N <= 32, "
-    "M <= 32, S <= 128) or flash_f16x3; ma_kernel needs mma_f16x3";
+    "mma_f16x3 (N <= 32, M <= 32, S <= 128), flash_f16x3 or long_f32; ma_kernel needs "
+    "mma_f16x3";
 // 7 = small_f32 (N <= 16, S <= 128, M <= 32: lanes over time, FP32)
 bool small_applicable(const prnet_handle* h) {
   return h->N <= 16 && h->cfg.seg_len <= 128 && h->M <= 32;
@@ -184,14 +184,15 @@ int pick_variant(const prnet_handle* h) {
   if (widening_on(h)) {
     if (comp_on(h)) {
       if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
-      return h->cfg.ma_kernel == 0 && flash_applicable(h) ? 5 : -1;
+      if (h->cfg.ma_kernel == 0 && flash_applicable(h)) return 5;
+      return h->cfg.ma_kernel == 0 && h->N > 32 ? 1 : -1;
     }
     // (widened, the generic mma_f16x3 path is slower than tc_quad's WIDE instantiation from
     // N = 14 on: stress L336/S24 0.278 vs 0.259 ms; equal at N = 8)
     if (tcq_applicable(h) && h->N > 8) return 6;
     if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
     if (flash_applicable(h)) return 5;
-    if (!comp_on(h) && h->N > 32) return 1;   // long_f32 (N <= 512; S > 96 or M > 32)
+    if (h->cfg.ma_kernel == 0 && h->N > 32) return 1;   // long_f32 (N <= 512; S > 96 or M > 32)
     return -1;   // no kernel implements it for this shape
   }
   // measured on B200 (profiles/README.md): small_f32 is the fastest N <= 8 path (stress

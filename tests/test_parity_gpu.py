@@ -359,10 +359,11 @@ def test_widening_parity_long_lookback(oracle_mod, L, S, H, mv, rev):
     _check_widening(oracle_mod, x, S, H, mv, rev)
 
 
-@pytest.mark.parametrize("mv,rev", [(1, False), (2, False), (3, True), (0, True)])
+@pytest.mark.parametrize("mv,rev", [(1, False), (2, False), (3, True), (0, True), (4, False),
+                                    (5, True), (6, False), (7, True)])
 @pytest.mark.parametrize("L,S,H", [(1440, 24, 96), (1536, 12, 200), (97, 7, 13)])
 def test_widening_parity_long_f32(oracle_mod, L, S, H, mv, rev):
-    """The FP32 row-streaming kernel under every detrend / RevIN flag (forced)."""
+    """The FP32 row-streaming kernel under every detrend / RevIN / component flag (forced)."""
     x = synth.random_windows(2, 3, L, kind="mixed")
     _check_widening(oracle_mod, x, S, H, mv, rev, variant="long_f32")
 
@@ -372,7 +373,7 @@ def test_widening_parity_long_f32(oracle_mod, L, S, H, mv, rev):
 @pytest.mark.parametrize("L,S,H", [(720, 24, 720), (720, 24, 336), (100, 24, 90), (96, 24, 96),
                                    (97, 7, 13), (128, 8, 64), (270, 9, 31), (384, 128, 200),
                                    (1440, 24, 96), (1536, 12, 200), (2880, 48, 96),
-                                   (3840, 96, 96), (5760, 12, 96)])
+                                   (3840, 96, 96), (5760, 12, 96), (4000, 120, 100)])
 def test_component_values_parity(oracle_mod, L, S, H, mv, rev):
     """metric_variant bit 2 (component values, reading R-f4): mma_f16x3 (N <= 32), the
     flash_f16x3 COMP instantiation (N > 32)."""
