@@ -92,7 +92,8 @@ typedef struct {
                                after instance_norm): the seasonal branch (Def 3-4, 6, 9)
                                runs on x - MA_k(x), the trend branch (Def 3-5, 7, 9) on
                                MA_k(x) (R-f5).  N <= 32, M <= 32, S <= 128
-                               (mma_f16x3); other shapes: PRNET_ERR_UNSUPPORTED           */
+                               (mma_f16x3) or 32 < N <= 512 (long_f32); other shapes:
+                               PRNET_ERR_UNSUPPORTED                                      */
 } prnet_config;
 
 /* Create a handle: validates cfg, checks the device is compute capability 10.x,

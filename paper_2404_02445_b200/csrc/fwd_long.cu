@@ -34,6 +34,10 @@ __global__ void __launch_bounds__(256) prnet_fwd_long_kernel(FwdArgs a, int rs) 
   float* red = invS + N;          // [64]     block reduction scratch
   float* wrow = red + 64;         // [nwarps][2][N]  softmax rows
   float* yw = wrow + nwarps * 2 * N;  // [nwarps][M*S] per-warp head accumulators
+  float* muZ = yw + nwarps * MS;      // [N] seasonal-branch level (= muS unless ma_kernel)
+  float* kapZ = muZ + N;              // [N] seasonal-branch slope
+  float* trr = kapZ + N;              // [N][rs] trend rows (ma_kernel only)
+  const bool dec = a.ma_k > 0;
 
   const int64_t total = a.B * (int64_t)C;
   for (int64_t series = blockIdx.x; series < total; series += gridDim.x) {
@@ -50,6 +54,53 @@ __global__ void __launch_bounds__(256) prnet_fwd_long_kernel(FwdArgs a, int rs) 
     }
     for (int k = lane; k < MS; k += 32) yw[warp * MS + k] = 0.f;
     __syncthreads();
+    // ma_kernel (R-f5): trend = moving average of the N S segmented points (ends repeated),
+    // thread-chunked running sums; RevIN statistics of the raw points; then xr holds the
+    // seasonal rows x - trend and trr the trend rows
+    float dec_mr = 0.f, dec_var = 0.f;
+    if (dec) {
+      const int NS = N * S, hk = (a.ma_k - 1) >> 1;
+      auto xat = [&](int q) {
+        q = q < 0 ? 0 : (q > NS - 1 ? NS - 1 : q);
+        const int n = q / S;
+        return xr[n * rs + (q - n * S)];
+      };
+      const int cnk = (NS + blockDim.x - 1) / blockDim.x;
+      const int i0 = threadIdx.x * cnk, i1 = min(i0 + cnk, NS);
+      if (i0 < i1) {
+        float sacc = 0.f;
+        for (int d = -hk; d <= hk; d++) sacc += xat(i0 + d);
+        for (int q = i0; q < i1; q++) {
+          if (q > i0) sacc += xat(q + hk) - xat(q - 1 - hk);
+          const int n = q / S;
+          trr[n * rs + (q - n * S)] = sacc * a.ma_inv;
+        }
+      }
+      float ps = 0.f;
+      for (int q = threadIdx.x; q < NS; q += blockDim.x) ps += xat(q);
+      ps = warp_sum(ps);
+      if (lane == 0) red[warp] = ps;
+      __syncthreads();
+      for (int w = 0; w < nwarps; w++) dec_mr += red[w];
+      dec_mr *= a.inv_ns;
+      __syncthreads();
+      ps = 0.f;
+      for (int q = threadIdx.x; q < NS; q += blockDim.x) {
+        const float d = xat(q) - dec_mr;
+        ps = fmaf(d, d, ps);
+      }
+      ps = warp_sum(ps);
+      if (lane == 0) red[warp] = ps;
+      __syncthreads();
+      for (int w = 0; w < nwarps; w++) dec_var += red[w];
+      dec_var *= a.inv_ns;
+      __syncthreads();
+      for (int q = threadIdx.x; q < NS; q += blockDim.x) {
+        const int n = q / S, o = n * rs + (q - n * S);
+        xr[o] -= trr[o];
+      }
+      __syncthreads();
+    }
 
     // ---- a2: descriptors, one thread per segment (shifted by the first value); with
     // metric_variant bit 1 the seasonal rows are the residuals e = z - kappa t~ (R-f3)
@@ -71,12 +122,34 @@ __global__ void __launch_bounds__(256) prnet_fwd_long_kernel(FwdArgs a, int rs) 
         nu2 = fmaf(z, z, nu2);
         zr[n * rs + t] = z;
       }
-      muS[n] = x0 + m1;
-      kapS[n] = kap;
+      muZ[n] = x0 + m1;
+      kapZ[n] = kap;
       invS[n] = nu2;   // seasonal |z|^2 (|e|^2); the normaliser follows the RevIN scale below
-      // |z|^2 for sigma^2 (= |e|^2 + kappa^2 V when detrended) in the wrow scratch (free until
-      // phase 2)
-      wrow[n] = a.detrend ? fmaf(kap * kap, 1.f / a.inv_v, nu2) : nu2;
+      if (!dec) {
+        muS[n] = x0 + m1;
+        kapS[n] = kap;
+        // |z|^2 for sigma^2 (= |e|^2 + kappa^2 V when detrended) in the wrow scratch (free
+        // until phase 2)
+        wrow[n] = a.detrend ? fmaf(kap * kap, 1.f / a.inv_v, nu2) : nu2;
+      } else {   // trend branch: the trend row's level, slope and |z|^2 (sigma^2)
+        const float* tr = trr + n * rs;
+        const float y0 = tr[0];
+        float st = 0.f, st3 = 0.f;
+        for (int t = 0; t < S; t++) {
+          const float d = tr[t] - y0;
+          st += d;
+          st3 = fmaf((float)t - a.half_s, d, st3);
+        }
+        const float mt1 = st * a.inv_s;
+        float q2 = 0.f;
+        for (int t = 0; t < S; t++) {
+          const float z = (tr[t] - y0) - mt1;
+          q2 = fmaf(z, z, q2);
+        }
+        muS[n] = y0 + mt1;
+        kapS[n] = st3 * a.inv_v;
+        wrow[n] = q2;
+      }
     }
     __syncthreads();
     // sigma^2: fixed-order block reduction (deterministic)
@@ -103,8 +176,8 @@ __global__ void __launch_bounds__(256) prnet_fwd_long_kernel(FwdArgs a, int rs) 
     // of the one of x; the patterns are mapped back in a6 (P - mr) and a8 adds sr b + mr
     float mr = 0.f, rr = 1.f, sr = 1.f;
     if (a.revin) {
-      const float vr = sig * a.inv_ns;
-      mr = mbar;
+      const float vr = dec ? dec_var : sig * a.inv_ns;   // of the raw segmented points
+      mr = dec ? dec_mr : mbar;
       rr = rsqrtf(vr + kEpsRevin);
       sr = (vr + kEpsRevin) * rr;
     }
@@ -185,8 +258,8 @@ __global__ void __launch_bounds__(256) prnet_fwd_long_kernel(FwdArgs a, int rs) 
       float asm_ = 0.f, ask = 0.f, atm = 0.f, atk = 0.f;
       if (a.comp) {
         for (int j = lane; j < N; j += 32) {
-          asm_ = fmaf(wr[j], muS[j], asm_);
-          ask = fmaf(wr[j], kapS[j], ask);
+          asm_ = fmaf(wr[j], muZ[j], asm_);
+          ask = fmaf(wr[j], kapZ[j], ask);
           atm = fmaf(wr[N + j], muS[j], atm);
           atk = fmaf(wr[N + j], kapS[j], atk);
         }
@@ -198,19 +271,21 @@ __global__ void __launch_bounds__(256) prnet_fwd_long_kernel(FwdArgs a, int rs) 
       // a6: P_s[i][t], P_t[i][t] by lane t; a7: fold row i into Y
       for (int t = lane; t < S; t += 32) {
         float ps = 0.f, pt = 0.f;
+        const float* tx = dec ? trr : xr;   // trend-branch rows
         for (int j = 0; j < N; j++) {
-          const float xv = xr[j * rs + t];
-          ps = fmaf(wr[j], xv, ps);
-          pt = fmaf(wr[N + j], xv, pt);
+          ps = fmaf(wr[j], xr[j * rs + t], ps);
+          pt = fmaf(wr[N + j], tx[j * rs + t], pt);
         }
         if (a.comp) {
-          // P_s = A (x - mu - d1 kappa t~) carries no level; P_t = A (mu + d0 kappa t~) the
-          // level (its RevIN shift below)
+          // P_s = A (x - mu - d1 kappa t~), P_t = A (mu + d0 kappa t~)
           const float tt = (float)t - a.half_s;
-          ps = ps - fmaf(ask, tt, asm_) + mr;
+          ps = ps - fmaf(ask, tt, asm_);
           pt = fmaf(atk, tt, atm);
         }
-        ps -= mr;   // RevIN: rows of A sum to 1, so A xhat = rr (A x - mr); rr sr = 1
+        // RevIN: rows of A sum to 1, so A xhat = rr (A x - mr) (rr sr = 1); only the branches
+        // that carry the level (both for the raw reading, the trend one for component values
+        // or the decomposition) shift by mr
+        if (!(a.comp || dec)) ps -= mr;
         pt -= mr;
         float* yr = yw + warp * MS + t;
         for (int m = 0; m < M; m++)
@@ -237,7 +312,8 @@ bool plan_long_kernel(const FwdArgs& a, int max_smem_optin, int sm_count, LongPl
   p->rs = a.S | 1;
   p->warps_per_cta = 8;
   const size_t floats = (size_t)2 * a.N * p->rs + 3 * a.N + 64 +
-                        (size_t)p->warps_per_cta * (2 * a.N + a.M * a.S);
+                        (size_t)p->warps_per_cta * (2 * a.N + a.M * a.S) + 2 * a.N +
+                        (a.ma_k > 0 ? (size_t)a.N * p->rs : 0);
   p->smem_bytes = floats * sizeof(float);
   if (p->smem_bytes > (size_t)max_smem_optin) return false;
   const int64_t total = a.B * (int64_t)a.C;

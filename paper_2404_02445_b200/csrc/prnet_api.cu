@@ -161,12 +161,13 @@ bool tcq_applicable(const prnet_handle* h) {
 bool widening_on(const prnet_handle* h) {
   return (h->cfg.metric_variant & 6) != 0 || h->cfg.instance_norm != 0 || h->cfg.ma_kernel > 0;
 }
-// component values: mma_f16x3 and flash_f16x3; the moving-average decomposition: mma_f16x3
+// component values: mma_f16x3, flash_f16x3, long_f32; the moving-average decomposition:
+// mma_f16x3 (N <= 32), long_f32
 bool comp_on(const prnet_handle* h) {
   return (h->cfg.metric_variant & 4) != 0 || h->cfg.ma_kernel > 0;
 }
 bool variant_supports_widening(const prnet_handle* h, int v) {
-  if (h->cfg.ma_kernel > 0) return v == 2;
+  if (h->cfg.ma_kernel > 0) return v == 1 || v == 2;
   if (comp_on(h)) return v == 1 || v == 2 || v == 5;
   return v == 1 || v == 2 || v == 5 || v == 6;
 }
@@ -174,7 +175,7 @@ const char* kWideningMsg =
     "metric_variant bit 1 / instance_norm need tc_quad, mma_f16x3 (N <= 32) or flash_f16x3 "
     "(16 < N <= 512, S <= 96, M <= 32) or long_f32 (N <= 512); metric_variant bit 2 needs "
     "mma_f16x3 (N <= 32, M <= 32, S <= 128), flash_f16x3 or long_f32; ma_kernel needs "
-    "mma_f16x3";
+    "mma_f16x3 (N <= 32) or long_f32 (N > 32)";
 // 7 = small_f32 (N <= 16, S <= 128, M <= 32: lanes over time, FP32)
 bool small_applicable(const prnet_handle* h) {
   return h->N <= 16 && h->cfg.seg_len <= 128 && h->M <= 32;
@@ -185,7 +186,7 @@ int pick_variant(const prnet_handle* h) {
     if (comp_on(h)) {
       if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
       if (h->cfg.ma_kernel == 0 && flash_applicable(h)) return 5;
-      return h->cfg.ma_kernel == 0 && h->N > 32 ? 1 : -1;
+      return h->N > 32 ? 1 : -1;   // long_f32
     }
     // (widened, the generic mma_f16x3 path is slower than tc_quad's WIDE instantiation from
     // N = 14 on: stress L336/S24 0.278 vs 0.259 ms; equal at N = 8)

@@ -400,6 +400,15 @@ def test_ma_decomposition_parity(oracle_mod, L, S, H, mv, rev, ma):
     _check_widening(oracle_mod, x, S, H, mv, rev, ma=ma)
 
 
+@pytest.mark.parametrize("ma", [1, 5, 25])
+@pytest.mark.parametrize("mv,rev", [(0, False), (3, True), (4, False), (7, True)])
+@pytest.mark.parametrize("L,S,H", [(1440, 24, 96), (1536, 12, 200), (4000, 120, 100)])
+def test_ma_decomposition_parity_long(oracle_mod, L, S, H, mv, rev, ma):
+    """N > 32: long_f32 implements the decomposition."""
+    x = synth.random_windows(2, 3, L, kind="mixed")
+    _check_widening(oracle_mod, x, S, H, mv, rev, ma=ma)
+
+
 @pytest.mark.parametrize("kind", ["normal", "constant", "scaled"])
 @pytest.mark.parametrize("tau,hpc", [(0.05, True), (1.0, False), (10.0, True)])
 def test_ma_decomposition_distributions(oracle_mod, kind, tau, hpc):
@@ -420,10 +429,10 @@ def test_ma_decomposition_attention_dump():
 
 
 def test_component_values_unsupported_paths():
-    m = PRNet(3, 1440, 24, 96, ma_kernel=5)             # N = 60: the decomposition is N <= 32
+    m = PRNet(3, 3000, 150, 96, ma_kernel=5)            # N = 20, S = 150: no kernel
     m.load(np.zeros((3, m.M, m.N)), np.zeros((3, m.M, m.N)), np.zeros((3, 96)))
     with pytest.raises(PrnetError) as e:
-        m.forward(torch.zeros((2, 3, 1440), device="cuda"))
+        m.forward(torch.zeros((2, 3, 3000), device="cuda"))
     assert e.value.status == 3
     m2 = PRNet(3, 720, 24, 96, metric_variant=4)
     for v in ("tc_quad", "small_f32", "warp_f32"):
