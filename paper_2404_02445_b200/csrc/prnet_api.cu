@@ -186,14 +186,14 @@ int pick_variant(const prnet_handle* h) {
     if (comp_on(h)) {
       if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
       if (h->cfg.ma_kernel == 0 && flash_applicable(h)) return 5;
-      return h->N > 32 ? 1 : -1;   // long_f32
+      return 1;   // long_f32 (any S, N <= 512)
     }
     // (widened, the generic mma_f16x3 path is slower than tc_quad's WIDE instantiation from
     // N = 14 on: stress L336/S24 0.278 vs 0.259 ms; equal at N = 8)
     if (tcq_applicable(h) && h->N > 8) return 6;
     if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
     if (flash_applicable(h)) return 5;
-    if (h->cfg.ma_kernel == 0 && h->N > 32) return 1;   // long_f32 (N <= 512; S > 96 or M > 32)
+    return 1;   // long_f32: any S and M (N <= 512), e.g. N <= 32 with S > 128
     return -1;   // no kernel implements it for this shape
   }
   // measured on B200 (profiles/README.md): small_f32 is the fastest N <= 8 path (stress

@@ -402,9 +402,10 @@ def test_ma_decomposition_parity(oracle_mod, L, S, H, mv, rev, ma):
 
 @pytest.mark.parametrize("ma", [1, 5, 25])
 @pytest.mark.parametrize("mv,rev", [(0, False), (3, True), (4, False), (7, True)])
-@pytest.mark.parametrize("L,S,H", [(1440, 24, 96), (1536, 12, 200), (4000, 120, 100)])
+@pytest.mark.parametrize("L,S,H", [(1440, 24, 96), (1536, 12, 200), (4000, 120, 100),
+                                   (3000, 150, 96), (700, 200, 450)])
 def test_ma_decomposition_parity_long(oracle_mod, L, S, H, mv, rev, ma):
-    """N > 32: long_f32 implements the decomposition."""
+    """N > 32, or S > 128: long_f32 implements every widening flag."""
     x = synth.random_windows(2, 3, L, kind="mixed")
     _check_widening(oracle_mod, x, S, H, mv, rev, ma=ma)
 
@@ -429,11 +430,9 @@ def test_ma_decomposition_attention_dump():
 
 
 def test_component_values_unsupported_paths():
-    m = PRNet(3, 3000, 150, 96, ma_kernel=5)            # N = 20, S = 150: no kernel
+    m = PRNet(3, 3000, 150, 96, ma_kernel=5)            # N = 20, S = 150: long_f32 runs it
     m.load(np.zeros((3, m.M, m.N)), np.zeros((3, m.M, m.N)), np.zeros((3, 96)))
-    with pytest.raises(PrnetError) as e:
-        m.forward(torch.zeros((2, 3, 3000), device="cuda"))
-    assert e.value.status == 3
+    m.forward(torch.zeros((2, 3, 3000), device="cuda"))
     m2 = PRNet(3, 720, 24, 96, metric_variant=4)
     for v in ("tc_quad", "small_f32", "warp_f32"):
         with pytest.raises(PrnetError) as e:
@@ -444,10 +443,8 @@ def test_component_values_unsupported_paths():
 
 
 def test_widening_unsupported_paths():
-    m = PRNet(3, 3000, 150, 96, metric_variant=2)       # N = 20, S = 150: no kernel for bit 1
-    m.load(np.zeros((3, m.M, m.N)), np.zeros((3, m.M, m.N)), np.zeros((3, 96)))
-    with pytest.raises(PrnetError) as e:
-        m.forward(torch.zeros((2, 3, 3000), device="cuda"))
+    with pytest.raises(PrnetError) as e:                 # N = 516 > 512: rejected at create
+        PRNet(3, 6192, 12, 96, metric_variant=2)
     assert e.value.status == 3
     m2 = PRNet(3, 720, 24, 96, instance_norm=True)
     with pytest.raises(PrnetError) as e:
