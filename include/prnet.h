@@ -49,10 +49,10 @@ typedef enum {
   PRNET_ERR_BAD_STATE = 2,   /* forward before load_params; NULL handle                  */
   PRNET_ERR_UNSUPPORTED = 3, /* device is not sm_100 (cc 10.x); x/y not 16-byte aligned;
                                 x and y overlap; pointer not on the handle's device;
-                                shape beyond the compiled limits (N > 512, S > 128);
-                                widening (metric_variant bits 1-2, instance_norm) on a
-                                shape no kernel implements it for (see
-                                prnet_set_kernel_variant)                               */
+                                shape beyond the compiled limits (N > 512; shared
+                                memory of the long_f32 fallback); a forced variant
+                                (prnet_set_kernel_variant) that does not cover the
+                                shape or the widening flags                             */
   PRNET_ERR_CUDA = 4,        /* CUDA runtime or launch error (text: prnet_last_error)    */
   PRNET_ERR_OOM = 5          /* device or pinned-host allocation failed                  */
 } prnet_status;
@@ -91,9 +91,8 @@ typedef struct {
                                decomposition of the segmented points (edge-replicated ends,
                                after instance_norm): the seasonal branch (Def 3-4, 6, 9)
                                runs on x - MA_k(x), the trend branch (Def 3-5, 7, 9) on
-                               MA_k(x) (R-f5).  N <= 32, M <= 32, S <= 128
-                               (mma_f16x3) or 32 < N <= 512 (long_f32); other shapes:
-                               PRNET_ERR_UNSUPPORTED                                      */
+                               MA_k(x) (R-f5).  Runs in mma_f16x3 (N <= 32,
+                               M <= 32, S <= 128), else in long_f32 (N <= 512)            */
 } prnet_config;
 
 /* Create a handle: validates cfg, checks the device is compute capability 10.x,
