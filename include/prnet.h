@@ -193,9 +193,10 @@ prnet_status prnet_error_sums(prnet_handle* h, const float* y, const float* targ
  *   dws, dwt  device [Cw][M][N] fp32, db device [Cw][H] fp32: overwritten (B = 0 -> zeros)
  * FP32 recomputation of the attention, fixed-order reductions (fp64 across CTAs): the result
  * is deterministic.  Uses a per-handle device workspace (grown on demand, which synchronises
- * the stream once).  Errors: INVALID_ARG (B < 0, NULL pointers), UNSUPPORTED (N, M > 32,
- * S > 128, metric_variant bit 2, ma_kernel > 0, pointers not on the handle's device), CUDA,
- * OOM. */
+ * the stream once).  N <= 32 (S <= 128): one warp per series; N > 32 or S > 128: one CTA
+ * per series, rows streamed.  Errors: INVALID_ARG (B < 0, NULL pointers), UNSUPPORTED
+ * (N > 512, M > 32, metric_variant bit 2, ma_kernel > 0, pointers not on the handle's
+ * device), CUDA, OOM. */
 prnet_status prnet_backward_head(prnet_handle* h, const float* x, int64_t batch,
                                  const float* dy, float* dws, float* dwt, float* db,
                                  void* cuda_stream);

@@ -227,10 +227,226 @@ __global__ void prnet_bwd_reduce_kernel(const float* __restrict__ part, int C, i
   }
 }
 
+// Long lookbacks (32 < N <= 512): one CTA per (channel, block of windows), series one after
+// the other; per series the segment rows, z rows and dY live in shared memory, warp w takes
+// query rows i = w, w + nwarps, ... (as fwd_long.cu): the row's two softmaxes over the keys
+// (lanes over j), its pattern row P^[i][t] (lanes over t), and dW[m][i] += sum_t dY[m][t] P^
+// by a warp reduction per m into the CTA's accumulator (row i has one owner warp: no atomics).
+template <int KJ>
+__global__ void __launch_bounds__(256) prnet_bwd_long_kernel(FwdArgs a, const float* __restrict__ dy,
+                                                          float* __restrict__ part, int rs,
+                                                          int wins_per_cta) {
+  extern __shared__ float4 smem4[];
+  float* smem = reinterpret_cast<float*>(smem4);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int c = blockIdx.y, C = a.C;
+  const int S = a.S, N = a.N, M = a.M, H = a.H, MS = M * S;
+  float* xr = smem;               // [N][rs]
+  float* zr = xr + N * rs;        // [N][rs]
+  float* muS = zr + N * rs;       // [N]
+  float* kapS = muS + N;          // [N]
+  float* invS = kapS + N;         // [N]
+  float* red = invS + N;          // [64]
+  float* wrow = red + 64;         // [nwarps][2][N]
+  float* dYs = wrow + nwarps * 2 * N;   // [M S]
+  float* acc = dYs + MS;          // [2][M][N] dW_s, dW_t
+  float* accB = acc + 2 * M * N;  // [H]
+  for (int k = threadIdx.x; k < 2 * M * N; k += blockDim.x) acc[k] = 0.f;
+  for (int k = threadIdx.x; k < H; k += blockDim.x) accB[k] = 0.f;
+
+  const int64_t b0 = (int64_t)blockIdx.x * wins_per_cta;
+  int64_t b1 = b0 + wins_per_cta;
+  if (b1 > a.B) b1 = a.B;
+  for (int64_t b = b0; b < b1; b++) {
+    const int64_t series = b * C + c;
+    const float* xg = a.x + b * a.xsb + c * a.xsc + a.r;
+    __syncthreads();
+    for (int k = threadIdx.x; k < N * S; k += blockDim.x) {
+      const int n = k / S;
+      xr[n * rs + (k - n * S)] = __ldg(xg + k);
+    }
+    for (int k = threadIdx.x; k < MS; k += blockDim.x) dYs[k] = k < H ? __ldg(dy + series * H + k) : 0.f;
+    __syncthreads();
+    // descriptors (Def 3-4, residuals with metric_variant bit 1), as fwd_long.cu
+    for (int n = threadIdx.x; n < N; n += blockDim.x) {
+      const float* row = xr + n * rs;
+      const float x0 = row[0];
+      float s1 = 0.f, s3 = 0.f;
+      for (int t = 0; t < S; t++) {
+        const float d = row[t] - x0;
+        s1 += d;
+        s3 = fmaf((float)t - a.half_s, d, s3);
+      }
+      const float m1 = s1 * a.inv_s, kap = s3 * a.inv_v, kd = a.detrend ? kap : 0.f;
+      float nu2 = 0.f;
+      for (int t = 0; t < S; t++) {
+        const float z = fmaf(-kd, (float)t - a.half_s, (row[t] - x0) - m1);
+        nu2 = fmaf(z, z, nu2);
+        zr[n * rs + t] = z;
+      }
+      muS[n] = x0 + m1;
+      kapS[n] = kap;
+      invS[n] = nu2;
+      wrow[n] = a.detrend ? fmaf(kap * kap, 1.f / a.inv_v, nu2) : nu2;
+    }
+    __syncthreads();
+    float p0 = 0.f;
+    for (int n = threadIdx.x; n < N; n += blockDim.x) p0 += muS[n];
+    p0 = warp_sum(p0);
+    if (lane == 0) red[warp] = p0;
+    __syncthreads();
+    float mbar = 0.f;
+    for (int w = 0; w < nwarps; w++) mbar += red[w];
+    mbar *= a.inv_n;
+    __syncthreads();
+    p0 = 0.f;
+    for (int n = threadIdx.x; n < N; n += blockDim.x) {
+      const float d = muS[n] - mbar;
+      p0 += wrow[n] + (float)S * d * d;
+    }
+    p0 = warp_sum(p0);
+    if (lane == 0) red[32 + warp] = p0;
+    __syncthreads();
+    float sig = 0.f;
+    for (int w = 0; w < nwarps; w++) sig += red[32 + w];
+    float mr = 0.f, rr = 1.f, sr = 1.f;
+    if (a.revin) {
+      const float vr = sig * a.inv_ns;
+      mr = mbar;
+      rr = rsqrtf(vr + kEpsRevin);
+      sr = (vr + kEpsRevin) * rr;
+    }
+    const float inv_var = rr * rr / fmaf(sig * a.inv_ns * rr, rr, kEpsTrend);
+    __syncthreads();
+    for (int n = threadIdx.x; n < N; n += blockDim.x)
+      invS[n] = rsqrtf(invS[n] * rr * rr + kEpsSeasonal) * rr;
+    __syncthreads();
+
+    float* wr = wrow + warp * 2 * N;
+    for (int i = warp; i < N; i += nwarps) {
+      float g[KJ];
+#pragma unroll
+      for (int k = 0; k < KJ; k++) g[k] = 0.f;
+      const float* zi = zr + i * rs;
+      for (int t = 0; t < S; t++) {
+        const float zv = zi[t];
+#pragma unroll
+        for (int k = 0; k < KJ; k++) {
+          const int j = lane + 32 * k;
+          if (j < N) g[k] = fmaf(zv, zr[j * rs + t], g[k]);
+        }
+      }
+      const float inv_i = invS[i], mu_i = muS[i], k_i = kapS[i];
+      float mx = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < KJ; k++) {
+        const int j = lane + 32 * k;
+        g[k] = j < N ? g[k] * inv_i * invS[j] * a.ks : -INFINITY;
+        mx = fmaxf(mx, g[k]);
+      }
+      mx = warp_max(mx);
+      float sum = 0.f;
+#pragma unroll
+      for (int k = 0; k < KJ; k++) {
+        const int j = lane + 32 * k;
+        g[k] = j < N ? exp2f(g[k] - mx) : 0.f;
+        sum += g[k];
+      }
+      float rsum = 1.f / warp_sum(sum);
+#pragma unroll
+      for (int k = 0; k < KJ; k++) {
+        const int j = lane + 32 * k;
+        if (j < N) wr[j] = g[k] * rsum;
+      }
+      mx = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < KJ; k++) {
+        const int j = lane + 32 * k;
+        float v = -INFINITY;
+        if (j < N) {
+          const float dm = mu_i - muS[j], dk = k_i - kapS[j];
+          v = -(fmaf(a.vtrend * dk, dk, dm * dm) * inv_var) * a.kt;
+        }
+        g[k] = v;
+        mx = fmaxf(mx, v);
+      }
+      mx = warp_max(mx);
+      sum = 0.f;
+#pragma unroll
+      for (int k = 0; k < KJ; k++) {
+        const int j = lane + 32 * k;
+        g[k] = j < N ? exp2f(g[k] - mx) : 0.f;
+        sum += g[k];
+      }
+      rsum = 1.f / warp_sum(sum);
+#pragma unroll
+      for (int k = 0; k < KJ; k++) {
+        const int j = lane + 32 * k;
+        if (j < N) wr[N + j] = g[k] * rsum;
+      }
+      __syncwarp();
+      // pattern row i (lanes over t), P^ s_r = (P - mr) (rr s_r = 1), and its gradient terms
+      float cs[32], ct[32];
+#pragma unroll
+      for (int m = 0; m < 32; m++) cs[m] = ct[m] = 0.f;
+      for (int t = lane; t < S; t += 32) {
+        float ps = 0.f, pt = 0.f;
+        for (int j = 0; j < N; j++) {
+          const float xv = xr[j * rs + t];
+          ps = fmaf(wr[j], xv, ps);
+          pt = fmaf(wr[N + j], xv, pt);
+        }
+        ps -= mr;
+        pt -= mr;
+#pragma unroll
+        for (int m = 0; m < 32; m++) {
+          if (m < M) {
+            const float gy = dYs[m * S + t];
+            cs[m] = fmaf(gy, ps, cs[m]);
+            ct[m] = fmaf(gy, pt, ct[m]);
+          }
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < 32; m++) {
+        if (m < M) {
+          const float vs = warp_sum(cs[m]), vt = warp_sum(ct[m]);
+          if (lane == 0) {
+            acc[m * N + i] += vs;
+            acc[(M + m) * N + i] += vt;
+          }
+        }
+      }
+      __syncwarp();
+    }
+    for (int k = threadIdx.x; k < H; k += blockDim.x) accB[k] = fmaf(dYs[k], sr, accB[k]);
+  }
+  __syncthreads();
+  const int E = 2 * M * N + H;
+  float* out = part + ((int64_t)c * gridDim.x + blockIdx.x) * E;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) out[e] = e < 2 * M * N ? acc[e] : accB[e - 2 * M * N];
+}
+
 }  // namespace
 
 bool plan_bwd_head(const FwdArgs& a, int max_smem_optin, BwdPlan* p) {
-  if (a.N < 1 || a.N > 32 || a.M > 32 || a.S > 128) return false;
+  if (a.N < 1 || a.M > 32) return false;
+  if (a.N > 32 || a.S > 128) {   // long mode (prnet_bwd_long_kernel)
+    if (a.N > 512) return false;
+    p->long_mode = true;
+    p->ly.np = a.N <= 64 ? 2 : (a.N <= 128 ? 4 : (a.N <= 256 ? 8 : 16));   // KJ
+    p->ly.mp = a.S | 1;                                                     // row stride
+    p->warps = 8;
+    const size_t floats = (size_t)2 * a.N * p->ly.mp + 3 * a.N + 64 + (size_t)p->warps * 2 * a.N +
+                          (size_t)a.M * a.S + 2 * (size_t)a.M * a.N + a.H;
+    p->smem_bytes = floats * 4;
+    if (p->smem_bytes > (size_t)max_smem_optin) return false;
+    p->ly.wins_per_cta = 16;
+    p->nblk = (int)((a.B + p->ly.wins_per_cta - 1) / p->ly.wins_per_cta);
+    p->elems = 2 * a.M * a.N + a.H;
+    return true;
+  }
+  p->long_mode = false;
   BwdLayout& ly = p->ly;
   ly.np = a.N <= 8 ? 8 : (a.N <= 16 ? 16 : 32);
   ly.mp = a.M <= 8 ? 8 : (a.M <= 16 ? 16 : 32);
@@ -272,7 +488,24 @@ static cudaError_t launch_bwd_n(const FwdArgs& a, const BwdPlan& p, const float*
 
 cudaError_t launch_bwd_head(const FwdArgs& a, const BwdPlan& p, const float* dy, float* part,
                             float* dws, float* dwt, float* db, int Cw, cudaStream_t st) {
-  if (p.nblk > 0) {
+  if (p.nblk > 0 && p.long_mode) {
+    cudaError_t e;
+    auto go = [&](auto kern) {
+      cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)p.smem_bytes);
+      if (r != cudaSuccess) return r;
+      dim3 grid((unsigned)p.nblk, (unsigned)a.C);
+      kern<<<grid, 32 * p.warps, p.smem_bytes, st>>>(a, dy, part, p.ly.mp, p.ly.wins_per_cta);
+      return cudaGetLastError();
+    };
+    switch (p.ly.np) {
+      case 2: e = go(prnet_bwd_long_kernel<2>); break;
+      case 4: e = go(prnet_bwd_long_kernel<4>); break;
+      case 8: e = go(prnet_bwd_long_kernel<8>); break;
+      default: e = go(prnet_bwd_long_kernel<16>); break;
+    }
+    if (e != cudaSuccess) return e;
+  } else if (p.nblk > 0) {
     cudaError_t e;
     switch (p.ly.np) {
       case 8: e = launch_bwd_n<8>(a, p, dy, part, st); break;

@@ -733,7 +733,8 @@ prnet_status prnet_backward_head(prnet_handle* h, const float* x, int64_t batch,
   prnet::FwdArgs a = make_args(h, x, batch, nullptr);
   prnet::BwdPlan p;
   if (!prnet::plan_bwd_head(a, h->max_smem_optin, &p))
-    return fail(h, PRNET_ERR_UNSUPPORTED, "backward_head needs N <= 32, M <= 32, S <= 128");
+    return fail(h, PRNET_ERR_UNSUPPORTED, "backward_head needs N <= 512, M <= 32 (and the "
+                                          "long-lookback rows within shared memory)");
   cudaStream_t st = (cudaStream_t)cuda_stream;
   const int64_t need = (int64_t)h->cfg.channels * p.nblk * p.elems;
   if (need > h->bwd_floats) {

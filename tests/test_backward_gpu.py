@@ -58,6 +58,16 @@ def test_backward_head_parity(oracle_mod, L, S, H, mv, rev, hpc):
     _check(got, ref, x, dy)
 
 
+@pytest.mark.parametrize("hpc", [True, False])
+@pytest.mark.parametrize("mv,rev", [(0, False), (1, False), (2, False), (3, True)])
+@pytest.mark.parametrize("L,S,H", [(1440, 24, 96), (1536, 12, 200), (4000, 120, 100),
+                                   (3000, 150, 96), (5760, 12, 96)])
+def test_backward_head_parity_long(oracle_mod, L, S, H, mv, rev, hpc):
+    """N > 32 or S > 128: the row-streaming backward kernel."""
+    got, ref, _, x, dy = _grads(oracle_mod, 3, 2, L, S, H, hpc, mv, rev)
+    _check(got, ref, x, dy)
+
+
 @pytest.mark.parametrize("kind", ["normal", "constant", "scaled"])
 @pytest.mark.parametrize("tau", [0.05, 1.0, 10.0])
 def test_backward_head_distributions_and_temperatures(oracle_mod, kind, tau):
@@ -85,9 +95,9 @@ def test_backward_head_edge_cases():
             PRNet(3, 96, 24, 96, **kw).backward_head(torch.zeros((1, 3, 96), device="cuda"),
                                                      torch.zeros((1, 3, 96), device="cuda"))
         assert e.value.status == 3
-    with pytest.raises(PrnetError) as e:   # N = 60 > 32
-        PRNet(3, 1440, 24, 96).backward_head(torch.zeros((1, 3, 1440), device="cuda"),
-                                             torch.zeros((1, 3, 96), device="cuda"))
+    with pytest.raises(PrnetError) as e:   # M = 34 > 32
+        PRNet(3, 96, 24, 800).backward_head(torch.zeros((1, 3, 96), device="cuda"),
+                                            torch.zeros((1, 3, 800), device="cuda"))
     assert e.value.status == 3
     with pytest.raises(PrnetError) as e:   # host pointer
         m.backward_head(torch.zeros((1, 3, 96)), torch.zeros((1, 3, 96)))
