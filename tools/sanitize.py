@@ -67,7 +67,8 @@ for L, S, H, t0 in [(720, 24, 720, 1), (720, 24, 96, 0), (97, 7, 13, 3)]:
     print("ok sliding", L, S, H, t0, flush=True)
 # head backward
 for L, S, H, mv, rev, hpc in [(720, 24, 336, 0, False, True), (97, 7, 13, 3, True, False),
-                              (384, 128, 200, 2, False, True)]:
+                              (384, 128, 200, 2, False, True), (1440, 24, 96, 3, True, True),
+                              (3000, 150, 96, 0, False, False)]:
     x = torch.from_numpy(synth.random_windows(40, 3, L)).cuda()
     dy = torch.randn((40, 3, H), device="cuda")
     g = PRNet(3, L, S, H, head_per_channel=hpc, metric_variant=mv,
