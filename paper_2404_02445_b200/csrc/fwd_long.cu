@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(256) prnet_fwd_long_kernel(FwdArgs a, int rs) 
       for (int k = 0; k < KJ; k++) {
         const int j = lane + 32 * k;
         if (j < N) wr[j] = g[k] * rsum;
+        if (a.a_s_dbg != nullptr && j < N) a.a_s_dbg[(series * N + i) * N + j] = g[k] * rsum;
       }
       // trend softmax
       mx = -INFINITY;
@@ -252,6 +253,7 @@ __global__ void __launch_bounds__(256) prnet_fwd_long_kernel(FwdArgs a, int rs) 
       for (int k = 0; k < KJ; k++) {
         const int j = lane + 32 * k;
         if (j < N) wr[N + j] = g[k] * rsum;
+        if (a.a_t_dbg != nullptr && j < N) a.a_t_dbg[(series * N + i) * N + j] = g[k] * rsum;
       }
       __syncwarp();
       // component values (metric_variant bit 2, R-f4): row sums A mu, A kappa of both branches

@@ -28,10 +28,12 @@ struct prnet_handle {
   float* d_invsw_fl = nullptr;
   bool loaded = false;
   int forced_variant = -1;  // prnet_set_kernel_variant
+  mutable std::mutex err_mu;   // err is written by any thread that calls into the handle
   std::string err;
   // host-forward runtime
   int64_t host_chunk = 0;   // windows per chunk (0 = default)
-  int64_t stage_windows = 0;
+  int64_t stage_windows = 0;    // windows the x staging ring holds
+  int64_t ystage_windows = 0;   // windows the y staging ring holds
   static constexpr int kStages = 3;
   float* d_xstage[kStages] = {nullptr, nullptr, nullptr};
   float* d_ystage[kStages] = {nullptr, nullptr, nullptr};
@@ -47,8 +49,12 @@ namespace {
 thread_local std::string g_create_error;
 
 prnet_status fail(prnet_handle* h, prnet_status s, const std::string& msg) {
-  if (h) h->err = msg;
-  else g_create_error = msg;
+  if (h) {
+    std::lock_guard<std::mutex> lk(h->err_mu);
+    h->err = msg;
+  } else {
+    g_create_error = msg;
+  }
   return s;
 }
 
@@ -169,19 +175,28 @@ bool comp_on(const prnet_handle* h) {
 bool variant_supports_widening(const prnet_handle* h, int v) {
   if (h->cfg.ma_kernel > 0) return v == 1 || v == 2;
   if (comp_on(h)) return v == 1 || v == 2 || v == 5;
-  return v == 1 || v == 2 || v == 5 || v == 6;
+  return v == 1 || v == 2 || v == 5 || v == 6 || v == 8;
 }
 const char* kWideningMsg =
-    "metric_variant bit 1 / instance_norm need tc_quad, mma_f16x3 (N <= 32) or flash_f16x3 "
-    "(16 < N <= 512, S <= 96, M <= 32) or long_f32 (N <= 512); metric_variant bit 2 needs "
-    "mma_f16x3 (N <= 32, M <= 32, S <= 128), flash_f16x3 or long_f32; ma_kernel needs "
-    "mma_f16x3 (N <= 32) or long_f32 (N > 32)";
+    "metric_variant bit 1 / instance_norm need tc_pipe, tc_quad, mma_f16x3 (N <= 32), "
+    "flash_f16x3 (16 < N <= 512, S <= 96, M <= 32) or long_f32 (N <= 512); metric_variant "
+    "bit 2 needs mma_f16x3 (N <= 32, M <= 32, S <= 128), flash_f16x3 or long_f32; ma_kernel "
+    "needs mma_f16x3 (N <= 32, M <= 32, S <= 128) or long_f32 (any N <= 512)";
+// The kernels that shift the seasonal logits by a KNOWN row bound instead of searching the
+// row maximum (small_f32, mma_f16x3, flash_f16x3: f_i = nu_i / sqrt(nu_i^2 + eps_s) >= rho_ij;
+// DESIGN.md §3) keep the largest term of a row >= 2^(-ks/4), a normal float for
+// ks = log2(e) / tau_s <= 4 x 115, i.e. tau_s >= 1/320.  Below that the row-max-searching
+// FP32 kernels run (warp_f32, long_f32); tc_quad / tc_pipe (shift 1) need tau_s >= 1/80.
+constexpr float kTauKnownMax = 1.0f / 320.0f;
+bool known_max_ok(const prnet_handle* h) { return h->cfg.tau_seasonal >= kTauKnownMax; }
 // 7 = small_f32 (N <= 16, S <= 128, M <= 32: lanes over time, FP32)
 bool small_applicable(const prnet_handle* h) {
   return h->N <= 16 && h->cfg.seg_len <= 128 && h->M <= 32;
 }
 int pick_variant(const prnet_handle* h) {
   if (h->forced_variant >= 0) return h->forced_variant;
+  // seasonal temperatures below the known-maximum kernels' domain: row-max search (FP32)
+  if (!known_max_ok(h)) return (h->N <= 32 && !widening_on(h)) ? 0 : 1;
   if (widening_on(h)) {
     if (comp_on(h)) {
       if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
@@ -190,11 +205,10 @@ int pick_variant(const prnet_handle* h) {
     }
     // (widened, the generic mma_f16x3 path is slower than tc_quad's WIDE instantiation from
     // N = 14 on: stress L336/S24 0.278 vs 0.259 ms; equal at N = 8)
-    if (tcq_applicable(h) && h->N > 8) return 6;
+    if (tcq_applicable(h) && h->N > 8) return 8;
     if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
     if (flash_applicable(h)) return 5;
     return 1;   // long_f32: any S and M (N <= 512), e.g. N <= 32 with S > 128
-    return -1;   // no kernel implements it for this shape
   }
   // measured on B200 (profiles/README.md): small_f32 is the fastest N <= 8 path (stress
   // sweep 2-9x over tc_quad / mma_f16x3) and the fastest N <= 16 path for S > 64 (2.3x);
@@ -203,7 +217,7 @@ int pick_variant(const prnet_handle* h) {
   // fastest other N <= 32 path; tc_fold and tc_full are selectable with
   // prnet_set_kernel_variant
   if (small_applicable(h) && (h->N <= 8 || h->cfg.seg_len > 64)) return 7;
-  if (tcq_applicable(h) && h->N > 16) return 6;
+  if (tcq_applicable(h) && h->N > 16) return 8;
   if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
   if (h->N > 32 && flash_applicable(h)) return 5;
   return h->N <= 32 ? 0 : 1;
@@ -226,14 +240,29 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
   int v = pick_variant(h);
   if (v < 0 || (widening_on(h) && !variant_supports_widening(h, v)))
     return fail(h, PRNET_ERR_UNSUPPORTED, kWideningMsg);
-  if (v == 1 && a_s != nullptr) v = 0;  // the attention dump lives in the N <= 32 kernels
-  if (v == 7 && a_s != nullptr) v = 2;
-  if (v == 6 && a_s != nullptr) v = 2;
+  if (a_s != nullptr) {
+    // prnet_debug_attention: the dump is written by warp_f32 (the plain reading and the
+    // level-only trend), mma_f16x3, long_f32 (every flag) and tc_pipe (detrend /
+    // instance_norm), each from the values its own fold consumes; small_f32 and tc_quad map
+    // to mma_f16x3 (same domain, every flag), flash_f16x3 to long_f32 (every flag and N)
+    if (v == 7 || v == 6) v = 2;
+    if (v == 5) v = 1;
+    if (v == 0 && widening_on(h)) v = 1;
+  }
   static const int wpc_env = [] {  // tuning knob: windows per CTA (0 = plan default)
     const char* e = getenv("PRNET_WINDOWS_PER_CTA");
     return e ? atoi(e) : 0;
   }();
-  if (v == 7) {
+  if (v == 8) {
+    prnet::TcqPlan p;
+    if (!prnet::plan_tcp_kernel(a, h->max_smem_optin, h->sm_count, &p))
+      return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the tc_pipe kernel");
+    if (wpc_env > 0) {
+      p.wins_per_group = (wpc_env + 3) & ~3;
+      p.ctas_per_channel = 0;
+    }
+    e = prnet::launch_tcp_kernel(a, p, st);
+  } else if (v == 7) {
     prnet::SmallPlan p;
     if (!prnet::plan_small_kernel(a, h->max_smem_optin, &p))
       return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the small_f32 kernel");
@@ -283,6 +312,41 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
     e = prnet::launch_long_kernel(a, p, st);
   }
   if (e != cudaSuccess) return cuda_fail(h, e, "forward launch");
+  return PRNET_OK;
+}
+
+// The host-buffer runtime's staging rings (x: [chunk][C][L], y: [chunk][C][H], kStages
+// each) and streams; x staging only when need_x (prnet_forward_host).
+prnet_status ensure_staging(prnet_handle* h, int64_t chunk, bool need_x) {
+  const int64_t C = h->cfg.channels, L = h->cfg.lookback, H = h->cfg.horizon;
+  cudaError_t e;
+  if (need_x && chunk > h->stage_windows) {
+    for (int k = 0; k < prnet_handle::kStages; k++) {
+      cudaFree(h->d_xstage[k]);
+      h->d_xstage[k] = nullptr;
+    }
+    h->stage_windows = 0;
+    for (int k = 0; k < prnet_handle::kStages; k++)
+      if ((e = cudaMalloc(&h->d_xstage[k], chunk * C * L * 4)) != cudaSuccess)
+        return cuda_fail(h, e, "cudaMalloc(x staging)");
+    h->stage_windows = chunk;
+  }
+  if (chunk > h->ystage_windows) {
+    for (int k = 0; k < prnet_handle::kStages; k++) {
+      cudaFree(h->d_ystage[k]);
+      h->d_ystage[k] = nullptr;
+    }
+    h->ystage_windows = 0;
+    for (int k = 0; k < prnet_handle::kStages; k++)
+      if ((e = cudaMalloc(&h->d_ystage[k], chunk * C * H * 4)) != cudaSuccess)
+        return cuda_fail(h, e, "cudaMalloc(y staging)");
+    h->ystage_windows = chunk;
+  }
+  for (int k = 0; k < prnet_handle::kStages; k++) {
+    if (!h->streams[k] &&
+        (e = cudaStreamCreateWithFlags(&h->streams[k], cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(h, e, "cudaStreamCreate");
+  }
   return PRNET_OK;
 }
 
@@ -475,25 +539,7 @@ prnet_status prnet_forward_host(prnet_handle* h, const float* x_host, int64_t ba
   }
   if (chunk > batch) chunk = batch;
   cudaError_t e;
-  if (chunk > h->stage_windows) {  // (re)allocate the staging ring
-    for (int k = 0; k < prnet_handle::kStages; k++) {
-      cudaFree(h->d_xstage[k]);
-      cudaFree(h->d_ystage[k]);
-      h->d_xstage[k] = h->d_ystage[k] = nullptr;
-    }
-    h->stage_windows = 0;
-    for (int k = 0; k < prnet_handle::kStages; k++) {
-      if ((e = cudaMalloc(&h->d_xstage[k], chunk * C * L * 4)) != cudaSuccess ||
-          (e = cudaMalloc(&h->d_ystage[k], chunk * C * H * 4)) != cudaSuccess)
-        return cuda_fail(h, e, "cudaMalloc(staging)");
-    }
-    h->stage_windows = chunk;
-  }
-  for (int k = 0; k < prnet_handle::kStages; k++) {
-    if (!h->streams[k] &&
-        (e = cudaStreamCreateWithFlags(&h->streams[k], cudaStreamNonBlocking)) != cudaSuccess)
-      return cuda_fail(h, e, "cudaStreamCreate");
-  }
+  if ((s = ensure_staging(h, chunk, true)) != PRNET_OK) return s;
   // Chunk k goes to stage k % 3 on stream k % 3: H2D -> kernel -> D2H in stream
   // order, so the copy engines overlap chunk k+1's upload, chunk k's kernel and
   // chunk k-1's download across the three streams.
@@ -575,25 +621,8 @@ prnet_status prnet_forward_sliding_host(prnet_handle* h, const float* series, in
     if (chunk < 1) chunk = 1;
   }
   if (chunk > batch) chunk = batch;
-  if (chunk > h->stage_windows) {  // (re)allocate the output staging ring
-    for (int k = 0; k < prnet_handle::kStages; k++) {
-      cudaFree(h->d_xstage[k]);
-      cudaFree(h->d_ystage[k]);
-      h->d_xstage[k] = h->d_ystage[k] = nullptr;
-    }
-    h->stage_windows = 0;
-    for (int k = 0; k < prnet_handle::kStages; k++) {
-      if ((e = cudaMalloc(&h->d_xstage[k], chunk * C * L * 4)) != cudaSuccess ||
-          (e = cudaMalloc(&h->d_ystage[k], chunk * C * H * 4)) != cudaSuccess)
-        return cuda_fail(h, e, "cudaMalloc(staging)");
-    }
-    h->stage_windows = chunk;
-  }
-  for (int k = 0; k < prnet_handle::kStages; k++) {
-    if (!h->streams[k] &&
-        (e = cudaStreamCreateWithFlags(&h->streams[k], cudaStreamNonBlocking)) != cudaSuccess)
-      return cuda_fail(h, e, "cudaStreamCreate");
-  }
+  // only the output staging ring: the windows are read from the uploaded series span
+  if ((s = ensure_staging(h, chunk, false)) != PRNET_OK) return s;
   // the series span goes up once (C rows of `span` floats, pitched); windows are then
   // forecast in chunks on three streams so chunk k's D2H overlaps chunk k+1's kernel
   if ((e = cudaMemcpy2DAsync(h->d_series, Tp * 4, series + t0, T * 4, span * 4, C,
@@ -648,7 +677,14 @@ void prnet_destroy(prnet_handle* h) {
 }
 
 const char* prnet_last_error(const prnet_handle* h) {
-  return h ? h->err.c_str() : g_create_error.c_str();
+  if (!h) return g_create_error.c_str();
+  // a per-thread copy: another thread may overwrite h->err while the caller reads it
+  thread_local std::string copy;
+  {
+    std::lock_guard<std::mutex> lk(h->err_mu);
+    copy = h->err;
+  }
+  return copy.c_str();
 }
 
 prnet_status prnet_get_dims(const prnet_handle* h, int32_t* N, int32_t* M, int32_t* r) {
@@ -678,7 +714,6 @@ prnet_status prnet_debug_segments(prnet_handle* h, const float* x, int64_t batch
 prnet_status prnet_debug_attention(prnet_handle* h, const float* x, int64_t batch, float* a_s,
                                    float* a_t, void* cuda_stream) {
   if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
-  if (h->N > 32) return fail(h, PRNET_ERR_UNSUPPORTED, "debug_attention needs N <= 32");
   if (!a_s || !a_t) return fail(h, PRNET_ERR_INVALID_ARG, "NULL attention buffer");
   const int64_t C = h->cfg.channels, H = h->cfg.horizon;
   prnet_status s = validate_forward(h, x, batch, a_s, true);  // x checks (a_s as dummy y)
@@ -753,13 +788,20 @@ prnet_status prnet_backward_head(prnet_handle* h, const float* x, int64_t batch,
 
 prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {
   if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
-  if (variant < -1 || variant > 7)
-    return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,...,7}");
+  if (variant < -1 || variant > 8)
+    return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,...,8}");
+  if (variant == 8 && !tcq_applicable(h))
+    return fail(h, PRNET_ERR_UNSUPPORTED,
+                "tc_pipe variant needs S = 24, N <= 32, M <= 32, tau_seasonal >= 1/80");
   if (variant == 7 && !small_applicable(h))
     return fail(h, PRNET_ERR_UNSUPPORTED, "small_f32 variant needs N <= 16, S <= 128, M <= 32");
   if (variant == 6 && !tcq_applicable(h))
     return fail(h, PRNET_ERR_UNSUPPORTED,
                 "tc_quad variant needs S = 24, N <= 32, M <= 32, tau_seasonal >= 1/80");
+  if ((variant == 2 || variant == 5 || variant == 7) && !known_max_ok(h))
+    return fail(h, PRNET_ERR_UNSUPPORTED,
+                "small_f32 / mma_f16x3 / flash_f16x3 need tau_seasonal >= 1/320 (known-maximum "
+                "softmax shift); warp_f32 and long_f32 take any temperature");
   if (variant == 5 && !flash_applicable(h))
     return fail(h, PRNET_ERR_UNSUPPORTED, "flash variant needs 16 < N <= 512, S <= 96, M <= 32");
   if (variant == 4 && !tc2_applicable(h))

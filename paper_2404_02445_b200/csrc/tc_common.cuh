@@ -87,6 +87,27 @@ __device__ __forceinline__ void tst16_x2(uint32_t taddr, const uint32_t (&r)[8])
       "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
       : "memory");
 }
+// the inverse of tld16_x4: r[4k + 2v + e] -> lane (base + t/4 + 8v), column 8k + 2(t%4) + e,
+// i.e. an m16n8 mma.sync accumulator tile k per 8 columns
+__device__ __forceinline__ void tst16_x4(uint32_t taddr, const float (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x256b.x4.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15,%16};" ::"r"(taddr),
+      "f"(r[0]), "f"(r[1]), "f"(r[2]), "f"(r[3]), "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7]),
+      "f"(r[8]), "f"(r[9]), "f"(r[10]), "f"(r[11]), "f"(r[12]), "f"(r[13]), "f"(r[14]),
+      "f"(r[15])
+      : "memory");
+}
+// shared-memory counter increment with acquire-release semantics (returns the old value):
+// the arrival that completes a group of warps observes every earlier arrival's prior writes
+__device__ __forceinline__ uint32_t atom_add_acqrel(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;"
+               : "=r"(old)
+               : "r"(smem_u32(p)), "r"(v)
+               : "memory");
+  return old;
+}
 // TMEM lane (base lane + t) <- thread t: 16 consecutive 32-bit columns
 __device__ __forceinline__ void tst_x16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
@@ -140,6 +161,21 @@ __device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity
 #endif
     if (done) return;
     if (it > (1u << 26)) __trap();
+  }
+}
+// as mbar_wait_bounded, with a suspend-time hint: a warp whose phase is not complete sleeps
+// (up to ns) instead of re-polling, so it does not take issue slots from the other warps
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  uint32_t done;
+  for (uint32_t it = 0;; it++) {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+        : "memory");
+    if (done) return;
+    if (it > (1u << 22)) __trap();
   }
 }
 // one elected lane of the (converged) warp returns true

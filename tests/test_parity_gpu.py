@@ -36,7 +36,7 @@ def _applicable(variant, L, S, H):
         return N <= 32 and M <= 32 and S <= 128
     if variant == "tc_fold":
         return S == 24 and 16 < N <= 32 and M <= 32
-    if variant in ("tc_full", "tc_quad"):
+    if variant in ("tc_full", "tc_quad", "tc_pipe"):
         return S == 24 and N <= 32 and M <= 32
     if variant == "small_f32":
         return N <= 16 and S <= 128 and M <= 32
@@ -46,8 +46,8 @@ def _applicable(variant, L, S, H):
 
 
 VARIANTS = [None, "warp_f32", "mma_f16x3", "tc_fold", "tc_full", "long_f32", "flash_f16x3",
-            "tc_quad", "small_f32"]
-SHORT_VARIANTS = [None, "warp_f32", "mma_f16x3", "tc_fold", "tc_full", "tc_quad", "small_f32"]
+            "tc_quad", "small_f32", "tc_pipe"]
+SHORT_VARIANTS = [None, "warp_f32", "mma_f16x3", "tc_fold", "tc_full", "tc_quad", "small_f32", "tc_pipe"]
 
 
 def _check_small(oracle_mod, x, S, H, hpc=True, tau_s=1.0, tau_t=1.0, scale=None, variant=None):
@@ -78,7 +78,7 @@ FULL = ["weather_h96", "weather_h192", "weather_h336", "weather_h720", "electric
 
 
 @pytest.mark.parametrize("variant", [None, "warp_f32", "mma_f16x3", "tc_fold", "tc_full",
-                                     "tc_quad"])
+                                     "tc_quad", "tc_pipe"])
 @pytest.mark.parametrize("name", FULL)
 def test_full_size_sampled(oracle_mod, name, variant):
     """The whole test set runs on the GPU in the bench's launch configuration; the
@@ -204,7 +204,7 @@ def test_segment_gather_bit_exact(L, S):
     np.testing.assert_array_equal(seg, x[:, :, idx])
 
 
-@pytest.mark.parametrize("variant", ["warp_f32", "mma_f16x3", "tc_fold", "tc_full"])
+@pytest.mark.parametrize("variant", ["warp_f32", "mma_f16x3", "tc_fold", "tc_full", "tc_pipe"])
 @pytest.mark.parametrize("L,S", [(720, 24), (96, 24), (384, 24), (480, 24)])
 def test_attention_matrices(oracle_mod, L, S, variant):
     x = synth.random_windows(2, 3, L, kind="mixed")
@@ -311,13 +311,13 @@ def _check_widening(oracle_mod, x, S, H, mv, rev, variant=None, tau_s=1.0, tau_t
     return assert_parity(y, y64, scale=scale)
 
 
-@pytest.mark.parametrize("variant", [None, "tc_quad", "mma_f16x3"])
+@pytest.mark.parametrize("variant", [None, "tc_quad", "tc_pipe", "mma_f16x3"])
 @pytest.mark.parametrize("mv,rev", [(1, False), (2, False), (3, False), (0, True), (3, True)])
 @pytest.mark.parametrize("L,S,H", [(720, 24, 720), (720, 24, 336), (100, 24, 90), (96, 24, 96),
                                    (97, 7, 13), (128, 8, 64), (270, 9, 31)])
 def test_widening_parity(oracle_mod, L, S, H, mv, rev, variant):
-    if variant == "tc_quad" and S != 24:
-        pytest.skip("tc_quad needs S = 24")
+    if variant in ("tc_quad", "tc_pipe") and S != 24:
+        pytest.skip("tc_quad / tc_pipe need S = 24")
     x = synth.random_windows(3, 5, L, kind="mixed")
     _check_widening(oracle_mod, x, S, H, mv, rev, variant)
 
