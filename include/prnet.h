@@ -1,5 +1,6 @@
 /*
- * prnet.h -- C ABI (v1) of the B200-native PRNet pattern-attention forward.
+ * prnet.h -- C ABI (version 3, PRNET_ABI_VERSION) of the B200-native PRNet pattern-attention
+ * forward.
  *
  * The operation (abstract, conclusion; reading fixed in
  * SURVEY.md §8(c) and restated in DESIGN.md §3): every (window b, channel c)
@@ -26,6 +27,21 @@
  *  - Results are deterministic: no atomics; a series' arithmetic does not
  *    depend on the batch it is in, the launch configuration or the device,
  *    so a sharded run's outputs equal the unsharded run's bitwise.
+ *  - Thread safety: one handle may be used from several host threads; the
+ *    last-error text is kept per handle under a lock and returned as a
+ *    per-thread copy.  Stream concurrency: prnet_forward, prnet_forward_sliding
+ *    and prnet_debug_* keep no per-call device state and may run concurrently
+ *    on different streams with one handle.  prnet_error_sums and
+ *    prnet_backward_head write a per-handle device scratch buffer, and
+ *    prnet_forward_host / prnet_forward_sliding_host use the handle's staging
+ *    ring: calls of these on one handle must not overlap (serialise them, or
+ *    use one handle per stream).
+ *  - Temperatures: every tau > 0 is accepted.  The automatic kernel choice
+ *    keeps each kernel inside its numerical domain: kernels that shift the
+ *    seasonal logits by a known row bound need tau_seasonal >= 1/320 (tc_quad:
+ *    >= 1/80); below that the row-maximum-searching FP32 kernels run
+ *    (warp_f32, long_f32).  A forced variant outside its domain is rejected
+ *    with PRNET_ERR_UNSUPPORTED (prnet_set_kernel_variant).
  */
 #ifndef PRNET_H
 #define PRNET_H
@@ -52,7 +68,7 @@ typedef enum {
                                 shape beyond the compiled limits (N > 512; shared
                                 memory of the long_f32 fallback); a forced variant
                                 (prnet_set_kernel_variant) that does not cover the
-                                shape or the widening flags                             */
+                                shape, the widening flags or the seasonal temperature    */
   PRNET_ERR_CUDA = 4,        /* CUDA runtime or launch error (text: prnet_last_error)    */
   PRNET_ERR_OOM = 5          /* device or pinned-host allocation failed                  */
 } prnet_status;
@@ -170,8 +186,11 @@ prnet_status prnet_get_dims(const prnet_handle* h, int32_t* N, int32_t* M, int32
 prnet_status prnet_debug_segments(prnet_handle* h, const float* x, int64_t batch, float* seg,
                                   void* cuda_stream);
 
-/* a_s, a_t [B][C][N][N] (device): the two attention matrices the forward
- * computes (same kernel, same arithmetic), rows summing to 1.  Requires N <= 32. */
+/* a_s, a_t [B][C][N][N] (device): the two attention matrices, rows summing to 1, from the
+ * kernel the forward runs (same arithmetic, written from the registers its fold consumes)
+ * for warp_f32, mma_f16x3, tc_quad and long_f32; a handle whose forward runs small_f32 is
+ * dumped by mma_f16x3, flash_f16x3 by long_f32 (same reading; every N <= 512 and every
+ * widening flag).  Errors as prnet_forward; uses a stream-ordered scratch y. */
 prnet_status prnet_debug_attention(prnet_handle* h, const float* x, int64_t batch, float* a_s,
                                    float* a_t, void* cuda_stream);
 
@@ -209,16 +228,17 @@ prnet_status prnet_backward_head(prnet_handle* h, const float* x, int64_t batch,
  *   2 = mma_f16x3    one warp per series, mma.sync m16n8k16 with split-fp16
  *                    hi/lo operands, 3 products, fp32 accumulation
  *                    (N <= 32, M <= 32, S <= 128)  [auto: N <= 32 unless 6, 7 apply]
- *   3 = tc_fold      as 2, fold Q = W A on tcgen05.mma with a TMEM accumulator
- *                    (S = 24, 16 < N <= 32, M <= 32)
- *   4 = tc_full      Gram, fold and head on tcgen05 / TMEM, lane-per-row softmax
- *                    (S = 24, N <= 32, M <= 32)
+ *   3, 4             retired (round-1 tcgen05 prototypes, superseded by 6):
+ *                    PRNET_ERR_INVALID_ARG
  *   5 = flash_f16x3  one CTA per series, 16-key tiles streamed, mma.sync
  *                    split-fp16 (16 < N <= 512, S <= 96, M <= 32)  [auto: N > 32]
  *   6 = tc_quad      groups of 4 warps take quads of 4 series; Gram of the
- *                    row-normalised segments, fold and head on tcgen05 / TMEM,
- *                    lane-per-row softmaxes (S = 24, N <= 32, M <= 32,
- *                    tau_seasonal >= 1/80)              [auto: N > 16]
+ *                    row-normalised segments and the fold on tcgen05 / TMEM,
+ *                    head on per-warp mma.sync (split fp16), lane-per-row
+ *                    softmaxes (S = 24, N <= 32, M <= 32, tau_seasonal >= 1/80)
+ *                    [auto: N > 16]
+ * Variants 2, 5, 7 need tau_seasonal >= 1/320 (known-maximum softmax shift); below the
+ * floors the automatic choice is 0 (N <= 32, no widening) or 1.
  *   7 = small_f32    one warp per series with lanes over TIME, FP32, warp
  *                    butterfly reductions (N <= 16, S <= 128, M <= 32)
  *                    [auto: N <= 8, or S > 64]

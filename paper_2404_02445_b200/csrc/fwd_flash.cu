@@ -218,6 +218,11 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
     }
     const float inv_var = 1.0f / fmaf(var * rr, rr, kEpsTrend);
     const float cmt = sqrtf(inv_var * a.kt) * rr, ckt = sqrtf(a.vtrend * inv_var * a.kt) * rr;
+    // a row whose known bound f_n sits far above its true maximum (between f_n^2 and f_n:
+    // a segment with nu^2 not >> eps_s, e.g. constant to within rounding) would leave its
+    // largest exponential below 2^-6 at low tau_s, where the fp16 hi/lo split of E loses
+    // precision (and below 2^-24 it underflows): such series take exact row maxima (below)
+    int loose = 0;
     for (int n = tid; n < NP; n += nthr) {
       if (n < N) {
         const float nu2 = c_inv[n] * rr * rr;
@@ -238,6 +243,7 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
         }
         c_inv[n] = 1.f;                // column factor of rho: 1 (row-normalised Gram)
         c_max[n] = sqrtf(nu2) * inv;   // f_n: known row maximum of rho (Cauchy-Schwarz)
+        loose |= (c_max[n] - c_max[n] * c_max[n]) * a.ks > 6.f;
         if (COMP) {
           c_vm[n] = c_mu[n];
           c_vk[n] = c_ka[n];
@@ -252,7 +258,7 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
         if (COMP) c_vm[n] = c_vk[n] = 0.f;
       }
     }
-    __syncthreads();
+    loose = __syncthreads_or(loose);
 
     // (KS <= 3: one chunk, compile-time, so the loop and the offsets fold away)
     const int nch = KS >= 4 ? ly.nch : 1;
@@ -283,6 +289,47 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
         nb[h] = -c_max[ii] * a.ks;
         mi[h] = ii < N ? c_mu[ii] : 0.f;
         ki[h] = c_ka[ii];
+      }
+      if (loose) {
+        // exact row maxima of rho over the key tiles (a Gram-only pass; CTA-uniform branch,
+        // taken only by series with a loose bound) as the softmax shift
+        float rmx[2] = {-INFINITY, -INFINITY};
+        for (int jt = 0; jt < NT; jt++) {
+          float g[2][4];
+#pragma unroll
+          for (int nt = 0; nt < 2; nt++)
+#pragma unroll
+            for (int e = 0; e < 4; e++) g[nt][e] = 0.f;
+#pragma unroll
+          for (int ks = 0; ks < KS; ks++) {
+            uint32_t bh[4], bl[4];
+            const int off = (16 * jt + (lane & 7) + 8 * (q8 >> 1)) * ZP + 16 * ks + 8 * (q8 & 1);
+            ldsm_x4(bh, z_hi + off);
+            ldsm_x4(bl, z_lo + off);
+            mma16816(g[0], zal[ks], bh[0], bh[1]);
+            mma16816(g[1], zal[ks], bh[2], bh[3]);
+            mma16816(g[0], zah[ks], bl[0], bl[1]);
+            mma16816(g[1], zah[ks], bl[2], bl[3]);
+            mma16816(g[0], zah[ks], bh[0], bh[1]);
+            mma16816(g[1], zah[ks], bh[2], bh[3]);
+          }
+#pragma unroll
+          for (int nt = 0; nt < 2; nt++) {
+            const int j = 16 * jt + 8 * nt + 2 * cq;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              if (j < N) rmx[h] = fmaxf(rmx[h], g[nt][2 * h]);
+              if (j + 1 < N) rmx[h] = fmaxf(rmx[h], g[nt][2 * h + 1]);
+            }
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          rmx[h] = fmaxf(rmx[h], __shfl_xor_sync(0xffffffffu, rmx[h], 1));
+          rmx[h] = fmaxf(rmx[h], __shfl_xor_sync(0xffffffffu, rmx[h], 2));
+          const int ii = 16 * qt + 8 * h + gq;
+          if (ii < N) nb[h] = -rmx[h] * rk[h];   // c_inv = 1: the Gram is rho itself
+        }
       }
       float as_[NTT][4], at_[NTT][4];
 #pragma unroll

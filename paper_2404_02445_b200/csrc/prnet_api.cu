@@ -143,16 +143,13 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
 
 // 0 = warp_f32 (N <= 32, CUDA-core FP32), 1 = long_f32 (32 < N <= 512),
 // 2 = mma_f16x3 (N <= 32, M <= 32: mma.sync tensor cores, split-fp16 3-product),
-// 3 = tc_fold (S = 24, 16 < N <= 32, M <= 32: fold on tcgen05 / TMEM, rest as 2).
-bool tc_applicable(const prnet_handle* h) {
-  return h->cfg.seg_len == 24 && h->N > 16 && h->N <= 32 && h->M <= 32;
-}
+// 3, 4 = retired (round-1 tcgen05 prototypes tc_fold / tc_full, superseded by 6).
 // 5 = flash_f16x3 (16 < N <= 512, S <= 96, M <= 32: key-streaming mma.sync, long lookbacks)
 bool flash_applicable(const prnet_handle* h) {
   return h->N > 16 && h->N <= 512 && h->cfg.seg_len <= 96 && h->M <= 32;
 }
-// 4 = tc_full (S = 24, N <= 32, M <= 32: Gram, fold and head on tcgen05 / TMEM)
-bool tc2_applicable(const prnet_handle* h) {
+// the tcgen05 head tile (pack_tc_head) is packed for every S = 24, N <= 32, M <= 32 handle
+bool tc_head_shape(const prnet_handle* h) {
   return h->cfg.seg_len == 24 && h->N <= 32 && h->M <= 32;
 }
 // 6 = tc_quad (S = 24, N <= 32, M <= 32, tau_s >= 1/80: quads of series on tcgen05 / TMEM,
@@ -175,10 +172,10 @@ bool comp_on(const prnet_handle* h) {
 bool variant_supports_widening(const prnet_handle* h, int v) {
   if (h->cfg.ma_kernel > 0) return v == 1 || v == 2;
   if (comp_on(h)) return v == 1 || v == 2 || v == 5;
-  return v == 1 || v == 2 || v == 5 || v == 6 || v == 8;
+  return v == 1 || v == 2 || v == 5 || v == 6;
 }
 const char* kWideningMsg =
-    "metric_variant bit 1 / instance_norm need tc_pipe, tc_quad, mma_f16x3 (N <= 32), "
+    "metric_variant bit 1 / instance_norm need tc_quad, mma_f16x3 (N <= 32), "
     "flash_f16x3 (16 < N <= 512, S <= 96, M <= 32) or long_f32 (N <= 512); metric_variant "
     "bit 2 needs mma_f16x3 (N <= 32, M <= 32, S <= 128), flash_f16x3 or long_f32; ma_kernel "
     "needs mma_f16x3 (N <= 32, M <= 32, S <= 128) or long_f32 (any N <= 512)";
@@ -205,7 +202,7 @@ int pick_variant(const prnet_handle* h) {
     }
     // (widened, the generic mma_f16x3 path is slower than tc_quad's WIDE instantiation from
     // N = 14 on: stress L336/S24 0.278 vs 0.259 ms; equal at N = 8)
-    if (tcq_applicable(h) && h->N > 8) return 8;
+    if (tcq_applicable(h) && h->N > 8) return 6;
     if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
     if (flash_applicable(h)) return 5;
     return 1;   // long_f32: any S and M (N <= 512), e.g. N <= 32 with S > 128
@@ -214,10 +211,9 @@ int pick_variant(const prnet_handle* h) {
   // sweep 2-9x over tc_quad / mma_f16x3) and the fastest N <= 16 path for S > 64 (2.3x);
   // tc_quad the fastest S = 24 path for N > 16 (Traffic 5.4 ms vs 6.6 ms for mma_f16x3; its
   // MMA tiles pad N to 32, so mma_f16x3 wins at N = 14: 0.166 vs 0.255 ms); mma_f16x3 the
-  // fastest other N <= 32 path; tc_fold and tc_full are selectable with
-  // prnet_set_kernel_variant
+  // fastest other N <= 32 path
   if (small_applicable(h) && (h->N <= 8 || h->cfg.seg_len > 64)) return 7;
-  if (tcq_applicable(h) && h->N > 16) return 8;
+  if (tcq_applicable(h) && h->N > 16) return 6;
   if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
   if (h->N > 32 && flash_applicable(h)) return 5;
   return h->N <= 32 ? 0 : 1;
@@ -242,10 +238,10 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
     return fail(h, PRNET_ERR_UNSUPPORTED, kWideningMsg);
   if (a_s != nullptr) {
     // prnet_debug_attention: the dump is written by warp_f32 (the plain reading and the
-    // level-only trend), mma_f16x3, long_f32 (every flag) and tc_pipe (detrend /
-    // instance_norm), each from the values its own fold consumes; small_f32 and tc_quad map
-    // to mma_f16x3 (same domain, every flag), flash_f16x3 to long_f32 (every flag and N)
-    if (v == 7 || v == 6) v = 2;
+    // level-only trend), mma_f16x3, long_f32 (every flag) and tc_quad (detrend /
+    // instance_norm), each from the values its own fold consumes; small_f32 maps to
+    // mma_f16x3 (same domain, every flag), flash_f16x3 to long_f32 (every flag and N)
+    if (v == 7) v = 2;
     if (v == 5) v = 1;
     if (v == 0 && widening_on(h)) v = 1;
   }
@@ -253,16 +249,7 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
     const char* e = getenv("PRNET_WINDOWS_PER_CTA");
     return e ? atoi(e) : 0;
   }();
-  if (v == 8) {
-    prnet::TcqPlan p;
-    if (!prnet::plan_tcp_kernel(a, h->max_smem_optin, h->sm_count, &p))
-      return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the tc_pipe kernel");
-    if (wpc_env > 0) {
-      p.wins_per_group = (wpc_env + 3) & ~3;
-      p.ctas_per_channel = 0;
-    }
-    e = prnet::launch_tcp_kernel(a, p, st);
-  } else if (v == 7) {
+  if (v == 7) {
     prnet::SmallPlan p;
     if (!prnet::plan_small_kernel(a, h->max_smem_optin, &p))
       return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the small_f32 kernel");
@@ -282,18 +269,6 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
     if (!prnet::plan_flash_kernel(a, h->max_smem_optin, &p))
       return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the flash kernel");
     e = prnet::launch_flash_kernel(a, p, st);
-  } else if (v == 4) {
-    prnet::Tc2Plan p;
-    if (!prnet::plan_tc2_kernel(a, h->max_smem_optin, &p))
-      return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the tcgen05 kernel");
-    if (wpc_env > 0) p.wins_per_group = (wpc_env + 3) & ~3;
-    e = prnet::launch_tc2_kernel(a, p, st);
-  } else if (v == 3) {
-    prnet::TcPlan p;
-    if (!prnet::plan_tc_kernel(a, h->max_smem_optin, &p))
-      return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the tcgen05 kernel");
-    if (wpc_env > 0) p.wins_per_cta = (wpc_env + 3) & ~3;
-    e = prnet::launch_tc_kernel(a, p, st);
   } else if (v == 2) {
     prnet::MmaPlan p;
     if (!prnet::plan_mma_kernel(a, h->max_smem_optin, &p))
@@ -496,7 +471,7 @@ prnet_status prnet_load_params(prnet_handle* h, const float* w_seasonal, const f
             cudaSuccess)
       return cuda_fail(h, e, "cudaMemcpy(flash head)");
   }
-  if (tc2_applicable(h)) {  // the same head as the tcgen05 B operand (K-major core matrices)
+  if (tc_head_shape(h)) {  // the same head as the tcgen05 B operand (K-major core matrices)
     const int bytes = prnet::tc_wpack_bytes();
     std::vector<unsigned char> pack((size_t)h->Cw * bytes);
     std::vector<float> inv(h->Cw);
@@ -788,11 +763,11 @@ prnet_status prnet_backward_head(prnet_handle* h, const float* x, int64_t batch,
 
 prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {
   if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
-  if (variant < -1 || variant > 8)
-    return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,...,8}");
-  if (variant == 8 && !tcq_applicable(h))
-    return fail(h, PRNET_ERR_UNSUPPORTED,
-                "tc_pipe variant needs S = 24, N <= 32, M <= 32, tau_seasonal >= 1/80");
+  if (variant < -1 || variant > 7)
+    return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,...,7}");
+  if (variant == 3 || variant == 4)
+    return fail(h, PRNET_ERR_INVALID_ARG,
+                "variants 3 (tc_fold) and 4 (tc_full) are retired: 6 (tc_quad) supersedes them");
   if (variant == 7 && !small_applicable(h))
     return fail(h, PRNET_ERR_UNSUPPORTED, "small_f32 variant needs N <= 16, S <= 128, M <= 32");
   if (variant == 6 && !tcq_applicable(h))
@@ -804,10 +779,6 @@ prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {
                 "softmax shift); warp_f32 and long_f32 take any temperature");
   if (variant == 5 && !flash_applicable(h))
     return fail(h, PRNET_ERR_UNSUPPORTED, "flash variant needs 16 < N <= 512, S <= 96, M <= 32");
-  if (variant == 4 && !tc2_applicable(h))
-    return fail(h, PRNET_ERR_UNSUPPORTED, "tc_full variant needs S = 24, N <= 32, M <= 32");
-  if (variant == 3 && !tc_applicable(h))
-    return fail(h, PRNET_ERR_UNSUPPORTED, "tc_fold variant needs S = 24, 16 < N <= 32, M <= 32");
   if ((variant == 0 || variant == 2) && h->N > 32)
     return fail(h, PRNET_ERR_UNSUPPORTED, "variant needs N <= 32");
   if (variant == 2 && (h->M > 32 || h->cfg.seg_len > 128))

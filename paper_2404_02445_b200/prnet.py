@@ -25,8 +25,9 @@ EXPORTS = ("prnet_create", "prnet_load_params", "prnet_forward", "prnet_forward_
            "prnet_debug_segments", "prnet_debug_attention", "prnet_error_sums",
            "prnet_forward_plan", "prnet_set_kernel_variant", "prnet_forward_sliding",
            "prnet_forward_sliding_host", "prnet_backward_head")
-VARIANTS = ("warp_f32", "long_f32", "mma_f16x3", "tc_fold", "tc_full", "flash_f16x3", "tc_quad", "small_f32",
-            "tc_pipe")
+# index = the C ABI's variant id (include/prnet.h); 3 and 4 are retired round-1 prototypes
+VARIANTS = ("warp_f32", "long_f32", "mma_f16x3", "retired_tc_fold", "retired_tc_full",
+            "flash_f16x3", "tc_quad", "small_f32")
 
 
 class PrnetError(RuntimeError):

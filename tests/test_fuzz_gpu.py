@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 import synth
-from parity_util import assert_parity
+from parity_util import assert_parity, assert_parity_revin
 
 pytestmark = pytest.mark.gpu
 
@@ -52,10 +52,10 @@ def test_fuzz_forward(oracle_mod, k):
     _, y64 = oracle_mod.forward(x, S, H, ws, wt, b, cf["hpc"], cf["tau_s"], cf["tau_t"],
                                 metric_variant=cf["mv"], instance_norm=cf["rev"],
                                 ma_kernel=cf["ma"])
-    scale = None
-    if cf["rev"]:
-        scale = np.maximum(np.abs(x).max(axis=2, keepdims=True)[..., :1], 1.0)
-    assert_parity(y, y64, scale=scale)
+    if cf["rev"]:   # reading R-tol-revin
+        assert_parity_revin(y, y64, x, S)
+    else:
+        assert_parity(y, y64)
 
 
 @pytest.mark.parametrize("k", range(40))

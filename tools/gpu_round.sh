@@ -12,7 +12,7 @@ step 120 $OUT/smoke.log python -c "import __graft_entry__ as g; g.smoke()" || ex
 step 900 $OUT/pytest_gpu.log python -m pytest tests -m gpu -q
 timeout -s KILL 600 python bench.py > $OUT/bench_default.json 2> $OUT/bench_default.err; [ $? -eq 137 ] && exit 3
 timeout -s KILL 400 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_reference.json 2> $OUT/bench_reference.err; [ $? -eq 137 ] && exit 3
-SWEEP="${SWEEP:-tc_quad:0 mma_f16x3:0 tc_fold:0 tc_full:0 warp_f32:0}" step 600 $OUT/sweep.log ./tools/sweep.sh
+SWEEP="${SWEEP:-tc_quad:0 mma_f16x3:0 warp_f32:0}" step 600 $OUT/sweep.log ./tools/sweep.sh
 for wl in ${EXTRA_WORKLOADS:-weather_h96 electricity stress_L720_S24_H96 stress_L1440_S24_H96 stress_L5760_S12_H96}; do
   timeout -s KILL 300 python bench.py --workload $wl --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/bench_$wl.json 2> $OUT/bench_$wl.err; [ $? -eq 137 ] && exit 3
 done

@@ -9,13 +9,15 @@ if [ -n "${K:-}" ]; then
   echo "rc=$?" >> $OUT/pytest_iter.log; tail -5 $OUT/pytest_iter.log
 fi
 : > $OUT/ab.jsonl
+for wl in ${WLS:-${WL:-traffic}}; do
 for rep in 1 2; do
-  for v in ${VARIANTS:-tc_quad tc_pipe}; do
+  for v in ${VARIANTS:-tc_quad}; do
     for lib in ${LIBS:-libprnet.so}; do
-      PRNET_LIB=$PWD/paper_2404_02445_b200/$lib timeout -s KILL 200 python bench.py --workload ${WL:-traffic} --variant $v --steps 20 --warmup 5 --no-cpu-baseline --no-e2e ${BENCH_EXTRA:-} > $OUT/ab_$v.json 2> $OUT/ab_$v.err
-      python -c "import json; d=json.load(open('$OUT/ab_$v.json')); print(json.dumps({'v':'$v','lib':'$lib','rep':$rep,'ms':round(d['ms_per_step'],4),'frac':round(d['roofline']['frac'],4),'mhz':d.get('clocks',{}).get('sm_mhz')}))" >> $OUT/ab.jsonl 2>>$OUT/ab_err.log
+      PRNET_LIB=$PWD/paper_2404_02445_b200/$lib timeout -s KILL 200 python bench.py --workload $wl --variant $v --steps 20 --warmup 5 --no-cpu-baseline --no-e2e ${BENCH_EXTRA:-} > $OUT/ab_$v.json 2> $OUT/ab_$v.err
+      python -c "import json; d=json.load(open('$OUT/ab_$v.json')); print(json.dumps({'wl':'$wl','v':'$v','lib':'$lib','rep':$rep,'ms':round(d['ms_per_step'],4),'frac':round(d['roofline']['frac'],4),'mhz':d.get('clocks',{}).get('sm_mhz')}))" >> $OUT/ab.jsonl 2>>$OUT/ab_err.log
     done
   done
+done
 done
 cat $OUT/ab.jsonl
 if [ -n "${NCU:-}" ]; then

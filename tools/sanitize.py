@@ -11,8 +11,8 @@ import synth  # noqa: E402
 from paper_2404_02445_b200 import PRNet  # noqa: E402
 
 CASES = [  # (L, S, H, variants)
-    (720, 24, 720, ["tc_quad", "mma_f16x3", "tc_fold", "tc_full", "warp_f32"]),
-    (96, 24, 96, ["tc_quad", "mma_f16x3", "tc_full", "warp_f32"]),
+    (720, 24, 720, ["tc_quad", "mma_f16x3", "warp_f32"]),
+    (96, 24, 96, ["tc_quad", "mma_f16x3", "warp_f32"]),
     (100, 24, 90, ["tc_quad"]),
     (97, 7, 13, ["mma_f16x3", "warp_f32", "long_f32"]),
     (1440, 24, 96, ["flash_f16x3", "long_f32"]),
