@@ -50,6 +50,27 @@ def flops_per_series(N, S, M):
     return 2 * N * N * S + 4 * M * N * N + 2 * M * N * S
 
 
+def _up(v, m):
+    return -(-v // m) * m
+
+
+def tensor_flops_per_series(variant, N, S, M):
+    """FLOPs the tensor cores are ISSUED per series by a tensor-core variant (split-fp16 hi/lo:
+    3 products per contraction, tiles padded to the MMA shapes), or None for the CUDA-core
+    FP32 variants.  tc_quad: Gram of a quad on tcgen05 (M = N = 128, 5 K-steps of 16; 4x of
+    it is the discarded off-diagonal blocks), fold on tcgen05 (12 MMAs M = 128, N = 32,
+    K = 16 per quad), head on mma.sync (36 m16n8k16 per series).  mma_f16x3 / flash_f16x3:
+    m16n8k16 tiles of the Gram, of the fold (mma) or of P = E X (flash), and of the head."""
+    NP, MP, SP, KZ = _up(N, 16), _up(M, 16), _up(S, 8), _up(S, 16)
+    if variant == "tc_quad":
+        return (5 * 2 * 128 * 128 * 16 + 12 * 2 * 128 * 32 * 16) / 4 + 36 * 2 * 16 * 8 * 16
+    if variant == "mma_f16x3":
+        return 3 * 2 * (NP * NP * KZ + 2 * MP * NP * NP + MP * SP * NP)
+    if variant == "flash_f16x3":
+        return 3 * 2 * (NP * NP * KZ + 2 * NP * NP * SP + 2 * MP * NP * SP)
+    return None
+
+
 # inputs up to this size get an L2 flush between timed steps (B200 L2: 126 MB)
 L2_FLUSH_BELOW = 256 << 20
 
@@ -245,7 +266,10 @@ def main():
         ob = CpuOracleBench(w.name, args.seed, budget_s=per_step)
         for _ in range(args.warmup):
             ob.step()
-        rates = [ob.step() for _ in range(args.steps)]
+        rates, sample_s = [], []
+        for _ in range(args.steps):
+            rates.append(ob.step())
+            sample_s.append(ob.compute)
         value = len(rates) / sum(1.0 / r for r in rates)      # windows / total time
         sample = ob.describe()
         cores = len(ob.jobs)
@@ -254,6 +278,11 @@ def main():
             "impl": "reference", "metric": METRIC, "value": value, "unit": "windows/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * B / value, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step_note": ("EXTRAPOLATED to the whole workload from the measured sample "
+                                 "rate; each timed step runs only the sample "
+                                 "(sample_ms_per_step, measured)"),
+            "sample_ms_per_step": 1e3 * statistics.mean(sample_s),
+            "sample_windows_per_step": len(ob.widx),
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
             "cpu_baseline": {"value": value, "unit": "windows/s", "cores": cores,
                              "kind": "oracle", "sample": sample},
@@ -332,14 +361,21 @@ def main():
     flush = None
     if count * w.C * w.L * 4 <= L2_FLUSH_BELOW or args.sliding:
         flush = torch.empty(512 << 18, dtype=torch.float32, device=dev)   # 512 MB
+    nvtx = torch.cuda.nvtx
     with ClockSampler(dev) as clk:
         t_wall = time.perf_counter()
-        for e0, e1 in ev:
+        nvtx.range_push(f"bench timed region: {args.steps} steps of {w.name}")
+        for k, (e0, e1) in enumerate(ev):
             if flush is not None:
+                nvtx.range_push("L2 flush (untimed)")
                 flush.zero_()
+                nvtx.range_pop()
+            nvtx.range_push(f"step {k}: prnet_forward ({count} windows x {w.C} channels)")
             e0.record(stream)
             fwd()
             e1.record(stream)
+            nvtx.range_pop()
+        nvtx.range_pop()
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall
     if world > 1:
@@ -443,6 +479,11 @@ def main():
             traffic = None if (widened or t_full is None) else t_full * count / w.windows
         except Exception:
             traffic = None
+    traffic_src = ("STATIC: dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full "
+                   "capture of this workload's launch (profiles/ncu_traffic.json, tools/"
+                   "summarize_profile.py), scaled to this rank's windows; not measured in this run"
+                   if traffic is not None else "no ncu capture for this mode")
+    tflops = tensor_flops_per_series(plan["variant"], N, w.S, M)
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline and not (args.metric_variant or args.instance_norm
@@ -464,12 +505,25 @@ def main():
         "hbm_gbs": B * w.C * bytes_per_series / (ms_per_step / 1e3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak_gbs, "unit": "GB/s",
                      "frac": achieved_gbs / peak_gbs, "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "kernel": f"prnet_fwd_{plan['variant']}", "launch_ms": launch_ms,
                      "bytes_per_launch": launch_bytes, "peak_source": peak_src},
-        "roofline_alu": {"bound": "alu", "achieved": achieved_tf, "unit": "TFLOP/s",
-                         "peak": fp32_peak, "frac": achieved_tf / fp32_peak,
-                         "flops_per_series": fl,
-                         "peak_note": "FP32 FFMA: 148 SMs x 128 lanes x 2 x max SM clock"},
+        "roofline_compute": (
+            {"bound": "tensor", "unit": "TFLOP/s",
+             "achieved": count * w.C * tflops / (launch_ms / 1e3) / 1e12,
+             "peak": float(peaks.get("bf16_tflops_sustained", 1400.0)),
+             "frac": count * w.C * tflops / (launch_ms / 1e3) / 1e12
+             / float(peaks.get("bf16_tflops_sustained", 1400.0)),
+             "issued_flops_per_series": tflops, "algorithmic_flops_per_series": fl,
+             "peak_source": f"{peak_src}: bf16_tflops_sustained (f16 dense = bf16 rate)",
+             "note": "ISSUED tensor FLOPs: split-fp16 3 products, tile padding, tc_quad's "
+                     "block-diagonal Gram waste; the mma.sync share runs at ~1/4 of the "
+                     "tcgen05 peak (profiles/r01_microbench.txt: 554 TF/s)"}
+            if tflops is not None else
+            {"bound": "alu", "achieved": achieved_tf, "unit": "TFLOP/s",
+             "peak": fp32_peak, "frac": achieved_tf / fp32_peak,
+             "flops_per_series": fl,
+             "peak_note": "FP32 FFMA: 148 SMs x 128 lanes x 2 x max SM clock (CUDA-core variant)"}),
         "accuracy": {"mse": mse, "mae": mae},
         "cpu_baseline": cpu,
         "e2e": e2e,
