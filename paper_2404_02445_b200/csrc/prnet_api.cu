@@ -148,14 +148,20 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
 bool flash_applicable(const prnet_handle* h) {
   return h->N > 16 && h->N <= 512 && h->cfg.seg_len <= 96 && h->M <= 32;
 }
-// the tcgen05 head tile (pack_tc_head) is packed for every S = 24, N <= 32, M <= 32 handle
+// the tcgen05 head tile (pack_tc_head) is packed for every N <= 32, M <= 32 handle with a
+// tc_quad instantiation (S = 24: fwd_tcq.cu; S in {12, 16, 32, 48, 64, 96}: fwd_tcg.cu)
 bool tc_head_shape(const prnet_handle* h) {
-  return h->cfg.seg_len == 24 && h->N <= 32 && h->M <= 32;
+  return (h->cfg.seg_len == 24 || prnet::tcg_supported_s(h->cfg.seg_len)) && h->N <= 32 &&
+         h->M <= 32;
 }
 // 6 = tc_quad (S = 24, N <= 32, M <= 32, tau_s >= 1/80: quads of series on tcgen05 / TMEM,
 // seasonal shift 1 >= rho keeps the diagonal term normal only down to tau_s = 1/80)
 bool tcq_applicable(const prnet_handle* h) {
-  return h->cfg.seg_len == 24 && h->N <= 32 && h->M <= 32 && h->cfg.tau_seasonal >= 0.0125f;
+  return tc_head_shape(h) && h->cfg.tau_seasonal >= 0.0125f;
+}
+// the widening flags are compiled into the S = 24 kernel only (its WIDE instantiation)
+bool tcq_wide_applicable(const prnet_handle* h) {
+  return tcq_applicable(h) && h->cfg.seg_len == 24;
 }
 // Variants that implement the SURVEY §8(f) widening: the level-only trend runs in every
 // kernel (a.vtrend = 0); the detrended seasonal metric and instance normalisation in
@@ -172,7 +178,7 @@ bool comp_on(const prnet_handle* h) {
 bool variant_supports_widening(const prnet_handle* h, int v) {
   if (h->cfg.ma_kernel > 0) return v == 1 || v == 2;
   if (comp_on(h)) return v == 1 || v == 2 || v == 5;
-  return v == 1 || v == 2 || v == 5 || v == 6;
+  return v == 1 || v == 2 || v == 5 || (v == 6 && h->cfg.seg_len == 24);
 }
 const char* kWideningMsg =
     "metric_variant bit 1 / instance_norm need tc_quad, mma_f16x3 (N <= 32), "
@@ -202,7 +208,7 @@ int pick_variant(const prnet_handle* h) {
     }
     // (widened, the generic mma_f16x3 path is slower than tc_quad's WIDE instantiation from
     // N = 14 on: stress L336/S24 0.278 vs 0.259 ms; equal at N = 8)
-    if (tcq_applicable(h) && h->N > 8) return 6;
+    if (tcq_wide_applicable(h) && h->N > 8) return 6;
     if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
     if (flash_applicable(h)) return 5;
     return 1;   // long_f32: any S and M (N <= 512), e.g. N <= 32 with S > 128
@@ -255,7 +261,7 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
       return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the small_f32 kernel");
     if (wpc_env > 0) p.wins_per_cta = wpc_env;
     e = prnet::launch_small_kernel(a, p, st);
-  } else if (v == 6) {
+  } else if (v == 6 && h->cfg.seg_len == 24) {
     prnet::TcqPlan p;
     if (!prnet::plan_tcq_kernel(a, h->max_smem_optin, h->sm_count, &p))
       return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the tc_quad kernel");
@@ -264,6 +270,15 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
       p.ctas_per_channel = 0;
     }
     e = prnet::launch_tcq_kernel(a, p, st);
+  } else if (v == 6) {
+    prnet::TcqPlan p;
+    if (!prnet::plan_tcg_kernel(a, h->max_smem_optin, h->sm_count, &p))
+      return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the tc_quad kernel");
+    if (wpc_env > 0) {
+      p.wins_per_group = (wpc_env + 3) & ~3;
+      p.ctas_per_channel = 0;
+    }
+    e = prnet::launch_tcg_kernel(a, p, st);
   } else if (v == 5) {
     prnet::FlashPlan p;
     if (!prnet::plan_flash_kernel(a, h->max_smem_optin, &p))
@@ -772,7 +787,7 @@ prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {
     return fail(h, PRNET_ERR_UNSUPPORTED, "small_f32 variant needs N <= 16, S <= 128, M <= 32");
   if (variant == 6 && !tcq_applicable(h))
     return fail(h, PRNET_ERR_UNSUPPORTED,
-                "tc_quad variant needs S = 24, N <= 32, M <= 32, tau_seasonal >= 1/80");
+                "tc_quad variant needs S in {12, 16, 24, 32, 48, 64, 96}, N <= 32, M <= 32, tau_seasonal >= 1/80");
   if ((variant == 2 || variant == 5 || variant == 7) && !known_max_ok(h))
     return fail(h, PRNET_ERR_UNSUPPORTED,
                 "small_f32 / mma_f16x3 / flash_f16x3 need tau_seasonal >= 1/320 (known-maximum "
