@@ -1,0 +1,614 @@
+// fwd_tcl.cu -- "tc_long": the PRNet pattern-attention forward for long lookbacks
+// (32 < N <= 512 segments, S in {12, 24, 48, 96}, M <= 32; the long end of the BASELINE.json
+// configs[4] stress sweep) on the 5th-gen tensor cores, flash-attention style.
+//
+// Same reading (SURVEY §8(c) Definition steps 1-11) and split-fp16 3-product
+// arithmetic as every other variant.  One CTA of 16 warps owns one series at a
+// time (the CTA walks a contiguous window range of one channel):
+//
+//  a1/a2  the series (N S floats) arrives by 1-D bulk copies into one of two staging buffers
+//         (the next series is fetched while this one is processed); thread r computes the
+//         descriptors of segment r and writes its Z' row (K-major, [hi t | lo t]) and its X'
+//         row (MN-major B operand, [t][key]) as split fp16; sigma^2 and the X' scale are CTA
+//         reductions;
+//  a3     per (query tile of 128 rows, key tile of 64 rows): G = Z'_q Z'_k^T on tcgen05.mma
+//         (SS, TMEM accumulator, 64 columns);
+//  a4/a5  thread (row quarter w%4, column quarter w/4) reads 16 columns of its row of G
+//         (tcgen05.ld), forms the seasonal exponentials 2^((rho_ij - f_i) ks) with the KNOWN row
+//         bound f_i = nu_i / sqrt(nu_i^2 + eps_s) >= rho_ij (Cauchy-Schwarz; no online
+//         rescaling) and the trend exponentials 2^(-(mu~_i - mu~_j)^2 - (k~_i - k~_j)^2) (row max
+//         0 at j = i), accumulates row sums, and stores E as split fp16 into TMEM (two
+//         buffers, so the next key tile's exponentials never wait for this tile's MMA);
+//  a6     P_s += E_s X'_k, P_t += E_t X'_k on tcgen05.mma (TS: E from TMEM, X' from shared
+//         memory), P in TMEM; the Gram of the next tile is issued as soon as G is read;
+//  a7     per query tile, 4 warps fold the normalised patterns into the head (per-warp
+//         mma.sync, W' fragments from the flash head pack, P^T by movmatrix), partial Y in
+//         fixed-order shared-memory slots;
+//  a8     y = Y / (sw sx) + b, coalesced stores by the whole CTA.
+//
+// TMEM (512 columns): G [0,64) | E buffer 0 [64,192) | E buffer 1 [192,320) | P_s, P_t
+// [320, 320 + 2 SP); an E buffer = E_s hi, E_s lo, E_t hi, E_t lo (32 columns each: 64 keys
+// packed two per column).  Every tcgen05.mma is issued by thread 0, so each commit covers all
+// earlier MMAs: waiting for the Gram of tile k+2 also proves the P-MMA of tile k (the reader
+// of the E buffer about to be rewritten) complete.
+#include <cuda_fp16.h>
+
+#include <cmath>
+
+#include "tc_common.cuh"
+
+namespace prnet {
+using namespace tcq;
+
+namespace {
+
+template <int S>
+struct TclCfg {
+  static_assert(S % 4 == 0 && S <= 96, "S");
+  static constexpr int SP = (S + 15) / 16 * 16;   // Gram K per product; P columns
+  static constexpr int NCT = (S + 7) / 8;         // head n-tiles
+  static constexpr int NQ = S / 4;
+  static constexpr int PITCH = ((S / 4) & 1) ? 4 * S : 4 * S + 16;   // staging row bytes
+  static constexpr bool ROWCOPY = PITCH != 4 * S;
+  static constexpr int SBO = 32 * SP;             // Z' row block stride (8 rows x 2 SP halves)
+  static constexpr uint32_t TG = 0, TE0 = 64, TE1 = 192, TP = 320;
+  static_assert(TP + 2 * SP <= 512, "TMEM");
+};
+
+__device__ __forceinline__ void sts128(unsigned char* p, uint4 v) {
+  *reinterpret_cast<uint4*>(p) = v;
+}
+__device__ __forceinline__ void bulk_copy_tx(void* dst, const void* src, uint32_t bytes,
+                                             uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+template <int S>
+__device__ __forceinline__ constexpr float ttl(int t) {
+  return (float)t - 0.5f * (float)(S - 1);
+}
+__device__ __forceinline__ void tld_x16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : PRNET_TLD_R8(r, 0), PRNET_TLD_R8(r, 8)
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tst_x8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+      : "memory");
+}
+// 16x256b.x1: thread t <- lanes base + t/4 and base + 8 + t/4, columns 2(t%4), 2(t%4)+1
+__device__ __forceinline__ void tld16_x1(uint32_t taddr, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
+// A fragment (16 x 16, rows r0.., cols c0..) of a row-major global fp16 matrix
+__device__ __forceinline__ void ldg_afrag16(const __half* base, int ld, int r0, int c0, int lane,
+                                            uint32_t (&f)[4]) {
+  const int g = lane >> 2, c = lane & 3;
+  const __half* p = base + (size_t)(r0 + g) * ld + c0 + 2 * c;
+  f[0] = __ldg(reinterpret_cast<const unsigned int*>(p));
+  f[1] = __ldg(reinterpret_cast<const unsigned int*>(p + 8 * ld));
+  f[2] = __ldg(reinterpret_cast<const unsigned int*>(p + 8));
+  f[3] = __ldg(reinterpret_cast<const unsigned int*>(p + 8 * ld + 8));
+}
+
+}  // namespace
+
+template <int S, int MT>
+__global__ void __launch_bounds__(512, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLayout ly,
+                                                                int ctas_per_channel) {
+  using K = TclCfg<S>;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const int wq = warp & 3, wc = warp >> 2;   // row quarter (TMEM lanes), column quarter
+  const int c = blockIdx.y;
+  const int cw = a.head_per_channel ? c : 0;
+  const int N = a.N, M = a.M, H = a.H, C = a.C;
+  const int NQT = ly.nqt, NKT = ly.nkt, NK = 64 * NKT;
+
+  unsigned char* zt = smem + ly.off_z;
+  unsigned char* xhi = smem + ly.off_x;
+  unsigned char* xlo = xhi + 2 * K::SP * NK;
+  unsigned char* const stg0 = smem + ly.off_stage;
+  float* fks = reinterpret_cast<float*>(smem + ly.off_vec);    // [Rpad] f_i ks (seasonal shift)
+  float* mtv = fks + ly.rpad;                                  // [Rpad] mu~
+  float* ktv = mtv + ly.rpad;                                  // [Rpad] kappa~
+  float* lpart = ktv + ly.rpad;                                // [2][4][128] row-sum partials
+  float* red = lpart + 2 * 4 * 128;                            // [16][4] reduction scratch
+  float* yslot = reinterpret_cast<float*>(smem + ly.off_y);    // [4][16 MT][8 NCT]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ly.off_bar);
+  uint64_t* mbarG = bars + 0;
+  uint64_t* mbarP = bars + 1;
+  uint64_t* xbar = bars + 2;                                   // + buffer
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + ly.off_bar + 64);
+  constexpr int YW = 16 * MT * 8 * K::NCT;                     // floats per Y slot
+
+  if (tid == 0) {
+    for (int k = 0; k < 4; k++) mbar_init(bars + k, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int k = tid; k < 4 * YW; k += 512) yslot[k] = 0.f;
+  if (warp == 0) tmem_alloc(tmem_slot, 512);
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem0 = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  const uint32_t tl = tmem0 + ((uint32_t)(32 * wq) << 16);   // this warp's lanes
+  const uint32_t z_s = smem_u32(zt), xhi_s = smem_u32(xhi), xlo_s = smem_u32(xlo);
+  const float inv_sw = __ldg(a.wpack_flash_inv_sw + cw);
+  const int npf = (N + 15) & ~15;                 // the flash head pack's K padding
+  const int ldw = 2 * npf;
+  const __half* whi = reinterpret_cast<const __half*>(a.wpack_flash) +
+                      (size_t)cw * (ly.wpack_bytes / 2);
+  const __half* wlo = whi + (M <= 16 ? 16 : 32) * ldw;
+
+  const int64_t b0 = a.B * blockIdx.x / ctas_per_channel;
+  const int64_t b1 = a.B * (blockIdx.x + 1) / ctas_per_channel;
+  const int NS = N * S;
+  const bool bulk = a.x_vec;
+  auto xptr = [&](int64_t b) { return a.x + b * a.xsb + c * a.xsc + a.r; };
+  // series -> staging buffer (thread 0 arms the barrier; row copies by warp 0's lanes, or one
+  // span copy; unaligned windows: 4-byte cp.async by the whole CTA, waited with the barrier)
+  auto issue_load = [&](int64_t b, int buf) {
+    const float* xg = xptr(b);
+    unsigned char* st = stg0 + (buf ? ly.stage_bytes : 0);
+    if (bulk) {
+      if (warp == 0) {
+        if constexpr (K::ROWCOPY) {
+          if (lane == 0) mbar_expect(xbar + buf, (uint32_t)NS * 4u);
+          __syncwarp();
+          for (int n = lane; n < N; n += 32) bulk_copy_tx(st + n * K::PITCH, xg + n * S, 4u * S, xbar + buf);
+        } else {
+          if (lane == 0) bulk_load(st, xg, (uint32_t)NS * 4u, xbar + buf);
+        }
+      }
+    } else {
+      for (int k = tid; k < NS; k += 512) {
+        const int n = k / S, t = k - n * S;
+        cp_async4(st + n * K::PITCH + 4 * t, xg + k);
+      }
+      cp_async_commit();
+    }
+  };
+
+  uint32_t phG = 0, phP = 0, phX = 0;   // phX: bit k = parity of staging buffer k
+  if (b0 < b1) {
+    fence_proxy_async();
+    issue_load(b0, 0);
+  }
+  int buf = 0;
+  for (int64_t b = b0; b < b1; b++, buf ^= 1) {
+    // ---------------- a1+a2: wait for this series, prefetch the next one
+    if (bulk) {
+      mbar_wait_bounded(xbar + buf, (phX >> buf) & 1u);
+      phX ^= 1u << buf;
+    } else {
+      cp_async_wait_all();
+      __syncthreads();
+    }
+    if (b + 1 < b1) {
+      fence_proxy_async();
+      issue_load(b + 1, buf ^ 1);
+    }
+    const float4* st4 = reinterpret_cast<const float4*>(stg0 + (buf ? ly.stage_bytes : 0));
+    const int r = tid;                 // this thread's segment row (N <= 512)
+    const bool rv = r < N;
+    const float4* xr4 = st4 + (rv ? r : 0) * (K::PITCH / 16);
+    float mu = 0.f, kap = 0.f, nu2 = 0.f, x0 = 0.f, m1 = 0.f;
+    if (rv) {
+      x0 = reinterpret_cast<const float*>(xr4)[0];
+      const float2 nx0 = f2(-x0);
+      float2 s1a = f2(0.f), s1b = f2(0.f), s3a = f2(0.f), s3b = f2(0.f);
+#pragma unroll
+      for (int q = 0; q < K::NQ; q++) {
+        const float4 v = xr4[q];
+        const float2 d0 = add2(make_float2(v.x, v.y), nx0);
+        const float2 d1 = add2(make_float2(v.z, v.w), nx0);
+        s1a = add2(s1a, d0);
+        s1b = add2(s1b, d1);
+        s3a = fma2(make_float2(ttl<S>(4 * q), ttl<S>(4 * q + 1)), d0, s3a);
+        s3b = fma2(make_float2(ttl<S>(4 * q + 2), ttl<S>(4 * q + 3)), d1, s3b);
+      }
+      const float2 s1 = add2(s1a, s1b), s3 = add2(s3a, s3b);
+      m1 = (s1.x + s1.y) * a.inv_s;
+      mu = x0 + m1;
+      kap = (s3.x + s3.y) * a.inv_v;
+      const float2 nm1 = f2(-m1);
+      float2 qa = f2(0.f), qb = f2(0.f);
+#pragma unroll
+      for (int q = 0; q < K::NQ; q++) {
+        const float4 v = xr4[q];
+        const float2 z0 = add2(add2(make_float2(v.x, v.y), nx0), nm1);
+        const float2 z1 = add2(add2(make_float2(v.z, v.w), nx0), nm1);
+        qa = fma2(z0, z0, qa);
+        qb = fma2(z1, z1, qb);
+      }
+      const float2 q2 = add2(qa, qb);
+      nu2 = q2.x + q2.y;
+    }
+    // Z' row r = z / sqrt(nu2 + eps_s) (rows N..Rpad-1 zero)
+    if (r < ly.rpad) {
+      const float zsc = rv ? rsqrtf(nu2 + kEpsSeasonal) : 0.f;
+      const float2 zs2 = f2(zsc), nx0 = f2(-x0), nm1 = f2(-m1);
+      unsigned char* zr = zt + (r >> 3) * K::SBO + (r & 7) * 16;
+#pragma unroll
+      for (int ch = 0; ch < K::SP / 8; ch++) {
+        uint4 hv = make_uint4(0u, 0u, 0u, 0u), lv = make_uint4(0u, 0u, 0u, 0u);
+        if (8 * ch < S) {
+          const float4 v0 = xr4[2 * ch];
+          split2(mul2(add2(add2(make_float2(v0.x, v0.y), nx0), nm1), zs2), hv.x, lv.x);
+          split2(mul2(add2(add2(make_float2(v0.z, v0.w), nx0), nm1), zs2), hv.y, lv.y);
+          if (8 * ch + 4 < S) {
+            const float4 v1 = xr4[2 * ch + 1];
+            split2(mul2(add2(add2(make_float2(v1.x, v1.y), nx0), nm1), zs2), hv.z, lv.z);
+            split2(mul2(add2(add2(make_float2(v1.z, v1.w), nx0), nm1), zs2), hv.w, lv.w);
+          }
+        }
+        if (!rv) { hv = make_uint4(0u, 0u, 0u, 0u); lv = hv; }
+        sts128(zr + ch * 128, hv);
+        sts128(zr + (K::SP / 8 + ch) * 128, lv);
+      }
+    }
+    // CTA reductions: sum (mu - m0), sum [S (mu - m0)^2 + nu2] (sigma^2, Def 5, about the
+    // reference m0 = mu_0) and max (|mu| + |z|) (the X' scale); m0 from thread 0 via smem
+    if (tid == 0) red[63] = mu;
+    __syncthreads();
+    const float m0 = red[63];
+    {
+      const float dd = rv ? mu - m0 : 0.f;
+      float s_a = dd, s_b = rv ? fmaf((float)S * dd, dd, nu2) : 0.f;
+      const float bnd = rv ? fabsf(mu) + sqrtf(nu2) : 0.f;
+      s_a = warp_sum(s_a);
+      s_b = warp_sum(s_b);
+      const float mx = warp_max_nonneg(bnd);
+      if (lane == 0) {
+        red[3 * warp] = s_a;
+        red[3 * warp + 1] = s_b;
+        red[3 * warp + 2] = mx;
+      }
+    }
+    __syncthreads();
+    float sa = 0.f, sb = 0.f, mxa = 0.f;
+#pragma unroll
+    for (int w = 0; w < 16; w++) {
+      sa += red[3 * w];
+      sb += red[3 * w + 1];
+      mxa = fmaxf(mxa, red[3 * w + 2]);
+    }
+    const float var = fmaf(-(float)S * sa, sa * a.inv_n, sb) * a.inv_ns;
+    const float inv_var = 1.0f / (var + kEpsTrend);
+    const float sx = pow2_scale(mxa);
+    // X' row r (MN-major B of the P-MMA: element (t, key r) at (t/8) 16 NK + (r/8) 128 +
+    // (r%8) 16 + (t%8) 2), rows N..NK-1 zero; the per-row vectors
+    if (r < NK) {
+      const float2 xs2 = f2(rv ? sx : 0.f);
+#pragma unroll
+      for (int ch = 0; ch < K::SP / 8; ch++) {
+        uint4 hv = make_uint4(0u, 0u, 0u, 0u), lv = make_uint4(0u, 0u, 0u, 0u);
+        if (8 * ch < S) {
+          const float4 v0 = xr4[2 * ch];
+          split2(mul2(make_float2(v0.x, v0.y), xs2), hv.x, lv.x);
+          split2(mul2(make_float2(v0.z, v0.w), xs2), hv.y, lv.y);
+          if (8 * ch + 4 < S) {
+            const float4 v1 = xr4[2 * ch + 1];
+            split2(mul2(make_float2(v1.x, v1.y), xs2), hv.z, lv.z);
+            split2(mul2(make_float2(v1.z, v1.w), xs2), hv.w, lv.w);
+          }
+        }
+        const int o = ch * 16 * NK + (r >> 3) * 128 + (r & 7) * 16;
+        sts128(xhi + o, hv);
+        sts128(xlo + o, lv);
+      }
+    }
+    if (r < ly.rpad) {
+      // f_i = nu_i / sqrt(nu_i^2 + eps_s) >= rho_ij: the seasonal shift (rows >= N: 0)
+      fks[r] = rv ? sqrtf(nu2 / (nu2 + kEpsSeasonal)) * a.ks : 0.f;
+      mtv[r] = rv ? mu * sqrtf(inv_var * a.kt) : 0.f;
+      ktv[r] = rv ? kap * sqrtf(a.vtrend * inv_var * a.kt) : 0.f;
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    // ---------------- a3..a6 over (query tile, key tile)
+    auto issue_gram = [&](int qt, int kt) {
+      const uint32_t za = z_s + 16 * qt * K::SBO, zb = z_s + 8 * kt * K::SBO;
+      constexpr uint32_t LO = (K::SP / 8) * 128;
+      constexpr uint32_t id = idesc_f16(128, 64, false, false);
+#pragma unroll
+      for (int k = 0; k < K::SP / 16; k++) {
+        const uint32_t o = k * 256;
+        umma(tmem0 + K::TG, sdesc(za + o, 128, K::SBO), sdesc(zb + o, 128, K::SBO), id, k > 0);
+        umma(tmem0 + K::TG, sdesc(za + o, 128, K::SBO), sdesc(zb + LO + o, 128, K::SBO), id, true);
+        umma(tmem0 + K::TG, sdesc(za + LO + o, 128, K::SBO), sdesc(zb + o, 128, K::SBO), id, true);
+      }
+      umma_commit(mbarG);
+    };
+    if (tid == 0) issue_gram(0, 0);
+    const uint32_t sbo_x = 16u * (uint32_t)NK;
+    for (int qt = 0; qt < NQT; qt++) {
+      const int row = 128 * qt + 32 * wq + lane;   // this thread's query row
+      const bool warp_rows = 128 * qt + 32 * wq < N;   // warp-uniform: any valid row
+      const float fk = fks[row], mi = mtv[row], ki = ktv[row];
+      float ls = 0.f, lt = 0.f;
+      for (int kt = 0; kt < NKT; kt++) {
+        const int eb = kt & 1;
+        const uint32_t te = tmem0 + (eb ? K::TE1 : K::TE0);
+        mbar_wait_bounded(mbarG, phG);
+        phG ^= 1u;
+        tc_fence_after();
+        uint32_t g[16];
+        tld_x16(tl + K::TG + 16u * wc, g);
+        tld_wait();
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+        if (tid == 0) {   // the next Gram (G is read)
+          if (kt + 1 < NKT) issue_gram(qt, kt + 1);
+          else if (qt + 1 < NQT) issue_gram(qt + 1, 0);
+        }
+        const int j0 = 64 * kt + 16 * wc;           // this thread's first key
+        uint32_t eh[8], el[8], th[8], tlo[8];
+        if (warp_rows) {
+          const bool full = j0 + 16 <= N;
+          // seasonal: 2^(rho ks - f_i ks)
+          const float2 ks2 = f2(a.ks), nf2 = f2(-fk);
+          float2 sa2 = f2(0.f), sb2 = f2(0.f);
+#pragma unroll
+          for (int j = 0; j < 16; j += 2) {
+            const float2 arg = fma2(make_float2(__uint_as_float(g[j]), __uint_as_float(g[j + 1])), ks2, nf2);
+            float e0 = fast_ex2(arg.x), e1 = fast_ex2(arg.y);
+            if (!full) {
+              if (j0 + j >= N) e0 = 0.f;
+              if (j0 + j + 1 >= N) e1 = 0.f;
+            }
+            if (j & 2) sb2 = add2(sb2, make_float2(e0, e1));
+            else sa2 = add2(sa2, make_float2(e0, e1));
+            split2(make_float2(e0, e1), eh[j / 2], el[j / 2]);
+          }
+          const float2 s2 = add2(sa2, sb2);
+          ls += s2.x + s2.y;
+          // trend: 2^(-(mu~_i - mu~_j)^2 - (k~_i - k~_j)^2)
+          const float2 mi2 = f2(mi), ki2 = f2(ki);
+          const float4* cm4 = reinterpret_cast<const float4*>(mtv + j0);
+          const float4* ck4 = reinterpret_cast<const float4*>(ktv + j0);
+          float2 ta2 = f2(0.f), tb2 = f2(0.f);
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const float4 mj = cm4[q], kj = ck4[q];
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              const int j = 4 * q + 2 * h;
+              const float2 dm = add2(mi2, h ? make_float2(-mj.z, -mj.w) : make_float2(-mj.x, -mj.y));
+              const float2 dk = add2(ki2, h ? make_float2(-kj.z, -kj.w) : make_float2(-kj.x, -kj.y));
+              const float2 ex = fma2(make_float2(-dk.x, -dk.y), dk, mul2(make_float2(-dm.x, -dm.y), dm));
+              float e0 = fast_ex2(ex.x), e1 = fast_ex2(ex.y);
+              if (!full) {
+                if (j0 + j >= N) e0 = 0.f;
+                if (j0 + j + 1 >= N) e1 = 0.f;
+              }
+              if (h) tb2 = add2(tb2, make_float2(e0, e1));
+              else ta2 = add2(ta2, make_float2(e0, e1));
+              split2(make_float2(e0, e1), th[j / 2], tlo[j / 2]);
+            }
+          }
+          const float2 t2 = add2(ta2, tb2);
+          lt += t2.x + t2.y;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; j++) eh[j] = el[j] = th[j] = tlo[j] = 0u;
+        }
+        // E into TMEM buffer eb: [0,32) E_s hi, [32,64) E_s lo, [64,96) E_t hi, [96,128) E_t lo
+        // (this thread's 16 keys = 8 packed columns at 8 wc).  The P-MMA that last read this
+        // buffer (tile kt - 2) completed before the Gram just waited for.
+        tst_x8(te + ((uint32_t)(32 * wq) << 16) + 8u * wc, eh);
+        tst_x8(te + ((uint32_t)(32 * wq) << 16) + 32u + 8u * wc, el);
+        tst_x8(te + ((uint32_t)(32 * wq) << 16) + 64u + 8u * wc, th);
+        tst_x8(te + ((uint32_t)(32 * wq) << 16) + 96u + 8u * wc, tlo);
+        tst_wait();
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+        if (tid == 0) {
+          // P_s += E_s X'_k, P_t += E_t X'_k: M = 128, N = SP, K = 64 keys in 4 steps, hh, hl, lh
+          constexpr uint32_t id = idesc_f16(128, K::SP, false, true);
+#pragma unroll
+          for (int br = 0; br < 2; br++) {
+            const uint32_t dp = tmem0 + K::TP + (uint32_t)(br * K::SP);
+            const uint32_t ah = te + 64u * br, al = ah + 32u;
+#pragma unroll
+            for (int ks = 0; ks < 4; ks++) {
+              const uint32_t ob = (uint32_t)(1024 * kt + 256 * ks);
+              const uint64_t bh = sdesc(xhi_s + ob, 128, sbo_x), bl = sdesc(xlo_s + ob, 128, sbo_x);
+              umma_ts(dp, ah + 8u * ks, bh, id, kt > 0 || ks > 0);
+              umma_ts(dp, ah + 8u * ks, bl, id, true);
+              umma_ts(dp, al + 8u * ks, bh, id, true);
+            }
+          }
+          if (kt + 1 == NKT) umma_commit(mbarP);
+        }
+      }
+      // ---------------- a7: row sums -> 1/l; the head over this query tile's rows
+      lpart[wc * 128 + 32 * wq + lane] = ls;
+      lpart[512 + wc * 128 + 32 * wq + lane] = lt;
+      mbar_wait_bounded(mbarP, phP);
+      phP ^= 1u;
+      tc_fence_after();
+      __syncthreads();
+      if (wc == 0 && warp_rows) {
+        const int g = lane >> 2;
+        // 1/l of the rows this lane's B fragments touch (rows g, g + 8 of each 16-row step)
+        float il[2][2][2];   // [kb][branch][v]
+#pragma unroll
+        for (int kb = 0; kb < 2; kb++)
+#pragma unroll
+          for (int v = 0; v < 2; v++) {
+            const int rr = 32 * wq + 16 * kb + g + 8 * v;
+            const float s_ = ((lpart[rr] + lpart[128 + rr]) + lpart[256 + rr]) + lpart[384 + rr];
+            const float t_ = ((lpart[512 + rr] + lpart[640 + rr]) + lpart[768 + rr]) + lpart[896 + rr];
+            const bool ok = 128 * qt + rr < N;
+            il[kb][0][v] = ok ? 1.f / s_ : 0.f;
+            il[kb][1][v] = ok ? 1.f / t_ : 0.f;
+          }
+        float* ys = yslot + wq * YW;
+        // per n-tile: Y[m][8 nt..] += sum over this warp's 32 rows and both branches
+#pragma unroll 1
+        for (int nt = 0; nt < K::NCT; nt++) {
+          float acc[MT][4];
+#pragma unroll
+          for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+            for (int e = 0; e < 4; e++) acc[mt][e] = 0.f;
+#pragma unroll
+          for (int kb = 0; kb < 2; kb++) {
+            const int i0 = 128 * qt + 32 * wq + 16 * kb;   // K rows of this step
+            if (i0 >= npf) break;
+#pragma unroll
+            for (int br = 0; br < 2; br++) {
+              uint32_t pr[4];
+              tld16_x1(tmem0 + ((uint32_t)(32 * wq + 16 * kb) << 16) + K::TP +
+                           (uint32_t)(br * K::SP + 8 * nt), pr);
+              uint32_t ah[MT][4], al[MT][4];
+#pragma unroll
+              for (int mt = 0; mt < MT; mt++) {
+                ldg_afrag16(whi, ldw, 16 * mt, (br ? npf : 0) + i0, lane, ah[mt]);
+                ldg_afrag16(wlo, ldw, 16 * mt, (br ? npf : 0) + i0, lane, al[mt]);
+              }
+              tld_wait();
+              uint32_t h0, l0, h1, l1;
+              const float i0v = il[kb][br][0], i1v = il[kb][br][1];
+              split2(make_float2(__uint_as_float(pr[0]) * i0v, __uint_as_float(pr[1]) * i0v), h0, l0);
+              split2(make_float2(__uint_as_float(pr[2]) * i1v, __uint_as_float(pr[3]) * i1v), h1, l1);
+              const uint32_t bh0 = movm_t(h0), bh1 = movm_t(h1), bl0 = movm_t(l0), bl1 = movm_t(l1);
+#pragma unroll
+              for (int mt = 0; mt < MT; mt++) {
+                mma16816_nv(acc[mt], al[mt], bh0, bh1);
+                mma16816_nv(acc[mt], ah[mt], bl0, bl1);
+                mma16816_nv(acc[mt], ah[mt], bh0, bh1);
+              }
+            }
+          }
+          // fixed-order partial sums: slot wq accumulates this warp's rows over the query tiles
+#pragma unroll
+          for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+              const int m = 16 * mt + g + 8 * (e >> 1), t = 8 * nt + 2 * (lane & 3) + (e & 1);
+              ys[m * (8 * K::NCT) + t] += acc[mt][e];
+            }
+        }
+      }
+      tc_fence_before();
+      __syncthreads();
+      tc_fence_after();
+    }
+    // ---------------- a8: y = (sum of the slots) / (sw sx) + b, coalesced over h
+    {
+      const float ysc = inv_sw / sx;
+      float* yg = a.y + (b * C + c) * (int64_t)H;
+      const float* bg = a.bias + (int64_t)cw * H;
+      for (int h = tid; h < H; h += 512) {
+        const int m = h / S, t = h - m * S;
+        const int o = m * (8 * K::NCT) + t;
+        const float yv = ((yslot[o] + yslot[YW + o]) + yslot[2 * YW + o]) + yslot[3 * YW + o];
+        yg[h] = fmaf(yv, ysc, __ldg(bg + h));
+      }
+    }
+    __syncthreads();
+    for (int k = tid; k < 4 * YW; k += 512) yslot[k] = 0.f;
+    // (the next series' Z' / X' writes follow the last P-MMA, whose completion was waited)
+  }
+  cp_async_wait_all();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc(tmem0, 512);
+}
+
+bool tcl_supported_s(int S) { return S == 12 || S == 24 || S == 48 || S == 96; }
+
+bool plan_tcl_kernel(const FwdArgs& a, int max_smem_optin, int sm_count, TclPlan* p) {
+  if (!tcl_supported_s(a.S) || a.N <= 32 || a.N > 512 || a.M > 32) return false;
+  const int S = a.S, SP = (S + 15) / 16 * 16, NCT = (S + 7) / 8;
+  const int pitch = ((S / 4) & 1) ? 4 * S : 4 * S + 16;
+  TclLayout& ly = p->ly;
+  ly.nqt = (a.N + 127) / 128;
+  ly.nkt = (a.N + 63) / 64;
+  ly.rpad = 128 * ly.nqt;
+  const int NK = 64 * ly.nkt;
+  const int MT = a.M <= 16 ? 1 : 2;
+  p->mt = MT;
+  int off = 0;
+  ly.off_z = off;
+  off += ly.rpad * 4 * SP;                  // Z' [Rpad][hi SP | lo SP] halves
+  ly.off_x = off;
+  off += 4 * SP * NK;                       // X' hi | lo, [SP/8][NK/8] core matrices each
+  ly.stage_bytes = (a.N * pitch + 127) & ~127;
+  ly.off_stage = off;
+  off += 2 * ly.stage_bytes;
+  ly.off_vec = off;
+  off += (3 * ly.rpad + 2 * 4 * 128 + 64) * 4;
+  off = (off + 127) & ~127;
+  ly.off_y = off;
+  off += 4 * 16 * MT * 8 * NCT * 4;
+  ly.off_bar = off;
+  off += 128;
+  ly.wpack_bytes = flash_wpack_bytes(a.N, a.M);
+  p->smem_bytes = (size_t)off;
+  if (p->smem_bytes > (size_t)max_smem_optin) return false;
+  // one CTA per SM (TMEM: 512 columns); channels x k CTAs, k against wave quantisation
+  const int64_t sms = sm_count > 0 ? sm_count : 148;
+  int64_t best_k = 1, best = -1;
+  for (int64_t k = 1; k <= 64 && k <= a.B; k++) {
+    const int64_t waves = ((int64_t)a.C * k + sms - 1) / sms;
+    const int64_t cost = waves * ((a.B + k - 1) / k + 1);
+    if (best < 0 || cost < best) best = cost, best_k = k;
+  }
+  p->ctas_per_channel = (int)best_k;
+  return true;
+}
+
+template <int S, int MT>
+static cudaError_t launch_tcl_t(const FwdArgs& a, const TclPlan& p, cudaStream_t st) {
+  auto k = prnet_fwd_tcl_kernel<S, MT>;
+  cudaError_t e =
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)p.ctas_per_channel, (unsigned)a.C);
+  k<<<grid, 512, p.smem_bytes, st>>>(a, p.ly, p.ctas_per_channel);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tcl_kernel(const FwdArgs& a, const TclPlan& p, cudaStream_t st) {
+  switch (a.S) {
+#define PRNET_TCL_L(SV)                                                                 \
+  case SV:                                                                              \
+    return p.mt == 1 ? launch_tcl_t<SV, 1>(a, p, st) : launch_tcl_t<SV, 2>(a, p, st);
+    PRNET_TCL_L(12)
+    PRNET_TCL_L(24)
+    PRNET_TCL_L(48)
+    PRNET_TCL_L(96)
+#undef PRNET_TCL_L
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace prnet

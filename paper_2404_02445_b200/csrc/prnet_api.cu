@@ -192,6 +192,12 @@ const char* kWideningMsg =
 // FP32 kernels run (warp_f32, long_f32); tc_quad / tc_pipe (shift 1) need tau_s >= 1/80.
 constexpr float kTauKnownMax = 1.0f / 320.0f;
 bool known_max_ok(const prnet_handle* h) { return h->cfg.tau_seasonal >= kTauKnownMax; }
+// 8 = tc_long (32 < N <= 512, S in {12, 24, 48, 96}, M <= 32, plain reading, tau_s >= 1/320:
+// 128-row query tiles on tcgen05 / TMEM, key tiles of 64, known seasonal row bound)
+bool tcl_applicable(const prnet_handle* h) {
+  return h->N > 32 && h->N <= 512 && h->M <= 32 && prnet::tcl_supported_s(h->cfg.seg_len) &&
+         h->cfg.tau_seasonal >= 1.0f / 320.0f;
+}
 // 7 = small_f32 (N <= 16, S <= 128, M <= 32: lanes over time, FP32)
 bool small_applicable(const prnet_handle* h) {
   return h->N <= 16 && h->cfg.seg_len <= 128 && h->M <= 32;
@@ -221,6 +227,7 @@ int pick_variant(const prnet_handle* h) {
   if (small_applicable(h) && (h->N <= 8 || h->cfg.seg_len > 64)) return 7;
   if (tcq_applicable(h) && h->N > 16) return 6;
   if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
+  if (tcl_applicable(h)) return 8;
   if (h->N > 32 && flash_applicable(h)) return 5;
   return h->N <= 32 ? 0 : 1;
 }
@@ -248,14 +255,19 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
     // instance_norm), each from the values its own fold consumes; small_f32 maps to
     // mma_f16x3 (same domain, every flag), flash_f16x3 to long_f32 (every flag and N)
     if (v == 7) v = 2;
-    if (v == 5) v = 1;
+    if (v == 5 || v == 8) v = 1;
     if (v == 0 && widening_on(h)) v = 1;
   }
   static const int wpc_env = [] {  // tuning knob: windows per CTA (0 = plan default)
     const char* e = getenv("PRNET_WINDOWS_PER_CTA");
     return e ? atoi(e) : 0;
   }();
-  if (v == 7) {
+  if (v == 8) {
+    prnet::TclPlan p;
+    if (!prnet::plan_tcl_kernel(a, h->max_smem_optin, h->sm_count, &p))
+      return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the tc_long kernel");
+    e = prnet::launch_tcl_kernel(a, p, st);
+  } else if (v == 7) {
     prnet::SmallPlan p;
     if (!prnet::plan_small_kernel(a, h->max_smem_optin, &p))
       return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the small_f32 kernel");
@@ -778,8 +790,12 @@ prnet_status prnet_backward_head(prnet_handle* h, const float* x, int64_t batch,
 
 prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {
   if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
-  if (variant < -1 || variant > 7)
-    return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,...,7}");
+  if (variant < -1 || variant > 8)
+    return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,...,8}");
+  if (variant == 8 && !tcl_applicable(h))
+    return fail(h, PRNET_ERR_UNSUPPORTED,
+                "tc_long variant needs 32 < N <= 512, S in {12, 24, 48, 96}, M <= 32, "
+                "tau_seasonal >= 1/320");
   if (variant == 3 || variant == 4)
     return fail(h, PRNET_ERR_INVALID_ARG,
                 "variants 3 (tc_fold) and 4 (tc_full) are retired: 6 (tc_quad) supersedes them");

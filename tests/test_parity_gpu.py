@@ -40,10 +40,13 @@ def _applicable(variant, L, S, H):
         return N <= 16 and S <= 128 and M <= 32
     if variant == "flash_f16x3":
         return 16 < N <= 512 and S <= 96 and M <= 32
+    if variant == "tc_long":
+        return 32 < N <= 512 and S in (12, 24, 48, 96) and M <= 32
     return True
 
 
-VARIANTS = [None, "warp_f32", "mma_f16x3", "long_f32", "flash_f16x3", "tc_quad", "small_f32"]
+VARIANTS = [None, "warp_f32", "mma_f16x3", "long_f32", "flash_f16x3", "tc_quad", "small_f32",
+            "tc_long"]
 SHORT_VARIANTS = [None, "warp_f32", "mma_f16x3", "tc_quad", "small_f32"]
 
 
@@ -162,7 +165,7 @@ def test_long_lookback_temperatures_and_head_modes(oracle_mod, L, S, H, tau, hpc
     _check_small(oracle_mod, x, S, H, hpc=hpc, tau_s=tau, tau_t=tau * 0.7)
 
 
-@pytest.mark.parametrize("variant", [None, "flash_f16x3", "long_f32"])
+@pytest.mark.parametrize("variant", [None, "flash_f16x3", "long_f32", "tc_long"])
 @pytest.mark.parametrize("kind", ["normal", "constant", "scaled"])
 def test_long_lookback_value_distributions(oracle_mod, kind, variant):
     x = synth.random_windows(2, 3, 1440, kind=kind)

@@ -1,0 +1,100 @@
+"""GPU parity of tc_long (fwd_tcl.cu: 32 < N <= 512, S in {12, 24, 48, 96}, M <= 32; 128-row query
+tiles on tcgen05 / TMEM) against the fp64 oracle, through the C ABI.  Tolerance
+|d| <= 1e-5 + 1e-4 |ref| (north_star).  Shapes span every instantiation, N across the 64-key and
+128-row tile boundaries (masked key columns, idle row quarters), r > 0 (bulk copies vs the
+4-byte cp.async path), H not a multiple of S, one or two head m-tiles, several series per CTA
+(the staging double buffer), temperatures down to the known-bound domain."""
+import numpy as np
+import pytest
+
+import synth
+from parity_util import assert_parity
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2404_02445_b200 import PRNet  # noqa: E402
+
+
+def _run(oracle_mod, B, C, L, S, H, kind="mixed", tau_s=1.0, tau_t=1.0, hpc=True, seed=13):
+    N, _, M = synth.derived_dims(L, S, H)
+    x = synth.random_windows(B, C, L, seed=seed, kind=kind)
+    ws, wt, b = synth.make_params(C, M, N, H, hpc, synth.DEFAULT_SEED, 0)
+    m = PRNet(C, L, S, H, head_per_channel=hpc, tau_s=tau_s, tau_t=tau_t).load(ws, wt, b)
+    m.set_variant("tc_long")
+    y = m.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+    _, y64 = oracle_mod.forward(x, S, H, ws, wt, b, hpc, tau_s, tau_t)
+    scale = None
+    if kind == "scaled":
+        scale = np.maximum(np.abs(x).max(axis=-1, keepdims=True), 1.0)
+    return assert_parity(y, y64, scale=scale)
+
+
+@pytest.mark.parametrize("S,N", [(12, 33), (12, 64), (12, 65), (12, 127), (12, 128), (12, 129),
+                                 (12, 200), (12, 333), (12, 480), (12, 512), (24, 40), (24, 60),
+                                 (24, 120), (24, 240), (24, 255), (48, 33), (48, 60), (48, 120),
+                                 (96, 34), (96, 60), (96, 64)])
+def test_tcl_segments(oracle_mod, S, N):
+    _run(oracle_mod, 3, 3, N * S, S, 96)
+
+
+@pytest.mark.parametrize("S", [12, 24, 48, 96])
+@pytest.mark.parametrize("H", [1, 7, 97, 200, 384])
+def test_tcl_horizons(oracle_mod, S, H):
+    N = {12: 100, 24: 70, 48: 40, 96: 36}[S]
+    if -(-H // S) > 32:
+        pytest.skip("M > 32")
+    _run(oracle_mod, 2, 3, N * S + 4, S, H)
+
+
+@pytest.mark.parametrize("S", [12, 24, 48, 96])
+@pytest.mark.parametrize("r", [1, 2, 3, 8])
+def test_tcl_ragged_start(oracle_mod, S, r):
+    N = {12: 150, 24: 61, 48: 45, 96: 33}[S]
+    _run(oracle_mod, 2, 3, N * S + r, S, 96)
+
+
+@pytest.mark.parametrize("S", [12, 48])
+@pytest.mark.parametrize("kind", ["normal", "constant", "scaled"])
+def test_tcl_value_kinds(oracle_mod, S, kind):
+    N = {12: 130, 48: 50}[S]
+    _run(oracle_mod, 2, 3, N * S, S, 96, kind=kind)
+
+
+@pytest.mark.parametrize("S", [12, 24])
+@pytest.mark.parametrize("tau", [0.005, 0.05, 0.3, 4.0])
+@pytest.mark.parametrize("hpc", [True, False])
+def test_tcl_temperatures(oracle_mod, S, tau, hpc):
+    _run(oracle_mod, 2, 3, 90 * S, S, 2 * S + 3, tau_s=tau, tau_t=tau * 0.7, hpc=hpc)
+
+
+@pytest.mark.parametrize("B", [1, 2, 7, 33])
+def test_tcl_window_counts(oracle_mod, B):
+    """Several series per CTA (double-buffered staging, TMEM reuse across series)."""
+    _run(oracle_mod, B, 2, 1440, 12, 96)
+
+
+def test_tcl_sliding_equals_materialised():
+    L, S, H, C, B = 1440, 12, 96, 2, 9
+    T = L + B + 5
+    s = synth.random_windows(1, C, T, kind="mixed")[0]
+    N = L // S
+    ws, wt, b = synth.make_params(C, H // S, N, H, True, synth.DEFAULT_SEED, 0)
+    m = PRNet(C, L, S, H).load(ws, wt, b)
+    m.set_variant("tc_long")
+    sd = torch.from_numpy(s).cuda()
+    y_sl = m.forward_sliding(sd, 3, B)
+    xw = sd.unfold(1, L, 1)[:, 3:3 + B, :].permute(1, 0, 2).contiguous()
+    assert torch.equal(y_sl, m.forward(xw))
+
+
+def test_tcl_deterministic():
+    x = torch.from_numpy(synth.random_windows(5, 3, 2880)).cuda()
+    N = 2880 // 24
+    ws, wt, b = synth.make_params(3, 4, N, 96, True, synth.DEFAULT_SEED, 0)
+    m = PRNet(3, 2880, 24, 96).load(ws, wt, b)
+    m.set_variant("tc_long")
+    assert torch.equal(m.forward(x), m.forward(x))
