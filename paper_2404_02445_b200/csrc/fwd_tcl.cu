@@ -71,6 +71,9 @@ __device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 template <int S>
 __device__ __forceinline__ constexpr float ttl(int t) {
   return (float)t - 0.5f * (float)(S - 1);
@@ -105,17 +108,69 @@ __device__ __forceinline__ void ldg_afrag16(const __half* base, int ld, int r0, 
   f[3] = __ldg(reinterpret_cast<const unsigned int*>(p + 8 * ld + 8));
 }
 
+// The exponentials of one thread's 16 key columns (a4/a5): seasonal 2^(rho ks - f_i ks), trend
+// 2^(-(mu~_i - mu~_j)^2 - (k~_i - k~_j)^2), split fp16 hi/lo for the TMEM store, row sums added
+// to ls / lt.  MASK: columns j >= nvalid get 0 (the last key tile only).
+template <bool MASK>
+__device__ __forceinline__ void tcl_exps(const uint32_t (&g)[16], float ks, float fk, float mi,
+                                         float ki, const float* mt, const float* kt, int nvalid,
+                                         uint32_t (&eh)[8], uint32_t (&el)[8], uint32_t (&th)[8],
+                                         uint32_t (&tlo)[8], float& ls, float& lt) {
+  const float2 ks2 = f2(ks), nf2 = f2(-fk);
+  float2 sa2 = f2(0.f), sb2 = f2(0.f);
+#pragma unroll
+  for (int j = 0; j < 16; j += 2) {
+    const float2 arg = fma2(make_float2(__uint_as_float(g[j]), __uint_as_float(g[j + 1])), ks2, nf2);
+    float e0 = fast_ex2(arg.x), e1 = fast_ex2(arg.y);
+    if (MASK) {
+      e0 = j < nvalid ? e0 : 0.f;
+      e1 = j + 1 < nvalid ? e1 : 0.f;
+    }
+    if (j & 2) sb2 = add2(sb2, make_float2(e0, e1));
+    else sa2 = add2(sa2, make_float2(e0, e1));
+    split2(make_float2(e0, e1), eh[j / 2], el[j / 2]);
+  }
+  const float2 s2 = add2(sa2, sb2);
+  ls += s2.x + s2.y;
+  const float2 mi2 = f2(mi), ki2 = f2(ki);
+  const float4* cm4 = reinterpret_cast<const float4*>(mt);
+  const float4* ck4 = reinterpret_cast<const float4*>(kt);
+  float2 ta2 = f2(0.f), tb2 = f2(0.f);
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const float4 mj = cm4[q], kj = ck4[q];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int j = 4 * q + 2 * h;
+      const float2 dm = add2(mi2, h ? make_float2(-mj.z, -mj.w) : make_float2(-mj.x, -mj.y));
+      const float2 dk = add2(ki2, h ? make_float2(-kj.z, -kj.w) : make_float2(-kj.x, -kj.y));
+      const float2 ex = fma2(make_float2(-dk.x, -dk.y), dk, mul2(make_float2(-dm.x, -dm.y), dm));
+      float e0 = fast_ex2(ex.x), e1 = fast_ex2(ex.y);
+      if (MASK) {
+        e0 = j < nvalid ? e0 : 0.f;
+        e1 = j + 1 < nvalid ? e1 : 0.f;
+      }
+      if (h) tb2 = add2(tb2, make_float2(e0, e1));
+      else ta2 = add2(ta2, make_float2(e0, e1));
+      split2(make_float2(e0, e1), th[j / 2], tlo[j / 2]);
+    }
+  }
+  const float2 t2 = add2(ta2, tb2);
+  lt += t2.x + t2.y;
+}
+
 }  // namespace
 
 template <int S, int MT>
-__global__ void __launch_bounds__(512, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLayout ly,
+__global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLayout ly,
                                                                 int ctas_per_channel) {
   using K = TclCfg<S>;
   extern __shared__ __align__(1024) unsigned char smem[];
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
-  const int wq = warp & 3, wc = warp >> 2;   // row quarter (TMEM lanes), column quarter
+  const bool mma_warp = warp == 16;            // warp 16 issues every tcgen05.mma (lane 0)
+  const int wq = warp & 3, wc = (warp >> 2) & 3;   // row quarter (TMEM lanes), column quarter
   const int c = blockIdx.y;
   const int cw = a.head_per_channel ? c : 0;
   const int N = a.N, M = a.M, H = a.H, C = a.C;
@@ -129,20 +184,33 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
   float* mtv = fks + ly.rpad;                                  // [Rpad] mu~
   float* ktv = mtv + ly.rpad;                                  // [Rpad] kappa~
   float* lpart = ktv + ly.rpad;                                // [2][4][128] row-sum partials
-  float* red = lpart + 2 * 4 * 128;                            // [16][4] reduction scratch
-  float* yslot = reinterpret_cast<float*>(smem + ly.off_y);    // [4][16 MT][8 NCT]
+  float* red = lpart + 2 * 4 * 128;                            // [17][3] reduction scratch, [63] m0
+  float* yslot = reinterpret_cast<float*>(smem + ly.off_y);    // [2 branch][4 wq][16 MT][8 NCT]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ly.off_bar);
-  uint64_t* mbarG = bars + 0;
-  uint64_t* mbarP = bars + 1;
-  uint64_t* xbar = bars + 2;                                   // + buffer
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + ly.off_bar + 64);
+  uint64_t* gfull = bars + 0;    // Gram committed (tcgen05.commit)
+  uint64_t* gfree = bars + 1;    // 16 softmax warps have read G
+  uint64_t* efull = bars + 2;    // [2] 16 softmax warps have stored E buffer b
+  uint64_t* efree = bars + 4;    // [2] P-MMA reading E buffer b committed
+  uint64_t* pfull = bars + 6;    // last P-MMA of a query tile committed
+  uint64_t* pfree = bars + 7;    // 16 softmax warps have read P (the head)
+  uint64_t* xbar = bars + 8;     // [2] staging buffers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + ly.off_bar + 128);
   constexpr int YW = 16 * MT * 8 * K::NCT;                     // floats per Y slot
 
   if (tid == 0) {
-    for (int k = 0; k < 4; k++) mbar_init(bars + k, 1);
+    mbar_init(gfull, 1);
+    mbar_init(gfree, 16);
+    mbar_init(efull, 16);
+    mbar_init(efull + 1, 16);
+    mbar_init(efree, 1);
+    mbar_init(efree + 1, 1);
+    mbar_init(pfull, 1);
+    mbar_init(pfree, 16);
+    mbar_init(xbar, 1);
+    mbar_init(xbar + 1, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int k = tid; k < 4 * YW; k += 512) yslot[k] = 0.f;
+  for (int k = tid; k < 8 * YW; k += blockDim.x) yslot[k] = 0.f;
   if (warp == 0) tmem_alloc(tmem_slot, 512);
   fence_proxy_async();
   tc_fence_before();
@@ -164,7 +232,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
   const bool bulk = a.x_vec;
   auto xptr = [&](int64_t b) { return a.x + b * a.xsb + c * a.xsc + a.r; };
   // series -> staging buffer (thread 0 arms the barrier; row copies by warp 0's lanes, or one
-  // span copy; unaligned windows: 4-byte cp.async by the whole CTA, waited with the barrier)
+  // span copy; unaligned windows: 4-byte cp.async by the softmax threads)
   auto issue_load = [&](int64_t b, int buf) {
     const float* xg = xptr(b);
     unsigned char* st = stg0 + (buf ? ly.stage_bytes : 0);
@@ -178,7 +246,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
           if (lane == 0) bulk_load(st, xg, (uint32_t)NS * 4u, xbar + buf);
         }
       }
-    } else {
+    } else if (!mma_warp) {
       for (int k = tid; k < NS; k += 512) {
         const int n = k / S, t = k - n * S;
         cp_async4(st + n * K::PITCH + 4 * t, xg + k);
@@ -187,7 +255,8 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
     }
   };
 
-  uint32_t phG = 0, phP = 0, phX = 0;   // phX: bit k = parity of staging buffer k
+  // tile counter (query tile x key tile, over every series of the CTA): mbarrier parities
+  uint32_t tile = 0, qcount = 0, phX = 0;
   if (b0 < b1) {
     fence_proxy_async();
     issue_load(b0, 0);
@@ -207,7 +276,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
       issue_load(b + 1, buf ^ 1);
     }
     const float4* st4 = reinterpret_cast<const float4*>(stg0 + (buf ? ly.stage_bytes : 0));
-    const int r = tid;                 // this thread's segment row (N <= 512)
+    const int r = tid;                 // this thread's segment row (N <= 512; warp 16: none)
     const bool rv = r < N;
     const float4* xr4 = st4 + (rv ? r : 0) * (K::PITCH / 16);
     float mu = 0.f, kap = 0.f, nu2 = 0.f, x0 = 0.f, m1 = 0.f;
@@ -277,7 +346,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
       s_a = warp_sum(s_a);
       s_b = warp_sum(s_b);
       const float mx = warp_max_nonneg(bnd);
-      if (lane == 0) {
+      if (lane == 0 && warp < 16) {
         red[3 * warp] = s_a;
         red[3 * warp + 1] = s_b;
         red[3 * warp + 2] = mx;
@@ -327,107 +396,43 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
     __syncthreads();
     tc_fence_after();
 
-    // ---------------- a3..a6 over (query tile, key tile)
-    auto issue_gram = [&](int qt, int kt) {
-      const uint32_t za = z_s + 16 * qt * K::SBO, zb = z_s + 8 * kt * K::SBO;
-      constexpr uint32_t LO = (K::SP / 8) * 128;
-      constexpr uint32_t id = idesc_f16(128, 64, false, false);
+    const int ntiles = NQT * NKT;
+    if (mma_warp) {
+      // ---------------- the MMA warp: Gram of tile t+1 as soon as G(t) is read, P-MMA of tile t
+      // as soon as E(t) is stored; commits drive the softmax warps
+      if (lane == 0) {
+        const uint32_t sbo_x = 16u * (uint32_t)NK;
+        auto issue_gram = [&](int qt, int kt) {
+          const uint32_t za = z_s + 16 * qt * K::SBO, zb = z_s + 8 * kt * K::SBO;
+          constexpr uint32_t LO = (K::SP / 8) * 128;
+          constexpr uint32_t id = idesc_f16(128, 64, false, false);
 #pragma unroll
-      for (int k = 0; k < K::SP / 16; k++) {
-        const uint32_t o = k * 256;
-        umma(tmem0 + K::TG, sdesc(za + o, 128, K::SBO), sdesc(zb + o, 128, K::SBO), id, k > 0);
-        umma(tmem0 + K::TG, sdesc(za + o, 128, K::SBO), sdesc(zb + LO + o, 128, K::SBO), id, true);
-        umma(tmem0 + K::TG, sdesc(za + LO + o, 128, K::SBO), sdesc(zb + o, 128, K::SBO), id, true);
-      }
-      umma_commit(mbarG);
-    };
-    if (tid == 0) issue_gram(0, 0);
-    const uint32_t sbo_x = 16u * (uint32_t)NK;
-    for (int qt = 0; qt < NQT; qt++) {
-      const int row = 128 * qt + 32 * wq + lane;   // this thread's query row
-      const bool warp_rows = 128 * qt + 32 * wq < N;   // warp-uniform: any valid row
-      const float fk = fks[row], mi = mtv[row], ki = ktv[row];
-      float ls = 0.f, lt = 0.f;
-      for (int kt = 0; kt < NKT; kt++) {
-        const int eb = kt & 1;
-        const uint32_t te = tmem0 + (eb ? K::TE1 : K::TE0);
-        mbar_wait_bounded(mbarG, phG);
-        phG ^= 1u;
-        tc_fence_after();
-        uint32_t g[16];
-        tld_x16(tl + K::TG + 16u * wc, g);
-        tld_wait();
-        tc_fence_before();
-        __syncthreads();
-        tc_fence_after();
-        if (tid == 0) {   // the next Gram (G is read)
-          if (kt + 1 < NKT) issue_gram(qt, kt + 1);
-          else if (qt + 1 < NQT) issue_gram(qt + 1, 0);
-        }
-        const int j0 = 64 * kt + 16 * wc;           // this thread's first key
-        uint32_t eh[8], el[8], th[8], tlo[8];
-        if (warp_rows) {
-          const bool full = j0 + 16 <= N;
-          // seasonal: 2^(rho ks - f_i ks)
-          const float2 ks2 = f2(a.ks), nf2 = f2(-fk);
-          float2 sa2 = f2(0.f), sb2 = f2(0.f);
-#pragma unroll
-          for (int j = 0; j < 16; j += 2) {
-            const float2 arg = fma2(make_float2(__uint_as_float(g[j]), __uint_as_float(g[j + 1])), ks2, nf2);
-            float e0 = fast_ex2(arg.x), e1 = fast_ex2(arg.y);
-            if (!full) {
-              if (j0 + j >= N) e0 = 0.f;
-              if (j0 + j + 1 >= N) e1 = 0.f;
-            }
-            if (j & 2) sb2 = add2(sb2, make_float2(e0, e1));
-            else sa2 = add2(sa2, make_float2(e0, e1));
-            split2(make_float2(e0, e1), eh[j / 2], el[j / 2]);
+          for (int k = 0; k < K::SP / 16; k++) {
+            const uint32_t o = k * 256;
+            umma(tmem0 + K::TG, sdesc(za + o, 128, K::SBO), sdesc(zb + o, 128, K::SBO), id, k > 0);
+            umma(tmem0 + K::TG, sdesc(za + o, 128, K::SBO), sdesc(zb + LO + o, 128, K::SBO), id, true);
+            umma(tmem0 + K::TG, sdesc(za + LO + o, 128, K::SBO), sdesc(zb + o, 128, K::SBO), id, true);
           }
-          const float2 s2 = add2(sa2, sb2);
-          ls += s2.x + s2.y;
-          // trend: 2^(-(mu~_i - mu~_j)^2 - (k~_i - k~_j)^2)
-          const float2 mi2 = f2(mi), ki2 = f2(ki);
-          const float4* cm4 = reinterpret_cast<const float4*>(mtv + j0);
-          const float4* ck4 = reinterpret_cast<const float4*>(ktv + j0);
-          float2 ta2 = f2(0.f), tb2 = f2(0.f);
-#pragma unroll
-          for (int q = 0; q < 4; q++) {
-            const float4 mj = cm4[q], kj = ck4[q];
-#pragma unroll
-            for (int h = 0; h < 2; h++) {
-              const int j = 4 * q + 2 * h;
-              const float2 dm = add2(mi2, h ? make_float2(-mj.z, -mj.w) : make_float2(-mj.x, -mj.y));
-              const float2 dk = add2(ki2, h ? make_float2(-kj.z, -kj.w) : make_float2(-kj.x, -kj.y));
-              const float2 ex = fma2(make_float2(-dk.x, -dk.y), dk, mul2(make_float2(-dm.x, -dm.y), dm));
-              float e0 = fast_ex2(ex.x), e1 = fast_ex2(ex.y);
-              if (!full) {
-                if (j0 + j >= N) e0 = 0.f;
-                if (j0 + j + 1 >= N) e1 = 0.f;
-              }
-              if (h) tb2 = add2(tb2, make_float2(e0, e1));
-              else ta2 = add2(ta2, make_float2(e0, e1));
-              split2(make_float2(e0, e1), th[j / 2], tlo[j / 2]);
-            }
+          umma_commit(gfull);
+        };
+        issue_gram(0, 0);
+        for (int t = 0; t < ntiles; t++) {
+          const uint32_t tg = tile + (uint32_t)t;   // global tile index
+          const int qt = t / NKT, kt = t - qt * NKT;
+          if (t + 1 < ntiles) {
+            mbar_wait_bounded(gfree, tg & 1u);
+            tc_fence_after();
+            const int qn = (t + 1) / NKT;
+            issue_gram(qn, t + 1 - qn * NKT);
           }
-          const float2 t2 = add2(ta2, tb2);
-          lt += t2.x + t2.y;
-        } else {
-#pragma unroll
-          for (int j = 0; j < 8; j++) eh[j] = el[j] = th[j] = tlo[j] = 0u;
-        }
-        // E into TMEM buffer eb: [0,32) E_s hi, [32,64) E_s lo, [64,96) E_t hi, [96,128) E_t lo
-        // (this thread's 16 keys = 8 packed columns at 8 wc).  The P-MMA that last read this
-        // buffer (tile kt - 2) completed before the Gram just waited for.
-        tst_x8(te + ((uint32_t)(32 * wq) << 16) + 8u * wc, eh);
-        tst_x8(te + ((uint32_t)(32 * wq) << 16) + 32u + 8u * wc, el);
-        tst_x8(te + ((uint32_t)(32 * wq) << 16) + 64u + 8u * wc, th);
-        tst_x8(te + ((uint32_t)(32 * wq) << 16) + 96u + 8u * wc, tlo);
-        tst_wait();
-        tc_fence_before();
-        __syncthreads();
-        tc_fence_after();
-        if (tid == 0) {
-          // P_s += E_s X'_k, P_t += E_t X'_k: M = 128, N = SP, K = 64 keys in 4 steps, hh, hl, lh
+          if (kt == 0 && qcount + qt > 0) {   // the previous query tile's head has read P
+            mbar_wait_bounded(pfree, (qcount + qt - 1) & 1u);
+            tc_fence_after();
+          }
+          const uint32_t eb = tg & 1u;
+          mbar_wait_bounded(efull + eb, (tg >> 1) & 1u);
+          tc_fence_after();
+          const uint32_t te = tmem0 + (eb ? K::TE1 : K::TE0);
           constexpr uint32_t id = idesc_f16(128, K::SP, false, true);
 #pragma unroll
           for (int br = 0; br < 2; br++) {
@@ -442,46 +447,86 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
               umma_ts(dp, al + 8u * ks, bh, id, true);
             }
           }
-          if (kt + 1 == NKT) umma_commit(mbarP);
+          umma_commit(efree + eb);
+          if (kt + 1 == NKT) umma_commit(pfull);
         }
       }
-      // ---------------- a7: row sums -> 1/l; the head over this query tile's rows
-      lpart[wc * 128 + 32 * wq + lane] = ls;
-      lpart[512 + wc * 128 + 32 * wq + lane] = lt;
-      mbar_wait_bounded(mbarP, phP);
-      phP ^= 1u;
-      tc_fence_after();
-      __syncthreads();
-      if (wc == 0 && warp_rows) {
-        const int g = lane >> 2;
-        // 1/l of the rows this lane's B fragments touch (rows g, g + 8 of each 16-row step)
-        float il[2][2][2];   // [kb][branch][v]
+      __syncwarp();
+    } else {
+      // ---------------- a3..a6 softmax warps over (query tile, key tile)
+      for (int qt = 0; qt < NQT; qt++) {
+        const int row = 128 * qt + 32 * wq + lane;   // this thread's query row
+        const bool warp_rows = 128 * qt + 32 * wq < N;   // warp-uniform: any valid row
+        const float fk = fks[row], mi = mtv[row], ki = ktv[row];
+        float ls = 0.f, lt = 0.f;
+        for (int kt = 0; kt < NKT; kt++) {
+          const uint32_t tg = tile + (uint32_t)(qt * NKT + kt);
+          const uint32_t eb = tg & 1u;
+          const uint32_t te = tmem0 + (eb ? K::TE1 : K::TE0);
+          mbar_wait_bounded(gfull, tg & 1u);
+          tc_fence_after();
+          uint32_t g[16];
+          tld_x16(tl + K::TG + 16u * wc, g);
+          tld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(gfree);
+          const int j0 = 64 * kt + 16 * wc;           // this thread's first key
+          uint32_t eh[8], el[8], th[8], tlo[8];
+          if (warp_rows) {
+            // key columns past N only in the last key tile: a separately compiled masked body
+            if (j0 + 16 <= N)
+              tcl_exps<false>(g, a.ks, fk, mi, ki, mtv + j0, ktv + j0, N - j0, eh, el, th, tlo, ls, lt);
+            else
+              tcl_exps<true>(g, a.ks, fk, mi, ki, mtv + j0, ktv + j0, N - j0, eh, el, th, tlo, ls, lt);
+          } else {
 #pragma unroll
-        for (int kb = 0; kb < 2; kb++)
-#pragma unroll
-          for (int v = 0; v < 2; v++) {
-            const int rr = 32 * wq + 16 * kb + g + 8 * v;
-            const float s_ = ((lpart[rr] + lpart[128 + rr]) + lpart[256 + rr]) + lpart[384 + rr];
-            const float t_ = ((lpart[512 + rr] + lpart[640 + rr]) + lpart[768 + rr]) + lpart[896 + rr];
-            const bool ok = 128 * qt + rr < N;
-            il[kb][0][v] = ok ? 1.f / s_ : 0.f;
-            il[kb][1][v] = ok ? 1.f / t_ : 0.f;
+            for (int j = 0; j < 8; j++) eh[j] = el[j] = th[j] = tlo[j] = 0u;
           }
-        float* ys = yslot + wq * YW;
-        // per n-tile: Y[m][8 nt..] += sum over this warp's 32 rows and both branches
-#pragma unroll 1
-        for (int nt = 0; nt < K::NCT; nt++) {
-          float acc[MT][4];
+          // E buffer eb is free once the P-MMA of tile tg - 2 committed
+          if (tg >= 2) {
+            mbar_wait_bounded(efree + eb, ((tg >> 1) - 1) & 1u);
+            tc_fence_after();
+          }
+          // E into TMEM buffer eb: [0,32) E_s hi, [32,64) E_s lo, [64,96) E_t hi, [96,128)
+          // E_t lo (this thread's 16 keys = 8 packed columns at 8 wc)
+          tst_x8(tl + (te - tmem0) + 8u * wc, eh);
+          tst_x8(tl + (te - tmem0) + 32u + 8u * wc, el);
+          tst_x8(tl + (te - tmem0) + 64u + 8u * wc, th);
+          tst_x8(tl + (te - tmem0) + 96u + 8u * wc, tlo);
+          tst_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(efull + eb);
+        }
+        // ---------------- a7: row sums -> 1/l; the head over this query tile's rows
+        lpart[wc * 128 + 32 * wq + lane] = ls;
+        lpart[512 + wc * 128 + 32 * wq + lane] = lt;
+        named_bar(1, 512);
+        mbar_wait_bounded(pfull, (qcount + qt) & 1u);
+        tc_fence_after();
+        if (warp_rows) {
+          const int g = lane >> 2;
+          // work items (branch, n-tile) of this row quarter, split over the column quarters
+          for (int it = wc; it < 2 * K::NCT; it += 4) {
+            const int br = it / K::NCT, nt = it - br * K::NCT;
+            float acc[MT][4];
 #pragma unroll
-          for (int mt = 0; mt < MT; mt++)
+            for (int mt = 0; mt < MT; mt++)
 #pragma unroll
-            for (int e = 0; e < 4; e++) acc[mt][e] = 0.f;
+              for (int e = 0; e < 4; e++) acc[mt][e] = 0.f;
 #pragma unroll
-          for (int kb = 0; kb < 2; kb++) {
-            const int i0 = 128 * qt + 32 * wq + 16 * kb;   // K rows of this step
-            if (i0 >= npf) break;
+            for (int kb = 0; kb < 2; kb++) {
+              const int i0 = 128 * qt + 32 * wq + 16 * kb;   // K rows of this step
+              if (i0 >= npf) break;
+              float il[2];
 #pragma unroll
-            for (int br = 0; br < 2; br++) {
+              for (int v = 0; v < 2; v++) {
+                const int rr = 32 * wq + 16 * kb + g + 8 * v;
+                const float* lp = lpart + 512 * br + rr;
+                const float l_ = ((lp[0] + lp[128]) + lp[256]) + lp[384];
+                il[v] = 128 * qt + rr < N ? 1.f / l_ : 0.f;
+              }
               uint32_t pr[4];
               tld16_x1(tmem0 + ((uint32_t)(32 * wq + 16 * kb) << 16) + K::TP +
                            (uint32_t)(br * K::SP + 8 * nt), pr);
@@ -493,9 +538,8 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
               }
               tld_wait();
               uint32_t h0, l0, h1, l1;
-              const float i0v = il[kb][br][0], i1v = il[kb][br][1];
-              split2(make_float2(__uint_as_float(pr[0]) * i0v, __uint_as_float(pr[1]) * i0v), h0, l0);
-              split2(make_float2(__uint_as_float(pr[2]) * i1v, __uint_as_float(pr[3]) * i1v), h1, l1);
+              split2(make_float2(__uint_as_float(pr[0]) * il[0], __uint_as_float(pr[1]) * il[0]), h0, l0);
+              split2(make_float2(__uint_as_float(pr[2]) * il[1], __uint_as_float(pr[3]) * il[1]), h1, l1);
               const uint32_t bh0 = movm_t(h0), bh1 = movm_t(h1), bl0 = movm_t(l0), bl1 = movm_t(l1);
 #pragma unroll
               for (int mt = 0; mt < MT; mt++) {
@@ -504,35 +548,42 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
                 mma16816_nv(acc[mt], ah[mt], bh0, bh1);
               }
             }
+            // fixed-order partial sums: slot (branch, row quarter) over the query tiles
+            float* ys = yslot + (br * 4 + wq) * YW;
+#pragma unroll
+            for (int mt = 0; mt < MT; mt++)
+#pragma unroll
+              for (int e = 0; e < 4; e++) {
+                const int m = 16 * mt + g + 8 * (e >> 1), t = 8 * nt + 2 * (lane & 3) + (e & 1);
+                ys[m * (8 * K::NCT) + t] += acc[mt][e];
+              }
           }
-          // fixed-order partial sums: slot wq accumulates this warp's rows over the query tiles
-#pragma unroll
-          for (int mt = 0; mt < MT; mt++)
-#pragma unroll
-            for (int e = 0; e < 4; e++) {
-              const int m = 16 * mt + g + 8 * (e >> 1), t = 8 * nt + 2 * (lane & 3) + (e & 1);
-              ys[m * (8 * K::NCT) + t] += acc[mt][e];
-            }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(pfree);
+        named_bar(1, 512);   // lpart is rewritten by the next query tile
       }
-      tc_fence_before();
-      __syncthreads();
-      tc_fence_after();
     }
+    tile += (uint32_t)ntiles;
+    qcount += (uint32_t)NQT;
+    __syncthreads();
     // ---------------- a8: y = (sum of the slots) / (sw sx) + b, coalesced over h
     {
       const float ysc = inv_sw / sx;
       float* yg = a.y + (b * C + c) * (int64_t)H;
       const float* bg = a.bias + (int64_t)cw * H;
-      for (int h = tid; h < H; h += 512) {
+      for (int h = tid; h < H; h += blockDim.x) {
         const int m = h / S, t = h - m * S;
         const int o = m * (8 * K::NCT) + t;
-        const float yv = ((yslot[o] + yslot[YW + o]) + yslot[2 * YW + o]) + yslot[3 * YW + o];
+        float yv = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; k++) yv += yslot[k * YW + o];
         yg[h] = fmaf(yv, ysc, __ldg(bg + h));
       }
     }
     __syncthreads();
-    for (int k = tid; k < 4 * YW; k += 512) yslot[k] = 0.f;
+    for (int k = tid; k < 8 * YW; k += blockDim.x) yslot[k] = 0.f;
     // (the next series' Z' / X' writes follow the last P-MMA, whose completion was waited)
   }
   cp_async_wait_all();
@@ -567,9 +618,9 @@ bool plan_tcl_kernel(const FwdArgs& a, int max_smem_optin, int sm_count, TclPlan
   off += (3 * ly.rpad + 2 * 4 * 128 + 64) * 4;
   off = (off + 127) & ~127;
   ly.off_y = off;
-  off += 4 * 16 * MT * 8 * NCT * 4;
+  off += 8 * 16 * MT * 8 * NCT * 4;
   ly.off_bar = off;
-  off += 128;
+  off += 256;
   ly.wpack_bytes = flash_wpack_bytes(a.N, a.M);
   p->smem_bytes = (size_t)off;
   if (p->smem_bytes > (size_t)max_smem_optin) return false;
@@ -592,7 +643,7 @@ static cudaError_t launch_tcl_t(const FwdArgs& a, const TclPlan& p, cudaStream_t
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)p.ctas_per_channel, (unsigned)a.C);
-  k<<<grid, 512, p.smem_bytes, st>>>(a, p.ly, p.ctas_per_channel);
+  k<<<grid, 544, p.smem_bytes, st>>>(a, p.ly, p.ctas_per_channel);
   return cudaGetLastError();
 }
 
