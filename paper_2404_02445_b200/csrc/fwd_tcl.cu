@@ -37,6 +37,12 @@
 
 #include "tc_common.cuh"
 
+// ablation switches for A/B builds (results invalid when non-zero): 1 no P-MMA, 2 no Gram MMA,
+// 4 no exponentials, 8 no head
+#ifndef PRNET_TCL_ABL
+#define PRNET_TCL_ABL 0
+#endif
+
 namespace prnet {
 using namespace tcq;
 
@@ -51,8 +57,15 @@ struct TclCfg {
   static constexpr int PITCH = ((S / 4) & 1) ? 4 * S : 4 * S + 16;   // staging row bytes
   static constexpr bool ROWCOPY = PITCH != 4 * S;
   static constexpr int SBO = 32 * SP;             // Z' row block stride (8 rows x 2 SP halves)
-  static constexpr uint32_t TG = 0, TE0 = 64, TE1 = 192, TP = 320;
-  static_assert(TP + 2 * SP <= 512, "TMEM");
+  // P-MMA B operand: NM = 2 -> [X' hi | X' lo] as one N = 2 SP operand (the lo tile follows the
+  // hi tile along N), so each E half is read once per K-step: D = [hh + lh | hl + ll] per
+  // branch (P = the two halves summed); NM = 1 (S = 96) -> N = SP, three products hh, hl, lh
+  static constexpr int NM = 320 + 4 * SP <= 512 ? 2 : 1;
+  static constexpr int PW = NM * SP;                // P columns per branch
+  // TMEM columns: G buffers (64 each; two when they fit), two E buffers (128 each), P_s | P_t
+  static constexpr int GB = 384 + 2 * PW <= 512 ? 2 : 1;
+  static constexpr uint32_t TG = 0, TE0 = 64 * GB, TE1 = TE0 + 128, TP = TE1 + 128;
+  static_assert(TP + 2 * PW <= 512, "TMEM");
 };
 
 __device__ __forceinline__ void sts128(unsigned char* p, uint4 v) {
@@ -187,8 +200,9 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
   float* red = lpart + 2 * 4 * 128;                            // [17][3] reduction scratch, [63] m0
   float* yslot = reinterpret_cast<float*>(smem + ly.off_y);    // [2 branch][4 wq][16 MT][8 NCT]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ly.off_bar);
-  uint64_t* gfull = bars + 0;    // Gram committed (tcgen05.commit)
-  uint64_t* gfree = bars + 1;    // 16 softmax warps have read G
+  uint64_t* gfree = bars + 12;   // [GB] 16 softmax warps have read G buffer b (per-buffer
+                                 // barriers: a completion two tiles ahead needs the next Gram)
+  uint64_t* gfull = bars + 10;   // [GB] Gram into G buffer b committed (tcgen05.commit)
   uint64_t* efull = bars + 2;    // [2] 16 softmax warps have stored E buffer b
   uint64_t* efree = bars + 4;    // [2] P-MMA reading E buffer b committed
   uint64_t* pfull = bars + 6;    // last P-MMA of a query tile committed
@@ -199,7 +213,9 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
 
   if (tid == 0) {
     mbar_init(gfull, 1);
+    mbar_init(gfull + 1, 1);
     mbar_init(gfree, 16);
+    mbar_init(gfree + 1, 16);
     mbar_init(efull, 16);
     mbar_init(efull + 1, 16);
     mbar_init(efree, 1);
@@ -402,28 +418,32 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
       // as soon as E(t) is stored; commits drive the softmax warps
       if (lane == 0) {
         const uint32_t sbo_x = 16u * (uint32_t)NK;
-        auto issue_gram = [&](int qt, int kt) {
+        auto issue_gram = [&](int t) {   // series tile t -> G buffer (tile + t) % GB
+          const int qt = t / NKT, kt = t - qt * NKT;
+          const uint32_t gb = K::GB == 2 ? ((tile + (uint32_t)t) & 1u) : 0u;
+          const uint32_t dg = tmem0 + K::TG + 64u * gb;
           const uint32_t za = z_s + 16 * qt * K::SBO, zb = z_s + 8 * kt * K::SBO;
           constexpr uint32_t LO = (K::SP / 8) * 128;
           constexpr uint32_t id = idesc_f16(128, 64, false, false);
 #pragma unroll
-          for (int k = 0; k < K::SP / 16; k++) {
+          for (int k = 0; k < ((PRNET_TCL_ABL & 2) ? 0 : K::SP / 16); k++) {
             const uint32_t o = k * 256;
-            umma(tmem0 + K::TG, sdesc(za + o, 128, K::SBO), sdesc(zb + o, 128, K::SBO), id, k > 0);
-            umma(tmem0 + K::TG, sdesc(za + o, 128, K::SBO), sdesc(zb + LO + o, 128, K::SBO), id, true);
-            umma(tmem0 + K::TG, sdesc(za + LO + o, 128, K::SBO), sdesc(zb + o, 128, K::SBO), id, true);
+            umma(dg, sdesc(za + o, 128, K::SBO), sdesc(zb + o, 128, K::SBO), id, k > 0);
+            umma(dg, sdesc(za + o, 128, K::SBO), sdesc(zb + LO + o, 128, K::SBO), id, true);
+            umma(dg, sdesc(za + LO + o, 128, K::SBO), sdesc(zb + o, 128, K::SBO), id, true);
           }
-          umma_commit(gfull);
+          umma_commit(gfull + gb);
         };
-        issue_gram(0, 0);
+        issue_gram(0);
+        if (K::GB == 2 && ntiles > 1) issue_gram(1);
         for (int t = 0; t < ntiles; t++) {
           const uint32_t tg = tile + (uint32_t)t;   // global tile index
           const int qt = t / NKT, kt = t - qt * NKT;
-          if (t + 1 < ntiles) {
-            mbar_wait_bounded(gfree, tg & 1u);
+          if (t + K::GB < ntiles) {   // G buffer of tile t is read: the Gram of tile t + GB
+            if (K::GB == 2) mbar_wait_bounded(gfree + (tg & 1u), (tg >> 1) & 1u);
+            else mbar_wait_bounded(gfree, tg & 1u);
             tc_fence_after();
-            const int qn = (t + 1) / NKT;
-            issue_gram(qn, t + 1 - qn * NKT);
+            issue_gram(t + K::GB);
           }
           if (kt == 0 && qcount + qt > 0) {   // the previous query tile's head has read P
             mbar_wait_bounded(pfree, (qcount + qt - 1) & 1u);
@@ -433,18 +453,27 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
           mbar_wait_bounded(efull + eb, (tg >> 1) & 1u);
           tc_fence_after();
           const uint32_t te = tmem0 + (eb ? K::TE1 : K::TE0);
-          constexpr uint32_t id = idesc_f16(128, K::SP, false, true);
+          constexpr uint32_t id = idesc_f16(128, K::PW, false, true);
+          // branches interleaved (consecutive MMAs accumulate into different D)
 #pragma unroll
-          for (int br = 0; br < 2; br++) {
-            const uint32_t dp = tmem0 + K::TP + (uint32_t)(br * K::SP);
-            const uint32_t ah = te + 64u * br, al = ah + 32u;
-#pragma unroll
-            for (int ks = 0; ks < 4; ks++) {
-              const uint32_t ob = (uint32_t)(1024 * kt + 256 * ks);
-              const uint64_t bh = sdesc(xhi_s + ob, 128, sbo_x), bl = sdesc(xlo_s + ob, 128, sbo_x);
-              umma_ts(dp, ah + 8u * ks, bh, id, kt > 0 || ks > 0);
-              umma_ts(dp, ah + 8u * ks, bl, id, true);
-              umma_ts(dp, al + 8u * ks, bh, id, true);
+          for (int ks = 0; ks < ((PRNET_TCL_ABL & 1) ? 0 : 4); ks++) {
+            const uint32_t ob = (uint32_t)(1024 * kt + 256 * ks);
+            const uint64_t bh = sdesc(xhi_s + ob, 128, sbo_x), bl = sdesc(xlo_s + ob, 128, sbo_x);
+            const bool acc = kt > 0 || ks > 0;
+            const uint32_t d0 = tmem0 + K::TP, d1 = d0 + (uint32_t)K::PW;
+            const uint32_t ah0 = te + 8u * ks, ah1 = ah0 + 64u;   // E_s hi, E_t hi
+            if constexpr (K::NM == 2) {
+              umma_ts(d0, ah0, bh, id, acc);
+              umma_ts(d1, ah1, bh, id, acc);
+              umma_ts(d0, ah0 + 32u, bh, id, true);
+              umma_ts(d1, ah1 + 32u, bh, id, true);
+            } else {
+              umma_ts(d0, ah0, bh, id, acc);
+              umma_ts(d1, ah1, bh, id, acc);
+              umma_ts(d0, ah0, bl, id, true);
+              umma_ts(d1, ah1, bl, id, true);
+              umma_ts(d0, ah0 + 32u, bh, id, true);
+              umma_ts(d1, ah1 + 32u, bh, id, true);
             }
           }
           umma_commit(efree + eb);
@@ -463,17 +492,18 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
           const uint32_t tg = tile + (uint32_t)(qt * NKT + kt);
           const uint32_t eb = tg & 1u;
           const uint32_t te = tmem0 + (eb ? K::TE1 : K::TE0);
-          mbar_wait_bounded(gfull, tg & 1u);
+          const uint32_t gb = K::GB == 2 ? (tg & 1u) : 0u;
+          mbar_wait_bounded(gfull + gb, K::GB == 2 ? ((tg >> 1) & 1u) : (tg & 1u));
           tc_fence_after();
           uint32_t g[16];
-          tld_x16(tl + K::TG + 16u * wc, g);
+          tld_x16(tl + K::TG + 64u * gb + 16u * wc, g);
           tld_wait();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(gfree);
+          if (lane == 0) mbar_arrive(gfree + gb);
           const int j0 = 64 * kt + 16 * wc;           // this thread's first key
           uint32_t eh[8], el[8], th[8], tlo[8];
-          if (warp_rows) {
+          if (warp_rows && !(PRNET_TCL_ABL & 4)) {
             // key columns past N only in the last key tile: a separately compiled masked body
             if (j0 + 16 <= N)
               tcl_exps<false>(g, a.ks, fk, mi, ki, mtv + j0, ktv + j0, N - j0, eh, el, th, tlo, ls, lt);
@@ -505,7 +535,7 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
         named_bar(1, 512);
         mbar_wait_bounded(pfull, (qcount + qt) & 1u);
         tc_fence_after();
-        if (warp_rows) {
+        if (warp_rows && !(PRNET_TCL_ABL & 8)) {
           const int g = lane >> 2;
           // work items (branch, n-tile) of this row quarter, split over the column quarters
           for (int it = wc; it < 2 * K::NCT; it += 4) {
@@ -528,8 +558,11 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
                 il[v] = 128 * qt + rr < N ? 1.f / l_ : 0.f;
               }
               uint32_t pr[4];
-              tld16_x1(tmem0 + ((uint32_t)(32 * wq + 16 * kb) << 16) + K::TP +
-                           (uint32_t)(br * K::SP + 8 * nt), pr);
+              const uint32_t pa = tmem0 + ((uint32_t)(32 * wq + 16 * kb) << 16) + K::TP +
+                                  (uint32_t)(br * K::PW + 8 * nt);
+              tld16_x1(pa, pr);
+              uint32_t pr2[4];
+              if constexpr (K::NM == 2) tld16_x1(pa + (uint32_t)K::SP, pr2);
               uint32_t ah[MT][4], al[MT][4];
 #pragma unroll
               for (int mt = 0; mt < MT; mt++) {
@@ -537,6 +570,11 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
                 ldg_afrag16(wlo, ldw, 16 * mt, (br ? npf : 0) + i0, lane, al[mt]);
               }
               tld_wait();
+              if constexpr (K::NM == 2) {   // P = [hh + lh] + [hl + ll]
+#pragma unroll
+                for (int e = 0; e < 4; e++)
+                  pr[e] = __float_as_uint(__uint_as_float(pr[e]) + __uint_as_float(pr2[e]));
+              }
               uint32_t h0, l0, h1, l1;
               split2(make_float2(__uint_as_float(pr[0]) * il[0], __uint_as_float(pr[1]) * il[0]), h0, l0);
               split2(make_float2(__uint_as_float(pr[2]) * il[1], __uint_as_float(pr[3]) * il[1]), h1, l1);

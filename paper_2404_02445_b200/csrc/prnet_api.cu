@@ -225,9 +225,16 @@ int pick_variant(const prnet_handle* h) {
   // MMA tiles pad N to 32, so mma_f16x3 wins at N = 14: 0.166 vs 0.255 ms); mma_f16x3 the
   // fastest other N <= 32 path
   if (small_applicable(h) && (h->N <= 8 || h->cfg.seg_len > 64)) return 7;
-  if (tcq_applicable(h) && h->N > 16) return 6;
+  // tc_quad for S != 24 (fwd_tcg.cu), measured on B200 (profiles/README.md, round 2): stress
+  // L336/S12 (N = 28) 0.230 vs 0.353 ms (mma_f16x3), L1440/S48 0.403 vs 0.980, L2880/S96 0.747
+  // vs 2.444, L720/S48 (N = 15) 0.372 vs 0.434; mma_f16x3 stays ahead at L192/S12 (N = 16)
+  if (tcq_applicable(h) && (h->N > 16 || (h->N > 8 && h->cfg.seg_len == 48))) return 6;
   if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
-  if (tcl_applicable(h)) return 8;
+  // tc_long (tcgen05) against flash_f16x3 (mma.sync), measured on B200 (profiles/README.md,
+  // round 2): stress L5760/S96 (N = 60) 10.5 vs 11.9 ms, L5760/S48 (N = 120) 9.98 vs 11.6 ms;
+  // flash stays ahead for S <= 24 (L5760/S12 27.4 vs 34.4 ms) and at L2880/S48 (4.56 vs 6.86)
+  if (tcl_applicable(h) && (h->cfg.seg_len == 96 || (h->cfg.seg_len == 48 && h->N >= 100)))
+    return 8;
   if (h->N > 32 && flash_applicable(h)) return 5;
   return h->N <= 32 ? 0 : 1;
 }
