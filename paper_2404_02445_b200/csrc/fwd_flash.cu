@@ -51,8 +51,10 @@ __device__ __forceinline__ void ldg_afrag(const __half* base, int ld, int r0, in
 
 static int flash_npad(int N) { return (N + 15) & ~15; }
 
+// m-rows of the pack: 16 / 32 (the flash kernel, M <= 32), 64 (tc_long only, M <= 64)
+static int flash_rows(int M) { return M <= 16 ? 16 : (M <= 32 ? 32 : 64); }
 int flash_wpack_bytes(int N, int M) {
-  const int rows = M <= 16 ? 16 : 32;
+  const int rows = flash_rows(M);
   return 2 * rows * 2 * flash_npad(N) * 2;   // hi + lo, [rows][2 Npad] halves
 }
 
@@ -60,7 +62,7 @@ int flash_wpack_bytes(int N, int M) {
 // trend i at [Npad, 2 Npad); hi block then lo block.
 void pack_flash_head(const float* ws, const float* wt, int Cw, int M, int N, unsigned char* out,
                      float* inv_sw) {
-  const int rows = M <= 16 ? 16 : 32, np = flash_npad(N), ld = 2 * np;
+  const int rows = flash_rows(M), np = flash_npad(N), ld = 2 * np;
   const int bytes = flash_wpack_bytes(N, M);
   for (int c = 0; c < Cw; c++) {
     const float* s = ws + (size_t)c * M * N;

@@ -36,7 +36,7 @@ using namespace tcq;
 
 namespace {
 
-template <int S>
+template <int S, bool M64 = false>
 struct TcgCfg {
   static_assert(S % 4 == 0 && S >= 8 && S <= 96, "S");
   static constexpr int SP = (S + 15) / 16 * 16;   // Gram K per product (t zero-padded)
@@ -51,7 +51,8 @@ struct TcgCfg {
   static constexpr int COLV = 160 * 4;            // per warp column vectors [5][32] fp32
   static constexpr int GROUP = ZT + 4 * STAGE + 4 * COLV;
   static constexpr int BR = (NCT & 1) ? 8 * NCT : 8 * NCT + 8;   // bias row stride (floats)
-  static constexpr int FIXED = 8192 + 256 + 16 + 32 * BR * 4;    // W', barriers, TMEM slot, bias
+  static constexpr int WB = M64 ? 16384 : 8192;                   // W' tile (32 or 64 m-rows)
+  static constexpr int FIXED = WB + 256 + 16 + (M64 ? 64 : 32) * BR * 4;   // W', bars, slot, bias
   static_assert(ZQ >= NCT * 1024, "X' fits the quarter");
   // groups per CTA that fit the 227 KB opt-in shared memory (the launch-bounds thread count)
   static constexpr int MAXG = (232448 - FIXED) / GROUP >= 4 ? 4 : (232448 - FIXED) / GROUP;
@@ -60,6 +61,7 @@ struct TcgCfg {
 
 constexpr uint32_t kIdGramG = idesc_f16(128, 128, false, false);
 constexpr uint32_t kIdFoldG = idesc_f16(128, 32, false, false);
+constexpr uint32_t kIdFoldG64 = idesc_f16(128, 64, false, false);
 
 __device__ __forceinline__ void sts128(unsigned char* p, uint4 v) {
   *reinterpret_cast<uint4*>(p) = v;
@@ -87,9 +89,9 @@ __device__ __forceinline__ constexpr float ttl(int t) {
 
 // DUMP (prnet_debug_attention): the attention values each lane hands to the TMEM store are
 // also written to a_s_dbg / a_t_dbg from the same registers.
-template <int S, bool DUMP>
-__global__ void __launch_bounds__(128 * TcgCfg<S>::MAXG, 1) prnet_fwd_tcg_kernel(FwdArgs a, int ctas_per_channel) {
-  using K = TcgCfg<S>;
+template <int S, bool DUMP, bool M64>
+__global__ void __launch_bounds__(128 * TcgCfg<S, M64>::MAXG, 1) prnet_fwd_tcg_kernel(FwdArgs a, int ctas_per_channel) {
+  using K = TcgCfg<S, M64>;
   extern __shared__ __align__(1024) unsigned char smem[];
   const int ngroups = blockDim.x >> 7;
   const int lane = threadIdx.x & 31;
@@ -107,20 +109,20 @@ __global__ void __launch_bounds__(128 * TcgCfg<S>::MAXG, 1) prnet_fwd_tcg_kernel
   unsigned char* stage = gbase + K::ZT + s * K::STAGE;
   float* colv = reinterpret_cast<float*>(gbase + K::ZT + 4 * K::STAGE) + s * 160;
   const int offw = ngroups * K::GROUP;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + offw + 8192);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + offw + K::WB);
   uint64_t* mbar = bars + 2 * grp;                 // +0 Gram, +1 fold
   uint64_t* xbar = bars + 8 + warp;                // this warp's load
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + offw + 8192 + 256);
-  float* bS = reinterpret_cast<float*>(smem + offw + 8192 + 256 + 16);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + offw + K::WB + 256);
+  float* bS = reinterpret_cast<float*>(smem + offw + K::WB + 256 + 16);
 
   // ---------------- prologue: channel head W' (pack_tc_head layout), bias rows, barriers,
   // TMEM (128 columns per group)
   {
-    const uint4* src = a.wpack_tc + (int64_t)cw * (8192 / 16);
+    const uint4* src = a.wpack_tc + (int64_t)cw * (K::WB / 16);
     uint4* dst = reinterpret_cast<uint4*>(smem + offw);
-    for (int k = threadIdx.x; k < 8192 / 16; k += blockDim.x) dst[k] = __ldg(src + k);
+    for (int k = threadIdx.x; k < K::WB / 16; k += blockDim.x) dst[k] = __ldg(src + k);
     const float* gb = a.bias + (int64_t)cw * H;
-    for (int k = threadIdx.x; k < 32 * K::BR; k += blockDim.x) {
+    for (int k = threadIdx.x; k < (M64 ? 64 : 32) * K::BR; k += blockDim.x) {
       const int m = k / K::BR, t = k % K::BR, h = m * S + t;
       bS[k] = (t < S && h < H) ? __ldg(gb + h) : 0.f;
     }
@@ -141,7 +143,6 @@ __global__ void __launch_bounds__(128 * TcgCfg<S>::MAXG, 1) prnet_fwd_tcg_kernel
   const bool mma_warp = s == 0;
   const uint32_t zt_s = smem_u32(zt), w_s = smem_u32(smem + offw);
   const float inv_sw = __ldg(a.wpack_inv_sw + cw);
-  const bool two_mt = M > 16;
 
   const int64_t cb0 = a.B * blockIdx.x / ctas_per_channel;
   const int64_t cb1 = a.B * (blockIdx.x + 1) / ctas_per_channel;
@@ -433,9 +434,10 @@ __global__ void __launch_bounds__(128 * TcgCfg<S>::MAXG, 1) prnet_fwd_tcg_kernel
       for (int ks = 0; ks < 4; ks++) {
         const uint64_t bh = sdesc(w_s + ks * 256, 128, 2048);
         const uint64_t bl = sdesc(w_s + (8 + 2 * ks) * 128, 128, 2048);
-        umma_ts(tcol + 64u, tcol + 8u * ks, bh, kIdFoldG, ks > 0);
-        umma_ts(tcol + 64u, tcol + 8u * ks, bl, kIdFoldG, true);
-        umma_ts(tcol + 64u, tcol + 32u + 8u * ks, bh, kIdFoldG, true);
+        constexpr uint32_t idf = M64 ? kIdFoldG64 : kIdFoldG;
+        umma_ts(tcol + 64u, tcol + 8u * ks, bh, idf, ks > 0);
+        umma_ts(tcol + 64u, tcol + 8u * ks, bl, idf, true);
+        umma_ts(tcol + 64u, tcol + 32u + 8u * ks, bh, idf, true);
       }
       umma_commit(mbar + 1);
     }
@@ -444,12 +446,18 @@ __global__ void __launch_bounds__(128 * TcgCfg<S>::MAXG, 1) prnet_fwd_tcg_kernel
 
     // ---------------- a7 head on mma.sync, per warp: Y' = Q' X' (split fp16), Q' A-fragments
     // from TMEM (16x256b loads of Q'^T + movmatrix), X' B-fragments by ldmatrix.trans
+    // M64: two passes of 32 future segments (Q'^T columns 64 + 32 mp)
+#pragma unroll 1
+    for (int mp = 0; mp < (M64 ? 2 : 1); mp++) {
+    if (M64 && mp == 1 && M <= 32) break;
     if (active) {
+      const int m0 = 32 * mp;
+      const bool two_mt = M > m0 + 16;
       uint32_t qah[2][2][4], qal[2][2][4];   // [mt][kt][reg]
       {
         uint32_t r0[16], r1[16];
-        tld16_x4(tcol + ((uint32_t)(32 * s) << 16) + 64u, r0);
-        tld16_x4(tcol + ((uint32_t)(32 * s + 16) << 16) + 64u, r1);
+        tld16_x4(tcol + ((uint32_t)(32 * s) << 16) + 64u + 32u * mp, r0);
+        tld16_x4(tcol + ((uint32_t)(32 * s + 16) << 16) + 64u + 32u * mp, r1);
         tld_wait();
 #pragma unroll
         for (int h = 0; h < 2; h++)
@@ -524,7 +532,7 @@ __global__ void __launch_bounds__(128 * TcgCfg<S>::MAXG, 1) prnet_fwd_tcg_kernel
           if (mt == 1 && !two_mt) break;
 #pragma unroll
           for (int hh = 0; hh < 2; hh++) {
-            const int m = 16 * mt + 8 * hh + (lane >> 2);
+            const int m = m0 + 16 * mt + 8 * hh + (lane >> 2);
             if (m >= M) continue;
 #pragma unroll
             for (int nt = 0; nt < NG; nt++) {
@@ -546,6 +554,7 @@ __global__ void __launch_bounds__(128 * TcgCfg<S>::MAXG, 1) prnet_fwd_tcg_kernel
         }
       }
     }
+    }
     ph ^= 1u;
     ycur += ystep;
   }
@@ -557,16 +566,16 @@ __global__ void __launch_bounds__(128 * TcgCfg<S>::MAXG, 1) prnet_fwd_tcg_kernel
 }
 
 namespace {
-template <int S>
+template <int S, bool M64>
 int tcg_groups(int max_smem_optin) {
-  using K = TcgCfg<S>;
+  using K = TcgCfg<S, M64>;
   int g = 4;
   while (g > 1 && (size_t)g * K::GROUP + K::FIXED > (size_t)max_smem_optin) g--;
   return (size_t)g * K::GROUP + K::FIXED <= (size_t)max_smem_optin ? g : 0;
 }
-template <int S>
+template <int S, bool M64>
 size_t tcg_smem(int g) {
-  using K = TcgCfg<S>;
+  using K = TcgCfg<S, M64>;
   return (size_t)g * K::GROUP + K::FIXED;
 }
 }  // namespace
@@ -576,14 +585,15 @@ bool tcg_supported_s(int S) {
 }
 
 bool plan_tcg_kernel(const FwdArgs& a, int max_smem_optin, int sm_count, TcqPlan* p) {
-  if (!tcg_supported_s(a.S) || a.N < 1 || a.N > 32 || a.M > 32) return false;
+  if (!tcg_supported_s(a.S) || a.N < 1 || a.N > 32 || a.M > 64) return false;
+  const bool m64 = a.M > 32;
   int g = 0;
   size_t smem = 0;
   switch (a.S) {
-#define PRNET_TCG_CASE(SV)             \
-  case SV:                             \
-    g = tcg_groups<SV>(max_smem_optin); \
-    smem = tcg_smem<SV>(g);            \
+#define PRNET_TCG_CASE(SV)                                                       \
+  case SV:                                                                       \
+    g = m64 ? tcg_groups<SV, true>(max_smem_optin) : tcg_groups<SV, false>(max_smem_optin); \
+    smem = m64 ? tcg_smem<SV, true>(g) : tcg_smem<SV, false>(g);                 \
     break;
     PRNET_TCG_CASE(12)
     PRNET_TCG_CASE(16)
@@ -614,9 +624,9 @@ bool plan_tcg_kernel(const FwdArgs& a, int max_smem_optin, int sm_count, TcqPlan
   return true;
 }
 
-template <int S, bool DUMP>
+template <int S, bool DUMP, bool M64>
 static cudaError_t launch_tcg_t(const FwdArgs& a, const TcqPlan& p, cudaStream_t st) {
-  auto k = prnet_fwd_tcg_kernel<S, DUMP>;
+  auto k = prnet_fwd_tcg_kernel<S, DUMP, M64>;
   cudaError_t e =
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
@@ -633,7 +643,9 @@ cudaError_t launch_tcg_kernel(const FwdArgs& a, const TcqPlan& p, cudaStream_t s
   switch (a.S) {
 #define PRNET_TCG_L(SV) \
   case SV:              \
-    return dump ? launch_tcg_t<SV, true>(a, p, st) : launch_tcg_t<SV, false>(a, p, st);
+    if (a.M > 32)                                                                        \
+      return dump ? launch_tcg_t<SV, true, true>(a, p, st) : launch_tcg_t<SV, false, true>(a, p, st); \
+    return dump ? launch_tcg_t<SV, true, false>(a, p, st) : launch_tcg_t<SV, false, false>(a, p, st);
     PRNET_TCG_L(12)
     PRNET_TCG_L(16)
     PRNET_TCG_L(32)

@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
   const int ldw = 2 * npf;
   const __half* whi = reinterpret_cast<const __half*>(a.wpack_flash) +
                       (size_t)cw * (ly.wpack_bytes / 2);
-  const __half* wlo = whi + (M <= 16 ? 16 : 32) * ldw;
+  const __half* wlo = whi + (M <= 16 ? 16 : (M <= 32 ? 32 : 64)) * ldw;
 
   const int64_t b0 = a.B * blockIdx.x / ctas_per_channel;
   const int64_t b1 = a.B * (blockIdx.x + 1) / ctas_per_channel;
@@ -634,7 +634,7 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
 bool tcl_supported_s(int S) { return S == 12 || S == 24 || S == 48 || S == 96; }
 
 bool plan_tcl_kernel(const FwdArgs& a, int max_smem_optin, int sm_count, TclPlan* p) {
-  if (!tcl_supported_s(a.S) || a.N <= 32 || a.N > 512 || a.M > 32) return false;
+  if (!tcl_supported_s(a.S) || a.N <= 32 || a.N > 512 || a.M > 64) return false;
   const int S = a.S, SP = (S + 15) / 16 * 16, NCT = (S + 7) / 8;
   const int pitch = ((S / 4) & 1) ? 4 * S : 4 * S + 16;
   TclLayout& ly = p->ly;
@@ -642,7 +642,7 @@ bool plan_tcl_kernel(const FwdArgs& a, int max_smem_optin, int sm_count, TclPlan
   ly.nkt = (a.N + 63) / 64;
   ly.rpad = 128 * ly.nqt;
   const int NK = 64 * ly.nkt;
-  const int MT = a.M <= 16 ? 1 : 2;
+  const int MT = a.M <= 16 ? 1 : (a.M <= 32 ? 2 : 4);
   p->mt = MT;
   int off = 0;
   ly.off_z = off;
@@ -689,7 +689,9 @@ cudaError_t launch_tcl_kernel(const FwdArgs& a, const TclPlan& p, cudaStream_t s
   switch (a.S) {
 #define PRNET_TCL_L(SV)                                                                 \
   case SV:                                                                              \
-    return p.mt == 1 ? launch_tcl_t<SV, 1>(a, p, st) : launch_tcl_t<SV, 2>(a, p, st);
+    return p.mt == 1   ? launch_tcl_t<SV, 1>(a, p, st)                                 \
+           : p.mt == 2 ? launch_tcl_t<SV, 2>(a, p, st)                                 \
+                       : launch_tcl_t<SV, 4>(a, p, st);
     PRNET_TCL_L(12)
     PRNET_TCL_L(24)
     PRNET_TCL_L(48)

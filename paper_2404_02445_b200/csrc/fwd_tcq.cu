@@ -274,20 +274,27 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
       xnext += xstep;
       if (b + 4 < g1) issue_load(xnext);
       const float x0 = xv[0];
-      float2 s1 = f2(0.f), s3 = f2(0.f);
+      float2 s1 = f2(0.f), s3 = f2(0.f), s1b = f2(0.f), s3b = f2(0.f);   // two chains each
 #pragma unroll
       for (int t = 0; t < 24; t += 2) {
         const float2 d = add2(make_float2(xv[t], xv[t + 1]), f2(-x0));
         dv[t] = d.x;
         dv[t + 1] = d.y;
-        s1 = add2(s1, d);
-        s3 = fma2(c_ttilde[t / 2], d, s3);
+        if (t & 2) {
+          s1b = add2(s1b, d);
+          s3b = fma2(c_ttilde[t / 2], d, s3b);
+        } else {
+          s1 = add2(s1, d);
+          s3 = fma2(c_ttilde[t / 2], d, s3);
+        }
       }
+      s1 = add2(s1, s1b);
+      s3 = add2(s3, s3b);
       const float m1 = (s1.x + s1.y) * (1.f / 24.f);
       const float mu = x0 + m1;
       const float s3s = s3.x + s3.y;
       const float kap = s3s * a.inv_v;
-      float2 q2 = f2(0.f);
+      float2 q2 = f2(0.f), q2b = f2(0.f);
       const float2 nm1 = f2(-m1);
       if (!detrend) {
 #pragma unroll
@@ -295,8 +302,10 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
           const float2 z = add2(make_float2(dv[t], dv[t + 1]), nm1);
           dv[t] = z.x;
           dv[t + 1] = z.y;
-          q2 = fma2(z, z, q2);
+          if (t & 2) q2b = fma2(z, z, q2b);
+          else q2 = fma2(z, z, q2);
         }
+        q2 = add2(q2, q2b);
       } else {
         // metric_variant bit 1: the seasonal metric sees the residual
         // e = z - kappa t~ about the segment's least-squares line
@@ -414,7 +423,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
     if (active) {
       float e[32];
       const float2 mi2 = f2(mi), ki2 = f2(ki);
-      float2 sum2 = f2(0.f);
+      float2 sum2 = f2(0.f), sumb = f2(0.f);   // two chains (ILP)
       const float4* cm4 = reinterpret_cast<const float4*>(colv);
       const float4* ck4 = reinterpret_cast<const float4*>(colv + 32);
 #pragma unroll
@@ -431,9 +440,11 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
               fma2(make_float2(-dkj.x, -dkj.y), dkj, mul2(make_float2(-dmj.x, -dmj.y), dmj));
           e[j] = fast_ex2(ex.x);
           e[j + 1] = fast_ex2(ex.y);
-          sum2 = add2(sum2, make_float2(e[j], e[j + 1]));
+          if (h) sumb = add2(sumb, make_float2(e[j], e[j + 1]));
+          else sum2 = add2(sum2, make_float2(e[j], e[j + 1]));
         }
       }
+      sum2 = add2(sum2, sumb);
       colv[64 + i] = valid ? fast_rcp(sum2.x + sum2.y) : 0.f;
       __syncwarp();
       const float4* cr4 = reinterpret_cast<const float4*>(colv + 64);
@@ -474,7 +485,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
         float e[32];
         const float2 ks2 = f2(a.ks), nks2 = f2(-a.ks);
         const float4* cx4 = reinterpret_cast<const float4*>(colv + 128);
-        float2 sum2 = f2(0.f);
+        float2 sum2 = f2(0.f), sumb = f2(0.f);   // two chains (ILP)
 #pragma unroll
         for (int j = 0; j < NJ; j += 2) {
           float2 arg = fma2(make_float2(__uint_as_float(gr[j]), __uint_as_float(gr[j + 1])), ks2,
@@ -485,8 +496,10 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
           }
           e[j] = fast_ex2(arg.x);
           e[j + 1] = fast_ex2(arg.y);
-          sum2 = add2(sum2, make_float2(e[j], e[j + 1]));
+          if (j & 2) sumb = add2(sumb, make_float2(e[j], e[j + 1]));
+          else sum2 = add2(sum2, make_float2(e[j], e[j + 1]));
         }
+        sum2 = add2(sum2, sumb);
         colv[96 + i] = valid ? fast_rcp(sum2.x + sum2.y) : 0.f;
         __syncwarp();
         const float4* cr4 = reinterpret_cast<const float4*>(colv + 96);
@@ -664,7 +677,8 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
 
 constexpr int kQWBytes = 8192;   // per-channel W' tile (hi | lo, K = 2 x 64)
 
-int tc_wpack_bytes() { return kQWBytes; }
+// per-channel W' bytes: 32 m-rows (M <= 32), or 64 (M <= 64, the generic-S kernel only)
+int tc_wpack_bytes(int M) { return M <= 32 ? kQWBytes : 2 * kQWBytes; }
 
 // (host) // W' as the K-major B operand: element (m, k) at (m/8)*2048 + (k/8)*128 + (m%8)*16 + (k%8)*2,
 // k = i (seasonal, 0..31) | 32 + i (trend) for hi, and +64 for lo.
@@ -682,8 +696,9 @@ void pack_tc_head(const float* ws, const float* wt, int Cw, int M, int N, unsign
       sw = ldexpf(1.f, -e);
     }
     inv_sw[c] = 1.f / sw;
-    __half* dst = reinterpret_cast<__half*>(out + (size_t)c * kQWBytes);
-    for (int m = 0; m < 32; m++)
+    const int rows = M <= 32 ? 32 : 64;
+    __half* dst = reinterpret_cast<__half*>(out + (size_t)c * tc_wpack_bytes(M));
+    for (int m = 0; m < rows; m++)
       for (int k = 0; k < 64; k++) {
         float v = 0.f;
         if (m < M) {

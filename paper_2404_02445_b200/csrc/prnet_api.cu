@@ -151,8 +151,9 @@ bool flash_applicable(const prnet_handle* h) {
 // the tcgen05 head tile (pack_tc_head) is packed for every N <= 32, M <= 32 handle with a
 // tc_quad instantiation (S = 24: fwd_tcq.cu; S in {12, 16, 32, 48, 64, 96}: fwd_tcg.cu)
 bool tc_head_shape(const prnet_handle* h) {
-  return (h->cfg.seg_len == 24 || prnet::tcg_supported_s(h->cfg.seg_len)) && h->N <= 32 &&
-         h->M <= 32;
+  if (h->N > 32) return false;
+  if (h->cfg.seg_len == 24) return h->M <= 32;
+  return prnet::tcg_supported_s(h->cfg.seg_len) && h->M <= 64;   // fwd_tcg.cu: M <= 64
 }
 // 6 = tc_quad (S = 24, N <= 32, M <= 32, tau_s >= 1/80: quads of series on tcgen05 / TMEM,
 // seasonal shift 1 >= rho keeps the diagonal term normal only down to tau_s = 1/80)
@@ -195,7 +196,7 @@ bool known_max_ok(const prnet_handle* h) { return h->cfg.tau_seasonal >= kTauKno
 // 8 = tc_long (32 < N <= 512, S in {12, 24, 48, 96}, M <= 32, plain reading, tau_s >= 1/320:
 // 128-row query tiles on tcgen05 / TMEM, key tiles of 64, known seasonal row bound)
 bool tcl_applicable(const prnet_handle* h) {
-  return h->N > 32 && h->N <= 512 && h->M <= 32 && prnet::tcl_supported_s(h->cfg.seg_len) &&
+  return h->N > 32 && h->N <= 512 && h->M <= 64 && prnet::tcl_supported_s(h->cfg.seg_len) &&
          h->cfg.tau_seasonal >= 1.0f / 320.0f;
 }
 // 7 = small_f32 (N <= 16, S <= 128, M <= 32: lanes over time, FP32)
@@ -228,13 +229,16 @@ int pick_variant(const prnet_handle* h) {
   // tc_quad for S != 24 (fwd_tcg.cu), measured on B200 (profiles/README.md, round 2): stress
   // L336/S12 (N = 28) 0.230 vs 0.353 ms (mma_f16x3), L1440/S48 0.403 vs 0.980, L2880/S96 0.747
   // vs 2.444, L720/S48 (N = 15) 0.372 vs 0.434; mma_f16x3 stays ahead at L192/S12 (N = 16)
-  if (tcq_applicable(h) && (h->N > 16 || (h->N > 8 && h->cfg.seg_len == 48))) return 6;
+  if (tcq_applicable(h) &&
+      (h->N > 16 || (h->N > 8 && h->cfg.seg_len == 48) || h->M > 32))   // (M > 32: else FP32)
+    return 6;
   if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
   // tc_long (tcgen05) against flash_f16x3 (mma.sync), measured on B200 (profiles/README.md,
   // round 2): stress L5760/S96 (N = 60) 10.5 vs 11.9 ms, L5760/S48 (N = 120) 9.98 vs 11.6 ms;
   // flash stays ahead for S <= 24 (L5760/S12 27.4 vs 34.4 ms) and at L2880/S48 (4.56 vs 6.86)
-  if (tcl_applicable(h) && (h->cfg.seg_len == 96 || (h->cfg.seg_len == 48 && h->N >= 100)))
-    return 8;
+  if (tcl_applicable(h) && (!flash_applicable(h) || h->cfg.seg_len == 96 ||
+                            (h->cfg.seg_len == 48 && h->N >= 100)))
+    return 8;   // (M > 32: the only tensor-core kernel for N > 32)
   if (h->N > 32 && flash_applicable(h)) return 5;
   return h->N <= 32 ? 0 : 1;
 }
@@ -491,7 +495,7 @@ prnet_status prnet_load_params(prnet_handle* h, const float* w_seasonal, const f
             cudaSuccess)
       return cuda_fail(h, e, "cudaMemcpy(packed head)");
   }
-  if (flash_applicable(h)) {  // head for the key-streaming kernel
+  if (flash_applicable(h) || tcl_applicable(h)) {  // head for the key-streaming kernels
     const int bytes = prnet::flash_wpack_bytes(h->N, h->M);
     std::vector<unsigned char> pack((size_t)h->Cw * bytes);
     std::vector<float> inv(h->Cw);
@@ -506,7 +510,7 @@ prnet_status prnet_load_params(prnet_handle* h, const float* w_seasonal, const f
       return cuda_fail(h, e, "cudaMemcpy(flash head)");
   }
   if (tc_head_shape(h)) {  // the same head as the tcgen05 B operand (K-major core matrices)
-    const int bytes = prnet::tc_wpack_bytes();
+    const int bytes = prnet::tc_wpack_bytes(h->M);
     std::vector<unsigned char> pack((size_t)h->Cw * bytes);
     std::vector<float> inv(h->Cw);
     prnet::pack_tc_head(w_seasonal, w_trend, h->Cw, h->M, h->N, pack.data(), inv.data());
@@ -515,6 +519,12 @@ prnet_status prnet_load_params(prnet_handle* h, const float* w_seasonal, const f
     if ((e = cudaMemcpy(h->d_wpack_tc, pack.data(), pack.size(), cudaMemcpyHostToDevice)) !=
         cudaSuccess)
       return cuda_fail(h, e, "cudaMemcpy(tc head)");
+    // 1 / sw (the same power-of-two scale as the mma pack's, which M > 32 handles do not build)
+    if (!h->d_invsw && (e = cudaMalloc(&h->d_invsw, inv.size() * 4)) != cudaSuccess)
+      return cuda_fail(h, e, "cudaMalloc(tc head scale)");
+    if ((e = cudaMemcpy(h->d_invsw, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice)) !=
+        cudaSuccess)
+      return cuda_fail(h, e, "cudaMemcpy(tc head scale)");
   }
   h->loaded = true;
   return PRNET_OK;
@@ -801,7 +811,7 @@ prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {
     return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,...,8}");
   if (variant == 8 && !tcl_applicable(h))
     return fail(h, PRNET_ERR_UNSUPPORTED,
-                "tc_long variant needs 32 < N <= 512, S in {12, 24, 48, 96}, M <= 32, "
+                "tc_long variant needs 32 < N <= 512, S in {12, 24, 48, 96}, M <= 64, "
                 "tau_seasonal >= 1/320");
   if (variant == 3 || variant == 4)
     return fail(h, PRNET_ERR_INVALID_ARG,
@@ -810,7 +820,7 @@ prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {
     return fail(h, PRNET_ERR_UNSUPPORTED, "small_f32 variant needs N <= 16, S <= 128, M <= 32");
   if (variant == 6 && !tcq_applicable(h))
     return fail(h, PRNET_ERR_UNSUPPORTED,
-                "tc_quad variant needs S in {12, 16, 24, 32, 48, 64, 96}, N <= 32, M <= 32, tau_seasonal >= 1/80");
+                "tc_quad variant needs S in {12, 16, 24, 32, 48, 64, 96}, N <= 32, M <= 32 (S = 24) or M <= 64, tau_seasonal >= 1/80");
   if ((variant == 2 || variant == 5 || variant == 7) && !known_max_ok(h))
     return fail(h, PRNET_ERR_UNSUPPORTED,
                 "small_f32 / mma_f16x3 / flash_f16x3 need tau_seasonal >= 1/320 (known-maximum "

@@ -85,8 +85,9 @@ WORKLOADS = {
 STRESS_GRID = [(L, S) for L in (96, 192, 336, 720, 1440, 2880, 5760) for S in (12, 24, 48, 96)
                if L // S >= 1]
 for _L, _S in STRESS_GRID:
-    _w = _stress(_L, _S)
-    WORKLOADS[_w.name] = _w
+    for _H in (96, 720):   # H = 96 is the proposed default; "also run H = 720"
+        _w = _stress(_L, _S, _H)
+        WORKLOADS[_w.name] = _w
 
 
 def _rng(seed: int, cfg_id: int, stream: int) -> np.random.Generator:

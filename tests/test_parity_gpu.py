@@ -35,13 +35,13 @@ def _applicable(variant, L, S, H):
     if variant == "mma_f16x3":
         return N <= 32 and M <= 32 and S <= 128
     if variant == "tc_quad":
-        return S in (12, 16, 24, 32, 48, 64, 96) and N <= 32 and M <= 32
+        return S in (12, 16, 24, 32, 48, 64, 96) and N <= 32 and M <= (32 if S == 24 else 64)
     if variant == "small_f32":
         return N <= 16 and S <= 128 and M <= 32
     if variant == "flash_f16x3":
         return 16 < N <= 512 and S <= 96 and M <= 32
     if variant == "tc_long":
-        return 32 < N <= 512 and S in (12, 24, 48, 96) and M <= 32
+        return 32 < N <= 512 and S in (12, 24, 48, 96) and M <= 64
     return True
 
 

@@ -23,7 +23,7 @@ S_VALUES = (12, 16, 32, 48, 64, 96)
 
 def _run(oracle_mod, B, C, L, S, H, kind="mixed", tau_s=1.0, tau_t=1.0, hpc=True, seed=11):
     N, _, M = synth.derived_dims(L, S, H)
-    assert N <= 32 and M <= 32
+    assert N <= 32 and M <= 64
     x = synth.random_windows(B, C, L, seed=seed, kind=kind)
     ws, wt, b = synth.make_params(C, M, N, H, hpc, synth.DEFAULT_SEED, 0)
     m = PRNet(C, L, S, H, head_per_channel=hpc, tau_s=tau_s, tau_t=tau_t).load(ws, wt, b)
@@ -44,12 +44,14 @@ def test_tcg_segments(oracle_mod, S, N):
 
 
 @pytest.mark.parametrize("S", S_VALUES)
-@pytest.mark.parametrize("L,H", [(None, 1), (None, 7), (None, 97), (None, 200), (None, 720)])
+@pytest.mark.parametrize("L,H", [(None, 1), (None, 7), (None, 97), (None, 200), (None, 720),
+                                 (None, 385), (None, 768)])
 def test_tcg_horizons(oracle_mod, S, L, H):
+    """H up to 64 S: M > 32 runs the head in two passes of 32 future segments."""
     N = min(32, max(1, 700 // S))
     M = -(-H // S)
-    if M > 32:
-        pytest.skip("M > 32")
+    if M > 64:
+        pytest.skip("M > 64")
     _run(oracle_mod, 6, 3, N * S + 5, S, H)
 
 

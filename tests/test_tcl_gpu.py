@@ -42,11 +42,11 @@ def test_tcl_segments(oracle_mod, S, N):
 
 
 @pytest.mark.parametrize("S", [12, 24, 48, 96])
-@pytest.mark.parametrize("H", [1, 7, 97, 200, 384])
+@pytest.mark.parametrize("H", [1, 7, 97, 200, 384, 720, 768])
 def test_tcl_horizons(oracle_mod, S, H):
     N = {12: 100, 24: 70, 48: 40, 96: 36}[S]
-    if -(-H // S) > 32:
-        pytest.skip("M > 32")
+    if -(-H // S) > 64:
+        pytest.skip("M > 64")
     _run(oracle_mod, 2, 3, N * S + 4, S, H)
 
 
