@@ -220,6 +220,23 @@ prnet_status prnet_backward_head(prnet_handle* h, const float* x, int64_t batch,
                                  const float* dy, float* dws, float* dwt, float* db,
                                  void* cuda_stream);
 
+/* SURVEY §8(f) f4, the full backward (reading R-f7 in DESIGN.md §3): for the upstream
+ * gradient dy = dL/dy [B][C][H] (device, fp32) of one forward over x [B][C][L], writes
+ *   dx   [B][C][L]   dL/dx (0 at the r dropped oldest points of each window),
+ *   dws, dwt [Cw][M][N], db [Cw][H]   the head gradients, summed over the batch (and over the
+ *                     channels for a shared head), as prnet_backward_head,
+ *   dtau [2]          dL/dtau_seasonal, dL/dtau_trend, summed over every series,
+ * all device fp32, overwritten (B = 0: zero head / temperature gradients).  The attention is
+ * recomputed in FP32 (row maxima searched: every tau > 0), each step the adjoint of one
+ * Definition step; deterministic (fixed-order reductions, no atomics).  Uses the per-handle
+ * device workspace of prnet_backward_head (not stream-concurrent on one handle).  Base reading
+ * only.  Errors: BAD_STATE (before load_params), INVALID_ARG (B < 0, NULL pointers),
+ * UNSUPPORTED (N > 32, M > 64, S > 128, metric_variant bits 1-2, instance_norm, ma_kernel,
+ * pointers not on the handle's device), CUDA, OOM. */
+prnet_status prnet_backward(prnet_handle* h, const float* x, int64_t batch, const float* dy,
+                            float* dx, float* dws, float* dwt, float* db, float* dtau,
+                            void* cuda_stream);
+
 /* Select the forward kernel (tuning / cross-checking; default -1 = automatic).
  * All variants compute the same reading to within the documented tolerance:
  *   0 = warp_f32     one warp per series, CUDA-core FP32                  (N <= 32)

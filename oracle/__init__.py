@@ -83,6 +83,11 @@ def _load():
             ctypes.c_double, ctypes.c_int32, ctypes.c_int32, ctypes.c_double, ctypes.c_int32,
             _f32p, _f64p, _f64p, _f64p]
         lib.oracle_backward_head_ex.restype = ctypes.c_int
+        lib.oracle_backward.argtypes = [
+            _f32p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+            ctypes.c_int32, _f32p, _f32p, _f32p, ctypes.c_int32, ctypes.c_double,
+            ctypes.c_double, ctypes.c_int32, _f32p, _f64p, _f64p, _f64p, _f64p, _f64p]
+        lib.oracle_backward.restype = ctypes.c_int
         lib.oracle_error_sums.argtypes = [_f32p, _f32p, ctypes.c_int64, _f64p]
         lib.oracle_error_sums.restype = None
         _lib = lib
@@ -172,6 +177,31 @@ def backward_head(x, S, H, ws, wt, bias, dy, head_per_channel=True, tau_s=1.0, t
                                        float(eps_r), int(ma_kernel), dy, dws, dwt, db) != 0:
         raise ValueError("oracle_backward_head rejected its arguments")
     return dws, dwt, db
+
+
+def backward(x, S, H, ws, wt, bias, dy, head_per_channel=True, tau_s=1.0, tau_t=1.0,
+             metric_variant=0):
+    """The full backward (reading R-f7), fp64: gradients of sum(dy * y)
+    with respect to x [B, C, L], the head (dws, dwt [Cw, M, N], db [Cw, H]) and the
+    temperatures (dtau = [dL/dtau_s, dL/dtau_t]).  Base reading (metric_variant 0 or 1)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    B, C, L = x.shape
+    N, r, M = dims(L, S, H)
+    Cw = C if head_per_channel else 1
+    ws = np.ascontiguousarray(ws, dtype=np.float32).reshape(Cw, M, N)
+    wt = np.ascontiguousarray(wt, dtype=np.float32).reshape(Cw, M, N)
+    bias = np.ascontiguousarray(bias, dtype=np.float32).reshape(Cw, H)
+    dy = np.ascontiguousarray(dy, dtype=np.float32).reshape(B, C, H)
+    dx = np.zeros((B, C, L))
+    dws = np.zeros((Cw, M, N))
+    dwt = np.zeros((Cw, M, N))
+    db = np.zeros((Cw, H))
+    dtau = np.zeros(2)
+    if _load().oracle_backward(x, B, C, L, S, H, ws, wt, bias, int(bool(head_per_channel)),
+                               float(tau_s), float(tau_t), int(metric_variant), dy, dx, dws,
+                               dwt, db, dtau) != 0:
+        raise ValueError("oracle_backward rejected its arguments")
+    return {"dx": dx, "dws": dws, "dwt": dwt, "db": db, "dtau": dtau}
 
 
 def error_sums(y, target):

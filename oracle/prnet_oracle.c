@@ -442,3 +442,266 @@ int oracle_backward_head_ex(const float* x, int64_t B, int32_t C, int32_t L, int
   free(Ps); free(Pt); free(X); free(yy);
   return rc;
 }
+
+/* ------------------------------------------------------------------------------------------
+ * SURVEY §8(f) f4, the full backward (reading R-f7 in DESIGN.md §3): gradients of
+ * L = sum_h dy[h] y[h] with respect to the input x, the head (ws, wt, bias) and the
+ * temperatures tau_s, tau_t, for the base reading (metric_variant bit 0, the level-only
+ * trend, allowed: it only zeroes the kappa weight of Def 7).  Each step below is the
+ * adjoint of one forward Definition step, applied in reverse order (Def 11 back to Def 2);
+ * the forward quantities come from the forward functions above, recomputed in fp64.
+ * ------------------------------------------------------------------------------------------ */
+
+/* adjoint of Def 10-11: dY[m][t] = dy[m S + t] (0 past H); db[h] += dy[h];
+ * dws[m][n] += sum_t dY[m][t] P_s[n][t] (dwt likewise);
+ * dP_s[n][t] = sum_m ws[m][n] dY[m][t] (dP_t likewise). */
+static void oracle_head_adj(const double* Ps, const double* Pt, const float* ws, const float* wt,
+                            const float* dy, int N, int S, int M, int H, double* dws,
+                            double* dwt, double* db, double* dPs, double* dPt) {
+  for (int h = 0; h < H; h++) db[h] += (double)dy[h];
+  for (int m = 0; m < M; m++)
+    for (int n = 0; n < N; n++) {
+      double as = 0.0, at = 0.0;
+      for (int t = 0; t < S; t++) {
+        int h = m * S + t;
+        double dY = h < H ? (double)dy[h] : 0.0;
+        as += dY * Ps[n * S + t];
+        at += dY * Pt[n * S + t];
+      }
+      dws[m * N + n] += as;
+      dwt[m * N + n] += at;
+    }
+  for (int n = 0; n < N; n++)
+    for (int t = 0; t < S; t++) {
+      double gs = 0.0, gt = 0.0;
+      for (int m = 0; m < M; m++) {
+        int h = m * S + t;
+        double dY = h < H ? (double)dy[h] : 0.0;
+        gs += (double)ws[m * N + n] * dY;
+        gt += (double)wt[m * N + n] * dY;
+      }
+      dPs[n * S + t] = gs;
+      dPt[n * S + t] = gt;
+    }
+}
+
+/* adjoint of Def 9 (P = A X): dA[i][j] = sum_t dP[i][t] X[j][t];
+ * dX[j][t] += sum_i A[i][j] dP[i][t]. */
+static void oracle_aggregate_adj(const double* A, const double* X, const double* dP, int N, int S,
+                                 double* dA, double* dX) {
+  for (int i = 0; i < N; i++)
+    for (int j = 0; j < N; j++) {
+      double s = 0.0;
+      for (int t = 0; t < S; t++) s += dP[i * S + t] * X[j * S + t];
+      dA[i * N + j] = s;
+    }
+  for (int j = 0; j < N; j++)
+    for (int t = 0; t < S; t++) {
+      double s = 0.0;
+      for (int i = 0; i < N; i++) s += A[i * N + j] * dP[i * S + t];
+      dX[j * S + t] += s;
+    }
+}
+
+/* adjoint of one row softmax of Def 8 (A = softmax_j(l)): dl[i][j] = A[i][j] (dA[i][j] -
+ * sum_k A[i][k] dA[i][k]). */
+static void oracle_softmax_adj(const double* A, const double* dA, int N, double* dl) {
+  for (int i = 0; i < N; i++) {
+    double s = 0.0;
+    for (int k = 0; k < N; k++) s += A[i * N + k] * dA[i * N + k];
+    for (int j = 0; j < N; j++) dl[i * N + j] = A[i * N + j] * (dA[i * N + j] - s);
+  }
+}
+
+/* adjoint of Def 7 with its normalisation Dhat = D / (sigma2 + eps_t) and the trend logits
+ * l_t = -Dhat / tau_t: dDhat = -dl_t / tau_t; dtau_t += sum dl_t Dhat / tau_t^2;
+ * dD = dDhat / (sigma2 + eps_t); dsigma2 += -sum dDhat D / (sigma2 + eps_t)^2;
+ * D_ij = (mu_i - mu_j)^2 + w (kappa_i - kappa_j)^2 (w = (S^2 - 1)/12, 0 for bit 0):
+ * dmu_i += 2 (mu_i - mu_j) dD_ij, dmu_j -= 2 (mu_i - mu_j) dD_ij (kappa likewise with w). */
+static void oracle_trend_adj(const double* mu, const double* kappa, const double* D,
+                             double sigma2, const double* dlt, int N, int S, int level_only,
+                             double tau_t, double* dmu, double* dkappa, double* dsigma2,
+                             double* dtau_t) {
+  double w = level_only ? 0.0 : ((double)S * (double)S - 1.0) / 12.0;
+  double den = sigma2 + ORACLE_EPS_T;
+  for (int i = 0; i < N; i++)
+    for (int j = 0; j < N; j++) {
+      double Dh = D[i * N + j] / den;
+      double dDh = -dlt[i * N + j] / tau_t;
+      *dtau_t += dlt[i * N + j] * Dh / (tau_t * tau_t);
+      double dD = dDh / den;
+      *dsigma2 += -dDh * D[i * N + j] / (den * den);
+      double gm = 2.0 * (mu[i] - mu[j]) * dD;
+      double gk = 2.0 * w * (kappa[i] - kappa[j]) * dD;
+      dmu[i] += gm;
+      dmu[j] -= gm;
+      dkappa[i] += gk;
+      dkappa[j] -= gk;
+    }
+}
+
+/* adjoint of Def 6 with the seasonal logits l_s = rho / tau_s: drho = dl_s / tau_s;
+ * dtau_s += -sum dl_s rho / tau_s^2; rho_ij = <z_i, z_j> g_i g_j with
+ * g_n = (nu2_n + eps_s)^(-1/2):
+ *   dz_i[t] += sum_j drho_ij g_i g_j z_j[t],  dz_j[t] += sum_i drho_ij g_i g_j z_i[t],
+ *   dg_i += sum_j drho_ij <z_i, z_j> g_j,     dg_j += sum_i drho_ij <z_i, z_j> g_i,
+ *   dnu2_n += dg_n (-1/2) (nu2_n + eps_s)^(-3/2). */
+static void oracle_seasonal_adj(const double* z, const double* nu2, const double* rho,
+                                const double* dls, int N, int S, double tau_s, double* dz,
+                                double* dnu2, double* dtau_s) {
+  double* g = (double*)malloc(N * sizeof(double));
+  double* dg = (double*)calloc(N, sizeof(double));
+  for (int n = 0; n < N; n++) g[n] = 1.0 / sqrt(nu2[n] + ORACLE_EPS_S);
+  for (int i = 0; i < N; i++)
+    for (int j = 0; j < N; j++) {
+      double drho = dls[i * N + j] / tau_s;
+      *dtau_s += -dls[i * N + j] * rho[i * N + j] / (tau_s * tau_s);
+      double G = 0.0;
+      for (int t = 0; t < S; t++) G += z[i * S + t] * z[j * S + t];
+      for (int t = 0; t < S; t++) {
+        dz[i * S + t] += drho * g[i] * g[j] * z[j * S + t];
+        dz[j * S + t] += drho * g[i] * g[j] * z[i * S + t];
+      }
+      dg[i] += drho * G * g[j];
+      dg[j] += drho * G * g[i];
+    }
+  for (int n = 0; n < N; n++)
+    dnu2[n] += dg[n] * (-0.5) * pow(nu2[n] + ORACLE_EPS_S, -1.5);
+  free(g);
+  free(dg);
+}
+
+/* adjoint of Def 5: sigma2 = (1/(N S)) sum_n [nu2_n + S (mu_n - mubar)^2]:
+ * dnu2_n += dsigma2 / (N S);  dmu_n += dsigma2 2 (mu_n - mubar) / N
+ * (the mubar path contributes sum_n (mu_n - mubar) = 0). */
+static void oracle_series_variance_adj(const double* mu, int N, int S, double dsigma2,
+                                       double* dnu2, double* dmu) {
+  double mbar = 0.0;
+  for (int n = 0; n < N; n++) mbar += mu[n];
+  mbar /= (double)N;
+  for (int n = 0; n < N; n++) {
+    dnu2[n] += dsigma2 / ((double)N * (double)S);
+    dmu[n] += dsigma2 * 2.0 * (mu[n] - mbar) / (double)N;
+  }
+}
+
+/* adjoint of Def 3-4: nu2_n = sum_t z_n[t]^2 -> dz_n[t] += 2 z_n[t] dnu2_n;
+ * kappa_n = sum_t ttilde_t z_n[t] / V -> dz_n[t] += ttilde_t dkappa_n / V;
+ * z_n = X_n - mu_n -> dX_n[t] += dz_n[t], dmu_n -= sum_t dz_n[t];
+ * mu_n = (1/S) sum_t X_n[t] -> dX_n[t] += dmu_n / S. */
+static void oracle_descriptors_adj(const double* z, int N, int S, const double* dnu2,
+                                   const double* dkappa, double* dz, double* dmu, double* dX) {
+  double V = 0.0;
+  for (int t = 0; t < S; t++) {
+    double tt = (double)t - 0.5 * (double)(S - 1);
+    V += tt * tt;
+  }
+  for (int n = 0; n < N; n++) {
+    for (int t = 0; t < S; t++) {
+      double tt = (double)t - 0.5 * (double)(S - 1);
+      dz[n * S + t] += 2.0 * z[n * S + t] * dnu2[n] + tt * dkappa[n] / V;
+    }
+    double s = 0.0;
+    for (int t = 0; t < S; t++) {
+      dX[n * S + t] += dz[n * S + t];
+      s += dz[n * S + t];
+    }
+    dmu[n] -= s;
+    for (int t = 0; t < S; t++) dX[n * S + t] += dmu[n] / (double)S;
+  }
+}
+
+/* One series: the adjoint chain Def 11 -> Def 2.  dx (L doubles) is overwritten (0 for the
+ * r dropped points); dws/dwt ([M][N]), db ([H]) and dtau ([2]: tau_s, tau_t) accumulate. */
+int oracle_backward_series(const float* x, int32_t L, int32_t S, int32_t H, const float* ws,
+                           const float* wt, const float* bias, double tau_s, double tau_t,
+                           int32_t metric_variant, const float* dy, double* dx, double* dws,
+                           double* dwt, double* db, double* dtau) {
+  int32_t N, r, M;
+  if (oracle_dims(L, S, H, &N, &r, &M) != 0 || !(tau_s > 0.0) || !(tau_t > 0.0) ||
+      (metric_variant & ~1) != 0)
+    return -1;
+  size_t nS = (size_t)N * S, nN = (size_t)N * N;
+  double* X = (double*)malloc(nS * sizeof(double));
+  double* mu = (double*)malloc(N * sizeof(double));
+  double* z = (double*)malloc(nS * sizeof(double));
+  double* nu2 = (double*)malloc(N * sizeof(double));
+  double* kappa = (double*)malloc(N * sizeof(double));
+  double* rho = (double*)malloc(nN * sizeof(double));
+  double* D = (double*)malloc(nN * sizeof(double));
+  double* Dh = (double*)malloc(nN * sizeof(double));
+  double* As = (double*)malloc(nN * sizeof(double));
+  double* At = (double*)malloc(nN * sizeof(double));
+  double* Ps = (double*)malloc(nS * sizeof(double));
+  double* Pt = (double*)malloc(nS * sizeof(double));
+  double* dPs = (double*)malloc(nS * sizeof(double));
+  double* dPt = (double*)malloc(nS * sizeof(double));
+  double* dAs = (double*)malloc(nN * sizeof(double));
+  double* dAt = (double*)malloc(nN * sizeof(double));
+  double* dls = (double*)malloc(nN * sizeof(double));
+  double* dlt = (double*)malloc(nN * sizeof(double));
+  double* dX = (double*)calloc(nS, sizeof(double));
+  double* dz = (double*)calloc(nS, sizeof(double));
+  double* dmu = (double*)calloc(N, sizeof(double));
+  double* dkappa = (double*)calloc(N, sizeof(double));
+  double* dnu2 = (double*)calloc(N, sizeof(double));
+
+  /* forward, Def 2-9 (the functions above) */
+  oracle_segment(x, N, S, r, X);
+  oracle_descriptors(X, N, S, mu, z, nu2, kappa);
+  double sigma2 = oracle_series_variance(mu, nu2, N, S);
+  oracle_seasonal_similarity(z, nu2, N, S, rho);
+  oracle_trend_distance(mu, kappa, N, S, metric_variant & 1, D);
+  for (size_t k = 0; k < nN; k++) Dh[k] = D[k] / (sigma2 + ORACLE_EPS_T);
+  oracle_softmax_rows(rho, N, +1.0, 1.0 / tau_s, As);
+  oracle_softmax_rows(Dh, N, -1.0, 1.0 / tau_t, At);
+  oracle_aggregate(As, X, N, S, Ps);
+  oracle_aggregate(At, X, N, S, Pt);
+  (void)bias;   /* y = Y + b: the bias enters the gradient only as db */
+
+  /* adjoints, Def 11 -> Def 2 */
+  oracle_head_adj(Ps, Pt, ws, wt, dy, N, S, M, H, dws, dwt, db, dPs, dPt);   /* Def 10-11 */
+  oracle_aggregate_adj(As, X, dPs, N, S, dAs, dX);                          /* Def 9 (s) */
+  oracle_aggregate_adj(At, X, dPt, N, S, dAt, dX);                          /* Def 9 (t) */
+  oracle_softmax_adj(As, dAs, N, dls);                                      /* Def 8 (s) */
+  oracle_softmax_adj(At, dAt, N, dlt);                                      /* Def 8 (t) */
+  double dsigma2 = 0.0;
+  oracle_trend_adj(mu, kappa, D, sigma2, dlt, N, S, metric_variant & 1, tau_t, dmu, dkappa,
+                   &dsigma2, &dtau[1]);                                     /* Def 7     */
+  oracle_seasonal_adj(z, nu2, rho, dls, N, S, tau_s, dz, dnu2, &dtau[0]);   /* Def 6     */
+  oracle_series_variance_adj(mu, N, S, dsigma2, dnu2, dmu);                 /* Def 5     */
+  oracle_descriptors_adj(z, N, S, dnu2, dkappa, dz, dmu, dX);               /* Def 3-4   */
+  for (int32_t k = 0; k < L; k++) dx[k] = 0.0;                              /* Def 2     */
+  for (int n = 0; n < N; n++)
+    for (int t = 0; t < S; t++) dx[r + n * S + t] = dX[n * S + t];
+
+  free(X); free(mu); free(z); free(nu2); free(kappa); free(rho); free(D); free(Dh);
+  free(As); free(At); free(Ps); free(Pt); free(dPs); free(dPt); free(dAs); free(dAt);
+  free(dls); free(dlt); free(dX); free(dz); free(dmu); free(dkappa); free(dnu2);
+  return 0;
+}
+
+int oracle_backward(const float* x, int64_t B, int32_t C, int32_t L, int32_t S, int32_t H,
+                    const float* ws, const float* wt, const float* bias,
+                    int32_t head_per_channel, double tau_s, double tau_t,
+                    int32_t metric_variant, const float* dy, double* dx, double* dws,
+                    double* dwt, double* db, double* dtau) {
+  int32_t N, r, M;
+  if (B < 0 || C < 1 || oracle_dims(L, S, H, &N, &r, &M) != 0) return -1;
+  int32_t Cw = head_per_channel ? C : 1;
+  memset(dws, 0, (size_t)Cw * M * N * sizeof(double));
+  memset(dwt, 0, (size_t)Cw * M * N * sizeof(double));
+  memset(db, 0, (size_t)Cw * H * sizeof(double));
+  dtau[0] = dtau[1] = 0.0;
+  for (int64_t b = 0; b < B; b++)
+    for (int32_t c = 0; c < C; c++) {
+      int64_t cw = head_per_channel ? c : 0;
+      int64_t o = b * C + c;
+      if (oracle_backward_series(x + o * L, L, S, H, ws + cw * M * N, wt + cw * M * N,
+                                 bias + cw * H, tau_s, tau_t, metric_variant, dy + o * H,
+                                 dx + o * L, dws + cw * M * N, dwt + cw * M * N, db + cw * H,
+                                 dtau) != 0)
+        return -1;
+    }
+  return 0;
+}

@@ -109,6 +109,23 @@ int oracle_backward_head_ex(const float* x, int64_t B, int32_t C, int32_t L, int
                             int32_t ma_kernel, const float* dy, double* dws, double* dwt,
                             double* db);
 
+/* SURVEY §8(f) f4, the full backward (reading R-f7): gradients of L = sum dy * y with
+ * respect to the input x (dx [B][C][L], 0 at the r dropped points), the head (dws, dwt
+ * [Cw][M][N], db [Cw][H], summed over the batch) and the temperatures (dtau[0] = dL/dtau_s,
+ * dtau[1] = dL/dtau_t, summed over every series), for the base reading (metric_variant 0
+ * or 1).  The adjoint of each Definition step is its own function, applied Def 11 -> Def 2.
+ * Outputs are fp64 and overwritten.  Returns 0 or -1. */
+int oracle_backward(const float* x, int64_t B, int32_t C, int32_t L, int32_t S, int32_t H,
+                    const float* ws, const float* wt, const float* bias,
+                    int32_t head_per_channel, double tau_s, double tau_t,
+                    int32_t metric_variant, const float* dy, double* dx, double* dws,
+                    double* dwt, double* db, double* dtau);
+/* one series (dws, dwt, db, dtau accumulate; dx [L] overwritten) */
+int oracle_backward_series(const float* x, int32_t L, int32_t S, int32_t H, const float* ws,
+                           const float* wt, const float* bias, double tau_s, double tau_t,
+                           int32_t metric_variant, const float* dy, double* dx, double* dws,
+                           double* dwt, double* db, double* dtau);
+
 /* Sum of squared and absolute errors of y against target (n values), fp64,
  * in index order: out[0] = SSE, out[1] = SAE, out[2] = n.  (Bench metric,
  * PAPER.md:22 "accuracy"; MSE = SSE/n, MAE = SAE/n.) */

@@ -1,6 +1,7 @@
 // prnet_api.cu -- the C ABI of include/prnet.h: validation, handle state,
 // kernel-variant selection, and the host-buffer streaming runtime
 // (prnet_forward_host).  No torch types, no exceptions across the boundary.
+#include <algorithm>
 #include <cmath>
 #include <cstddef>
 #include <cstdio>
@@ -803,6 +804,50 @@ prnet_status prnet_backward_head(prnet_handle* h, const float* x, int64_t batch,
   }
   cudaError_t e = prnet::launch_bwd_head(a, p, dy, h->d_bwd, dws, dwt, db, h->Cw, st);
   return e == cudaSuccess ? PRNET_OK : cuda_fail(h, e, "backward_head launch");
+}
+
+prnet_status prnet_backward(prnet_handle* h, const float* x, int64_t batch, const float* dy,
+                            float* dx, float* dws, float* dwt, float* db, float* dtau,
+                            void* cuda_stream) {
+  if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
+  if (!h->loaded) return fail(h, PRNET_ERR_BAD_STATE, "backward before prnet_load_params");
+  if (batch < 0) return fail(h, PRNET_ERR_INVALID_ARG, "batch < 0");
+  if (!dws || !dwt || !db || !dtau || (batch > 0 && (!x || !dy || !dx)))
+    return fail(h, PRNET_ERR_INVALID_ARG, "NULL pointer");
+  if ((h->cfg.metric_variant & ~1) != 0 || h->cfg.instance_norm || h->cfg.ma_kernel > 0)
+    return fail(h, PRNET_ERR_UNSUPPORTED,
+                "backward: the base reading only (metric_variant 0 or 1, no instance_norm, no "
+                "ma_kernel)");
+  prnet_status s = PRNET_OK;
+  if (batch > 0) {
+    s = check_dev_ptr(h, x, "x");
+    if (s == PRNET_OK) s = check_dev_ptr(h, dy, "dy");
+    if (s == PRNET_OK) s = check_dev_ptr(h, dx, "dx");
+  }
+  if (s == PRNET_OK) s = check_dev_ptr(h, dws, "dws");
+  if (s == PRNET_OK) s = check_dev_ptr(h, dwt, "dwt");
+  if (s == PRNET_OK) s = check_dev_ptr(h, db, "db");
+  if (s == PRNET_OK) s = check_dev_ptr(h, dtau, "dtau");
+  if (s != PRNET_OK) return s;
+  DeviceGuard g(h->cfg.device);
+  prnet::FwdArgs a = make_args(h, x, batch, nullptr);
+  prnet::BwdFullPlan p;
+  if (!prnet::plan_bwd_full(a, h->max_smem_optin, &p))
+    return fail(h, PRNET_ERR_UNSUPPORTED, "backward needs N <= 32, M <= 64, S <= 128");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int64_t need = (int64_t)h->cfg.channels * std::max(p.nblk, 1) * p.ly.elems;
+  if (need > h->bwd_floats) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(h, e, "backward sync");
+    cudaFree(h->d_bwd);
+    h->d_bwd = nullptr;
+    h->bwd_floats = 0;
+    e = cudaMalloc(&h->d_bwd, (size_t)need * sizeof(float));
+    if (e != cudaSuccess) return cuda_fail(h, e, "backward workspace");
+    h->bwd_floats = need;
+  }
+  cudaError_t e = prnet::launch_bwd_full(a, p, dy, dx, h->d_bwd, dws, dwt, db, dtau, h->Cw, st);
+  return e == cudaSuccess ? PRNET_OK : cuda_fail(h, e, "backward launch");
 }
 
 prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {

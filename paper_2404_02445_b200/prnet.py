@@ -24,7 +24,7 @@ EXPORTS = ("prnet_create", "prnet_load_params", "prnet_forward", "prnet_forward_
            "prnet_set_host_chunk", "prnet_destroy", "prnet_last_error", "prnet_get_dims",
            "prnet_debug_segments", "prnet_debug_attention", "prnet_error_sums",
            "prnet_forward_plan", "prnet_set_kernel_variant", "prnet_forward_sliding",
-           "prnet_forward_sliding_host", "prnet_backward_head")
+           "prnet_forward_sliding_host", "prnet_backward_head", "prnet_backward")
 # index = the C ABI's variant id (include/prnet.h); 3 and 4 are retired round-1 prototypes
 VARIANTS = ("warp_f32", "long_f32", "mma_f16x3", "retired_tc_fold", "retired_tc_full",
             "flash_f16x3", "tc_quad", "small_f32", "tc_long")
@@ -73,6 +73,7 @@ def load_library(path: str | None = None):
         "prnet_forward_plan": ([vp, i64, i32p, i32p], ctypes.c_int),
         "prnet_set_kernel_variant": ([vp, ctypes.c_int32], ctypes.c_int),
         "prnet_backward_head": ([vp, vp, i64, vp, vp, vp, vp, vp], ctypes.c_int),
+        "prnet_backward": ([vp, vp, i64, vp, vp, vp, vp, vp, vp, vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -251,6 +252,24 @@ class PRNet:
             ctypes.c_void_p(dws.data_ptr()), ctypes.c_void_p(dwt.data_ptr()),
             ctypes.c_void_p(db.data_ptr()), _stream_ptr(stream)))
         return dws, dwt, db
+
+    def backward(self, x, dy, stream=None):
+        """The full backward (reading R-f7): gradients of sum(dy * y) with
+        respect to x (dx [B,C,L]), the head (dws, dwt [Cw,M,N], db [Cw,H]) and the
+        temperatures (dtau [2]: tau_s, tau_t), for the forward of x (include/prnet.h)."""
+        import torch
+        cw = self.C if self.head_per_channel else 1
+        dx = torch.empty_like(x)
+        dws = torch.empty((cw, self.M, self.N), dtype=torch.float32, device=x.device)
+        dwt = torch.empty_like(dws)
+        db = torch.empty((cw, self.H), dtype=torch.float32, device=x.device)
+        dtau = torch.empty(2, dtype=torch.float32, device=x.device)
+        self._check(self._lib.prnet_backward(
+            self._h, ctypes.c_void_p(x.data_ptr()), x.shape[0], ctypes.c_void_p(dy.data_ptr()),
+            ctypes.c_void_p(dx.data_ptr()), ctypes.c_void_p(dws.data_ptr()),
+            ctypes.c_void_p(dwt.data_ptr()), ctypes.c_void_p(db.data_ptr()),
+            ctypes.c_void_p(dtau.data_ptr()), _stream_ptr(stream)))
+        return {"dx": dx, "dws": dws, "dwt": dwt, "db": db, "dtau": dtau}
 
     def plan(self, batch: int):
         n, v = ctypes.c_int32(), ctypes.c_int32()

@@ -1,4 +1,5 @@
-"""Time prnet_backward_head on a workload's windows (CUDA events, after warm-up)."""
+"""Time prnet_backward_head (or, with --full, prnet_backward) on a workload's windows
+(CUDA events, after warm-up): python tools/bwd_time.py [workload] [--full]"""
 import json
 import sys
 
@@ -9,23 +10,28 @@ sys.path.insert(0, ".")
 import synth  # noqa: E402
 from paper_2404_02445_b200 import PRNet  # noqa: E402
 
-name = sys.argv[1] if len(sys.argv) > 1 else "traffic"
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+full = "--full" in sys.argv
+name = args[0] if args else "traffic"
 w = synth.WORKLOADS[name]
 s = synth.make_series(w)
 sd = torch.from_numpy(s).cuda()
 x = sd.unfold(1, w.L, 1)[:, w.t0:w.t0 + w.windows, :].permute(1, 0, 2).contiguous()
 dy = torch.randn((w.windows, w.C, w.H), device="cuda")
 m = PRNet(w.C, w.L, w.S, w.H)
+fn = (lambda: m.backward(x, dy)) if full else (lambda: m.backward_head(x, dy))
 for _ in range(2):
-    m.backward_head(x, dy)
+    fn()
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 for _ in range(5):
-    m.backward_head(x, dy)
+    fn()
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 5
 byts = (w.windows * w.C * (w.L + w.H)) * 4
-print(json.dumps({"workload": name, "ms": ms, "windows_per_s": w.windows / ms * 1e3,
+if full:
+    byts += w.windows * w.C * w.L * 4   # dx written
+print(json.dumps({"workload": name, "pass": "full" if full else "head", "ms": ms, "windows_per_s": w.windows / ms * 1e3,
                   "hbm_frac": byts / (ms / 1e3) / 6552.3e9}))
