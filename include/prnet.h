@@ -220,6 +220,16 @@ prnet_status prnet_backward_head(prnet_handle* h, const float* x, int64_t batch,
                                  const float* dy, float* dws, float* dwt, float* db,
                                  void* cuda_stream);
 
+/* the forward with x [B][C][L] and y [B][C][H] as bf16 bit patterns
+ * (device, uint16_t; half the HBM bytes of prnet_forward).  The values are widened to fp32
+ * exactly and every step runs as in prnet_forward's S = 24 tc_quad kernel; y is rounded to the
+ * nearest bf16 (ties to even) at the store.  Needs the S = 24 tc_quad domain (N <= 32,
+ * M <= 32, tau_seasonal >= 1/80) and the base reading (metric_variant 0, no instance_norm, no
+ * ma_kernel).  x, y 4-byte aligned (16 bytes, L % 8 == 0, r % 8 == 0: one bulk copy per
+ * series), not overlapping.  Errors as prnet_forward; UNSUPPORTED outside that domain. */
+prnet_status prnet_forward_bf16(prnet_handle* h, const uint16_t* x, int64_t batch, uint16_t* y,
+                                void* cuda_stream);
+
 /* SURVEY §8(f) f4, the full backward (reading R-f7 in DESIGN.md §3): for the upstream
  * gradient dy = dL/dy [B][C][H] (device, fp32) of one forward over x [B][C][L], writes
  *   dx   [B][C][L]   dL/dx (0 at the r dropped oldest points of each window),

@@ -50,6 +50,7 @@
 //
 // Numerical domain: tau_s >= 1/80 (prnet_api.cu routes smaller seasonal temperatures to
 // the mma_f16x3 kernel, whose known-max shift covers tau_s > 0.003).
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
 #include <cmath>
@@ -103,7 +104,10 @@ __device__ __forceinline__ void sts128(unsigned char* p, uint4 v) {
 // masks; NC = 0: runtime N <= 32 with masks.  DUMP (prnet_debug_attention): the attention
 // values each lane hands to the TMEM store are also written to a_s_dbg / a_t_dbg, from the
 // same registers (this kernel's own softmax arithmetic, not another kernel's).
-template <int NC, bool WIDE, bool DUMP = false>
+// BF: BF16 I/O (prnet_forward_bf16): x is read and y written as bf16 (half
+// the HBM bytes); the staging row holds bf16 and is widened to fp32 in registers (exact), every
+// step after that is the fp32 kernel's; y is rounded to bf16 (round to nearest even) at the store
+template <int NC, bool WIDE, bool DUMP = false, bool BF = false>
 __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ctas_per_channel) {
   // WIDE: the SURVEY §8(f) widening (detrended seasonal metric, instance normalisation) is
   // compiled in; the plain instantiation is exactly the reading's kernel
@@ -193,6 +197,17 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
     return slide && ((uintptr_t)xg & ~(uintptr_t)15) + slide_bytes(xg) <= (uintptr_t)a.x_end;
   };
   auto issue_load = [&](const float* xg) {
+    if constexpr (BF) {   // xg addresses bf16 elements (the float pointer's arithmetic is unused)
+      const uint16_t* xb = reinterpret_cast<const uint16_t*>(a.x) +
+                           ((const float*)xg - a.x);
+      if (bulk) {
+        if (lane == 0) bulk_load(xstage, xb, (uint32_t)NS * 2u, xbar);
+      } else {
+        uint16_t* st16 = reinterpret_cast<uint16_t*>(xstage);
+        for (int k = lane; k < NS; k += 32) st16[k] = __ldg(xb + k);
+      }
+      return;
+    }
     if (bulk) {
       if (lane == 0) bulk_load(xstage, xg, (uint32_t)NS * 4u, xbar);
     } else if (slide_bulk(xg)) {
@@ -219,15 +234,29 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
     // (Def 4-5) from d = x - x0 (a constant segment gives exact zeros), Z' = z inv and
     // X' = x sx as fp16 hi/lo rows of the Gram / head operand tiles
     if (active) {
-      if (bulk || slide_bulk(xnext)) {
+      if (bulk || (!BF && slide_bulk(xnext))) {
         mbar_wait_bounded(xbar, xph);
         xph ^= 1u;
-      } else {
+      } else if (!BF) {
         cp_async_wait_all();
       }
       __syncwarp();
       float dv[24];
-      {
+      if constexpr (BF) {
+        // row i = 24 bf16 = 48 bytes (conflict-free quarter-warp 16-byte reads), widened
+        const uint4* xr = reinterpret_cast<const uint4*>(
+            reinterpret_cast<const unsigned char*>(xstage) + (valid ? i : N - 1) * 48);
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+          const uint4 u = xr[q];
+          const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int e = 0; e < 4; e++) {
+            xv[8 * q + 2 * e] = __uint_as_float(w4[e] << 16);
+            xv[8 * q + 2 * e + 1] = __uint_as_float(w4[e] & 0xFFFF0000u);
+          }
+        }
+      } else {
         const int o = slide ? slide_o(xnext) : 0;   // warp-uniform
         const float4* xr = reinterpret_cast<const float4*>(xstage + (valid ? i : N - 1) * 24);
         if (o == 0) {
@@ -268,7 +297,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
             for (int t = 0; t < 24; t++) xv[t] = w[t + 3];
           }
         }
-      }
+      }   // (fp32 staging)
       __syncwarp();
       // the staging row is in registers: fetch this warp's next series now
       xnext += xstep;
@@ -640,9 +669,16 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
                 float2 bb = *reinterpret_cast<const float2*>(br + 8 * nt);
                 if (revin) bb = fma2(bb, sr2, mr2);   // y = yhat sr + mr
                 const float2 o = fma2(make_float2(acc[mt][nt][2 * h], acc[mt][nt][2 * h + 1]), ys2, bb);
-                asm volatile("st.global.cs.v2.f32 [%0], {%1,%2};" ::"l"(yr + 8 * nt), "f"(o.x),
-                             "f"(o.y)
-                             : "memory");
+                if constexpr (BF) {
+                  uint32_t pk;
+                  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(pk) : "f"(o.y), "f"(o.x));
+                  uint16_t* yb = reinterpret_cast<uint16_t*>(a.y) + ((yr + 8 * nt) - a.y);
+                  asm volatile("st.global.cs.b32 [%0], %1;" ::"l"(yb), "r"(pk) : "memory");
+                } else {
+                  asm volatile("st.global.cs.v2.f32 [%0], {%1,%2};" ::"l"(yr + 8 * nt), "f"(o.x),
+                               "f"(o.y)
+                               : "memory");
+                }
               }
             }
           }
@@ -659,8 +695,14 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
               float2 bb = *reinterpret_cast<const float2*>(bq + m * kQBiasRow + 8 * nt);
               if (revin) bb = fma2(bb, sr2, mr2);
               const float2 o = fma2(make_float2(acc[mt][nt][2 * h], acc[mt][nt][2 * h + 1]), ys2, bb);
-              if (hh < H) yg[m * 24 + 8 * nt] = o.x;
-              if (hh + 1 < H) yg[m * 24 + 8 * nt + 1] = o.y;
+              if constexpr (BF) {
+                uint16_t* yb = reinterpret_cast<uint16_t*>(a.y) + ((yg + m * 24 + 8 * nt) - a.y);
+                if (hh < H) yb[0] = __bfloat16_as_ushort(__float2bfloat16_rn(o.x));
+                if (hh + 1 < H) yb[1] = __bfloat16_as_ushort(__float2bfloat16_rn(o.y));
+              } else {
+                if (hh < H) yg[m * 24 + 8 * nt] = o.x;
+                if (hh + 1 < H) yg[m * 24 + 8 * nt + 1] = o.y;
+              }
             }
           }
       }
@@ -740,9 +782,9 @@ bool plan_tcq_kernel(const FwdArgs& a, int max_smem_optin, int sm_count, TcqPlan
   return true;
 }
 
-template <int NC, bool WIDE, bool DUMP = false>
+template <int NC, bool WIDE, bool DUMP = false, bool BF = false>
 static cudaError_t launch_tcq_t(const FwdArgs& a, const TcqPlan& p, cudaStream_t st) {
-  auto k = prnet_fwd_tcq_kernel<NC, WIDE, DUMP>;
+  auto k = prnet_fwd_tcq_kernel<NC, WIDE, DUMP, BF>;
   cudaError_t e =
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
@@ -758,6 +800,9 @@ cudaError_t launch_tcq_kernel(const FwdArgs& a, const TcqPlan& p, cudaStream_t s
   // the attention dump: the generic-N instantiation with the widening compiled in (for the
   // plain reading its arithmetic is the N = 30 instantiation's: zero-mask adds, no flags)
   if (a.a_s_dbg != nullptr) return launch_tcq_t<0, true, true>(a, p, st);
+  if (a.io_bf16)   // BF16 I/O: the plain reading (prnet_forward_bf16 rejects the widening)
+    return a.N == 30 ? launch_tcq_t<30, false, false, true>(a, p, st)
+                     : launch_tcq_t<0, false, false, true>(a, p, st);
   const bool wide = a.detrend || a.revin;
   if (a.N == 30) return wide ? launch_tcq_t<30, true>(a, p, st) : launch_tcq_t<30, false>(a, p, st);
   return wide ? launch_tcq_t<0, true>(a, p, st) : launch_tcq_t<0, false>(a, p, st);

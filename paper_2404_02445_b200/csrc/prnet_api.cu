@@ -806,6 +806,38 @@ prnet_status prnet_backward_head(prnet_handle* h, const float* x, int64_t batch,
   return e == cudaSuccess ? PRNET_OK : cuda_fail(h, e, "backward_head launch");
 }
 
+prnet_status prnet_forward_bf16(prnet_handle* h, const uint16_t* x, int64_t batch, uint16_t* y,
+                                void* cuda_stream) {
+  if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
+  if (!h->loaded) return fail(h, PRNET_ERR_BAD_STATE, "forward before prnet_load_params");
+  if (batch < 0) return fail(h, PRNET_ERR_INVALID_ARG, "batch < 0");
+  if (batch > 0 && (!x || !y)) return fail(h, PRNET_ERR_INVALID_ARG, "NULL pointer");
+  if (!tcq_wide_applicable(h) || widening_on(h) || (h->cfg.metric_variant & 1) != 0)
+    return fail(h, PRNET_ERR_UNSUPPORTED,
+                "forward_bf16 runs the S = 24 tc_quad kernel: N <= 32, M <= 32, "
+                "tau_seasonal >= 1/80, the base reading");
+  if (batch == 0) return PRNET_OK;
+  prnet_status s = check_dev_ptr(h, x, "x");
+  if (s == PRNET_OK) s = check_dev_ptr(h, y, "y");
+  if (s != PRNET_OK) return s;
+  const int64_t C = h->cfg.channels, L = h->cfg.lookback, H = h->cfg.horizon;
+  if (((uintptr_t)x & 3u) != 0 || ((uintptr_t)y & 3u) != 0)
+    return fail(h, PRNET_ERR_UNSUPPORTED, "x / y not 4-byte aligned");
+  if (overlaps(x, (size_t)(batch * C * L) * 2, y, (size_t)(batch * C * H) * 2))
+    return fail(h, PRNET_ERR_UNSUPPORTED, "x and y overlap");
+  DeviceGuard g(h->cfg.device);
+  prnet::FwdArgs a = make_args(h, reinterpret_cast<const float*>(x), batch,
+                               reinterpret_cast<float*>(y));
+  a.io_bf16 = 1;
+  // one 1-D bulk copy per series: 16-byte aligned bf16 window starts
+  a.x_vec = (L % 8 == 0) && (h->r % 8 == 0) && (((uintptr_t)x & 15u) == 0);
+  prnet::TcqPlan p;
+  if (!prnet::plan_tcq_kernel(a, h->max_smem_optin, h->sm_count, &p))
+    return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the tc_quad kernel");
+  cudaError_t e = prnet::launch_tcq_kernel(a, p, (cudaStream_t)cuda_stream);
+  return e == cudaSuccess ? PRNET_OK : cuda_fail(h, e, "forward_bf16 launch");
+}
+
 prnet_status prnet_backward(prnet_handle* h, const float* x, int64_t batch, const float* dy,
                             float* dx, float* dws, float* dwt, float* db, float* dtau,
                             void* cuda_stream) {

@@ -24,7 +24,7 @@ EXPORTS = ("prnet_create", "prnet_load_params", "prnet_forward", "prnet_forward_
            "prnet_set_host_chunk", "prnet_destroy", "prnet_last_error", "prnet_get_dims",
            "prnet_debug_segments", "prnet_debug_attention", "prnet_error_sums",
            "prnet_forward_plan", "prnet_set_kernel_variant", "prnet_forward_sliding",
-           "prnet_forward_sliding_host", "prnet_backward_head", "prnet_backward")
+           "prnet_forward_sliding_host", "prnet_backward_head", "prnet_backward", "prnet_forward_bf16")
 # index = the C ABI's variant id (include/prnet.h); 3 and 4 are retired round-1 prototypes
 VARIANTS = ("warp_f32", "long_f32", "mma_f16x3", "retired_tc_fold", "retired_tc_full",
             "flash_f16x3", "tc_quad", "small_f32", "tc_long")
@@ -74,6 +74,7 @@ def load_library(path: str | None = None):
         "prnet_set_kernel_variant": ([vp, ctypes.c_int32], ctypes.c_int),
         "prnet_backward_head": ([vp, vp, i64, vp, vp, vp, vp, vp], ctypes.c_int),
         "prnet_backward": ([vp, vp, i64, vp, vp, vp, vp, vp, vp, vp], ctypes.c_int),
+        "prnet_forward_bf16": ([vp, vp, i64, vp, vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -252,6 +253,17 @@ class PRNet:
             ctypes.c_void_p(dws.data_ptr()), ctypes.c_void_p(dwt.data_ptr()),
             ctypes.c_void_p(db.data_ptr()), _stream_ptr(stream)))
         return dws, dwt, db
+
+    def forward_bf16(self, x, stream=None):
+        """BF16 I/O forward: x cuda bfloat16 [B, C, L] contiguous -> y cuda bfloat16 [B, C, H]
+        (the S = 24 tc_quad kernel, include/prnet.h)."""
+        import torch
+        assert x.dtype == torch.bfloat16 and x.is_cuda and x.is_contiguous()
+        y = torch.empty((x.shape[0], self.C, self.H), dtype=torch.bfloat16, device=x.device)
+        self._check(self._lib.prnet_forward_bf16(
+            self._h, ctypes.c_void_p(x.data_ptr()), x.shape[0], ctypes.c_void_p(y.data_ptr()),
+            _stream_ptr(stream)))
+        return y
 
     def backward(self, x, dy, stream=None):
         """The full backward (reading R-f7): gradients of sum(dy * y) with

@@ -22,7 +22,7 @@ def lib():
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "prnet.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(prnet_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(prnet_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_header_declares_the_abi():
