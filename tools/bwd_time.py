@@ -18,7 +18,9 @@ s = synth.make_series(w)
 sd = torch.from_numpy(s).cuda()
 x = sd.unfold(1, w.L, 1)[:, w.t0:w.t0 + w.windows, :].permute(1, 0, 2).contiguous()
 dy = torch.randn((w.windows, w.C, w.H), device="cuda")
-m = PRNet(w.C, w.L, w.S, w.H)
+N, _, M = synth.derived_dims(w.L, w.S, w.H)
+ws, wt, b = synth.make_params(w.C, M, N, w.H, True, synth.DEFAULT_SEED, w.cfg_id)
+m = PRNet(w.C, w.L, w.S, w.H).load(ws, wt, b)
 fn = (lambda: m.backward(x, dy)) if full else (lambda: m.backward_head(x, dy))
 for _ in range(2):
     fn()
