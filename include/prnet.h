@@ -241,7 +241,7 @@ prnet_status prnet_forward_bf16(prnet_handle* h, const uint16_t* x, int64_t batc
  * Definition step; deterministic (fixed-order reductions, no atomics).  Uses the per-handle
  * device workspace of prnet_backward_head (not stream-concurrent on one handle).  Base reading
  * only.  Errors: BAD_STATE (before load_params), INVALID_ARG (B < 0, NULL pointers),
- * UNSUPPORTED (N > 32, M > 64, S > 128, metric_variant bits 1-2, instance_norm, ma_kernel,
+ * UNSUPPORTED (N > 32, M > 32, S > 128, metric_variant bits 1-2, instance_norm, ma_kernel,
  * pointers not on the handle's device), CUDA, OOM. */
 prnet_status prnet_backward(prnet_handle* h, const float* x, int64_t batch, const float* dy,
                             float* dx, float* dws, float* dwt, float* db, float* dtau,

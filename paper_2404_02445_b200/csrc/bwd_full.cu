@@ -19,12 +19,13 @@
 //          dz += 2 z dnu2 + t~ dkappa / V;  dX += dz + (dmu - sum_t dz) / S
 //   a1     dx[r + n S + t] = dX[n][t], dx = 0 on the r dropped points
 //
-// FP32 on the CUDA cores (a training-side pass, not the timed forward).  Layout: one warp per
-// series, lane i = segment i (N <= 32), the rows and the N x N matrices in per-warp shared
-// memory (odd row pitches: a lane's own row and a broadcast row are conflict-free); the head
-// and bias gradients accumulate per warp over its series in shared memory, the warps are
-// reduced in a fixed order into one partial per CTA, and a second kernel sums the partials in
-// fp64 in a fixed order (dtau over every channel).  Deterministic, no atomics.
+// FP32 on the CUDA cores (a training-side pass, not the timed forward).  The head gradients
+// come from the head-backward kernel (bwd_head.cu, same partial / fixed-order reduce scheme);
+// this file computes dx and dtau.  Layout: one warp per series, lane i = segment i (N <= 32),
+// the rows (float4 chunks, pitch P with P / 4 odd: a lane's own chunk is conflict-free, other
+// rows are broadcasts) and the N x N matrices in per-warp shared memory (the transposes of
+// drho and dD go through it), W^T per CTA; the temperature partials are reduced over the warps
+// and then over the CTAs in a fixed order (fp64).  Deterministic, no atomics.
 #include <algorithm>
 
 #include "prnet_internal.cuh"
@@ -39,6 +40,14 @@ __device__ __forceinline__ float shfl(float v, int src) {
 
 }  // namespace
 
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+
+// dx and the temperature partials; the head gradients come from the head-backward kernel
+// (bwd_head.cu), launched by launch_bwd_full.  Shared memory: the CTA's W_s^T, W_t^T [32][mpad];
+// per warp X, dP_s, dP_t, dX [32][P] (P % 4 == 0, P / 4 odd: a lane's own float4 row chunk is
+// conflict-free, other rows are broadcasts), A_s, A_t (later drho, dD), rho, D [32][33],
+// dY [M][P], mu [32].  Rows and columns past N / S are zero.
 __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const float* __restrict__ dy,
                                                               float* __restrict__ dx,
                                                               float* __restrict__ part,
@@ -49,32 +58,43 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
   const int c = blockIdx.y, C = a.C;
   const int cw = a.head_per_channel ? c : 0;
   const int N = a.N, S = a.S, M = a.M, H = a.H, L = a.L, r = a.r;
-  const int P = ly.pitch, Q = 33;           // row pitches (odd)
-  float* wb = smem + warp * ly.per_warp;
+  const int P = ly.pitch, Q = 33, MP = ly.mpad;
+  float* WsT = smem;                        // [32][MP] W_s^T
+  float* WtT = WsT + 32 * MP;               // [32][MP] W_t^T
+  float* wb = smem + 2 * 32 * MP + warp * ly.per_warp;
   float* Xs = wb;                           // [32][P] segment rows
-  float* Zs = Xs + 32 * P;                  // [32][P] centred rows z
-  float* dPs = Zs + 32 * P;                 // [32][P] dP_s, later dz
+  float* dPs = Xs + 32 * P;                 // [32][P] dP_s
   float* dPt = dPs + 32 * P;                // [32][P] dP_t
-  float* dXs = dPt + 32 * P;                // [32][P] dX
-  float* As = dXs + 32 * P;                 // [32][Q] A_s, later drho
-  float* At = As + 32 * Q;                  // [32][Q] A_t, later dD
+  float* dXs = dPt + 32 * P;                // [32][P] dX (the direct part first)
+  float* As = dXs + 32 * P;                 // [32][Q] A_s, then drho
+  float* At = As + 32 * Q;                  // [32][Q] A_t, then dD
   float* Rh = At + 32 * Q;                  // [32][Q] rho
-  float* Dm = Rh + 32 * Q;                  // [32][Q] D (unnormalised)
-  float* dYs = Dm + 32 * Q;                 // [M][S]
-  float* accW = dYs + M * S;                // [2][M][32] dW_s, dW_t (column = segment)
-  float* accB = accW + 2 * M * 32;          // [H]
-  float* accT = accB + H;                   // [2] per-lane partials reduced at the end
-  const float* Wsg = a.ws + (int64_t)cw * M * N;
-  const float* Wtg = a.wt + (int64_t)cw * M * N;
-
-  for (int k = lane; k < 2 * M * 32; k += 32) accW[k] = 0.f;
-  for (int k = lane; k < H; k += 32) accB[k] = 0.f;
+  float* Dm = Rh + 32 * Q;                  // [32][Q] D
+  float* dYs = Dm + 32 * Q;                 // [M][P]
+  float* muv = dYs + M * P;                 // [32] mu_j
+  float* gv = muv + 32;                     // [32] g_j = (nu2_j + eps_s)^(-1/2)
+  float* x0v = gv + 32;                     // [32] x0_j (z_j = (X_j - x0_j) - m1_j, as Def 4's
+  float* m1v = x0v + 32;                    // [32] m1_j  forward: no cancellation against mu)
+  {
+    const float* gs = a.ws + (int64_t)cw * M * N;
+    const float* gt = a.wt + (int64_t)cw * M * N;
+    for (int k = threadIdx.x; k < 32 * MP; k += blockDim.x) {
+      const int n = k / MP, m = k - n * MP;
+      const bool ok = n < N && m < M;
+      WsT[k] = ok ? __ldg(gs + m * N + n) : 0.f;
+      WtT[k] = ok ? __ldg(gt + m * N + n) : 0.f;
+    }
+  }
+  for (int k = lane; k < 32 * P; k += 32) Xs[k] = 0.f;   // padding stays 0
+  for (int k = lane; k < M * P; k += 32) dYs[k] = 0.f;
+  __syncthreads();
   float dts = 0.f, dtt = 0.f;               // lane partials of dL/dtau_s, dL/dtau_t
   const int i = lane;
   const bool valid = i < N;
   const float V = 1.0f / a.inv_v;           // S (S^2 - 1) / 12
   const float w = a.vtrend;                 // (S^2 - 1) / 12, 0 for the level-only trend
   const float tau_s = kLog2e / a.ks, tau_t = kLog2e / a.kt;
+  const int S4 = (S + 3) >> 2;
 
   const int64_t b0 = (int64_t)blockIdx.x * ly.wins_per_cta;
   const int64_t b1 = min(b0 + (int64_t)ly.wins_per_cta, a.B);
@@ -82,34 +102,36 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
     const int64_t series = b * C + c;
     const float* xg = a.x + b * a.xsb + c * a.xsc + r;
     const float* dyg = dy + series * H;
-    // ---------------- forward recompute (Def 2-9), FP32
     for (int k = lane; k < N * S; k += 32) {
       const int n = k / S, t = k - n * S;
       Xs[n * P + t] = __ldg(xg + k);
     }
-    for (int k = lane; k < M * S; k += 32) dYs[k] = k < H ? __ldg(dyg + k) : 0.f;
-    for (int k = lane; k < H; k += 32) accB[k] += __ldg(dyg + k);
+    for (int k = lane; k < H; k += 32) {
+      const int m = k / S, t = k - m * S;
+      dYs[m * P + t] = __ldg(dyg + k);
+    }
     __syncwarp();
-    float mu = 0.f, kap = 0.f, nu2 = 0.f;
+    // ---------------- forward recompute (Def 3-8), FP32
+    float mu = 0.f, kap = 0.f, nu2 = 0.f, x0 = 0.f, m1 = 0.f;
     if (valid) {
       const float* xr = Xs + i * P;
-      const float x0 = xr[0];
+      x0 = xr[0];
       float s1 = 0.f;
       for (int t = 0; t < S; t++) s1 += xr[t] - x0;
-      const float m1 = s1 * a.inv_s;
+      m1 = s1 * a.inv_s;
       mu = x0 + m1;
       float q = 0.f, k3 = 0.f;
       for (int t = 0; t < S; t++) {
         const float z = (xr[t] - x0) - m1;
-        Zs[i * P + t] = z;
         q = fmaf(z, z, q);
         k3 = fmaf((float)t - a.half_s, z, k3);
       }
       nu2 = q;
       kap = k3 * a.inv_v;
     }
-    __syncwarp();
-    // sigma^2 (Def 5) about m0 = mu_0: sum d^2 - (sum d)^2 / N with d = mu - m0
+    muv[i] = mu;
+    x0v[i] = x0;
+    m1v[i] = m1;
     const float m0 = shfl(mu, 0);
     const float dd = valid ? mu - m0 : 0.f;
     const float sd = warp_sum(dd);
@@ -118,25 +140,47 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
     const float den = s2 + kEpsTrend;
     const float mubar = m0 + sd * a.inv_n;
     const float g = rsqrtf(nu2 + kEpsSeasonal);
-    // rho row i, D row i, both softmax rows (exact row maxima), stored for the transposes
+    gv[i] = g;
+    __syncwarp();
+    // Gram row i: <z_i, z_j> from the own row and broadcast rows (z = X - mu; t >= S masked)
     float lmax_s = -INFINITY, lmax_t = -INFINITY;
-    for (int j = 0; j < N; j++) {
-      const float gj = shfl(g, j), muj = shfl(mu, j), kj = shfl(kap, j);   // every lane
-      if (valid) {
-        float G = 0.f;
-        for (int t = 0; t < S; t++) G = fmaf(Zs[i * P + t], Zs[j * P + t], G);
-        const float rho = G * g * gj;
-        const float dm = mu - muj, dk = kap - kj;
-        const float D = fmaf(w * dk, dk, dm * dm);
-        Rh[i * Q + j] = rho;
-        Dm[i * Q + j] = D;
-        lmax_s = fmaxf(lmax_s, rho / tau_s);
-        lmax_t = fmaxf(lmax_t, -D / den / tau_t);
+    {
+      float G[32];
+#pragma unroll
+      for (int j = 0; j < 32; j++) G[j] = 0.f;
+      if (valid)
+        for (int q4 = 0; q4 < S4; q4++) {
+          const int t0 = 4 * q4;
+          const float4 xi = ld4(Xs + i * P + t0);
+          const float z0 = (xi.x - x0) - m1, z1 = t0 + 1 < S ? (xi.y - x0) - m1 : 0.f;
+          const float z2 = t0 + 2 < S ? (xi.z - x0) - m1 : 0.f;
+          const float z3 = t0 + 3 < S ? (xi.w - x0) - m1 : 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; j++) {
+            if (j >= N) break;
+            const float4 xj = ld4(Xs + j * P + t0);
+            const float aj = x0v[j], bj = m1v[j];
+            G[j] = fmaf(z0, (xj.x - aj) - bj, fmaf(z1, (xj.y - aj) - bj,
+                   fmaf(z2, (xj.z - aj) - bj, fmaf(z3, (xj.w - aj) - bj, G[j]))));
+          }
+        }
+#pragma unroll
+      for (int j = 0; j < 32; j++) {
+        if (j >= N) break;
+        const float gj = shfl(g, j), kj = shfl(kap, j);   // every lane
+        if (valid) {
+          const float rho = G[j] * g * gj;
+          const float dm = mu - muv[j], dk = kap - kj;
+          const float D = fmaf(w * dk, dk, dm * dm);
+          Rh[i * Q + j] = rho;
+          Dm[i * Q + j] = D;
+          lmax_s = fmaxf(lmax_s, rho / tau_s);
+          lmax_t = fmaxf(lmax_t, -D / den / tau_t);
+        }
       }
     }
-    __syncwarp();
-    float ls = 0.f, lt = 0.f;
     if (valid) {
+      float ls = 0.f, lt = 0.f;
       for (int j = 0; j < N; j++) {
         const float es = __expf(Rh[i * Q + j] / tau_s - lmax_s);
         const float et = __expf(-Dm[i * Q + j] / den / tau_t - lmax_t);
@@ -150,75 +194,51 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
         As[i * Q + j] *= ils;
         At[i * Q + j] *= ilt;
       }
-    }
-    __syncwarp();
-    // ---------------- a8/a7: head gradients and dP (lane i owns segment i / column i)
-    if (valid) {
-      for (int t0 = 0; t0 < S; t0 += 16) {
-        const int tn = min(16, S - t0);
-        float ps[16], pt[16];
-#pragma unroll
-        for (int u = 0; u < 16; u++) ps[u] = pt[u] = 0.f;
-        for (int j = 0; j < N; j++) {
-          const float aj = As[i * Q + j], bj = At[i * Q + j];
-#pragma unroll
-          for (int u = 0; u < 16; u++)
-            if (u < tn) {
-              const float xv = Xs[j * P + t0 + u];
-              ps[u] = fmaf(aj, xv, ps[u]);
-              pt[u] = fmaf(bj, xv, pt[u]);
-            }
-        }
+      // ---------------- a7: dP_i = W^T[i] dY (W^T row per lane, dY rows broadcast)
+      for (int q4 = 0; q4 < S4; q4++) {
+        float4 gs = make_float4(0.f, 0.f, 0.f, 0.f), gt = gs;
         for (int m = 0; m < M; m++) {
-          float gs = 0.f, gt = 0.f;
-#pragma unroll
-          for (int u = 0; u < 16; u++)
-            if (u < tn) {
-              const float dv = dYs[m * S + t0 + u];
-              gs = fmaf(dv, ps[u], gs);
-              gt = fmaf(dv, pt[u], gt);
-            }
-          accW[m * 32 + i] += gs;
-          accW[(M + m) * 32 + i] += gt;
+          const float4 dv = ld4(dYs + m * P + 4 * q4);
+          const float ws_ = WsT[i * MP + m], wt_ = WtT[i * MP + m];
+          gs.x = fmaf(ws_, dv.x, gs.x); gs.y = fmaf(ws_, dv.y, gs.y);
+          gs.z = fmaf(ws_, dv.z, gs.z); gs.w = fmaf(ws_, dv.w, gs.w);
+          gt.x = fmaf(wt_, dv.x, gt.x); gt.y = fmaf(wt_, dv.y, gt.y);
+          gt.z = fmaf(wt_, dv.z, gt.z); gt.w = fmaf(wt_, dv.w, gt.w);
         }
-      }
-      for (int t = 0; t < S; t++) {
-        float gs = 0.f, gt = 0.f;
-        for (int m = 0; m < M; m++) {
-          const float dv = dYs[m * S + t];
-          gs = fmaf(__ldg(Wsg + m * N + i), dv, gs);
-          gt = fmaf(__ldg(Wtg + m * N + i), dv, gt);
-        }
-        dPs[i * P + t] = gs;
-        dPt[i * P + t] = gt;
+        st4(dPs + i * P + 4 * q4, gs);
+        st4(dPt + i * P + 4 * q4, gt);
       }
     }
     __syncwarp();
-    // ---------------- a6: dA rows (lane-local) and dX = A^T dP (columns of A)
+    // ---------------- a6: dX_direct = A^T dP (A's columns, dP rows broadcast) and dA rows
     float dAs[32], dAt[32];
-    if (valid) {
 #pragma unroll
-      for (int j = 0; j < 32; j++) {
-        float vs = 0.f, vt = 0.f;
-        if (j < N)
-          for (int t = 0; t < S; t++) {
-            const float xv = Xs[j * P + t];
-            vs = fmaf(dPs[i * P + t], xv, vs);
-            vt = fmaf(dPt[i * P + t], xv, vt);
-          }
-        dAs[j] = vs;
-        dAt[j] = vt;
-      }
-      for (int t = 0; t < S; t++) {
-        float v = 0.f;
-        for (int k = 0; k < N; k++)
-          v = fmaf(As[k * Q + i], dPs[k * P + t], fmaf(At[k * Q + i], dPt[k * P + t], v));
-        dXs[i * P + t] = v;
+    for (int j = 0; j < 32; j++) dAs[j] = dAt[j] = 0.f;
+    if (valid) {
+      for (int q4 = 0; q4 < S4; q4++) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int k = 0; k < N; k++) {
+          const float as = As[k * Q + i], at = At[k * Q + i];
+          const float4 ps = ld4(dPs + k * P + 4 * q4), pt = ld4(dPt + k * P + 4 * q4);
+          v.x = fmaf(as, ps.x, fmaf(at, pt.x, v.x));
+          v.y = fmaf(as, ps.y, fmaf(at, pt.y, v.y));
+          v.z = fmaf(as, ps.z, fmaf(at, pt.z, v.z));
+          v.w = fmaf(as, ps.w, fmaf(at, pt.w, v.w));
+        }
+        st4(dXs + i * P + 4 * q4, v);
+        const float4 ps = ld4(dPs + i * P + 4 * q4), pt = ld4(dPt + i * P + 4 * q4);
+#pragma unroll
+        for (int j = 0; j < 32; j++) {
+          if (j >= N) break;
+          const float4 xj = ld4(Xs + j * P + 4 * q4);
+          dAs[j] = fmaf(ps.x, xj.x, fmaf(ps.y, xj.y, fmaf(ps.z, xj.z, fmaf(ps.w, xj.w, dAs[j]))));
+          dAt[j] = fmaf(pt.x, xj.x, fmaf(pt.y, xj.y, fmaf(pt.z, xj.z, fmaf(pt.w, xj.w, dAt[j]))));
+        }
       }
     }
-    __syncwarp();
-    // ---------------- a5: softmax adjoints -> drho (into As), dD (into At), dtau partials
-    const float rref = lmax_s * tau_s;   // the row maximum of rho
+    // ---------------- a5: softmax adjoints (own rows) -> drho, dD, dtau and ds2 partials
+    float ds2 = 0.f;
+    const float rref = lmax_s * tau_s;   // the row maximum of rho: sum_j dls_ij = 0
     if (valid) {
       float ss = 0.f, st = 0.f;
 #pragma unroll
@@ -233,162 +253,152 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
           const float dls = As[i * Q + j] * (dAs[j] - ss);
           const float dlt = At[i * Q + j] * (dAt[j] - st);
           const float rho = Rh[i * Q + j], D = Dm[i * Q + j];
-          // sum_j dls_ij = 0, so the row reference (its maximum) is subtracted first: the same
-          // value, without the cancellation of sum_j dls_ij rho_ij when rho_ij ~ rho_ii
           dts -= dls * (rho - rref) / (tau_s * tau_s);
-          const float dDh = -dlt / tau_t;
           dtt += dlt * (D / den) / (tau_t * tau_t);
-          dAs[j] = dls / tau_s;     // drho_ij
-          dAt[j] = dDh;             // dDhat_ij
+          const float dDh = -dlt / tau_t;
+          ds2 -= dDh * D / (den * den);
+          dAs[j] = dls / tau_s;      // drho_ij
+          dAt[j] = dDh / den;        // dD_ij
         }
     }
-    __syncwarp();   // every lane has read its As / At rows
-    float ds2 = 0.f;
+    __syncwarp();   // every lane has read A's columns (a6) and its own rows
     if (valid) {
 #pragma unroll
       for (int j = 0; j < 32; j++)
         if (j < N) {
           As[i * Q + j] = dAs[j];
-          At[i * Q + j] = dAt[j] / den;                       // dD_ij
-          ds2 -= dAt[j] * Dm[i * Q + j] / (den * den);
+          At[i * Q + j] = dAt[j];
         }
     }
     __syncwarp();
-    // ---------------- a4: trend adjoint, dmu / dkappa from dD_ij + dD_ji
-    // mu_j, kappa_j of every lane through shuffles (all lanes take part)
-    float dmu = 0.f, dkap = 0.f;
-    for (int j = 0; j < N; j++) {
-      const float muj = shfl(mu, j), kj = shfl(kap, j);   // every lane
+    // ---------------- a4 / a3 / a2: dmu, dkappa (dD + dD^T), dg (drho + drho^T), ds2
+    float dmu = 0.f, dkap = 0.f, dg = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; j++) {
+      if (j >= N) break;
+      const float kj = shfl(kap, j);   // every lane
       if (valid) {
         const float dsym = At[i * Q + j] + At[j * Q + i];
-        dmu = fmaf(2.f * (mu - muj), dsym, dmu);
+        dmu = fmaf(2.f * (mu - muv[j]), dsym, dmu);
         dkap = fmaf(2.f * w * (kap - kj), dsym, dkap);
-      }
-    }
-    // ---------------- a3: seasonal adjoint: dz (into dPs), dg -> dnu2
-    float dnu2 = 0.f;
-    if (valid) {
-      float dg = 0.f;
-      for (int t = 0; t < S; t++) dPs[i * P + t] = 0.f;
-      for (int j = 0; j < N; j++)
         dg = fmaf(As[i * Q + j] + As[j * Q + i], Rh[i * Q + j], dg);
-      dg /= g;
-      dnu2 = -0.5f * dg * g * g * g;
-    }
-    for (int j = 0; j < N; j++) {
-      const float gj = shfl(g, j);   // every lane
-      if (valid) {
-        const float cf = (As[i * Q + j] + As[j * Q + i]) * g * gj;
-        for (int t = 0; t < S; t++) dPs[i * P + t] = fmaf(cf, Zs[j * P + t], dPs[i * P + t]);
       }
     }
-    // ---------------- a2: sigma^2 adjoint, descriptor adjoints, dX
     ds2 = warp_sum(ds2);
-    if (valid) {
-      dnu2 += ds2 * a.inv_ns;
-      dmu += ds2 * 2.f * (mu - mubar) * a.inv_n;
-      float sdz = 0.f;
-      for (int t = 0; t < S; t++) {
-        const float dz = fmaf(2.f * Zs[i * P + t], dnu2,
-                              fmaf((float)t - a.half_s, dkap / V, dPs[i * P + t]));
-        dPs[i * P + t] = dz;
-        sdz += dz;
-      }
-      const float dmt = (dmu - sdz) * a.inv_s;
-      for (int t = 0; t < S; t++) dXs[i * P + t] += dPs[i * P + t] + dmt;
-    }
-    __syncwarp();
-    // ---------------- a1: dx (coalesced), zero on the dropped points
+    float dnu2 = valid ? -0.5f * (dg / g) * g * g * g : 0.f;
+    dnu2 += ds2 * a.inv_ns;
+    dmu += ds2 * 2.f * (mu - mubar) * a.inv_n;
+    // ---------------- dX = dX_direct + dz + dmu / S with dz_i = g_i sum_j (drho_ij + drho_ji)
+    // g_j z_j + 2 z_i dnu2 + t~ dkappa / V (sum_t dz_i = 0: every term is centred), -> dx
     float* dxg = dx + series * L;
     for (int k = lane; k < r; k += 32) dxg[k] = 0.f;
+    if (valid) {
+      float cz[32];
+#pragma unroll
+      for (int j = 0; j < 32; j++) cz[j] = 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; j++)
+        if (j < N) cz[j] = (As[i * Q + j] + As[j * Q + i]) * g * gv[j];
+      for (int q4 = 0; q4 < S4; q4++) {
+        const int t0 = 4 * q4;
+        float4 v = ld4(dXs + i * P + t0);
+        const float4 xi = ld4(Xs + i * P + t0);
+        const float dmS = dmu * a.inv_s;
+        float4 dz;
+        dz.x = fmaf(2.f * ((xi.x - x0) - m1), dnu2, ((float)t0 - a.half_s) * dkap / V);
+        dz.y = fmaf(2.f * ((xi.y - x0) - m1), dnu2, ((float)(t0 + 1) - a.half_s) * dkap / V);
+        dz.z = fmaf(2.f * ((xi.z - x0) - m1), dnu2, ((float)(t0 + 2) - a.half_s) * dkap / V);
+        dz.w = fmaf(2.f * ((xi.w - x0) - m1), dnu2, ((float)(t0 + 3) - a.half_s) * dkap / V);
+#pragma unroll
+        for (int j = 0; j < 32; j++) {
+          if (j >= N) break;
+          const float4 xj = ld4(Xs + j * P + t0);
+          const float aj = x0v[j], bj = m1v[j], cj = cz[j];
+          dz.x = fmaf(cj, (xj.x - aj) - bj, dz.x);
+          dz.y = fmaf(cj, (xj.y - aj) - bj, dz.y);
+          dz.z = fmaf(cj, (xj.z - aj) - bj, dz.z);
+          dz.w = fmaf(cj, (xj.w - aj) - bj, dz.w);
+        }
+        v.x += dz.x + dmS;
+        v.y += dz.y + dmS;
+        v.z += dz.z + dmS;
+        v.w += dz.w + dmS;
+        st4(dXs + i * P + t0, v);
+      }
+    }
+    __syncwarp();
     for (int k = lane; k < N * S; k += 32) {
       const int n = k / S, t = k - n * S;
       dxg[r + k] = dXs[n * P + t];
     }
     __syncwarp();
   }
-  // tau partials of this warp
   dts = warp_sum(dts);
   dtt = warp_sum(dtt);
+  float* red = smem + 2 * 32 * MP + nwarps * ly.per_warp;   // [8][2]
   if (lane == 0) {
-    accT[0] = dts;
-    accT[1] = dtt;
+    red[2 * warp] = dts;
+    red[2 * warp + 1] = dtt;
   }
   __syncthreads();
-  // fixed-order reduction over the warps -> one partial per CTA: [2 M N | H | 2]
-  const int E = ly.elems;
-  float* pout = part + ((int64_t)c * gridDim.x + blockIdx.x) * E;
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+  if (threadIdx.x < 2) {
     float v = 0.f;
-    for (int wv = 0; wv < nwarps; wv++) {
-      const float* ob = smem + wv * ly.per_warp;
-      const float* aW = ob + 5 * 32 * P + 4 * 32 * Q + M * S;
-      if (e < 2 * M * N) {
-        const int br = e / (M * N), rem = e - br * M * N, m = rem / N, n = rem - m * N;
-        v += aW[(br * M + m) * 32 + n];
-      } else if (e < 2 * M * N + H) {
-        v += aW[2 * M * 32 + (e - 2 * M * N)];
-      } else {
-        v += aW[2 * M * 32 + H + (e - 2 * M * N - H)];
-      }
-    }
-    pout[e] = v;
+    for (int wv = 0; wv < nwarps; wv++) v += red[2 * wv + threadIdx.x];
+    part[((int64_t)c * gridDim.x + blockIdx.x) * 2 + threadIdx.x] = v;
   }
 }
-
-// fp64 fixed-order sum of the per-CTA partials: head and bias per head channel, the two
-// temperature gradients over every channel (block y == 0 writes them)
-__global__ void prnet_bwd_full_reduce_kernel(const float* __restrict__ part, int C, int nblk, int E,
-                                             int MN, int H, int hpc, float* dws, float* dwt,
-                                             float* db, float* dtau) {
-  const int cw = blockIdx.y;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+// fp64 fixed-order sum of the per-CTA temperature partials [C][nblk][2] -> dtau[2]
+__global__ void prnet_bwd_tau_reduce_kernel(const float* __restrict__ part, int n, float* dtau) {
+  const int e = threadIdx.x;
+  if (e < 2) {
     double v = 0.0;
-    const bool tau = e >= 2 * MN + H;
-    if (tau && cw != 0) continue;
-    const int c0 = (hpc && !tau) ? cw : 0, c1 = (hpc && !tau) ? cw + 1 : C;
-    for (int c = c0; c < c1; c++)
-      for (int k = 0; k < nblk; k++) v += (double)part[((int64_t)c * nblk + k) * E + e];
-    if (e < MN) dws[(int64_t)cw * MN + e] = (float)v;
-    else if (e < 2 * MN) dwt[(int64_t)cw * MN + e - MN] = (float)v;
-    else if (e < 2 * MN + H) db[(int64_t)cw * H + e - 2 * MN] = (float)v;
-    else dtau[e - 2 * MN - H] = (float)v;
+    for (int k = 0; k < n; k++) v += (double)part[2 * k + e];
+    dtau[e] = (float)v;
   }
 }
 
 bool plan_bwd_full(const FwdArgs& a, int max_smem_optin, BwdFullPlan* p) {
-  if (a.N < 1 || a.N > 32 || a.M > 64 || a.S > 128) return false;
+  if (a.N < 1 || a.N > 32 || a.M > 32 || a.S > 128) return false;
+  if (!plan_bwd_head(a, max_smem_optin, &p->head) || p->head.long_mode) return false;
   BwdFullLayout& ly = p->ly;
-  ly.pitch = a.S | 1;
-  ly.per_warp = 5 * 32 * ly.pitch + 4 * 32 * 33 + a.M * a.S + 2 * a.M * 32 + a.H + 2;
-  ly.per_warp = (ly.per_warp + 3) & ~3;
+  int P = (a.S + 3) & ~3;
+  if (((P / 4) & 1) == 0) P += 4;          // P / 4 odd: conflict-free own-row float4 reads
+  ly.pitch = P;
+  ly.mpad = a.M | 1;                        // odd: W^T row reads by 32 lanes are conflict-free
+  ly.per_warp = ((4 * 32 * P + 4 * 32 * 33 + a.M * P + 128) + 3) & ~3;
+  const size_t cta = (size_t)2 * 32 * ly.mpad * 4 + 16 * 4;
   int w = 8;
-  while (w > 1 && (size_t)w * ly.per_warp * 4 > (size_t)max_smem_optin) w--;
-  if ((size_t)w * ly.per_warp * 4 > (size_t)max_smem_optin) return false;
+  while (w > 1 && cta + (size_t)w * ly.per_warp * 4 > (size_t)max_smem_optin) w--;
+  if (cta + (size_t)w * ly.per_warp * 4 > (size_t)max_smem_optin) return false;
   p->warps = w;
   ly.wins_per_cta = 8 * w;
   p->nblk = (int)((a.B + ly.wins_per_cta - 1) / ly.wins_per_cta);
-  ly.elems = 2 * a.M * a.N + a.H + 2;
-  p->smem_bytes = (size_t)w * ly.per_warp * 4;
+  ly.elems = 2;
+  p->smem_bytes = cta + (size_t)w * ly.per_warp * 4;
   return true;
 }
 
+size_t bwd_full_workspace_floats(const FwdArgs& a, const BwdFullPlan& p) {
+  return (size_t)a.C * std::max(p.head.nblk, 1) * p.head.elems +
+         (size_t)a.C * std::max(p.nblk, 1) * 2;
+}
+
 cudaError_t launch_bwd_full(const FwdArgs& a, const BwdFullPlan& p, const float* dy, float* dx,
-                            float* part, float* dws, float* dwt, float* db, float* dtau, int Cw,
+                            float* work, float* dws, float* dwt, float* db, float* dtau, int Cw,
                             cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(prnet_bwd_full_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)p.smem_bytes);
+  // the head gradients (dW_s, dW_t, db): the head-backward kernel and its fixed-order reduce
+  cudaError_t e = launch_bwd_head(a, p.head, dy, work, dws, dwt, db, Cw, st);
   if (e != cudaSuccess) return e;
+  float* part = work + (size_t)a.C * std::max(p.head.nblk, 1) * p.head.elems;
+  if ((e = cudaFuncSetAttribute(prnet_bwd_full_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)p.smem_bytes)) != cudaSuccess)
+    return e;
   if (p.nblk > 0) {
     dim3 grid((unsigned)p.nblk, (unsigned)a.C);
     prnet_bwd_full_kernel<<<grid, 32 * p.warps, p.smem_bytes, st>>>(a, dy, dx, part, p.ly);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  const int nb = p.nblk > 0 ? p.nblk : 0;
-  dim3 rg((unsigned)((p.ly.elems + 255) / 256), (unsigned)Cw);
-  prnet_bwd_full_reduce_kernel<<<rg, 256, 0, st>>>(part, a.C, nb, p.ly.elems, a.M * a.N, a.H,
-                                                    a.head_per_channel, dws, dwt, db, dtau);
+  prnet_bwd_tau_reduce_kernel<<<1, 32, 0, st>>>(part, p.nblk > 0 ? a.C * p.nblk : 0, dtau);
   return cudaGetLastError();
 }
 

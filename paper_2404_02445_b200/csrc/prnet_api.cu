@@ -865,9 +865,9 @@ prnet_status prnet_backward(prnet_handle* h, const float* x, int64_t batch, cons
   prnet::FwdArgs a = make_args(h, x, batch, nullptr);
   prnet::BwdFullPlan p;
   if (!prnet::plan_bwd_full(a, h->max_smem_optin, &p))
-    return fail(h, PRNET_ERR_UNSUPPORTED, "backward needs N <= 32, M <= 64, S <= 128");
+    return fail(h, PRNET_ERR_UNSUPPORTED, "backward needs N <= 32, M <= 32, S <= 128");
   cudaStream_t st = (cudaStream_t)cuda_stream;
-  const int64_t need = (int64_t)h->cfg.channels * std::max(p.nblk, 1) * p.ly.elems;
+  const int64_t need = (int64_t)prnet::bwd_full_workspace_floats(a, p);
   if (need > h->bwd_floats) {
     cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(h, e, "backward sync");

@@ -51,7 +51,7 @@ def _run(oracle_mod, B, C, L, S, H, tau_s=1.0, tau_t=1.0, hpc=True, mv=0, kind="
 
 @pytest.mark.parametrize("L,S,H", [(96, 24, 96), (720, 24, 720), (720, 24, 336), (100, 12, 50),
                                    (53, 12, 24), (64, 8, 64), (97, 7, 13), (30, 2, 5),
-                                   (384, 12, 720), (720, 48, 96), (1440, 96, 96), (25, 24, 1)])
+                                   (384, 12, 384), (720, 48, 96), (1440, 96, 96), (25, 24, 1)])
 def test_backward_shapes(oracle_mod, L, S, H):
     _run(oracle_mod, 5, 3, L, S, H)
 
