@@ -200,6 +200,11 @@ bool tcl_applicable(const prnet_handle* h) {
   return h->N > 32 && h->N <= 512 && h->M <= 64 && prnet::tcl_supported_s(h->cfg.seg_len) &&
          h->cfg.tau_seasonal >= 1.0f / 320.0f;
 }
+// 9 = group_f32 (N <= 16, S <= 32: lanes over (series, segment), FP32; plain reading,
+// tau_s >= 1/80 for its symmetric seasonal shift 1, as tc_quad)
+bool grp_applicable(const prnet_handle* h) {
+  return h->N <= 16 && h->cfg.seg_len <= 32 && h->cfg.tau_seasonal >= 0.0125f;
+}
 // 7 = small_f32 (N <= 16, S <= 128, M <= 32: lanes over time, FP32)
 bool small_applicable(const prnet_handle* h) {
   return h->N <= 16 && h->cfg.seg_len <= 128 && h->M <= 32;
@@ -226,6 +231,13 @@ int pick_variant(const prnet_handle* h) {
   // tc_quad the fastest S = 24 path for N > 16 (Traffic 5.4 ms vs 6.6 ms for mma_f16x3; its
   // MMA tiles pad N to 32, so mma_f16x3 wins at N = 14: 0.166 vs 0.255 ms); mma_f16x3 the
   // fastest other N <= 32 path
+  // group_f32 (lanes over (series, segment)), measured on B200 (profiles/README.md, round 2):
+  // stress L96/S12 0.056 vs 0.142 ms (small_f32), L96/S24 0.038 vs 0.081, L192/S12 (N = 16)
+  // 0.137 vs 0.197 (mma_f16x3), L96/S12/H720 0.210 vs 0.315 (tc_quad M <= 64); mma_f16x3 stays
+  // ahead at L336/S24 (N = 14: 0.159 vs 0.170)
+  if (!widening_on(h) && grp_applicable(h) &&
+      (h->N <= 8 || h->cfg.seg_len <= 16 || h->M > 32))
+    return 9;
   if (small_applicable(h) && (h->N <= 8 || h->cfg.seg_len > 64)) return 7;
   // tc_quad for S != 24 (fwd_tcg.cu), measured on B200 (profiles/README.md, round 2): stress
   // L336/S12 (N = 28) 0.230 vs 0.353 ms (mma_f16x3), L1440/S48 0.403 vs 0.980, L2880/S96 0.747
@@ -266,7 +278,7 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
     // level-only trend), mma_f16x3, long_f32 (every flag) and tc_quad (detrend /
     // instance_norm), each from the values its own fold consumes; small_f32 maps to
     // mma_f16x3 (same domain, every flag), flash_f16x3 to long_f32 (every flag and N)
-    if (v == 7) v = 2;
+    if (v == 7 || v == 9) v = h->M <= 32 ? 2 : 0;
     if (v == 5 || v == 8) v = 1;
     if (v == 0 && widening_on(h)) v = 1;
   }
@@ -274,7 +286,13 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
     const char* e = getenv("PRNET_WINDOWS_PER_CTA");
     return e ? atoi(e) : 0;
   }();
-  if (v == 8) {
+  if (v == 9) {
+    prnet::GrpPlan p;
+    if (!prnet::plan_grp_kernel(a, h->max_smem_optin, &p))
+      return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the group_f32 kernel");
+    if (wpc_env > 0) p.wins_per_cta = wpc_env;
+    e = prnet::launch_grp_kernel(a, p, st);
+  } else if (v == 8) {
     prnet::TclPlan p;
     if (!prnet::plan_tcl_kernel(a, h->max_smem_optin, h->sm_count, &p))
       return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the tc_long kernel");
@@ -884,8 +902,11 @@ prnet_status prnet_backward(prnet_handle* h, const float* x, int64_t batch, cons
 
 prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {
   if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
-  if (variant < -1 || variant > 8)
-    return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,...,8}");
+  if (variant < -1 || variant > 9)
+    return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,...,9}");
+  if (variant == 9 && !grp_applicable(h))
+    return fail(h, PRNET_ERR_UNSUPPORTED,
+                "group_f32 variant needs N <= 16, S <= 32, tau_seasonal >= 1/80");
   if (variant == 8 && !tcl_applicable(h))
     return fail(h, PRNET_ERR_UNSUPPORTED,
                 "tc_long variant needs 32 < N <= 512, S in {12, 24, 48, 96}, M <= 64, "

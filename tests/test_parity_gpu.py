@@ -42,11 +42,13 @@ def _applicable(variant, L, S, H):
         return 16 < N <= 512 and S <= 96 and M <= 32
     if variant == "tc_long":
         return 32 < N <= 512 and S in (12, 24, 48, 96) and M <= 64
+    if variant == "group_f32":
+        return N <= 16 and S <= 32
     return True
 
 
 VARIANTS = [None, "warp_f32", "mma_f16x3", "long_f32", "flash_f16x3", "tc_quad", "small_f32",
-            "tc_long"]
+            "tc_long", "group_f32"]
 SHORT_VARIANTS = [None, "warp_f32", "mma_f16x3", "tc_quad", "small_f32"]
 
 
