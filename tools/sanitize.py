@@ -22,6 +22,13 @@ CASES = [  # (L, S, H, variants)
     (1440, 96, 96, ["small_f32", "mma_f16x3"]),
     (3840, 96, 96, ["flash_f16x3"]),
     (1290, 64, 400, ["flash_f16x3"]),
+    # round 2: tc_quad generic S (incl. M > 32), tc_long, group_f32
+    (336, 12, 96, ["tc_quad"]), (389, 12, 720, ["tc_quad"]), (1443, 48, 97, ["tc_quad"]),
+    (2880, 96, 96, ["tc_quad"]), (403, 16, 200, ["tc_quad"]),
+    (720, 12, 96, ["tc_long"]), (1540, 12, 720, ["tc_long"]), (2880, 48, 97, ["tc_long"]),
+    (5760, 96, 96, ["tc_long"]), (1441, 24, 200, ["tc_long"]),
+    (96, 12, 96, ["group_f32"]), (99, 12, 720, ["group_f32"]), (30, 2, 5, ["group_f32"]),
+    (192, 12, 50, ["group_f32"]),
 ]
 for L, S, H, variants in CASES:
     x = torch.from_numpy(synth.random_windows(5, 3, L)).cuda()
@@ -76,4 +83,22 @@ for L, S, H, mv, rev, hpc in [(720, 24, 336, 0, False, True), (97, 7, 13, 3, Tru
     torch.cuda.synchronize()
     assert all(torch.isfinite(t).all() for t in g), (L, S, H)
     print("ok backward", L, S, H, mv, rev, hpc, flush=True)
+# full backward and BF16 I/O (round 2)
+for L, S, H, hpc in [(720, 24, 336, True), (97, 7, 13, False), (30, 2, 5, True)]:
+    x = torch.from_numpy(synth.random_windows(20, 3, L)).cuda()
+    dy = torch.randn((20, 3, H), device="cuda")
+    N, _, M = synth.derived_dims(L, S, H)
+    ws, wt, b = synth.make_params(3, M, N, H, hpc)
+    g = PRNet(3, L, S, H, head_per_channel=hpc).load(ws, wt, b).backward(x, dy)
+    torch.cuda.synchronize()
+    assert all(torch.isfinite(t).all() for t in g.values()), (L, S, H)
+    print("ok full backward", L, S, H, hpc, flush=True)
+for L, H in [(720, 720), (100, 90)]:
+    x = torch.from_numpy(synth.random_windows(9, 3, L)).to(torch.bfloat16).cuda()
+    N, _, M = synth.derived_dims(L, 24, H)
+    ws, wt, b = synth.make_params(3, M, N, H)
+    y = PRNet(3, L, 24, H).load(ws, wt, b).forward_bf16(x)
+    torch.cuda.synchronize()
+    assert torch.isfinite(y.float()).all(), (L, H)
+    print("ok bf16", L, H, flush=True)
 print("sanitize cases done")
