@@ -250,25 +250,36 @@ prnet_status prnet_backward(prnet_handle* h, const float* x, int64_t batch, cons
 /* Select the forward kernel (tuning / cross-checking; default -1 = automatic).
  * All variants compute the same reading to within the documented tolerance:
  *   0 = warp_f32     one warp per series, CUDA-core FP32                  (N <= 32)
+ *                    [auto: fallback, e.g. S > 128 or tau_seasonal < 1/320]
  *   1 = long_f32     one CTA per series, rows streamed, FP32              (N <= 512)
- *                    [auto: N > 32 when flash_f16x3 does not apply]
+ *                    [auto: N > 32 when neither 5 nor 8 applies]
  *   2 = mma_f16x3    one warp per series, mma.sync m16n8k16 with split-fp16
  *                    hi/lo operands, 3 products, fp32 accumulation
- *                    (N <= 32, M <= 32, S <= 128)  [auto: N <= 32 unless 6, 7 apply]
+ *                    (N <= 32, M <= 32, S <= 128)  [auto: N <= 32 unless 6, 7, 9 apply]
  *   3, 4             retired (round-1 tcgen05 prototypes, superseded by 6):
  *                    PRNET_ERR_INVALID_ARG
  *   5 = flash_f16x3  one CTA per series, 16-key tiles streamed, mma.sync
- *                    split-fp16 (16 < N <= 512, S <= 96, M <= 32)  [auto: N > 32]
+ *                    split-fp16 (16 < N <= 512, S <= 96, M <= 32)  [auto: N > 32 unless 8]
  *   6 = tc_quad      groups of 4 warps take quads of 4 series; Gram of the
  *                    row-normalised segments and the fold on tcgen05 / TMEM,
  *                    head on per-warp mma.sync (split fp16), lane-per-row
- *                    softmaxes (S = 24, N <= 32, M <= 32, tau_seasonal >= 1/80)
- *                    [auto: N > 16]
- * Variants 2, 5, 7 need tau_seasonal >= 1/320 (known-maximum softmax shift); below the
- * floors the automatic choice is 0 (N <= 32, no widening) or 1.
+ *                    softmaxes (S in {12, 16, 24, 32, 48, 64, 96}, N <= 32,
+ *                    M <= 32 for S = 24 else M <= 64, tau_seasonal >= 1/80)
+ *                    [auto: N > 16; S = 48 with N > 8; M > 32]
  *   7 = small_f32    one warp per series with lanes over TIME, FP32, warp
  *                    butterfly reductions (N <= 16, S <= 128, M <= 32)
- *                    [auto: N <= 8, or S > 64]
+ *                    [auto: N <= 8 or S > 64 where 9 does not apply]
+ *   8 = tc_long      one CTA (16 softmax warps + 1 MMA warp) per series; 128-row query
+ *                    x 64-key tiles: Gram and P = E X' on tcgen05 / TMEM, exponentials
+ *                    in TMEM, head on mma.sync (32 < N <= 512, S in {12, 24, 48, 96},
+ *                    M <= 64, tau_seasonal >= 1/320)
+ *                    [auto: S = 96, S = 48 with N >= 100, or M > 32]
+ *   9 = group_f32    lanes over (series, segment), 32 / NP series per warp, FP32
+ *                    (N <= 16, S <= 32, tau_seasonal >= 1/80)
+ *                    [auto: N <= 8, S <= 16 or M > 32]
+ * Variants 2, 5, 7, 8 need tau_seasonal >= 1/320 (known-maximum softmax shift); 6 and 9
+ * tau_seasonal >= 1/80 (the symmetric shift 1); below the floors the automatic choice is 0
+ * (N <= 32, no widening) or 1.
  * Returns PRNET_ERR_UNSUPPORTED when the variant does not cover the handle's shape. */
 prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant);
 
