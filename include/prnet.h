@@ -31,15 +31,17 @@
  *    last-error text is kept per handle under a lock and returned as a
  *    per-thread copy.  Stream concurrency: prnet_forward, prnet_forward_sliding
  *    and prnet_debug_* keep no per-call device state and may run concurrently
- *    on different streams with one handle.  prnet_error_sums and
- *    prnet_backward_head write a per-handle device scratch buffer, and
+ *    on different streams with one handle (so may prnet_forward_bf16).
+ *    prnet_error_sums, prnet_backward_head and prnet_backward write a per-handle
+ *    device scratch buffer, and
  *    prnet_forward_host / prnet_forward_sliding_host use the handle's staging
  *    ring: calls of these on one handle must not overlap (serialise them, or
  *    use one handle per stream).
  *  - Temperatures: every tau > 0 is accepted.  The automatic kernel choice
  *    keeps each kernel inside its numerical domain: kernels that shift the
- *    seasonal logits by a known row bound need tau_seasonal >= 1/320 (tc_quad:
- *    >= 1/80); below that the row-maximum-searching FP32 kernels run
+ *    seasonal logits by a known row bound need tau_seasonal >= 1/320 (tc_quad and
+ *    group_f32, which shift by 1: >= 1/80); below that the row-maximum-searching FP32
+ *    kernels run
  *    (warp_f32, long_f32).  A forced variant outside its domain is rejected
  *    with PRNET_ERR_UNSUPPORTED (prnet_set_kernel_variant).
  */
