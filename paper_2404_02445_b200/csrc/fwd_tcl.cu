@@ -48,24 +48,35 @@ using namespace tcq;
 
 namespace {
 
-template <int S>
+// NWS = softmax warps: 16 (one CTA per SM, 512 TMEM columns: two E buffers and, when they fit,
+// two G buffers) or 8 (two CTAs per SM, 256 columns each: one G, one E buffer, S <= 24; every
+// softmax thread then covers 32 of a tile's 64 keys)
+template <int S, int NWS = 16>
 struct TclCfg {
   static_assert(S % 4 == 0 && S <= 96, "S");
+  static_assert(NWS == 16 || NWS == 8, "NWS");
   static constexpr int SP = (S + 15) / 16 * 16;   // Gram K per product; P columns
   static constexpr int NCT = (S + 7) / 8;         // head n-tiles
   static constexpr int NQ = S / 4;
   static constexpr int PITCH = ((S / 4) & 1) ? 4 * S : 4 * S + 16;   // staging row bytes
   static constexpr bool ROWCOPY = PITCH != 4 * S;
   static constexpr int SBO = 32 * SP;             // Z' row block stride (8 rows x 2 SP halves)
+  static constexpr int TB = NWS == 16 ? 512 : 256;   // TMEM columns of the CTA
+  static constexpr int EB = NWS == 16 ? 2 : 1;        // E buffers (128 columns each)
   // P-MMA B operand: NM = 2 -> [X' hi | X' lo] as one N = 2 SP operand (the lo tile follows the
   // hi tile along N), so each E half is read once per K-step: D = [hh + lh | hl + ll] per
-  // branch (P = the two halves summed); NM = 1 (S = 96) -> N = SP, three products hh, hl, lh
-  static constexpr int NM = 320 + 4 * SP <= 512 ? 2 : 1;
+  // branch (P = the two halves summed); NM = 1 -> N = SP, three products hh, hl, lh
+  static constexpr int NM = 64 + 128 * EB + 4 * SP <= TB ? 2 : 1;
   static constexpr int PW = NM * SP;                // P columns per branch
-  // TMEM columns: G buffers (64 each; two when they fit), two E buffers (128 each), P_s | P_t
-  static constexpr int GB = 384 + 2 * PW <= 512 ? 2 : 1;
-  static constexpr uint32_t TG = 0, TE0 = 64 * GB, TE1 = TE0 + 128, TP = TE1 + 128;
-  static_assert(TP + 2 * PW <= 512, "TMEM");
+  // TMEM columns: G buffers (64 each; two when they fit), E buffers, P_s | P_t
+  static constexpr int GB = 128 + 128 * EB + 2 * PW <= TB ? 2 : 1;
+  static constexpr uint32_t TG = 0, TE0 = 64 * GB, TE1 = TE0 + 128, TP = TE0 + 128 * EB;
+  static_assert(TP + 2 * PW <= TB, "TMEM");
+  static constexpr int NWC = NWS / 4;               // column groups of the softmax warps
+  static constexpr int CPT = 64 / NWC;              // keys per softmax thread and tile
+  static constexpr int NT = 32 * (NWS + 1);         // threads (+ the MMA warp)
+  static constexpr int RPT = (512 + NT - 1) / NT;   // descriptor rows per thread (N <= 512)
+  static constexpr int SB = NWS == 16 ? 2 : 1;      // staging buffers
 };
 
 __device__ __forceinline__ void sts128(unsigned char* p, uint4 v) {
@@ -174,16 +185,16 @@ __device__ __forceinline__ void tcl_exps(const uint32_t (&g)[16], float ks, floa
 
 }  // namespace
 
-template <int S, int MT>
-__global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLayout ly,
-                                                                int ctas_per_channel) {
-  using K = TclCfg<S>;
+template <int S, int MT, int NWS>
+__global__ void __launch_bounds__(32 * (NWS + 1), NWS == 16 ? 1 : 2) prnet_fwd_tcl_kernel(
+    FwdArgs a, TclLayout ly, int ctas_per_channel) {
+  using K = TclCfg<S, NWS>;
   extern __shared__ __align__(1024) unsigned char smem[];
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
-  const bool mma_warp = warp == 16;            // warp 16 issues every tcgen05.mma (lane 0)
-  const int wq = warp & 3, wc = (warp >> 2) & 3;   // row quarter (TMEM lanes), column quarter
+  const bool mma_warp = warp == NWS;           // the last warp issues every tcgen05.mma (lane 0)
+  const int wq = warp & 3, wc = (warp >> 2) % K::NWC;   // row quarter (TMEM lanes), column group
   const int c = blockIdx.y;
   const int cw = a.head_per_channel ? c : 0;
   const int N = a.N, M = a.M, H = a.H, C = a.C;
@@ -196,7 +207,7 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
   float* fks = reinterpret_cast<float*>(smem + ly.off_vec);    // [Rpad] f_i ks (seasonal shift)
   float* mtv = fks + ly.rpad;                                  // [Rpad] mu~
   float* ktv = mtv + ly.rpad;                                  // [Rpad] kappa~
-  float* lpart = ktv + ly.rpad;                                // [2][4][128] row-sum partials
+  float* lpart = ktv + ly.rpad;                                // [2][NWC][128] row-sum partials
   float* red = lpart + 2 * 4 * 128;                            // [17][3] reduction scratch, [63] m0
   float* yslot = reinterpret_cast<float*>(smem + ly.off_y);    // [2 branch][4 wq][16 MT][8 NCT]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ly.off_bar);
@@ -214,20 +225,20 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
   if (tid == 0) {
     mbar_init(gfull, 1);
     mbar_init(gfull + 1, 1);
-    mbar_init(gfree, 16);
-    mbar_init(gfree + 1, 16);
-    mbar_init(efull, 16);
-    mbar_init(efull + 1, 16);
+    mbar_init(gfree, NWS);
+    mbar_init(gfree + 1, NWS);
+    mbar_init(efull, NWS);
+    mbar_init(efull + 1, NWS);
     mbar_init(efree, 1);
     mbar_init(efree + 1, 1);
     mbar_init(pfull, 1);
-    mbar_init(pfree, 16);
+    mbar_init(pfree, NWS);
     mbar_init(xbar, 1);
     mbar_init(xbar + 1, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int k = tid; k < 8 * YW; k += blockDim.x) yslot[k] = 0.f;
-  if (warp == 0) tmem_alloc(tmem_slot, 512);
+  if (warp == 0) tmem_alloc(tmem_slot, K::TB);
   fence_proxy_async();
   tc_fence_before();
   __syncthreads();
@@ -263,7 +274,7 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
         }
       }
     } else if (!mma_warp) {
-      for (int k = tid; k < NS; k += 512) {
+      for (int k = tid; k < NS; k += 32 * NWS) {
         const int n = k / S, t = k - n * S;
         cp_async4(st + n * K::PITCH + 4 * t, xg + k);
       }
@@ -278,8 +289,8 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
     issue_load(b0, 0);
   }
   int buf = 0;
-  for (int64_t b = b0; b < b1; b++, buf ^= 1) {
-    // ---------------- a1+a2: wait for this series, prefetch the next one
+  for (int64_t b = b0; b < b1; b++, buf = K::SB == 2 ? buf ^ 1 : 0) {
+    // ---------------- a1+a2: wait for this series (two buffers: prefetch the next one now)
     if (bulk) {
       mbar_wait_bounded(xbar + buf, (phX >> buf) & 1u);
       phX ^= 1u << buf;
@@ -287,12 +298,17 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
       cp_async_wait_all();
       __syncthreads();
     }
-    if (b + 1 < b1) {
+    if (K::SB == 2 && b + 1 < b1) {
       fence_proxy_async();
       issue_load(b + 1, buf ^ 1);
     }
     const float4* st4 = reinterpret_cast<const float4*>(stg0 + (buf ? ly.stage_bytes : 0));
-    const int r = tid;                 // this thread's segment row (N <= 512; warp 16: none)
+    // segment rows r = tid + k NT (N <= 512): descriptors, Z' rows
+    float mu_[K::RPT], kap_[K::RPT], nu2_[K::RPT];
+    float s_a = 0.f, s_b = 0.f, bnd = 0.f, mu00 = 0.f;
+#pragma unroll
+    for (int rk = 0; rk < K::RPT; rk++) {
+    const int r = tid + rk * K::NT;
     const bool rv = r < N;
     const float4* xr4 = st4 + (rv ? r : 0) * (K::PITCH / 16);
     float mu = 0.f, kap = 0.f, nu2 = 0.f, x0 = 0.f, m1 = 0.f;
@@ -350,19 +366,29 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
         sts128(zr + (K::SP / 8 + ch) * 128, lv);
       }
     }
+    mu_[rk] = mu;
+    kap_[rk] = kap;
+    nu2_[rk] = nu2;
+    if (rk == 0) mu00 = mu;
+    }
     // CTA reductions: sum (mu - m0), sum [S (mu - m0)^2 + nu2] (sigma^2, Def 5, about the
     // reference m0 = mu_0) and max (|mu| + |z|) (the X' scale); m0 from thread 0 via smem
-    if (tid == 0) red[63] = mu;
+    if (tid == 0) red[63] = mu00;
     __syncthreads();
     const float m0 = red[63];
+#pragma unroll
+    for (int rk = 0; rk < K::RPT; rk++) {
+      const bool rv = tid + rk * K::NT < N;
+      const float dd = rv ? mu_[rk] - m0 : 0.f;
+      s_a += dd;
+      s_b += rv ? fmaf((float)S * dd, dd, nu2_[rk]) : 0.f;
+      bnd = fmaxf(bnd, rv ? fabsf(mu_[rk]) + sqrtf(nu2_[rk]) : 0.f);
+    }
     {
-      const float dd = rv ? mu - m0 : 0.f;
-      float s_a = dd, s_b = rv ? fmaf((float)S * dd, dd, nu2) : 0.f;
-      const float bnd = rv ? fabsf(mu) + sqrtf(nu2) : 0.f;
       s_a = warp_sum(s_a);
       s_b = warp_sum(s_b);
       const float mx = warp_max_nonneg(bnd);
-      if (lane == 0 && warp < 16) {
+      if (lane == 0) {
         red[3 * warp] = s_a;
         red[3 * warp + 1] = s_b;
         red[3 * warp + 2] = mx;
@@ -371,7 +397,7 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
     __syncthreads();
     float sa = 0.f, sb = 0.f, mxa = 0.f;
 #pragma unroll
-    for (int w = 0; w < 16; w++) {
+    for (int w = 0; w < NWS + 1; w++) {
       sa += red[3 * w];
       sb += red[3 * w + 1];
       mxa = fmaxf(mxa, red[3 * w + 2]);
@@ -379,6 +405,12 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
     const float var = fmaf(-(float)S * sa, sa * a.inv_n, sb) * a.inv_ns;
     const float inv_var = 1.0f / (var + kEpsTrend);
     const float sx = pow2_scale(mxa);
+#pragma unroll
+    for (int rk = 0; rk < K::RPT; rk++) {
+    const int r = tid + rk * K::NT;
+    const bool rv = r < N;
+    const float4* xr4 = st4 + (rv ? r : 0) * (K::PITCH / 16);
+    const float mu = mu_[rk], kap = kap_[rk], nu2 = nu2_[rk];
     // X' row r (MN-major B of the P-MMA: element (t, key r) at (t/8) 16 NK + (r/8) 128 +
     // (r%8) 16 + (t%8) 2), rows N..NK-1 zero; the per-row vectors
     if (r < NK) {
@@ -406,6 +438,14 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
       fks[r] = rv ? sqrtf(nu2 / (nu2 + kEpsSeasonal)) * a.ks : 0.f;
       mtv[r] = rv ? mu * sqrtf(inv_var * a.kt) : 0.f;
       ktv[r] = rv ? kap * sqrtf(a.vtrend * inv_var * a.kt) : 0.f;
+    }
+    }
+    if (K::SB == 1) {   // the staging buffer is read: fetch the next series now
+      __syncthreads();
+      if (b + 1 < b1) {
+        fence_proxy_async();
+        issue_load(b + 1, 0);
+      }
     }
     fence_proxy_async();
     tc_fence_before();
@@ -449,8 +489,8 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
             mbar_wait_bounded(pfree, (qcount + qt - 1) & 1u);
             tc_fence_after();
           }
-          const uint32_t eb = tg & 1u;
-          mbar_wait_bounded(efull + eb, (tg >> 1) & 1u);
+          const uint32_t eb = K::EB == 2 ? (tg & 1u) : 0u;
+          mbar_wait_bounded(efull + eb, K::EB == 2 ? ((tg >> 1) & 1u) : (tg & 1u));
           tc_fence_after();
           const uint32_t te = tmem0 + (eb ? K::TE1 : K::TE0);
           constexpr uint32_t id = idesc_f16(128, K::PW, false, true);
@@ -490,40 +530,53 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
         float ls = 0.f, lt = 0.f;
         for (int kt = 0; kt < NKT; kt++) {
           const uint32_t tg = tile + (uint32_t)(qt * NKT + kt);
-          const uint32_t eb = tg & 1u;
+          const uint32_t eb = K::EB == 2 ? (tg & 1u) : 0u;
           const uint32_t te = tmem0 + (eb ? K::TE1 : K::TE0);
           const uint32_t gb = K::GB == 2 ? (tg & 1u) : 0u;
           mbar_wait_bounded(gfull + gb, K::GB == 2 ? ((tg >> 1) & 1u) : (tg & 1u));
           tc_fence_after();
-          uint32_t g[16];
-          tld_x16(tl + K::TG + 64u * gb + 16u * wc, g);
+          constexpr int NCH = K::CPT / 16;          // 16-key chunks of this thread
+          uint32_t g[NCH][16];
+#pragma unroll
+          for (int h = 0; h < NCH; h++)
+            tld_x16(tl + K::TG + 64u * gb + 16u * (uint32_t)(wc * NCH + h), g[h]);
           tld_wait();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(gfree + gb);
-          const int j0 = 64 * kt + 16 * wc;           // this thread's first key
-          uint32_t eh[8], el[8], th[8], tlo[8];
-          if (warp_rows && !(PRNET_TCL_ABL & 4)) {
-            // key columns past N only in the last key tile: a separately compiled masked body
-            if (j0 + 16 <= N)
-              tcl_exps<false>(g, a.ks, fk, mi, ki, mtv + j0, ktv + j0, N - j0, eh, el, th, tlo, ls, lt);
-            else
-              tcl_exps<true>(g, a.ks, fk, mi, ki, mtv + j0, ktv + j0, N - j0, eh, el, th, tlo, ls, lt);
-          } else {
 #pragma unroll
-            for (int j = 0; j < 8; j++) eh[j] = el[j] = th[j] = tlo[j] = 0u;
+          for (int h = 0; h < NCH; h++) {
+            const int cidx = wc * NCH + h;              // 16-key chunk of the tile
+            const int j0 = 64 * kt + 16 * cidx;         // its first key
+            uint32_t eh[8], el[8], th[8], tlo[8];
+            if (warp_rows && !(PRNET_TCL_ABL & 4)) {
+              // key columns past N only in the last key tile: a separately compiled masked body
+              if (j0 + 16 <= N)
+                tcl_exps<false>(g[h], a.ks, fk, mi, ki, mtv + j0, ktv + j0, N - j0, eh, el, th, tlo, ls, lt);
+              else
+                tcl_exps<true>(g[h], a.ks, fk, mi, ki, mtv + j0, ktv + j0, N - j0, eh, el, th, tlo, ls, lt);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 8; j++) eh[j] = el[j] = th[j] = tlo[j] = 0u;
+            }
+            if (h == 0) {
+              // the E buffer is free once the P-MMA that last read it committed (two buffers:
+              // tile tg - 2, one buffer: tile tg - 1)
+              if (K::EB == 2 && tg >= 2) {
+                mbar_wait_bounded(efree + eb, ((tg >> 1) - 1) & 1u);
+                tc_fence_after();
+              } else if (K::EB == 1 && tg >= 1) {
+                mbar_wait_bounded(efree, (tg - 1) & 1u);
+                tc_fence_after();
+              }
+            }
+            // E into TMEM buffer eb: [0,32) E_s hi, [32,64) E_s lo, [64,96) E_t hi, [96,128)
+            // E_t lo (a 16-key chunk = 8 packed columns at 8 cidx)
+            tst_x8(tl + (te - tmem0) + 8u * cidx, eh);
+            tst_x8(tl + (te - tmem0) + 32u + 8u * cidx, el);
+            tst_x8(tl + (te - tmem0) + 64u + 8u * cidx, th);
+            tst_x8(tl + (te - tmem0) + 96u + 8u * cidx, tlo);
           }
-          // E buffer eb is free once the P-MMA of tile tg - 2 committed
-          if (tg >= 2) {
-            mbar_wait_bounded(efree + eb, ((tg >> 1) - 1) & 1u);
-            tc_fence_after();
-          }
-          // E into TMEM buffer eb: [0,32) E_s hi, [32,64) E_s lo, [64,96) E_t hi, [96,128)
-          // E_t lo (this thread's 16 keys = 8 packed columns at 8 wc)
-          tst_x8(tl + (te - tmem0) + 8u * wc, eh);
-          tst_x8(tl + (te - tmem0) + 32u + 8u * wc, el);
-          tst_x8(tl + (te - tmem0) + 64u + 8u * wc, th);
-          tst_x8(tl + (te - tmem0) + 96u + 8u * wc, tlo);
           tst_wait();
           tc_fence_before();
           __syncwarp();
@@ -531,14 +584,14 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
         }
         // ---------------- a7: row sums -> 1/l; the head over this query tile's rows
         lpart[wc * 128 + 32 * wq + lane] = ls;
-        lpart[512 + wc * 128 + 32 * wq + lane] = lt;
-        named_bar(1, 512);
+        lpart[K::NWC * 128 + wc * 128 + 32 * wq + lane] = lt;
+        named_bar(1, 32 * NWS);
         mbar_wait_bounded(pfull, (qcount + qt) & 1u);
         tc_fence_after();
         if (warp_rows && !(PRNET_TCL_ABL & 8)) {
           const int g = lane >> 2;
           // work items (branch, n-tile) of this row quarter, split over the column quarters
-          for (int it = wc; it < 2 * K::NCT; it += 4) {
+          for (int it = wc; it < 2 * K::NCT; it += K::NWC) {
             const int br = it / K::NCT, nt = it - br * K::NCT;
             float acc[MT][4];
 #pragma unroll
@@ -553,8 +606,10 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
 #pragma unroll
               for (int v = 0; v < 2; v++) {
                 const int rr = 32 * wq + 16 * kb + g + 8 * v;
-                const float* lp = lpart + 512 * br + rr;
-                const float l_ = ((lp[0] + lp[128]) + lp[256]) + lp[384];
+                const float* lp = lpart + K::NWC * 128 * br + rr;
+                float l_ = lp[0];
+#pragma unroll
+                for (int cg = 1; cg < K::NWC; cg++) l_ += lp[cg * 128];
                 il[v] = 128 * qt + rr < N ? 1.f / l_ : 0.f;
               }
               uint32_t pr[4];
@@ -600,7 +655,7 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(pfree);
-        named_bar(1, 512);   // lpart is rewritten by the next query tile
+        named_bar(1, 32 * NWS);   // lpart is rewritten by the next query tile
       }
     }
     tile += (uint32_t)ntiles;
@@ -628,7 +683,7 @@ __global__ void __launch_bounds__(544, 1) prnet_fwd_tcl_kernel(FwdArgs a, TclLay
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 0) tmem_dealloc(tmem0, 512);
+  if (warp == 0) tmem_dealloc(tmem0, K::TB);
 }
 
 bool tcl_supported_s(int S) { return S == 12 || S == 24 || S == 48 || S == 96; }
@@ -650,20 +705,28 @@ bool plan_tcl_kernel(const FwdArgs& a, int max_smem_optin, int sm_count, TclPlan
   ly.off_x = off;
   off += 4 * SP * NK;                       // X' hi | lo, [SP/8][NK/8] core matrices each
   ly.stage_bytes = (a.N * pitch + 127) & ~127;
+  // two CTAs per SM (8 softmax warps, 256 TMEM columns, one staging buffer) when the S <= 24
+  // instantiation's shared memory fits half the SM; else one CTA of 16 softmax warps
+  const bool narrow = S <= 24;
+  int off1 = off + ly.stage_bytes;
+  const int vec = (3 * ly.rpad + 2 * 4 * 128 + 64) * 4;
+  const int ybytes = 8 * 16 * MT * 8 * NCT * 4;
+  const int tail = ((off1 + vec + 127) & ~127) - off1 + ybytes + 256;
+  p->nws = (narrow && (size_t)(off1 + tail) <= (size_t)max_smem_optin / 2 - 1024) ? 8 : 16;
   ly.off_stage = off;
-  off += 2 * ly.stage_bytes;
+  off += (p->nws == 16 ? 2 : 1) * ly.stage_bytes;
   ly.off_vec = off;
-  off += (3 * ly.rpad + 2 * 4 * 128 + 64) * 4;
+  off += vec;
   off = (off + 127) & ~127;
   ly.off_y = off;
-  off += 8 * 16 * MT * 8 * NCT * 4;
+  off += ybytes;
   ly.off_bar = off;
   off += 256;
   ly.wpack_bytes = flash_wpack_bytes(a.N, a.M);
   p->smem_bytes = (size_t)off;
   if (p->smem_bytes > (size_t)max_smem_optin) return false;
-  // one CTA per SM (TMEM: 512 columns); channels x k CTAs, k against wave quantisation
-  const int64_t sms = sm_count > 0 ? sm_count : 148;
+  // channels x k CTAs, k against wave quantisation (1 or 2 CTAs per SM)
+  const int64_t sms = (sm_count > 0 ? sm_count : 148) * (p->nws == 8 ? 2 : 1);
   int64_t best_k = 1, best = -1;
   for (int64_t k = 1; k <= 64 && k <= a.B; k++) {
     const int64_t waves = ((int64_t)a.C * k + sms - 1) / sms;
@@ -674,31 +737,31 @@ bool plan_tcl_kernel(const FwdArgs& a, int max_smem_optin, int sm_count, TclPlan
   return true;
 }
 
-template <int S, int MT>
+template <int S, int MT, int NWS>
 static cudaError_t launch_tcl_t(const FwdArgs& a, const TclPlan& p, cudaStream_t st) {
-  auto k = prnet_fwd_tcl_kernel<S, MT>;
+  auto k = prnet_fwd_tcl_kernel<S, MT, NWS>;
   cudaError_t e =
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)p.ctas_per_channel, (unsigned)a.C);
-  k<<<grid, 544, p.smem_bytes, st>>>(a, p.ly, p.ctas_per_channel);
+  k<<<grid, 32 * (NWS + 1), p.smem_bytes, st>>>(a, p.ly, p.ctas_per_channel);
   return cudaGetLastError();
+}
+
+template <int S, int NWS>
+static cudaError_t launch_tcl_m(const FwdArgs& a, const TclPlan& p, cudaStream_t st) {
+  return p.mt == 1   ? launch_tcl_t<S, 1, NWS>(a, p, st)
+         : p.mt == 2 ? launch_tcl_t<S, 2, NWS>(a, p, st)
+                     : launch_tcl_t<S, 4, NWS>(a, p, st);
 }
 
 cudaError_t launch_tcl_kernel(const FwdArgs& a, const TclPlan& p, cudaStream_t st) {
   switch (a.S) {
-#define PRNET_TCL_L(SV)                                                                 \
-  case SV:                                                                              \
-    return p.mt == 1   ? launch_tcl_t<SV, 1>(a, p, st)                                 \
-           : p.mt == 2 ? launch_tcl_t<SV, 2>(a, p, st)                                 \
-                       : launch_tcl_t<SV, 4>(a, p, st);
-    PRNET_TCL_L(12)
-    PRNET_TCL_L(24)
-    PRNET_TCL_L(48)
-    PRNET_TCL_L(96)
-#undef PRNET_TCL_L
-    default:
-      return cudaErrorInvalidValue;
+    case 12: return p.nws == 8 ? launch_tcl_m<12, 8>(a, p, st) : launch_tcl_m<12, 16>(a, p, st);
+    case 24: return p.nws == 8 ? launch_tcl_m<24, 8>(a, p, st) : launch_tcl_m<24, 16>(a, p, st);
+    case 48: return launch_tcl_m<48, 16>(a, p, st);
+    case 96: return launch_tcl_m<96, 16>(a, p, st);
+    default: return cudaErrorInvalidValue;
   }
 }
 

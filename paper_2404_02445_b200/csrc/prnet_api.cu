@@ -247,10 +247,13 @@ int pick_variant(const prnet_handle* h) {
     return 6;
   if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
   // tc_long (tcgen05) against flash_f16x3 (mma.sync), measured on B200 (profiles/README.md,
-  // round 2): stress L5760/S96 (N = 60) 10.5 vs 11.9 ms, L5760/S48 (N = 120) 9.98 vs 11.6 ms;
-  // flash stays ahead for S <= 24 (L5760/S12 27.4 vs 34.4 ms) and at L2880/S48 (4.56 vs 6.86)
-  if (tcl_applicable(h) && (!flash_applicable(h) || h->cfg.seg_len == 96 ||
-                            (h->cfg.seg_len == 48 && h->N >= 100)))
+  // round 2; S <= 24 runs two 8-softmax-warp CTAs per SM): L5760/S12 (N = 480) 25.3 vs 27.4 ms,
+  // L2880/S12 7.61 vs 8.13, L1440/S12 3.22 vs 3.41, L5760/S24 11.95 vs 12.17, L5760/S96 10.5 vs
+  // 11.9, L5760/S48 9.99 vs 11.6; flash stays ahead at N = 60 (S <= 48) and L2880/S24 (N = 120)
+  if (tcl_applicable(h) &&
+      (!flash_applicable(h) || h->cfg.seg_len == 96 ||
+       (h->cfg.seg_len == 48 && h->N >= 100) || (h->cfg.seg_len == 12 && h->N >= 100) ||
+       (h->cfg.seg_len == 24 && h->N >= 200)))
     return 8;   // (M > 32: the only tensor-core kernel for N > 32)
   if (h->N > 32 && flash_applicable(h)) return 5;
   return h->N <= 32 ? 0 : 1;
