@@ -194,16 +194,26 @@ const char* kWideningMsg =
 // FP32 kernels run (warp_f32, long_f32); tc_quad / tc_pipe (shift 1) need tau_s >= 1/80.
 constexpr float kTauKnownMax = 1.0f / 320.0f;
 bool known_max_ok(const prnet_handle* h) { return h->cfg.tau_seasonal >= kTauKnownMax; }
-// 8 = tc_long (32 < N <= 512, S in {12, 24, 48, 96}, M <= 32, plain reading, tau_s >= 1/320:
-// 128-row query tiles on tcgen05 / TMEM, key tiles of 64, known seasonal row bound)
+// 8 = tc_long (32 < N <= 512, S in {12, 24, 48, 96}, M <= 64, plain reading, tau_s >= 1/16:
+// 128-row query tiles on tcgen05 / TMEM, key tiles of 64, known seasonal row bound f_i).  Its
+// unnormalised E = 2^((rho - f_i) ks) is the P-MMA's fp16 hi/lo operand; a row whose true
+// maximum f_i^2 sits below the bound (nu_i^2 not >> eps_s: f_i - f_i^2 up to 1/4) keeps its
+// largest term >= 2^(-ks/4) >= 2^-5.8 only for tau_s >= 1/16 (below, fp16 subnormals lose the
+// row: measured 275x the tolerance at tau_s = 0.01 on near-constant segments, DESIGN.md R-tcl)
+constexpr float kTauTcl = 1.0f / 16.0f;
 bool tcl_applicable(const prnet_handle* h) {
   return h->N > 32 && h->N <= 512 && h->M <= 64 && prnet::tcl_supported_s(h->cfg.seg_len) &&
-         h->cfg.tau_seasonal >= 1.0f / 320.0f;
+         h->cfg.tau_seasonal >= kTauTcl;
 }
 // 9 = group_f32 (N <= 16, S <= 32: lanes over (series, segment), FP32; plain reading,
 // tau_s >= 1/80 for its symmetric seasonal shift 1, as tc_quad)
 bool grp_applicable(const prnet_handle* h) {
   return h->N <= 16 && h->cfg.seg_len <= 32 && h->cfg.tau_seasonal >= 0.0125f;
+}
+// 10 = lane_f32 (N <= 8, S % 4 == 0, N S <= 192, H % 4 == 0: one lane per series, FP32,
+// searched seasonal row maximum, so any tau_s)
+bool lane_applicable(const prnet_handle* h) {
+  return prnet::lane_shape_ok(h->N, h->cfg.seg_len, h->cfg.horizon, h->cfg.lookback);
 }
 // 7 = small_f32 (N <= 16, S <= 128, M <= 32: lanes over time, FP32)
 bool small_applicable(const prnet_handle* h) {
@@ -249,11 +259,13 @@ int pick_variant(const prnet_handle* h) {
   // tc_long (tcgen05) against flash_f16x3 (mma.sync), measured on B200 (profiles/README.md,
   // round 2; S <= 24 runs two 8-softmax-warp CTAs per SM): L5760/S12 (N = 480) 25.3 vs 27.4 ms,
   // L2880/S12 7.61 vs 8.13, L1440/S12 3.22 vs 3.41, L5760/S24 11.95 vs 12.17, L5760/S96 10.5 vs
-  // 11.9, L5760/S48 9.99 vs 11.6; flash stays ahead at N = 60 (S <= 48) and L2880/S24 (N = 120)
+  // 11.9, L5760/S48 9.99 vs 11.6; flash stays ahead at N = 60 (S <= 48), L2880/S24 (N = 120)
+  // and for S = 24 with a long head (L5760/S24/H720, M = 30: 13.4 vs 18.2 ms)
   if (tcl_applicable(h) &&
       (!flash_applicable(h) || h->cfg.seg_len == 96 ||
-       (h->cfg.seg_len == 48 && h->N >= 100) || (h->cfg.seg_len == 12 && h->N >= 100) ||
-       (h->cfg.seg_len == 24 && h->N >= 200)))
+       (h->cfg.seg_len == 48 && h->N >= 100) ||
+       (h->M <= 8 && ((h->cfg.seg_len == 12 && h->N >= 100) ||
+                      (h->cfg.seg_len == 24 && h->N >= 200)))))
     return 8;   // (M > 32: the only tensor-core kernel for N > 32)
   if (h->N > 32 && flash_applicable(h)) return 5;
   return h->N <= 32 ? 0 : 1;
@@ -281,7 +293,7 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
     // level-only trend), mma_f16x3, long_f32 (every flag) and tc_quad (detrend /
     // instance_norm), each from the values its own fold consumes; small_f32 maps to
     // mma_f16x3 (same domain, every flag), flash_f16x3 to long_f32 (every flag and N)
-    if (v == 7 || v == 9) v = h->M <= 32 ? 2 : 0;
+    if (v == 7 || v == 9 || v == 10) v = h->M <= 32 ? 2 : 0;
     if (v == 5 || v == 8) v = 1;
     if (v == 0 && widening_on(h)) v = 1;
   }
@@ -289,7 +301,12 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
     const char* e = getenv("PRNET_WINDOWS_PER_CTA");
     return e ? atoi(e) : 0;
   }();
-  if (v == 9) {
+  if (v == 10) {
+    prnet::LanePlan p;
+    if (!prnet::plan_lane_kernel(a, h->max_smem_optin, h->sm_count, &p))
+      return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the lane_f32 kernel");
+    e = prnet::launch_lane_kernel(a, p, st);
+  } else if (v == 9) {
     prnet::GrpPlan p;
     if (!prnet::plan_grp_kernel(a, h->max_smem_optin, &p))
       return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the group_f32 kernel");
@@ -905,15 +922,18 @@ prnet_status prnet_backward(prnet_handle* h, const float* x, int64_t batch, cons
 
 prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {
   if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
-  if (variant < -1 || variant > 9)
-    return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,...,9}");
+  if (variant < -1 || variant > 10)
+    return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,...,10}");
+  if (variant == 10 && !lane_applicable(h))
+    return fail(h, PRNET_ERR_UNSUPPORTED,
+                "lane_f32 variant needs N <= 8, S % 4 == 0, N S <= 192, H % 4 == 0");
   if (variant == 9 && !grp_applicable(h))
     return fail(h, PRNET_ERR_UNSUPPORTED,
                 "group_f32 variant needs N <= 16, S <= 32, tau_seasonal >= 1/80");
   if (variant == 8 && !tcl_applicable(h))
     return fail(h, PRNET_ERR_UNSUPPORTED,
                 "tc_long variant needs 32 < N <= 512, S in {12, 24, 48, 96}, M <= 64, "
-                "tau_seasonal >= 1/320");
+                "tau_seasonal >= 1/16");
   if (variant == 3 || variant == 4)
     return fail(h, PRNET_ERR_INVALID_ARG,
                 "variants 3 (tc_fold) and 4 (tc_full) are retired: 6 (tc_quad) supersedes them");

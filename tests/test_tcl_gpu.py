@@ -16,7 +16,7 @@ torch = pytest.importorskip("torch")
 if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
-from paper_2404_02445_b200 import PRNet  # noqa: E402
+from paper_2404_02445_b200 import PRNet, PrnetError  # noqa: E402
 
 
 def _run(oracle_mod, B, C, L, S, H, kind="mixed", tau_s=1.0, tau_t=1.0, hpc=True, seed=13):
@@ -65,7 +65,7 @@ def test_tcl_value_kinds(oracle_mod, S, kind):
 
 
 @pytest.mark.parametrize("S", [12, 24])
-@pytest.mark.parametrize("tau", [0.005, 0.05, 0.3, 4.0])
+@pytest.mark.parametrize("tau", [0.0625, 0.1, 0.3, 4.0])
 @pytest.mark.parametrize("hpc", [True, False])
 def test_tcl_temperatures(oracle_mod, S, tau, hpc):
     _run(oracle_mod, 2, 3, 90 * S, S, 2 * S + 3, tau_s=tau, tau_t=tau * 0.7, hpc=hpc)
@@ -98,3 +98,36 @@ def test_tcl_deterministic():
     m = PRNet(3, 2880, 24, 96).load(ws, wt, b)
     m.set_variant("tc_long")
     assert torch.equal(m.forward(x), m.forward(x))
+
+
+@pytest.mark.parametrize("noise", [1e-6, 3e-7])
+@pytest.mark.parametrize("S", [12, 48])
+def test_tcl_near_constant_at_floor(oracle_mod, S, noise):
+    """Segments constant to within `noise` (nu^2 ~ eps_s: the known bound f_i sits up to 1/4 above
+    the row maximum f_i^2) at the temperature floor tau_s = 1/16 (DESIGN.md R-tcl)."""
+    B, C, L, H = 2, 3, 60 * S, 96
+    x = synth.random_windows(B, C, L, seed=5, kind="mixed").astype(np.float64)
+    rng = np.random.default_rng(5)
+    N = L // S
+    for b in range(B):
+        for c in range(C):
+            for n in rng.choice(N, size=N // 5, replace=False):
+                x[b, c, n * S:(n + 1) * S] = x[b, c, n * S] + noise * rng.standard_normal(S)
+    x = x.astype(np.float32)
+    _, _, M = synth.derived_dims(L, S, H)
+    ws, wt, b = synth.make_params(C, M, N, H, True, synth.DEFAULT_SEED, 0)
+    m = PRNet(C, L, S, H, tau_s=1 / 16, tau_t=0.5).load(ws, wt, b)
+    m.set_variant("tc_long")
+    y = m.forward(torch.from_numpy(x).cuda()).cpu().numpy()
+    _, y64 = oracle_mod.forward(x, S, H, ws, wt, b, True, 1 / 16, 0.5)
+    assert_parity(y, y64)
+
+
+def test_tcl_rejects_below_floor():
+    S, L, H = 12, 60 * 12, 96
+    N, _, M = synth.derived_dims(L, S, H)
+    ws, wt, b = synth.make_params(2, M, N, H, True, synth.DEFAULT_SEED, 0)
+    m = PRNet(2, L, S, H, tau_s=0.05).load(ws, wt, b)
+    with pytest.raises(PrnetError):
+        m.set_variant("tc_long")
+    assert m.plan(4)["variant"] != "tc_long"
