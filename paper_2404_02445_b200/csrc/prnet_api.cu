@@ -210,11 +210,6 @@ bool tcl_applicable(const prnet_handle* h) {
 bool grp_applicable(const prnet_handle* h) {
   return h->N <= 16 && h->cfg.seg_len <= 32 && h->cfg.tau_seasonal >= 0.0125f;
 }
-// 10 = lane_f32 (N <= 8, S % 4 == 0, N S <= 192, H % 4 == 0: one lane per series, FP32,
-// searched seasonal row maximum, so any tau_s)
-bool lane_applicable(const prnet_handle* h) {
-  return prnet::lane_shape_ok(h->N, h->cfg.seg_len, h->cfg.horizon, h->cfg.lookback);
-}
 // 7 = small_f32 (N <= 16, S <= 128, M <= 32: lanes over time, FP32)
 bool small_applicable(const prnet_handle* h) {
   return h->N <= 16 && h->cfg.seg_len <= 128 && h->M <= 32;
@@ -293,7 +288,7 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
     // level-only trend), mma_f16x3, long_f32 (every flag) and tc_quad (detrend /
     // instance_norm), each from the values its own fold consumes; small_f32 maps to
     // mma_f16x3 (same domain, every flag), flash_f16x3 to long_f32 (every flag and N)
-    if (v == 7 || v == 9 || v == 10) v = h->M <= 32 ? 2 : 0;
+    if (v == 7 || v == 9) v = h->M <= 32 ? 2 : 0;
     if (v == 5 || v == 8) v = 1;
     if (v == 0 && widening_on(h)) v = 1;
   }
@@ -301,12 +296,7 @@ prnet_status enqueue_forward(prnet_handle* h, const float* x, int64_t B, float* 
     const char* e = getenv("PRNET_WINDOWS_PER_CTA");
     return e ? atoi(e) : 0;
   }();
-  if (v == 10) {
-    prnet::LanePlan p;
-    if (!prnet::plan_lane_kernel(a, h->max_smem_optin, h->sm_count, &p))
-      return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the lane_f32 kernel");
-    e = prnet::launch_lane_kernel(a, p, st);
-  } else if (v == 9) {
+  if (v == 9) {
     prnet::GrpPlan p;
     if (!prnet::plan_grp_kernel(a, h->max_smem_optin, &p))
       return fail(h, PRNET_ERR_UNSUPPORTED, "shape not supported by the group_f32 kernel");
@@ -922,11 +912,8 @@ prnet_status prnet_backward(prnet_handle* h, const float* x, int64_t batch, cons
 
 prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant) {
   if (!h) return fail(nullptr, PRNET_ERR_BAD_STATE, "NULL handle");
-  if (variant < -1 || variant > 10)
-    return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,...,10}");
-  if (variant == 10 && !lane_applicable(h))
-    return fail(h, PRNET_ERR_UNSUPPORTED,
-                "lane_f32 variant needs N <= 8, S % 4 == 0, N S <= 192, H % 4 == 0");
+  if (variant < -1 || variant > 9)
+    return fail(h, PRNET_ERR_INVALID_ARG, "variant in {-1,...,9}");
   if (variant == 9 && !grp_applicable(h))
     return fail(h, PRNET_ERR_UNSUPPORTED,
                 "group_f32 variant needs N <= 16, S <= 32, tau_seasonal >= 1/80");

@@ -27,7 +27,7 @@ EXPORTS = ("prnet_create", "prnet_load_params", "prnet_forward", "prnet_forward_
            "prnet_forward_sliding_host", "prnet_backward_head", "prnet_backward", "prnet_forward_bf16")
 # index = the C ABI's variant id (include/prnet.h); 3 and 4 are retired round-1 prototypes
 VARIANTS = ("warp_f32", "long_f32", "mma_f16x3", "retired_tc_fold", "retired_tc_full",
-            "flash_f16x3", "tc_quad", "small_f32", "tc_long", "group_f32", "lane_f32")
+            "flash_f16x3", "tc_quad", "small_f32", "tc_long", "group_f32")
 
 
 class PrnetError(RuntimeError):

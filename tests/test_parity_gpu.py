@@ -44,13 +44,11 @@ def _applicable(variant, L, S, H):
         return 32 < N <= 512 and S in (12, 24, 48, 96) and M <= 64
     if variant == "group_f32":
         return N <= 16 and S <= 32
-    if variant == "lane_f32":
-        return N <= 8 and S % 4 == 0 and N * S <= 192 and H % 4 == 0
     return True
 
 
 VARIANTS = [None, "warp_f32", "mma_f16x3", "long_f32", "flash_f16x3", "tc_quad", "small_f32",
-            "tc_long", "group_f32", "lane_f32"]
+            "tc_long", "group_f32"]
 SHORT_VARIANTS = [None, "warp_f32", "mma_f16x3", "tc_quad", "small_f32"]
 
 
