@@ -69,28 +69,47 @@ __global__ void __launch_bounds__(256) prnet_fwd_grp_kernel(FwdArgs a, int wins_
   const float w = a.vtrend;
   const int64_t b_begin = (int64_t)blockIdx.x * wins_per_cta;
   const int64_t b_end = min(b_begin + (int64_t)wins_per_cta, a.B);
-  for (int64_t bb = b_begin + (int64_t)warp * G; bb < b_end; bb += (int64_t)nwarps * G) {
-    const int64_t b = bb + gi;
-    const bool vs = b < b_end;                // this group's series exists
-    const bool valid = vs && i < N;
-    // ---------------- a1: segment row i into registers (Def 2)
-    float x[SP];
+  // a1: segment row i of the group's series into registers (Def 2); the next round's row is
+  // loaded while this round computes (software pipelining: the DRAM latency of round k + 1
+  // overlaps round k's arithmetic instead of stalling every round)
+  auto load_row = [&](int64_t bbr, float (&xr)[SP]) {
 #pragma unroll
-    for (int t = 0; t < SP; t++) x[t] = 0.f;
-    if (valid) {
-      const float* xg = a.x + b * a.xsb + c * a.xsc + a.r + (int64_t)i * S;
+    for (int t = 0; t < SP; t++) xr[t] = 0.f;
+    const int64_t br = bbr + gi;
+    if (br < b_end && i < N) {
+      const float* xg = a.x + br * a.xsb + c * a.xsc + a.r + (int64_t)i * S;
       if (vec) {
 #pragma unroll
         for (int q = 0; q < SQ; q++)
           if (4 * q < S) {
             const float4 v = __ldg(reinterpret_cast<const float4*>(xg) + q);
-            x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
+            xr[4 * q] = v.x; xr[4 * q + 1] = v.y; xr[4 * q + 2] = v.z; xr[4 * q + 3] = v.w;
           }
       } else {
 #pragma unroll
         for (int t = 0; t < SP; t++)
-          if (t < S) x[t] = __ldg(xg + t);
+          if (t < S) xr[t] = __ldg(xg + t);
       }
+    }
+  };
+  // (S <= 16 only: measured, the second row costs S = 24 more occupancy than it hides, L96/S24
+  // 0.037 -> 0.046 ms; L96/S12 0.057 -> 0.053, L192/S12 0.137 -> 0.127)
+  constexpr bool PF = SP <= 16;
+  const int64_t bstep = (int64_t)nwarps * G;
+  float xnext[SP];
+  if constexpr (PF) load_row(b_begin + (int64_t)warp * G, xnext);
+  for (int64_t bb = b_begin + (int64_t)warp * G; bb < b_end; bb += bstep) {
+    const int64_t b = bb + gi;
+    const bool vs = b < b_end;                // this group's series exists
+    const bool valid = vs && i < N;
+    // ---------------- a1: segment row i (prefetched), then the next round's row
+    float x[SP];
+    if constexpr (PF) {
+#pragma unroll
+      for (int t = 0; t < SP; t++) x[t] = xnext[t];
+      if (bb + bstep < b_end) load_row(bb + bstep, xnext);
+    } else {
+      load_row(bb, x);
     }
     // ---------------- a2: descriptors (Def 3-5) from d = x - x0
     const float x0 = x[0];
