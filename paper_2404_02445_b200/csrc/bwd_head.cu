@@ -14,6 +14,7 @@
 // warps are reduced in a fixed order into one partial per CTA, and prnet_bwd_reduce sums the
 // partials in fp64 in a fixed order.  Deterministic, no atomics.
 #include <algorithm>
+#include <cstdlib>
 
 #include "prnet_internal.cuh"
 
@@ -431,6 +432,13 @@ __global__ void __launch_bounds__(256) prnet_bwd_long_kernel(FwdArgs a, const fl
 
 bool plan_bwd_head(const FwdArgs& a, int max_smem_optin, BwdPlan* p) {
   if (a.N < 1 || a.M > 32) return false;
+  p->mma_mode = false;
+  // the tensor-core kernel where it applies (PRNET_BWD_F32=1: this file's FP32 kernel, A/B)
+  static const bool force_f32 = [] {
+    const char* e = getenv("PRNET_BWD_F32");
+    return e && atoi(e) != 0;
+  }();
+  if (!force_f32 && plan_bwd_head_mma(a, max_smem_optin, p)) return true;
   if (a.N > 32 || a.S > 128) {   // long mode (prnet_bwd_long_kernel)
     if (a.N > 512) return false;
     p->long_mode = true;
@@ -488,7 +496,10 @@ static cudaError_t launch_bwd_n(const FwdArgs& a, const BwdPlan& p, const float*
 
 cudaError_t launch_bwd_head(const FwdArgs& a, const BwdPlan& p, const float* dy, float* part,
                             float* dws, float* dwt, float* db, int Cw, cudaStream_t st) {
-  if (p.nblk > 0 && p.long_mode) {
+  if (p.nblk > 0 && p.mma_mode) {
+    cudaError_t e = launch_bwd_head_mma(a, p, dy, part, st);
+    if (e != cudaSuccess) return e;
+  } else if (p.nblk > 0 && p.long_mode) {
     cudaError_t e;
     auto go = [&](auto kern) {
       cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
