@@ -30,7 +30,8 @@ namespace prnet {
 
 namespace {
 
-constexpr int kBmWarps = 8;
+constexpr int kBmWarps = 4;
+constexpr int kBmMinBlocks = 3;   // 12 warps per SM: <= 168 registers
 
 // split a pair into (hi, lo) f16x2 registers (mma_common.cuh's split2)
 __device__ __forceinline__ void split_pair(float a, float b, uint32_t& hi, uint32_t& lo) {
@@ -67,7 +68,7 @@ struct BmCfg {
 };
 
 template <int S>
-__global__ void __launch_bounds__(32 * kBmWarps, 1) prnet_bwd_head_mma_kernel(FwdArgs a, const float* __restrict__ dy,
+__global__ void __launch_bounds__(32 * kBmWarps, kBmMinBlocks) prnet_bwd_head_mma_kernel(FwdArgs a, const float* __restrict__ dy,
                                                                            float* __restrict__ part,
                                                                            int wins_per_cta, int per_warp) {
   using K = BmCfg<S>;
@@ -99,6 +100,12 @@ __global__ void __launch_bounds__(32 * kBmWarps, 1) prnet_bwd_head_mma_kernel(Fw
 #pragma unroll
         for (int r = 0; r < 4; r++) acc[br][mt][nt][r] = 0.f;
 
+  // column masks of the logits (0 or -inf): j = 8 nt + 2 q + u < N
+  float cneg[4][2];
+#pragma unroll
+  for (int nt = 0; nt < 4; nt++)
+#pragma unroll
+    for (int u = 0; u < 2; u++) cneg[nt][u] = 8 * nt + 2 * q + u < N ? 0.f : -INFINITY;
   const int i = lane;
   const bool xvec = a.x_vec != 0;
   const bool yvec = (H & 3) == 0 && (((uintptr_t)dy) & 15u) == 0;
@@ -273,7 +280,9 @@ __global__ void __launch_bounds__(32 * kBmWarps, 1) prnet_bwd_head_mma_kernel(Fw
         rmt[mt][h] = __shfl_sync(0xffffffffu, mtc, 16 * mt + g + 8 * h);
         rkt[mt][h] = __shfl_sync(0xffffffffu, ktc, 16 * mt + g + 8 * h);
       }
-    float pacc[2][2][KT][4];   // [branch][m-tile (rows n)][t-tile][4]
+    // per branch: softmax -> P' = A X' -> G = dY' P'^T -> dW += G / (sx sy) (one branch's
+    // patterns live at a time)
+    const float gsc = 1.f / (sx * sy);   // exact (powers of two)
 #pragma unroll
     for (int br = 0; br < 2; br++) {
       float e[2][4][4];
@@ -288,15 +297,13 @@ __global__ void __launch_bounds__(32 * kBmWarps, 1) prnet_bwd_head_mma_kernel(Fw
           for (int nt = 0; nt < 4; nt++)
 #pragma unroll
             for (int u = 0; u < 2; u++) {
-              const int col = 8 * nt + 2 * q + u;
               float v;
               if (br == 0) {
-                v = gacc[mt][nt][2 * h + u] * a.ks;
+                v = fmaf(gacc[mt][nt][2 * h + u], a.ks, cneg[nt][u]);
               } else {
                 const float dm = rmt[mt][h] - cmt[nt][u], dk = rkt[mt][h] - ckt[nt][u];
-                v = -fmaf(dm, dm, dk * dk);
+                v = cneg[nt][u] - fmaf(dm, dm, dk * dk);
               }
-              v = col < N ? v : -INFINITY;
               lg[nt][u] = v;
               rmax = fmaxf(rmax, v);
             }
@@ -322,12 +329,13 @@ __global__ void __launch_bounds__(32 * kBmWarps, 1) prnet_bwd_head_mma_kernel(Fw
         }
       // P' = A X': A fragments from e (k-step kk = j in [16 kk, 16 kk + 16)), B = X' by
       // ldmatrix.trans of the [j][t] rows
+      float pacc[2][KT][4];   // [m-tile (rows n)][t-tile][4]
 #pragma unroll
       for (int mt = 0; mt < 2; mt++)
 #pragma unroll
         for (int tt = 0; tt < KT; tt++)
 #pragma unroll
-          for (int r = 0; r < 4; r++) pacc[br][mt][tt][r] = 0.f;
+          for (int r = 0; r < 4; r++) pacc[mt][tt][r] = 0.f;
 #pragma unroll
       for (int kk = 0; kk < 2; kk++) {
         uint32_t ah[2][4], al[2][4];
@@ -345,65 +353,51 @@ __global__ void __launch_bounds__(32 * kBmWarps, 1) prnet_bwd_head_mma_kernel(Fw
           ldsm_x2_t(bh0, bh1, p);
           ldsm_x2_t(bl0, bl1, p + K::TILE);
 #pragma unroll
-          for (int mt = 0; mt < 2; mt++) mma3(pacc[br][mt][tt], ah[mt], al[mt], bh0, bh1, bl0, bl1);
+          for (int mt = 0; mt < 2; mt++) mma3(pacc[mt][tt], ah[mt], al[mt], bh0, bh1, bl0, bl1);
         }
       }
-    }
-
-    // ---------------- gradient: G = dY' P'^T per branch, dW += G / (sx sy)
-    const float gsc = 1.f / (sx * sy);   // exact (powers of two)
+      // ---------------- gradient: G = dY' P'^T (B fragments from P's accumulators: row n of
+      // P' is column n of the B tile), one m-tile of dW at a time
 #pragma unroll
-    for (int br = 0; br < 2; br++) {
-      float gtmp[2][4][4];
-#pragma unroll
-      for (int mt = 0; mt < 2; mt++)
+      for (int mt = 0; mt < 2; mt++) {
+        float gtmp[4][4];
 #pragma unroll
         for (int nt = 0; nt < 4; nt++)
 #pragma unroll
-          for (int r = 0; r < 4; r++) gtmp[mt][nt][r] = 0.f;
+          for (int r = 0; r < 4; r++) gtmp[nt][r] = 0.f;
 #pragma unroll
-      for (int kk = 0; kk < KT / 2; kk++) {   // k16 over t-tiles 2 kk, 2 kk + 1
-        uint32_t ah[2][4], al[2][4];
-#pragma unroll
-        for (int mt = 0; mt < 2; mt++) {
+        for (int kk = 0; kk < KT / 2; kk++) {   // k16 over t-tiles 2 kk, 2 kk + 1
+          uint32_t ah[4], al[4];
           const unsigned char* p = Yh + (16 * mt + (lane & 15)) * PB + 2 * (16 * kk + 8 * (lane >> 4));
-          ldsm_x4(ah[mt], p);
-          ldsm_x4(al[mt], p + K::TILE);
+          ldsm_x4(ah, p);
+          ldsm_x4(al, p + K::TILE);
+#pragma unroll
+          for (int nt = 0; nt < 4; nt++) {   // n = 8 nt + g: row g + 8 (nt & 1) of P's m-tile nt / 2
+            const int pm = nt >> 1, ph = nt & 1;
+            uint32_t bh0, bl0, bh1, bl1;
+            split_pair(pacc[pm][2 * kk][2 * ph], pacc[pm][2 * kk][2 * ph + 1], bh0, bl0);
+            split_pair(pacc[pm][2 * kk + 1][2 * ph], pacc[pm][2 * kk + 1][2 * ph + 1], bh1, bl1);
+            mma3(gtmp[nt], ah, al, bh0, bh1, bl0, bl1);
+          }
         }
-#pragma unroll
-        for (int nt = 0; nt < 4; nt++) {   // n = 8 nt + g: row g + 8 (nt & 1) of P's m-tile nt / 2
-          const int pm = nt >> 1, ph = nt & 1;
-          uint32_t bh0, bl0, bh1, bl1;
-          split_pair(pacc[br][pm][2 * kk][2 * ph], pacc[br][pm][2 * kk][2 * ph + 1], bh0, bl0);
-          split_pair(pacc[br][pm][2 * kk + 1][2 * ph], pacc[br][pm][2 * kk + 1][2 * ph + 1], bh1, bl1);
-#pragma unroll
-          for (int mt = 0; mt < 2; mt++) mma3(gtmp[mt][nt], ah[mt], al[mt], bh0, bh1, bl0, bl1);
-        }
-      }
-      if constexpr (KT & 1) {   // k8 tail over t-tile KT - 1
-        uint32_t ah[2][2], al[2][2];
-#pragma unroll
-        for (int mt = 0; mt < 2; mt++) {
+        if constexpr (KT & 1) {   // k8 tail over t-tile KT - 1
+          uint32_t ah0, ah1, al0, al1;
           const unsigned char* p = Yh + (16 * mt + (lane & 15)) * PB + 2 * (S - 8);
-          ldsm_x2(ah[mt][0], ah[mt][1], p);
-          ldsm_x2(al[mt][0], al[mt][1], p + K::TILE);
+          ldsm_x2(ah0, ah1, p);
+          ldsm_x2(al0, al1, p + K::TILE);
+#pragma unroll
+          for (int nt = 0; nt < 4; nt++) {
+            const int pm = nt >> 1, ph = nt & 1;
+            uint32_t bh, bl;
+            split_pair(pacc[pm][KT - 1][2 * ph], pacc[pm][KT - 1][2 * ph + 1], bh, bl);
+            mma3k8(gtmp[nt], ah0, ah1, al0, al1, bh, bl);
+          }
         }
-#pragma unroll
-        for (int nt = 0; nt < 4; nt++) {
-          const int pm = nt >> 1, ph = nt & 1;
-          uint32_t bh, bl;
-          split_pair(pacc[br][pm][KT - 1][2 * ph], pacc[br][pm][KT - 1][2 * ph + 1], bh, bl);
-#pragma unroll
-          for (int mt = 0; mt < 2; mt++)
-            mma3k8(gtmp[mt][nt], ah[mt][0], ah[mt][1], al[mt][0], al[mt][1], bh, bl);
-        }
-      }
-#pragma unroll
-      for (int mt = 0; mt < 2; mt++)
 #pragma unroll
         for (int nt = 0; nt < 4; nt++)
 #pragma unroll
-          for (int r = 0; r < 4; r++) acc[br][mt][nt][r] = fmaf(gtmp[mt][nt][r], gsc, acc[br][mt][nt][r]);
+          for (int r = 0; r < 4; r++) acc[br][mt][nt][r] = fmaf(gtmp[nt][r], gsc, acc[br][mt][nt][r]);
+      }
     }
   }
 
