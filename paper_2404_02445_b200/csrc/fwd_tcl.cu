@@ -39,6 +39,11 @@
 
 // ablation switches for A/B builds (results invalid when non-zero): 1 no P-MMA, 2 no Gram MMA,
 // 4 no exponentials, 8 no head
+// the MMA thread's mbarrier waits carry a suspend-time hint (ns; 0 = plain polling).  A/B
+// (profiles/README.md): 2000 ns 0.7-0.9 % faster at S <= 24 than polling, equal at S = 48
+#ifndef PRNET_TCL_SLEEP_NS
+#define PRNET_TCL_SLEEP_NS 2000
+#endif
 #ifndef PRNET_TCL_ABL
 #define PRNET_TCL_ABL 0
 #endif
@@ -458,6 +463,16 @@ __global__ void __launch_bounds__(32 * (NWS + 1), NWS == 16 ? 1 : 2) prnet_fwd_t
       // as soon as E(t) is stored; commits drive the softmax warps
       if (lane == 0) {
         const uint32_t sbo_x = 16u * (uint32_t)NK;
+        // the MMA thread's waits: with PRNET_TCL_SLEEP_NS a suspend-time hint (the thread sleeps
+        // until the phase completes instead of re-polling, leaving issue slots to the softmax
+        // warps of the SM)
+        auto mma_wait = [](uint64_t* bar, uint32_t parity) {
+#if PRNET_TCL_SLEEP_NS
+          mbar_wait_sleep(bar, parity, PRNET_TCL_SLEEP_NS);
+#else
+          mbar_wait_bounded(bar, parity);
+#endif
+        };
         auto issue_gram = [&](int t) {   // series tile t -> G buffer (tile + t) % GB
           const int qt = t / NKT, kt = t - qt * NKT;
           const uint32_t gb = K::GB == 2 ? ((tile + (uint32_t)t) & 1u) : 0u;
@@ -480,17 +495,17 @@ __global__ void __launch_bounds__(32 * (NWS + 1), NWS == 16 ? 1 : 2) prnet_fwd_t
           const uint32_t tg = tile + (uint32_t)t;   // global tile index
           const int qt = t / NKT, kt = t - qt * NKT;
           if (t + K::GB < ntiles) {   // G buffer of tile t is read: the Gram of tile t + GB
-            if (K::GB == 2) mbar_wait_bounded(gfree + (tg & 1u), (tg >> 1) & 1u);
-            else mbar_wait_bounded(gfree, tg & 1u);
+            if (K::GB == 2) mma_wait(gfree + (tg & 1u), (tg >> 1) & 1u);
+            else mma_wait(gfree, tg & 1u);
             tc_fence_after();
             issue_gram(t + K::GB);
           }
           if (kt == 0 && qcount + qt > 0) {   // the previous query tile's head has read P
-            mbar_wait_bounded(pfree, (qcount + qt - 1) & 1u);
+            mma_wait(pfree, (qcount + qt - 1) & 1u);
             tc_fence_after();
           }
           const uint32_t eb = K::EB == 2 ? (tg & 1u) : 0u;
-          mbar_wait_bounded(efull + eb, K::EB == 2 ? ((tg >> 1) & 1u) : (tg & 1u));
+          mma_wait(efull + eb, K::EB == 2 ? ((tg >> 1) & 1u) : (tg & 1u));
           tc_fence_after();
           const uint32_t te = tmem0 + (eb ? K::TE1 : K::TE0);
           constexpr uint32_t id = idesc_f16(128, K::PW, false, true);
