@@ -564,16 +564,14 @@ __global__ void __launch_bounds__(32 * (NWS + 1), NWS == 16 ? 1 : 2) prnet_fwd_t
             const int cidx = wc * NCH + h;              // 16-key chunk of the tile
             const int j0 = 64 * kt + 16 * cidx;         // its first key
             uint32_t eh[8], el[8], th[8], tlo[8];
-            if (warp_rows && !(PRNET_TCL_ABL & 4)) {
-              // key columns past N only in the last key tile: a separately compiled masked body
-              if (j0 + 16 <= N)
-                tcl_exps<false>(g[h], a.ks, fk, mi, ki, mtv + j0, ktv + j0, N - j0, eh, el, th, tlo, ls, lt);
-              else
-                tcl_exps<true>(g[h], a.ks, fk, mi, ki, mtv + j0, ktv + j0, N - j0, eh, el, th, tlo, ls, lt);
-            } else {
-#pragma unroll
-              for (int j = 0; j < 8; j++) eh[j] = el[j] = th[j] = tlo[j] = 0u;
-            }
+            // key columns past N (the last key tile) and rows past N (warp_rows false: no valid
+            // key) take the separately compiled masked body, which writes zeros (no separate
+            // zero-fill branch; measured neutral on B200, 25.03 vs 25.07 ms at stress L5760/S12)
+            const int nv = warp_rows ? N - j0 : 0;
+            if (nv >= 16)
+              tcl_exps<false>(g[h], a.ks, fk, mi, ki, mtv + j0, ktv + j0, nv, eh, el, th, tlo, ls, lt);
+            else
+              tcl_exps<true>(g[h], a.ks, fk, mi, ki, mtv + j0, ktv + j0, nv, eh, el, th, tlo, ls, lt);
             if (h == 0) {
               // the E buffer is free once the P-MMA that last read it committed (two buffers:
               // tile tg - 2, one buffer: tile tg - 1)
@@ -605,6 +603,22 @@ __global__ void __launch_bounds__(32 * (NWS + 1), NWS == 16 ? 1 : 2) prnet_fwd_t
         tc_fence_after();
         if (warp_rows && !(PRNET_TCL_ABL & 8)) {
           const int g = lane >> 2;
+          // 1 / l of this lane's fragment rows (branch, k-step, row half), once per query tile
+          // rather than per work item (MUFU reciprocal, <= 1 ulp, as the other kernels' softmax)
+          float ilv[2][2][2];
+#pragma unroll
+          for (int br = 0; br < 2; br++)
+#pragma unroll
+            for (int kb = 0; kb < 2; kb++)
+#pragma unroll
+              for (int v = 0; v < 2; v++) {
+                const int rr = 32 * wq + 16 * kb + g + 8 * v;
+                const float* lp = lpart + K::NWC * 128 * br + rr;
+                float l_ = lp[0];
+#pragma unroll
+                for (int cg = 1; cg < K::NWC; cg++) l_ += lp[cg * 128];
+                ilv[br][kb][v] = 128 * qt + rr < N ? fast_rcp(l_) : 0.f;
+              }
           // work items (branch, n-tile) of this row quarter, split over the column quarters
           for (int it = wc; it < 2 * K::NCT; it += K::NWC) {
             const int br = it / K::NCT, nt = it - br * K::NCT;
@@ -617,16 +631,8 @@ __global__ void __launch_bounds__(32 * (NWS + 1), NWS == 16 ? 1 : 2) prnet_fwd_t
             for (int kb = 0; kb < 2; kb++) {
               const int i0 = 128 * qt + 32 * wq + 16 * kb;   // K rows of this step
               if (i0 >= npf) break;
-              float il[2];
-#pragma unroll
-              for (int v = 0; v < 2; v++) {
-                const int rr = 32 * wq + 16 * kb + g + 8 * v;
-                const float* lp = lpart + K::NWC * 128 * br + rr;
-                float l_ = lp[0];
-#pragma unroll
-                for (int cg = 1; cg < K::NWC; cg++) l_ += lp[cg * 128];
-                il[v] = 128 * qt + rr < N ? 1.f / l_ : 0.f;
-              }
+              const float il[2] = {br ? ilv[1][kb][0] : ilv[0][kb][0],
+                                   br ? ilv[1][kb][1] : ilv[0][kb][1]};
               uint32_t pr[4];
               const uint32_t pa = tmem0 + ((uint32_t)(32 * wq + 16 * kb) << 16) + K::TP +
                                   (uint32_t)(br * K::PW + 8 * nt);
