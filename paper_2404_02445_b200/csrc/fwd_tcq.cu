@@ -82,6 +82,11 @@ constexpr int kQOffBias = kQOffTmem + 16;
 constexpr int kQBiasRow = 24;
 constexpr int kQBias = 32 * kQBiasRow;             // bias rows m < 32, zero-padded
 constexpr int kQSmem = kQOffBias + kQBias * 4;
+// component values (metric_variant bit 2, reading R-f4): each warp's X' tile has a 4th n-block
+// (the columns mu^ sx, kappa^ sx), 1 KB more per warp
+constexpr int kQXTComp = kQXT + 4096;
+constexpr int kQGroupComp = kQGroup + 4096;
+constexpr int kQSmemComp = kQSmem + kQGroups * 4096;
 static_assert(kQGroup % 16 == 0, "16-byte aligned tiles");
 
 constexpr uint32_t kIdGram = idesc_f16(128, 128, false, false);
@@ -107,11 +112,23 @@ __device__ __forceinline__ void sts128(unsigned char* p, uint4 v) {
 // BF: BF16 I/O (prnet_forward_bf16): x is read and y written as bf16 (half
 // the HBM bytes); the staging row holds bf16 and is widened to fp32 in registers (exact), every
 // step after that is the fp32 kernel's; y is rounded to bf16 (round to nearest even) at the store
-template <int NC, bool WIDE, bool DUMP = false, bool BF = false>
+// COMP (metric_variant bit 2, reading R-f4): the branches aggregate their
+// components, Y = W_s A_s Vs + W_t A_t Vt with Vs = xhat - mu^ 1' - d1 kappa^ t~', Vt = mu^ 1' +
+// d0 kappa^ t~' (d0 = 1 - bit 0, d1 = bit 1), i.e. Y = Q_s xhat + alpha 1' + beta t~' with
+// alpha = (Q_t - Q_s) mu^, beta = (d0 Q_t - d1 Q_s) kappa^ (exact in real arithmetic).  The fold
+// writes Q_s and Q_t into separate TMEM columns; the head multiplies Q_s by [X' | mu^ sx,
+// kappa^ sx] (a 4th n-tile) and Q_t by the 4th n-tile only.
+template <int NC, bool WIDE, bool DUMP = false, bool BF = false, bool COMP = false>
 __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ctas_per_channel) {
   // WIDE: the SURVEY §8(f) widening (detrended seasonal metric, instance normalisation) is
   // compiled in; the plain instantiation is exactly the reading's kernel
   const bool detrend = WIDE && a.detrend, revin = WIDE && a.revin;
+  static_assert(!COMP || (WIDE && !BF && !DUMP), "COMP: the widened fp32 instantiation");
+  constexpr int XT = COMP ? kQXTComp : kQXT;          // X' tile per group
+  constexpr int XW = XT / 4;                          // per warp: 3 (4 with COMP) n-blocks
+  constexpr int GRP = COMP ? kQGroupComp : kQGroup;
+  constexpr int OFFW = kQGroups * GRP, OFFBAR = OFFW + 8192, OFFTMEM = OFFBAR + 256,
+                OFFBIAS = OFFTMEM + 16;
   static_assert(NC % 2 == 0 && NC <= 32, "NC");
   extern __shared__ __align__(1024) unsigned char smem[];
   constexpr int S = 24;
@@ -128,17 +145,17 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
   const int i = lane;
   const bool valid = i < N;
 
-  unsigned char* gbase = smem + grp * kQGroup;
+  unsigned char* gbase = smem + grp * GRP;
   unsigned char* zq = gbase;
   unsigned char* xt = gbase + kQZQ;
-  float* xstage = reinterpret_cast<float*>(gbase + kQZQ + kQXT + s * kQStage);
+  float* xstage = reinterpret_cast<float*>(gbase + kQZQ + XT + s * kQStage);
   // column vectors: [0] mu~, [1] kappa~, [2] 1/l_t, [3] 1/l_s, [4] seasonal mask (NC = 0)
-  float* colv = reinterpret_cast<float*>(gbase + kQZQ + kQXT + 4 * kQStage) + s * kQColW;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kQOffBar);
+  float* colv = reinterpret_cast<float*>(gbase + kQZQ + XT + 4 * kQStage) + s * kQColW;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFFBAR);
   uint64_t* mbar = bars + 3 * grp;                  // +0 Gram, +1 fold, +2 head done
   uint64_t* xbar = bars + 3 * kQGroups + warp;      // this warp's TMA load
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kQOffTmem);
-  const float* bS = reinterpret_cast<const float*>(smem + kQOffBias);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFFTMEM);
+  const float* bS = reinterpret_cast<const float*>(smem + OFFBIAS);
 
   // ---------------- prologue: channel head W' and bias, barriers, TMEM.  The operand
   // tiles need no zero fill: every row an active series reads is written each round
@@ -146,10 +163,10 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
   // discarded off-diagonal blocks and idle rows.
   {
     const uint4* src = a.wpack_tc + (int64_t)cw * (8192 / 16);
-    uint4* dst = reinterpret_cast<uint4*>(smem + kQOffW);
+    uint4* dst = reinterpret_cast<uint4*>(smem + OFFW);
     for (int k = threadIdx.x; k < 8192 / 16; k += blockDim.x) dst[k] = __ldg(src + k);
     const float* gb = a.bias + (int64_t)cw * H;
-    float* bw = reinterpret_cast<float*>(smem + kQOffBias);
+    float* bw = reinterpret_cast<float*>(smem + OFFBIAS);
     for (int k = threadIdx.x; k < kQBias; k += blockDim.x) {
       const int h = (k / kQBiasRow) * 24 + k % kQBiasRow;
       bw[k] = (k % kQBiasRow < 24 && h < H) ? __ldg(gb + h) : 0.f;
@@ -168,7 +185,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
   const uint32_t tcol = tmem0 + 128u * (uint32_t)grp;   // the group's 128 columns
   const uint32_t tlane = (uint32_t)(32 * s) << 16;        // this warp's 32 lanes
   const bool mma_warp = s == 0;
-  const uint32_t zq_s = smem_u32(zq), xt_s = smem_u32(xt), w_s = smem_u32(smem + kQOffW);
+  const uint32_t zq_s = smem_u32(zq), xt_s = smem_u32(xt), w_s = smem_u32(smem + OFFW);
   const float inv_sw = __ldg(a.wpack_inv_sw + cw);
   const bool full_rows = H == 24 * M && (H & 1) == 0;   // the output rows tile H exactly
 
@@ -227,6 +244,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
     const int64_t b = g0 + 4 * rd + s;
     const bool active = b < g1;
     float sx = 1.f, mi = 0.f, ki = 0.f;
+    [[maybe_unused]] float cmu = 0.f, ckap = 0.f;   // COMP: mu^ = (mu - mu_r) rr, kappa^ = kappa rr
     float sr = 1.f, mr = 0.f;   // forecast de-normalisation y = yhat sr + mr (instance_norm)
     float xv[24];   // the segment row, then X' = x sx (stored after the Gram issue)
 
@@ -411,6 +429,10 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
       const float inv_var = 1.0f / fmaf(var * rr, rr, kEpsTrend);
       // trend (Def 7-8): exponent -(mu~_i - mu~_j)^2 - (k~_i - k~_j)^2, mu~ = muhat sqrt(kt/var'),
       // k~ = kappahat sqrt(vtrend kt/var')
+      if constexpr (COMP) {
+        cmu = (mu - mu_r) * rr;
+        ckap = kap * rr;
+      }
       mi = (mu - mu_r) * rr * sqrtf(inv_var * a.kt);
       ki = kap * rr * sqrtf(a.vtrend * inv_var * a.kt);
       colv[i] = (NC > 0 || valid) ? mi : INFINITY;   // -> exponent -inf past N
@@ -436,13 +458,20 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
     }
     // X' rows -> head B tile (read only by the head, after the next barrier)
     if (active) {
-      unsigned char* xr = xt + 3 * s * 1024 + (i >> 3) * 128 + (i & 7) * 16;
+      unsigned char* xr = xt + XW * s + (i >> 3) * 128 + (i & 7) * 16;
 #pragma unroll
       for (int q = 0; q < 3; q++) {
         uint4 h, l;
         split8(xv + 8 * q, h, l);
         sts128(xr + q * 1024, h);
         sts128(xr + q * 1024 + 512, l);
+      }
+      if constexpr (COMP) {
+        // n-block 3: columns t = 24, 25 <- mu^ sx, kappa^ sx of row i (|.| < 1 like X'), 0 past N
+        uint32_t h, l;
+        split2(valid ? make_float2(cmu * sx, ckap * sx) : make_float2(0.f, 0.f), h, l);
+        sts128(xr + 3 * 1024, make_uint4(h, 0u, 0u, 0u));
+        sts128(xr + 3 * 1024 + 512, make_uint4(l, 0u, 0u, 0u));
       }
     }
 
@@ -575,9 +604,12 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
       for (int ks = 0; ks < 4; ks++) {
         const uint64_t bh = sdesc(w_s + ks * 256, 128, 2048);
         const uint64_t bl = sdesc(w_s + (8 + 2 * ks) * 128, 128, 2048);
-        umma_ts(tcol + 64u, tcol + 8u * ks, bh, kIdFold, ks > 0);
-        umma_ts(tcol + 64u, tcol + 8u * ks, bl, kIdFold, true);
-        umma_ts(tcol + 64u, tcol + 32u + 8u * ks, bh, kIdFold, true);
+        // COMP: Q_s^T (ks 0, 1: A_s) in [64, 96), Q_t^T (ks 2, 3: A_t) in [96, 128)
+        const uint32_t dq = tcol + ((COMP && ks >= 2) ? 96u : 64u);
+        const bool acc0 = COMP ? (ks & 1) != 0 : ks > 0;
+        umma_ts(dq, tcol + 8u * ks, bh, kIdFold, acc0);
+        umma_ts(dq, tcol + 8u * ks, bl, kIdFold, true);
+        umma_ts(dq, tcol + 32u + 8u * ks, bh, kIdFold, true);
       }
       umma_commit(mbar + 1);
     }
@@ -588,10 +620,10 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
     // in registers (movmatrix), block (j-half h, j-octet v, m-octet k) is A-fragment
     // register (k & 1) + 2v of tile (m-tile k / 2, k-tile h).  No shared-memory round trip.
     uint32_t qah[2][2][4], qal[2][2][4];   // [mt][kt][reg]
-    if (active) {
+    auto load_q = [&](uint32_t qcol) {
       uint32_t r0[16], r1[16];
-      tld16_x4(tcol + ((uint32_t)(32 * s) << 16) + 64u, r0);
-      tld16_x4(tcol + ((uint32_t)(32 * s + 16) << 16) + 64u, r1);
+      tld16_x4(tcol + ((uint32_t)(32 * s) << 16) + qcol, r0);
+      tld16_x4(tcol + ((uint32_t)(32 * s + 16) << 16) + qcol, r1);
       tld_wait();
 #pragma unroll
       for (int h = 0; h < 2; h++)
@@ -606,14 +638,15 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
             qah[k >> 1][h][(k & 1) + 2 * v] = movm_t(hi);
             qal[k >> 1][h][(k & 1) + 2 * v] = movm_t(lo);
           }
-    }
+    };
+    if (active) load_q(64u);
     // ---------------- a7 head on mma.sync, per warp (its own series only, so no group
     // barrier and no block-diagonal waste): Y' = Q' X' with m16n8k16 split-fp16 MMAs,
     // A = Q' and B = X' fragments by ldmatrix.trans from the core-matrix tiles
     if (active) {
       __syncwarp();
       const int l8 = lane & 7, g4 = lane >> 3;
-      const unsigned char* xs = xt + 3 * s * 1024;
+      const unsigned char* xs = xt + XW * s;
       float acc[2][3][4];
 #pragma unroll
       for (int mt = 0; mt < 2; mt++)
@@ -649,6 +682,51 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
         for (int mt = 0; mt < 2; mt++)
 #pragma unroll
           for (int nt = 0; nt < 3; nt++) mma16816_nv(acc[mt][nt], qah[mt][kt], xh[nt][0], xh[nt][1]);
+      }
+      if constexpr (COMP) {
+        // the 4th n-tile [mu^ sx, kappa^ sx, 0 ..]: Q_s (still in qah / qal), then Q_t
+        float ce[2][2][4];   // [Q_s, Q_t][mt][e]
+        auto ext = [&](float (&c4)[2][4]) {
+#pragma unroll
+          for (int mt = 0; mt < 2; mt++)
+#pragma unroll
+            for (int e = 0; e < 4; e++) c4[mt][e] = 0.f;
+#pragma unroll
+          for (int kt = 0; kt < 2; kt++) {
+            uint32_t b0h, b1h, b0l, b1l;
+            const unsigned char* p3 = xs + 3 * 1024 + (2 * kt + (g4 & 1)) * 128 + l8 * 16;
+            ldsm_x2_t(b0h, b1h, p3);
+            ldsm_x2_t(b0l, b1l, p3 + 512);
+#pragma unroll
+            for (int mt = 0; mt < 2; mt++) {
+              mma16816_nv(c4[mt], qal[mt][kt], b0h, b1h);
+              mma16816_nv(c4[mt], qah[mt][kt], b0l, b1l);
+              mma16816_nv(c4[mt], qah[mt][kt], b0h, b1h);
+            }
+          }
+        };
+        ext(ce[0]);
+        load_q(96u);
+        ext(ce[1]);
+        // alpha' = (Q_t - Q_s) mu^ sx, beta' = (d0 Q_t - d1 Q_s) kappa^ sx on rows (g, g + 8) of
+        // each m-tile, held by the lane with c = 0 (columns 0, 1); Y' += alpha' + beta' t~
+        const float d0 = a.vtrend != 0.f ? 1.f : 0.f, d1 = detrend ? 1.f : 0.f;
+        const int src = lane & ~3;
+#pragma unroll
+        for (int mt = 0; mt < 2; mt++)
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const float al = __shfl_sync(0xffffffffu, ce[1][mt][2 * h] - ce[0][mt][2 * h], src);
+            const float be = __shfl_sync(0xffffffffu,
+                                         d0 * ce[1][mt][2 * h + 1] - d1 * ce[0][mt][2 * h + 1], src);
+#pragma unroll
+            for (int nt = 0; nt < 3; nt++)
+#pragma unroll
+              for (int e = 0; e < 2; e++) {
+                const float tt = (float)(8 * nt + 2 * (lane & 3) + e) - 11.5f;
+                acc[mt][nt][2 * h + e] += fmaf(be, tt, al);
+              }
+          }
       }
       // ---------------- a8 store: y = Y' / (sw sx) + b (Def 11), pairs (m, t..t+1)
       const float2 ys2 = f2(inv_sw * sr / sx);
@@ -761,7 +839,7 @@ void pack_tc_head(const float* ws, const float* wt, int Cw, int M, int N, unsign
 
 bool plan_tcq_kernel(const FwdArgs& a, int max_smem_optin, int sm_count, TcqPlan* p) {
   if (a.S != 24 || a.N < 1 || a.N > 32 || a.M > 32) return false;
-  p->smem_bytes = (size_t)kQSmem;
+  p->smem_bytes = (size_t)(a.comp ? kQSmemComp : kQSmem);
   if (p->smem_bytes > (size_t)max_smem_optin) return false;
   p->wins_per_group = 128;
   // one CTA per SM: a small launch (few channels x few windows) ends in a partial wave.
@@ -782,9 +860,9 @@ bool plan_tcq_kernel(const FwdArgs& a, int max_smem_optin, int sm_count, TcqPlan
   return true;
 }
 
-template <int NC, bool WIDE, bool DUMP = false, bool BF = false>
+template <int NC, bool WIDE, bool DUMP = false, bool BF = false, bool COMP = false>
 static cudaError_t launch_tcq_t(const FwdArgs& a, const TcqPlan& p, cudaStream_t st) {
-  auto k = prnet_fwd_tcq_kernel<NC, WIDE, DUMP, BF>;
+  auto k = prnet_fwd_tcq_kernel<NC, WIDE, DUMP, BF, COMP>;
   cudaError_t e =
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
@@ -803,6 +881,9 @@ cudaError_t launch_tcq_kernel(const FwdArgs& a, const TcqPlan& p, cudaStream_t s
   if (a.io_bf16)   // BF16 I/O: the plain reading (prnet_forward_bf16 rejects the widening)
     return a.N == 30 ? launch_tcq_t<30, false, false, true>(a, p, st)
                      : launch_tcq_t<0, false, false, true>(a, p, st);
+  if (a.comp)   // component values (reading R-f4), with or without detrend / instance_norm
+    return a.N == 30 ? launch_tcq_t<30, true, false, false, true>(a, p, st)
+                     : launch_tcq_t<0, true, false, false, true>(a, p, st);
   const bool wide = a.detrend || a.revin;
   if (a.N == 30) return wide ? launch_tcq_t<30, true>(a, p, st) : launch_tcq_t<30, false>(a, p, st);
   return wide ? launch_tcq_t<0, true>(a, p, st) : launch_tcq_t<0, false>(a, p, st);

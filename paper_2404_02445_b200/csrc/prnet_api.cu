@@ -168,7 +168,7 @@ bool tcq_wide_applicable(const prnet_handle* h) {
 // Variants that implement the SURVEY §8(f) widening: the level-only trend runs in every
 // kernel (a.vtrend = 0); the detrended seasonal metric and instance normalisation in
 // tc_quad, mma_f16x3 (N <= 32) and flash_f16x3 (16 < N <= 512, S <= 96); component values
-// (bit 2) in mma_f16x3.
+// (bit 2) in mma_f16x3, tc_quad (S = 24), flash_f16x3 and long_f32.
 bool widening_on(const prnet_handle* h) {
   return (h->cfg.metric_variant & 6) != 0 || h->cfg.instance_norm != 0 || h->cfg.ma_kernel > 0;
 }
@@ -179,13 +179,14 @@ bool comp_on(const prnet_handle* h) {
 }
 bool variant_supports_widening(const prnet_handle* h, int v) {
   if (h->cfg.ma_kernel > 0) return v == 1 || v == 2;
-  if (comp_on(h)) return v == 1 || v == 2 || v == 5;
+  if (comp_on(h)) return v == 1 || v == 2 || v == 5 || (v == 6 && h->cfg.seg_len == 24);
   return v == 1 || v == 2 || v == 5 || (v == 6 && h->cfg.seg_len == 24);
 }
 const char* kWideningMsg =
     "metric_variant bit 1 / instance_norm need tc_quad, mma_f16x3 (N <= 32), "
     "flash_f16x3 (16 < N <= 512, S <= 96, M <= 32) or long_f32 (N <= 512); metric_variant "
-    "bit 2 needs mma_f16x3 (N <= 32, M <= 32, S <= 128), flash_f16x3 or long_f32; ma_kernel "
+    "bit 2 needs tc_quad (S = 24), mma_f16x3 (N <= 32, M <= 32, S <= 128), flash_f16x3 or "
+    "long_f32; ma_kernel "
     "needs mma_f16x3 (N <= 32, M <= 32, S <= 128) or long_f32 (any N <= 512)";
 // The kernels that shift the seasonal logits by a KNOWN row bound instead of searching the
 // row maximum (small_f32, mma_f16x3, flash_f16x3: f_i = nu_i / sqrt(nu_i^2 + eps_s) >= rho_ij;
@@ -220,6 +221,8 @@ int pick_variant(const prnet_handle* h) {
   if (!known_max_ok(h)) return (h->N <= 32 && !widening_on(h)) ? 0 : 1;
   if (widening_on(h)) {
     if (comp_on(h)) {
+      // component values at S = 24 (no decomposition): tc_quad's COMP instantiation
+      if (h->cfg.ma_kernel == 0 && tcq_wide_applicable(h) && h->N > 8) return 6;
       if (h->N <= 32 && h->M <= 32 && h->cfg.seg_len <= 128) return 2;
       if (h->cfg.ma_kernel == 0 && flash_applicable(h)) return 5;
       return 1;   // long_f32 (any S, N <= 512)

@@ -381,6 +381,17 @@ def test_component_values_parity(oracle_mod, L, S, H, mv, rev):
     _check_widening(oracle_mod, x, S, H, mv, rev)
 
 
+@pytest.mark.parametrize("mv,rev", [(4, False), (5, False), (6, False), (7, False), (4, True),
+                                    (6, True), (7, True)])
+@pytest.mark.parametrize("L,H", [(720, 720), (720, 336), (100, 90), (96, 96), (480, 200),
+                                 (744, 24)])
+def test_component_values_tc_quad(oracle_mod, L, H, mv, rev):
+    """The S = 24 tc_quad COMP instantiation (forced, every N it takes): Q_s and Q_t folded into
+    separate TMEM columns, alpha / beta from the head's 4th n-tile [mu^, kappa^] (reading R-f4)."""
+    x = synth.random_windows(3, 5, L, kind="mixed")
+    _check_widening(oracle_mod, x, 24, H, mv, rev, variant="tc_quad")
+
+
 @pytest.mark.parametrize("kind", ["normal", "constant", "scaled"])
 @pytest.mark.parametrize("tau,hpc", [(0.05, True), (1.0, False), (10.0, True)])
 def test_component_values_distributions(oracle_mod, kind, tau, hpc):
@@ -434,10 +445,15 @@ def test_component_values_unsupported_paths():
     m.load(np.zeros((3, m.M, m.N)), np.zeros((3, m.M, m.N)), np.zeros((3, 96)))
     m.forward(torch.zeros((2, 3, 3000), device="cuda"))
     m2 = PRNet(3, 720, 24, 96, metric_variant=4)
-    for v in ("tc_quad", "small_f32", "warp_f32"):
+    for v in ("small_f32", "warp_f32"):
         with pytest.raises(PrnetError) as e:
             m2.set_variant(v)
         assert e.value.status == 3
+    m2.set_variant("tc_quad")   # S = 24: the COMP instantiation (round 2)
+    m3 = PRNet(3, 720, 24, 96, metric_variant=4, ma_kernel=5)
+    with pytest.raises(PrnetError) as e:   # the decomposition is not compiled into tc_quad
+        m3.set_variant("tc_quad")
+    assert e.value.status == 3
     m2.set_variant("mma_f16x3")
     m2.set_variant("flash_f16x3")
 
