@@ -98,17 +98,24 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
 
   const int64_t b0 = (int64_t)blockIdx.x * ly.wins_per_cta;
   const int64_t b1 = min(b0 + (int64_t)ly.wins_per_cta, a.B);
+  // (n, t) of flat index k = lane + 32 u, stepped without an integer division per element
+  const int q32 = 32 / S, r32 = 32 - q32 * S;
+  const int n_l = lane / S, t_l = lane - n_l * S;
   for (int64_t b = b0 + warp; b < b1; b += nwarps) {
     const int64_t series = b * C + c;
     const float* xg = a.x + b * a.xsb + c * a.xsc + r;
     const float* dyg = dy + series * H;
-    for (int k = lane; k < N * S; k += 32) {
-      const int n = k / S, t = k - n * S;
+    for (int k = lane, n = n_l, t = t_l; k < N * S; k += 32) {
       Xs[n * P + t] = __ldg(xg + k);
+      n += q32;
+      t += r32;
+      if (t >= S) { t -= S; n++; }
     }
-    for (int k = lane; k < H; k += 32) {
-      const int m = k / S, t = k - m * S;
+    for (int k = lane, m = n_l, t = t_l; k < H; k += 32) {
       dYs[m * P + t] = __ldg(dyg + k);
+      m += q32;
+      t += r32;
+      if (t >= S) { t -= S; m++; }
     }
     __syncwarp();
     // ---------------- forward recompute (Def 3-8), FP32
@@ -141,6 +148,10 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
     const float mubar = m0 + sd * a.inv_n;
     const float g = rsqrtf(nu2 + kEpsSeasonal);
     gv[i] = g;
+    // series-level reciprocals, formed once: the per-element steps below multiply (IEEE
+    // divisions inside the N x N loops were 37 % of the kernel's instructions)
+    const float its = 1.f / tau_s, itt = 1.f / tau_t, iden = 1.f / den;
+    const float ct = iden * itt;             // Dhat / tau_t = D / (den tau_t)
     __syncwarp();
     // Gram row i: <z_i, z_j> from the own row and broadcast rows (z = X - mu; t >= S masked)
     float lmax_s = -INFINITY, lmax_t = -INFINITY;
@@ -174,16 +185,16 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
           const float D = fmaf(w * dk, dk, dm * dm);
           Rh[i * Q + j] = rho;
           Dm[i * Q + j] = D;
-          lmax_s = fmaxf(lmax_s, rho / tau_s);
-          lmax_t = fmaxf(lmax_t, -D / den / tau_t);
+          lmax_s = fmaxf(lmax_s, rho * its);
+          lmax_t = fmaxf(lmax_t, -D * ct);
         }
       }
     }
     if (valid) {
       float ls = 0.f, lt = 0.f;
       for (int j = 0; j < N; j++) {
-        const float es = __expf(Rh[i * Q + j] / tau_s - lmax_s);
-        const float et = __expf(-Dm[i * Q + j] / den / tau_t - lmax_t);
+        const float es = __expf(Rh[i * Q + j] * its - lmax_s);
+        const float et = __expf(-Dm[i * Q + j] * ct - lmax_t);
         As[i * Q + j] = es;
         At[i * Q + j] = et;
         ls += es;
@@ -239,6 +250,7 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
     // ---------------- a5: softmax adjoints (own rows) -> drho, dD, dtau and ds2 partials
     float ds2 = 0.f;
     const float rref = lmax_s * tau_s;   // the row maximum of rho: sum_j dls_ij = 0
+    const float its2 = its * its, ctt = ct * itt, iden2 = iden * iden;
     if (valid) {
       float ss = 0.f, st = 0.f;
 #pragma unroll
@@ -253,12 +265,12 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
           const float dls = As[i * Q + j] * (dAs[j] - ss);
           const float dlt = At[i * Q + j] * (dAt[j] - st);
           const float rho = Rh[i * Q + j], D = Dm[i * Q + j];
-          dts -= dls * (rho - rref) / (tau_s * tau_s);
-          dtt += dlt * (D / den) / (tau_t * tau_t);
-          const float dDh = -dlt / tau_t;
-          ds2 -= dDh * D / (den * den);
-          dAs[j] = dls / tau_s;      // drho_ij
-          dAt[j] = dDh / den;        // dD_ij
+          dts -= dls * (rho - rref) * its2;
+          dtt += dlt * D * ctt;      // dlt Dhat / tau_t^2
+          const float dDh = -dlt * itt;
+          ds2 -= dDh * D * iden2;
+          dAs[j] = dls * its;        // drho_ij
+          dAt[j] = dDh * iden;       // dD_ij
         }
     }
     __syncwarp();   // every lane has read A's columns (a6) and its own rows
@@ -327,9 +339,11 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
       }
     }
     __syncwarp();
-    for (int k = lane; k < N * S; k += 32) {
-      const int n = k / S, t = k - n * S;
+    for (int k = lane, n = n_l, t = t_l; k < N * S; k += 32) {
       dxg[r + k] = dXs[n * P + t];
+      n += q32;
+      t += r32;
+      if (t >= S) { t -= S; n++; }
     }
     __syncwarp();
   }
