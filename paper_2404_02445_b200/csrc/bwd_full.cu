@@ -122,17 +122,22 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
     float mu = 0.f, kap = 0.f, nu2 = 0.f, x0 = 0.f, m1 = 0.f;
     if (valid) {
       const float* xr = Xs + i * P;
+      float* zr = dXs + i * P;   // z rows for the Gram (dXs is first written at a6)
       x0 = xr[0];
       float s1 = 0.f;
       for (int t = 0; t < S; t++) s1 += xr[t] - x0;
       m1 = s1 * a.inv_s;
       mu = x0 + m1;
       float q = 0.f, k3 = 0.f;
+      // z (Def 4) formed once into the dX buffer for the Gram below, 0 past S up to the
+      // float4 chunk end (the a6 / dz steps keep forming z_j from X_j, exactly as before)
       for (int t = 0; t < S; t++) {
         const float z = (xr[t] - x0) - m1;
+        zr[t] = z;
         q = fmaf(z, z, q);
         k3 = fmaf((float)t - a.half_s, z, k3);
       }
+      for (int t = S; t < 4 * S4; t++) zr[t] = 0.f;
       nu2 = q;
       kap = k3 * a.inv_v;
     }
@@ -162,17 +167,12 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
       if (valid)
         for (int q4 = 0; q4 < S4; q4++) {
           const int t0 = 4 * q4;
-          const float4 xi = ld4(Xs + i * P + t0);
-          const float z0 = (xi.x - x0) - m1, z1 = t0 + 1 < S ? (xi.y - x0) - m1 : 0.f;
-          const float z2 = t0 + 2 < S ? (xi.z - x0) - m1 : 0.f;
-          const float z3 = t0 + 3 < S ? (xi.w - x0) - m1 : 0.f;
+          const float4 zi = ld4(dXs + i * P + t0);   // z rows, 0 past S
 #pragma unroll
           for (int j = 0; j < 32; j++) {
             if (j >= N) break;
-            const float4 xj = ld4(Xs + j * P + t0);
-            const float aj = x0v[j], bj = m1v[j];
-            G[j] = fmaf(z0, (xj.x - aj) - bj, fmaf(z1, (xj.y - aj) - bj,
-                   fmaf(z2, (xj.z - aj) - bj, fmaf(z3, (xj.w - aj) - bj, G[j]))));
+            const float4 zj = ld4(dXs + j * P + t0);
+            G[j] = fmaf(zi.x, zj.x, fmaf(zi.y, zj.y, fmaf(zi.z, zj.z, fmaf(zi.w, zj.w, G[j]))));
           }
         }
 #pragma unroll
@@ -316,11 +316,12 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
         float4 v = ld4(dXs + i * P + t0);
         const float4 xi = ld4(Xs + i * P + t0);
         const float dmS = dmu * a.inv_s;
+        const float dkv = dkap / V;
         float4 dz;
-        dz.x = fmaf(2.f * ((xi.x - x0) - m1), dnu2, ((float)t0 - a.half_s) * dkap / V);
-        dz.y = fmaf(2.f * ((xi.y - x0) - m1), dnu2, ((float)(t0 + 1) - a.half_s) * dkap / V);
-        dz.z = fmaf(2.f * ((xi.z - x0) - m1), dnu2, ((float)(t0 + 2) - a.half_s) * dkap / V);
-        dz.w = fmaf(2.f * ((xi.w - x0) - m1), dnu2, ((float)(t0 + 3) - a.half_s) * dkap / V);
+        dz.x = fmaf(2.f * ((xi.x - x0) - m1), dnu2, ((float)t0 - a.half_s) * dkv);
+        dz.y = fmaf(2.f * ((xi.y - x0) - m1), dnu2, ((float)(t0 + 1) - a.half_s) * dkv);
+        dz.z = fmaf(2.f * ((xi.z - x0) - m1), dnu2, ((float)(t0 + 2) - a.half_s) * dkv);
+        dz.w = fmaf(2.f * ((xi.w - x0) - m1), dnu2, ((float)(t0 + 3) - a.half_s) * dkv);
 #pragma unroll
         for (int j = 0; j < 32; j++) {
           if (j >= N) break;
