@@ -54,7 +54,9 @@ for L, S, H, mv, rev, ma in [(720, 24, 336, 4, False, 0), (720, 24, 336, 7, True
                              (720, 24, 336, 0, False, 25), (97, 7, 13, 6, True, 3),
                              (384, 128, 200, 7, True, 9), (1440, 24, 96, 4, True, 0),
                              (1536, 12, 200, 7, False, 0), (1440, 24, 96, 7, True, 5),
-                             (700, 200, 450, 3, True, 9)]:
+                             (700, 200, 450, 3, True, 9),
+                             # round 2: the tc_quad COMP instantiation (full rows, tail rows)
+                             (720, 24, 720, 6, True, 0), (480, 24, 200, 5, False, 0)]:
     x = torch.from_numpy(synth.random_windows(5, 3, L)).cuda()
     N, _, M = synth.derived_dims(L, S, H)
     ws, wt, b = synth.make_params(3, M, N, H)
