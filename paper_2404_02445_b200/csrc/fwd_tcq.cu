@@ -91,6 +91,7 @@ static_assert(kQGroup % 16 == 0, "16-byte aligned tiles");
 
 constexpr uint32_t kIdGram = idesc_f16(128, 128, false, false);
 constexpr uint32_t kIdFold = idesc_f16(128, 32, false, false);
+constexpr uint32_t kIdFold16 = idesc_f16(128, 16, false, false);   // M <= 16: one head m-tile
 
 // 8 consecutive fp32 -> 16-byte fp16 hi and lo rows (v = hi + lo)
 __device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
@@ -118,12 +119,16 @@ __device__ __forceinline__ void sts128(unsigned char* p, uint4 v) {
 // alpha = (Q_t - Q_s) mu^, beta = (d0 Q_t - d1 Q_s) kappa^ (exact in real arithmetic).  The fold
 // writes Q_s and Q_t into separate TMEM columns; the head multiplies Q_s by [X' | mu^ sx,
 // kappa^ sx] (a 4th n-tile) and Q_t by the 4th n-tile only.
-template <int NC, bool WIDE, bool DUMP = false, bool BF = false, bool COMP = false>
+// MTL: head m-tiles of 16 future segments, 2 (M <= 32) or 1 (M <= 16: the fold's N, the Q'
+// read-back, the head MMAs and the epilogue halve)
+template <int NC, bool WIDE, bool DUMP = false, bool BF = false, bool COMP = false, int MTL = 2>
 __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ctas_per_channel) {
   // WIDE: the SURVEY §8(f) widening (detrended seasonal metric, instance normalisation) is
   // compiled in; the plain instantiation is exactly the reading's kernel
   const bool detrend = WIDE && a.detrend, revin = WIDE && a.revin;
   static_assert(!COMP || (WIDE && !BF && !DUMP), "COMP: the widened fp32 instantiation");
+  static_assert(MTL == 2 || (MTL == 1 && !COMP && !DUMP), "MTL = 1: the plain / widened forward");
+  constexpr uint32_t kIdF = MTL == 1 ? kIdFold16 : kIdFold;
   constexpr int XT = COMP ? kQXTComp : kQXT;          // X' tile per group
   constexpr int XW = XT / 4;                          // per warp: 3 (4 with COMP) n-blocks
   constexpr int GRP = COMP ? kQGroupComp : kQGroup;
@@ -607,9 +612,9 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
         // COMP: Q_s^T (ks 0, 1: A_s) in [64, 96), Q_t^T (ks 2, 3: A_t) in [96, 128)
         const uint32_t dq = tcol + ((COMP && ks >= 2) ? 96u : 64u);
         const bool acc0 = COMP ? (ks & 1) != 0 : ks > 0;
-        umma_ts(dq, tcol + 8u * ks, bh, kIdFold, acc0);
-        umma_ts(dq, tcol + 8u * ks, bl, kIdFold, true);
-        umma_ts(dq, tcol + 32u + 8u * ks, bh, kIdFold, true);
+        umma_ts(dq, tcol + 8u * ks, bh, kIdF, acc0);
+        umma_ts(dq, tcol + 8u * ks, bl, kIdF, true);
+        umma_ts(dq, tcol + 32u + 8u * ks, bh, kIdF, true);
       }
       umma_commit(mbar + 1);
     }
@@ -619,18 +624,23 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
     // (rows j, columns m) in the mma accumulator layout; split to fp16 hi/lo and transposed
     // in registers (movmatrix), block (j-half h, j-octet v, m-octet k) is A-fragment
     // register (k & 1) + 2v of tile (m-tile k / 2, k-tile h).  No shared-memory round trip.
-    uint32_t qah[2][2][4], qal[2][2][4];   // [mt][kt][reg]
+    uint32_t qah[MTL][2][4], qal[MTL][2][4];   // [mt][kt][reg]
     auto load_q = [&](uint32_t qcol) {
-      uint32_t r0[16], r1[16];
-      tld16_x4(tcol + ((uint32_t)(32 * s) << 16) + qcol, r0);
-      tld16_x4(tcol + ((uint32_t)(32 * s + 16) << 16) + qcol, r1);
+      uint32_t r0[8 * MTL], r1[8 * MTL];
+      if constexpr (MTL == 2) {
+        tld16_x4(tcol + ((uint32_t)(32 * s) << 16) + qcol, r0);
+        tld16_x4(tcol + ((uint32_t)(32 * s + 16) << 16) + qcol, r1);
+      } else {
+        tld16_x2(tcol + ((uint32_t)(32 * s) << 16) + qcol, r0);
+        tld16_x2(tcol + ((uint32_t)(32 * s + 16) << 16) + qcol, r1);
+      }
       tld_wait();
 #pragma unroll
       for (int h = 0; h < 2; h++)
 #pragma unroll
         for (int v = 0; v < 2; v++)
 #pragma unroll
-          for (int k = 0; k < 4; k++) {
+          for (int k = 0; k < 2 * MTL; k++) {
             const uint32_t* r = h ? r1 : r0;
             uint32_t hi, lo;
             split2(make_float2(__uint_as_float(r[4 * k + 2 * v]), __uint_as_float(r[4 * k + 2 * v + 1])),
@@ -647,9 +657,9 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
       __syncwarp();
       const int l8 = lane & 7, g4 = lane >> 3;
       const unsigned char* xs = xt + XW * s;
-      float acc[2][3][4];
+      float acc[MTL][3][4];
 #pragma unroll
-      for (int mt = 0; mt < 2; mt++)
+      for (int mt = 0; mt < MTL; mt++)
 #pragma unroll
         for (int nt = 0; nt < 3; nt++)
 #pragma unroll
@@ -671,15 +681,15 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
         }
         // product-major: 6 independent accumulators between dependent MMAs
 #pragma unroll
-        for (int mt = 0; mt < 2; mt++)
+        for (int mt = 0; mt < MTL; mt++)
 #pragma unroll
           for (int nt = 0; nt < 3; nt++) mma16816_nv(acc[mt][nt], qal[mt][kt], xh[nt][0], xh[nt][1]);
 #pragma unroll
-        for (int mt = 0; mt < 2; mt++)
+        for (int mt = 0; mt < MTL; mt++)
 #pragma unroll
           for (int nt = 0; nt < 3; nt++) mma16816_nv(acc[mt][nt], qah[mt][kt], xl[nt][0], xl[nt][1]);
 #pragma unroll
-        for (int mt = 0; mt < 2; mt++)
+        for (int mt = 0; mt < MTL; mt++)
 #pragma unroll
           for (int nt = 0; nt < 3; nt++) mma16816_nv(acc[mt][nt], qah[mt][kt], xh[nt][0], xh[nt][1]);
       }
@@ -688,7 +698,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
         float ce[2][2][4];   // [Q_s, Q_t][mt][e]
         auto ext = [&](float (&c4)[2][4]) {
 #pragma unroll
-          for (int mt = 0; mt < 2; mt++)
+          for (int mt = 0; mt < MTL; mt++)
 #pragma unroll
             for (int e = 0; e < 4; e++) c4[mt][e] = 0.f;
 #pragma unroll
@@ -698,7 +708,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
             ldsm_x2_t(b0h, b1h, p3);
             ldsm_x2_t(b0l, b1l, p3 + 512);
 #pragma unroll
-            for (int mt = 0; mt < 2; mt++) {
+            for (int mt = 0; mt < MTL; mt++) {
               mma16816_nv(c4[mt], qal[mt][kt], b0h, b1h);
               mma16816_nv(c4[mt], qah[mt][kt], b0l, b1l);
               mma16816_nv(c4[mt], qah[mt][kt], b0h, b1h);
@@ -713,7 +723,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
         const float d0 = a.vtrend != 0.f ? 1.f : 0.f, d1 = detrend ? 1.f : 0.f;
         const int src = lane & ~3;
 #pragma unroll
-        for (int mt = 0; mt < 2; mt++)
+        for (int mt = 0; mt < MTL; mt++)
 #pragma unroll
           for (int h = 0; h < 2; h++) {
             const float al = __shfl_sync(0xffffffffu, ce[1][mt][2 * h] - ce[0][mt][2 * h], src);
@@ -735,7 +745,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
       const float* bq = bS + 2 * (lane & 3);
       if (full_rows) {   // H = 24 M, H even: every (m < M, t) pair is stored, no tail
 #pragma unroll
-        for (int mt = 0; mt < 2; mt++)
+        for (int mt = 0; mt < MTL; mt++)
 #pragma unroll
           for (int h = 0; h < 2; h++) {
             const int m = 16 * mt + 8 * h + (lane >> 2);
@@ -762,7 +772,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
           }
       } else {
 #pragma unroll
-        for (int mt = 0; mt < 2; mt++)
+        for (int mt = 0; mt < MTL; mt++)
 #pragma unroll
           for (int h = 0; h < 2; h++) {
             const int m = 16 * mt + 8 * h + (lane >> 2);
@@ -860,9 +870,9 @@ bool plan_tcq_kernel(const FwdArgs& a, int max_smem_optin, int sm_count, TcqPlan
   return true;
 }
 
-template <int NC, bool WIDE, bool DUMP = false, bool BF = false, bool COMP = false>
+template <int NC, bool WIDE, bool DUMP = false, bool BF = false, bool COMP = false, int MTL = 2>
 static cudaError_t launch_tcq_t(const FwdArgs& a, const TcqPlan& p, cudaStream_t st) {
-  auto k = prnet_fwd_tcq_kernel<NC, WIDE, DUMP, BF, COMP>;
+  auto k = prnet_fwd_tcq_kernel<NC, WIDE, DUMP, BF, COMP, MTL>;
   cudaError_t e =
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_bytes);
   if (e != cudaSuccess) return e;
@@ -885,6 +895,13 @@ cudaError_t launch_tcq_kernel(const FwdArgs& a, const TcqPlan& p, cudaStream_t s
     return a.N == 30 ? launch_tcq_t<30, true, false, false, true>(a, p, st)
                      : launch_tcq_t<0, true, false, false, true>(a, p, st);
   const bool wide = a.detrend || a.revin;
+  if (a.M <= 16) {   // one head m-tile (e.g. Electricity H = 336, Weather H = 96)
+    if (a.N == 30)
+      return wide ? launch_tcq_t<30, true, false, false, false, 1>(a, p, st)
+                  : launch_tcq_t<30, false, false, false, false, 1>(a, p, st);
+    return wide ? launch_tcq_t<0, true, false, false, false, 1>(a, p, st)
+                : launch_tcq_t<0, false, false, false, false, 1>(a, p, st);
+  }
   if (a.N == 30) return wide ? launch_tcq_t<30, true>(a, p, st) : launch_tcq_t<30, false>(a, p, st);
   return wide ? launch_tcq_t<0, true>(a, p, st) : launch_tcq_t<0, false>(a, p, st);
 }

@@ -81,6 +81,12 @@ __device__ __forceinline__ void tld16_x4(uint32_t taddr, uint32_t (&r)[16]) {
       : PRNET_TLD_R8(r, 0), PRNET_TLD_R8(r, 8)
       : "r"(taddr));
 }
+// the first two 8-column groups of tld16_x4 (r[4k + 2v + e], k < 2)
+__device__ __forceinline__ void tld16_x2(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : PRNET_TLD_R8(r, 0)
+               : "r"(taddr));
+}
 __device__ __forceinline__ void tst16_x2(uint32_t taddr, const uint32_t (&r)[8]) {
   asm volatile(
       "tcgen05.st.sync.aligned.16x256b.x2.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
