@@ -62,6 +62,7 @@ struct TcgCfg {
 constexpr uint32_t kIdGramG = idesc_f16(128, 128, false, false);
 constexpr uint32_t kIdFoldG = idesc_f16(128, 32, false, false);
 constexpr uint32_t kIdFoldG64 = idesc_f16(128, 64, false, false);
+constexpr uint32_t kIdFoldG16 = idesc_f16(128, 16, false, false);   // M <= 16: one head m-tile
 
 __device__ __forceinline__ void sts128(unsigned char* p, uint4 v) {
   *reinterpret_cast<uint4*>(p) = v;
@@ -434,7 +435,7 @@ __global__ void __launch_bounds__(128 * TcgCfg<S, M64>::MAXG, 1) prnet_fwd_tcg_k
       for (int ks = 0; ks < 4; ks++) {
         const uint64_t bh = sdesc(w_s + ks * 256, 128, 2048);
         const uint64_t bl = sdesc(w_s + (8 + 2 * ks) * 128, 128, 2048);
-        constexpr uint32_t idf = M64 ? kIdFoldG64 : kIdFoldG;
+        const uint32_t idf = M64 ? kIdFoldG64 : (M <= 16 ? kIdFoldG16 : kIdFoldG);
         umma_ts(tcol + 64u, tcol + 8u * ks, bh, idf, ks > 0);
         umma_ts(tcol + 64u, tcol + 8u * ks, bl, idf, true);
         umma_ts(tcol + 64u, tcol + 32u + 8u * ks, bh, idf, true);
@@ -454,7 +455,26 @@ __global__ void __launch_bounds__(128 * TcgCfg<S, M64>::MAXG, 1) prnet_fwd_tcg_k
       const int m0 = 32 * mp;
       const bool two_mt = M > m0 + 16;
       uint32_t qah[2][2][4], qal[2][2][4];   // [mt][kt][reg]
-      {
+      if (!M64 && !two_mt) {
+        // M <= 16 (one m-tile; the fold wrote 16 columns): the first two 8-column groups only
+        uint32_t r0[8], r1[8];
+        tld16_x2(tcol + ((uint32_t)(32 * s) << 16) + 64u, r0);
+        tld16_x2(tcol + ((uint32_t)(32 * s + 16) << 16) + 64u, r1);
+        tld_wait();
+#pragma unroll
+        for (int h = 0; h < 2; h++)
+#pragma unroll
+          for (int v = 0; v < 2; v++)
+#pragma unroll
+            for (int k = 0; k < 2; k++) {
+              const uint32_t* r = h ? r1 : r0;
+              uint32_t hi, lo;
+              split2(make_float2(__uint_as_float(r[4 * k + 2 * v]), __uint_as_float(r[4 * k + 2 * v + 1])),
+                     hi, lo);
+              qah[0][h][(k & 1) + 2 * v] = movm_t(hi);
+              qal[0][h][(k & 1) + 2 * v] = movm_t(lo);
+            }
+      } else {
         uint32_t r0[16], r1[16];
         tld16_x4(tcol + ((uint32_t)(32 * s) << 16) + 64u + 32u * mp, r0);
         tld16_x4(tcol + ((uint32_t)(32 * s + 16) << 16) + 64u + 32u * mp, r1);
