@@ -69,12 +69,14 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
   float* As = dXs + 32 * P;                 // [32][Q] A_s, then drho
   float* At = As + 32 * Q;                  // [32][Q] A_t, then dD
   float* Rh = At + 32 * Q;                  // [32][Q] rho
-  float* Dm = Rh + 32 * Q;                  // [32][Q] D
-  float* dYs = Dm + 32 * Q;                 // [M][P]
-  float* muv = dYs + M * P;                 // [32] mu_j
+  // dY [M][P] lives in the dX buffer between the Gram (its z rows) and the aggregation
+  // adjoint (dX), and D_ij is recomputed from (mu_j, kappa_j): 8 warps per SM instead of 6
+  float* dYs = dXs;
+  float* muv = Rh + 32 * Q;                 // [32] mu_j
   float* gv = muv + 32;                     // [32] g_j = (nu2_j + eps_s)^(-1/2)
   float* x0v = gv + 32;                     // [32] x0_j (z_j = (X_j - x0_j) - m1_j, as Def 4's
   float* m1v = x0v + 32;                    // [32] m1_j  forward: no cancellation against mu)
+  float* kv = m1v + 32;                     // [32] kappa_j
   {
     const float* gs = a.ws + (int64_t)cw * M * N;
     const float* gt = a.wt + (int64_t)cw * M * N;
@@ -86,7 +88,6 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
     }
   }
   for (int k = lane; k < 32 * P; k += 32) Xs[k] = 0.f;   // padding stays 0
-  for (int k = lane; k < M * P; k += 32) dYs[k] = 0.f;
   __syncthreads();
   float dts = 0.f, dtt = 0.f;               // lane partials of dL/dtau_s, dL/dtau_t
   const int i = lane;
@@ -110,12 +111,6 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
       n += q32;
       t += r32;
       if (t >= S) { t -= S; n++; }
-    }
-    for (int k = lane, m = n_l, t = t_l; k < H; k += 32) {
-      dYs[m * P + t] = __ldg(dyg + k);
-      m += q32;
-      t += r32;
-      if (t >= S) { t -= S; m++; }
     }
     __syncwarp();
     // ---------------- forward recompute (Def 3-8), FP32
@@ -142,6 +137,7 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
       kap = k3 * a.inv_v;
     }
     muv[i] = mu;
+    kv[i] = kap;
     x0v[i] = x0;
     m1v[i] = m1;
     const float m0 = shfl(mu, 0);
@@ -184,17 +180,25 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
           const float dm = mu - muv[j], dk = kap - kj;
           const float D = fmaf(w * dk, dk, dm * dm);
           Rh[i * Q + j] = rho;
-          Dm[i * Q + j] = D;
           lmax_s = fmaxf(lmax_s, rho * its);
           lmax_t = fmaxf(lmax_t, -D * ct);
         }
       }
     }
+    __syncwarp();   // every lane has read the z rows (the Gram): the dX buffer takes dY [M][P]
+    for (int m = 0; m < M; m++)
+      for (int t = lane; t < P; t += 32) {
+        const int h = m * S + t;
+        dYs[m * P + t] = (t < S && h < H) ? __ldg(dyg + h) : 0.f;
+      }
+    __syncwarp();
     if (valid) {
       float ls = 0.f, lt = 0.f;
       for (int j = 0; j < N; j++) {
+        const float dm = mu - muv[j], dk = kap - kv[j];
+        const float D = fmaf(w * dk, dk, dm * dm);   // as in the Gram loop (same operations)
         const float es = __expf(Rh[i * Q + j] * its - lmax_s);
-        const float et = __expf(-Dm[i * Q + j] * ct - lmax_t);
+        const float et = __expf(-D * ct - lmax_t);
         As[i * Q + j] = es;
         At[i * Q + j] = et;
         ls += es;
@@ -264,7 +268,8 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
         if (j < N) {
           const float dls = As[i * Q + j] * (dAs[j] - ss);
           const float dlt = At[i * Q + j] * (dAt[j] - st);
-          const float rho = Rh[i * Q + j], D = Dm[i * Q + j];
+          const float dm = mu - muv[j], dk = kap - kv[j];
+          const float rho = Rh[i * Q + j], D = fmaf(w * dk, dk, dm * dm);
           dts -= dls * (rho - rref) * its2;
           dtt += dlt * D * ctt;      // dlt Dhat / tau_t^2
           const float dDh = -dlt * itt;
@@ -380,7 +385,7 @@ bool plan_bwd_full(const FwdArgs& a, int max_smem_optin, BwdFullPlan* p) {
   if (((P / 4) & 1) == 0) P += 4;          // P / 4 odd: conflict-free own-row float4 reads
   ly.pitch = P;
   ly.mpad = a.M | 1;                        // odd: W^T row reads by 32 lanes are conflict-free
-  ly.per_warp = ((4 * 32 * P + 4 * 32 * 33 + a.M * P + 128) + 3) & ~3;
+  ly.per_warp = ((4 * 32 * P + 3 * 32 * 33 + 160) + 3) & ~3;
   const size_t cta = (size_t)2 * 32 * ly.mpad * 4 + 16 * 4;
   int w = 8;
   while (w > 1 && cta + (size_t)w * ly.per_warp * 4 > (size_t)max_smem_optin) w--;
