@@ -451,7 +451,11 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
     tc_fence_before();
     named_bar(1 + grp, 128);
     tc_fence_after();
+#ifndef PRNET_TCQ_ABL
+#define PRNET_TCQ_ABL 0   // ablation builds only (invalid results): 1 = no Gram MMAs, 2 = no fold MMAs
+#endif
     if (mma_warp && elect_one()) {
+      if (!(PRNET_TCQ_ABL & 1)) {
       // 5 K-steps of 2 chunks (c, c + LBO/128) cover hh + hl + lh with no zero K-step:
       // (h0 h1)(h0 h1), (h2 0)(h2 0), (h0 h1)(l0 l1), (l0 l1)(h0 h1), (h2 l2)(l2 h2')
       umma(tcol, sdesc(zq_s, 128, 1024), sdesc(zq_s, 128, 1024), kIdGram, false);
@@ -459,6 +463,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
       umma(tcol, sdesc(zq_s, 128, 1024), sdesc(zq_s + 384, 128, 1024), kIdGram, true);
       umma(tcol, sdesc(zq_s + 384, 128, 1024), sdesc(zq_s, 128, 1024), kIdGram, true);
       umma(tcol, sdesc(zq_s + 256, 384, 1024), sdesc(zq_s + 640, 128, 1024), kIdGram, true);
+      }
       umma_commit(mbar);
     }
     // X' rows -> head B tile (read only by the head, after the next barrier)
@@ -606,7 +611,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
     tc_fence_after();
     if (mma_warp && elect_one()) {
 #pragma unroll
-      for (int ks = 0; ks < 4; ks++) {
+      for (int ks = 0; ks < ((PRNET_TCQ_ABL & 2) ? 0 : 4); ks++) {
         const uint64_t bh = sdesc(w_s + ks * 256, 128, 2048);
         const uint64_t bl = sdesc(w_s + (8 + 2 * ks) * 128, 128, 2048);
         // COMP: Q_s^T (ks 0, 1: A_s) in [64, 96), Q_t^T (ks 2, 3: A_t) in [96, 128)
