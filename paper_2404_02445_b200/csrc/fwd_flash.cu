@@ -25,15 +25,24 @@ namespace prnet {
 
 namespace {
 
-__device__ __forceinline__ float block_reduce(float v, float* scratch, bool is_max) {
+// two block reductions for the price of one pair of barriers (scratch holds 2 nw floats)
+__device__ __forceinline__ void block_reduce2(float& u, float& v, float* scratch, bool is_max) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  u = is_max ? warp_max(u) : warp_sum(u);
   v = is_max ? warp_max(v) : warp_sum(v);
   __syncthreads();
-  if (lane == 0) scratch[warp] = v;
+  if (lane == 0) {
+    scratch[2 * warp] = u;
+    scratch[2 * warp + 1] = v;
+  }
   __syncthreads();
-  float r = is_max ? 0.f : 0.f;
-  for (int w = 0; w < nw; w++) r = is_max ? fmaxf(r, scratch[w]) : r + scratch[w];
-  return r;
+  float ru = 0.f, rv = 0.f;
+  for (int w = 0; w < nw; w++) {
+    ru = is_max ? fmaxf(ru, scratch[2 * w]) : ru + scratch[2 * w];
+    rv = is_max ? fmaxf(rv, scratch[2 * w + 1]) : rv + scratch[2 * w + 1];
+  }
+  u = ru;
+  v = rv;
 }
 
 // A-fragment (16 x 16, rows r0.., cols c0..) of a row-major global fp16 matrix
@@ -179,9 +188,13 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
       // |z| <= 2 max|d|; detrended (metric_variant bit 1): |e| <= |z| + |kappa| (S-1)/2
       dmx = fmaxf(dmx, 2.f * dm + (a.detrend ? fabsf(c_ka[n]) * half_s : 0.f));
     }
-    const float sx = pow2_scale(block_reduce(amx, scr, true));
-    const float sz = pow2_scale(block_reduce(dmx, scr, true));
-    float musum = 0.f;
+    block_reduce2(amx, dmx, scr, true);
+    const float sx = pow2_scale(amx);
+    const float sz = pow2_scale(dmx);
+    // Def 5 in one reduction about the reference m0 = mu_0 (as tc_quad): with d = mu - m0,
+    // sum (mu - mubar)^2 = sum d^2 - (sum d)^2 / N
+    const float m0 = xbuf[0] + c_nu[0];
+    float dsum1 = 0.f, dsum2 = 0.f;
     for (int n = tid; n < N; n += nthr) {
       const float* xr = xbuf + n * S;
       const float x0 = xr[0], m1 = c_nu[n];
@@ -199,17 +212,15 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
       const float mu = x0 + m1;
       c_mu[n] = mu;        // temporarily mu
       c_inv[n] = q;        // temporarily nu2
-      musum += mu;
-    }
-    const float mbar = block_reduce(musum, scr, false) * a.inv_n;
-    float dsum = 0.f;
-    for (int n = tid; n < N; n += nthr) {
-      const float d = c_mu[n] - mbar;
       // Def 5 uses |z|^2 = |e|^2 + kappa^2 V when the seasonal metric is detrended
-      const float nz2 = a.detrend ? fmaf(c_ka[n] * c_ka[n], 1.f / a.inv_v, c_inv[n]) : c_inv[n];
-      dsum += nz2 + (float)S * d * d;
+      const float nz2 = a.detrend ? fmaf(c_ka[n] * c_ka[n], 1.f / a.inv_v, q) : q;
+      const float d = mu - m0;
+      dsum1 += d;
+      dsum2 += fmaf((float)S * d, d, nz2);
     }
-    const float var = block_reduce(dsum, scr, false) * a.inv_ns;
+    block_reduce2(dsum1, dsum2, scr, false);
+    const float mbar = fmaf(dsum1, a.inv_n, m0);
+    const float var = fmaf(-(float)S * dsum1, dsum1 * a.inv_n, dsum2) * a.inv_ns;
     // instance normalisation: descriptors of xhat = (x - mu_r) rr are
     // affine images of those of x; the head runs on x and a8 adds mu_r (1 - w1[m]) + sr b
     float mu_r = 0.f, rr = 1.f, sr = 1.f;
