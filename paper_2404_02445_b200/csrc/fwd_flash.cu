@@ -170,83 +170,130 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
     // descriptor passes (the second hits L1/L2): no shared staging, so a 480-segment series
     // fits two CTAs per SM
     const float* xbuf = a.x + b * a.xsb + c * a.xsc + a.r;
-    // ---------------- a2: descriptors (Def 4-5), thread per segment
-    float amx = 0.f, dmx = 0.f;
-    for (int n = tid; n < N; n += nthr) {
-      const float* xr = xbuf + n * S;
-      const float x0 = xr[0];
-      float s1 = 0.f, s3 = 0.f, dm = 0.f;
-      for (int t = 0; t < S; t++) {
-        const float d = xr[t] - x0;
-        s1 += d;
-        s3 = fmaf((float)t - half_s, d, s3);
-        amx = fmaxf(amx, fabsf(xr[t]));
-        dm = fmaxf(dm, fabsf(d));
+    // KS >= 2 (S > 16): the descriptor passes with tps threads per segment; S <= 16 keeps one
+    // thread per segment (measured: L720/S12 1.18 ms against 1.27-1.39 with the grouped form)
+    float sx, sz, mu_r, rr, sr, cmt, ckt;
+    int loose;
+    if constexpr (KS >= 2) {
+      // ---------------- a2: descriptors (Def 4-5), tps threads per segment (the largest power of
+      // two <= 8 with N tps <= the CTA's threads and S / tps >= 8): thread r of a segment's group takes t = r, r +
+      // tps, .., the segment's sums and maxima by xor shuffles inside the group; the group's
+      // leader (r = 0) writes the per-segment scalars.  (Thread per segment left 3/4 of the CTA
+      // idle at N = 60 behind three serial S-long passes.)
+      // (and >= 8 elements per thread: at S = 12 the group shuffles cost more than they save,
+      // measured L720/S12 1.27 vs 1.18 ms with 4 threads per segment)
+      int tps = 1;
+      while (tps < 8 && N * tps * 2 <= nthr && S >= 16 * tps) tps <<= 1;
+      const int gsz = nthr / tps, nl = tid / tps, rr_ = tid - nl * tps;
+      auto gsum = [&](float v) {
+        for (int o = 1; o < tps; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        return v;
+      };
+      auto gmax = [&](float v) {
+        for (int o = 1; o < tps; o <<= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        return v;
+      };
+      float amx = 0.f, dmx = 0.f;
+      for (int base = 0; base < N; base += gsz) {   // CTA-uniform trip count (shuffles)
+        const int n = base + nl;
+        const bool on = n < N;
+        float s1 = 0.f, s3 = 0.f, dm = 0.f;
+        if (on) {
+          const float* xr = xbuf + n * S;
+          const float x0 = xr[0];
+          for (int t = rr_; t < S; t += tps) {
+            const float d = xr[t] - x0;
+            s1 += d;
+            s3 = fmaf((float)t - half_s, d, s3);
+            amx = fmaxf(amx, fabsf(xr[t]));
+            dm = fmaxf(dm, fabsf(d));
+          }
+        }
+        s1 = gsum(s1);
+        s3 = gsum(s3);
+        dm = gmax(dm);
+        if (on) {
+          const float ka = s3 * a.inv_v;
+          if (rr_ == 0) {
+            c_nu[n] = s1 * a.inv_s;          // m1 (mu - x0)
+            c_ka[n] = ka;                    // kappa
+          }
+          // |z| <= 2 max|d|; detrended (metric_variant bit 1): |e| <= |z| + |kappa| (S-1)/2
+          dmx = fmaxf(dmx, 2.f * dm + (a.detrend ? fabsf(ka) * half_s : 0.f));
+        }
       }
-      c_nu[n] = s1 * a.inv_s;          // m1 (mu - x0)
-      c_ka[n] = s3 * a.inv_v;          // kappa
-      // |z| <= 2 max|d|; detrended (metric_variant bit 1): |e| <= |z| + |kappa| (S-1)/2
-      dmx = fmaxf(dmx, 2.f * dm + (a.detrend ? fabsf(c_ka[n]) * half_s : 0.f));
-    }
-    block_reduce2(amx, dmx, scr, true);
-    const float sx = pow2_scale(amx);
-    const float sz = pow2_scale(dmx);
-    // Def 5 in one reduction about the reference m0 = mu_0 (as tc_quad): with d = mu - m0,
-    // sum (mu - mubar)^2 = sum d^2 - (sum d)^2 / N
-    const float m0 = xbuf[0] + c_nu[0];
-    float dsum1 = 0.f, dsum2 = 0.f;
-    for (int n = tid; n < N; n += nthr) {
-      const float* xr = xbuf + n * S;
-      const float x0 = xr[0], m1 = c_nu[n];
-      const float kd = a.detrend ? c_ka[n] : 0.f;   // e = z - kappa t~
-      float q = 0.f;
-      for (int t = 0; t < S; t++) {
-        const float v = xr[t];
-        const float z = fmaf(-kd, (float)t - half_s, (v - x0) - m1);
-        q = fmaf(z, z, q);
-        __half h, l;
-        split1(v * sx, h, l);
-        x_hi[n * XP + t] = h;
-        x_lo[n * XP + t] = l;
+      block_reduce2(amx, dmx, scr, true);
+      sx = pow2_scale(amx);
+      sz = pow2_scale(dmx);
+      // Def 5 in one reduction about the reference m0 = mu_0 (as tc_quad): with d = mu - m0,
+      // sum (mu - mubar)^2 = sum d^2 - (sum d)^2 / N
+      const float m0 = xbuf[0] + c_nu[0];
+      float dsum1 = 0.f, dsum2 = 0.f;
+      for (int base = 0; base < N; base += gsz) {
+        const int n = base + nl;
+        const bool on = n < N;
+        float q = 0.f, x0 = 0.f, m1 = 0.f, ka = 0.f;
+        if (on) {
+          const float* xr = xbuf + n * S;
+          x0 = xr[0];
+          m1 = c_nu[n];
+          ka = c_ka[n];
+          const float kd = a.detrend ? ka : 0.f;   // e = z - kappa t~
+          for (int t = rr_; t < S; t += tps) {
+            const float v = xr[t];
+            const float z = fmaf(-kd, (float)t - half_s, (v - x0) - m1);
+            q = fmaf(z, z, q);
+            __half h, l;
+            split1(v * sx, h, l);
+            x_hi[n * XP + t] = h;
+            x_lo[n * XP + t] = l;
+          }
+        }
+        q = gsum(q);
+        if (on && rr_ == 0) {
+          const float mu = x0 + m1;
+          c_mu[n] = mu;        // temporarily mu
+          c_inv[n] = q;        // temporarily nu2
+          // Def 5 uses |z|^2 = |e|^2 + kappa^2 V when the seasonal metric is detrended
+          const float nz2 = a.detrend ? fmaf(ka * ka, 1.f / a.inv_v, q) : q;
+          const float d = mu - m0;
+          dsum1 += d;
+          dsum2 += fmaf((float)S * d, d, nz2);
+        }
       }
-      const float mu = x0 + m1;
-      c_mu[n] = mu;        // temporarily mu
-      c_inv[n] = q;        // temporarily nu2
-      // Def 5 uses |z|^2 = |e|^2 + kappa^2 V when the seasonal metric is detrended
-      const float nz2 = a.detrend ? fmaf(c_ka[n] * c_ka[n], 1.f / a.inv_v, q) : q;
-      const float d = mu - m0;
-      dsum1 += d;
-      dsum2 += fmaf((float)S * d, d, nz2);
-    }
-    block_reduce2(dsum1, dsum2, scr, false);
-    const float mbar = fmaf(dsum1, a.inv_n, m0);
-    const float var = fmaf(-(float)S * dsum1, dsum1 * a.inv_n, dsum2) * a.inv_ns;
-    // instance normalisation: descriptors of xhat = (x - mu_r) rr are
-    // affine images of those of x; the head runs on x and a8 adds mu_r (1 - w1[m]) + sr b
-    float mu_r = 0.f, rr = 1.f, sr = 1.f;
-    if (a.revin) {
-      mu_r = mbar;
-      rr = rsqrtf(var + kEpsRevin);
-      sr = (var + kEpsRevin) * rr;
-    }
-    const float inv_var = 1.0f / fmaf(var * rr, rr, kEpsTrend);
-    const float cmt = sqrtf(inv_var * a.kt) * rr, ckt = sqrtf(a.vtrend * inv_var * a.kt) * rr;
-    // a row whose known bound f_n sits far above its true maximum (between f_n^2 and f_n:
-    // a segment with nu^2 not >> eps_s, e.g. constant to within rounding) would leave its
-    // largest exponential below 2^-6 at low tau_s, where the fp16 hi/lo split of E loses
-    // precision (and below 2^-24 it underflows): such series take exact row maxima (below)
-    int loose = 0;
-    for (int n = tid; n < NP; n += nthr) {
-      if (n < N) {
-        const float nu2 = c_inv[n] * rr * rr;
-        const float inv = rsqrtf(nu2 + kEpsSeasonal);
-        // row-normalised Gram operand Z'_n = z_n rr / sqrt(nu2_n rr^2 + eps_s) (|Z'_n| <= 1):
-        // the split keeps ~22 bits relative to every row, and the Gram is rho itself
-        {
+      block_reduce2(dsum1, dsum2, scr, false);
+      const float mbar = fmaf(dsum1, a.inv_n, m0);
+      const float var = fmaf(-(float)S * dsum1, dsum1 * a.inv_n, dsum2) * a.inv_ns;
+      // instance normalisation: descriptors of xhat = (x - mu_r) rr are
+      // affine images of those of x; the head runs on x and a8 adds mu_r (1 - w1[m]) + sr b
+      mu_r = 0.f, rr = 1.f, sr = 1.f;
+      if (a.revin) {
+        mu_r = mbar;
+        rr = rsqrtf(var + kEpsRevin);
+        sr = (var + kEpsRevin) * rr;
+      }
+      const float inv_var = 1.0f / fmaf(var * rr, rr, kEpsTrend);
+      cmt = sqrtf(inv_var * a.kt) * rr, ckt = sqrtf(a.vtrend * inv_var * a.kt) * rr;
+      // a row whose known bound f_n sits far above its true maximum (between f_n^2 and f_n:
+      // a segment with nu^2 not >> eps_s, e.g. constant to within rounding) would leave its
+      // largest exponential below 2^-6 at low tau_s, where the fp16 hi/lo split of E loses
+      // precision (and below 2^-24 it underflows): such series take exact row maxima (below)
+      loose = 0;
+      for (int base = 0; base < NP; base += gsz) {
+        const int n = base + nl;
+        const bool on = n < N;
+        float nu2 = 0.f, inv = 0.f, cmu = 0.f, cka = 0.f;
+        if (on) {
+          nu2 = c_inv[n] * rr * rr;
+          inv = rsqrtf(nu2 + kEpsSeasonal);
+          cmu = c_mu[n];
+          cka = c_ka[n];
+          // row-normalised Gram operand Z'_n = z_n rr / sqrt(nu2_n rr^2 + eps_s) (|Z'_n| <= 1):
+          // the split keeps ~22 bits relative to every row, and the Gram is rho itself
           const float* xr = xbuf + n * S;
           const float x0 = xr[0], m1 = c_nu[n], q = inv * rr;
-          const float kd = a.detrend ? c_ka[n] : 0.f;
-          for (int t = 0; t < S; t++) {
+          const float kd = a.detrend ? cka : 0.f;
+          for (int t = rr_; t < S; t += tps) {
             const float z = fmaf(-kd, (float)t - half_s, (xr[t] - x0) - m1);
             __half h, l;
             split1(z * q, h, l);
@@ -254,21 +301,128 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
             z_lo[n * ZP + t] = l;
           }
         }
-        c_inv[n] = 1.f;                // column factor of rho: 1 (row-normalised Gram)
-        c_max[n] = sqrtf(nu2) * inv;   // f_n: known row maximum of rho (Cauchy-Schwarz)
-        loose |= (c_max[n] - c_max[n] * c_max[n]) * a.ks > 6.f;
-        if (COMP) {
-          c_vm[n] = c_mu[n];
-          c_vk[n] = c_ka[n];
+        __syncwarp();   // the group has read the row's scalars: the leader rewrites them
+        if (rr_ == 0 && n < NP) {
+          if (on) {
+            c_inv[n] = 1.f;                // column factor of rho: 1 (row-normalised Gram)
+            c_max[n] = sqrtf(nu2) * inv;   // f_n: known row maximum of rho (Cauchy-Schwarz)
+            loose |= (c_max[n] - c_max[n] * c_max[n]) * a.ks > 6.f;
+            if (COMP) {
+              c_vm[n] = cmu;
+              c_vk[n] = cka;
+            }
+            c_mu[n] = (cmu - mu_r) * cmt;
+            c_ka[n] = cka * ckt;
+          } else {
+            c_inv[n] = 0.f;
+            c_max[n] = 0.f;
+            c_mu[n] = INFINITY;            // exponent -inf: masked key
+            c_ka[n] = 0.f;
+            if (COMP) c_vm[n] = c_vk[n] = 0.f;
+          }
         }
-        c_mu[n] = (c_mu[n] - mu_r) * cmt;
-        c_ka[n] = c_ka[n] * ckt;
-      } else {
-        c_inv[n] = 0.f;
-        c_max[n] = 0.f;
-        c_mu[n] = INFINITY;            // exponent -inf: masked key
-        c_ka[n] = 0.f;
-        if (COMP) c_vm[n] = c_vk[n] = 0.f;
+      }
+    } else {
+      // ---------------- a2: descriptors (Def 4-5), thread per segment
+      float amx = 0.f, dmx = 0.f;
+      for (int n = tid; n < N; n += nthr) {
+        const float* xr = xbuf + n * S;
+        const float x0 = xr[0];
+        float s1 = 0.f, s3 = 0.f, dm = 0.f;
+        for (int t = 0; t < S; t++) {
+          const float d = xr[t] - x0;
+          s1 += d;
+          s3 = fmaf((float)t - half_s, d, s3);
+          amx = fmaxf(amx, fabsf(xr[t]));
+          dm = fmaxf(dm, fabsf(d));
+        }
+        c_nu[n] = s1 * a.inv_s;          // m1 (mu - x0)
+        c_ka[n] = s3 * a.inv_v;          // kappa
+        // |z| <= 2 max|d|; detrended (metric_variant bit 1): |e| <= |z| + |kappa| (S-1)/2
+        dmx = fmaxf(dmx, 2.f * dm + (a.detrend ? fabsf(c_ka[n]) * half_s : 0.f));
+      }
+      block_reduce2(amx, dmx, scr, true);
+      sx = pow2_scale(amx);
+      sz = pow2_scale(dmx);
+      // Def 5 in one reduction about the reference m0 = mu_0 (as tc_quad): with d = mu - m0,
+      // sum (mu - mubar)^2 = sum d^2 - (sum d)^2 / N
+      const float m0 = xbuf[0] + c_nu[0];
+      float dsum1 = 0.f, dsum2 = 0.f;
+      for (int n = tid; n < N; n += nthr) {
+        const float* xr = xbuf + n * S;
+        const float x0 = xr[0], m1 = c_nu[n];
+        const float kd = a.detrend ? c_ka[n] : 0.f;   // e = z - kappa t~
+        float q = 0.f;
+        for (int t = 0; t < S; t++) {
+          const float v = xr[t];
+          const float z = fmaf(-kd, (float)t - half_s, (v - x0) - m1);
+          q = fmaf(z, z, q);
+          __half h, l;
+          split1(v * sx, h, l);
+          x_hi[n * XP + t] = h;
+          x_lo[n * XP + t] = l;
+        }
+        const float mu = x0 + m1;
+        c_mu[n] = mu;        // temporarily mu
+        c_inv[n] = q;        // temporarily nu2
+        // Def 5 uses |z|^2 = |e|^2 + kappa^2 V when the seasonal metric is detrended
+        const float nz2 = a.detrend ? fmaf(c_ka[n] * c_ka[n], 1.f / a.inv_v, q) : q;
+        const float d = mu - m0;
+        dsum1 += d;
+        dsum2 += fmaf((float)S * d, d, nz2);
+      }
+      block_reduce2(dsum1, dsum2, scr, false);
+      const float mbar = fmaf(dsum1, a.inv_n, m0);
+      const float var = fmaf(-(float)S * dsum1, dsum1 * a.inv_n, dsum2) * a.inv_ns;
+      // instance normalisation: descriptors of xhat = (x - mu_r) rr are
+      // affine images of those of x; the head runs on x and a8 adds mu_r (1 - w1[m]) + sr b
+      mu_r = 0.f, rr = 1.f, sr = 1.f;
+      if (a.revin) {
+        mu_r = mbar;
+        rr = rsqrtf(var + kEpsRevin);
+        sr = (var + kEpsRevin) * rr;
+      }
+      const float inv_var = 1.0f / fmaf(var * rr, rr, kEpsTrend);
+      cmt = sqrtf(inv_var * a.kt) * rr, ckt = sqrtf(a.vtrend * inv_var * a.kt) * rr;
+      // a row whose known bound f_n sits far above its true maximum (between f_n^2 and f_n:
+      // a segment with nu^2 not >> eps_s, e.g. constant to within rounding) would leave its
+      // largest exponential below 2^-6 at low tau_s, where the fp16 hi/lo split of E loses
+      // precision (and below 2^-24 it underflows): such series take exact row maxima (below)
+      loose = 0;
+      for (int n = tid; n < NP; n += nthr) {
+        if (n < N) {
+          const float nu2 = c_inv[n] * rr * rr;
+          const float inv = rsqrtf(nu2 + kEpsSeasonal);
+          // row-normalised Gram operand Z'_n = z_n rr / sqrt(nu2_n rr^2 + eps_s) (|Z'_n| <= 1):
+          // the split keeps ~22 bits relative to every row, and the Gram is rho itself
+          {
+            const float* xr = xbuf + n * S;
+            const float x0 = xr[0], m1 = c_nu[n], q = inv * rr;
+            const float kd = a.detrend ? c_ka[n] : 0.f;
+            for (int t = 0; t < S; t++) {
+              const float z = fmaf(-kd, (float)t - half_s, (xr[t] - x0) - m1);
+              __half h, l;
+              split1(z * q, h, l);
+              z_hi[n * ZP + t] = h;
+              z_lo[n * ZP + t] = l;
+            }
+          }
+          c_inv[n] = 1.f;                // column factor of rho: 1 (row-normalised Gram)
+          c_max[n] = sqrtf(nu2) * inv;   // f_n: known row maximum of rho (Cauchy-Schwarz)
+          loose |= (c_max[n] - c_max[n] * c_max[n]) * a.ks > 6.f;
+          if (COMP) {
+            c_vm[n] = c_mu[n];
+            c_vk[n] = c_ka[n];
+          }
+          c_mu[n] = (c_mu[n] - mu_r) * cmt;
+          c_ka[n] = c_ka[n] * ckt;
+        } else {
+          c_inv[n] = 0.f;
+          c_max[n] = 0.f;
+          c_mu[n] = INFINITY;            // exponent -inf: masked key
+          c_ka[n] = 0.f;
+          if (COMP) c_vm[n] = c_vk[n] = 0.f;
+        }
       }
     }
     loose = __syncthreads_or(loose);
