@@ -603,22 +603,27 @@ __global__ void __launch_bounds__(32 * (NWS + 1), NWS == 16 ? 1 : 2) prnet_fwd_t
         tc_fence_after();
         if (warp_rows && !(PRNET_TCL_ABL & 8)) {
           const int g = lane >> 2;
-          // 1 / l of this lane's fragment rows (branch, k-step, row half), once per query tile
-          // rather than per work item (MUFU reciprocal, <= 1 ulp, as the other kernels' softmax)
+          // 1 / l of this lane's fragment rows (branch, k-step, row half) by the MUFU reciprocal
+          // (<= 1 ulp, as the other kernels' softmax); for MT <= 2 once per query tile rather than
+          // per work item (measured: S = 96 10.58 -> 9.72 ms; with four head m-tiles, M > 32, the
+          // hoisted copies cost registers, L5760/S12/H720 46.2 vs 47.0 ms, so MT = 4 recomputes)
+          auto inv_l = [&](int br, int kb, int v) {
+            const int rr = 32 * wq + 16 * kb + g + 8 * v;
+            const float* lp = lpart + K::NWC * 128 * br + rr;
+            float l_ = lp[0];
+#pragma unroll
+            for (int cg = 1; cg < K::NWC; cg++) l_ += lp[cg * 128];
+            return 128 * qt + rr < N ? fast_rcp(l_) : 0.f;
+          };
           float ilv[2][2][2];
+          if constexpr (MT <= 2) {
 #pragma unroll
-          for (int br = 0; br < 2; br++)
+            for (int br = 0; br < 2; br++)
 #pragma unroll
-            for (int kb = 0; kb < 2; kb++)
+              for (int kb = 0; kb < 2; kb++)
 #pragma unroll
-              for (int v = 0; v < 2; v++) {
-                const int rr = 32 * wq + 16 * kb + g + 8 * v;
-                const float* lp = lpart + K::NWC * 128 * br + rr;
-                float l_ = lp[0];
-#pragma unroll
-                for (int cg = 1; cg < K::NWC; cg++) l_ += lp[cg * 128];
-                ilv[br][kb][v] = 128 * qt + rr < N ? fast_rcp(l_) : 0.f;
-              }
+                for (int v = 0; v < 2; v++) ilv[br][kb][v] = inv_l(br, kb, v);
+          }
           // work items (branch, n-tile) of this row quarter, split over the column quarters
           for (int it = wc; it < 2 * K::NCT; it += K::NWC) {
             const int br = it / K::NCT, nt = it - br * K::NCT;
@@ -631,8 +636,14 @@ __global__ void __launch_bounds__(32 * (NWS + 1), NWS == 16 ? 1 : 2) prnet_fwd_t
             for (int kb = 0; kb < 2; kb++) {
               const int i0 = 128 * qt + 32 * wq + 16 * kb;   // K rows of this step
               if (i0 >= npf) break;
-              const float il[2] = {br ? ilv[1][kb][0] : ilv[0][kb][0],
-                                   br ? ilv[1][kb][1] : ilv[0][kb][1]};
+              float il[2];
+              if constexpr (MT <= 2) {
+                il[0] = br ? ilv[1][kb][0] : ilv[0][kb][0];
+                il[1] = br ? ilv[1][kb][1] : ilv[0][kb][1];
+              } else {
+                il[0] = inv_l(br, kb, 0);
+                il[1] = inv_l(br, kb, 1);
+              }
               uint32_t pr[4];
               const uint32_t pa = tmem0 + ((uint32_t)(32 * wq + 16 * kb) << 16) + K::TP +
                                   (uint32_t)(br * K::PW + 8 * nt);
