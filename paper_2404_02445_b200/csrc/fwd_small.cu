@@ -59,6 +59,20 @@ __device__ __forceinline__ void warp_reduce_to(float (&v)[P], float* out, int la
   if ((lane & ((1 << sh) - 1)) == 0) out[lane >> sh] = r;
 }
 
+// MUFU reciprocal / square root (approximate, <= ~1 ulp) for the per-series scalars and the
+// row-sum reciprocals: the IEEE sequences (slow-path branches) were ~20 % of this issue-bound
+// kernel's instructions
+__device__ __forceinline__ float rcp_a(float v) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ float sqrt_a(float v) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+
 }  // namespace
 
 // NP: padded segment count (power of two >= N, <= 8); TS: time slots per lane (S <= 32 TS)
@@ -131,6 +145,7 @@ __global__ void __launch_bounds__(256) prnet_fwd_small_kernel(FwdArgs a, int win
   float* at_ = as_ + NP * NP;
   float* qs = at_ + NP * NP;
 
+  const float sq_vtrend = sqrtf(a.vtrend);   // once, outside the series loop
   const int64_t b_begin = (int64_t)blockIdx.x * wins_per_cta;
   int64_t b_end = b_begin + wins_per_cta;
   if (b_end > a.B) b_end = a.B;
@@ -198,8 +213,8 @@ __global__ void __launch_bounds__(256) prnet_fwd_small_kernel(FwdArgs a, int win
 #pragma unroll
     for (int n = 0; n < NP; n++)
       var += n < N ? gram(n, n) + (float)S * (dtab[n] - mbar) * (dtab[n] - mbar) : 0.f;
-    const float inv_var = 1.0f / (var * a.inv_ns + kEpsTrend);
-    const float cm = sqrtf(inv_var * a.kt), ck = sqrtf(a.vtrend * inv_var * a.kt);
+    const float inv_var = rcp_a(var * a.inv_ns + kEpsTrend);
+    const float cm = sqrt_a(inv_var * a.kt), ck = cm * sq_vtrend;
 
     // ---------------- a3-a5: attention, element e = i NP + j per lane; known row maxima
 #pragma unroll
@@ -210,7 +225,7 @@ __global__ void __launch_bounds__(256) prnet_fwd_small_kernel(FwdArgs a, int win
       const float nui = gram(i, i), nuj = gram(j, j);
       const float invi = rsqrtf(nui + kEpsSeasonal), invj = rsqrtf(nuj + kEpsSeasonal);
       const float rho = gram(i, j) * invi * invj;
-      const float fi = sqrtf(nui) * invi;             // rho_ij <= f_i (Cauchy-Schwarz)
+      const float fi = sqrt_a(nui) * invi;            // rho_ij <= f_i (Cauchy-Schwarz)
       float es = ok ? fast_ex2((rho - fi) * a.ks) : 0.f;
       const float mui = dtab[i], muj = dtab[j], ki = dtab[NP + i], kj = dtab[NP + j];
       const float dm = (mui - muj) * cm, dk = (ki - kj) * ck;
@@ -222,8 +237,8 @@ __global__ void __launch_bounds__(256) prnet_fwd_small_kernel(FwdArgs a, int win
         st += __shfl_xor_sync(0xffffffffu, st, o);
       }
       if (e < NP * NP) {
-        as_[e] = ok ? es / ss : 0.f;
-        at_[e] = ok ? et / st : 0.f;
+        as_[e] = ok ? es * rcp_a(ss) : 0.f;   // ss >= its largest term (normal), st >= 1
+        at_[e] = ok ? et * rcp_a(st) : 0.f;
       }
     }
     __syncwarp();
