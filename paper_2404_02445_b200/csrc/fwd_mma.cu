@@ -502,10 +502,10 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
     if constexpr (SC > 0) {
       const float mbar = warp_sum(i < N ? mu : 0.f) * a.inv_n;
       const float dv = i < N ? nu2 + (float)S * (mu - mbar) * (mu - mbar) : 0.f;
-      inv_var = 1.0f / (warp_sum(dv) * a.inv_ns + kEpsTrend);
+      inv_var = fast_rcp(warp_sum(dv) * a.inv_ns + kEpsTrend);
     } else {
       // of the (normalised) input: var rr^2
-      inv_var = 1.0f / fmaf(gen_var * rr, rr, kEpsTrend);
+      inv_var = fast_rcp(fmaf(gen_var * rr, rr, kEpsTrend));
     }
     {
       // trend: mu~ = mu sqrt(inv_var kt), k~ = kappa sqrt(vtrend inv_var kt) (Def 7-8);
@@ -514,14 +514,16 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
       // of it, so exp((rho_ij - f_i) / tau_s) never overflows and its largest term never
       // underflows for tau_s > 0.003; softmax is shift-invariant, so this is the same result
       // as subtracting the searched max (Def 8).
-      const float cm = sqrtf(inv_var * a.kt) * rr, ck = sqrtf(a.vtrend * inv_var * a.kt) * rr;
+      // (MUFU square roots: a common relative factor per series, <= ~1 ulp)
+      const float cmr = fast_sqrt(inv_var * a.kt);
+      const float cm = cmr * rr, ck = cmr * fast_sqrt(a.vtrend) * rr;
       // seasonal normaliser of the normalised input: 1/sqrt(nu2 rr^2 + eps_s); the Gram is of
       // z sz (unnormalised), so the column factor carries one rr and rk the other
       const float nh2 = nu2 * rr * rr;
       const float invh = rsqrtf(nh2 + kEpsSeasonal);
       // generic path: the Gram of the row-normalised Z' is rho itself (column factor 1)
       dsc[lane] = i < N ? make_float4((mu_t - mr) * cm, kap_t * ck, SC == 0 ? 1.f : invh * rr,
-                                      sqrtf(nh2) * invh)
+                                      fast_sqrt(nh2) * invh)
                         : make_float4(0.f, 0.f, 1.f, 0.f);
       if ((SC == 0 || COMP) && a.comp) {   // the (normalised) segment levels and slopes
         cvec[lane] = i < N ? (DEC ? mu : mu - mr) * rr : 0.f;
@@ -638,7 +640,7 @@ __global__ void __launch_bounds__(PRNET_MMA_THREADS, PRNET_MMA_MINB) prnet_fwd_m
     // Gram rows G'[16 mt .. 16 mt + 15][:] = Z' Z'^T (= sz^2 G), rho_ij = G'_ij inv_i inv_j / sz^2
     // with inv = 1/sqrt(nu2 + eps_s) (Def 6), row softmax on the fragments, fold Q' += W'_s A_s
     {
-      const float ks_z = SC == 0 ? a.ks : a.ks / (sz * sz);
+      const float ks_z = SC == 0 ? a.ks : a.ks * fast_rcp(sz * sz);   // sz^2: a power of two
       float2 cinv[2 * MT], cmask[2 * MT];
 #pragma unroll
       for (int nt = 0; nt < 2 * MT; nt++) {

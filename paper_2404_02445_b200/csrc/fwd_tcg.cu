@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(128 * TcgCfg<S, M64>::MAXG, 1) prnet_fwd_tcg_k
         }
       }
       // |x_t| <= |mu| + |z|: the exact power-of-two scale of X'
-      sx = pow2_scale(warp_max_nonneg(valid ? fabsf(mu) + sqrtf(nu2) : 0.f));
+      sx = pow2_scale(warp_max_nonneg(valid ? fabsf(mu) + fast_sqrt(nu2) : 0.f));
       // Def 5: sigma^2 = (1/(N S)) sum_n [nu2_n + S (mu_n - mubar)^2], both sums in one tree
       const float m0 = __shfl_sync(0xffffffffu, mu, 0);
       const float dd = valid ? mu - m0 : 0.f;
@@ -267,9 +267,12 @@ __global__ void __launch_bounds__(128 * TcgCfg<S, M64>::MAXG, 1) prnet_fwd_tcg_k
         acc = add2(acc, make_float2(__shfl_xor_sync(0xffffffffu, acc.x, o),
                                     __shfl_xor_sync(0xffffffffu, acc.y, o)));
       const float var = fmaf(-(float)S * acc.x, acc.x * a.inv_n, acc.y) * a.inv_ns;
-      const float inv_var = 1.0f / (var + kEpsTrend);
-      mi = mu * sqrtf(inv_var * a.kt);
-      ki = kap * sqrtf(a.vtrend * inv_var * a.kt);
+      // series-level factors by MUFU reciprocal / square root (<= ~1 ulp, a common relative
+      // factor on every trend logit of the series)
+      const float inv_var = fast_rcp(var + kEpsTrend);
+      const float tsc = fast_sqrt(inv_var * a.kt);
+      mi = mu * tsc;
+      ki = kap * (tsc * fast_sqrt(a.vtrend));
       colv[i] = valid ? mi : INFINITY;
       colv[32 + i] = ki;
       colv[128 + i] = valid ? 0.f : -INFINITY;

@@ -176,6 +176,14 @@ __device__ __forceinline__ float warp_max_nonneg(float v) {
   return __uint_as_float(r);
 }
 
+// sqrt(v) via MUFU (approximate, ~1 ulp): series-level scale factors and bounds, where the IEEE
+// sequence's slow-path branches cost more than the rest of the scalar work
+__device__ __forceinline__ float fast_sqrt(float v) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+
 // 1/v via MUFU.RCP (approximate, <= 1 ulp; v a normal softmax row sum >= 2^-126)
 __device__ __forceinline__ float fast_rcp(float v) {
   float r;
