@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
   const bool mma_warp = s == 0;
   const uint32_t zq_s = smem_u32(zq), xt_s = smem_u32(xt), w_s = smem_u32(smem + OFFW);
   const float inv_sw = __ldg(a.wpack_inv_sw + cw);
+  const float sq_vtrend = sqrtf(a.vtrend);   // once per thread, outside the rounds
   const bool full_rows = H == 24 * M && (H & 1) == 0;   // the output rows tile H exactly
 
   // windows of channel c: CTA k of the channel takes [B k / K, B (k+1) / K), split into
@@ -381,7 +382,7 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
         // |xhat_t| <= (|mu - mu_r| + |kappa| 11.5 [detrended] + |e or z|) rr: an exact
         // power-of-two scale for X' from it
         const float bnd =
-            (fabsf(mu - mu_r) + (detrend ? 11.5f * fabsf(kap) : 0.f) + sqrtf(nu2s)) * rr;
+            (fabsf(mu - mu_r) + (detrend ? 11.5f * fabsf(kap) : 0.f) + fast_sqrt(nu2s)) * rr;
         sx = pow2_scale(warp_max_nonneg(valid ? bnd : 0.f));
         const float2 zs2 = f2(valid ? zsc : 0.f), xs2 = f2(valid ? rr * sx : 0.f);
         const float2 xo2 = f2(valid ? -mu_r * rr * sx : 0.f);
@@ -431,15 +432,18 @@ __global__ void __launch_bounds__(512, 1) prnet_fwd_tcq_kernel(FwdArgs a, int ct
         mr = mu_r;
         write_operands(mu_r, rr);
       }
-      const float inv_var = 1.0f / fmaf(var * rr, rr, kEpsTrend);
+      // series-level factors by MUFU reciprocal / square root (<= ~1 ulp, a common relative
+      // factor on every trend logit of the series)
+      const float inv_var = fast_rcp(fmaf(var * rr, rr, kEpsTrend));
+      const float tsc = fast_sqrt(inv_var * a.kt) * rr;
       // trend (Def 7-8): exponent -(mu~_i - mu~_j)^2 - (k~_i - k~_j)^2, mu~ = muhat sqrt(kt/var'),
       // k~ = kappahat sqrt(vtrend kt/var')
       if constexpr (COMP) {
         cmu = (mu - mu_r) * rr;
         ckap = kap * rr;
       }
-      mi = (mu - mu_r) * rr * sqrtf(inv_var * a.kt);
-      ki = kap * rr * sqrtf(a.vtrend * inv_var * a.kt);
+      mi = (mu - mu_r) * tsc;
+      ki = kap * (tsc * sq_vtrend);
       colv[i] = (NC > 0 || valid) ? mi : INFINITY;   // -> exponent -inf past N
       colv[32 + i] = ki;
       if constexpr (NC == 0) colv[128 + i] = valid ? 0.f : -INFINITY;

@@ -3,7 +3,7 @@
 # repetitions, one gpurun call -> gpurun_out/ab_libs.jsonl
 set -u
 OUT=gpurun_out; mkdir -p $OUT; : > $OUT/ab_libs.jsonl
-for rep in 1 2 3; do
+for rep in ${REPS:-1 2 3}; do
   for wl in ${WLS}; do
     for lib in ${LIBS}; do
       PRNET_LIB=$PWD/paper_2404_02445_b200/$lib timeout -s KILL 200 python bench.py --workload $wl --steps ${STEPS:-20} --warmup 5 --no-cpu-baseline --no-e2e > $OUT/abl.json 2>$OUT/abl.err
