@@ -41,6 +41,12 @@ __device__ __forceinline__ float shfl(float v, int src) {
 }  // namespace
 
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+// 1/v via MUFU.RCP (approximate, <= 1 ulp; v a normal positive float)
+__device__ __forceinline__ float rcp_a(float v) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
 __device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
 
 // dx and the temperature partials; the head gradients come from the head-backward kernel
@@ -92,7 +98,6 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
   float dts = 0.f, dtt = 0.f;               // lane partials of dL/dtau_s, dL/dtau_t
   const int i = lane;
   const bool valid = i < N;
-  const float V = 1.0f / a.inv_v;           // S (S^2 - 1) / 12
   const float w = a.vtrend;                 // (S^2 - 1) / 12, 0 for the level-only trend
   const float tau_s = kLog2e / a.ks, tau_t = kLog2e / a.kt;
   const int S4 = (S + 3) >> 2;
@@ -151,7 +156,7 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
     gv[i] = g;
     // series-level reciprocals, formed once: the per-element steps below multiply (IEEE
     // divisions inside the N x N loops were 37 % of the kernel's instructions)
-    const float its = 1.f / tau_s, itt = 1.f / tau_t, iden = 1.f / den;
+    const float its = 1.f / tau_s, itt = 1.f / tau_t, iden = rcp_a(den);
     const float ct = iden * itt;             // Dhat / tau_t = D / (den tau_t)
     __syncwarp();
     // Gram row i: <z_i, z_j> from the own row and broadcast rows (z = X - mu; t >= S masked)
@@ -204,7 +209,7 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
         ls += es;
         lt += et;
       }
-      const float ils = 1.f / ls, ilt = 1.f / lt;
+      const float ils = rcp_a(ls), ilt = rcp_a(lt);   // row sums >= 1 (the row maximum's term)
       for (int j = 0; j < N; j++) {
         As[i * Q + j] *= ils;
         At[i * Q + j] *= ilt;
@@ -302,7 +307,7 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
       }
     }
     ds2 = warp_sum(ds2);
-    float dnu2 = valid ? -0.5f * (dg / g) * g * g * g : 0.f;
+    float dnu2 = valid ? -0.5f * dg * g * g : 0.f;   // d(nu2) = -dg g^3 / (2 g) (no division)
     dnu2 += ds2 * a.inv_ns;
     dmu += ds2 * 2.f * (mu - mubar) * a.inv_n;
     // ---------------- dX = dX_direct + dz + dmu / S with dz_i = g_i sum_j (drho_ij + drho_ji)
@@ -321,7 +326,7 @@ __global__ void __launch_bounds__(256) prnet_bwd_full_kernel(FwdArgs a, const fl
         float4 v = ld4(dXs + i * P + t0);
         const float4 xi = ld4(Xs + i * P + t0);
         const float dmS = dmu * a.inv_s;
-        const float dkv = dkap / V;
+        const float dkv = dkap * a.inv_v;   // 1 / V
         float4 dz;
         dz.x = fmaf(2.f * ((xi.x - x0) - m1), dnu2, ((float)t0 - a.half_s) * dkv);
         dz.y = fmaf(2.f * ((xi.y - x0) - m1), dnu2, ((float)(t0 + 1) - a.half_s) * dkv);

@@ -165,8 +165,10 @@ __global__ void __launch_bounds__(32 * kBmWarps, kBmMinBlocks) prnet_bwd_head_mm
     }
     const float mbar = warp_sum(valid ? mu : 0.f) * a.inv_n;
     const float var = warp_sum(valid ? nu2 + (float)S * (mu - mbar) * (mu - mbar) : 0.f) * a.inv_ns;
-    const float inv_var = 1.f / (var + kEpsTrend);
-    const float mtc = mu * sqrtf(inv_var * a.kt), ktc = kap * sqrtf(a.vtrend * inv_var * a.kt);
+    // series-level factors by MUFU reciprocal / square root (<= ~1 ulp), as the forward kernels
+    const float inv_var = fast_rcp(var + kEpsTrend);
+    const float tsc = fast_sqrt(inv_var * a.kt);
+    const float mtc = mu * tsc, ktc = kap * (tsc * fast_sqrt(a.vtrend));
     const float zsc = valid ? rsqrtf(nu2 + kEpsSeasonal) : 0.f;
     // exact power-of-two scales: |X'| = |x sx| < 1, |dY'| = |dy sy| < 1
     float mx = 0.f, my = 0.f;
@@ -321,7 +323,7 @@ __global__ void __launch_bounds__(32 * kBmWarps, kBmMinBlocks) prnet_bwd_head_mm
             }
           sum += __shfl_xor_sync(0xffffffffu, sum, 1);
           sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-          const float rs = row < N ? 1.f / sum : 0.f;
+          const float rs = row < N ? fast_rcp(sum) : 0.f;   // sum >= 1 (the row maximum's term)
 #pragma unroll
           for (int nt = 0; nt < 4; nt++)
 #pragma unroll
