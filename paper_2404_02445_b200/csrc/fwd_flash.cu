@@ -272,8 +272,8 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
         rr = rsqrtf(var + kEpsRevin);
         sr = (var + kEpsRevin) * rr;
       }
-      const float inv_var = 1.0f / fmaf(var * rr, rr, kEpsTrend);
-      cmt = sqrtf(inv_var * a.kt) * rr, ckt = sqrtf(a.vtrend * inv_var * a.kt) * rr;
+      const float inv_var = fast_rcp(fmaf(var * rr, rr, kEpsTrend));   // MUFU, <= ~1 ulp
+      cmt = fast_sqrt(inv_var * a.kt) * rr, ckt = cmt * fast_sqrt(a.vtrend);
       // a row whose known bound f_n sits far above its true maximum (between f_n^2 and f_n:
       // a segment with nu^2 not >> eps_s, e.g. constant to within rounding) would leave its
       // largest exponential below 2^-6 at low tau_s, where the fp16 hi/lo split of E loses
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
         if (rr_ == 0 && n < NP) {
           if (on) {
             c_inv[n] = 1.f;                // column factor of rho: 1 (row-normalised Gram)
-            c_max[n] = sqrtf(nu2) * inv;   // f_n: known row maximum of rho (Cauchy-Schwarz)
+            c_max[n] = fast_sqrt(nu2) * inv;   // f_n: known row maximum of rho (Cauchy-Schwarz)
             loose |= (c_max[n] - c_max[n] * c_max[n]) * a.ks > 6.f;
             if (COMP) {
               c_vm[n] = cmu;
@@ -382,8 +382,8 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
         rr = rsqrtf(var + kEpsRevin);
         sr = (var + kEpsRevin) * rr;
       }
-      const float inv_var = 1.0f / fmaf(var * rr, rr, kEpsTrend);
-      cmt = sqrtf(inv_var * a.kt) * rr, ckt = sqrtf(a.vtrend * inv_var * a.kt) * rr;
+      const float inv_var = fast_rcp(fmaf(var * rr, rr, kEpsTrend));   // MUFU, <= ~1 ulp
+      cmt = fast_sqrt(inv_var * a.kt) * rr, ckt = cmt * fast_sqrt(a.vtrend);
       // a row whose known bound f_n sits far above its true maximum (between f_n^2 and f_n:
       // a segment with nu^2 not >> eps_s, e.g. constant to within rounding) would leave its
       // largest exponential below 2^-6 at low tau_s, where the fp16 hi/lo split of E loses
@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
             }
           }
           c_inv[n] = 1.f;                // column factor of rho: 1 (row-normalised Gram)
-          c_max[n] = sqrtf(nu2) * inv;   // f_n: known row maximum of rho (Cauchy-Schwarz)
+          c_max[n] = fast_sqrt(nu2) * inv;   // f_n: known row maximum of rho (Cauchy-Schwarz)
           loose |= (c_max[n] - c_max[n] * c_max[n]) * a.ks > 6.f;
           if (COMP) {
             c_vm[n] = c_mu[n];
@@ -600,8 +600,8 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
         tsum[h] += __shfl_xor_sync(0xffffffffu, tsum[h], 1);
         tsum[h] += __shfl_xor_sync(0xffffffffu, tsum[h], 2);
         const int ii = 16 * qt + 8 * h + gq;
-        ssum[h] = ii < N ? 1.f / ssum[h] : 0.f;
-        tsum[h] = ii < N ? 1.f / tsum[h] : 0.f;
+        ssum[h] = ii < N ? fast_rcp(ssum[h]) : 0.f;   // row sums >= the largest term (normal)
+        tsum[h] = ii < N ? fast_rcp(tsum[h]) : 0.f;
         if (COMP) {
 #pragma unroll
           for (int o = 1; o <= 2; o <<= 1) {
