@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(32 * (NWS + 1), NWS == 16 ? 1 : 2) prnet_fwd_t
       const float dd = rv ? mu_[rk] - m0 : 0.f;
       s_a += dd;
       s_b += rv ? fmaf((float)S * dd, dd, nu2_[rk]) : 0.f;
-      bnd = fmaxf(bnd, rv ? fabsf(mu_[rk]) + sqrtf(nu2_[rk]) : 0.f);
+      bnd = fmaxf(bnd, rv ? fabsf(mu_[rk]) + fast_sqrt(nu2_[rk]) : 0.f);
     }
     {
       s_a = warp_sum(s_a);
@@ -408,7 +408,9 @@ __global__ void __launch_bounds__(32 * (NWS + 1), NWS == 16 ? 1 : 2) prnet_fwd_t
       mxa = fmaxf(mxa, red[3 * w + 2]);
     }
     const float var = fmaf(-(float)S * sa, sa * a.inv_n, sb) * a.inv_ns;
-    const float inv_var = 1.0f / (var + kEpsTrend);
+    // series-level factors once (MUFU reciprocal / square root, <= ~1 ulp), not per row
+    const float inv_var = fast_rcp(var + kEpsTrend);
+    const float tsc = fast_sqrt(inv_var * a.kt), tsk = tsc * fast_sqrt(a.vtrend);
     const float sx = pow2_scale(mxa);
 #pragma unroll
     for (int rk = 0; rk < K::RPT; rk++) {
@@ -440,9 +442,9 @@ __global__ void __launch_bounds__(32 * (NWS + 1), NWS == 16 ? 1 : 2) prnet_fwd_t
     }
     if (r < ly.rpad) {
       // f_i = nu_i / sqrt(nu_i^2 + eps_s) >= rho_ij: the seasonal shift (rows >= N: 0)
-      fks[r] = rv ? sqrtf(nu2 / (nu2 + kEpsSeasonal)) * a.ks : 0.f;
-      mtv[r] = rv ? mu * sqrtf(inv_var * a.kt) : 0.f;
-      ktv[r] = rv ? kap * sqrtf(a.vtrend * inv_var * a.kt) : 0.f;
+      fks[r] = rv ? fast_sqrt(nu2) * rsqrtf(nu2 + kEpsSeasonal) * a.ks : 0.f;
+      mtv[r] = rv ? mu * tsc : 0.f;
+      ktv[r] = rv ? kap * tsk : 0.f;
     }
     }
     if (K::SB == 1) {   // the staging buffer is read: fetch the next series now
