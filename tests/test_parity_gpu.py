@@ -705,6 +705,29 @@ def test_tc_quad_attention_dump(oracle_mod, L, mv, rev):
             np.testing.assert_allclose(a_t[b, c], r["a_t"], atol=2e-6)
 
 
+@pytest.mark.parametrize("mv,rev,ma", [(2, False, 25), (6, True, 25), (4, False, 0),
+                                       (7, True, 0), (2, False, 3)])
+@pytest.mark.parametrize("L,S", [(720, 24), (336, 12), (100, 24)])
+def test_attention_dump_widened(oracle_mod, L, S, mv, rev, ma):
+    """debug_attention on widened handles with N <= 32 (detrended metric, component values,
+    instance normalisation, moving-average decomposition), compared element-wise with the
+    oracle's attention rows (round-1 advice: the dump must follow the handle's flags)."""
+    C, B, H = 2, 3, 96
+    x = synth.random_windows(B, C, L, kind="mixed")
+    N, _, M = synth.derived_dims(L, S, H)
+    m = PRNet(C, L, S, H, tau_s=0.5, tau_t=2.0, metric_variant=mv, instance_norm=rev,
+              ma_kernel=ma)
+    m.load(*synth.make_params(C, M, N, H, True, synth.DEFAULT_SEED, 0))
+    a_s, a_t = (a.cpu().numpy() for a in m.debug_attention(torch.from_numpy(x).cuda()))
+    for b in range(B):
+        for c in range(C):
+            r = oracle_mod.series(x[b, c], S, S, np.zeros((1, N)), np.zeros((1, N)),
+                                  np.zeros(S), 0.5, 2.0, metric_variant=mv, instance_norm=rev,
+                                  ma_kernel=ma)   # (H = S: one future segment, zero head)
+            np.testing.assert_allclose(a_s[b, c], r["a_s"], atol=2e-6)
+            np.testing.assert_allclose(a_t[b, c], r["a_t"], atol=2e-6)
+
+
 @pytest.mark.parametrize("L,S", [(1440, 24), (2880, 48), (1536, 24)])
 @pytest.mark.parametrize("ma", [0, 9])
 def test_attention_dump_long_n(oracle_mod, L, S, ma):
