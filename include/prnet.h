@@ -266,22 +266,26 @@ prnet_status prnet_backward(prnet_handle* h, const float* x, int64_t batch, cons
  *                    row-normalised segments and the fold on tcgen05 / TMEM,
  *                    head on per-warp mma.sync (split fp16), lane-per-row
  *                    softmaxes (S in {12, 16, 24, 32, 48, 64, 96}, N <= 32,
- *                    M <= 32 for S = 24 else M <= 64, tau_seasonal >= 1/80)
- *                    [auto: N > 16; S = 48 with N > 8; M > 32]
+ *                    M <= 32 for S = 24 else M <= 64, tau_seasonal >= 1/80;
+ *                    S = 24 also takes metric_variant bits 1-2 and instance_norm,
+ *                    not ma_kernel)  [auto: N > 16; S = 48 with N > 8; M > 32;
+ *                    S = 24 with the widening for N > 8]
  *   7 = small_f32    one warp per series with lanes over TIME, FP32, warp
  *                    butterfly reductions (N <= 16, S <= 128, M <= 32)
  *                    [auto: N <= 8 or S > 64 where 9 does not apply]
  *   8 = tc_long      one CTA (16 softmax warps + 1 MMA warp) per series; 128-row query
  *                    x 64-key tiles: Gram and P = E X' on tcgen05 / TMEM, exponentials
  *                    in TMEM, head on mma.sync (32 < N <= 512, S in {12, 24, 48, 96},
- *                    M <= 64, tau_seasonal >= 1/320)
- *                    [auto: S = 96, S = 48 with N >= 100, or M > 32]
+ *                    M <= 64, tau_seasonal >= 1/16, plain reading)
+ *                    [auto: S >= 48 with N >= 100; M <= 8 with S = 12, N >= 100 or
+ *                    S = 24, N >= 200; M > 32]
  *   9 = group_f32    lanes over (series, segment), 32 / NP series per warp, FP32
  *                    (N <= 16, S <= 32, tau_seasonal >= 1/80)
  *                    [auto: N <= 8, S <= 16 or M > 32]
- * Variants 2, 5, 7, 8 need tau_seasonal >= 1/320 (known-maximum softmax shift); 6 and 9
- * tau_seasonal >= 1/80 (the symmetric shift 1); below the floors the automatic choice is 0
- * (N <= 32, no widening) or 1.
+ * Variants 2, 5, 7 need tau_seasonal >= 1/320 (known-maximum softmax shift), 8 needs
+ * tau_seasonal >= 1/16 (its fp16 E operand, DESIGN.md R-tcl); 6 and 9 tau_seasonal >= 1/80
+ * (the symmetric shift 1); below the floors the automatic choice is 0 (N <= 32, no
+ * widening) or 1.
  * Returns PRNET_ERR_UNSUPPORTED when the variant does not cover the handle's shape. */
 prnet_status prnet_set_kernel_variant(prnet_handle* h, int32_t variant);
 
