@@ -25,6 +25,21 @@ namespace prnet {
 
 namespace {
 
+// a hi/lo fp16 pair of consecutive columns (t, t + 1) of a row: one packed split, 4-byte stores;
+// the last column of an odd-length row alone
+__device__ __forceinline__ void store_split_pair(__half* hi, __half* lo, int o, float v0, float v1,
+                                                 bool two) {
+  uint32_t h2, l2;
+  split2(make_float2(v0, v1), h2, l2);
+  if (two) {
+    *reinterpret_cast<uint32_t*>(hi + o) = h2;
+    *reinterpret_cast<uint32_t*>(lo + o) = l2;
+  } else {
+    hi[o] = __ushort_as_half((unsigned short)(h2 & 0xFFFFu));
+    lo[o] = __ushort_as_half((unsigned short)(l2 & 0xFFFFu));
+  }
+}
+
 // two block reductions for the price of one pair of barriers (scratch holds 2 nw floats)
 __device__ __forceinline__ void block_reduce2(float& u, float& v, float* scratch, bool is_max) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -239,14 +254,13 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
           m1 = c_nu[n];
           ka = c_ka[n];
           const float kd = a.detrend ? ka : 0.f;   // e = z - kappa t~
-          for (int t = rr_; t < S; t += tps) {
-            const float v = xr[t];
-            const float z = fmaf(-kd, (float)t - half_s, (v - x0) - m1);
-            q = fmaf(z, z, q);
-            __half h, l;
-            split1(v * sx, h, l);
-            x_hi[n * XP + t] = h;
-            x_lo[n * XP + t] = l;
+          for (int t = 2 * rr_; t < S; t += 2 * tps) {   // column pairs (t, t + 1)
+            const bool two = t + 1 < S;
+            const float v0 = xr[t], v1 = two ? xr[t + 1] : 0.f;
+            const float z0 = fmaf(-kd, (float)t - half_s, (v0 - x0) - m1);
+            const float z1 = two ? fmaf(-kd, (float)(t + 1) - half_s, (v1 - x0) - m1) : 0.f;
+            q = fmaf(z1, z1, fmaf(z0, z0, q));
+            store_split_pair(x_hi, x_lo, n * XP + t, v0 * sx, v1 * sx, two);
           }
         }
         q = gsum(q);
@@ -293,12 +307,11 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
           const float* xr = xbuf + n * S;
           const float x0 = xr[0], m1 = c_nu[n], q = inv * rr;
           const float kd = a.detrend ? cka : 0.f;
-          for (int t = rr_; t < S; t += tps) {
-            const float z = fmaf(-kd, (float)t - half_s, (xr[t] - x0) - m1);
-            __half h, l;
-            split1(z * q, h, l);
-            z_hi[n * ZP + t] = h;
-            z_lo[n * ZP + t] = l;
+          for (int t = 2 * rr_; t < S; t += 2 * tps) {   // column pairs (t, t + 1)
+            const bool two = t + 1 < S;
+            const float z0 = fmaf(-kd, (float)t - half_s, (xr[t] - x0) - m1);
+            const float z1 = two ? fmaf(-kd, (float)(t + 1) - half_s, (xr[t + 1] - x0) - m1) : 0.f;
+            store_split_pair(z_hi, z_lo, n * ZP + t, z0 * q, z1 * q, two);
           }
         }
         __syncwarp();   // the group has read the row's scalars: the leader rewrites them
@@ -353,14 +366,13 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
         const float x0 = xr[0], m1 = c_nu[n];
         const float kd = a.detrend ? c_ka[n] : 0.f;   // e = z - kappa t~
         float q = 0.f;
-        for (int t = 0; t < S; t++) {
-          const float v = xr[t];
-          const float z = fmaf(-kd, (float)t - half_s, (v - x0) - m1);
-          q = fmaf(z, z, q);
-          __half h, l;
-          split1(v * sx, h, l);
-          x_hi[n * XP + t] = h;
-          x_lo[n * XP + t] = l;
+        for (int t = 0; t < S; t += 2) {   // column pairs (t, t + 1)
+          const bool two = t + 1 < S;
+          const float v0 = xr[t], v1 = two ? xr[t + 1] : 0.f;
+          const float z0 = fmaf(-kd, (float)t - half_s, (v0 - x0) - m1);
+          const float z1 = two ? fmaf(-kd, (float)(t + 1) - half_s, (v1 - x0) - m1) : 0.f;
+          q = fmaf(z1, z1, fmaf(z0, z0, q));
+          store_split_pair(x_hi, x_lo, n * XP + t, v0 * sx, v1 * sx, two);
         }
         const float mu = x0 + m1;
         c_mu[n] = mu;        // temporarily mu
@@ -399,12 +411,11 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
             const float* xr = xbuf + n * S;
             const float x0 = xr[0], m1 = c_nu[n], q = inv * rr;
             const float kd = a.detrend ? c_ka[n] : 0.f;
-            for (int t = 0; t < S; t++) {
-              const float z = fmaf(-kd, (float)t - half_s, (xr[t] - x0) - m1);
-              __half h, l;
-              split1(z * q, h, l);
-              z_hi[n * ZP + t] = h;
-              z_lo[n * ZP + t] = l;
+            for (int t = 0; t < S; t += 2) {   // column pairs (t, t + 1)
+              const bool two = t + 1 < S;
+              const float z0 = fmaf(-kd, (float)t - half_s, (xr[t] - x0) - m1);
+              const float z1 = two ? fmaf(-kd, (float)(t + 1) - half_s, (xr[t + 1] - x0) - m1) : 0.f;
+              store_split_pair(z_hi, z_lo, n * ZP + t, z0 * q, z1 * q, two);
             }
           }
           c_inv[n] = 1.f;                // column factor of rho: 1 (row-normalised Gram)
