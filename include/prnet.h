@@ -277,7 +277,7 @@ prnet_status prnet_backward(prnet_handle* h, const float* x, int64_t batch, cons
  *                    x 64-key tiles: Gram and P = E X' on tcgen05 / TMEM, exponentials
  *                    in TMEM, head on mma.sync (32 < N <= 512, S in {12, 24, 48, 96},
  *                    M <= 64, tau_seasonal >= 1/16, plain reading)
- *                    [auto: S >= 48 with N >= 100; M <= 8 with S = 12, N >= 100 or
+ *                    [auto: S >= 48 with N >= 200; M <= 8 with S = 12, N >= 100 or
  *                    S = 24, N >= 200; M > 32]
  *   9 = group_f32    lanes over (series, segment), 32 / NP series per warp, FP32
  *                    (N <= 16, S <= 32, tau_seasonal >= 1/80)

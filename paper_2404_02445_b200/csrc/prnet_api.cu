@@ -259,10 +259,11 @@ int pick_variant(const prnet_handle* h) {
   // L2880/S12 7.61 vs 8.13, L1440/S12 3.22 vs 3.41, L5760/S24 11.95 vs 12.17, L5760/S96 10.5 vs
   // 11.9, L5760/S48 9.99 vs 11.6; flash stays ahead at N = 60 (S <= 48), L2880/S24 (N = 120)
   // and for S = 24 with a long head (L5760/S24/H720, M = 30: 13.4 vs 18.2 ms)
-  // (last round-2 session, after the flash descriptor-phase changes: L5760/S96 (N = 60) flash 9.10
-  // vs tc_long 9.72 ms, with H = 720 10.04 vs 10.00; S >= 48 keeps tc_long from N = 100 on)
+  // (last round-2 session, after the flash descriptor-phase changes: L5760/S96 (N = 60) flash 8.38
+  // vs tc_long 9.72 ms; L5760/S48 (N = 120) flash 9.27 vs 9.45; L5760/S24 (N = 240) tc_long 11.15
+  // vs 11.28: S >= 48 takes tc_long from N = 200 on, the S = 24 crossover)
   if (tcl_applicable(h) &&
-      (!flash_applicable(h) || (h->cfg.seg_len >= 48 && h->N >= 100) ||
+      (!flash_applicable(h) || (h->cfg.seg_len >= 48 && h->N >= 200) ||
        (h->M <= 8 && ((h->cfg.seg_len == 12 && h->N >= 100) ||
                       (h->cfg.seg_len == 24 && h->N >= 200)))))
     return 8;   // (M > 32: the only tensor-core kernel for N > 32)
