@@ -185,6 +185,15 @@ __global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel
     // descriptor passes (the second hits L1/L2): no shared staging, so a 480-segment series
     // fits two CTAs per SM
     const float* xbuf = a.x + b * a.xsb + c * a.xsc + a.r;
+    // the next series' span into L2 (one bulk prefetch): the descriptor passes of series b + 1
+    // then start from L2 instead of DRAM (16-byte aligned windows; the size rounded down)
+    if (tid == 0 && a.x_vec && b + 1 < b_end) {
+      const float* nx = xbuf + a.xsb;
+      const uint32_t nbytes = (uint32_t)(N * S * 4) & ~15u;
+      if (nbytes > 0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nx), "r"(nbytes)
+                     : "memory");
+    }
     // KS >= 2 (S > 16): the descriptor passes with tps threads per segment; S <= 16 keeps one
     // thread per segment (measured: L720/S12 1.18 ms against 1.27-1.39 with the grouped form)
     float sx, sz, mu_r, rr, sr, cmt, ckt;
