@@ -62,10 +62,11 @@ def tensor_flops_per_series(variant, N, S, M):
     K = 16 per quad), head on mma.sync (36 m16n8k16 per series).  mma_f16x3 / flash_f16x3:
     m16n8k16 tiles of the Gram, of the fold (mma) or of P = E X (flash), and of the head."""
     NP, MP, SP, KZ = _up(N, 16), _up(M, 16), _up(S, 8), _up(S, 16)
-    if variant == "tc_quad" and S == 24:
-        return (5 * 2 * 128 * 128 * 16 + 12 * 2 * 128 * 32 * 16) / 4 + 36 * 2 * 16 * 8 * 16
-    if variant == "tc_quad":   # generic S (fwd_tcg.cu): 3 runs of KZ/16 Gram K-steps, fold N 32/64
-        mf = 32 if M <= 32 else 64
+    if variant == "tc_quad" and S == 24:   # M <= 16: fold N = 16 and one head m-tile (MTL = 1)
+        mf, mt = (16, 1) if M <= 16 else (32, 2)
+        return (5 * 2 * 128 * 128 * 16 + 12 * 2 * 128 * mf * 16) / 4 + 18 * mt * 2 * 16 * 8 * 16
+    if variant == "tc_quad":   # generic S (fwd_tcg.cu): 3 runs of KZ/16 Gram K-steps, fold N 16/32/64
+        mf = 16 if M <= 16 else (32 if M <= 32 else 64)
         return ((3 * (KZ // 16) * 2 * 128 * 128 * 16 + 12 * 2 * 128 * mf * 16) / 4
                 + 3 * (MP // 16) * (SP // 8) * 2 * 2 * 16 * 8 * 16)
     if variant == "tc_long":   # fwd_tcl.cu: 128-row query x 64-key tiles, Gram + P = E X' + head
