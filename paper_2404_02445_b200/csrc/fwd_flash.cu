@@ -21,6 +21,18 @@
 
 #include "mma_common.cuh"
 
+// CTAs per SM by register budget: S <= 32 (KS <= 2) and S in (32, 48] (KS = 3) two CTAs at 128
+// registers (measured, round 2: KS = 3 spills 200-400 bytes and is still 16-20 % faster, stress
+// L2880/S48 3.49 -> 2.91 ms, L2880/S48/H720 4.08 -> 3.25, L5760/S48 9.09 -> 7.61); S > 48 (two
+// t-chunks) one CTA (at 128 registers it spills more and was 19-24 % slower, L5760/S96 8.14 ->
+// 10.07)
+#ifndef PRNET_FLASH_MINB3
+#define PRNET_FLASH_MINB3 2
+#endif
+#ifndef PRNET_FLASH_MINB4
+#define PRNET_FLASH_MINB4 1
+#endif
+
 namespace prnet {
 
 namespace {
@@ -128,7 +140,7 @@ void pack_flash_head(const float* ws, const float* wt, int Cw, int M, int N, uns
 // d1 (A_s kappa) t~^T and P_t = (A_t mu) 1^T + d0 (A_t kappa) t~^T, from four row sums
 // accumulated with the exponentials (no A_t X product)
 template <int KS, int NTT, int MMT, bool COMP = false>
-__global__ void __launch_bounds__(256, (KS <= 2 ? 2 : 1)) prnet_fwd_flash_kernel(FwdArgs a, FlashLayout ly,
+__global__ void __launch_bounds__(256, (KS <= 2 ? 2 : (KS == 3 ? PRNET_FLASH_MINB3 : PRNET_FLASH_MINB4))) prnet_fwd_flash_kernel(FwdArgs a, FlashLayout ly,
                                                                  int wins_per_cta) {
   extern __shared__ float4 smem4[];
   unsigned char* smem = reinterpret_cast<unsigned char*>(smem4);
